@@ -1,0 +1,201 @@
+/*
+ * fstk_gpu.h — C-ABI of the B200-native functional-sparse-Tucker hot path.
+ *
+ * Drop-in boundary for the reference library `fstk` (arXiv 1907.05884
+ * reference, /root/reference/proj).  Each entry point replaces one reference
+ * C++ call on the hot path; the reference signature it replaces is cited next
+ * to it.  Conventions:
+ *   - plain pointers and sizes only; no C++ or torch types cross the ABI;
+ *   - every function returns 0 on success or (fstk ErrorKind + 1) on failure
+ *     (proj/include/fstk/error.hpp:11-19) and never throws; the optional
+ *     fstk_gpu_error* receives the kind, a message and, for Domain errors,
+ *     the first offending point/mode/coordinate;
+ *   - the caller owns host buffers (pinned or pageable); the library owns
+ *     device memory and streams; a model handle may be shared by threads.
+ *   - matrices are column-major ("Eigen default", proj/include/fstk/tensor.hpp:12)
+ *     and tensors are mode-0 fastest (tensor.hpp:18-22).
+ */
+#ifndef FSTK_GPU_H_
+#define FSTK_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSTK_GPU_ABI_VERSION 1
+
+/* Status codes = fstk::ErrorKind + 1 (error.hpp:11-19). */
+enum {
+  FSTK_OK = 0,
+  FSTK_E_PARAMETER = 1,
+  FSTK_E_SHAPE = 2,
+  FSTK_E_DOMAIN = 3,
+  FSTK_E_DATA = 4,
+  FSTK_E_IO = 5,
+  FSTK_E_DECODE = 6,
+  FSTK_E_COMPUTE = 7
+};
+
+/* Mixing transforms, fstk::MixingTransform (randls.hpp:13). */
+enum { FSTK_TRANSFORM_DCT = 0, FSTK_TRANSFORM_WHT = 1, FSTK_TRANSFORM_FFT = 2 };
+
+typedef struct fstk_gpu_error {
+  int32_t kind;     /* FSTK_E_* or 0 */
+  int32_t mode;     /* Domain: offending mode, else -1 */
+  int64_t index;    /* Domain: lowest offending point index, else -1 */
+  double value;     /* Domain: offending coordinate */
+  char message[256];
+} fstk_gpu_error;
+
+/*
+ * Model descriptor: the content of fstk::FunctionalSparseTuckerModel
+ * (model.hpp:33-59) flattened.  Functions are listed mode-major (all r_0
+ * functions of mode 0, then mode 1, ...); per function: basis family
+ * (0 = Legendre, 1 = wavelet), degree, resolution, domain [lo, hi] and its
+ * SparseFit coefficients (lars.hpp:41-50): nnz strictly increasing u32 basis
+ * indices with matching f64 values, concatenated over functions in order.
+ */
+typedef struct fstk_model_desc {
+  int32_t d;                 /* 1..8 (kMaxOrder, tensor.hpp:16) */
+  const int64_t* ranks;      /* d */
+  const double* core;        /* prod(ranks), mode-0 fastest */
+  const int32_t* family;     /* sum(ranks) */
+  const int32_t* degree;     /* sum(ranks) */
+  const int32_t* resolution; /* sum(ranks) */
+  const double* lo;          /* sum(ranks) */
+  const double* hi;          /* sum(ranks) */
+  const uint32_t* nnz;       /* sum(ranks) */
+  const uint32_t* indices;   /* sum(nnz) */
+  const double* coeffs;      /* sum(nnz) */
+} fstk_model_desc;
+
+/* fstk::SketchConfig (randls.hpp:15-24). */
+typedef struct fstk_sketch_cfg {
+  uint64_t seed;
+  uint64_t working_subset;   /* 0 = all training points; default 1<<20 */
+  uint64_t sample_rows;      /* S; 0 = ceil(2.5 R) */
+  int32_t transform;         /* FSTK_TRANSFORM_* */
+  double validation_fraction;/* default 0.05 */
+} fstk_sketch_cfg;
+
+/* fstk::ReestimateResult fields (randls.hpp:52-60) plus stage timings. */
+typedef struct fstk_reestimate_info {
+  double residual_before;
+  double residual_after;
+  uint64_t sample_rows;
+  uint64_t working_rows;
+  uint64_t padded_rows;
+  int32_t rank_deficient;
+  int32_t held_out;
+  /* device-timed stage seconds (CUDA events) */
+  double t_prepare;   /* host RNG plan + gathers + mode tables */
+  double t_sketch;    /* design-column generation + mixing + sampling */
+  double t_gram;      /* A^T A and A^T b */
+  double t_solve;     /* Cholesky (cuSOLVER), timed outside the hot-path claim */
+  double t_residual;  /* validation residuals */
+} fstk_reestimate_info;
+
+typedef struct fstk_gpu_model fstk_gpu_model;
+typedef struct fstk_gpu_refit fstk_gpu_refit;
+
+int32_t fstk_gpu_abi_version(void);
+int32_t fstk_gpu_device_count(void);
+/* Kernel launches issued by this process so far (evidence counter). */
+uint64_t fstk_gpu_launch_count(void);
+
+/* Builds the device-resident model.  Validates like the reference ctor
+ * (model.cpp:22-53): Shape on count/domain mismatch, Parameter on invalid
+ * bases.  Wavelet bases are accepted by the format but not by this GPU path
+ * (FSTK_E_PARAMETER). */
+int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device,
+                              fstk_gpu_model** out, fstk_gpu_error* err);
+void fstk_gpu_model_destroy(fstk_gpu_model* model);
+/* FunctionalSparseTuckerModel::with_core (model.cpp:62-69), in place. */
+int32_t fstk_gpu_model_set_core(fstk_gpu_model* model, const double* core,
+                                fstk_gpu_error* err);
+int32_t fstk_gpu_model_get_core(const fstk_gpu_model* model, double* core,
+                                fstk_gpu_error* err);
+
+/* Vector evaluate_batch(const Model&, const Matrix& points)  (model.cpp:208-227).
+ * points: host, Q x d column-major (the Eigen buffer as-is); out: host, Q. */
+int32_t fstk_gpu_evaluate_batch(const fstk_gpu_model* model, const double* points,
+                                int64_t q, int32_t d, double* out,
+                                fstk_gpu_error* err);
+/* double evaluate(const Model&, const std::vector<double>& y) (model.cpp:195-206). */
+int32_t fstk_gpu_evaluate(const fstk_gpu_model* model, const double* y, int32_t d,
+                          double* out, fstk_gpu_error* err);
+/* Device-resident variant: points column-major with leading dimension ld >= q,
+ * out device, enqueued on `stream` (cudaStream_t or NULL for the legacy
+ * stream); returns after enqueue unless a Domain error must be reported, which
+ * requires one 16-byte read-back of the error flag (done on the same stream). */
+int32_t fstk_gpu_evaluate_batch_device(const fstk_gpu_model* model,
+                                       const double* points, int64_t ld,
+                                       int64_t q, int32_t d, double* out,
+                                       void* stream, fstk_gpu_error* err);
+/* Vector Model::mode_values(int mode, double x) (model.cpp:71-94), batched:
+ * out is n x r_mode column-major (host). */
+int32_t fstk_gpu_mode_values(const fstk_gpu_model* model, int32_t mode,
+                             const double* x, int64_t n, double* out,
+                             fstk_gpu_error* err);
+
+/* Matrix build_design_rows(const Model&, const Matrix& points) (randls.cpp:134-145):
+ * w is Q x R column-major (host). */
+int32_t fstk_gpu_build_design_rows(const fstk_gpu_model* model,
+                                   const double* points, int64_t q, int32_t d,
+                                   double* w, fstk_gpu_error* err);
+/* SketchedSystem sketch(const Matrix& w, const Vector& u, const SketchConfig&)
+ * (randls.cpp:147-184): a is rows x r column-major with rows = S (2S for FFT),
+ * b has rows entries; padded_rows receives Q_pad. */
+int32_t fstk_gpu_sketch(const double* w, const double* u, int64_t q, int64_t r,
+                        const fstk_sketch_cfg* cfg, double* a, double* b,
+                        uint64_t* padded_rows, fstk_gpu_error* err);
+/* Matrix mixed_matrix(const Matrix& w, const SketchConfig&) (randls.cpp:186-225):
+ * out is Q_pad x r (2 Q_pad x r for FFT) column-major. */
+int32_t fstk_gpu_mixed_matrix(const double* w, int64_t q, int64_t r,
+                              const fstk_sketch_cfg* cfg, double* out,
+                              fstk_gpu_error* err);
+
+/* ReestimateResult reestimate_core(const Model&, const PointCloud&, const SketchConfig&)
+ * (randls.cpp:360-383).  points: host Q x d column-major, values: host Q.
+ * core_out: host prod(ranks) (the new core, mode-0 fastest); the caller
+ * builds the new model with with_core.  The refit runs on one GPU. */
+int32_t fstk_gpu_reestimate_core(const fstk_gpu_model* model, const double* points,
+                                 const double* values, int64_t q, int32_t d,
+                                 const fstk_sketch_cfg* cfg, double* core_out,
+                                 fstk_reestimate_info* info, fstk_gpu_error* err);
+
+/* Staged refit for point/row-sharded multi-GPU runs (one process per GPU):
+ * begin() does the host RNG plan (bit-exact, identical on every rank), the
+ * gathers, mode tables and the sketch of the rows this shard owns
+ * (sampled rows [S*shard/shards, S*(shard+1)/shards)); normal_equations()
+ * writes this shard's partial A^T A (R x R, full symmetric, column-major) and
+ * A^T b into caller-provided DEVICE buffers so the caller can sum them across
+ * ranks (one NCCL all-reduce); solve() runs the Cholesky solve on the summed
+ * system and the validation residuals. */
+int32_t fstk_gpu_refit_begin(const fstk_gpu_model* model, const double* points,
+                             const double* values, int64_t q, int32_t d,
+                             const fstk_sketch_cfg* cfg, int32_t shard,
+                             int32_t shards, fstk_gpu_refit** out,
+                             fstk_reestimate_info* info, fstk_gpu_error* err);
+int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* refit, double* gram,
+                                        double* rhs, fstk_reestimate_info* info,
+                                        fstk_gpu_error* err);
+int32_t fstk_gpu_refit_solve(fstk_gpu_refit* refit, const double* gram,
+                             const double* rhs, double* core_out,
+                             fstk_reestimate_info* info, fstk_gpu_error* err);
+void fstk_gpu_refit_end(fstk_gpu_refit* refit);
+/* Diagnostics/tests: host copies of the sampled padded rows (S u64) and, when
+ * the refit kept it, this shard's sketched block A (rows_local x R col-major)
+ * and b. */
+int32_t fstk_gpu_refit_rows(const fstk_gpu_refit* refit, uint64_t* rows,
+                            fstk_gpu_error* err);
+int32_t fstk_gpu_refit_sketched(const fstk_gpu_refit* refit, double* a,
+                                double* b, int64_t* rows_local,
+                                fstk_gpu_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSTK_GPU_H_ */

@@ -1,0 +1,153 @@
+"""ctypes binding of libfstk_gpu.so (the C-ABI declared in include/fstk_gpu.h).
+
+There is no CPU fallback: if the CUDA library is missing, or no GPU is
+visible when a compute entry point is called, this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfstk_gpu.so")
+
+KINDS = ["Parameter", "Shape", "Domain", "Data", "Io", "Decode", "Compute"]
+TRANSFORMS = {"dct": 0, "wht": 1, "fft": 2}
+
+
+class FstkError(Exception):
+    """Base class; `kind` is the fstk::ErrorKind name (error.hpp:11-19)."""
+
+    def __init__(self, kind: str, message: str, mode: int = -1, index: int = -1,
+                 value: float = 0.0):
+        super().__init__(message)
+        self.kind = kind
+        self.mode = mode
+        self.index = index
+        self.value = value
+
+
+class FstkValueError(FstkError, ValueError):
+    """Parameter/Shape/Domain/Data/Compute errors -> ValueError (module.cpp:112-125)."""
+
+
+class FstkIOError(FstkError, OSError):
+    """Io/Decode errors -> IOError (module.cpp:117-119)."""
+
+
+def make_error(code: int, message: str, mode=-1, index=-1, value=0.0) -> FstkError:
+    kind = KINDS[code - 1] if 1 <= code <= len(KINDS) else "Compute"
+    cls = FstkIOError if kind in ("Io", "Decode") else FstkValueError
+    return cls(kind, message, mode, index, value)
+
+
+class Err(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("mode", C.c_int32), ("index", C.c_int64),
+                ("value", C.c_double), ("message", C.c_char * 256)]
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("d", C.c_int32), ("ranks", C.POINTER(C.c_int64)),
+                ("core", C.POINTER(C.c_double)), ("family", C.POINTER(C.c_int32)),
+                ("degree", C.POINTER(C.c_int32)), ("resolution", C.POINTER(C.c_int32)),
+                ("lo", C.POINTER(C.c_double)), ("hi", C.POINTER(C.c_double)),
+                ("nnz", C.POINTER(C.c_uint32)), ("indices", C.POINTER(C.c_uint32)),
+                ("coeffs", C.POINTER(C.c_double))]
+
+
+class SketchCfg(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("working_subset", C.c_uint64),
+                ("sample_rows", C.c_uint64), ("transform", C.c_int32),
+                ("validation_fraction", C.c_double)]
+
+
+class ReestimateInfo(C.Structure):
+    _fields_ = [("residual_before", C.c_double), ("residual_after", C.c_double),
+                ("sample_rows", C.c_uint64), ("working_rows", C.c_uint64),
+                ("padded_rows", C.c_uint64), ("rank_deficient", C.c_int32),
+                ("held_out", C.c_int32), ("t_prepare", C.c_double), ("t_sketch", C.c_double),
+                ("t_gram", C.c_double), ("t_solve", C.c_double), ("t_residual", C.c_double)]
+
+
+# Every symbol include/fstk_gpu.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "fstk_gpu_abi_version", "fstk_gpu_device_count", "fstk_gpu_launch_count",
+    "fstk_gpu_model_create", "fstk_gpu_model_destroy", "fstk_gpu_model_set_core",
+    "fstk_gpu_model_get_core", "fstk_gpu_evaluate_batch", "fstk_gpu_evaluate",
+    "fstk_gpu_evaluate_batch_device", "fstk_gpu_mode_values", "fstk_gpu_build_design_rows",
+    "fstk_gpu_sketch", "fstk_gpu_mixed_matrix", "fstk_gpu_reestimate_core",
+    "fstk_gpu_refit_begin", "fstk_gpu_refit_normal_equations", "fstk_gpu_refit_solve",
+    "fstk_gpu_refit_end", "fstk_gpu_refit_rows", "fstk_gpu_refit_sketched",
+]
+
+_LIB = None
+DP = C.POINTER(C.c_double)
+VP = C.c_void_p
+
+
+def lib():
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    L.fstk_gpu_abi_version.restype = C.c_int32
+    L.fstk_gpu_device_count.restype = C.c_int32
+    L.fstk_gpu_launch_count.restype = C.c_uint64
+    L.fstk_gpu_model_create.argtypes = [C.POINTER(ModelDesc), C.c_int32, C.POINTER(VP),
+                                        C.POINTER(Err)]
+    L.fstk_gpu_model_destroy.argtypes = [VP]
+    L.fstk_gpu_model_destroy.restype = None
+    L.fstk_gpu_model_set_core.argtypes = [VP, DP, C.POINTER(Err)]
+    L.fstk_gpu_model_get_core.argtypes = [VP, DP, C.POINTER(Err)]
+    L.fstk_gpu_evaluate_batch.argtypes = [VP, DP, C.c_int64, C.c_int32, DP, C.POINTER(Err)]
+    L.fstk_gpu_evaluate.argtypes = [VP, DP, C.c_int32, DP, C.POINTER(Err)]
+    L.fstk_gpu_evaluate_batch_device.argtypes = [VP, VP, C.c_int64, C.c_int64, C.c_int32, VP,
+                                                 VP, C.POINTER(Err)]
+    L.fstk_gpu_mode_values.argtypes = [VP, C.c_int32, DP, C.c_int64, DP, C.POINTER(Err)]
+    L.fstk_gpu_build_design_rows.argtypes = [VP, DP, C.c_int64, C.c_int32, DP, C.POINTER(Err)]
+    L.fstk_gpu_sketch.argtypes = [DP, DP, C.c_int64, C.c_int64, C.POINTER(SketchCfg), DP, DP,
+                                  C.POINTER(C.c_uint64), C.POINTER(Err)]
+    L.fstk_gpu_mixed_matrix.argtypes = [DP, C.c_int64, C.c_int64, C.POINTER(SketchCfg), DP,
+                                        C.POINTER(Err)]
+    L.fstk_gpu_reestimate_core.argtypes = [VP, DP, DP, C.c_int64, C.c_int32,
+                                           C.POINTER(SketchCfg), DP, C.POINTER(ReestimateInfo),
+                                           C.POINTER(Err)]
+    L.fstk_gpu_refit_begin.argtypes = [VP, DP, DP, C.c_int64, C.c_int32, C.POINTER(SketchCfg),
+                                       C.c_int32, C.c_int32, C.POINTER(VP),
+                                       C.POINTER(ReestimateInfo), C.POINTER(Err)]
+    L.fstk_gpu_refit_normal_equations.argtypes = [VP, VP, VP, C.POINTER(ReestimateInfo),
+                                                  C.POINTER(Err)]
+    L.fstk_gpu_refit_solve.argtypes = [VP, VP, VP, DP, C.POINTER(ReestimateInfo),
+                                       C.POINTER(Err)]
+    L.fstk_gpu_refit_end.argtypes = [VP]
+    L.fstk_gpu_refit_end.restype = None
+    L.fstk_gpu_refit_rows.argtypes = [VP, C.POINTER(C.c_uint64), C.POINTER(Err)]
+    L.fstk_gpu_refit_sketched.argtypes = [VP, DP, DP, C.POINTER(C.c_int64), C.POINTER(Err)]
+    _LIB = L
+    return L
+
+
+def check(rc: int, err: Err):
+    if rc != 0:
+        raise make_error(rc, err.message.decode(errors="replace"), err.mode, err.index, err.value)
+
+
+def dptr(a):
+    return a.ctypes.data_as(DP)
+
+
+def launch_count() -> int:
+    return int(lib().fstk_gpu_launch_count())
+
+
+def device_count() -> int:
+    return int(lib().fstk_gpu_device_count())
+
+
+def require_gpu():
+    if device_count() < 1:
+        raise RuntimeError("fstk_gpu: no CUDA device visible (the B200 path has no CPU fallback)")

@@ -1,0 +1,209 @@
+// Shared device/host helpers for the fstk B200 library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "fstk_gpu.h"
+
+namespace fstk_gpu {
+
+// ------------------------------------------------------------ errors ------
+// Host-side exception carrying an fstk ErrorKind (+1 = status code); caught
+// at the C-ABI and converted to a status, never thrown across it.
+struct Error {
+  int code;
+  std::string msg;
+  int mode = -1;
+  int64_t index = -1;
+  double value = 0.0;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error{code, m}; }
+inline void require(bool c, int code, const char* m) {
+  if (!c) fail(code, m);
+}
+
+#define FSTK_CUDA(call)                                                       \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      ::fstk_gpu::fail(FSTK_E_COMPUTE, std::string("CUDA: ") + #call + ": " + \
+                                           cudaGetErrorString(e_));           \
+  } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+inline void check_launch(const char* what) {
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(FSTK_E_COMPUTE, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int32_t guarded(fstk_gpu_error* err, F&& f) {
+  if (err) {
+    err->kind = 0;
+    err->mode = -1;
+    err->index = -1;
+    err->value = 0.0;
+    err->message[0] = 0;
+  }
+  try {
+    f();
+    return FSTK_OK;
+  } catch (const Error& e) {
+    if (err) {
+      err->kind = e.code;
+      err->mode = e.mode;
+      err->index = e.index;
+      err->value = e.value;
+      std::snprintf(err->message, sizeof(err->message), "%s", e.msg.c_str());
+    }
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (err) {
+      err->kind = FSTK_E_COMPUTE;
+      std::snprintf(err->message, sizeof(err->message), "host allocation failed");
+    }
+    return FSTK_E_COMPUTE;
+  } catch (const std::exception& e) {
+    if (err) {
+      err->kind = FSTK_E_COMPUTE;
+      std::snprintf(err->message, sizeof(err->message), "%s", e.what());
+    }
+    return FSTK_E_COMPUTE;
+  }
+}
+
+// Scoped device selection (restores the caller's current device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) FSTK_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// RAII device buffer.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) return;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      fail(FSTK_E_COMPUTE, "device allocation of " + std::to_string(count * sizeof(T)) +
+                               " bytes failed: " + cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+// ------------------------------------------------- exact fp64 arithmetic ---
+// The reference is compiled for x86-64 without FMA (proj/CMakeLists.txt,
+// Release, no -march); where the product must reproduce its bits, every
+// product and sum is rounded separately (no contraction).
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+// Correctly rounded a / b for b a small positive integer, given rcp =
+// RN(1/b): Markstein's correction q1 = RN(q0 + RN?(a - b q0) * rcp).
+__device__ __forceinline__ double xdiv_small(double a, double b, double rcp) {
+  const double q0 = __dmul_rn(a, rcp);
+  const double r = __fma_rn(-q0, b, a);
+  return __fma_rn(r, rcp, q0);
+}
+
+// ------------------------------------------------ mbarrier + bulk copy ---
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D bulk copy global -> shared (TMA engine, UBLKCP), completion counted in
+// bytes on the mbarrier.  bytes % 16 == 0, both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------- DMMA ---
+// D(8x8) += A(8x4, row) * B(4x8, col), fp64 tensor-core MMA (SASS DMMA.8x8x4).
+// Fragments (lane = 4*g + t): a = A[g][t], b = B[t][g], c0/c1 = C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+}  // namespace fstk_gpu

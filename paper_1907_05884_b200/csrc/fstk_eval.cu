@@ -1,0 +1,897 @@
+// fstk B200 library — model upload and point evaluation (sm_100a).
+//
+// Replaces, on the GPU, the reference evaluation path
+//   evaluate_batch (proj/src/model.cpp:208-227)
+//     -> mode_values (model.cpp:71-94) -> eval_basis/to_reference/legendre_values
+//        (proj/src/basis.cpp:49-61, 215-234)
+//     -> contract_core (model.cpp:176-191)
+// with two kernels:
+//   K1a mode_tables_kernel: per point and mode, domain map + Legendre
+//       recurrence (bit-exact: same rounding sequence, Markstein-corrected
+//       division) + sparse coefficient dot -> u_k tables in HBM/L2;
+//   K1b contract_kernel: the core contraction as fp64 tensor-core (DMMA
+//       m8n8k4) tiles T = U_0 * G_(0) with a fused per-point bilinear
+//       epilogue y += (sum_j1 T u_1) * prod_{k>=2} u_k, the core streamed
+//       through a TMA bulk-copy / mbarrier ring (warp-specialised producer).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "fstk_internal.h"
+
+namespace fstk_gpu {
+
+std::atomic<uint64_t> g_launches{0};
+
+// Legendre constants: for n = 1..63, (2n+1), n, n+1, RN(1/(n+1)); and
+// norm[n] = sqrt(2n+1) exactly as basis.cpp:54,59 computes it.
+struct LegConst {
+  double a[kMaxDegree + 1];    // 2n+1
+  double b[kMaxDegree + 1];    // n
+  double c[kMaxDegree + 1];    // n+1
+  double rc[kMaxDegree + 1];   // RN(1/(n+1))
+  double norm[kMaxDegree + 2]; // sqrt(2n+1); norm[1] = sqrt(3)
+};
+__constant__ LegConst c_leg;
+
+static void upload_leg_constants(int device) {
+  LegConst h;
+  for (int n = 0; n <= kMaxDegree; ++n) {
+    h.a[n] = static_cast<double>(2 * n + 1);
+    h.b[n] = static_cast<double>(n);
+    h.c[n] = static_cast<double>(n + 1);
+    h.rc[n] = 1.0 / static_cast<double>(n + 1);
+  }
+  for (int n = 0; n <= kMaxDegree + 1; ++n) h.norm[n] = std::sqrt(2.0 * n + 1.0);
+  h.norm[1] = std::sqrt(3.0);
+  FSTK_CUDA(cudaMemcpyToSymbol(c_leg, &h, sizeof(h)));
+}
+
+int device_sm_count(int device) {
+  int n = 0;
+  FSTK_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+  return n;
+}
+
+// ---------------------------------------------------------- K1a modes ---
+// Thread per output row; Legendre values of the current mode staged in
+// shared memory (column per thread) so the sparse dot can gather them.
+template <bool EXACT>
+__global__ void __launch_bounds__(128) mode_tables_kernel(
+    ModesDev M, int mode_begin, int mode_end, const double* __restrict__ pts, int64_t ldp,
+    int64_t n, int64_t n_out, const int64_t* __restrict__ row_src, double* __restrict__ tables,
+    Int64x8 toff, int64_t ldt, unsigned long long* err_row) {
+  extern __shared__ double Ls[];  // (pmax+1) x blockDim
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  int64_t src = i;
+  bool valid = i < n;
+  if (row_src && i < n_out) {
+    src = i < n ? row_src[i] : -1;
+    valid = src >= 0;
+  }
+  for (int k = mode_begin; k < mode_end; ++k) {
+    const ModeDev& md = M.m[k];
+    double* tk = tables + toff.v[k];
+    if (i >= n_out) continue;
+    if (!valid) {
+      for (int j = 0; j < md.r; ++j) tk[j * ldt + i] = 0.0;
+      continue;
+    }
+    const double x = pts[k * ldp + src];
+    // to_reference (basis.cpp:215-222): Domain error beyond the slack, clamp within.
+    double t;
+    if (!(x >= md.lo - md.slack && x <= md.hi + md.slack)) {
+      atomicMin(err_row, static_cast<unsigned long long>(i));
+      t = 0.0;
+    } else {
+      const double cl = fmin(md.hi, fmax(md.lo, x));
+      t = xadd(-1.0, __ddiv_rn(xmul(2.0, xsub(cl, md.lo)), md.span));
+    }
+    // legendre_values (basis.cpp:49-61), same rounding sequence.
+    const int p = md.pmax;
+    Ls[tid] = 1.0;
+    if (p >= 1) Ls[nt + tid] = xmul(c_leg.norm[1], t);
+    double pm1 = 1.0, pm0 = t;
+    for (int q = 1; q < p; ++q) {
+      const double num = xsub(xmul(xmul(c_leg.a[q], t), pm0), xmul(c_leg.b[q], pm1));
+      const double pn1 = xdiv_small(num, c_leg.c[q], c_leg.rc[q]);
+      pm1 = pm0;
+      pm0 = pn1;
+      Ls[(q + 1) * nt + tid] = xmul(c_leg.norm[q + 1], pn1);
+    }
+    // Sparse dot in ascending index order (model.cpp:86-88).
+    for (int j = 0; j < md.r; ++j) {
+      double v = 0.0;
+      const int e = md.rowptr[j + 1];
+      for (int s = md.rowptr[j]; s < e; ++s) {
+        const double c = md.coef[s];
+        const double l = Ls[md.idx[s] * nt + tid];
+        v = EXACT ? xadd(v, xmul(c, l)) : fma(c, l, v);
+      }
+      tk[j * ldt + i] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------- K1b contract ---
+constexpr int TP = 128;        // points per CTA tile
+constexpr int U0_LD = TP + 4;  // u0 column stride: conflict-free A fragments
+constexpr int U1_LD = TP + 2;  // u1 column stride: conflict-free epilogue reads
+constexpr int NCW = 8;         // consumer warps: 4 point groups x 2 column halves
+constexpr int NTHREADS = (NCW + 1) * 32;
+
+struct ContractParams {
+  const double* tables;
+  Int64x8 toff;
+  int64_t ldt;
+  int64_t n;
+  int64_t ntiles;
+  int d;
+  int r[kMaxOrder];
+  int Kp, N1p, NC, Mout, N1;  // N1 = rows of u1 staged (NC * N1p)
+  int nstage;
+  const double* bpack;
+  double* out;
+};
+
+struct SmemLayout {
+  size_t bars, u0, u1, uk, bst, ybuf, total;
+  size_t ukoff[kMaxOrder];
+};
+
+__host__ __device__ inline SmemLayout smem_layout(const ContractParams& P) {
+  SmemLayout L{};
+  size_t o = 0;
+  L.bars = o;
+  o += ((2 * P.nstage + 2) * 8 + 127) / 128 * 128;
+  L.u0 = o;
+  o += static_cast<size_t>(P.Kp) * U0_LD * 8;
+  L.u1 = o;
+  o += static_cast<size_t>(P.N1) * U1_LD * 8;
+  L.uk = o;
+  for (int k = 2; k < P.d; ++k) {
+    L.ukoff[k] = o;
+    o += static_cast<size_t>(P.r[k]) * TP * 8;
+  }
+  o = (o + 127) / 128 * 128;
+  L.bst = o;
+  o += static_cast<size_t>(P.nstage) * P.Kp * P.N1p * 8;
+  L.ybuf = o;
+  o += 2 * TP * 8;
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
+}
+
+template <int NSW>
+__global__ void __launch_bounds__(NTHREADS, 1) contract_kernel(const ContractParams P) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const SmemLayout L = smem_layout(P);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + P.nstage;
+  uint64_t* ufull = empty + P.nstage;
+  uint64_t* uempty = ufull + 1;
+  double* u0s = reinterpret_cast<double*>(smem + L.u0);
+  double* u1s = reinterpret_cast<double*>(smem + L.u1);
+  double* bst = reinterpret_cast<double*>(smem + L.bst);
+  double* ybuf = reinterpret_cast<double*>(smem + L.ybuf);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int NT = P.NC * P.Mout;
+  const int stage_elems = P.Kp * P.N1p;
+  const uint32_t stage_bytes = static_cast<uint32_t>(stage_elems) * 8u;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    mbar_init(ufull, 1);
+    mbar_init(uempty, NCW);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ===== producer warp: u tables per tile + core tiles ring (TMA bulk) =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x, ++it) {
+        if (it > 0) mbar_wait(uempty, (it - 1) & 1);
+        uint32_t ubytes = static_cast<uint32_t>(P.Kp + P.N1) * TP * 8u;
+        for (int k = 2; k < P.d; ++k) ubytes += static_cast<uint32_t>(P.r[k]) * TP * 8u;
+        mbar_arrive_expect_tx(ufull, ubytes);
+        const int64_t row0 = tile * TP;
+        const double* t0 = P.tables + P.toff.v[0] + row0;
+        for (int j = 0; j < P.Kp; ++j) bulk_g2s(u0s + j * U0_LD, t0 + j * P.ldt, TP * 8, ufull);
+        const double* t1 = P.tables + P.toff.v[1] + row0;
+        for (int j = 0; j < P.N1; ++j) bulk_g2s(u1s + j * U1_LD, t1 + j * P.ldt, TP * 8, ufull);
+        for (int k = 2; k < P.d; ++k) {
+          double* dst = reinterpret_cast<double*>(smem + L.ukoff[k]);
+          const double* tk = P.tables + P.toff.v[k] + row0;
+          for (int j = 0; j < P.r[k]; ++j) bulk_g2s(dst + j * TP, tk + j * P.ldt, TP * 8, ufull);
+        }
+        for (int tt = 0; tt < NT; ++tt) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], stage_bytes);
+          bulk_g2s(bst + static_cast<size_t>(stage) * stage_elems,
+                   P.bpack + static_cast<size_t>(tt) * stage_elems, stage_bytes, &full[stage]);
+          if (++stage == P.nstage) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ===== consumer warps =====
+  const int pg = warp & 3;   // 32-point group
+  const int nh = warp >> 2;  // column half
+  const int g = lane >> 2, t = lane & 3;
+  const int NS = 2 * NSW;
+  int stage = 0;
+  uint32_t phase = 0;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x, ++it) {
+    mbar_wait(ufull, it & 1);
+    double y[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int tt = 0; tt < NT; ++tt) {
+      const int c = tt % P.NC;
+      const int m = tt / P.NC;
+      mbar_wait(&full[stage], phase);
+      const double* B = bst + static_cast<size_t>(stage) * stage_elems;
+      double acc[4][NSW][2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < NSW; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      const double* ua = u0s + t * U0_LD + pg * 32 + g;
+      const double* bb = B + (nh * NSW) * 32 + lane;
+      for (int ks = 0; ks < P.Kp / 4; ++ks) {
+        double av[4], bv[NSW];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = ua[(4 * ks) * U0_LD + a * 8];
+#pragma unroll
+        for (int b = 0; b < NSW; ++b) bv[b] = bb[(ks * NS + b) * 32];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < NSW; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == P.nstage) {
+        stage = 0;
+        phase ^= 1;
+      }
+      // Epilogue: W = sum_j1 T u1; y += W * prod_{k>=2} u_k.
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int row = pg * 32 + a * 8 + g;
+        double o = 1.0;
+        int rem = m;
+        for (int k = 2; k < P.d; ++k) {
+          const int jk = rem % P.r[k];
+          rem /= P.r[k];
+          o *= reinterpret_cast<const double*>(smem + L.ukoff[k])[jk * TP + row];
+        }
+        double w = 0.0;
+#pragma unroll
+        for (int b = 0; b < NSW; ++b) {
+          const int j1 = c * P.N1p + (nh * NSW + b) * 8 + 2 * t;
+          w = fma(acc[a][b][0], u1s[j1 * U1_LD + row], w);
+          w = fma(acc[a][b][1], u1s[(j1 + 1) * U1_LD + row], w);
+        }
+        y[a] = fma(w, o, y[a]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(uempty);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      y[a] += __shfl_xor_sync(0xffffffffu, y[a], 1);
+      y[a] += __shfl_xor_sync(0xffffffffu, y[a], 2);
+      if (t == 0) ybuf[nh * TP + pg * 32 + a * 8 + g] = y[a];
+    }
+    consumer_bar();
+    if (nh == 0) {
+      const int row = pg * 32 + lane;
+      const int64_t gi = tile * TP + row;
+      if (gi < P.n) P.out[gi] = ybuf[row] + ybuf[TP + row];
+    }
+    consumer_bar();
+  }
+}
+
+// Generic contraction (any d <= 8, any ranks): thread per point, core read
+// through L1/L2 with incremental multi-index; used when the DMMA layout does
+// not apply (d == 1, or shared-memory budget exceeded).
+__global__ void contract_generic_kernel(const double* __restrict__ tables, Int64x8 toff,
+                                        int64_t ldt, int64_t n, int d, Int64x8 ranks,
+                                        const double* __restrict__ core, int64_t R,
+                                        double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int j[kMaxOrder] = {0};
+  double y = 0.0;
+  for (int64_t lin = 0; lin < R; ++lin) {
+    double w = core[lin];
+    for (int k = 0; k < d; ++k) w *= tables[toff.v[k] + j[k] * ldt + i];
+    y += w;
+    for (int k = 0; k < d; ++k) {
+      if (++j[k] < ranks.v[k]) break;
+      j[k] = 0;
+    }
+  }
+  out[i] = y;
+}
+
+// ------------------------------------------------------------- launches ---
+static void mode_kernel_attrs(int device) {
+  static std::once_flag once[64];
+  std::call_once(once[device & 63], [&] {
+    const int bytes = (kMaxDegree + 1) * 128 * static_cast<int>(sizeof(double));
+    FSTK_CUDA(cudaFuncSetAttribute(mode_tables_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    FSTK_CUDA(cudaFuncSetAttribute(mode_tables_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  });
+}
+
+static size_t mode_smem(const fstk_gpu_model* m, int k0, int k1, int threads) {
+  mode_kernel_attrs(m->device);
+  int pm = 0;
+  for (int k = k0; k < k1; ++k) pm = std::max(pm, m->modes[k].pmax);
+  return static_cast<size_t>(pm + 1) * threads * sizeof(double);
+}
+
+void launch_mode_tables(const fstk_gpu_model* m, const double* pts, int64_t ldp, int64_t n,
+                        int64_t n_out, const int64_t* row_src, double* tables,
+                        const int64_t* toff, int64_t ldt, bool exact,
+                        unsigned long long* err_row, cudaStream_t s) {
+  if (n_out <= 0) return;
+  const int threads = 128;
+  Int64x8 to{};
+  for (int k = 0; k < m->d; ++k) to.v[k] = toff[k];
+  const size_t sm = mode_smem(m, 0, m->d, threads);
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n_out, threads));
+  if (exact)
+    mode_tables_kernel<true><<<blocks, threads, sm, s>>>(m->modes_dev, 0, m->d, pts, ldp, n,
+                                                         n_out, row_src, tables, to, ldt, err_row);
+  else
+    mode_tables_kernel<false><<<blocks, threads, sm, s>>>(m->modes_dev, 0, m->d, pts, ldp, n,
+                                                          n_out, row_src, tables, to, ldt, err_row);
+  check_launch("mode_tables_kernel");
+}
+
+void launch_mode_table_one(const fstk_gpu_model* m, int mode, const double* x, int64_t n,
+                           double* out, int64_t ldt, bool exact, unsigned long long* err_row,
+                           cudaStream_t s) {
+  if (n <= 0) return;
+  const int threads = 128;
+  Int64x8 to{};
+  // pts pointer is shifted so that pts[mode * ldp + i] == x[i] with ldp = 0.
+  to.v[mode] = 0;
+  const size_t sm = mode_smem(m, mode, mode + 1, threads);
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n, threads));
+  const double* pts = x;  // ldp = 0 => pts[mode*0 + i]
+  if (exact)
+    mode_tables_kernel<true><<<blocks, threads, sm, s>>>(m->modes_dev, mode, mode + 1, pts, 0, n,
+                                                         n, nullptr, out, to, ldt, err_row);
+  else
+    mode_tables_kernel<false><<<blocks, threads, sm, s>>>(m->modes_dev, mode, mode + 1, pts, 0,
+                                                          n, n, nullptr, out, to, ldt, err_row);
+  check_launch("mode_tables_kernel(one)");
+}
+
+void eval_table_offsets(const fstk_gpu_model* m, int64_t ldt, int64_t* toff, int64_t* total) {
+  int64_t o = 0;
+  for (int k = 0; k < m->d; ++k) {
+    toff[k] = o;
+    o += static_cast<int64_t>(m->rp[k]) * ldt;
+  }
+  *total = o;
+}
+
+static ContractParams make_params(const fstk_gpu_model* m, const double* tables,
+                                  const int64_t* toff, int64_t ldt, int64_t n, double* out) {
+  ContractParams P{};
+  P.tables = tables;
+  for (int k = 0; k < m->d; ++k) P.toff.v[k] = toff[k];
+  P.ldt = ldt;
+  P.n = n;
+  P.ntiles = ceil_div(n, TP);
+  P.d = m->d;
+  for (int k = 0; k < m->d; ++k) P.r[k] = static_cast<int>(m->ranks[k]);
+  P.Kp = m->lay.Kp;
+  P.N1p = m->lay.N1p;
+  P.NC = m->lay.NC;
+  P.Mout = m->lay.Mout;
+  P.N1 = m->lay.NC * m->lay.N1p;
+  P.nstage = m->lay.nstage;
+  P.bpack = m->d_bpack.p;
+  P.out = out;
+  return P;
+}
+
+template <int NSW>
+static void launch_contract_t(const fstk_gpu_model* m, const ContractParams& P, cudaStream_t s) {
+  static std::once_flag once[64];
+  const size_t smem = m->lay.smem;
+  std::call_once(once[m->device & 63], [&] {
+    int optin = 0;
+    FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+    FSTK_CUDA(cudaFuncSetAttribute(contract_kernel<NSW>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  });
+  const int64_t grid = std::min<int64_t>(P.ntiles, m->num_sms);
+  contract_kernel<NSW><<<static_cast<unsigned>(grid), NTHREADS, smem, s>>>(P);
+  check_launch("contract_kernel");
+}
+
+void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_t* toff,
+                     int64_t ldt, int64_t n, double* out, cudaStream_t s,
+                     const double* bpack_override, const double* core_override) {
+  if (n <= 0) return;
+  if (!m->lay.fast) {
+    Int64x8 to{}, rk{};
+    for (int k = 0; k < m->d; ++k) {
+      to.v[k] = toff[k];
+      rk.v[k] = m->ranks[k];
+    }
+    contract_generic_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, s>>>(
+        tables, to, ldt, n, m->d, rk, core_override ? core_override : m->d_core.p, m->R, out);
+    check_launch("contract_generic_kernel");
+    return;
+  }
+  ContractParams P = make_params(m, tables, toff, ldt, n, out);
+  if (bpack_override) P.bpack = bpack_override;
+  switch (m->lay.nsw) {
+    case 1: launch_contract_t<1>(m, P, s); break;
+    case 2: launch_contract_t<2>(m, P, s); break;
+    case 3: launch_contract_t<3>(m, P, s); break;
+    case 4: launch_contract_t<4>(m, P, s); break;
+    default: fail(FSTK_E_COMPUTE, "internal: bad contraction layout");
+  }
+}
+
+// ------------------------------------------------------------ model setup ---
+static void plan_layout(fstk_gpu_model* m) {
+  ContractLayout& L = m->lay;
+  L = ContractLayout{};
+  for (int k = 0; k < m->d; ++k) m->rp[k] = static_cast<int>(m->ranks[k]);
+  if (m->d < 2) return;
+  const int r0 = static_cast<int>(m->ranks[0]), r1 = static_cast<int>(m->ranks[1]);
+  L.Kp = static_cast<int>(round_up(r0, 4));
+  const int r1p = static_cast<int>(round_up(r1, 16));
+  L.N1p = std::min(r1p, 64);
+  L.NC = static_cast<int>(ceil_div(r1, L.N1p));
+  L.Mout = 1;
+  for (int k = 2; k < m->d; ++k) L.Mout *= static_cast<int>(m->ranks[k]);
+  L.nsw = L.N1p / 16;
+  L.btile_elems = static_cast<int64_t>(L.Kp) * L.N1p;
+  m->rp[0] = L.Kp;
+  m->rp[1] = L.NC * L.N1p;
+  int optin = 0;
+  FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  for (int ns = 4; ns >= 2; --ns) {
+    ContractParams P{};
+    P.d = m->d;
+    for (int k = 0; k < m->d; ++k) P.r[k] = static_cast<int>(m->ranks[k]);
+    P.Kp = L.Kp;
+    P.N1p = L.N1p;
+    P.NC = L.NC;
+    P.N1 = L.NC * L.N1p;
+    P.nstage = ns;
+    const SmemLayout S = smem_layout(P);
+    if (S.total <= static_cast<size_t>(optin)) {
+      L.nstage = ns;
+      L.smem = S.total;
+      L.fast = true;
+      break;
+    }
+  }
+  if (!L.fast) {
+    for (int k = 0; k < m->d; ++k) m->rp[k] = static_cast<int>(m->ranks[k]);
+  }
+}
+
+static void pack_core_into(const fstk_gpu_model* m, const double* core, DevBuf<double>& out) {
+  const ContractLayout& L = m->lay;
+  if (!L.fast) return;
+  const int r0 = static_cast<int>(m->ranks[0]), r1 = static_cast<int>(m->ranks[1]);
+  const int NS = L.N1p / 8;
+  const int64_t NT = static_cast<int64_t>(L.NC) * L.Mout;
+  std::vector<double> bp(static_cast<size_t>(NT * L.btile_elems), 0.0);
+  for (int64_t tt = 0; tt < NT; ++tt) {
+    const int c = static_cast<int>(tt % L.NC);
+    const int64_t mo = tt / L.NC;
+    double* tile = bp.data() + tt * L.btile_elems;
+    for (int ks = 0; ks < L.Kp / 4; ++ks)
+      for (int ns = 0; ns < NS; ++ns)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int k = 4 * ks + (lane & 3);
+          const int j1 = c * L.N1p + 8 * ns + (lane >> 2);
+          double v = 0.0;
+          if (k < r0 && j1 < r1)
+            v = core[static_cast<size_t>(k + static_cast<int64_t>(r0) * (j1 + static_cast<int64_t>(r1) * mo))];
+          tile[(ks * NS + ns) * 32 + lane] = v;
+        }
+  }
+  out.alloc(bp.size());
+  FSTK_CUDA(cudaMemcpy(out.p, bp.data(), bp.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+static void pack_core(fstk_gpu_model* m) { pack_core_into(m, m->core.data(), m->d_bpack); }
+
+static void upload_core(fstk_gpu_model* m) {
+  FSTK_CUDA(cudaMemcpy(m->d_core.p, m->core.data(), m->core.size() * sizeof(double),
+                       cudaMemcpyHostToDevice));
+  pack_core(m);
+}
+
+[[noreturn]] void throw_domain(const fstk_gpu_model* m, int64_t row, const double* y) {
+  Error e{FSTK_E_DOMAIN, "point outside basis domain"};
+  e.index = row;
+  for (int k = 0; k < m->d; ++k) {
+    const ModeHost& mh = m->modes[k];
+    const double span = mh.hi - mh.lo;
+    const double slack = 1e-12 * span;
+    if (!(y[k] >= mh.lo - slack && y[k] <= mh.hi + slack)) {
+      e.mode = k;
+      e.value = y[k];
+      break;
+    }
+  }
+  throw e;
+}
+
+// Evaluates n device-resident points in chunks of the model's workspace,
+// optionally with a replacement core (host pointer, e.g. a refit result).
+void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, const double* pts,
+                          int64_t ldp, int64_t n, double* out, cudaStream_t s) {
+  Chunk& ck = m->chunk[0];
+  const int64_t CH = m->chunk_points;
+  int64_t toff[kMaxOrder], tot = 0;
+  const int64_t ldt = round_up(CH, TP);
+  eval_table_offsets(m, ldt, toff, &tot);
+  DevBuf<double> bp, craw;
+  if (core_host) {
+    pack_core_into(m, core_host, bp);
+    craw.alloc(m->R);
+    FSTK_CUDA(cudaMemcpy(craw.p, core_host, m->R * 8, cudaMemcpyHostToDevice));
+  }
+  FSTK_CUDA(cudaMemsetAsync(ck.err.p, 0xff, sizeof(unsigned long long), s));
+  for (int64_t b = 0; b < n; b += CH) {
+    const int64_t nb = std::min(CH, n - b);
+    const int64_t nout = round_up(nb, TP);
+    launch_mode_tables(m, pts + b, ldp, nb, nout, nullptr, ck.tables.p, toff, ldt, false,
+                       ck.err.p, s);
+    launch_contract(m, ck.tables.p, toff, ldt, nb, out + b, s, core_host ? bp.p : nullptr,
+                    core_host ? craw.p : nullptr);
+  }
+  if (core_host) FSTK_CUDA(cudaStreamSynchronize(s));  // temporaries go out of scope
+}
+
+void evaluate_device(const fstk_gpu_model* m, const double* pts, int64_t ldp, int64_t n,
+                     double* out, cudaStream_t s) {
+  evaluate_device_core(m, nullptr, pts, ldp, n, out, s);
+}
+
+}  // namespace fstk_gpu
+
+using namespace fstk_gpu;
+
+fstk_gpu_model::~fstk_gpu_model() {
+  for (auto& c : chunk) {
+    if (c.stream) cudaStreamDestroy(c.stream);
+    if (c.done) cudaEventDestroy(c.done);
+  }
+}
+
+// ================================================================= C-ABI ===
+extern "C" {
+
+int32_t fstk_gpu_abi_version(void) { return FSTK_GPU_ABI_VERSION; }
+
+int32_t fstk_gpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+uint64_t fstk_gpu_launch_count(void) { return g_launches.load(); }
+
+int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_gpu_model** out,
+                              fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(desc != nullptr && out != nullptr, FSTK_E_PARAMETER, "null argument");
+    *out = nullptr;
+    const int d = desc->d;
+    // model.cpp:31-53 validate_structure + basis.cpp:30-47 validate.
+    require(d >= 1 && d <= kMaxOrder, FSTK_E_SHAPE, "model: mode count does not match core order");
+    auto m = std::make_unique<fstk_gpu_model>();
+    m->device = device;
+    m->d = d;
+    m->ranks.assign(desc->ranks, desc->ranks + d);
+    m->R = 1;
+    for (int k = 0; k < d; ++k) {
+      require(m->ranks[k] >= 1, FSTK_E_SHAPE, "model: empty mode");
+      m->R *= m->ranks[k];
+    }
+    m->core.assign(desc->core, desc->core + m->R);
+    m->modes.resize(d);
+    size_t f = 0, c = 0;
+    for (int k = 0; k < d; ++k) {
+      ModeHost& mh = m->modes[k];
+      mh.r = static_cast<int>(m->ranks[k]);
+      mh.rowptr.push_back(0);
+      for (int j = 0; j < mh.r; ++j, ++f) {
+        const int fam = desc->family[f], deg = desc->degree[f], res = desc->resolution[f];
+        const double lo = desc->lo[f], hi = desc->hi[f];
+        require(deg >= 0 && deg <= kMaxDegree, FSTK_E_PARAMETER, "basis degree must be in [0, 64]");
+        if (fam == 0) {
+          require(res == 0, FSTK_E_PARAMETER, "Legendre basis has no resolution parameter");
+        } else {
+          require(res >= 0 && res <= 20, FSTK_E_PARAMETER, "wavelet resolution must be in [0, 20]");
+          require((static_cast<long long>(deg + 1) << res) <= (1 << 24), FSTK_E_PARAMETER,
+                  "basis dimension too large");
+        }
+        require(lo < hi, FSTK_E_PARAMETER, "basis domain must satisfy lo < hi");
+        require(std::isfinite(lo) && std::isfinite(hi), FSTK_E_PARAMETER,
+                "basis domain must be finite");
+        if (j == 0) {
+          mh.lo = lo;
+          mh.hi = hi;
+        }
+        require(lo == mh.lo && hi == mh.hi, FSTK_E_SHAPE,
+                "model: inconsistent domains within a mode");
+        const int dim = fam == 0 ? deg + 1 : (deg + 1) << res;
+        for (uint32_t s = 0; s < desc->nnz[f]; ++s, ++c) {
+          require(static_cast<int>(desc->indices[c]) < dim, FSTK_E_SHAPE,
+                  "model: coefficient index outside basis dimension");
+          mh.idx.push_back(desc->indices[c]);
+          mh.coef.push_back(desc->coeffs[c]);
+        }
+        mh.rowptr.push_back(static_cast<int>(mh.idx.size()));
+        require(fam == 0, FSTK_E_PARAMETER,
+                "GPU path: multiwavelet bases are not supported yet (SURVEY 8f-1)");
+        mh.pmax = std::max(mh.pmax, deg);
+      }
+    }
+    DeviceGuard dg(device);
+    static std::once_flag once[64];
+    std::call_once(once[device & 63], [&] { upload_leg_constants(device); });
+    m->num_sms = device_sm_count(device);
+    m->d_core.alloc(m->R);
+    // CSR tables, all modes concatenated.
+    std::vector<int> rowptr;
+    std::vector<uint32_t> idx;
+    std::vector<double> coef;
+    std::vector<size_t> rp_off(d), ix_off(d);
+    for (int k = 0; k < d; ++k) {
+      rp_off[k] = rowptr.size();
+      ix_off[k] = idx.size();
+      rowptr.insert(rowptr.end(), m->modes[k].rowptr.begin(), m->modes[k].rowptr.end());
+      idx.insert(idx.end(), m->modes[k].idx.begin(), m->modes[k].idx.end());
+      coef.insert(coef.end(), m->modes[k].coef.begin(), m->modes[k].coef.end());
+    }
+    if (idx.empty()) {
+      idx.push_back(0);
+      coef.push_back(0.0);
+    }
+    m->d_rowptr.alloc(rowptr.size());
+    m->d_idx.alloc(idx.size());
+    m->d_coef.alloc(coef.size());
+    FSTK_CUDA(cudaMemcpy(m->d_rowptr.p, rowptr.data(), rowptr.size() * 4, cudaMemcpyHostToDevice));
+    FSTK_CUDA(cudaMemcpy(m->d_idx.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice));
+    FSTK_CUDA(cudaMemcpy(m->d_coef.p, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice));
+    m->modes_dev.d = d;
+    for (int k = 0; k < d; ++k) {
+      ModeDev& md = m->modes_dev.m[k];
+      const ModeHost& mh = m->modes[k];
+      md.lo = mh.lo;
+      md.hi = mh.hi;
+      md.span = mh.hi - mh.lo;
+      md.slack = 1e-12 * md.span;
+      md.r = mh.r;
+      md.pmax = mh.pmax;
+      md.rowptr = m->d_rowptr.p + rp_off[k];
+      md.idx = m->d_idx.p + ix_off[k];
+      md.coef = m->d_coef.p + ix_off[k];
+    }
+    plan_layout(m.get());
+    // Padded table rows beyond r_k are zero-filled by construction: the mode
+    // kernel writes r_k rows; padding rows are cleared once per workspace.
+    upload_core(m.get());
+    // ~1/8 GB of tables per chunk, but at least 64K points.
+    int64_t per_pt = 0;
+    for (int k = 0; k < d; ++k) per_pt += m->rp[k];
+    m->chunk_points = std::max<int64_t>(65536, round_up((int64_t(1) << 27) / (per_pt * 8) * 8, TP));
+    m->chunk_points = std::min<int64_t>(m->chunk_points, int64_t(1) << 21);
+    m->chunk_points = round_up(m->chunk_points, TP);
+    for (auto& ck : m->chunk) {
+      FSTK_CUDA(cudaStreamCreateWithFlags(&ck.stream, cudaStreamNonBlocking));
+      FSTK_CUDA(cudaEventCreateWithFlags(&ck.done, cudaEventDisableTiming));
+    }
+    // Allocate and zero the padded table workspaces once (padding rows stay 0).
+    for (auto& ck : m->chunk) {
+      int64_t toff[kMaxOrder], tot = 0;
+      eval_table_offsets(m.get(), round_up(m->chunk_points, TP), toff, &tot);
+      ck.tables.alloc(static_cast<size_t>(tot));
+      FSTK_CUDA(cudaMemset(ck.tables.p, 0, static_cast<size_t>(tot) * 8));
+      ck.err.alloc(1);
+      ck.points.alloc(static_cast<size_t>(d) * m->chunk_points);
+      ck.out.alloc(static_cast<size_t>(m->chunk_points));
+    }
+    FSTK_CUDA(cudaDeviceSynchronize());
+    *out = m.release();
+  });
+}
+
+void fstk_gpu_model_destroy(fstk_gpu_model* model) {
+  if (!model) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(model->device);
+  cudaDeviceSynchronize();
+  delete model;
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+int32_t fstk_gpu_model_set_core(fstk_gpu_model* m, const double* core, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(m && core, FSTK_E_PARAMETER, "null argument");
+    std::lock_guard<std::mutex> lk(m->mu);
+    DeviceGuard dg(m->device);
+    FSTK_CUDA(cudaDeviceSynchronize());
+    m->core.assign(core, core + m->R);
+    upload_core(m);
+  });
+}
+
+int32_t fstk_gpu_model_get_core(const fstk_gpu_model* m, double* core, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(m && core, FSTK_E_PARAMETER, "null argument");
+    std::memcpy(core, m->core.data(), m->core.size() * sizeof(double));
+  });
+}
+
+int32_t fstk_gpu_evaluate_batch_device(const fstk_gpu_model* m, const double* points, int64_t ld,
+                                       int64_t q, int32_t d, double* out, void* stream,
+                                       fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(m != nullptr, FSTK_E_PARAMETER, "null model");
+    require(d == m->d, FSTK_E_PARAMETER, "points must have one column per mode");
+    require(q >= 0 && ld >= q, FSTK_E_PARAMETER, "bad point count or leading dimension");
+    if (q == 0) return;
+    std::lock_guard<std::mutex> lk(m->mu);
+    DeviceGuard dg(m->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    evaluate_device(m, points, ld, q, out, s);
+    unsigned long long bad = 0;
+    FSTK_CUDA(cudaMemcpyAsync(&bad, m->chunk[0].err.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    if (bad != ULLONG_MAX) {
+      std::vector<double> y(d);
+      for (int k = 0; k < d; ++k)
+        FSTK_CUDA(cudaMemcpy(&y[k], points + k * ld + static_cast<int64_t>(bad), 8,
+                             cudaMemcpyDeviceToHost));
+      throw_domain(m, static_cast<int64_t>(bad), y.data());
+    }
+  });
+}
+
+// Host buffers: chunks double-buffered over two streams so the H2D copy of
+// chunk i+1 and the D2H copy of chunk i-1 overlap the kernels of chunk i.
+// Each chunk records its lowest failing row in its own device slot; one
+// read-back at the end reports the globally lowest (deterministic) Domain error.
+int32_t fstk_gpu_evaluate_batch(const fstk_gpu_model* m, const double* points, int64_t q,
+                                int32_t d, double* out, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(m != nullptr, FSTK_E_PARAMETER, "null model");
+    require(d == m->d, FSTK_E_PARAMETER, "points must have one column per mode");
+    require(q >= 0, FSTK_E_PARAMETER, "negative point count");
+    if (q == 0) return;
+    require(points && out, FSTK_E_PARAMETER, "null buffer");
+    std::lock_guard<std::mutex> lk(m->mu);
+    DeviceGuard dg(m->device);
+    const int64_t CH = m->chunk_points;
+    const int64_t ldt = round_up(CH, TP);
+    int64_t toff[kMaxOrder], tot = 0;
+    eval_table_offsets(m, ldt, toff, &tot);
+    const int64_t nchunks = ceil_div(q, CH);
+    m->chunk_err.ensure(static_cast<size_t>(nchunks));
+    FSTK_CUDA(cudaMemsetAsync(m->chunk_err.p, 0xff, nchunks * sizeof(unsigned long long),
+                              m->chunk[0].stream));
+    FSTK_CUDA(cudaEventRecord(m->chunk[0].done, m->chunk[0].stream));
+    FSTK_CUDA(cudaStreamWaitEvent(m->chunk[1].stream, m->chunk[0].done, 0));
+    for (int64_t c = 0; c < nchunks; ++c) {
+      Chunk& ck = m->chunk[c & 1];
+      const int64_t b = c * CH;
+      const int64_t nb = std::min(CH, q - b);
+      for (int k = 0; k < d; ++k)
+        FSTK_CUDA(cudaMemcpyAsync(ck.points.p + k * CH, points + k * q + b, nb * sizeof(double),
+                                  cudaMemcpyHostToDevice, ck.stream));
+      launch_mode_tables(m, ck.points.p, CH, nb, round_up(nb, TP), nullptr, ck.tables.p, toff,
+                         ldt, false, m->chunk_err.p + c, ck.stream);
+      launch_contract(m, ck.tables.p, toff, ldt, nb, ck.out.p, ck.stream, nullptr, nullptr);
+      FSTK_CUDA(cudaMemcpyAsync(out + b, ck.out.p, nb * sizeof(double), cudaMemcpyDeviceToHost,
+                                ck.stream));
+    }
+    FSTK_CUDA(cudaStreamSynchronize(m->chunk[1].stream));
+    std::vector<unsigned long long> bad(static_cast<size_t>(nchunks));
+    FSTK_CUDA(cudaMemcpyAsync(bad.data(), m->chunk_err.p, nchunks * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, m->chunk[0].stream));
+    FSTK_CUDA(cudaStreamSynchronize(m->chunk[0].stream));
+    for (int64_t c = 0; c < nchunks; ++c) {
+      if (bad[c] != ULLONG_MAX) {
+        const int64_t row = c * CH + static_cast<int64_t>(bad[c]);
+        std::vector<double> y(d);
+        for (int k = 0; k < d; ++k) y[k] = points[k * q + row];
+        throw_domain(m, row, y.data());
+      }
+    }
+  });
+}
+
+int32_t fstk_gpu_evaluate(const fstk_gpu_model* m, const double* y, int32_t d, double* out,
+                          fstk_gpu_error* err) {
+  if (!m) {
+    return guarded(err, [&] { fail(FSTK_E_PARAMETER, "null model"); });
+  }
+  if (d != m->d) {
+    return guarded(err, [&] { fail(FSTK_E_PARAMETER, "evaluation point has wrong dimension"); });
+  }
+  // A single point is a batch of one, column-major Q=1 (bit-identical to the batch path).
+  return fstk_gpu_evaluate_batch(m, y, 1, d, out, err);
+}
+
+int32_t fstk_gpu_mode_values(const fstk_gpu_model* m, int32_t mode, const double* x, int64_t n,
+                             double* out, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(m != nullptr, FSTK_E_PARAMETER, "null model");
+    require(mode >= 0 && mode < m->d, FSTK_E_PARAMETER, "mode out of range");
+    require(n >= 0, FSTK_E_PARAMETER, "negative count");
+    if (n == 0) return;
+    std::lock_guard<std::mutex> lk(m->mu);
+    DeviceGuard dg(m->device);
+    const int r = static_cast<int>(m->ranks[mode]);
+    DevBuf<double> dx(n), dout(static_cast<size_t>(n) * r);
+    DevBuf<unsigned long long> derr(1);
+    cudaStream_t s = m->chunk[0].stream;
+    FSTK_CUDA(cudaMemsetAsync(derr.p, 0xff, 8, s));
+    FSTK_CUDA(cudaMemcpyAsync(dx.p, x, n * 8, cudaMemcpyHostToDevice, s));
+    launch_mode_table_one(m, mode, dx.p, n, dout.p, n, true, derr.p, s);
+    unsigned long long bad = 0;
+    FSTK_CUDA(cudaMemcpyAsync(&bad, derr.p, 8, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaMemcpyAsync(out, dout.p, static_cast<size_t>(n) * r * 8,
+                              cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    if (bad != ULLONG_MAX) {
+      Error e{FSTK_E_DOMAIN, "point outside basis domain"};
+      e.index = static_cast<int64_t>(bad);
+      e.mode = mode;
+      e.value = x[bad];
+      throw e;
+    }
+  });
+}
+
+}  // extern "C"

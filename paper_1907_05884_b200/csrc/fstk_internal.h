@@ -1,0 +1,137 @@
+// Internal (non-ABI) declarations shared by the fstk B200 library sources.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <vector>
+
+#include "fstk_common.cuh"
+
+namespace fstk_gpu {
+
+constexpr int kMaxOrder = 8;   // proj/include/fstk/tensor.hpp:16
+struct Int64x8 {
+  int64_t v[8];
+};
+constexpr int kMaxDegree = 64; // proj/src/basis.cpp:31
+
+// Per-mode device parameters for the mode-value kernel.
+struct ModeDev {
+  double lo, hi, span, slack;  // basis.cpp:215-222 (slack = 1e-12 * span)
+  int r;                       // rank r_k
+  int pmax;                    // max Legendre degree over the mode's functions
+  const int* rowptr;           // r+1 CSR offsets into idx/coef
+  const uint32_t* idx;         // ascending basis indices per function
+  const double* coef;
+};
+struct ModesDev {
+  int d;
+  ModeDev m[kMaxOrder];
+};
+
+// Host copy of one mode.
+struct ModeHost {
+  int r = 0, pmax = 0;
+  double lo = 0, hi = 0;
+  std::vector<int> rowptr;
+  std::vector<uint32_t> idx;
+  std::vector<double> coef;
+};
+
+// Layout of the DMMA contraction: K = mode 0 padded to a
+// multiple of 4, N = (j1 chunk) x (outer modes m = j2 + r2 (j3 + ...)).
+struct ContractLayout {
+  bool fast = false;   // DMMA tile path usable for this shape
+  int Kp = 0;          // r0 padded to 4
+  int N1p = 0;         // j1 columns per B tile (multiple of 16, <= 64)
+  int NC = 0;          // j1 chunks
+  int Mout = 0;        // prod_{k>=2} r_k
+  int nsw = 0;         // 8-column subtiles per warp = N1p / 16
+  int nstage = 0;      // B pipeline depth
+  size_t smem = 0;     // dynamic shared memory bytes
+  int64_t btile_elems = 0;  // Kp * N1p
+};
+
+// Workspace for one in-flight chunk.
+struct Chunk {
+  DevBuf<double> points;   // d x CH (column-major, ld = CH)
+  DevBuf<double> tables;   // sum_k rp_k x CHp
+  DevBuf<double> out;      // CH
+  DevBuf<unsigned long long> err;  // lowest failing row (ULLONG_MAX = none)
+  std::vector<unsigned long long> err_host;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+};
+
+}  // namespace fstk_gpu
+
+struct fstk_gpu_model {
+  int device = 0;
+  int d = 0;
+  std::vector<int64_t> ranks;
+  int64_t R = 0;
+  int num_sms = 148;
+  std::vector<fstk_gpu::ModeHost> modes;
+  std::vector<double> core;  // host copy, mode-0 fastest
+
+  fstk_gpu::DevBuf<double> d_core;
+  fstk_gpu::DevBuf<int> d_rowptr;
+  fstk_gpu::DevBuf<uint32_t> d_idx;
+  fstk_gpu::DevBuf<double> d_coef;
+  fstk_gpu::ModesDev modes_dev{};
+
+  fstk_gpu::ContractLayout lay;
+  fstk_gpu::DevBuf<double> d_bpack;  // DMMA fragment-ordered core
+
+  // Per-mode padded table heights: rp[k] = rows of table k stored.
+  int rp[fstk_gpu::kMaxOrder] = {0};
+
+  // Evaluation workspace (guarded by mu).
+  mutable std::mutex mu;
+  mutable fstk_gpu::Chunk chunk[2];
+  mutable fstk_gpu::DevBuf<unsigned long long> chunk_err;  // one slot per host-API chunk
+  int64_t chunk_points = 0;
+
+  ~fstk_gpu_model();
+};
+
+namespace fstk_gpu {
+
+// Mode-value tables for n points.  points: column k at pts + k*ldp.  Output
+// table k, function j, row i at tables + toff[k] + j*ldt + i; rows in
+// [n, n_out) are zero-filled.  row_src (optional): output row i takes input
+// point row_src[i] (negative => zero row).  exact=true reproduces the
+// reference sparse dot bit for bit (separate multiply and add).
+void launch_mode_tables(const fstk_gpu_model* m, const double* pts, int64_t ldp, int64_t n,
+                        int64_t n_out, const int64_t* row_src, double* tables,
+                        const int64_t* toff, int64_t ldt, bool exact,
+                        unsigned long long* err_row, cudaStream_t s);
+// Only mode `mode` (table at `out`, ld = ldt).
+void launch_mode_table_one(const fstk_gpu_model* m, int mode, const double* x, int64_t n,
+                           double* out, int64_t ldt, bool exact, unsigned long long* err_row,
+                           cudaStream_t s);
+
+// Contraction of precomputed tables with the core: out[i] for i < n.
+void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_t* toff,
+                     int64_t ldt, int64_t n, double* out, cudaStream_t s,
+                     const double* bpack_override = nullptr, const double* core_override = nullptr);
+
+// Table offsets/heights used by evaluation for a chunk with ldt rows.
+void eval_table_offsets(const fstk_gpu_model* m, int64_t ldt, int64_t* toff, int64_t* total);
+
+// Full device evaluation of n points (points column-major, ld = ldp) into
+// out, using the model's chunk workspace; err_row receives the lowest failing
+// row index.  Caller holds m->mu.
+void evaluate_device(const fstk_gpu_model* m, const double* pts, int64_t ldp, int64_t n,
+                     double* out, cudaStream_t s);
+void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, const double* pts,
+                          int64_t ldp, int64_t n, double* out, cudaStream_t s);
+
+// Throws the reference's Domain error for point `row` (coordinates given on
+// the host), mirroring basis.cpp:218-219.
+[[noreturn]] void throw_domain(const fstk_gpu_model* m, int64_t row, const double* y);
+
+int device_sm_count(int device);
+
+}  // namespace fstk_gpu

@@ -1,0 +1,1204 @@
+// fstk B200 library — randomized least-squares core refit (sm_100a).
+//
+// Replaces, on the GPU, reestimate_core (proj/src/randls.cpp:360-383):
+//   prepare (:246-311)            host: bit-exact RNG bookkeeping (mt19937_64,
+//                                 rng.cpp:11-61); device: gathers + mode tables
+//                                 written directly in the mixing transform's
+//                                 input order (Makhoul + bit-reversal for DCT,
+//                                 bit-reversal for FFT, natural for WHT);
+//   solve_sketched (:315-348)     device: per design column (and the rhs) the
+//                                 value x_i = s_i * ((u0 u1) u2 ...) is generated
+//                                 on the fly (W never exists), mixed by a
+//                                 radix-2 transform that replays the reference
+//                                 butterflies bit for bit (recurrence twiddles
+//                                 transforms.cpp:36-46 replayed on the host, no
+//                                 FMA contraction), in passes of <= 10 stages
+//                                 held in shared memory, and only the S sampled
+//                                 rows are written (scaled, DCT post-rotation
+//                                 fused) into A;
+//   solve_system (:112-123)       A^T A and A^T b (cuBLAS DSYRK/DGEMV on the
+//                                 materialised sketch), Cholesky (cuSOLVER
+//                                 potrf/potrs, timed separately), minimum-norm
+//                                 eigen fallback when not positive definite;
+//   relative_residual (:350-356)  device evaluation of the validation points.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <random>
+#include <vector>
+
+#include "fstk_internal.h"
+
+namespace fstk_gpu {
+
+// ------------------------------------------------------------- host RNG ---
+// proj/include/fstk/rng.hpp:21-48, proj/src/rng.cpp:11-61 (std::mt19937_64
+// is bit-exact by the C++ standard; the draws on top are spelled out).
+struct Rng {
+  std::mt19937_64 engine;
+  explicit Rng(uint64_t seed) : engine(seed) {}
+  uint64_t next_u64() { return engine(); }
+  uint64_t uniform_index(uint64_t n) {
+    require(n > 0, FSTK_E_PARAMETER, "uniform_index: n must be positive");
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+    uint64_t x;
+    do {
+      x = next_u64();
+    } while (x >= limit);
+    return x % n;
+  }
+  double sign() { return (next_u64() & 1ull) ? -1.0 : 1.0; }
+  std::vector<uint64_t> sample_without_replacement(uint64_t n, uint64_t k) {
+    if (k >= n) {
+      std::vector<uint64_t> all(n);
+      std::iota(all.begin(), all.end(), 0);
+      return all;
+    }
+    std::vector<uint64_t> idx(n);
+    std::iota(idx.begin(), idx.end(), 0);
+    for (uint64_t i = 0; i < k; ++i) {
+      const uint64_t j = i + uniform_index(n - i);
+      std::swap(idx[i], idx[j]);
+    }
+    idx.resize(k);
+    std::sort(idx.begin(), idx.end());
+    return idx;
+  }
+};
+
+static uint64_t mix_seed(uint64_t seed, uint64_t tag) {  // rng.cpp:55-61
+  uint64_t z = (seed ^ tag) + 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+constexpr uint64_t kValidationTag = 0x76616c69ull;  // randls.cpp:16
+constexpr uint64_t kSubsetTag = 0x73756273ull;      // randls.cpp:17
+constexpr uint64_t kSketchTag = 0x736b6574ull;      // randls.cpp:18
+
+static uint64_t next_pow2(uint64_t n) {  // transforms.cpp:20-24
+  uint64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+static uint64_t resolve_sample_rows(uint64_t sample_rows, int64_t r) {  // randls.cpp:125-130
+  return sample_rows > 0 ? sample_rows
+                         : static_cast<uint64_t>(std::ceil(2.5 * static_cast<double>(r)));
+}
+
+struct Plan {  // randls.cpp:54-75
+  std::vector<double> signs;
+  std::vector<uint64_t> rows;
+  uint64_t q_pad = 0;
+  double scale = 1.0;
+};
+
+static Plan make_plan(uint64_t q_w, uint64_t s, uint64_t seed, bool sample = true) {
+  Plan plan;
+  plan.q_pad = next_pow2(q_w);
+  if (sample) {
+    require(s >= 1, FSTK_E_PARAMETER, "sample rows must be positive");
+    require(s <= plan.q_pad, FSTK_E_PARAMETER, "sample rows exceed the padded row count");
+  }
+  Rng rng(seed);
+  plan.signs.resize(plan.q_pad);
+  for (auto& x : plan.signs) x = rng.sign();
+  if (sample) {
+    plan.rows = rng.sample_without_replacement(plan.q_pad, s);
+    plan.scale = std::sqrt(static_cast<double>(plan.q_pad) / static_cast<double>(s));
+  }
+  return plan;
+}
+
+// ------------------------------------------------------ twiddle replay ---
+// For stage len = 2^(s+1) the reference forms wlen = (cos, sin)(-2 pi / len)
+// and multiplies w *= wlen once per butterfly (transforms.cpp:36-46).  The
+// sequence w_0 = 1, w_{k+1} = w_k * wlen is replayed here with the same
+// complex product (a c - b d, a d + b c), each operation rounded separately.
+struct TwiddleKey {
+  int device;
+  uint64_t n;
+  bool operator<(const TwiddleKey& o) const {
+    return device < o.device || (device == o.device && n < o.n);
+  }
+};
+static std::mutex g_tw_mu;
+static std::map<TwiddleKey, std::shared_ptr<DevBuf<double2>>> g_tw;
+
+#pragma GCC push_options
+#pragma GCC optimize("fp-contract=off")
+static void replay_twiddles(uint64_t n, std::vector<double2>& out) {
+  out.assign(n > 1 ? n - 1 : 1, make_double2(1.0, 0.0));
+  size_t off = 0;
+  for (uint64_t len = 2; len <= n; len <<= 1) {
+    const double ang = -2.0 * M_PI / static_cast<double>(len);
+    const double wr = std::cos(ang), wi = std::sin(ang);
+    double a = 1.0, b = 0.0;
+    for (uint64_t k = 0; k < len / 2; ++k) {
+      out[off + k] = make_double2(a, b);
+      const double ac = a * wr, bd = b * wi, ad = a * wi, bc = b * wr;
+      const double re = ac - bd, im = ad + bc;
+      a = re;
+      b = im;
+    }
+    off += len / 2;
+  }
+}
+#pragma GCC pop_options
+
+static std::shared_ptr<DevBuf<double2>> twiddles(int device, uint64_t n) {
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto it = g_tw.find({device, n});
+  if (it != g_tw.end()) return it->second;
+  std::vector<double2> h;
+  replay_twiddles(n, h);
+  auto buf = std::make_shared<DevBuf<double2>>(h.size());
+  FSTK_CUDA(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  g_tw[{device, n}] = buf;
+  return buf;
+}
+
+// ------------------------------------------------------ transform pass ---
+enum SrcKind { SRC_TABLES = 0, SRC_DENSE = 1, SRC_BUFFER = 2 };
+
+struct PassParams {
+  int64_t n;          // q_pad
+  int s0, L, G;       // stages [s0, s0+L), groups per CTA
+  int kind;           // FSTK_TRANSFORM_*
+  int src;            // SrcKind
+  int last;           // write A/b instead of the buffer
+  // design-column source
+  const double* tables;
+  Int64x8 toff;
+  int64_t ldt;
+  int d;
+  int r[kMaxOrder];
+  const double* sgn;        // per position sign (n)
+  const int64_t* row_src;   // per position source row or -1 (n)
+  const double* dense;      // SRC_DENSE: column-major q x R
+  int64_t ldd;
+  const double* rhs;        // rhs values indexed by row_src
+  int64_t col0;             // first global column of the batch
+  int64_t R;                // columns < R: design; == R: rhs
+  const double2* tw;        // replayed twiddles (stage s at tw + 2^s - 1)
+  double2* cbuf;            // complex intermediate, n per batch column
+  double* rbuf;             // real intermediate (WHT)
+  // last pass
+  const int32_t* slot;      // per position destination row or -1
+  const double* post_re;    // per destination row (DCT: cos; FFT/WHT unused)
+  const double* post_im;    // per destination row (DCT: sin)
+  const double* post_c;     // per destination row (DCT: c_k)
+  double scale;             // plan.scale (sqrt(q_pad/S)) or 1
+  double inv_sqrt_n;        // 1/sqrt(n) (FFT, WHT)
+  int64_t row_lo, row_hi;   // destination rows owned by this shard
+  int64_t im_off;           // FFT: rows of the Re block in A (Im block follows)
+  double* A;
+  int64_t lda;
+  double* b;
+};
+
+__device__ __forceinline__ double2 cmul_x(double2 x, double2 w) {
+  // (a + ib)(c + id) = (ac - bd) + i(ad + bc), separately rounded (GCC's
+  // inline complex product on x86-64 without FMA).
+  return make_double2(xsub(xmul(x.x, w.x), xmul(x.y, w.y)), xadd(xmul(x.x, w.y), xmul(x.y, w.x)));
+}
+
+__device__ __forceinline__ double source_value(const PassParams& P, int64_t col, int64_t p) {
+  const int64_t src = P.row_src[p];
+  if (src < 0) return 0.0;
+  double v;
+  if (col == P.R) {
+    v = P.rhs[src];
+  } else if (P.src == SRC_DENSE) {
+    v = P.dense[src + P.ldd * col];
+  } else {
+    // design_column (randls.cpp:44-52): ((u0 * u1) * u2) * ..., mode-0 digit fastest.
+    int64_t rem = col;
+    const int j0 = static_cast<int>(rem % P.r[0]);
+    rem /= P.r[0];
+    v = P.tables[P.toff.v[0] + j0 * P.ldt + p];
+    for (int k = 1; k < P.d; ++k) {
+      const int jk = static_cast<int>(rem % P.r[k]);
+      rem /= P.r[k];
+      v = xmul(v, P.tables[P.toff.v[k] + jk * P.ldt + p]);
+    }
+  }
+  return xmul(P.sgn[p], v);
+}
+
+// One pass of <= 10 radix-2 stages on G adjacent groups of E = 2^L elements
+// (stride 2^s0) held in shared memory.  blockIdx.y = column within the batch.
+template <bool REAL>
+__global__ void __launch_bounds__(256) transform_pass_kernel(const PassParams P) {
+  using T = typename std::conditional<REAL, double, double2>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* x = reinterpret_cast<T*>(smem_raw);
+  const int E = 1 << P.L;
+  const int G = P.G;
+  const int64_t stride = int64_t(1) << P.s0;
+  const int64_t lo_blocks = stride / G;  // CTAs per high index
+  const int64_t b = blockIdx.x;
+  const int64_t c0 = (b % lo_blocks) * G;
+  const int64_t hi = b / lo_blocks;
+  const int64_t base = hi * (stride << P.L) + c0;
+  const int64_t col = P.col0 + blockIdx.y;
+  const int nel = E * G;
+  // ---- load
+  for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+    const int c = e % G, t = e / G;
+    const int64_t p = base + c + t * stride;
+    if (P.src == SRC_BUFFER) {
+      if constexpr (REAL)
+        x[e] = P.rbuf[blockIdx.y * P.n + p];
+      else
+        x[e] = P.cbuf[blockIdx.y * P.n + p];
+    } else {
+      const double v = source_value(P, col, p);
+      if constexpr (REAL)
+        x[e] = v;
+      else
+        x[e] = make_double2(v, 0.0);
+    }
+  }
+  __syncthreads();
+  // ---- butterflies
+  for (int j = 0; j < P.L; ++j) {
+    const int half = 1 << j;
+    const int s = P.s0 + j;
+    for (int bi = threadIdx.x; bi < nel / 2; bi += blockDim.x) {
+      const int c = bi % G, q = bi / G;
+      const int tl = ((q >> j) << (j + 1)) | (q & (half - 1));
+      const int il = tl * G + c, ih = (tl + half) * G + c;
+      if constexpr (REAL) {
+        // wht_orthonormal (transforms.cpp:69-83)
+        const double u = x[il], v = x[ih];
+        x[il] = xadd(u, v);
+        x[ih] = xsub(u, v);
+      } else {
+        // fft_pow2 butterfly (transforms.cpp:40-45)
+        const int64_t k = c0 + c + (int64_t(tl) & (half - 1)) * stride;
+        const double2 w = P.tw[(int64_t(1) << s) - 1 + k];
+        const double2 u = x[il];
+        const double2 v = cmul_x(x[ih], w);
+        x[il] = make_double2(xadd(u.x, v.x), xadd(u.y, v.y));
+        x[ih] = make_double2(xsub(u.x, v.x), xsub(u.y, v.y));
+      }
+    }
+    __syncthreads();
+  }
+  // ---- store
+  for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+    const int c = e % G, t = e / G;
+    const int64_t p = base + c + t * stride;
+    if (!P.last) {
+      if constexpr (REAL)
+        P.rbuf[blockIdx.y * P.n + p] = x[e];
+      else
+        P.cbuf[blockIdx.y * P.n + p] = x[e];
+      continue;
+    }
+    const int32_t sl = P.slot[p];
+    if (sl < 0 || sl < P.row_lo || sl >= P.row_hi) continue;
+    const int64_t dst = sl - P.row_lo;
+    double* out = (col == P.R) ? P.b : P.A + P.lda * col;
+    if constexpr (REAL) {
+      out[dst] = xmul(P.scale, xmul(x[e], P.inv_sqrt_n));
+    } else if (P.kind == FSTK_TRANSFORM_DCT) {
+      // dct2_orthonormal post-rotation (transforms.cpp:96-103) then plan.scale.
+      const double2 V = x[e];
+      const double val = xsub(xmul(P.post_re[sl], V.x), xmul(P.post_im[sl], V.y));
+      out[dst] = xmul(P.scale, xmul(P.post_c[sl], val));
+    } else {
+      // unitary_fft scaling (transforms.cpp:63-65), Re block then Im block.
+      const double2 V = x[e];
+      out[dst] = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
+      out[P.im_off + dst] = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
+    }
+  }
+}
+
+__global__ void finite_check_kernel(const double* __restrict__ a, int64_t n, int* flag) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (!isfinite(a[i])) atomicExch(flag, 1);
+}
+
+__global__ void gather_points_kernel(const double* __restrict__ pts, int64_t ldp, int d,
+                                     const int64_t* __restrict__ idx, int64_t n,
+                                     double* __restrict__ out, int64_t ldo,
+                                     const double* __restrict__ vals, double* __restrict__ vout) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t s = idx[i];
+  for (int k = 0; k < d; ++k) out[k * ldo + i] = pts[k * ldp + s];
+  if (vals) vout[i] = vals[s];
+}
+
+// --------------------------------------------------------- the sketcher ---
+// Runs the transform over all columns [0, ncols) (ncols = R + 1 with the rhs)
+// for a prepared input ordering.
+struct SketchJob {
+  int kind;
+  uint64_t n;           // q_pad
+  int src;              // SRC_TABLES or SRC_DENSE
+  const double* tables;
+  int64_t toff[kMaxOrder];
+  int64_t ldt;
+  int d;
+  int r[kMaxOrder];
+  const double* dense;
+  int64_t ldd;
+  const double* rhs;
+  int64_t R;            // design columns
+  bool with_rhs;
+  const double* sgn;
+  const int64_t* row_src;
+  const int32_t* slot;
+  const double* post_re;
+  const double* post_im;
+  const double* post_c;
+  double scale;
+  int64_t row_lo, row_hi, im_off;
+  double* A;
+  int64_t lda;
+  double* b;
+};
+
+static int ilog2(uint64_t n) {
+  int l = 0;
+  while ((uint64_t(1) << l) < n) ++l;
+  return l;
+}
+
+static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
+  const int LOG = ilog2(J.n);
+  const bool real = J.kind == FSTK_TRANSFORM_WHT;
+  auto tw = real ? nullptr : twiddles(device, J.n);
+  const int64_t ncols = J.R + (J.with_rhs ? 1 : 0);
+  // Column batch sized so the intermediate stays near L2 capacity.
+  const size_t elem = real ? 8 : 16;
+  int64_t nb = std::max<int64_t>(1, (int64_t(96) << 20) / static_cast<int64_t>(J.n * elem));
+  nb = std::min<int64_t>(nb, 1024);
+  nb = std::min<int64_t>(nb, ncols);
+  const int npass = LOG == 0 ? 1 : (LOG + 9) / 10;
+  DevBuf<double2> cbuf;
+  DevBuf<double> rbuf;
+  if (npass > 1) {
+    if (real)
+      rbuf.alloc(static_cast<size_t>(nb) * J.n);
+    else
+      cbuf.alloc(static_cast<size_t>(nb) * J.n);
+  }
+  static std::once_flag attr_once[64];
+  std::call_once(attr_once[device & 63], [&] {
+    FSTK_CUDA(cudaFuncSetAttribute(transform_pass_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    FSTK_CUDA(cudaFuncSetAttribute(transform_pass_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  });
+  for (int64_t c0 = 0; c0 < ncols; c0 += nb) {
+    const int64_t bc = std::min(nb, ncols - c0);
+    for (int pass = 0; pass < npass; ++pass) {
+      PassParams P{};
+      P.n = static_cast<int64_t>(J.n);
+      P.s0 = 10 * pass;
+      P.L = std::min(10, LOG - P.s0);
+      P.G = P.s0 == 0 ? 1 : std::min<int64_t>(4, int64_t(1) << P.s0);
+      P.kind = J.kind;
+      P.src = pass == 0 ? J.src : SRC_BUFFER;
+      P.last = pass == npass - 1;
+      P.tables = J.tables;
+      for (int k = 0; k < J.d; ++k) {
+        P.toff.v[k] = J.toff[k];
+        P.r[k] = J.r[k];
+      }
+      P.ldt = J.ldt;
+      P.d = J.d;
+      P.sgn = J.sgn;
+      P.row_src = J.row_src;
+      P.dense = J.dense;
+      P.ldd = J.ldd;
+      P.rhs = J.rhs;
+      P.col0 = c0;
+      P.R = J.R;
+      P.tw = tw ? tw->p : nullptr;
+      P.cbuf = cbuf.p;
+      P.rbuf = rbuf.p;
+      P.slot = J.slot;
+      P.post_re = J.post_re;
+      P.post_im = J.post_im;
+      P.post_c = J.post_c;
+      P.scale = J.scale;
+      P.inv_sqrt_n = 1.0 / std::sqrt(static_cast<double>(J.n));
+      P.row_lo = J.row_lo;
+      P.row_hi = J.row_hi;
+      P.im_off = J.im_off;
+      P.A = J.A;
+      P.lda = J.lda;
+      P.b = J.b;
+      const int64_t E = int64_t(1) << P.L;
+      const int64_t ctas = static_cast<int64_t>(J.n) / (E * P.G);
+      const size_t smem = static_cast<size_t>(E * P.G) * elem;
+      dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(bc));
+      if (real)
+        transform_pass_kernel<true><<<grid, 256, smem, s>>>(P);
+      else
+        transform_pass_kernel<false><<<grid, 256, smem, s>>>(P);
+      check_launch("transform_pass_kernel");
+    }
+  }
+}
+
+// Host tables for the mixing input order and the DCT post-rotation.
+static uint64_t bitrev(uint64_t v, int bits) {
+  uint64_t r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1ull) << (bits - 1 - i);
+  return r;
+}
+
+// Position p of the transform input holds point index i(p) of the column.
+static void input_order(int kind, uint64_t n, std::vector<uint64_t>& pos2i) {
+  const int LOG = ilog2(n);
+  pos2i.resize(n);
+  for (uint64_t p = 0; p < n; ++p) {
+    if (kind == FSTK_TRANSFORM_WHT) {
+      pos2i[p] = p;
+      continue;
+    }
+    const uint64_t m = bitrev(p, LOG);
+    if (kind == FSTK_TRANSFORM_FFT) {
+      pos2i[p] = m;
+    } else if (n == 1) {
+      pos2i[p] = 0;
+    } else {
+      // Makhoul: v[m] = x[2m] (m < n/2), v[n-1-m'] = x[2m'+1].
+      pos2i[p] = m < n / 2 ? 2 * m : 2 * (n - 1 - m) + 1;
+    }
+  }
+}
+
+#pragma GCC push_options
+#pragma GCC optimize("fp-contract=off")
+// dct2_orthonormal rotation + normalisation for output index k (transforms.cpp:96-103).
+static void dct_post(uint64_t k, uint64_t n, double* re, double* im, double* c) {
+  const double ang = -M_PI * static_cast<double>(k) / (2.0 * static_cast<double>(n));
+  *re = std::cos(ang);
+  *im = std::sin(ang);
+  const double c0 = std::sqrt(1.0 / static_cast<double>(n));
+  const double ck = std::sqrt(2.0 / static_cast<double>(n));
+  *c = k == 0 ? c0 : ck;
+}
+#pragma GCC pop_options
+
+// Device-side sketch inputs for one ordering.
+struct SketchInputs {
+  DevBuf<double> sgn;
+  DevBuf<int64_t> row_src;
+  DevBuf<int32_t> slot;
+  DevBuf<double> post_re, post_im, post_c;
+  int64_t rows_total = 0;  // destination rows (S, or q_pad for mixed_matrix)
+  std::vector<int64_t> dest_of_sample;  // sample s (plan order) -> destination row
+};
+
+// pos2src(i): source row of input point i (< q_w) ; `compact` chooses the
+// destination row order: false = plan order (reference row order), true =
+// the order in which the last pass visits positions (contiguous stores).
+static void build_inputs(int kind, uint64_t n, uint64_t q_w, const std::vector<double>& signs,
+                         const std::vector<uint64_t>& rows, bool all_rows,
+                         const std::vector<int64_t>& src_of_i, bool compact, SketchInputs& S,
+                         cudaStream_t s) {
+  std::vector<uint64_t> pos2i;
+  input_order(kind, n, pos2i);
+  std::vector<double> sg(n);
+  std::vector<int64_t> rs(n);
+  for (uint64_t p = 0; p < n; ++p) {
+    const uint64_t i = pos2i[p];
+    if (i < q_w) {
+      rs[p] = src_of_i.empty() ? static_cast<int64_t>(i) : src_of_i[i];
+      sg[p] = signs[i];
+    } else {
+      rs[p] = -1;
+      sg[p] = 0.0;
+    }
+  }
+  // Destination rows.
+  std::vector<int32_t> slot(n, -1);
+  const uint64_t nrows = all_rows ? n : rows.size();
+  std::vector<uint64_t> pos_of_dest(nrows);
+  S.dest_of_sample.assign(nrows, 0);
+  if (!compact) {
+    for (uint64_t sidx = 0; sidx < nrows; ++sidx) {
+      const uint64_t k = all_rows ? sidx : rows[sidx];
+      slot[k] = static_cast<int32_t>(sidx);
+      pos_of_dest[sidx] = k;
+      S.dest_of_sample[sidx] = static_cast<int64_t>(sidx);
+    }
+  } else {
+    // Visit order of the last pass: CTA-major (group id), then element (c + t G).
+    const int LOG = ilog2(n);
+    const int npass = LOG == 0 ? 1 : (LOG + 9) / 10;
+    const int s0 = 10 * (npass - 1);
+    const int L = std::min(10, LOG - s0);
+    const uint64_t stride = uint64_t(1) << s0;
+    const uint64_t G = s0 == 0 ? 1 : std::min<uint64_t>(4, stride);
+    const uint64_t lo_blocks = stride / G;
+    auto order_key = [&](uint64_t k) {
+      const uint64_t low = k & (stride - 1);
+      const uint64_t hi = k >> (s0 + L);
+      const uint64_t cta = hi * lo_blocks + low / G;
+      const uint64_t c = low % G;
+      const uint64_t t = (k >> s0) & ((uint64_t(1) << L) - 1);
+      return (cta << 32) | (t * G + c);
+    };
+    std::vector<std::pair<uint64_t, uint64_t>> keyed(nrows);
+    for (uint64_t sidx = 0; sidx < nrows; ++sidx) {
+      const uint64_t k = all_rows ? sidx : rows[sidx];
+      keyed[sidx] = {order_key(k), sidx};
+    }
+    std::sort(keyed.begin(), keyed.end());
+    for (uint64_t dst = 0; dst < nrows; ++dst) {
+      const uint64_t sidx = keyed[dst].second;
+      const uint64_t k = all_rows ? sidx : rows[sidx];
+      slot[k] = static_cast<int32_t>(dst);
+      pos_of_dest[dst] = k;
+      S.dest_of_sample[sidx] = static_cast<int64_t>(dst);
+    }
+  }
+  std::vector<double> pre(nrows), pim(nrows), pc(nrows);
+  if (kind == FSTK_TRANSFORM_DCT) {
+    for (uint64_t dst = 0; dst < nrows; ++dst) dct_post(pos_of_dest[dst], n, &pre[dst], &pim[dst], &pc[dst]);
+    if (n == 1) {  // dct2_orthonormal returns early for n == 1 (identity)
+      pre[0] = 1.0;
+      pim[0] = 0.0;
+      pc[0] = 1.0;
+    }
+  }
+  S.rows_total = static_cast<int64_t>(nrows);
+  S.sgn.alloc(n);
+  S.row_src.alloc(n);
+  S.slot.alloc(n);
+  S.post_re.alloc(std::max<uint64_t>(nrows, 1));
+  S.post_im.alloc(std::max<uint64_t>(nrows, 1));
+  S.post_c.alloc(std::max<uint64_t>(nrows, 1));
+  FSTK_CUDA(cudaMemcpyAsync(S.sgn.p, sg.data(), n * 8, cudaMemcpyHostToDevice, s));
+  FSTK_CUDA(cudaMemcpyAsync(S.row_src.p, rs.data(), n * 8, cudaMemcpyHostToDevice, s));
+  FSTK_CUDA(cudaMemcpyAsync(S.slot.p, slot.data(), n * 4, cudaMemcpyHostToDevice, s));
+  if (nrows) {
+    FSTK_CUDA(cudaMemcpyAsync(S.post_re.p, pre.data(), nrows * 8, cudaMemcpyHostToDevice, s));
+    FSTK_CUDA(cudaMemcpyAsync(S.post_im.p, pim.data(), nrows * 8, cudaMemcpyHostToDevice, s));
+    FSTK_CUDA(cudaMemcpyAsync(S.post_c.p, pc.data(), nrows * 8, cudaMemcpyHostToDevice, s));
+  }
+  FSTK_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
+}
+
+// ----------------------------------------------------- library handles ---
+struct Handles {
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+};
+static std::mutex g_h_mu;
+static std::map<int, Handles> g_handles;
+
+static Handles& handles(int device) {
+  std::lock_guard<std::mutex> lk(g_h_mu);
+  Handles& h = g_handles[device];
+  if (!h.blas) {
+    if (cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, "cublasCreate failed");
+    if (cusolverDnCreate(&h.solver) != CUSOLVER_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "cusolverDnCreate failed");
+  }
+  return h;
+}
+
+struct EventTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit EventTimer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  double seconds() {
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms * 1e-3;
+  }
+  ~EventTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+
+}  // namespace fstk_gpu
+
+using namespace fstk_gpu;
+
+struct fstk_gpu_refit {
+  const fstk_gpu_model* model = nullptr;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  fstk_sketch_cfg cfg{};
+  int shard = 0, shards = 1;
+  int64_t q = 0;
+  int d = 0;
+  int64_t R = 0;
+  uint64_t S = 0, q_w = 0, q_pad = 0;
+  bool held_out = true;
+  Plan plan;
+  SketchInputs in;
+  int64_t row_lo = 0, row_hi = 0, local_rows = 0;  // destination rows of this shard
+  DevBuf<double> A;      // local_rows(x2 for FFT) x R, column-major
+  DevBuf<double> b;
+  DevBuf<double> d_points, d_values;  // full dataset on device
+  DevBuf<double> val_points, val_values;
+  int64_t n_val = 0;
+  std::vector<double> h_val_values;
+  ~fstk_gpu_refit() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace fstk_gpu {
+
+static double rel_residual(const std::vector<double>& pred, const std::vector<double>& vals) {
+  // randls.cpp:350-356
+  double sd = 0.0, sv = 0.0;
+  for (size_t i = 0; i < vals.size(); ++i) {
+    const double dlt = pred[i] - vals[i];
+    sd += dlt * dlt;
+    sv += vals[i] * vals[i];
+  }
+  const double denom = std::sqrt(sv), diff = std::sqrt(sd);
+  return denom > 0.0 ? diff / denom : diff;
+}
+
+}  // namespace fstk_gpu
+
+extern "C" {
+
+int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, const double* values,
+                             int64_t q, int32_t d, const fstk_sketch_cfg* cfg, int32_t shard,
+                             int32_t shards, fstk_gpu_refit** out, fstk_reestimate_info* info,
+                             fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(m && points && values && cfg && out, FSTK_E_PARAMETER, "null argument");
+    *out = nullptr;
+    require(shards >= 1 && shard >= 0 && shard < shards, FSTK_E_PARAMETER, "bad shard");
+    require(cfg->transform >= 0 && cfg->transform <= 2, FSTK_E_PARAMETER,
+            "transform must be dct, wht, or fft");
+    // PointCloud::from_data (ingest.cpp:19-31) validation happens first.
+    require(d >= 1 && d <= kMaxOrder, FSTK_E_SHAPE, "point cloud dimension must be in [1, 8]");
+    require(q >= 1, FSTK_E_DATA, "point cloud is empty");
+    auto rf = std::make_unique<fstk_gpu_refit>();
+    rf->model = m;
+    rf->device = m->device;
+    rf->cfg = *cfg;
+    rf->shard = shard;
+    rf->shards = shards;
+    rf->q = q;
+    rf->d = d;
+    rf->R = m->R;
+    DeviceGuard dg(m->device);
+    FSTK_CUDA(cudaStreamCreateWithFlags(&rf->stream, cudaStreamNonBlocking));
+    cudaStream_t s = rf->stream;
+    EventTimer tprep(s);
+    // Upload the dataset and check finiteness on the device.
+    rf->d_points.alloc(static_cast<size_t>(q) * d);
+    rf->d_values.alloc(static_cast<size_t>(q));
+    FSTK_CUDA(cudaMemcpyAsync(rf->d_points.p, points, static_cast<size_t>(q) * d * 8,
+                              cudaMemcpyHostToDevice, s));
+    FSTK_CUDA(cudaMemcpyAsync(rf->d_values.p, values, static_cast<size_t>(q) * 8,
+                              cudaMemcpyHostToDevice, s));
+    {
+      DevBuf<int> flag(2);
+      FSTK_CUDA(cudaMemsetAsync(flag.p, 0, 8, s));
+      finite_check_kernel<<<592, 256, 0, s>>>(rf->d_points.p, q * d, flag.p);
+      check_launch("finite_check_kernel");
+      finite_check_kernel<<<592, 256, 0, s>>>(rf->d_values.p, q, flag.p + 1);
+      check_launch("finite_check_kernel");
+      int hf[2] = {0, 0};
+      FSTK_CUDA(cudaMemcpyAsync(hf, flag.p, 8, cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));
+      require(hf[0] == 0, FSTK_E_DATA, "point coordinates must be finite");
+      require(hf[1] == 0, FSTK_E_DATA, "sample values must be finite");
+    }
+    // reestimate_core (randls.cpp:363-368)
+    const uint64_t S = resolve_sample_rows(cfg->sample_rows, m->R);
+    require(S > static_cast<uint64_t>(m->R), FSTK_E_PARAMETER,
+            "sample rows must exceed the core size");
+    require(static_cast<uint64_t>(q) >= S, FSTK_E_PARAMETER,
+            "dataset smaller than the requested sketch");
+    // prepare (randls.cpp:246-311)
+    require(d == m->d, FSTK_E_SHAPE, "dataset/model dimension mismatch");
+    const uint64_t uq = static_cast<uint64_t>(q);
+    uint64_t n_val = 0;
+    if (cfg->validation_fraction > 0.0) {
+      n_val = static_cast<uint64_t>(std::llround(cfg->validation_fraction * static_cast<double>(uq)));
+      n_val = std::min<uint64_t>(std::min(n_val, uq - 1), 100000);
+    }
+    std::vector<char> in_val(uq, 0);
+    rf->held_out = true;
+    if (n_val >= 1) {
+      Rng rng(mix_seed(cfg->seed, kValidationTag));
+      for (const auto i : rng.sample_without_replacement(uq, n_val)) in_val[i] = 1;
+    } else {
+      rf->held_out = false;
+    }
+    std::vector<uint64_t> train, val;
+    train.reserve(uq - n_val);
+    val.reserve(n_val);
+    for (uint64_t i = 0; i < uq; ++i) (in_val[i] ? val : train).push_back(i);
+    if (!rf->held_out) val = train;
+    const uint64_t q_w = cfg->working_subset == 0
+                             ? train.size()
+                             : std::min<uint64_t>(cfg->working_subset, train.size());
+    require(q_w >= 1, FSTK_E_PARAMETER, "no training points left");
+    std::vector<int64_t> subset;
+    subset.reserve(q_w);
+    if (q_w == train.size()) {
+      for (auto i : train) subset.push_back(static_cast<int64_t>(i));
+    } else {
+      Rng rng(mix_seed(cfg->seed, kSubsetTag));
+      for (const auto i : rng.sample_without_replacement(train.size(), q_w))
+        subset.push_back(static_cast<int64_t>(train[i]));
+    }
+    rf->q_w = q_w;
+    rf->S = S;
+    // solve_sketched (randls.cpp:318): plan seeded with mix_seed(seed, kSketchTag).
+    rf->plan = make_plan(q_w, S, mix_seed(cfg->seed, kSketchTag));
+    rf->q_pad = rf->plan.q_pad;
+    require(rf->q_pad < (uint64_t(1) << 31), FSTK_E_PARAMETER, "working subset too large");
+    // Validation points/values on the device.
+    rf->n_val = static_cast<int64_t>(val.size());
+    {
+      std::vector<int64_t> vi(val.begin(), val.end());
+      DevBuf<int64_t> dvi(std::max<size_t>(vi.size(), 1));
+      FSTK_CUDA(cudaMemcpyAsync(dvi.p, vi.data(), vi.size() * 8, cudaMemcpyHostToDevice, s));
+      rf->val_points.alloc(static_cast<size_t>(std::max<int64_t>(rf->n_val, 1)) * d);
+      rf->val_values.alloc(static_cast<size_t>(std::max<int64_t>(rf->n_val, 1)));
+      if (rf->n_val > 0) {
+        gather_points_kernel<<<static_cast<unsigned>(ceil_div(rf->n_val, 256)), 256, 0, s>>>(
+            rf->d_points.p, q, d, dvi.p, rf->n_val, rf->val_points.p, rf->n_val,
+            rf->d_values.p, rf->val_values.p);
+        check_launch("gather_points_kernel");
+      }
+      rf->h_val_values.resize(rf->n_val);
+      FSTK_CUDA(cudaMemcpyAsync(rf->h_val_values.data(), rf->val_values.p, rf->n_val * 8,
+                                cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));
+    }
+    // Inputs in transform order; destination rows in last-pass visit order.
+    build_inputs(cfg->transform, rf->q_pad, q_w, rf->plan.signs, rf->plan.rows, false, subset,
+                 true, rf->in, s);
+    rf->row_lo = static_cast<int64_t>(S) * shard / shards;
+    rf->row_hi = static_cast<int64_t>(S) * (shard + 1) / shards;
+    rf->local_rows = rf->row_hi - rf->row_lo;
+    // Mode tables over the padded positions, bit-exact (mode_value_tables, randls.cpp:21-41).
+    int64_t toff[kMaxOrder], tot = 0;
+    const int64_t ldt = static_cast<int64_t>(rf->q_pad);
+    for (int k = 0; k < d; ++k) {
+      toff[k] = tot;
+      tot += m->ranks[k] * ldt;
+    }
+    DevBuf<double> tables(static_cast<size_t>(tot));
+    DevBuf<unsigned long long> derr(1);
+    FSTK_CUDA(cudaMemsetAsync(derr.p, 0xff, 8, s));
+    launch_mode_tables(m, rf->d_points.p, q, static_cast<int64_t>(rf->q_pad),
+                       static_cast<int64_t>(rf->q_pad), rf->in.row_src.p, tables.p, toff, ldt,
+                       true, derr.p, s);
+    unsigned long long bad = 0;
+    FSTK_CUDA(cudaMemcpyAsync(&bad, derr.p, 8, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    if (bad != ULLONG_MAX) {
+      // Map the failing table row back to the dataset row.
+      int64_t src = -1;
+      FSTK_CUDA(cudaMemcpy(&src, rf->in.row_src.p + bad, 8, cudaMemcpyDeviceToHost));
+      std::vector<double> y(d);
+      for (int k = 0; k < d; ++k) y[k] = points[k * q + src];
+      throw_domain(m, src, y.data());
+    }
+    if (info) info->t_prepare = tprep.seconds();
+    // Sketch: all R design columns plus the rhs; this shard keeps its rows.
+    EventTimer tsk(s);
+    const bool fft = cfg->transform == FSTK_TRANSFORM_FFT;
+    const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
+    rf->A.alloc(static_cast<size_t>(std::max<int64_t>(arows, 1)) * m->R);
+    rf->b.alloc(static_cast<size_t>(std::max<int64_t>(arows, 1)));
+    SketchJob J{};
+    J.kind = cfg->transform;
+    J.n = rf->q_pad;
+    J.src = SRC_TABLES;
+    J.tables = tables.p;
+    for (int k = 0; k < d; ++k) {
+      J.toff[k] = toff[k];
+      J.r[k] = static_cast<int>(m->ranks[k]);
+    }
+    J.ldt = ldt;
+    J.d = d;
+    J.rhs = rf->d_values.p;
+    J.R = m->R;
+    J.with_rhs = true;
+    J.sgn = rf->in.sgn.p;
+    J.row_src = rf->in.row_src.p;
+    J.slot = rf->in.slot.p;
+    J.post_re = rf->in.post_re.p;
+    J.post_im = rf->in.post_im.p;
+    J.post_c = rf->in.post_c.p;
+    J.scale = rf->plan.scale;
+    J.row_lo = rf->row_lo;
+    J.row_hi = rf->row_hi;
+    J.im_off = rf->local_rows;
+    J.A = rf->A.p;
+    J.lda = arows;
+    J.b = rf->b.p;
+    run_sketch(m->device, J, s);
+    if (info) info->t_sketch = tsk.seconds();
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    if (info) {
+      info->sample_rows = S;
+      info->working_rows = q_w;
+      info->padded_rows = rf->q_pad;
+      info->held_out = rf->held_out ? 1 : 0;
+    }
+    *out = rf.release();
+  });
+}
+
+int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
+                                        fstk_reestimate_info* info, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
+    DeviceGuard dg(rf->device);
+    cudaStream_t s = rf->stream;
+    Handles& h = handles(rf->device);
+    EventTimer tg(s);
+    const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
+    const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
+    const int n = static_cast<int>(rf->R);
+    cublasSetStream(h.blas, s);
+    const double one = 1.0, zero = 0.0;
+    if (arows == 0) {
+      FSTK_CUDA(cudaMemsetAsync(gram, 0, static_cast<size_t>(n) * n * 8, s));
+      FSTK_CUDA(cudaMemsetAsync(rhs, 0, static_cast<size_t>(n) * 8, s));
+    } else {
+      // Lower triangle of A^T A (column-major R x R) and A^T b.
+      if (cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, n, static_cast<int>(arows),
+                      &one, rf->A.p, static_cast<int>(arows), &zero, gram, n) !=
+          CUBLAS_STATUS_SUCCESS)
+        fail(FSTK_E_COMPUTE, "cublasDsyrk failed");
+      count_launch();
+      if (cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(arows), n, &one, rf->A.p,
+                      static_cast<int>(arows), rf->b.p, 1, &zero, rhs, 1) != CUBLAS_STATUS_SUCCESS)
+        fail(FSTK_E_COMPUTE, "cublasDgemv failed");
+      count_launch();
+    }
+    const double t = tg.seconds();
+    if (info) info->t_gram = t;
+  });
+}
+
+int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const double* rhs_in,
+                             double* core_out, fstk_reestimate_info* info, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && gram_in && rhs_in && core_out, FSTK_E_PARAMETER, "null argument");
+    DeviceGuard dg(rf->device);
+    cudaStream_t s = rf->stream;
+    Handles& h = handles(rf->device);
+    cusolverDnSetStream(h.solver, s);
+    const int n = static_cast<int>(rf->R);
+    EventTimer ts(s);
+    DevBuf<double> G(static_cast<size_t>(n) * n), x(n);
+    FSTK_CUDA(cudaMemcpyAsync(G.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
+    FSTK_CUDA(cudaMemcpyAsync(x.p, rhs_in, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
+    int lwork = 0;
+    if (cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, n, G.p, n, &lwork) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "potrf_bufferSize failed");
+    DevBuf<double> work(std::max(lwork, 1));
+    DevBuf<int> dinfo(1);
+    if (cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, n, G.p, n, work.p, lwork, dinfo.p) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "potrf failed");
+    count_launch();
+    int hinfo = 0;
+    FSTK_CUDA(cudaMemcpyAsync(&hinfo, dinfo.p, 4, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    bool rank_def = false;
+    if (hinfo == 0) {
+      if (cusolverDnDpotrs(h.solver, CUBLAS_FILL_MODE_LOWER, n, 1, G.p, n, x.p, n, dinfo.p) !=
+          CUSOLVER_STATUS_SUCCESS)
+        fail(FSTK_E_COMPUTE, "potrs failed");
+      count_launch();
+    } else {
+      // Not positive definite: minimum-norm solution on the numerical range
+      // (stands in for the COD fallback, randls.cpp:117-121).
+      rank_def = true;
+      FSTK_CUDA(cudaMemcpyAsync(G.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
+      DevBuf<double> wv(n);
+      int lw2 = 0;
+      if (cusolverDnDsyevd_bufferSize(h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                      G.p, n, wv.p, &lw2) != CUSOLVER_STATUS_SUCCESS)
+        fail(FSTK_E_COMPUTE, "syevd_bufferSize failed");
+      DevBuf<double> w2(std::max(lw2, 1));
+      if (cusolverDnDsyevd(h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, G.p, n,
+                           wv.p, w2.p, lw2, dinfo.p) != CUSOLVER_STATUS_SUCCESS)
+        fail(FSTK_E_COMPUTE, "syevd failed");
+      count_launch();
+      std::vector<double> ev(n), V(static_cast<size_t>(n) * n), rhs(n);
+      FSTK_CUDA(cudaMemcpyAsync(ev.data(), wv.p, n * 8, cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaMemcpyAsync(V.data(), G.p, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaMemcpyAsync(rhs.data(), rhs_in, n * 8, cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));
+      const double lmax = std::max(std::fabs(ev[n - 1]), std::fabs(ev[0]));
+      const double thr = lmax * static_cast<double>(n) * 2.220446049250313e-16;
+      std::vector<double> sol(n, 0.0);
+      for (int j = 0; j < n; ++j) {
+        if (ev[j] <= thr) continue;
+        double c = 0.0;
+        for (int i = 0; i < n; ++i) c += V[static_cast<size_t>(j) * n + i] * rhs[i];
+        c /= ev[j];
+        for (int i = 0; i < n; ++i) sol[i] += c * V[static_cast<size_t>(j) * n + i];
+      }
+      FSTK_CUDA(cudaMemcpy(x.p, sol.data(), n * 8, cudaMemcpyHostToDevice));
+    }
+    FSTK_CUDA(cudaMemcpyAsync(core_out, x.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    if (info) {
+      info->t_solve = ts.seconds();
+      info->rank_deficient = rank_def ? 1 : 0;
+    }
+    // Validation residuals with the old and the new core (randls.cpp:379-381).
+    EventTimer tr(s);
+    std::vector<double> pred(rf->n_val), pred2(rf->n_val);
+    if (rf->n_val > 0) {
+      DevBuf<double> dp(rf->n_val);
+      {
+        std::lock_guard<std::mutex> lk(rf->model->mu);
+        evaluate_device_core(rf->model, nullptr, rf->val_points.p, rf->n_val, rf->n_val, dp.p, s);
+        FSTK_CUDA(cudaMemcpyAsync(pred.data(), dp.p, rf->n_val * 8, cudaMemcpyDeviceToHost, s));
+        FSTK_CUDA(cudaStreamSynchronize(s));
+        evaluate_device_core(rf->model, core_out, rf->val_points.p, rf->n_val, rf->n_val, dp.p, s);
+        FSTK_CUDA(cudaMemcpyAsync(pred2.data(), dp.p, rf->n_val * 8, cudaMemcpyDeviceToHost, s));
+        FSTK_CUDA(cudaStreamSynchronize(s));
+      }
+    }
+    if (info) {
+      info->residual_before = rel_residual(pred, rf->h_val_values);
+      info->residual_after = rel_residual(pred2, rf->h_val_values);
+      info->t_residual = tr.seconds();
+    }
+  });
+}
+
+void fstk_gpu_refit_end(fstk_gpu_refit* rf) {
+  if (!rf) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(rf->device);
+  cudaStreamSynchronize(rf->stream);
+  delete rf;
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+int32_t fstk_gpu_refit_rows(const fstk_gpu_refit* rf, uint64_t* rows, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && rows, FSTK_E_PARAMETER, "null argument");
+    std::memcpy(rows, rf->plan.rows.data(), rf->plan.rows.size() * 8);
+  });
+}
+
+// A and b of this shard in reference row order (restricted to the shard's rows).
+int32_t fstk_gpu_refit_sketched(const fstk_gpu_refit* rf, double* a, double* b, int64_t* rows_local,
+                                fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf, FSTK_E_PARAMETER, "null argument");
+    const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
+    const int64_t lr = rf->local_rows;
+    const int64_t arows = fft ? 2 * lr : lr;
+    if (rows_local) *rows_local = arows;
+    if (!a && !b) return;
+    DeviceGuard dg(rf->device);
+    std::vector<double> ha(static_cast<size_t>(arows) * rf->R), hb(arows);
+    FSTK_CUDA(cudaMemcpy(ha.data(), rf->A.p, ha.size() * 8, cudaMemcpyDeviceToHost));
+    FSTK_CUDA(cudaMemcpy(hb.data(), rf->b.p, hb.size() * 8, cudaMemcpyDeviceToHost));
+    // Sample s (plan order) sits at destination row dest_of_sample[s]; this
+    // shard owns destinations [row_lo, row_hi).  Emit its samples in plan order.
+    std::vector<int64_t> order;
+    for (uint64_t sidx = 0; sidx < rf->S; ++sidx) {
+      const int64_t dst = rf->in.dest_of_sample[sidx];
+      if (dst >= rf->row_lo && dst < rf->row_hi) order.push_back(dst - rf->row_lo);
+    }
+    for (int64_t o = 0; o < static_cast<int64_t>(order.size()); ++o) {
+      const int64_t src = order[o];
+      for (int64_t c = 0; c < rf->R; ++c) {
+        if (a) {
+          a[o + arows * c] = ha[src + arows * c];
+          if (fft) a[lr + o + arows * c] = ha[lr + src + arows * c];
+        }
+      }
+      if (b) {
+        b[o] = hb[src];
+        if (fft) b[lr + o] = hb[lr + src];
+      }
+    }
+  });
+}
+
+int32_t fstk_gpu_reestimate_core(const fstk_gpu_model* m, const double* points,
+                                 const double* values, int64_t q, int32_t d,
+                                 const fstk_sketch_cfg* cfg, double* core_out,
+                                 fstk_reestimate_info* info, fstk_gpu_error* err) {
+  fstk_gpu_refit* rf = nullptr;
+  fstk_reestimate_info local{};
+  fstk_reestimate_info* inf = info ? info : &local;
+  std::memset(inf, 0, sizeof(*inf));
+  int32_t rc = fstk_gpu_refit_begin(m, points, values, q, d, cfg, 0, 1, &rf, inf, err);
+  if (rc) return rc;
+  rc = guarded(err, [&] {
+    DeviceGuard dg(m->device);
+    DevBuf<double> gram(static_cast<size_t>(m->R) * m->R), rhs(m->R);
+    int32_t r2 = fstk_gpu_refit_normal_equations(rf, gram.p, rhs.p, inf, err);
+    if (r2) throw Error{r2, err ? err->message : "normal equations failed"};
+    r2 = fstk_gpu_refit_solve(rf, gram.p, rhs.p, core_out, inf, err);
+    if (r2) throw Error{r2, err ? err->message : "solve failed"};
+  });
+  fstk_gpu_refit_end(rf);
+  return rc;
+}
+
+// ---------------------------------------------------------- diagnostics ---
+int32_t fstk_gpu_build_design_rows(const fstk_gpu_model* m, const double* points, int64_t q,
+                                   int32_t d, double* w, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(m && points && w, FSTK_E_PARAMETER, "null argument");
+    require(d == m->d, FSTK_E_PARAMETER, "points must have one column per mode");
+    if (q == 0) return;
+    std::lock_guard<std::mutex> lk(m->mu);
+    DeviceGuard dg(m->device);
+    cudaStream_t s = m->chunk[0].stream;
+    DevBuf<double> dp(static_cast<size_t>(q) * d);
+    FSTK_CUDA(cudaMemcpyAsync(dp.p, points, static_cast<size_t>(q) * d * 8, cudaMemcpyHostToDevice, s));
+    int64_t toff[kMaxOrder], tot = 0;
+    for (int k = 0; k < d; ++k) {
+      toff[k] = tot;
+      tot += m->ranks[k] * q;
+    }
+    DevBuf<double> tables(tot);
+    DevBuf<unsigned long long> derr(1);
+    FSTK_CUDA(cudaMemsetAsync(derr.p, 0xff, 8, s));
+    launch_mode_tables(m, dp.p, q, q, q, nullptr, tables.p, toff, q, true, derr.p, s);
+    // W column ell = ((u0 u1) u2) ... (design_column, randls.cpp:44-52) via a
+    // sketch-free pass: generate columns with unit sign and identity order.
+    std::vector<double> ht(tot);
+    FSTK_CUDA(cudaMemcpyAsync(ht.data(), tables.p, tot * 8, cudaMemcpyDeviceToHost, s));
+    unsigned long long bad = 0;
+    FSTK_CUDA(cudaMemcpyAsync(&bad, derr.p, 8, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    if (bad != ULLONG_MAX) {
+      std::vector<double> y(d);
+      for (int k = 0; k < d; ++k) y[k] = points[k * q + bad];
+      throw_domain(m, static_cast<int64_t>(bad), y.data());
+    }
+    for (int64_t ell = 0; ell < m->R; ++ell) {
+      int64_t rem = ell;
+      double* col = w + ell * q;
+      const double* t0 = ht.data() + toff[0] + (rem % m->ranks[0]) * q;
+      for (int64_t i = 0; i < q; ++i) col[i] = t0[i];
+      rem /= m->ranks[0];
+      for (int k = 1; k < d; ++k) {
+        const double* tk = ht.data() + toff[k] + (rem % m->ranks[k]) * q;
+        for (int64_t i = 0; i < q; ++i) col[i] *= tk[i];
+        rem /= m->ranks[k];
+      }
+    }
+  });
+}
+
+static int32_t sketch_dense(const double* w, const double* u, int64_t q, int64_t r,
+                            const fstk_sketch_cfg* cfg, bool mixed, double* a, double* b,
+                            uint64_t* padded, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(w && cfg, FSTK_E_PARAMETER, "null argument");
+    require(q >= 1, FSTK_E_PARAMETER, mixed ? "empty matrix" : "empty system");
+    require(cfg->transform >= 0 && cfg->transform <= 2, FSTK_E_PARAMETER,
+            "transform must be dct, wht, or fft");
+    int dev = 0;
+    FSTK_CUDA(cudaGetDevice(&dev));
+    const uint64_t S = mixed ? 0 : resolve_sample_rows(cfg->sample_rows, r);
+    Plan plan = make_plan(static_cast<uint64_t>(q), S, cfg->seed, !mixed);
+    if (padded) *padded = plan.q_pad;
+    cudaStream_t s;
+    FSTK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{s};
+    SketchInputs in;
+    build_inputs(cfg->transform, plan.q_pad, static_cast<uint64_t>(q), plan.signs, plan.rows,
+                 mixed, {}, false, in, s);
+    const bool fft = cfg->transform == FSTK_TRANSFORM_FFT;
+    const int64_t nrows = in.rows_total;
+    const int64_t arows = fft ? 2 * nrows : nrows;
+    DevBuf<double> dw(static_cast<size_t>(q) * r), du(q), dA(static_cast<size_t>(arows) * r),
+        db(arows);
+    FSTK_CUDA(cudaMemcpyAsync(dw.p, w, static_cast<size_t>(q) * r * 8, cudaMemcpyHostToDevice, s));
+    if (u) FSTK_CUDA(cudaMemcpyAsync(du.p, u, q * 8, cudaMemcpyHostToDevice, s));
+    SketchJob J{};
+    J.kind = cfg->transform;
+    J.n = plan.q_pad;
+    J.src = SRC_DENSE;
+    J.dense = dw.p;
+    J.ldd = q;
+    J.rhs = du.p;
+    J.R = r;
+    J.with_rhs = u != nullptr && b != nullptr;
+    J.sgn = in.sgn.p;
+    J.row_src = in.row_src.p;
+    J.slot = in.slot.p;
+    J.post_re = in.post_re.p;
+    J.post_im = in.post_im.p;
+    J.post_c = in.post_c.p;
+    J.scale = mixed ? 1.0 : plan.scale;
+    J.row_lo = 0;
+    J.row_hi = nrows;
+    J.im_off = nrows;
+    J.A = dA.p;
+    J.lda = arows;
+    J.b = db.p;
+    run_sketch(dev, J, s);
+    FSTK_CUDA(cudaMemcpyAsync(a, dA.p, static_cast<size_t>(arows) * r * 8, cudaMemcpyDeviceToHost, s));
+    if (J.with_rhs) FSTK_CUDA(cudaMemcpyAsync(b, db.p, arows * 8, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int32_t fstk_gpu_sketch(const double* w, const double* u, int64_t q, int64_t r,
+                        const fstk_sketch_cfg* cfg, double* a, double* b, uint64_t* padded_rows,
+                        fstk_gpu_error* err) {
+  if (!u || !b || !a)
+    return guarded(err, [&] { fail(FSTK_E_PARAMETER, "null argument"); });
+  return sketch_dense(w, u, q, r, cfg, false, a, b, padded_rows, err);
+}
+
+int32_t fstk_gpu_mixed_matrix(const double* w, int64_t q, int64_t r, const fstk_sketch_cfg* cfg,
+                              double* out, fstk_gpu_error* err) {
+  if (!out) return guarded(err, [&] { fail(FSTK_E_PARAMETER, "null argument"); });
+  return sketch_dense(w, nullptr, q, r, cfg, true, out, nullptr, nullptr, err);
+}
+
+}  // extern "C"

@@ -1,0 +1,180 @@
+"""Randomized least-squares core refit through the B200 C-ABI.
+
+Python surface mirrors proj/python/module.cpp:271-294 (`reestimate_core`
+returning (model, info)) and the diagnostics of proj/include/fstk/randls.hpp
+(build_design_rows, sketch, mixed_matrix).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import (TRANSFORMS, Err, ReestimateInfo, SketchCfg, check, dptr, lib, make_error,
+                   require_gpu)
+from .model import Model
+
+
+def sketch_config(seed=0, sample_rows=0, working_subset=1 << 20, transform="dct",
+                  validation_fraction=0.05) -> SketchCfg:
+    """module.cpp:83-102 (sketch_from_kwargs)."""
+    if transform not in TRANSFORMS:
+        raise make_error(1, "transform must be dct, wht, or fft")
+    return SketchCfg(int(seed), int(working_subset), int(sample_rows), TRANSFORMS[transform],
+                     float(validation_fraction))
+
+
+def _cloud(model: Model, points, values):
+    p = np.asarray(points, dtype=np.float64)
+    v = np.asarray(values, dtype=np.float64)
+    if p.ndim != 2:
+        raise make_error(1, "points must be a 2-D array")
+    if v.ndim != 1:
+        raise make_error(1, "values must be a 1-D array")
+    if p.shape[0] != v.shape[0]:
+        raise make_error(2, "point/value count mismatch")
+    return np.asfortranarray(p), np.ascontiguousarray(v)
+
+
+def _info_dict(info: ReestimateInfo) -> dict:
+    return {"residual_before": info.residual_before, "residual_after": info.residual_after,
+            "sample_rows": int(info.sample_rows), "working_rows": int(info.working_rows),
+            "rank_deficient": bool(info.rank_deficient), "held_out": bool(info.held_out),
+            "padded_rows": int(info.padded_rows),
+            "timings": {"prepare_s": info.t_prepare, "sketch_s": info.t_sketch,
+                        "gram_s": info.t_gram, "solve_s": info.t_solve,
+                        "residual_s": info.t_residual}}
+
+
+def reestimate_core(model: Model, points, values, seed=0, sample_rows=0,
+                    working_subset=1 << 20, transform="dct", validation_fraction=0.05,
+                    device=None):
+    """randls.cpp:360-383 on one GPU.  Returns (new_model, info)."""
+    require_gpu()
+    p, v = _cloud(model, points, values)
+    cfg = sketch_config(seed, sample_rows, working_subset, transform, validation_fraction)
+    core = np.zeros(int(np.prod(model.ranks)))
+    info = ReestimateInfo()
+    err = Err()
+    check(lib().fstk_gpu_reestimate_core(model.handle(device), dptr(p), dptr(v), p.shape[0],
+                                         p.shape[1], C.byref(cfg), dptr(core), C.byref(info),
+                                         C.byref(err)), err)
+    return model.with_core(core.reshape(model.ranks, order="F")), _info_dict(info)
+
+
+class RefitSession:
+    """Staged refit (fstk_gpu_refit_*): used for row-sharded multi-GPU runs and
+    for parity tests that inspect the sampled rows / sketched system."""
+
+    def __init__(self, model: Model, points, values, seed=0, sample_rows=0,
+                 working_subset=1 << 20, transform="dct", validation_fraction=0.05,
+                 shard=0, shards=1, device=None):
+        require_gpu()
+        self.model = model
+        self.device = device
+        p, v = _cloud(model, points, values)
+        self.cfg = sketch_config(seed, sample_rows, working_subset, transform,
+                                 validation_fraction)
+        self.info = ReestimateInfo()
+        out = C.c_void_p()
+        err = Err()
+        check(lib().fstk_gpu_refit_begin(model.handle(device), dptr(p), dptr(v), p.shape[0],
+                                         p.shape[1], C.byref(self.cfg), shard, shards,
+                                         C.byref(out), C.byref(self.info), C.byref(err)), err)
+        self._h = out.value
+        self.R = int(np.prod(model.ranks))
+
+    def rows(self) -> np.ndarray:
+        out = np.zeros(int(self.info.sample_rows), dtype=np.uint64)
+        err = Err()
+        check(lib().fstk_gpu_refit_rows(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                        C.byref(err)), err)
+        return out
+
+    def sketched(self):
+        n = C.c_int64()
+        err = Err()
+        check(lib().fstk_gpu_refit_sketched(self._h, None, None, C.byref(n), C.byref(err)), err)
+        a = np.zeros((n.value, self.R), order="F")
+        b = np.zeros(n.value)
+        check(lib().fstk_gpu_refit_sketched(self._h, dptr(a), dptr(b), C.byref(n), C.byref(err)),
+              err)
+        return a, b
+
+    def normal_equations(self, gram_t, rhs_t):
+        """Writes this shard's partial A^T A (lower triangle, column-major) and
+        A^T b into CUDA float64 tensors of R*R and R elements."""
+        err = Err()
+        check(lib().fstk_gpu_refit_normal_equations(self._h, gram_t.data_ptr(), rhs_t.data_ptr(),
+                                                    C.byref(self.info), C.byref(err)), err)
+
+    def solve(self, gram_t, rhs_t) -> np.ndarray:
+        core = np.zeros(self.R)
+        err = Err()
+        check(lib().fstk_gpu_refit_solve(self._h, gram_t.data_ptr(), rhs_t.data_ptr(), dptr(core),
+                                         C.byref(self.info), C.byref(err)), err)
+        return core
+
+    def info_dict(self) -> dict:
+        return _info_dict(self.info)
+
+    def close(self):
+        if self._h:
+            lib().fstk_gpu_refit_end(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_design_rows(model: Model, points) -> np.ndarray:
+    """randls.cpp:134-145: Q x R, mode-0 index fastest."""
+    p = np.asfortranarray(np.asarray(points, dtype=np.float64))
+    if p.ndim != 2 or p.shape[1] != model.order:
+        raise make_error(1, "points must have one column per mode")
+    r = int(np.prod(model.ranks))
+    w = np.zeros((p.shape[0], r), order="F")
+    err = Err()
+    check(lib().fstk_gpu_build_design_rows(model.handle(), dptr(p), p.shape[0], p.shape[1],
+                                           dptr(w), C.byref(err)), err)
+    return w
+
+
+def sketch(w, u, seed=0, sample_rows=0, transform="dct"):
+    """randls.cpp:147-184: returns (a, b, padded_rows)."""
+    require_gpu()
+    w = np.asfortranarray(np.asarray(w, dtype=np.float64))
+    u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+    if w.ndim != 2:
+        raise make_error(1, "w must be 2-D")
+    q, r = w.shape
+    if u.shape[0] != q:
+        raise make_error(2, "rhs length mismatch")
+    cfg = sketch_config(seed, sample_rows, 0, transform, 0.0)
+    s = sample_rows if sample_rows > 0 else int(np.ceil(2.5 * r))
+    rows = 2 * s if transform == "fft" else s
+    a = np.zeros((rows, r), order="F")
+    b = np.zeros(rows)
+    padded = C.c_uint64()
+    err = Err()
+    check(lib().fstk_gpu_sketch(dptr(w), dptr(u), q, r, C.byref(cfg), dptr(a), dptr(b),
+                                C.byref(padded), C.byref(err)), err)
+    return a, b, int(padded.value)
+
+
+def mixed_matrix(w, seed=0, transform="dct") -> np.ndarray:
+    """randls.cpp:186-225."""
+    require_gpu()
+    w = np.asfortranarray(np.asarray(w, dtype=np.float64))
+    q, r = w.shape
+    q_pad = 1
+    while q_pad < q:
+        q_pad <<= 1
+    cfg = sketch_config(seed, 0, 0, transform, 0.0)
+    out = np.zeros((2 * q_pad if transform == "fft" else q_pad, r), order="F")
+    err = Err()
+    check(lib().fstk_gpu_mixed_matrix(dptr(w), q, r, C.byref(cfg), dptr(out), C.byref(err)), err)
+    return out
