@@ -1,0 +1,404 @@
+"""Benchmark: FST eval points/s (fp64) + randomized-LS core refit seconds.
+
+Workload (BASELINE.json configs[1] = "C2"): 16,777,216 points on a jittered
+256^3 mesh (seeded), flame-front field + 8 Gaussians + N(0, 1e-4) noise; a
+functional sparse Tucker model with ranks (32,32,32), Legendre degree 48,
+<= 24 nonzeros per function, fitted from seed by the upstream stand-in
+(synth.fitted_model); refit with M = 8R = 262,144 sketch rows (DCT).
+
+A step = one evaluation of all N points of this rank (weak scaling: every
+rank evaluates its own N points).  `value` is device-timed with the points
+already in HBM (inputs 384 MB > 126 MB L2, so no flush is needed); `e2e` is
+the same metric through the host C-ABI call (pinned host buffers, H2D of the
+points and D2H of the values inside the timed region).  The refit (one
+problem, rows sharded across ranks + one NCCL all-reduce of A^T A) is timed
+once after a warm-up and reported under "refit".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FST eval points/s (fp64) + randomized-LS core refit s, at 1/2/4/8 B200"
+UNIT = "points/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--points", type=int, default=0, help="override N per rank")
+    ap.add_argument("--no-refit", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--transform", default="dct")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------- workload ---
+def workload(cfg_name: str, n_override: int, rank: int):
+    from paper_1907_05884_b200 import synth
+
+    c = synth.CONFIGS[cfg_name]
+    seed = 0
+    if cfg_name == "C2":
+        n = n_override or 256 ** 3
+        m = round(n ** (1 / 3)) if not n_override else None
+        pts = synth.jittered_mesh(256, seed=seed + 1000 * rank) if not n_override else \
+            synth.uniform_points(n, 3, seed + 1000 * rank)
+        model = synth.fitted_model(256, c["ranks"], c["degrees"][0], c["nnz"], seed=seed,
+                                   n_gauss=8)
+        vals = synth.flame_field(pts, seed=seed, n_gauss=8, noise=1e-2)
+    elif cfg_name == "C1":
+        n = n_override or c["n"]
+        pts = synth.uniform_points(n, 3, seed + 1000 * rank)
+        model = synth.fitted_model(c["grid"], c["ranks"], c["degrees"][0], c["nnz"], seed=seed)
+        vals = synth.flame_field(pts, seed=seed, noise=1e-2)
+    else:
+        n = n_override or min(c["n"], 1 << 24)
+        d = c["d"]
+        pts = synth.uniform_points(n, d, seed + 1000 * rank) if d == 4 else \
+            synth.flame_surface_mixture(n, seed + 1000 * rank)
+        model = synth.random_model(c["ranks"], c["degrees"], c["nnz"], seed=seed)
+        vals = None
+    return model, np.asfortranarray(pts), vals, c
+
+
+def flops_per_point(model) -> tuple[float, float]:
+    """F_contract = 2 sum_k prod_{m<k} r_m, F_modes = sum_k (2 nnz_k + 6 p_k)."""
+    r = model.ranks
+    fc = 2.0 * sum(float(np.prod(r[:k + 1])) for k in range(len(r)))
+    fm = 0.0
+    for k, mode in enumerate(model.modes):
+        nnz = sum(len(fn.coeffs) for fn in mode)
+        p = max(fn.basis.degree for fn in mode)
+        fm += 2.0 * nnz + 6.0 * p
+    return fc, fm
+
+
+# ------------------------------------------------------------------ clocks ---
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.proc = None
+        self.path = os.path.join("/tmp", f"fstk_clocks_{os.getpid()}.csv")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 7:
+                    continue
+                try:
+                    sm.append(float(f[0]))
+                    mx = max(mx, float(f[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- helpers ---
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def maxreduce(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_eval_baseline(model, pts, budget_s: float = 12.0) -> dict:
+    """Oracle restatement (oracle/liboracle.so) on all host threads, bounded sample."""
+    from oracle import oracle as O
+
+    cores = O.max_threads()
+    n0 = min(pts.shape[0], 1 << 13)
+    t0 = time.perf_counter()
+    O.evaluate_batch(model, pts[:n0])
+    dt = max(time.perf_counter() - t0, 1e-6)
+    n = int(min(pts.shape[0], max(n0, n0 * budget_s / dt)))
+    t0 = time.perf_counter()
+    O.evaluate_batch(model, pts[:n])
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"first {n} points of this rank's workload, oracle evaluate_batch "
+                      f"(restated model.cpp:208-227, parallel_for over {cores} threads), {dt:.1f} s"}
+
+
+def traffic_from_profile(cfg: str):
+    """dram bytes per contraction launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_contract_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if d.get("config") == cfg:
+            return d.get("dram_bytes_per_launch"), d.get("points_per_launch")
+    except Exception:
+        pass
+    return None, None
+
+
+# ------------------------------------------------------------ reference arm ---
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    model, pts, vals, c = workload(args.config, args.points, 0)
+    cores = O.max_threads()
+    # each step: a bounded sample (~3 s of CPU work) of the same workload
+    n0 = min(pts.shape[0], 1 << 13)
+    t0 = time.perf_counter()
+    O.evaluate_batch(model, pts[:n0])
+    per = (time.perf_counter() - t0) / n0
+    n = int(min(pts.shape[0], max(n0, 3.0 / per)))
+    for _ in range(args.warmup):
+        O.evaluate_batch(model, pts[:min(n, 1 << 12)])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.evaluate_batch(model, pts[:n])
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    value = n / (ms * 1e-3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config}: eval of {pts.shape[0]} points (bounded sample "
+                                   f"of {n} per step on the host)",
+                       "ranks": model.ranks},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{n} points per step of the {args.config} workload; oracle "
+                                       "restatement of evaluate_batch (reference cannot build: "
+                                       "Eigen absent), all host threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm ---
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    rank, world, local = dist_env()
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1907_05884_b200 as F
+    from paper_1907_05884_b200 import _lib
+
+    model, pts, vals, cfgd = workload(args.config, args.points, rank)
+    n = pts.shape[0]
+    d = model.order
+    fc, fm = flops_per_point(model)
+    peak_mma, peak_fma = _lib.fp64_peak(local)
+
+    # ---- device-resident inputs for `value`
+    dpts = torch.from_numpy(np.ascontiguousarray(pts.T)).to(dev)  # (d, N): column-major N x d
+    dout = torch.empty(n, dtype=torch.float64, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        model.evaluate_device(dpts, dout)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = F.launch_count()
+    clocks = Clocks(local)
+    _lib.profile_enable(True)
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        model.evaluate_device(dpts, dout)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    _lib.profile_enable(False)
+    ck = clocks.stop()
+    launches = F.launch_count() - launches0
+    prof = _lib.profile_read()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = maxreduce(ms, world, dev)
+    value = world * n / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (the DMMA contraction)
+    c_ms, c_n = prof["contract"]
+    m_ms, m_n = prof["mode_tables"]
+    per_launch_pts = n * args.steps / max(c_n, 1)
+    achieved = fc * n * args.steps / (c_ms * 1e-3) / 1e12 if c_ms > 0 else None
+    traffic, tpts = traffic_from_profile(args.config)
+    roof = {"bound": "tensor", "kernel": "contract_kernel (fp64 DMMA m8n8k4)",
+            "achieved": achieved, "peak": peak_mma, "unit": "TFLOP/s",
+            "frac": (achieved / peak_mma) if achieved else None,
+            "traffic": (traffic * per_launch_pts / tpts) if traffic and tpts else None,
+            "peak_source": "fp64 DMMA throughput measured live on this GPU by fstk_gpu_fp64_peak "
+                           "(MEASURED_PEAKS.json has no fp64 entry); DFMA measured %.1f" % peak_fma,
+            "algorithmic_flops_per_point": fc,
+            "share_of_step": c_ms / (c_ms + m_ms) if c_ms + m_ms > 0 else None,
+            "step_tflops": (fc + fm) * n / (ms * 1e-3) / 1e12,
+            "step_frac": (fc + fm) * n / (ms * 1e-3) / 1e12 / peak_mma,
+            "mode_tables_ms_per_step": m_ms / args.steps,
+            "contract_ms_per_step": c_ms / args.steps}
+
+    # ---- e2e through the host C-ABI (pinned host buffers)
+    hp = torch.from_numpy(np.ascontiguousarray(pts.T)).pin_memory()
+    hout = torch.empty(n, dtype=torch.float64).pin_memory()
+    hp_np = hp.numpy().T  # (N, d) view, column-major
+    for _ in range(2):
+        model.evaluate_batch_into(hp_np, hout.numpy())
+    e2e_times = []
+    for _ in range(max(3, min(args.steps, 10))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        model.evaluate_batch_into(hp_np, hout.numpy())
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = maxreduce(float(np.median(e2e_times)), world, dev)
+    e2e = {"value": world * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(n * d * 8),
+           "d2h_bytes_per_step": int(n * 8), "ms_per_step": e2e_s * 1e3,
+           "path": "fstk_gpu_evaluate_batch (host C-ABI), pinned host buffers"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded jittered 256^3 mesh, analytic flame field; model fitted "
+                    "from seed by the upstream stand-in)",
+            "config": {"workload": f"{args.config}: evaluate {n} points per rank, ranks "
+                                   f"{tuple(model.ranks)}, Legendre p={cfgd['degrees'][0]}, "
+                                   f"<= {cfgd['nnz']} nnz",
+                       "points_per_rank": n, "flops_per_point": fc + fm,
+                       "l2": "inputs (N x d x 8 B) exceed the 126 MB L2; no flush needed",
+                       "parallelism": f"point-sharded x{world}"},
+            "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": ck}
+
+    # ---- refit (one problem; rows sharded across ranks; one all-reduce)
+    if not args.no_refit and vals is not None:
+        line["refit"] = run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak_mma)
+
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_eval_baseline(model, pts)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
+    import torch
+
+    import paper_1907_05884_b200 as F
+    from paper_1907_05884_b200 import synth
+
+    R = int(np.prod(model.ranks))
+    S = cfgd["m_factor"] * R
+    # warm-up on a small problem (cuBLAS/cuSOLVER handles, twiddle cache)
+    wm = synth.random_model((4, 4, 4), (6, 6, 6), 4, seed=1)
+    wp = synth.uniform_points(4096, 3, 2)
+    F.reestimate_core(wm, wp, np.sin(wp[:, 0]), seed=1, transform=args.transform)
+
+    def one():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        sess = F.RefitSession(model, pts, vals, seed=0, sample_rows=S, transform=args.transform,
+                              shard=rank, shards=world)
+        gram = torch.empty(R * R, dtype=torch.float64, device=dev)
+        rhs = torch.empty(R, dtype=torch.float64, device=dev)
+        sess.normal_equations(gram, rhs)
+        torch.cuda.synchronize()
+        t_ar = 0.0
+        if world > 1:
+            ta = time.perf_counter()
+            torch.distributed.all_reduce(gram)
+            torch.distributed.all_reduce(rhs)
+            torch.cuda.synchronize()
+            t_ar = time.perf_counter() - ta
+        t_hot = time.perf_counter() - t0
+        core = sess.solve(gram, rhs) if rank == 0 else None
+        t_all = time.perf_counter() - t0
+        info = sess.info_dict()
+        sess.close()
+        del gram
+        return t_hot, t_all, t_ar, info
+
+    t_hot, t_all, t_ar, info = one()
+    t_hot = maxreduce(t_hot, world, dev)
+    tm = info["timings"]
+    gram_flops = S / world * R * (R + 1)
+    return {"seconds": t_all, "hot_path_seconds": t_hot,
+            "scaling": "strong", "sample_rows": S, "working_rows": info["working_rows"],
+            "padded_rows": info["padded_rows"], "transform": args.transform,
+            "stages_s": {"prepare": tm["prepare_s"], "sketch": tm["sketch_s"],
+                         "gram": tm["gram_s"], "allreduce": t_ar, "solve": tm["solve_s"],
+                         "residual": tm["residual_s"]},
+            "gram_roofline": {"bound": "tensor", "achieved": gram_flops / tm["gram_s"] / 1e12
+                              if tm["gram_s"] else None, "peak": peak, "unit": "TFLOP/s",
+                              "kernel": "cublasDsyrk (library SYRK on the sketched A)"},
+            "residual_before": info["residual_before"], "residual_after": info["residual_after"],
+            "rank_deficient": info["rank_deficient"],
+            "note": "solve (cuSOLVER Cholesky) is outside the hot-path claim (north_star)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -195,6 +195,27 @@ int32_t fstk_gpu_refit_sketched(const fstk_gpu_refit* refit, double* a,
                                 double* b, int64_t* rows_local,
                                 fstk_gpu_error* err);
 
+/* ---- measurement hooks (bench.py) ------------------------------------- */
+/* Kernel classes timed by the profiling hook. */
+enum {
+  FSTK_PROF_MODE_TABLES = 0, /* K1a mode-value tables */
+  FSTK_PROF_CONTRACT = 1,    /* K1b DMMA core contraction */
+  FSTK_PROF_TRANSFORM = 2,   /* K3 design-column generation + mixing passes */
+  FSTK_PROF_GRAM = 3,        /* K4 A^T A / A^T b */
+  FSTK_PROF_SOLVE = 4,       /* Cholesky solve */
+  FSTK_PROF_KINDS = 5
+};
+/* enable != 0: record a CUDA event pair around every launch of the classes
+ * above, on the stream the kernel is launched on. */
+void fstk_gpu_profile_enable(int32_t enable);
+/* Synchronises the recorded events, writes per-class summed milliseconds and
+ * launch counts (arrays of FSTK_PROF_KINDS) and clears the record. */
+int32_t fstk_gpu_profile_read(double* ms, uint64_t* launches, fstk_gpu_error* err);
+/* Measured fp64 tensor-core (DMMA m8n8k4) throughput of `device` in TFLOP/s:
+ * the roofline denominator for the fp64 kernels (not in MEASURED_PEAKS.json). */
+int32_t fstk_gpu_fp64_peak(int32_t device, double* dmma_tflops, double* dfma_tflops,
+                           fstk_gpu_error* err);
+
 #ifdef __cplusplus
 }
 #endif

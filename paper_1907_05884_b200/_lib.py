@@ -78,7 +78,9 @@ EXPORTS = [
     "fstk_gpu_sketch", "fstk_gpu_mixed_matrix", "fstk_gpu_reestimate_core",
     "fstk_gpu_refit_begin", "fstk_gpu_refit_normal_equations", "fstk_gpu_refit_solve",
     "fstk_gpu_refit_end", "fstk_gpu_refit_rows", "fstk_gpu_refit_sketched",
+    "fstk_gpu_profile_enable", "fstk_gpu_profile_read", "fstk_gpu_fp64_peak",
 ]
+PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
 _LIB = None
 DP = C.POINTER(C.c_double)
@@ -127,6 +129,10 @@ def lib():
     L.fstk_gpu_refit_end.restype = None
     L.fstk_gpu_refit_rows.argtypes = [VP, C.POINTER(C.c_uint64), C.POINTER(Err)]
     L.fstk_gpu_refit_sketched.argtypes = [VP, DP, DP, C.POINTER(C.c_int64), C.POINTER(Err)]
+    L.fstk_gpu_profile_enable.argtypes = [C.c_int32]
+    L.fstk_gpu_profile_enable.restype = None
+    L.fstk_gpu_profile_read.argtypes = [DP, C.POINTER(C.c_uint64), C.POINTER(Err)]
+    L.fstk_gpu_fp64_peak.argtypes = [C.c_int32, DP, DP, C.POINTER(Err)]
     _LIB = L
     return L
 
@@ -151,3 +157,27 @@ def device_count() -> int:
 def require_gpu():
     if device_count() < 1:
         raise RuntimeError("fstk_gpu: no CUDA device visible (the B200 path has no CPU fallback)")
+
+
+def profile_enable(on: bool = True):
+    lib().fstk_gpu_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """Per kernel class: (summed device ms, launches) since the last read."""
+    import numpy as np
+
+    ms = np.zeros(len(PROF_KINDS))
+    n = np.zeros(len(PROF_KINDS), dtype=np.uint64)
+    err = Err()
+    check(lib().fstk_gpu_profile_read(dptr(ms), n.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                      C.byref(err)), err)
+    return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(PROF_KINDS)}
+
+
+def fp64_peak(device: int = 0):
+    """(DMMA TFLOP/s, DFMA TFLOP/s) measured on `device`."""
+    a, b = C.c_double(), C.c_double()
+    err = Err()
+    check(lib().fstk_gpu_fp64_peak(device, C.byref(a), C.byref(b), C.byref(err)), err)
+    return a.value, b.value

@@ -203,6 +203,28 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// Optional per-launch event timing (fstk_gpu_profile_enable).
+extern std::atomic<int> g_prof_on;
+void prof_record(int kind, cudaEvent_t a, cudaEvent_t b);
+struct ProfScope {
+  int kind;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(int k, cudaStream_t st) : kind(k), s(st) {
+    if (g_prof_on.load(std::memory_order_relaxed)) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEventRecord(b, s);
+      prof_record(kind, a, b);
+    }
+  }
+};
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 

@@ -368,6 +368,7 @@ void launch_mode_tables(const fstk_gpu_model* m, const double* pts, int64_t ldp,
   for (int k = 0; k < m->d; ++k) to.v[k] = toff[k];
   const size_t sm = mode_smem(m, 0, m->d, threads);
   const unsigned blocks = static_cast<unsigned>(ceil_div(n_out, threads));
+  ProfScope prof(FSTK_PROF_MODE_TABLES, s);
   if (exact)
     mode_tables_kernel<true><<<blocks, threads, sm, s>>>(m->modes_dev, 0, m->d, pts, ldp, n,
                                                          n_out, row_src, tables, to, ldt, err_row);
@@ -446,6 +447,7 @@ void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_
                      int64_t ldt, int64_t n, double* out, cudaStream_t s,
                      const double* bpack_override, const double* core_override) {
   if (n <= 0) return;
+  ProfScope prof(FSTK_PROF_CONTRACT, s);
   if (!m->lay.fast) {
     Int64x8 to{}, rk{};
     for (int k = 0; k < m->d; ++k) {

@@ -452,6 +452,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       const int64_t ctas = static_cast<int64_t>(J.n) / (E * P.G);
       const size_t smem = static_cast<size_t>(E * P.G) * elem;
       dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(bc));
+      ProfScope prof(FSTK_PROF_TRANSFORM, s);
       if (real)
         transform_pass_kernel<true><<<grid, 256, smem, s>>>(P);
       else
@@ -897,6 +898,7 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double
       FSTK_CUDA(cudaMemsetAsync(rhs, 0, static_cast<size_t>(n) * 8, s));
     } else {
       // Lower triangle of A^T A (column-major R x R) and A^T b.
+      ProfScope prof(FSTK_PROF_GRAM, s);
       if (cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, n, static_cast<int>(arows),
                       &one, rf->A.p, static_cast<int>(arows), &zero, gram, n) !=
           CUBLAS_STATUS_SUCCESS)
@@ -926,6 +928,7 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     FSTK_CUDA(cudaMemcpyAsync(G.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
     FSTK_CUDA(cudaMemcpyAsync(x.p, rhs_in, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
     int lwork = 0;
+    ProfScope prof(FSTK_PROF_SOLVE, s);
     if (cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, n, G.p, n, &lwork) !=
         CUSOLVER_STATUS_SUCCESS)
       fail(FSTK_E_COMPUTE, "potrf_bufferSize failed");

@@ -256,6 +256,24 @@ class Model:
                                             dptr(out), C.byref(err)), err)
         return out
 
+    def evaluate_batch_into(self, points, out) -> np.ndarray:
+        """evaluate_batch writing into `out` (float64, Q); `points` must already
+        be a column-major (Q, d) float64 array (e.g. a pinned buffer view), so
+        no host copy is made."""
+        if not (isinstance(points, np.ndarray) and points.dtype == np.float64
+                and points.ndim == 2 and points.flags.f_contiguous):
+            raise make_error(1, "points must be a column-major float64 (Q, d) array")
+        if points.shape[1] != self.order:
+            raise make_error(1, "points must have one column per mode")
+        if not (out.dtype == np.float64 and out.flags.c_contiguous and out.size == points.shape[0]):
+            raise make_error(1, "out must be a contiguous float64 array of Q values")
+        if points.shape[0] == 0:
+            return out
+        err = Err()
+        check(lib().fstk_gpu_evaluate_batch(self.handle(), dptr(points), points.shape[0],
+                                            points.shape[1], dptr(out), C.byref(err)), err)
+        return out
+
     def evaluate_device(self, points_t, out_t=None, stream=None):
         """Device-resident evaluation: `points_t` is a CUDA torch tensor of shape
         (d, Q) (row k = coordinate k, i.e. the column-major Q x d buffer) or a
