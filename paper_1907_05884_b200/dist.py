@@ -1,0 +1,61 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL on GPUs,
+gloo in the CPU tests).  SURVEY §8e:
+
+* evaluation shards points into contiguous slabs, no collective on the data
+  path (the caller owns each slab's output);
+* the refit is one problem: every rank runs the (cheap, bit-identical) host
+  plan and the sketch, keeps its contiguous block of sampled rows, forms its
+  partial A^T A / A^T b, and ONE all-reduce sums them; rank 0 solves.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of n items owned by `rank` (same rule the
+    library uses for sampled rows: floor(n*r/w))."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def reduce_normal_equations(gram, rhs, group=None):
+    """Sum per-rank partial normal equations in place (one collective each)."""
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(gram, group=group)
+        dist.all_reduce(rhs, group=group)
+    return gram, rhs
+
+
+def evaluate_sharded(model, points, rank: int, world: int):
+    """Evaluates this rank's slab of `points` (Q x d); returns (lo, hi, values)."""
+    lo, hi = shard_range(points.shape[0], rank, world)
+    return lo, hi, model.evaluate_batch(np.asfortranarray(points[lo:hi]))
+
+
+def refit_distributed(model, points, values, rank: int, world: int, device=None, **kw):
+    """Row-sharded refit: returns (new_model, info) on rank 0, (None, info) elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    from .refit import RefitSession
+
+    R = int(np.prod(model.ranks))
+    sess = RefitSession(model, points, values, shard=rank, shards=world, device=device, **kw)
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+    gram = torch.empty(R * R, dtype=torch.float64, device=dev)
+    rhs = torch.empty(R, dtype=torch.float64, device=dev)
+    sess.normal_equations(gram, rhs)
+    reduce_normal_equations(gram, rhs)
+    new = None
+    if rank == 0:
+        core = sess.solve(gram, rhs)
+        new = model.with_core(core)
+    info = sess.info_dict()
+    sess.close()
+    if dist.is_initialized():
+        dist.barrier()
+    return new, info

@@ -1,0 +1,157 @@
+"""GPU parity for evaluation (fstk_gpu_evaluate_batch & co. through the C-ABI)
+against the CPU oracle and the reference's own evaluation tests.
+
+Tolerance (north_star): fp64 values within 1e-12 relative L2 of the oracle.
+Mode values are bit-exact (same rounding sequence as basis.cpp:49-61 and the
+sparse dot of model.cpp:86-88)."""
+import numpy as np
+import pytest
+
+import paper_1907_05884_b200 as F
+from _models import const_one_model, legendre_model, one_sparse, random_points
+from conftest import rel
+from paper_1907_05884_b200 import synth
+from paper_1907_05884_b200.model import BasisSpec, Model
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+SHAPES = {
+    "C1": ((16, 16, 16), (20, 20, 20), 12),
+    "C2": ((32, 32, 32), (48, 48, 48), 24),
+    "C3": ((48, 48, 32), (64, 64, 64), 24),
+    "C4": ((16, 16, 16, 8), (32, 32, 32, 16), 12),
+    "d1": ((5,), (7,), 4),
+    "d2": ((7, 9), (6, 6), 5),
+    "ragged": ((5, 13, 3), (9, 17, 4), 6),
+    "wide_r1": ((8, 80, 3), (10, 64, 5), 7),
+    "d5": ((3, 2, 4, 2, 3), (4, 4, 4, 4, 4), 3),
+}
+
+
+@pytest.mark.parametrize("name", list(SHAPES))
+def test_eval_parity_shapes(O, name):
+    ranks, deg, nnz = SHAPES[name]
+    m = synth.random_model(ranks, deg, nnz, seed=1)
+    pts = synth.uniform_points(20000 if len(ranks) < 5 else 3000, len(ranks), seed=2)
+    got = m.evaluate_batch(pts)
+    want = O.evaluate_batch(m, pts)
+    assert rel(got, want) <= TOL
+
+
+def test_eval_parity_fitted_c1(O):
+    m = synth.fitted_model(64, (16, 16, 16), 20, 12)
+    pts = synth.uniform_points(200_000, 3, seed=0)
+    assert rel(m.evaluate_batch(pts), O.evaluate_batch(m, pts)) <= TOL
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_mode_values_bit_exact(O, mode):
+    m = synth.random_model((32, 32, 32), (48, 48, 48), 24, seed=4)
+    x = np.concatenate([np.random.default_rng(mode).random(500), [0.0, 1.0, 1.0 + 1e-13, -1e-13]])
+    got = m.mode_values(mode, x)
+    want = np.stack([O.mode_values(m, mode, xi) for xi in x])
+    assert np.array_equal(got, want)
+
+
+def test_batch_equals_scalar_bitexact():            # test_model.cpp:178-199
+    m = legendre_model((3, 3), 17)
+    pts = random_points(200, 2, 23)
+    v = m.evaluate_batch(pts)
+    for i in range(200):
+        assert v[i] == m.evaluate(pts[i])
+
+
+def test_position_independence_large():
+    """A point's value does not depend on its position in the batch (chunk and
+    tile boundaries): a full C2-sized evaluation equals evaluations of ragged
+    sub-slices bit for bit, and two runs are identical."""
+    m = synth.random_model((32, 32, 32), (48, 48, 48), 24, seed=1)
+    n = 1 << 22
+    pts = synth.uniform_points(n, 3, seed=9)
+    full = m.evaluate_batch(pts)
+    assert np.array_equal(full, m.evaluate_batch(pts))
+    for lo, hi in ((0, 1), (1, 130), (12345, 12345 + 3 * 128 + 7), (n - 1000, n),
+                   (2_000_001, 2_000_001 + (1 << 21) + 3)):
+        assert np.array_equal(m.evaluate_batch(pts[lo:hi]), full[lo:hi])
+
+
+def test_device_api_matches_host_api():
+    import torch
+
+    m = synth.random_model((16, 16, 16, 8), (32, 32, 32, 16), 12, seed=3)
+    pts = synth.uniform_points(100_003, 4, seed=5)
+    host = m.evaluate_batch(pts)
+    dp = torch.from_numpy(np.ascontiguousarray(pts.T)).cuda()
+    dev = m.evaluate_device(dp).cpu().numpy()
+    assert np.array_equal(host, dev)
+
+
+def test_const_model_and_linearity():               # test_model.cpp:113-137
+    m = const_one_model()
+    pts = np.array([[x, y, -y] for x in (-1.0, -0.25, 0.0, 0.8, 1.0) for y in (-1.0, 0.5)])
+    assert np.abs(m.evaluate_batch(pts) - 1.0).max() <= 1e-14
+    m = synth.random_model((8, 8, 8), (10, 10, 10), 5, seed=2)
+    pts = synth.uniform_points(1000, 3, seed=3)
+    a = m.evaluate_batch(pts)
+    b = m.with_core(3.5 * m.core).evaluate_batch(pts)
+    assert np.abs(b - 3.5 * a).max() <= 1e-14 * max(1.0, np.abs(3.5 * a).max())
+
+
+def test_domain_errors_and_clamp():                 # basis.cpp:215-222, test_model.cpp:201-210
+    m = Model(np.array([2.0]), [[one_sparse(BasisSpec.legendre(0, 0.0, 1.0), 0, 1.0)]])
+    assert m.evaluate([0.5]) == 2.0
+    with pytest.raises(ValueError) as e:
+        m.evaluate([1.75])
+    assert e.value.kind == "Domain"
+    with pytest.raises(ValueError) as e:
+        m.evaluate([0.5, 0.5])
+    assert e.value.kind == "Parameter"
+    m = synth.random_model((4, 4, 4), (6, 6, 6), 3, seed=1)
+    pts = synth.uniform_points(300_000, 3, seed=1)
+    pts[250_001, 1] = 1.0 + 1e-13      # inside the slack: clamped, accepted
+    ok = m.evaluate_batch(pts)
+    edge = pts.copy()
+    edge[250_001, 1] = 1.0
+    assert np.array_equal(ok, m.evaluate_batch(edge))
+    bad = pts.copy()
+    bad[270_000, 2] = 1.5
+    bad[280_000, 0] = -0.5
+    with pytest.raises(ValueError) as e:
+        m.evaluate_batch(bad)
+    assert e.value.kind == "Domain" and e.value.index == 270_000 and e.value.mode == 2
+    nan = pts.copy()
+    nan[5, 0] = np.nan
+    with pytest.raises(ValueError) as e:
+        m.evaluate_batch(nan)
+    assert e.value.index == 5
+
+
+def test_empty_and_single():
+    m = synth.random_model((4, 4, 4), (6, 6, 6), 3, seed=1)
+    assert m.evaluate_batch(np.zeros((0, 3))).shape == (0,)
+    assert m.evaluate_batch(np.full((1, 3), 0.5)).shape == (1,)
+
+
+def test_fstk_round_trip_evaluates_bit_identically(tmp_path):  # test_model.cpp:276-309
+    m = synth.random_model((6, 5, 7), (12, 10, 9), 5, seed=8, lo=0.0, hi=2.0)
+    p = tmp_path / "m.fstk"
+    m.save(str(p))
+    back = F.load_model(str(p))
+    pts = synth.uniform_points(1000, 3, seed=31) * 2.0
+    assert np.array_equal(m.evaluate_batch(pts), back.evaluate_batch(pts))
+
+
+def test_wavelet_model_rejected_loudly():
+    m = Model(np.ones(2), [[one_sparse(BasisSpec.wavelet(1, 0), 0, 1.0),
+                            one_sparse(BasisSpec.wavelet(1, 0), 1, 1.0)]])
+    with pytest.raises(ValueError) as e:
+        m.evaluate_batch(np.zeros((3, 1)))
+    assert e.value.kind == "Parameter"
+
+
+def test_native_library_is_what_ran():
+    before = F.launch_count()
+    m = synth.random_model((8, 8, 8), (6, 6, 6), 3, seed=1)
+    m.evaluate_batch(synth.uniform_points(1000, 3, 1))
+    assert F.launch_count() >= before + 2

@@ -1,0 +1,188 @@
+"""GPU parity for the randomized-LS refit (fstk_gpu_reestimate_core & the
+staged refit) against the CPU oracle.
+
+Bars (north_star): sampled-point indices bit-exact; the sketched system A, b
+bit-exact (the GPU replays the reference butterflies and twiddles); refit core
+within 1e-9 relative L2 of the oracle's QR solution."""
+import numpy as np
+import pytest
+
+import paper_1907_05884_b200 as F
+from _models import legendre_model, random_points
+from conftest import rel
+from paper_1907_05884_b200 import synth
+
+pytestmark = pytest.mark.gpu
+CORE_TOL = 1e-9
+
+
+def _data(O, model, q, seed, noise=0.01):
+    pts = synth.uniform_points(q, model.order, seed)
+    vals = O.evaluate_batch(model, pts) + noise * np.random.default_rng(seed).normal(size=q)
+    return pts, vals
+
+
+@pytest.mark.parametrize("t", ["dct", "wht", "fft"])
+@pytest.mark.parametrize("q,ranks,wsub", [(20_000, (4, 3, 2), 1 << 20), (5000, (3, 3, 2, 2), 3000),
+                                          (70_000, (6, 5, 4), 40_000)])
+def test_sketch_rows_and_core_parity(O, t, q, ranks, wsub):
+    m = synth.random_model(ranks, [6] * len(ranks), 4, seed=3)
+    pts, vals = _data(O, m, q, 4)
+    sess = F.RefitSession(m, pts, vals, seed=17, transform=t, working_subset=wsub)
+    a, b = sess.sketched()
+    ao, bo, rows_o, _, info_o = O.refit_system(m, pts, vals, seed=17, transform=t,
+                                               working_subset=wsub)
+    assert np.array_equal(sess.rows(), rows_o)
+    assert np.array_equal(a, ao) and np.array_equal(b, bo)
+    sess.close()
+    new, info = F.reestimate_core(m, pts, vals, seed=17, transform=t, working_subset=wsub)
+    core_o, info_o = O.reestimate_core(m, pts, vals, seed=17, transform=t, working_subset=wsub)
+    assert rel(new.core.reshape(-1, order="F"), core_o) <= CORE_TOL
+    for k in ("sample_rows", "working_rows", "held_out", "rank_deficient"):
+        assert info[k] == info_o[k]
+    assert abs(info["residual_after"] - info_o["residual_after"]) <= 1e-9 * max(
+        1.0, info_o["residual_after"])
+
+
+def test_c1_refit_parity(O):
+    """BASELINE C1: N=200k, ranks 16^3 (R=4096), M = 4R = 16384, DCT."""
+    m = synth.fitted_model(64, (16, 16, 16), 20, 12)
+    pts = synth.uniform_points(200_000, 3, seed=0)
+    vals = synth.flame_field(pts, seed=0, noise=1e-2)
+    new, info = F.reestimate_core(m, pts, vals, seed=0, sample_rows=16384)
+    core_o, info_o = O.reestimate_core(m, pts, vals, seed=0, sample_rows=16384)
+    assert info["working_rows"] == 190_000 and info["padded_rows"] == 1 << 18
+    assert rel(new.core.reshape(-1, order="F"), core_o) <= CORE_TOL
+    assert np.array_equal(F.RefitSession(m, pts, vals, seed=0, sample_rows=16384).rows(),
+                          info_o["rows"])
+
+
+def test_public_sketch_and_mixed_bitexact(O):
+    rng = np.random.default_rng(0)
+    for t in ("dct", "wht", "fft"):
+        for q in (1, 2, 24, 100, 3000, 70_000):
+            w, u = rng.random((q, 6)), rng.random(q)
+            s = min(40, q)
+            a1, b1, p1 = F.sketch(w, u, seed=5, sample_rows=s, transform=t)
+            a2, b2, p2 = O.sketch(w, u, seed=5, sample_rows=s, transform=t)
+            assert p1 == p2 and np.array_equal(a1, a2) and np.array_equal(b1, b2)
+        w = rng.random((100, 4))
+        assert np.array_equal(F.mixed_matrix(w, seed=11, transform=t),
+                              O.mixed_matrix(w, seed=11, transform=t))
+
+
+@pytest.mark.parametrize("t", ["dct", "wht", "fft"])
+def test_full_sampling_preserves_normal_equations(t):  # test_randls.cpp:118-141
+    w = random_points(24, 6, 19)
+    u = random_points(24, 1, 23)[:, 0]
+    a, b, padded = F.sketch(w, u, seed=5, sample_rows=32, transform=t)
+    assert padded == 32
+    assert np.abs(a.T @ a - w.T @ w).max() <= 1e-10 * max(1.0, np.abs(w.T @ w).max())
+    assert np.abs(a.T @ b - w.T @ u).max() <= 1e-10 * max(1.0, np.abs(w.T @ u).max())
+
+
+def test_design_rows(O):                             # test_randls.cpp:88-116
+    m = legendre_model((4, 3, 2), 13)
+    pts = random_points(64, 3, 17)
+    w = F.build_design_rows(m, pts)
+    assert np.array_equal(w, O.build_design_rows(m, pts))
+    v = m.evaluate_batch(pts)
+    assert np.abs(w @ m.core.reshape(-1, order="F") - v).max() <= 1e-10 * max(1, np.abs(v).max())
+
+
+def test_recovers_exact_and_planted_core(O):        # test_randls.cpp:255-288
+    m = legendre_model((3, 2, 2), 79)
+    pts = random_points(2000, 3, 83)
+    new, info = F.reestimate_core(m, pts, O.evaluate_batch(m, pts), seed=17)
+    assert rel(new.core, m.core) <= 1e-8 and info["residual_after"] <= 1e-8
+    assert not info["rank_deficient"]
+    m = legendre_model((2, 3, 2), 89)
+    planted = m.core + 0.5 * np.random.default_rng(97).normal(size=m.core.shape)
+    ground = m.with_core(planted)
+    pts = random_points(4000, 3, 101)
+    new, _ = F.reestimate_core(m, pts, O.evaluate_batch(ground, pts), seed=23, sample_rows=48)
+    assert rel(new.core, planted) <= 1e-6
+
+
+def test_biased_core_improves_and_holdout(O):       # test_randls.cpp:290-311
+    ground = legendre_model((3, 3), 103)
+    biased = ground.core + 0.2 * np.random.default_rng(107).normal(size=(3, 3)) * np.linalg.norm(
+        ground.core) / 3.0
+    m = ground.with_core(biased)
+    pts = random_points(3000, 2, 109)
+    new, info = F.reestimate_core(m, pts, O.evaluate_batch(ground, pts), seed=29)
+    assert info["residual_after"] <= info["residual_before"]
+    assert info["residual_after"] <= 1e-6 and info["held_out"]
+    _, info = F.reestimate_core(m, pts, O.evaluate_batch(ground, pts), seed=29,
+                                validation_fraction=0.0)
+    assert not info["held_out"]
+
+
+def test_rejections():                               # test_randls.cpp:185-191, 313-322
+    m = legendre_model((2, 2), 113)
+    pts = random_points(500, 2, 127)
+    vals = np.sin(pts[:, 0])
+    with pytest.raises(ValueError) as e:
+        F.reestimate_core(m, pts, vals, sample_rows=4)
+    assert e.value.kind == "Parameter"
+    with pytest.raises(ValueError):
+        F.reestimate_core(m, pts[:10], vals[:10], sample_rows=20)
+    with pytest.raises(ValueError):
+        F.sketch(random_points(8, 2, 41), random_points(8, 1, 43)[:, 0], sample_rows=9)
+    bad = vals.copy()
+    bad[3] = np.inf
+    with pytest.raises(ValueError) as e:
+        F.reestimate_core(m, pts, bad)
+    assert e.value.kind == "Data"
+    with pytest.raises(ValueError) as e:
+        F.reestimate_core(m, pts[:, :1], vals)
+    assert e.value.kind == "Shape"
+
+
+def test_rank_deficient_flagged(O):
+    """Duplicate mode functions make W rank deficient: the flag is raised (as
+    the reference's COD fallback does) and the fit still reproduces the data."""
+    from _models import one_sparse
+    from paper_1907_05884_b200.model import BasisSpec, Model
+
+    spec = BasisSpec.legendre(2)
+    modes = [[one_sparse(spec, 0, 1.0), one_sparse(spec, 1, 1.0), one_sparse(spec, 1, 1.0)],
+             [one_sparse(spec, 0, 1.0), one_sparse(spec, 2, 1.0)]]
+    m = Model(np.arange(6.0).reshape(3, 2), modes)
+    pts = random_points(2000, 2, 5)
+    vals = O.evaluate_batch(m, pts)
+    new, info = F.reestimate_core(m, pts, vals, seed=3)
+    _, info_o = O.reestimate_core(m, pts, vals, seed=3)
+    assert info["rank_deficient"] and info_o["rank_deficient"]
+    assert info["residual_after"] <= 1e-8
+
+
+def test_sharded_rows_sum_to_full_system(O):
+    """Row shards (multi-GPU refit) partition the sketched rows; their partial
+    normal equations sum to the full system (host-checked on one GPU)."""
+    import torch
+
+    m = synth.random_model((4, 3, 3), (5, 5, 5), 3, seed=2)
+    pts, vals = _data(O, m, 30_000, 6)
+    R = 36
+    full = F.RefitSession(m, pts, vals, seed=4)
+    gf = torch.empty(R * R, dtype=torch.float64, device="cuda")
+    rf = torch.empty(R, dtype=torch.float64, device="cuda")
+    full.normal_equations(gf, rf)
+    g = torch.zeros(R * R, dtype=torch.float64, device="cuda")
+    r = torch.zeros(R, dtype=torch.float64, device="cuda")
+    for s in range(3):
+        sess = F.RefitSession(m, pts, vals, seed=4, shard=s, shards=3)
+        gs = torch.empty_like(g)
+        rs = torch.empty_like(r)
+        sess.normal_equations(gs, rs)
+        g += gs
+        r += rs
+        sess.close()
+    low = np.tril(np.ones((R, R), dtype=bool))
+    G1 = gf.cpu().numpy().reshape(R, R, order="F")[low]
+    G2 = g.cpu().numpy().reshape(R, R, order="F")[low]
+    assert np.abs(G1 - G2).max() <= 1e-12 * np.abs(G1).max()
+    core = full.solve(g, r)
+    core_o, _ = O.reestimate_core(m, pts, vals, seed=4)
+    assert rel(core, core_o) <= CORE_TOL
