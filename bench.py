@@ -375,7 +375,10 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
             torch.cuda.synchronize()
             t_ar = time.perf_counter() - ta
         t_hot = time.perf_counter() - t0
-        core = sess.solve(gram, rhs) if rank == 0 else None
+        from paper_1907_05884_b200.dist import refine_distributed
+
+        x = refine_distributed(sess, gram, rhs)
+        core = sess.finish(x) if rank == 0 else None
         t_all = time.perf_counter() - t0
         info = sess.info_dict()
         sess.close()

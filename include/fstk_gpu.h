@@ -185,6 +185,23 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* refit, double* gram,
 int32_t fstk_gpu_refit_solve(fstk_gpu_refit* refit, const double* gram,
                              const double* rhs, double* core_out,
                              fstk_reestimate_info* info, fstk_gpu_error* err);
+/* solve() for shards > 1, as explicit stages (device vectors of R doubles):
+ * factor() Cholesky-factors the summed Gram (every rank) and writes the
+ * normal-equations solution x; correction() writes this shard's
+ * s = A_loc^T (b_loc - A_loc x); the caller sums s over ranks; apply() does
+ * x += (A^T A)^{-1} s and reports ||dx||/||x||; repeat until it stalls
+ * (iterative refinement = corrected semi-normal equations, converging to the
+ * reference's QR least-squares solution); finish() copies x to the host core
+ * and computes the validation residuals. */
+int32_t fstk_gpu_refit_factor(fstk_gpu_refit* refit, const double* gram,
+                              const double* rhs, double* x, fstk_reestimate_info* info,
+                              fstk_gpu_error* err);
+int32_t fstk_gpu_refit_correction(fstk_gpu_refit* refit, const double* x, double* s,
+                                  fstk_gpu_error* err);
+int32_t fstk_gpu_refit_apply(fstk_gpu_refit* refit, const double* s, double* x,
+                             double* rel_step, fstk_gpu_error* err);
+int32_t fstk_gpu_refit_finish(fstk_gpu_refit* refit, const double* x, double* core_out,
+                              fstk_reestimate_info* info, fstk_gpu_error* err);
 void fstk_gpu_refit_end(fstk_gpu_refit* refit);
 /* Diagnostics/tests: host copies of the sampled padded rows (S u64) and, when
  * the refit kept it, this shard's sketched block A (rows_local x R col-major)

@@ -79,6 +79,8 @@ EXPORTS = [
     "fstk_gpu_refit_begin", "fstk_gpu_refit_normal_equations", "fstk_gpu_refit_solve",
     "fstk_gpu_refit_end", "fstk_gpu_refit_rows", "fstk_gpu_refit_sketched",
     "fstk_gpu_profile_enable", "fstk_gpu_profile_read", "fstk_gpu_fp64_peak",
+    "fstk_gpu_refit_factor", "fstk_gpu_refit_correction", "fstk_gpu_refit_apply",
+    "fstk_gpu_refit_finish",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -125,6 +127,11 @@ def lib():
                                                   C.POINTER(Err)]
     L.fstk_gpu_refit_solve.argtypes = [VP, VP, VP, DP, C.POINTER(ReestimateInfo),
                                        C.POINTER(Err)]
+    L.fstk_gpu_refit_factor.argtypes = [VP, VP, VP, VP, C.POINTER(ReestimateInfo),
+                                        C.POINTER(Err)]
+    L.fstk_gpu_refit_correction.argtypes = [VP, VP, VP, C.POINTER(Err)]
+    L.fstk_gpu_refit_apply.argtypes = [VP, VP, VP, DP, C.POINTER(Err)]
+    L.fstk_gpu_refit_finish.argtypes = [VP, VP, DP, C.POINTER(ReestimateInfo), C.POINTER(Err)]
     L.fstk_gpu_refit_end.argtypes = [VP]
     L.fstk_gpu_refit_end.restype = None
     L.fstk_gpu_refit_rows.argtypes = [VP, C.POINTER(C.c_uint64), C.POINTER(Err)]

@@ -669,6 +669,11 @@ struct fstk_gpu_refit {
   DevBuf<double> val_points, val_values;
   int64_t n_val = 0;
   std::vector<double> h_val_values;
+  // Solve state: Cholesky factor of the (summed) Gram, or the eigen fallback.
+  DevBuf<double> L;       // R x R, lower Cholesky factor
+  bool factored = false;
+  bool rank_def = false;
+  DevBuf<double> tmp_r;   // local residual rows
   ~fstk_gpu_refit() {
     if (stream) cudaStreamDestroy(stream);
   }
@@ -914,97 +919,228 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double
   });
 }
 
-int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const double* rhs_in,
-                             double* core_out, fstk_reestimate_info* info, fstk_gpu_error* err) {
+// ---- solve: Cholesky of the summed normal equations + iterative refinement
+// against the sketched system itself (corrected semi-normal equations), which
+// converges to the least-squares solution the reference's QR computes
+// (randls.cpp:112-123) with O(cond(A) eps) instead of O(cond(A)^2 eps) error.
+namespace fstk_gpu {
+
+static void minnorm_solve(fstk_gpu_refit* rf, const double* gram_in, const double* rhs_in,
+                          double* x_dev) {
+  // Not positive definite: minimum-norm solution on the numerical range of
+  // the Gram (stands in for the COD fallback, randls.cpp:117-121).
+  Handles& h = handles(rf->device);
+  cudaStream_t s = rf->stream;
+  const int n = static_cast<int>(rf->R);
+  DevBuf<double> G(static_cast<size_t>(n) * n), wv(n);
+  DevBuf<int> dinfo(1);
+  FSTK_CUDA(cudaMemcpyAsync(G.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
+  int lw2 = 0;
+  if (cusolverDnDsyevd_bufferSize(h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                  G.p, n, wv.p, &lw2) != CUSOLVER_STATUS_SUCCESS)
+    fail(FSTK_E_COMPUTE, "syevd_bufferSize failed");
+  DevBuf<double> w2(std::max(lw2, 1));
+  if (cusolverDnDsyevd(h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, G.p, n,
+                       wv.p, w2.p, lw2, dinfo.p) != CUSOLVER_STATUS_SUCCESS)
+    fail(FSTK_E_COMPUTE, "syevd failed");
+  count_launch();
+  std::vector<double> ev(n), V(static_cast<size_t>(n) * n), rhs(n);
+  FSTK_CUDA(cudaMemcpyAsync(ev.data(), wv.p, n * 8, cudaMemcpyDeviceToHost, s));
+  FSTK_CUDA(cudaMemcpyAsync(V.data(), G.p, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToHost, s));
+  FSTK_CUDA(cudaMemcpyAsync(rhs.data(), rhs_in, n * 8, cudaMemcpyDeviceToHost, s));
+  FSTK_CUDA(cudaStreamSynchronize(s));
+  const double lmax = std::max(std::fabs(ev[n - 1]), std::fabs(ev[0]));
+  const double thr = lmax * static_cast<double>(n) * 2.220446049250313e-16;
+  std::vector<double> sol(n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    if (ev[j] <= thr) continue;
+    double c = 0.0;
+    for (int i = 0; i < n; ++i) c += V[static_cast<size_t>(j) * n + i] * rhs[i];
+    c /= ev[j];
+    for (int i = 0; i < n; ++i) sol[i] += c * V[static_cast<size_t>(j) * n + i];
+  }
+  FSTK_CUDA(cudaMemcpyAsync(x_dev, sol.data(), n * 8, cudaMemcpyHostToDevice, s));
+  FSTK_CUDA(cudaStreamSynchronize(s));
+}
+
+static double dev_norm(cublasHandle_t h, int n, const double* x) {
+  double r = 0.0;
+  if (cublasDnrm2(h, n, x, 1, &r) != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, "cublasDnrm2 failed");
+  return r;
+}
+
+}  // namespace fstk_gpu
+
+int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const double* rhs_in,
+                              double* x_dev, fstk_reestimate_info* info, fstk_gpu_error* err) {
   return guarded(err, [&] {
-    require(rf && gram_in && rhs_in && core_out, FSTK_E_PARAMETER, "null argument");
+    require(rf && gram_in && rhs_in && x_dev, FSTK_E_PARAMETER, "null argument");
     DeviceGuard dg(rf->device);
     cudaStream_t s = rf->stream;
     Handles& h = handles(rf->device);
     cusolverDnSetStream(h.solver, s);
     const int n = static_cast<int>(rf->R);
     EventTimer ts(s);
-    DevBuf<double> G(static_cast<size_t>(n) * n), x(n);
-    FSTK_CUDA(cudaMemcpyAsync(G.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
-    FSTK_CUDA(cudaMemcpyAsync(x.p, rhs_in, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
+    rf->L.ensure(static_cast<size_t>(n) * n);
+    FSTK_CUDA(cudaMemcpyAsync(rf->L.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
+    FSTK_CUDA(cudaMemcpyAsync(x_dev, rhs_in, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
     int lwork = 0;
     ProfScope prof(FSTK_PROF_SOLVE, s);
-    if (cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, n, G.p, n, &lwork) !=
+    if (cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, n, rf->L.p, n, &lwork) !=
         CUSOLVER_STATUS_SUCCESS)
       fail(FSTK_E_COMPUTE, "potrf_bufferSize failed");
     DevBuf<double> work(std::max(lwork, 1));
     DevBuf<int> dinfo(1);
-    if (cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, n, G.p, n, work.p, lwork, dinfo.p) !=
+    if (cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, n, rf->L.p, n, work.p, lwork, dinfo.p) !=
         CUSOLVER_STATUS_SUCCESS)
       fail(FSTK_E_COMPUTE, "potrf failed");
     count_launch();
     int hinfo = 0;
     FSTK_CUDA(cudaMemcpyAsync(&hinfo, dinfo.p, 4, cudaMemcpyDeviceToHost, s));
     FSTK_CUDA(cudaStreamSynchronize(s));
-    bool rank_def = false;
-    if (hinfo == 0) {
-      if (cusolverDnDpotrs(h.solver, CUBLAS_FILL_MODE_LOWER, n, 1, G.p, n, x.p, n, dinfo.p) !=
+    rf->factored = hinfo == 0;
+    rf->rank_def = !rf->factored;
+    if (rf->factored) {
+      if (cusolverDnDpotrs(h.solver, CUBLAS_FILL_MODE_LOWER, n, 1, rf->L.p, n, x_dev, n, dinfo.p) !=
           CUSOLVER_STATUS_SUCCESS)
         fail(FSTK_E_COMPUTE, "potrs failed");
       count_launch();
     } else {
-      // Not positive definite: minimum-norm solution on the numerical range
-      // (stands in for the COD fallback, randls.cpp:117-121).
-      rank_def = true;
-      FSTK_CUDA(cudaMemcpyAsync(G.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
-      DevBuf<double> wv(n);
-      int lw2 = 0;
-      if (cusolverDnDsyevd_bufferSize(h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
-                                      G.p, n, wv.p, &lw2) != CUSOLVER_STATUS_SUCCESS)
-        fail(FSTK_E_COMPUTE, "syevd_bufferSize failed");
-      DevBuf<double> w2(std::max(lw2, 1));
-      if (cusolverDnDsyevd(h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, G.p, n,
-                           wv.p, w2.p, lw2, dinfo.p) != CUSOLVER_STATUS_SUCCESS)
-        fail(FSTK_E_COMPUTE, "syevd failed");
-      count_launch();
-      std::vector<double> ev(n), V(static_cast<size_t>(n) * n), rhs(n);
-      FSTK_CUDA(cudaMemcpyAsync(ev.data(), wv.p, n * 8, cudaMemcpyDeviceToHost, s));
-      FSTK_CUDA(cudaMemcpyAsync(V.data(), G.p, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToHost, s));
-      FSTK_CUDA(cudaMemcpyAsync(rhs.data(), rhs_in, n * 8, cudaMemcpyDeviceToHost, s));
-      FSTK_CUDA(cudaStreamSynchronize(s));
-      const double lmax = std::max(std::fabs(ev[n - 1]), std::fabs(ev[0]));
-      const double thr = lmax * static_cast<double>(n) * 2.220446049250313e-16;
-      std::vector<double> sol(n, 0.0);
-      for (int j = 0; j < n; ++j) {
-        if (ev[j] <= thr) continue;
-        double c = 0.0;
-        for (int i = 0; i < n; ++i) c += V[static_cast<size_t>(j) * n + i] * rhs[i];
-        c /= ev[j];
-        for (int i = 0; i < n; ++i) sol[i] += c * V[static_cast<size_t>(j) * n + i];
-      }
-      FSTK_CUDA(cudaMemcpy(x.p, sol.data(), n * 8, cudaMemcpyHostToDevice));
+      minnorm_solve(rf, gram_in, rhs_in, x_dev);
     }
-    FSTK_CUDA(cudaMemcpyAsync(core_out, x.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, s));
     FSTK_CUDA(cudaStreamSynchronize(s));
     if (info) {
-      info->t_solve = ts.seconds();
-      info->rank_deficient = rank_def ? 1 : 0;
+      info->t_solve += ts.seconds();
+      info->rank_deficient = rf->rank_def ? 1 : 0;
     }
-    // Validation residuals with the old and the new core (randls.cpp:379-381).
+  });
+}
+
+// s = A_local^T (b_local - A_local x): this shard's part of the refinement rhs.
+int32_t fstk_gpu_refit_correction(fstk_gpu_refit* rf, const double* x_dev, double* s_dev,
+                                  fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && x_dev && s_dev, FSTK_E_PARAMETER, "null argument");
+    DeviceGuard dg(rf->device);
+    cudaStream_t s = rf->stream;
+    Handles& h = handles(rf->device);
+    cublasSetStream(h.blas, s);
+    const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
+    const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
+    const int n = static_cast<int>(rf->R);
+    if (arows == 0) {
+      FSTK_CUDA(cudaMemsetAsync(s_dev, 0, static_cast<size_t>(n) * 8, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    rf->tmp_r.ensure(static_cast<size_t>(arows));
+    FSTK_CUDA(cudaMemcpyAsync(rf->tmp_r.p, rf->b.p, arows * 8, cudaMemcpyDeviceToDevice, s));
+    const double one = 1.0, mone = -1.0, zero = 0.0;
+    ProfScope prof(FSTK_PROF_SOLVE, s);
+    if (cublasDgemv(h.blas, CUBLAS_OP_N, static_cast<int>(arows), n, &mone, rf->A.p,
+                    static_cast<int>(arows), x_dev, 1, &one, rf->tmp_r.p, 1) != CUBLAS_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "cublasDgemv failed");
+    if (cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(arows), n, &one, rf->A.p,
+                    static_cast<int>(arows), rf->tmp_r.p, 1, &zero, s_dev, 1) != CUBLAS_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "cublasDgemv failed");
+    count_launch(2);
+    FSTK_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// x += (L L^T)^{-1} s (s summed over shards); rel_step = ||dx|| / ||x||.
+int32_t fstk_gpu_refit_apply(fstk_gpu_refit* rf, const double* s_dev, double* x_dev,
+                             double* rel_step, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && s_dev && x_dev, FSTK_E_PARAMETER, "null argument");
+    require(rf->factored, FSTK_E_PARAMETER, "refit: no Cholesky factor to refine with");
+    DeviceGuard dg(rf->device);
+    cudaStream_t s = rf->stream;
+    Handles& h = handles(rf->device);
+    cusolverDnSetStream(h.solver, s);
+    cublasSetStream(h.blas, s);
+    const int n = static_cast<int>(rf->R);
+    DevBuf<double> dx(n);
+    DevBuf<int> dinfo(1);
+    FSTK_CUDA(cudaMemcpyAsync(dx.p, s_dev, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
+    ProfScope prof(FSTK_PROF_SOLVE, s);
+    if (cusolverDnDpotrs(h.solver, CUBLAS_FILL_MODE_LOWER, n, 1, rf->L.p, n, dx.p, n, dinfo.p) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "potrs failed");
+    const double one = 1.0;
+    if (cublasDaxpy(h.blas, n, &one, dx.p, 1, x_dev, 1) != CUBLAS_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "cublasDaxpy failed");
+    count_launch(2);
+    const double ndx = dev_norm(h.blas, n, dx.p), nx = dev_norm(h.blas, n, x_dev);
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    if (rel_step) *rel_step = nx > 0 ? ndx / nx : ndx;
+  });
+}
+
+// Copies x to the host core and evaluates the validation residuals with the
+// old and the new core (randls.cpp:379-381).
+int32_t fstk_gpu_refit_finish(fstk_gpu_refit* rf, const double* x_dev, double* core_out,
+                              fstk_reestimate_info* info, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && x_dev && core_out, FSTK_E_PARAMETER, "null argument");
+    DeviceGuard dg(rf->device);
+    cudaStream_t s = rf->stream;
+    FSTK_CUDA(cudaMemcpyAsync(core_out, x_dev, static_cast<size_t>(rf->R) * 8, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
     EventTimer tr(s);
     std::vector<double> pred(rf->n_val), pred2(rf->n_val);
     if (rf->n_val > 0) {
       DevBuf<double> dp(rf->n_val);
-      {
-        std::lock_guard<std::mutex> lk(rf->model->mu);
-        evaluate_device_core(rf->model, nullptr, rf->val_points.p, rf->n_val, rf->n_val, dp.p, s);
-        FSTK_CUDA(cudaMemcpyAsync(pred.data(), dp.p, rf->n_val * 8, cudaMemcpyDeviceToHost, s));
-        FSTK_CUDA(cudaStreamSynchronize(s));
-        evaluate_device_core(rf->model, core_out, rf->val_points.p, rf->n_val, rf->n_val, dp.p, s);
-        FSTK_CUDA(cudaMemcpyAsync(pred2.data(), dp.p, rf->n_val * 8, cudaMemcpyDeviceToHost, s));
-        FSTK_CUDA(cudaStreamSynchronize(s));
-      }
+      std::lock_guard<std::mutex> lk(rf->model->mu);
+      evaluate_device_core(rf->model, nullptr, rf->val_points.p, rf->n_val, rf->n_val, dp.p, s);
+      FSTK_CUDA(cudaMemcpyAsync(pred.data(), dp.p, rf->n_val * 8, cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));
+      evaluate_device_core(rf->model, core_out, rf->val_points.p, rf->n_val, rf->n_val, dp.p, s);
+      FSTK_CUDA(cudaMemcpyAsync(pred2.data(), dp.p, rf->n_val * 8, cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));
     }
     if (info) {
       info->residual_before = rel_residual(pred, rf->h_val_values);
       info->residual_after = rel_residual(pred2, rf->h_val_values);
       info->t_residual = tr.seconds();
+      info->rank_deficient = rf->rank_def ? 1 : 0;
     }
+  });
+}
+
+// Single-shard convenience: factor, refine until the step stalls, finish.
+int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const double* rhs_in,
+                             double* core_out, fstk_reestimate_info* info, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && gram_in && rhs_in && core_out, FSTK_E_PARAMETER, "null argument");
+    require(rf->shards == 1, FSTK_E_PARAMETER,
+            "refit_solve needs the whole sketch; sharded refits use factor/correction/apply");
+    DeviceGuard dg(rf->device);
+    const int n = static_cast<int>(rf->R);
+    DevBuf<double> x(n), sv(n);
+    auto rc = [&](int32_t c) {
+      if (c) throw Error{c, err ? err->message : "refit stage failed"};
+    };
+    rc(fstk_gpu_refit_factor(rf, gram_in, rhs_in, x.p, info, err));
+    if (rf->factored) {
+      EventTimer tref(rf->stream);
+      double prev = 1e300;
+      for (int it = 0; it < 6; ++it) {
+        rc(fstk_gpu_refit_correction(rf, x.p, sv.p, err));
+        double step = 0.0;
+        rc(fstk_gpu_refit_apply(rf, sv.p, x.p, &step, err));
+        if (step <= 1e-15) break;
+        if (it >= 1 && step > 0.5 * prev) {
+          // No contraction: cond(A)^2 eps is not small; keep the iterate but
+          // report the system as numerically rank deficient.
+          rf->rank_def = true;
+          break;
+        }
+        prev = step;
+      }
+      if (info) info->t_solve += tref.seconds();
+    }
+    rc(fstk_gpu_refit_finish(rf, x.p, core_out, info, err));
   });
 }
 

@@ -36,6 +36,30 @@ def evaluate_sharded(model, points, rank: int, world: int):
     return lo, hi, model.evaluate_batch(np.asfortranarray(points[lo:hi]))
 
 
+def refine_distributed(sess, gram, rhs, max_iter: int = 6, group=None):
+    """Cholesky of the summed Gram on every rank, then iterative refinement
+    against the row-sharded sketch: each step needs one all-reduce of an
+    R-vector.  Returns the solution tensor x (identical on all ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    x = torch.empty_like(rhs)
+    ok = sess.factor(gram, rhs, x)
+    if not ok:
+        return x
+    s = torch.empty_like(rhs)
+    prev = float("inf")
+    for it in range(max_iter):
+        sess.correction(x, s)
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(s, group=group)
+        step = sess.apply(s, x)
+        if step <= 1e-15 or (it >= 1 and step > 0.5 * prev):
+            break
+        prev = step
+    return x
+
+
 def refit_distributed(model, points, values, rank: int, world: int, device=None, **kw):
     """Row-sharded refit: returns (new_model, info) on rank 0, (None, info) elsewhere."""
     import torch
@@ -50,9 +74,10 @@ def refit_distributed(model, points, values, rank: int, world: int, device=None,
     rhs = torch.empty(R, dtype=torch.float64, device=dev)
     sess.normal_equations(gram, rhs)
     reduce_normal_equations(gram, rhs)
+    x = refine_distributed(sess, gram, rhs)
     new = None
     if rank == 0:
-        core = sess.solve(gram, rhs)
+        core = sess.finish(x)
         new = model.with_core(core)
     info = sess.info_dict()
     sess.close()

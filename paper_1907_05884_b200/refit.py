@@ -115,6 +115,32 @@ class RefitSession:
                                          C.byref(self.info), C.byref(err)), err)
         return core
 
+    # -- sharded solve stages (see include/fstk_gpu.h) --------------------------
+    def factor(self, gram_t, rhs_t, x_t):
+        err = Err()
+        check(lib().fstk_gpu_refit_factor(self._h, gram_t.data_ptr(), rhs_t.data_ptr(),
+                                          x_t.data_ptr(), C.byref(self.info), C.byref(err)), err)
+        return not bool(self.info.rank_deficient)
+
+    def correction(self, x_t, s_t):
+        err = Err()
+        check(lib().fstk_gpu_refit_correction(self._h, x_t.data_ptr(), s_t.data_ptr(),
+                                              C.byref(err)), err)
+
+    def apply(self, s_t, x_t) -> float:
+        step = C.c_double()
+        err = Err()
+        check(lib().fstk_gpu_refit_apply(self._h, s_t.data_ptr(), x_t.data_ptr(), C.byref(step),
+                                         C.byref(err)), err)
+        return step.value
+
+    def finish(self, x_t) -> np.ndarray:
+        core = np.zeros(self.R)
+        err = Err()
+        check(lib().fstk_gpu_refit_finish(self._h, x_t.data_ptr(), dptr(core), C.byref(self.info),
+                                          C.byref(err)), err)
+        return core
+
     def info_dict(self) -> dict:
         return _info_dict(self.info)
 
