@@ -119,13 +119,86 @@ __global__ void __launch_bounds__(128) mode_tables_kernel(
   }
 }
 
-// ------------------------------------------------------- K1b contract ---
-constexpr int TP = 128;        // points per CTA tile
-constexpr int U0_LD = TP + 4;  // u0 column stride: conflict-free A fragments
-constexpr int U1_LD = TP + 2;  // u1 column stride: conflict-free epilogue reads
-constexpr int NCW = 8;         // consumer warps: 4 point groups x 2 column halves
-constexpr int NTHREADS = (NCW + 1) * 32;
+// Dense-coefficient variant (the hot one): thread per (row, JC functions).
+// The mode's coefficient block C[i][j] (zero where a function has no index i)
+// sits in shared memory and is read with uniform (broadcast) loads; the
+// Legendre value L_i is produced by the recurrence in registers and applied
+// to JC independent accumulators, in ascending i.  Adding the zero entries
+// leaves every partial sum unchanged, so with EXACT (separate multiply/add)
+// this reproduces the reference's sparse dot (model.cpp:86-88) bit for bit
+// whenever the indices are strictly increasing (format.md:67).
+template <bool EXACT, int JC>
+__global__ void __launch_bounds__(128) mode_dense_kernel(
+    ModeDev md, const double* __restrict__ xs, int64_t n, int64_t n_out,
+    const int64_t* __restrict__ row_src, double* __restrict__ tk, int64_t ldt,
+    unsigned long long* err_row) {
+  extern __shared__ __align__(16) double Cs[];  // (pmax+1) x JC
+  const int j0 = blockIdx.y * JC;
+  const int p = md.pmax;
+  for (int e = threadIdx.x; e < (p + 1) * JC; e += blockDim.x)
+    Cs[e] = md.dense[(e / JC) * md.ldc + j0 + (e % JC)];
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_out) return;
+  int64_t src = i;
+  bool valid = i < n;
+  if (row_src) {
+    src = i < n ? row_src[i] : -1;
+    valid = src >= 0;
+  }
+  const int jn = min(JC, md.r - j0);
+  if (!valid) {
+#pragma unroll
+    for (int j = 0; j < JC; ++j)
+      if (j < jn) tk[(j0 + j) * ldt + i] = 0.0;
+    return;
+  }
+  const double x = xs[src];
+  double t;
+  if (!(x >= md.lo - md.slack && x <= md.hi + md.slack)) {
+    atomicMin(err_row, static_cast<unsigned long long>(i));
+    t = 0.0;
+  } else {
+    const double cl = fmin(md.hi, fmax(md.lo, x));
+    t = xadd(-1.0, __ddiv_rn(xmul(2.0, xsub(cl, md.lo)), md.span));
+  }
+  double acc[JC];
+#pragma unroll
+  for (int j = 0; j < JC; ++j) acc[j] = 0.0;
+  auto apply = [&](const double* row, double L) {
+    const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+    for (int j = 0; j < JC / 2; ++j) {
+      const double2 c = r2[j];
+      if (EXACT) {
+        acc[2 * j] = xadd(acc[2 * j], xmul(c.x, L));
+        acc[2 * j + 1] = xadd(acc[2 * j + 1], xmul(c.y, L));
+      } else {
+        acc[2 * j] = fma(c.x, L, acc[2 * j]);
+        acc[2 * j + 1] = fma(c.y, L, acc[2 * j + 1]);
+      }
+    }
+  };
+  // legendre_values (basis.cpp:49-61), same rounding sequence.
+  apply(Cs, 1.0);
+  if (p >= 1) apply(Cs + JC, xmul(c_leg.norm[1], t));
+  double pm1 = 1.0, pm0 = t;
+  for (int q = 1; q < p; ++q) {
+    const double num = xsub(xmul(xmul(c_leg.a[q], t), pm0), xmul(c_leg.b[q], pm1));
+    const double pn1 = xdiv_small(num, c_leg.c[q], c_leg.rc[q]);
+    pm1 = pm0;
+    pm0 = pn1;
+    apply(Cs + (q + 1) * JC, xmul(c_leg.norm[q + 1], pn1));
+  }
+#pragma unroll
+  for (int j = 0; j < JC; ++j)
+    if (j < jn) tk[(j0 + j) * ldt + i] = acc[j];
+}
 
+// ------------------------------------------------------- K1b contract ---
+// Tile of TP points per CTA; consumer warps = (TP/32 point groups) x 2 column
+// halves; one producer warp streams the u tables (per tile) and the core
+// tiles (ring of nstage) with TMA bulk copies completing on mbarriers.
 struct ContractParams {
   const double* tables;
   Int64x8 toff;
@@ -140,48 +213,81 @@ struct ContractParams {
   double* out;
 };
 
+__host__ __device__ constexpr int u0_ld(int tp) { return tp + 4; }  // conflict-free A fragments
+__host__ __device__ constexpr int u1_ld(int tp) { return tp + 2; }  // conflict-free epilogue
+
 struct SmemLayout {
-  size_t bars, u0, u1, uk, bst, ybuf, total;
-  size_t ukoff[kMaxOrder];
+  uint32_t bars, u0, u1, uk, bst, ybuf, total;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(const ContractParams& P) {
+__host__ __device__ inline SmemLayout smem_layout(const ContractParams& P, int tp) {
   SmemLayout L{};
-  size_t o = 0;
+  uint32_t o = 0;
   L.bars = o;
   o += ((2 * P.nstage + 2) * 8 + 127) / 128 * 128;
   L.u0 = o;
-  o += static_cast<size_t>(P.Kp) * U0_LD * 8;
+  o += static_cast<uint32_t>(P.Kp) * u0_ld(tp) * 8;
   L.u1 = o;
-  o += static_cast<size_t>(P.N1) * U1_LD * 8;
+  o += static_cast<uint32_t>(P.N1) * u1_ld(tp) * 8;
   L.uk = o;
-  for (int k = 2; k < P.d; ++k) {
-    L.ukoff[k] = o;
-    o += static_cast<size_t>(P.r[k]) * TP * 8;
-  }
+  for (int k = 2; k < P.d; ++k) o += static_cast<uint32_t>(P.r[k]) * tp * 8;
   o = (o + 127) / 128 * 128;
   L.bst = o;
-  o += static_cast<size_t>(P.nstage) * P.Kp * P.N1p * 8;
+  o += static_cast<uint32_t>(P.nstage) * P.Kp * P.N1p * 8;
   L.ybuf = o;
-  o += 2 * TP * 8;
+  o += 2 * tp * 8;
   L.total = o;
   return L;
 }
 
+template <int NCW>
 __device__ __forceinline__ void consumer_bar() {
   asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
 }
 
-template <int NSW>
-__global__ void __launch_bounds__(NTHREADS, 1) contract_kernel(const ContractParams P) {
+// Outer factor prod_{k>=2} u_k[j_k(m)] for one row; D = compile-time order
+// (0 = generic runtime order, d >= 5).
+template <int D>
+__device__ __forceinline__ double outer_factor(const ContractParams& P, const double* uk_base,
+                                               const int* jk, int row, int tp) {
+  if constexpr (D == 2) {
+    return 1.0;
+  } else if constexpr (D == 3) {
+    return uk_base[jk[0] * tp + row];
+  } else if constexpr (D > 3) {
+    double o = uk_base[jk[0] * tp + row];
+    const double* base = uk_base + P.r[2] * tp;
+#pragma unroll
+    for (int k = 3; k < D; ++k) {
+      o = o * base[jk[k - 2] * tp + row];
+      base += P.r[k] * tp;
+    }
+    return o;
+  } else {
+    double o = 1.0;
+    const double* base = uk_base;
+    for (int k = 2; k < P.d; ++k) {
+      o = o * base[jk[k - 2] * tp + row];
+      base += P.r[k] * tp;
+    }
+    return o;
+  }
+}
+
+template <int NSW, int D, int TP>
+__global__ void __launch_bounds__((TP / 32 * 2 + 1) * 32) contract_kernel(const ContractParams P) {
+  constexpr int NPG = TP / 32;        // 32-point groups
+  constexpr int NCW = NPG * 2;        // consumer warps
+  constexpr int U0_LD = u0_ld(TP), U1_LD = u1_ld(TP);
   extern __shared__ __align__(1024) unsigned char smem[];
-  const SmemLayout L = smem_layout(P);
+  const SmemLayout L = smem_layout(P, TP);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* empty = full + P.nstage;
   uint64_t* ufull = empty + P.nstage;
   uint64_t* uempty = ufull + 1;
   double* u0s = reinterpret_cast<double*>(smem + L.u0);
   double* u1s = reinterpret_cast<double*>(smem + L.u1);
+  double* uks = reinterpret_cast<double*>(smem + L.uk);
   double* bst = reinterpret_cast<double*>(smem + L.bst);
   double* ybuf = reinterpret_cast<double*>(smem + L.ybuf);
   const int warp = threadIdx.x >> 5;
@@ -207,20 +313,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) contract_kernel(const ContractPar
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      uint32_t ubytes = static_cast<uint32_t>(P.Kp + P.N1) * TP * 8u;
+      for (int k = 2; k < P.d; ++k) ubytes += static_cast<uint32_t>(P.r[k]) * TP * 8u;
       for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x, ++it) {
         if (it > 0) mbar_wait(uempty, (it - 1) & 1);
-        uint32_t ubytes = static_cast<uint32_t>(P.Kp + P.N1) * TP * 8u;
-        for (int k = 2; k < P.d; ++k) ubytes += static_cast<uint32_t>(P.r[k]) * TP * 8u;
         mbar_arrive_expect_tx(ufull, ubytes);
         const int64_t row0 = tile * TP;
         const double* t0 = P.tables + P.toff.v[0] + row0;
         for (int j = 0; j < P.Kp; ++j) bulk_g2s(u0s + j * U0_LD, t0 + j * P.ldt, TP * 8, ufull);
         const double* t1 = P.tables + P.toff.v[1] + row0;
         for (int j = 0; j < P.N1; ++j) bulk_g2s(u1s + j * U1_LD, t1 + j * P.ldt, TP * 8, ufull);
+        double* dst = uks;
         for (int k = 2; k < P.d; ++k) {
-          double* dst = reinterpret_cast<double*>(smem + L.ukoff[k]);
           const double* tk = P.tables + P.toff.v[k] + row0;
           for (int j = 0; j < P.r[k]; ++j) bulk_g2s(dst + j * TP, tk + j * P.ldt, TP * 8, ufull);
+          dst += P.r[k] * TP;
         }
         for (int tt = 0; tt < NT; ++tt) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -238,19 +345,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) contract_kernel(const ContractPar
   }
 
   // ===== consumer warps =====
-  const int pg = warp & 3;   // 32-point group
-  const int nh = warp >> 2;  // column half
+  const int pg = warp % NPG;  // 32-point group
+  const int nh = warp / NPG;  // column half
   const int g = lane >> 2, t = lane & 3;
-  const int NS = 2 * NSW;
+  constexpr int NS = 2 * NSW;
   int stage = 0;
   uint32_t phase = 0;
   int it = 0;
+  const int ksteps = P.Kp / 4;
   for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x, ++it) {
     mbar_wait(ufull, it & 1);
     double y[4] = {0.0, 0.0, 0.0, 0.0};
+    int c = 0;                              // j1 chunk
+    constexpr int NJK = D == 0 ? kMaxOrder - 2 : (D > 2 ? D - 2 : 1);
+    int jk[NJK] = {0};  // digits j_2, j_3, ... of m
     for (int tt = 0; tt < NT; ++tt) {
-      const int c = tt % P.NC;
-      const int m = tt / P.NC;
       mbar_wait(&full[stage], phase);
       const double* B = bst + static_cast<size_t>(stage) * stage_elems;
       double acc[4][NSW][2];
@@ -260,7 +369,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) contract_kernel(const ContractPar
         for (int b = 0; b < NSW; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
       const double* ua = u0s + t * U0_LD + pg * 32 + g;
       const double* bb = B + (nh * NSW) * 32 + lane;
-      for (int ks = 0; ks < P.Kp / 4; ++ks) {
+#pragma unroll 4
+      for (int ks = 0; ks < ksteps; ++ks) {
         double av[4], bv[NSW];
 #pragma unroll
         for (int a = 0; a < 4; ++a) av[a] = ua[(4 * ks) * U0_LD + a * 8];
@@ -277,25 +387,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) contract_kernel(const ContractPar
         stage = 0;
         phase ^= 1;
       }
-      // Epilogue: W = sum_j1 T u1; y += W * prod_{k>=2} u_k.
+      // Epilogue: W = sum_j1 T u1; y += W * prod_{k>=2} u_k (no integer division:
+      // the digits of m advance like an odometer).
+      const double* u1c = u1s + (c * P.N1p + nh * NSW * 8 + 2 * t) * U1_LD;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int row = pg * 32 + a * 8 + g;
-        double o = 1.0;
-        int rem = m;
-        for (int k = 2; k < P.d; ++k) {
-          const int jk = rem % P.r[k];
-          rem /= P.r[k];
-          o *= reinterpret_cast<const double*>(smem + L.ukoff[k])[jk * TP + row];
-        }
+        const double o = outer_factor<D>(P, uks, jk, row, TP);
         double w = 0.0;
 #pragma unroll
         for (int b = 0; b < NSW; ++b) {
-          const int j1 = c * P.N1p + (nh * NSW + b) * 8 + 2 * t;
-          w = fma(acc[a][b][0], u1s[j1 * U1_LD + row], w);
-          w = fma(acc[a][b][1], u1s[(j1 + 1) * U1_LD + row], w);
+          w = fma(acc[a][b][0], u1c[(b * 8) * U1_LD + row], w);
+          w = fma(acc[a][b][1], u1c[(b * 8 + 1) * U1_LD + row], w);
         }
         y[a] = fma(w, o, y[a]);
+      }
+      if (++c == P.NC) {
+        c = 0;
+        if constexpr (D != 2) {
+          const int dd = (D == 0) ? P.d : D;
+          for (int k = 2; k < dd; ++k) {
+            if (++jk[k - 2] < P.r[k]) break;
+            jk[k - 2] = 0;
+          }
+        }
       }
     }
     __syncwarp();
@@ -306,13 +421,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) contract_kernel(const ContractPar
       y[a] += __shfl_xor_sync(0xffffffffu, y[a], 2);
       if (t == 0) ybuf[nh * TP + pg * 32 + a * 8 + g] = y[a];
     }
-    consumer_bar();
+    consumer_bar<NCW>();
     if (nh == 0) {
       const int row = pg * 32 + lane;
       const int64_t gi = tile * TP + row;
       if (gi < P.n) P.out[gi] = ybuf[row] + ybuf[TP + row];
     }
-    consumer_bar();
+    consumer_bar<NCW>();
   }
 }
 
@@ -358,17 +473,58 @@ static size_t mode_smem(const fstk_gpu_model* m, int k0, int k1, int threads) {
   return static_cast<size_t>(pm + 1) * threads * sizeof(double);
 }
 
+template <bool EXACT, int JC>
+static void launch_dense_t(const ModeDev& md, const double* xs, int64_t n, int64_t n_out,
+                           const int64_t* row_src, double* tk, int64_t ldt,
+                           unsigned long long* err_row, cudaStream_t s, int device) {
+  static std::once_flag once[64];
+  std::call_once(once[device & 63], [&] {
+    FSTK_CUDA(cudaFuncSetAttribute(mode_dense_kernel<EXACT, JC>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (kMaxDegree + 1) * JC * static_cast<int>(sizeof(double))));
+  });
+  const size_t sm = static_cast<size_t>(md.pmax + 1) * JC * sizeof(double);
+  dim3 grid(static_cast<unsigned>(ceil_div(n_out, 128)), static_cast<unsigned>(md.nchunk));
+  mode_dense_kernel<EXACT, JC><<<grid, 128, sm, s>>>(md, xs, n, n_out, row_src, tk, ldt, err_row);
+  check_launch("mode_dense_kernel");
+}
+
+template <bool EXACT>
+static void launch_dense(const ModeDev& md, const double* xs, int64_t n, int64_t n_out,
+                         const int64_t* row_src, double* tk, int64_t ldt,
+                         unsigned long long* err_row, cudaStream_t s, int device) {
+  switch (md.jc) {
+#define FSTK_JC(J) \
+  case J: launch_dense_t<EXACT, J>(md, xs, n, n_out, row_src, tk, ldt, err_row, s, device); break;
+    FSTK_JC(8) FSTK_JC(16) FSTK_JC(24) FSTK_JC(32) FSTK_JC(40) FSTK_JC(48) FSTK_JC(56) FSTK_JC(64)
+#undef FSTK_JC
+    default: fail(FSTK_E_COMPUTE, "internal: bad dense chunk width");
+  }
+}
+
 void launch_mode_tables(const fstk_gpu_model* m, const double* pts, int64_t ldp, int64_t n,
                         int64_t n_out, const int64_t* row_src, double* tables,
                         const int64_t* toff, int64_t ldt, bool exact,
                         unsigned long long* err_row, cudaStream_t s) {
   if (n_out <= 0) return;
+  ProfScope prof(FSTK_PROF_MODE_TABLES, s);
+  if (m->dense_ok) {
+    for (int k = 0; k < m->d; ++k) {
+      const ModeDev& md = m->modes_dev.m[k];
+      if (exact)
+        launch_dense<true>(md, pts + k * ldp, n, n_out, row_src, tables + toff[k], ldt, err_row, s,
+                           m->device);
+      else
+        launch_dense<false>(md, pts + k * ldp, n, n_out, row_src, tables + toff[k], ldt, err_row, s,
+                            m->device);
+    }
+    return;
+  }
   const int threads = 128;
   Int64x8 to{};
   for (int k = 0; k < m->d; ++k) to.v[k] = toff[k];
   const size_t sm = mode_smem(m, 0, m->d, threads);
   const unsigned blocks = static_cast<unsigned>(ceil_div(n_out, threads));
-  ProfScope prof(FSTK_PROF_MODE_TABLES, s);
   if (exact)
     mode_tables_kernel<true><<<blocks, threads, sm, s>>>(m->modes_dev, 0, m->d, pts, ldp, n,
                                                          n_out, row_src, tables, to, ldt, err_row);
@@ -382,9 +538,16 @@ void launch_mode_table_one(const fstk_gpu_model* m, int mode, const double* x, i
                            double* out, int64_t ldt, bool exact, unsigned long long* err_row,
                            cudaStream_t s) {
   if (n <= 0) return;
+  if (m->dense_ok) {
+    const ModeDev& md = m->modes_dev.m[mode];
+    if (exact)
+      launch_dense<true>(md, x, n, n, nullptr, out, ldt, err_row, s, m->device);
+    else
+      launch_dense<false>(md, x, n, n, nullptr, out, ldt, err_row, s, m->device);
+    return;
+  }
   const int threads = 128;
   Int64x8 to{};
-  // pts pointer is shifted so that pts[mode * ldp + i] == x[i] with ldp = 0.
   to.v[mode] = 0;
   const size_t sm = mode_smem(m, mode, mode + 1, threads);
   const unsigned blocks = static_cast<unsigned>(ceil_div(n, threads));
@@ -414,7 +577,7 @@ static ContractParams make_params(const fstk_gpu_model* m, const double* tables,
   for (int k = 0; k < m->d; ++k) P.toff.v[k] = toff[k];
   P.ldt = ldt;
   P.n = n;
-  P.ntiles = ceil_div(n, TP);
+  P.ntiles = ceil_div(n, m->lay.tp);
   P.d = m->d;
   for (int k = 0; k < m->d; ++k) P.r[k] = static_cast<int>(m->ranks[k]);
   P.Kp = m->lay.Kp;
@@ -428,19 +591,37 @@ static ContractParams make_params(const fstk_gpu_model* m, const double* tables,
   return P;
 }
 
-template <int NSW>
+template <int NSW, int D, int TPL>
 static void launch_contract_t(const fstk_gpu_model* m, const ContractParams& P, cudaStream_t s) {
   static std::once_flag once[64];
   const size_t smem = m->lay.smem;
   std::call_once(once[m->device & 63], [&] {
     int optin = 0;
     FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
-    FSTK_CUDA(cudaFuncSetAttribute(contract_kernel<NSW>,
+    FSTK_CUDA(cudaFuncSetAttribute(contract_kernel<NSW, D, TPL>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   });
-  const int64_t grid = std::min<int64_t>(P.ntiles, m->num_sms);
-  contract_kernel<NSW><<<static_cast<unsigned>(grid), NTHREADS, smem, s>>>(P);
+  const int64_t grid = std::min<int64_t>(P.ntiles, static_cast<int64_t>(m->num_sms) * m->lay.ctas_per_sm);
+  contract_kernel<NSW, D, TPL><<<static_cast<unsigned>(grid), (TPL / 32 * 2 + 1) * 32, smem, s>>>(P);
   check_launch("contract_kernel");
+}
+
+template <int NSW, int D>
+static void launch_contract_tp(const fstk_gpu_model* m, const ContractParams& P, cudaStream_t s) {
+  if (m->lay.tp == 64)
+    launch_contract_t<NSW, D, 64>(m, P, s);
+  else
+    launch_contract_t<NSW, D, 128>(m, P, s);
+}
+
+template <int NSW>
+static void launch_contract_d(const fstk_gpu_model* m, const ContractParams& P, cudaStream_t s) {
+  switch (m->d) {
+    case 2: launch_contract_tp<NSW, 2>(m, P, s); break;
+    case 3: launch_contract_tp<NSW, 3>(m, P, s); break;
+    case 4: launch_contract_tp<NSW, 4>(m, P, s); break;
+    default: launch_contract_tp<NSW, 0>(m, P, s); break;
+  }
 }
 
 void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_t* toff,
@@ -462,15 +643,18 @@ void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_
   ContractParams P = make_params(m, tables, toff, ldt, n, out);
   if (bpack_override) P.bpack = bpack_override;
   switch (m->lay.nsw) {
-    case 1: launch_contract_t<1>(m, P, s); break;
-    case 2: launch_contract_t<2>(m, P, s); break;
-    case 3: launch_contract_t<3>(m, P, s); break;
-    case 4: launch_contract_t<4>(m, P, s); break;
+    case 1: launch_contract_d<1>(m, P, s); break;
+    case 2: launch_contract_d<2>(m, P, s); break;
+    case 3: launch_contract_d<3>(m, P, s); break;
+    case 4: launch_contract_d<4>(m, P, s); break;
     default: fail(FSTK_E_COMPUTE, "internal: bad contraction layout");
   }
 }
 
 // ------------------------------------------------------------ model setup ---
+// Chooses the tile (TP = 64 or 128 points) and ring depth that maximise
+// resident consumer warps per SM (so one CTA's u-table prologue overlaps the
+// other CTAs' DMMA work), preferring deeper rings at equal residency.
 static void plan_layout(fstk_gpu_model* m) {
   ContractLayout& L = m->lay;
   L = ContractLayout{};
@@ -485,29 +669,39 @@ static void plan_layout(fstk_gpu_model* m) {
   for (int k = 2; k < m->d; ++k) L.Mout *= static_cast<int>(m->ranks[k]);
   L.nsw = L.N1p / 16;
   L.btile_elems = static_cast<int64_t>(L.Kp) * L.N1p;
-  m->rp[0] = L.Kp;
-  m->rp[1] = L.NC * L.N1p;
-  int optin = 0;
+  int optin = 0, per_sm = 0;
   FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
-  for (int ns = 4; ns >= 2; --ns) {
-    ContractParams P{};
-    P.d = m->d;
-    for (int k = 0; k < m->d; ++k) P.r[k] = static_cast<int>(m->ranks[k]);
-    P.Kp = L.Kp;
-    P.N1p = L.N1p;
-    P.NC = L.NC;
-    P.N1 = L.NC * L.N1p;
-    P.nstage = ns;
-    const SmemLayout S = smem_layout(P);
-    if (S.total <= static_cast<size_t>(optin)) {
-      L.nstage = ns;
-      L.smem = S.total;
-      L.fast = true;
-      break;
+  FSTK_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device));
+  double best = -1;
+  for (int tp : {64, 128}) {
+    for (int ns = 2; ns <= 6; ++ns) {
+      ContractParams P{};
+      P.d = m->d;
+      for (int k = 0; k < m->d; ++k) P.r[k] = static_cast<int>(m->ranks[k]);
+      P.Kp = L.Kp;
+      P.N1p = L.N1p;
+      P.NC = L.NC;
+      P.N1 = L.NC * L.N1p;
+      P.nstage = ns;
+      const SmemLayout S = smem_layout(P, tp);
+      if (S.total > static_cast<uint32_t>(optin)) continue;
+      const int ctas = std::min<int>(per_sm / static_cast<int>(S.total + 1024), 4);
+      if (ctas < 1) continue;
+      const int warps = ctas * (tp / 32 * 2);
+      const double score = std::min(warps, 16) * 100.0 + std::min(ns, 4) * 10.0 + tp / 64.0;
+      if (score > best) {
+        best = score;
+        L.tp = tp;
+        L.nstage = ns;
+        L.smem = S.total;
+        L.ctas_per_sm = ctas;
+        L.fast = true;
+      }
     }
   }
-  if (!L.fast) {
-    for (int k = 0; k < m->d; ++k) m->rp[k] = static_cast<int>(m->ranks[k]);
+  if (L.fast) {
+    m->rp[0] = L.Kp;
+    m->rp[1] = L.NC * L.N1p;
   }
 }
 
@@ -568,7 +762,7 @@ void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, cons
   Chunk& ck = m->chunk[0];
   const int64_t CH = m->chunk_points;
   int64_t toff[kMaxOrder], tot = 0;
-  const int64_t ldt = round_up(CH, TP);
+  const int64_t ldt = round_up(CH, 128);
   eval_table_offsets(m, ldt, toff, &tot);
   DevBuf<double> bp, craw;
   if (core_host) {
@@ -579,7 +773,7 @@ void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, cons
   FSTK_CUDA(cudaMemsetAsync(ck.err.p, 0xff, sizeof(unsigned long long), s));
   for (int64_t b = 0; b < n; b += CH) {
     const int64_t nb = std::min(CH, n - b);
-    const int64_t nout = round_up(nb, TP);
+    const int64_t nout = round_up(nb, 128);
     launch_mode_tables(m, pts + b, ldp, nb, nout, nullptr, ck.tables.p, toff, ldt, false,
                        ck.err.p, s);
     launch_contract(m, ck.tables.p, toff, ldt, nb, out + b, s, core_host ? bp.p : nullptr,
@@ -668,6 +862,7 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
         for (uint32_t s = 0; s < desc->nnz[f]; ++s, ++c) {
           require(static_cast<int>(desc->indices[c]) < dim, FSTK_E_SHAPE,
                   "model: coefficient index outside basis dimension");
+          if (s > 0 && desc->indices[c] <= desc->indices[c - 1]) mh.sorted = false;
           mh.idx.push_back(desc->indices[c]);
           mh.coef.push_back(desc->coeffs[c]);
         }
@@ -704,7 +899,32 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
     FSTK_CUDA(cudaMemcpy(m->d_rowptr.p, rowptr.data(), rowptr.size() * 4, cudaMemcpyHostToDevice));
     FSTK_CUDA(cudaMemcpy(m->d_idx.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice));
     FSTK_CUDA(cudaMemcpy(m->d_coef.p, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice));
+    // Dense coefficient blocks (pmax+1) x ldc per mode, for the dense kernel.
+    std::vector<double> dense;
+    std::vector<size_t> dense_off(d);
+    std::vector<int> jc(d), nch(d);
+    for (int k = 0; k < d; ++k) {
+      const ModeHost& mh = m->modes[k];
+      m->dense_ok = m->dense_ok && mh.sorted;
+      jc[k] = static_cast<int>(std::min<int64_t>(round_up(mh.r, 8), 64));
+      nch[k] = static_cast<int>(ceil_div(mh.r, jc[k]));
+      const int ldc = jc[k] * nch[k];
+      dense_off[k] = dense.size();
+      dense.resize(dense.size() + static_cast<size_t>(mh.pmax + 1) * ldc, 0.0);
+      double* blk = dense.data() + dense_off[k];
+      for (int j = 0; j < mh.r; ++j)
+        for (int s2 = mh.rowptr[j]; s2 < mh.rowptr[j + 1]; ++s2)
+          blk[static_cast<size_t>(mh.idx[s2]) * ldc + j] = mh.coef[s2];
+    }
+    m->d_dense.alloc(dense.size());
+    FSTK_CUDA(cudaMemcpy(m->d_dense.p, dense.data(), dense.size() * 8, cudaMemcpyHostToDevice));
     m->modes_dev.d = d;
+    for (int k = 0; k < d; ++k) {
+      m->modes_dev.m[k].dense = m->d_dense.p + dense_off[k];
+      m->modes_dev.m[k].jc = jc[k];
+      m->modes_dev.m[k].nchunk = nch[k];
+      m->modes_dev.m[k].ldc = jc[k] * nch[k];
+    }
     for (int k = 0; k < d; ++k) {
       ModeDev& md = m->modes_dev.m[k];
       const ModeHost& mh = m->modes[k];
@@ -725,9 +945,12 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
     // ~1/8 GB of tables per chunk, but at least 64K points.
     int64_t per_pt = 0;
     for (int k = 0; k < d; ++k) per_pt += m->rp[k];
-    m->chunk_points = std::max<int64_t>(65536, round_up((int64_t(1) << 27) / (per_pt * 8) * 8, TP));
-    m->chunk_points = std::min<int64_t>(m->chunk_points, int64_t(1) << 21);
-    m->chunk_points = round_up(m->chunk_points, TP);
+    // Chunks large enough that the last wave of tiles is a small fraction
+    // (>= ~100 tiles per SM), capped near 2 GB of table workspace.
+    m->chunk_points = std::min<int64_t>(int64_t(1) << 21,
+                                        std::max<int64_t>(int64_t(1) << 16,
+                                                          (int64_t(1) << 31) / (per_pt * 8)));
+    m->chunk_points = round_up(m->chunk_points, 128);
     for (auto& ck : m->chunk) {
       FSTK_CUDA(cudaStreamCreateWithFlags(&ck.stream, cudaStreamNonBlocking));
       FSTK_CUDA(cudaEventCreateWithFlags(&ck.done, cudaEventDisableTiming));
@@ -735,7 +958,7 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
     // Allocate and zero the padded table workspaces once (padding rows stay 0).
     for (auto& ck : m->chunk) {
       int64_t toff[kMaxOrder], tot = 0;
-      eval_table_offsets(m.get(), round_up(m->chunk_points, TP), toff, &tot);
+      eval_table_offsets(m.get(), round_up(m->chunk_points, 128), toff, &tot);
       ck.tables.alloc(static_cast<size_t>(tot));
       FSTK_CUDA(cudaMemset(ck.tables.p, 0, static_cast<size_t>(tot) * 8));
       ck.err.alloc(1);
@@ -815,7 +1038,7 @@ int32_t fstk_gpu_evaluate_batch(const fstk_gpu_model* m, const double* points, i
     std::lock_guard<std::mutex> lk(m->mu);
     DeviceGuard dg(m->device);
     const int64_t CH = m->chunk_points;
-    const int64_t ldt = round_up(CH, TP);
+    const int64_t ldt = round_up(CH, 128);
     int64_t toff[kMaxOrder], tot = 0;
     eval_table_offsets(m, ldt, toff, &tot);
     const int64_t nchunks = ceil_div(q, CH);
@@ -831,7 +1054,7 @@ int32_t fstk_gpu_evaluate_batch(const fstk_gpu_model* m, const double* points, i
       for (int k = 0; k < d; ++k)
         FSTK_CUDA(cudaMemcpyAsync(ck.points.p + k * CH, points + k * q + b, nb * sizeof(double),
                                   cudaMemcpyHostToDevice, ck.stream));
-      launch_mode_tables(m, ck.points.p, CH, nb, round_up(nb, TP), nullptr, ck.tables.p, toff,
+      launch_mode_tables(m, ck.points.p, CH, nb, round_up(nb, 128), nullptr, ck.tables.p, toff,
                          ldt, false, m->chunk_err.p + c, ck.stream);
       launch_contract(m, ck.tables.p, toff, ldt, nb, ck.out.p, ck.stream, nullptr, nullptr);
       FSTK_CUDA(cudaMemcpyAsync(out + b, ck.out.p, nb * sizeof(double), cudaMemcpyDeviceToHost,

@@ -24,6 +24,10 @@ struct ModeDev {
   const int* rowptr;           // r+1 CSR offsets into idx/coef
   const uint32_t* idx;         // ascending basis indices per function
   const double* coef;
+  const double* dense;         // (pmax+1) x ldc dense coefficients (0 where absent)
+  int ldc;                     // nchunk * jc
+  int jc;                      // functions per dense-kernel thread (multiple of 8, <= 64)
+  int nchunk;
 };
 struct ModesDev {
   int d;
@@ -33,6 +37,7 @@ struct ModesDev {
 // Host copy of one mode.
 struct ModeHost {
   int r = 0, pmax = 0;
+  bool sorted = true;  // every function's indices strictly increasing (format.md:67)
   double lo = 0, hi = 0;
   std::vector<int> rowptr;
   std::vector<uint32_t> idx;
@@ -49,6 +54,8 @@ struct ContractLayout {
   int Mout = 0;        // prod_{k>=2} r_k
   int nsw = 0;         // 8-column subtiles per warp = N1p / 16
   int nstage = 0;      // B pipeline depth
+  int tp = 128;        // points per CTA tile (64 or 128)
+  int ctas_per_sm = 1; // resident CTAs per SM at this shared-memory footprint
   size_t smem = 0;     // dynamic shared memory bytes
   int64_t btile_elems = 0;  // Kp * N1p
 };
@@ -79,6 +86,8 @@ struct fstk_gpu_model {
   fstk_gpu::DevBuf<int> d_rowptr;
   fstk_gpu::DevBuf<uint32_t> d_idx;
   fstk_gpu::DevBuf<double> d_coef;
+  fstk_gpu::DevBuf<double> d_dense;  // all modes' dense coefficient blocks
+  bool dense_ok = true;              // dense kernel is bit-equivalent (sorted indices)
   fstk_gpu::ModesDev modes_dev{};
 
   fstk_gpu::ContractLayout lay;
