@@ -385,14 +385,22 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
         del gram
         return t_hot, t_all, t_ar, info
 
+    from paper_1907_05884_b200 import _lib
+
+    _lib.profile_read()
+    _lib.profile_enable(True)
     t_hot, t_all, t_ar, info = one()
+    _lib.profile_enable(False)
+    kprof = _lib.profile_read()
     t_hot = maxreduce(t_hot, world, dev)
     tm = info["timings"]
     gram_flops = S / world * R * (R + 1)
     return {"seconds": t_all, "hot_path_seconds": t_hot,
             "scaling": "strong", "sample_rows": S, "working_rows": info["working_rows"],
             "padded_rows": info["padded_rows"], "transform": args.transform,
-            "stages_s": {"prepare": tm["prepare_s"], "sketch": tm["sketch_s"],
+            "kernel_ms": {k: v[0] for k, v in kprof.items() if v[1]},
+            "kernel_launches": {k: v[1] for k, v in kprof.items() if v[1]},
+            "stages_s": {"prepare": tm["prepare_s"], "alloc": tm["alloc_s"], "sketch": tm["sketch_s"],
                          "gram": tm["gram_s"], "allreduce": t_ar, "solve": tm["solve_s"],
                          "residual": tm["residual_s"]},
             "gram_roofline": {"bound": "tensor", "achieved": gram_flops / tm["gram_s"] / 1e12

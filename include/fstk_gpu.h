@@ -95,6 +95,7 @@ typedef struct fstk_reestimate_info {
   double t_gram;      /* A^T A and A^T b */
   double t_solve;     /* Cholesky (cuSOLVER), timed outside the hot-path claim */
   double t_residual;  /* validation residuals */
+  double t_alloc;     /* host wall time of the sketch (A) allocation */
 } fstk_reestimate_info;
 
 typedef struct fstk_gpu_model fstk_gpu_model;

@@ -66,7 +66,8 @@ class ReestimateInfo(C.Structure):
                 ("sample_rows", C.c_uint64), ("working_rows", C.c_uint64),
                 ("padded_rows", C.c_uint64), ("rank_deficient", C.c_int32),
                 ("held_out", C.c_int32), ("t_prepare", C.c_double), ("t_sketch", C.c_double),
-                ("t_gram", C.c_double), ("t_solve", C.c_double), ("t_residual", C.c_double)]
+                ("t_gram", C.c_double), ("t_solve", C.c_double), ("t_residual", C.c_double),
+                ("t_alloc", C.c_double)]
 
 
 # Every symbol include/fstk_gpu.h declares (checked by tests/test_abi.py).

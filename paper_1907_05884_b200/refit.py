@@ -43,7 +43,7 @@ def _info_dict(info: ReestimateInfo) -> dict:
             "padded_rows": int(info.padded_rows),
             "timings": {"prepare_s": info.t_prepare, "sketch_s": info.t_sketch,
                         "gram_s": info.t_gram, "solve_s": info.t_solve,
-                        "residual_s": info.t_residual}}
+                        "residual_s": info.t_residual, "alloc_s": info.t_alloc}}
 
 
 def reestimate_core(model: Model, points, values, seed=0, sample_rows=0,
