@@ -688,7 +688,8 @@ static void plan_layout(fstk_gpu_model* m) {
       const int ctas = std::min<int>(per_sm / static_cast<int>(S.total + 1024), 4);
       if (ctas < 1) continue;
       const int warps = ctas * (tp / 32 * 2);
-      const double score = std::min(warps, 16) * 100.0 + std::min(ns, 4) * 10.0 + tp / 64.0;
+      const double score =
+          std::min(warps, 16) * 100.0 + std::min(ctas, 3) * 50.0 + std::min(ns, 4) * 10.0 + tp / 64.0;
       if (score > best) {
         best = score;
         L.tp = tp;
@@ -757,9 +758,13 @@ static void upload_core(fstk_gpu_model* m) {
 
 // Evaluates n device-resident points in chunks of the model's workspace,
 // optionally with a replacement core (host pointer, e.g. a refit result).
+// Chunks alternate between the two workspace streams so the mode-table
+// kernel of chunk i+1 runs concurrently with the DMMA contraction of chunk i
+// (both are fp64-pipe bound with complementary stalls).  Chunk c records its
+// lowest failing row in m->chunk_err[c]; the caller's stream `s` is joined
+// at the end.
 void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, const double* pts,
                           int64_t ldp, int64_t n, double* out, cudaStream_t s) {
-  Chunk& ck = m->chunk[0];
   const int64_t CH = m->chunk_points;
   int64_t toff[kMaxOrder], tot = 0;
   const int64_t ldt = round_up(CH, 128);
@@ -770,16 +775,40 @@ void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, cons
     craw.alloc(m->R);
     FSTK_CUDA(cudaMemcpy(craw.p, core_host, m->R * 8, cudaMemcpyHostToDevice));
   }
-  FSTK_CUDA(cudaMemsetAsync(ck.err.p, 0xff, sizeof(unsigned long long), s));
-  for (int64_t b = 0; b < n; b += CH) {
+  const int64_t nchunks = std::max<int64_t>(1, ceil_div(n, CH));
+  m->chunk_err.ensure(static_cast<size_t>(nchunks));
+  FSTK_CUDA(cudaMemsetAsync(m->chunk_err.p, 0xff, nchunks * sizeof(unsigned long long), s));
+  FSTK_CUDA(cudaEventRecord(m->fork_ev, s));
+  for (auto& ck : m->chunk) FSTK_CUDA(cudaStreamWaitEvent(ck.stream, m->fork_ev, 0));
+  for (int64_t c = 0; c * CH < n; ++c) {
+    Chunk& ck = m->chunk[c & 1];
+    const int64_t b = c * CH;
     const int64_t nb = std::min(CH, n - b);
     const int64_t nout = round_up(nb, 128);
     launch_mode_tables(m, pts + b, ldp, nb, nout, nullptr, ck.tables.p, toff, ldt, false,
-                       ck.err.p, s);
-    launch_contract(m, ck.tables.p, toff, ldt, nb, out + b, s, core_host ? bp.p : nullptr,
-                    core_host ? craw.p : nullptr);
+                       m->chunk_err.p + c, ck.stream);
+    launch_contract(m, ck.tables.p, toff, ldt, nb, out + b, ck.stream,
+                    core_host ? bp.p : nullptr, core_host ? craw.p : nullptr);
+  }
+  for (auto& ck : m->chunk) {
+    FSTK_CUDA(cudaEventRecord(ck.done, ck.stream));
+    FSTK_CUDA(cudaStreamWaitEvent(s, ck.done, 0));
   }
   if (core_host) FSTK_CUDA(cudaStreamSynchronize(s));  // temporaries go out of scope
+}
+
+// Lowest failing row over the chunks of the last evaluate_device call (or -1);
+// synchronises `s`.
+int64_t evaluate_device_error(const fstk_gpu_model* m, int64_t n, cudaStream_t s) {
+  const int64_t CH = m->chunk_points;
+  const int64_t nchunks = std::max<int64_t>(1, ceil_div(n, CH));
+  std::vector<unsigned long long> bad(static_cast<size_t>(nchunks));
+  FSTK_CUDA(cudaMemcpyAsync(bad.data(), m->chunk_err.p, nchunks * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+  FSTK_CUDA(cudaStreamSynchronize(s));
+  for (int64_t c = 0; c < nchunks; ++c)
+    if (bad[c] != ULLONG_MAX) return c * CH + static_cast<int64_t>(bad[c]);
+  return -1;
 }
 
 void evaluate_device(const fstk_gpu_model* m, const double* pts, int64_t ldp, int64_t n,
@@ -796,6 +825,7 @@ fstk_gpu_model::~fstk_gpu_model() {
     if (c.stream) cudaStreamDestroy(c.stream);
     if (c.done) cudaEventDestroy(c.done);
   }
+  if (fork_ev) cudaEventDestroy(fork_ev);
 }
 
 // ================================================================= C-ABI ===
@@ -951,6 +981,7 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
                                         std::max<int64_t>(int64_t(1) << 16,
                                                           (int64_t(1) << 31) / (per_pt * 8)));
     m->chunk_points = round_up(m->chunk_points, 128);
+    FSTK_CUDA(cudaEventCreateWithFlags(&m->fork_ev, cudaEventDisableTiming));
     for (auto& ck : m->chunk) {
       FSTK_CUDA(cudaStreamCreateWithFlags(&ck.stream, cudaStreamNonBlocking));
       FSTK_CUDA(cudaEventCreateWithFlags(&ck.done, cudaEventDisableTiming));
@@ -1010,14 +1041,11 @@ int32_t fstk_gpu_evaluate_batch_device(const fstk_gpu_model* m, const double* po
     DeviceGuard dg(m->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     evaluate_device(m, points, ld, q, out, s);
-    unsigned long long bad = 0;
-    FSTK_CUDA(cudaMemcpyAsync(&bad, m->chunk[0].err.p, sizeof(bad), cudaMemcpyDeviceToHost, s));
-    FSTK_CUDA(cudaStreamSynchronize(s));
-    if (bad != ULLONG_MAX) {
+    const int64_t bad = evaluate_device_error(m, q, s);
+    if (bad >= 0) {
       std::vector<double> y(d);
       for (int k = 0; k < d; ++k)
-        FSTK_CUDA(cudaMemcpy(&y[k], points + k * ld + static_cast<int64_t>(bad), 8,
-                             cudaMemcpyDeviceToHost));
+        FSTK_CUDA(cudaMemcpy(&y[k], points + k * ld + bad, 8, cudaMemcpyDeviceToHost));
       throw_domain(m, static_cast<int64_t>(bad), y.data());
     }
   });

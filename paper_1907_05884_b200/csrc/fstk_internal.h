@@ -99,7 +99,8 @@ struct fstk_gpu_model {
   // Evaluation workspace (guarded by mu).
   mutable std::mutex mu;
   mutable fstk_gpu::Chunk chunk[2];
-  mutable fstk_gpu::DevBuf<unsigned long long> chunk_err;  // one slot per host-API chunk
+  mutable fstk_gpu::DevBuf<unsigned long long> chunk_err;  // one slot per chunk
+  cudaEvent_t fork_ev = nullptr;
   int64_t chunk_points = 0;
 
   ~fstk_gpu_model();
@@ -136,6 +137,7 @@ void evaluate_device(const fstk_gpu_model* m, const double* pts, int64_t ldp, in
                      double* out, cudaStream_t s);
 void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, const double* pts,
                           int64_t ldp, int64_t n, double* out, cudaStream_t s);
+int64_t evaluate_device_error(const fstk_gpu_model* m, int64_t n, cudaStream_t s);
 
 // Throws the reference's Domain error for point `row` (coordinates given on
 // the host), mirroring basis.cpp:218-219.

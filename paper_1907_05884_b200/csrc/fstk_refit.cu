@@ -754,6 +754,7 @@ struct fstk_gpu_refit {
   DevBuf<double> val_points, val_values;
   int64_t n_val = 0;
   std::vector<double> h_val_values;
+  std::vector<int64_t> h_val_index;   // dataset rows of the validation points
   // Solve state: Cholesky factor of the (summed) Gram, or the eigen fallback.
   DevBuf<double> L;       // R x R, lower Cholesky factor
   bool factored = false;
@@ -878,6 +879,7 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     rf->n_val = static_cast<int64_t>(val.size());
     {
       std::vector<int64_t> vi(val.begin(), val.end());
+      rf->h_val_index = vi;
       DevBuf<int64_t> dvi(std::max<size_t>(vi.size(), 1));
       FSTK_CUDA(cudaMemcpyAsync(dvi.p, vi.data(), vi.size() * 8, cudaMemcpyHostToDevice, s));
       rf->val_points.alloc(static_cast<size_t>(std::max<int64_t>(rf->n_val, 1)) * d);
@@ -1071,6 +1073,18 @@ static void minnorm_solve(fstk_gpu_refit* rf, const double* gram_in, const doubl
   FSTK_CUDA(cudaStreamSynchronize(s));
 }
 
+// Re-raises a failed nested C-ABI stage with its full error record.
+static void rethrow_stage(int32_t c, const fstk_gpu_error* err) {
+  if (!c) return;
+  Error e{c, err ? err->message : "refit stage failed"};
+  if (err) {
+    e.index = err->index;
+    e.mode = err->mode;
+    e.value = err->value;
+  }
+  throw e;
+}
+
 static double dev_norm(cublasHandle_t h, int n, const double* x) {
   double r = 0.0;
   if (cublasDnrm2(h, n, x, 1, &r) != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, "cublasDnrm2 failed");
@@ -1201,6 +1215,15 @@ int32_t fstk_gpu_refit_finish(fstk_gpu_refit* rf, const double* x_dev, double* c
       DevBuf<double> dp(rf->n_val);
       std::lock_guard<std::mutex> lk(rf->model->mu);
       evaluate_device_core(rf->model, nullptr, rf->val_points.p, rf->n_val, rf->n_val, dp.p, s);
+      const int64_t bad = evaluate_device_error(rf->model, rf->n_val, s);
+      if (bad >= 0) {
+        // relative_residual -> evaluate_batch throws Domain (basis.cpp:218-219).
+        const int64_t row = rf->h_val_index[bad];
+        std::vector<double> y(rf->d);
+        for (int k = 0; k < rf->d; ++k)
+          FSTK_CUDA(cudaMemcpy(&y[k], rf->d_points.p + k * rf->q + row, 8, cudaMemcpyDeviceToHost));
+        throw_domain(rf->model, row, y.data());
+      }
       FSTK_CUDA(cudaMemcpyAsync(pred.data(), dp.p, rf->n_val * 8, cudaMemcpyDeviceToHost, s));
       FSTK_CUDA(cudaStreamSynchronize(s));
       evaluate_device_core(rf->model, core_out, rf->val_points.p, rf->n_val, rf->n_val, dp.p, s);
@@ -1226,9 +1249,7 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     DeviceGuard dg(rf->device);
     const int n = static_cast<int>(rf->R);
     DevBuf<double> x(n), sv(n);
-    auto rc = [&](int32_t c) {
-      if (c) throw Error{c, err ? err->message : "refit stage failed"};
-    };
+    auto rc = [&](int32_t c) { rethrow_stage(c, err); };
     rc(fstk_gpu_refit_factor(rf, gram_in, rhs_in, x.p, info, err));
     if (rf->factored) {
       EventTimer tref(rf->stream);
@@ -1319,10 +1340,8 @@ int32_t fstk_gpu_reestimate_core(const fstk_gpu_model* m, const double* points,
   rc = guarded(err, [&] {
     DeviceGuard dg(m->device);
     DevBuf<double> gram(static_cast<size_t>(m->R) * m->R), rhs(m->R);
-    int32_t r2 = fstk_gpu_refit_normal_equations(rf, gram.p, rhs.p, inf, err);
-    if (r2) throw Error{r2, err ? err->message : "normal equations failed"};
-    r2 = fstk_gpu_refit_solve(rf, gram.p, rhs.p, core_out, inf, err);
-    if (r2) throw Error{r2, err ? err->message : "solve failed"};
+    rethrow_stage(fstk_gpu_refit_normal_equations(rf, gram.p, rhs.p, inf, err), err);
+    rethrow_stage(fstk_gpu_refit_solve(rf, gram.p, rhs.p, core_out, inf, err), err);
   });
   fstk_gpu_refit_end(rf);
   return rc;

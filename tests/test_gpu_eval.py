@@ -155,3 +155,17 @@ def test_native_library_is_what_ran():
     m = synth.random_model((8, 8, 8), (6, 6, 6), 3, seed=1)
     m.evaluate_batch(synth.uniform_points(1000, 3, 1))
     assert F.launch_count() >= before + 2
+
+
+def test_domain_error_index_in_later_device_chunk():
+    """The device API reports the global (not chunk-relative) lowest bad row."""
+    import torch
+
+    m = synth.random_model((4, 4, 4), (6, 6, 6), 3, seed=1)
+    n = (1 << 21) * 2 + 1000
+    pts = synth.uniform_points(n, 3, seed=2)
+    pts[(1 << 21) + 777, 1] = 3.0
+    dp = torch.from_numpy(np.ascontiguousarray(pts.T)).cuda()
+    with pytest.raises(ValueError) as e:
+        m.evaluate_device(dp)
+    assert e.value.kind == "Domain" and e.value.index == (1 << 21) + 777 and e.value.mode == 1

@@ -186,3 +186,20 @@ def test_sharded_rows_sum_to_full_system(O):
     core = full.solve(g, r)
     core_o, _ = O.reestimate_core(m, pts, vals, seed=4)
     assert rel(core, core_o) <= CORE_TOL
+
+
+def test_validation_point_out_of_domain_is_domain_error(O):
+    """A held-out point outside the domain fails the refit with Domain, as the
+    reference's relative_residual -> evaluate_batch does (randls.cpp:350-356)."""
+    m = synth.random_model((3, 3, 2), (5, 5, 5), 3, seed=3)
+    pts, vals = _data(O, m, 20_000, 4)
+    sess = F.RefitSession(m, pts, vals, seed=17)
+    rows_val = None
+    sess.close()
+    # locate a validation row via the oracle's split and push it out of the domain
+    _, _, _, val_index, _ = O.refit_system(m, pts, vals, seed=17)
+    bad = pts.copy()
+    bad[int(val_index[5]), 0] = 7.0
+    with pytest.raises(ValueError) as e:
+        F.reestimate_core(m, bad, vals, seed=17)
+    assert e.value.kind == "Domain" and e.value.index == int(val_index[5])
