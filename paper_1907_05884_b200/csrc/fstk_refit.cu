@@ -29,6 +29,7 @@
 #include <climits>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -253,26 +254,39 @@ __device__ __forceinline__ void radix_round(typename std::conditional<REAL, doub
                                             const double2* tws, int nel, int j) {
   using T = typename std::conditional<REAL, double, double2>::type;
   constexpr int NV = 1 << NS;
+  const int jstep = (1 << j) * G;         // element step between the NV values
+  const int jmask = (1 << j) - 1;
   for (int blk = threadIdx.x; blk < (nel >> NS); blk += blockDim.x) {
     const int c = blk % G, q = blk / G;
-    const int tb = ((q >> j) << (j + NS)) | (q & ((1 << j) - 1));
+    const int tb = ((q >> j) << (j + NS)) | (q & jmask);
+    const int e0 = tb * G + c;
     T v[NV];
 #pragma unroll
-    for (int m = 0; m < NV; ++m) v[m] = x[spad((tb + (m << j)) * G + c)];
+    for (int m = 0; m < NV; ++m) v[m] = x[spad(e0 + m * jstep)];
+    if constexpr (REAL) {
 #pragma unroll
-    for (int jj = 0; jj < NS; ++jj) {
-      const int half = 1 << jj;
-      const int jl = j + jj;
+      for (int jj = 0; jj < NS; ++jj) {
+        const int half = 1 << jj;
 #pragma unroll
-      for (int a = 0; a < NV; ++a) {
-        if (a & half) continue;
-        if constexpr (REAL) {
+        for (int a = 0; a < NV; ++a) {
+          if (a & half) continue;
           const double u = v[a], w2 = v[a + half];
           v[a] = xadd(u, w2);
           v[a + half] = xsub(u, w2);
-        } else {
-          const int tl = tb + (a << j);
-          const double2 w = tws[((1 << jl) - 1) * G + (tl & ((1 << jl) - 1)) * G + c];
+        }
+      }
+    } else {
+      // Twiddle of stage jl = j + jj for lower element a: index
+      // (2^jl - 1) G + ((tb & jmask) + (a mod 2^jj) 2^j) G + c.
+      const int tw0 = (tb & jmask) * G + c;
+#pragma unroll
+      for (int jj = 0; jj < NS; ++jj) {
+        const int half = 1 << jj;
+        const double2* twj = tws + ((1 << (j + jj)) - 1) * G + tw0;
+#pragma unroll
+        for (int a = 0; a < NV; ++a) {
+          if (a & half) continue;
+          const double2 w = twj[(a & (half - 1)) * jstep];
           const double2 u = v[a];
           const double2 t2 = cmul_x(v[a + half], w);
           v[a] = make_double2(xadd(u.x, t2.x), xadd(u.y, t2.y));
@@ -281,7 +295,7 @@ __device__ __forceinline__ void radix_round(typename std::conditional<REAL, doub
       }
     }
 #pragma unroll
-    for (int m = 0; m < NV; ++m) x[spad((tb + (m << j)) * G + c)] = v[m];
+    for (int m = 0; m < NV; ++m) x[spad(e0 + m * jstep)] = v[m];
   }
 }
 
@@ -336,21 +350,18 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
       }
       for (int e = threadIdx.x; e < nel; e += blockDim.x) {
         const int64_t p = base + (e % G) + static_cast<int64_t>(e / G) * stride;
-        const int64_t src = P.row_src[p];
         double v = 0.0;
-        if (src >= 0) {
-          if (!design) {
-            v = P.rhs[src];
-          } else if (P.src == SRC_DENSE) {
-            v = P.dense[src + P.ldd * col];
-          } else {
-            // design_column (randls.cpp:44-52): ((u0 * u1) * u2) * ...
-            v = tc[0][p];
+        if (design && P.src == SRC_TABLES) {
+          // design_column (randls.cpp:44-52): ((u0 * u1) * u2) * ..., with the
+          // sign already folded into u0 and zero rows at padded positions:
+          // three independent loads, no gather.
+          v = tc[0][p];
 #pragma unroll
-            for (int k = 1; k < kMaxOrder; ++k)
-              if (k < P.d) v = xmul(v, tc[k][p]);
-          }
-          v = xmul(P.sgn[p], v);
+          for (int k = 1; k < kMaxOrder; ++k)
+            if (k < P.d) v = xmul(v, tc[k][p]);
+        } else {
+          const int64_t src = P.row_src[p];
+          if (src >= 0) v = xmul(P.sgn[p], design ? P.dense[src + P.ldd * col] : P.rhs[src]);
         }
         if constexpr (REAL)
           x[spad(e)] = v;
@@ -397,6 +408,17 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
       }
     }
   }
+}
+
+// u0[p] *= s_p for every function (sign folded into the mode-0 table: since
+// s = +-1 and IEEE products are sign-symmetric, ((s u0) u1) u2 == s ((u0 u1) u2)
+// bit for bit, which is what sketch_column feeds the transform).
+__global__ void fold_sign_kernel(double* __restrict__ t0, int64_t ldt, int r0,
+                                 const double* __restrict__ sgn, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double s = sgn[i];
+  for (int j = 0; j < r0; ++j) t0[j * ldt + i] = xmul(s, t0[j * ldt + i]);
 }
 
 __global__ void finite_check_kernel(const double* __restrict__ a, int64_t n, int* flag) {
@@ -459,9 +481,13 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
   const int64_t ncols = J.R + (J.with_rhs ? 1 : 0);
   const size_t elem = real ? 8 : 16;
   const int npass = LOG == 0 ? 1 : (LOG + 9) / 10;
-  // Column batch: intermediate of ~512 MB (streams through HBM between passes).
+  // Column batch: the inter-pass intermediate is sized to stay L2-resident
+  // (pass 1 reads it in 32-byte segments at a 16 KB stride, which is
+  // latency-bound from DRAM but cheap from L2).  FSTK_SKETCH_BATCH_MB overrides.
+  int64_t batch_mb = 2048;
+  if (const char* e = std::getenv("FSTK_SKETCH_BATCH_MB")) batch_mb = std::max(1, std::atoi(e));
   int64_t nb = ncols;
-  if (npass > 1) nb = std::max<int64_t>(1, std::min<int64_t>(ncols, (int64_t(512) << 20) /
+  if (npass > 1) nb = std::max<int64_t>(1, std::min<int64_t>(ncols, (batch_mb << 20) /
                                                                         static_cast<int64_t>(J.n * elem)));
   DevBuf<double2> cbuf;
   DevBuf<double> rbuf;
@@ -530,8 +556,12 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
                           (real ? 0 : static_cast<size_t>((E - 1) * P.G) * 16);
       // ~4 columns per CTA: many short CTAs (small tail wave), twiddles still
       // amortised over several columns.
+      static const int64_t cpc = [] {
+        const char* e = std::getenv("FSTK_SKETCH_COLS_PER_CTA");
+        return e ? std::max(1, std::atoi(e)) : 8;
+      }();
       const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(bc, std::max<int64_t>(
-                                                                    ceil_div(bc, 4), ceil_div(int64_t(sms) * 8, sets))));
+                                                                    ceil_div(bc, cpc), ceil_div(int64_t(sms) * 8, sets))));
       dim3 grid(static_cast<unsigned>(sets), static_cast<unsigned>(gy));
       ProfScope prof(FSTK_PROF_TRANSFORM, s);
       if (real && P.G == 1)
@@ -914,6 +944,9 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     launch_mode_tables(m, rf->d_points.p, q, static_cast<int64_t>(rf->q_pad),
                        static_cast<int64_t>(rf->q_pad), rf->in.row_src.p, tables.p, toff, ldt,
                        true, derr.p, s);
+    fold_sign_kernel<<<static_cast<unsigned>(ceil_div(ldt, 256)), 256, 0, s>>>(
+        tables.p + toff[0], ldt, static_cast<int>(m->ranks[0]), rf->in.sgn.p, ldt);
+    check_launch("fold_sign_kernel");
     unsigned long long bad = 0;
     FSTK_CUDA(cudaMemcpyAsync(&bad, derr.p, 8, cudaMemcpyDeviceToHost, s));
     FSTK_CUDA(cudaStreamSynchronize(s));
