@@ -31,6 +31,7 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <random>
@@ -293,16 +294,208 @@ static double to_reference(const BasisSpec& spec, double x) {  // :215-222
   return -1.0 + 2.0 * (clamped - spec.lo) / span;
 }
 
-static void eval_basis(const BasisSpec& spec, double x, double* out) {  // :226-234
+// basis.cpp:63-102 (Tricomi initial guess + Newton on P_n).
+static void gauss_legendre(int n, std::vector<double>& nodes, std::vector<double>& weights) {
+  require(n >= 1, Parameter, "quadrature order must be positive");
+  nodes.assign(n, 0.0);
+  weights.assign(n, 0.0);
+  const int m = (n + 1) / 2;
+  for (int j = 0; j < m; ++j) {
+    double x = std::cos(M_PI * (j + 0.75) / (n + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int k = 1; k < n; ++k) {
+        const double p2 = ((2 * k + 1) * x * p1 - k * p0) / (k + 1);
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1.0);
+      const double dx = p1 / dp;
+      x -= dx;
+      if (std::abs(dx) < 1e-15) break;
+    }
+    {
+      double p0 = 1.0, p1 = x;
+      for (int k = 1; k < n; ++k) {
+        const double p2 = ((2 * k + 1) * x * p1 - k * p0) / (k + 1);
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1.0);
+    }
+    nodes[j] = -x;
+    nodes[n - 1 - j] = x;
+    const double w = 2.0 / ((1.0 - x * x) * dp * dp);
+    weights[j] = w;
+    weights[n - 1 - j] = w;
+  }
+  if (n % 2 == 1) nodes[n / 2] = 0.0;
+}
+
+// Dense column-major helper and a Householder QR returning the full m x m Q
+// (stands in for Eigen::HouseholderQR::householderQ(), basis.cpp:147-148,173-174).
+struct Mat {
+  int r = 0, c = 0;
+  std::vector<double> a;
+  Mat(int rr, int cc) : r(rr), c(cc), a(static_cast<size_t>(rr) * cc, 0.0) {}
+  double& operator()(int i, int j) { return a[static_cast<size_t>(j) * r + i]; }
+  double operator()(int i, int j) const { return a[static_cast<size_t>(j) * r + i]; }
+};
+
+static Mat householder_q(Mat A) {
+  const int m = A.r, n = A.c;
+  std::vector<std::vector<double>> vs;
+  std::vector<double> taus;
+  for (int k = 0; k < std::min(m - 1, n); ++k) {
+    double norm = 0.0;
+    for (int i = k; i < m; ++i) norm += A(i, k) * A(i, k);
+    norm = std::sqrt(norm);
+    std::vector<double> v(m, 0.0);
+    double tau = 0.0;
+    if (norm > 0.0) {
+      const double alpha = A(k, k) >= 0 ? -norm : norm;
+      for (int i = k; i < m; ++i) v[i] = A(i, k);
+      v[k] -= alpha;
+      double vn = 0.0;
+      for (int i = k; i < m; ++i) vn += v[i] * v[i];
+      if (vn > 0.0) {
+        tau = 2.0 / vn;
+        for (int j = k; j < n; ++j) {
+          double d = 0.0;
+          for (int i = k; i < m; ++i) d += v[i] * A(i, j);
+          d *= tau;
+          for (int i = k; i < m; ++i) A(i, j) -= d * v[i];
+        }
+      }
+    }
+    vs.push_back(v);
+    taus.push_back(tau);
+  }
+  Mat Q(m, m);
+  for (int i = 0; i < m; ++i) Q(i, i) = 1.0;
+  for (int k = static_cast<int>(vs.size()) - 1; k >= 0; --k) {
+    const auto& v = vs[k];
+    if (taus[k] == 0.0) continue;
+    for (int j = 0; j < m; ++j) {
+      double d = 0.0;
+      for (int i = k; i < m; ++i) d += v[i] * Q(i, j);
+      d *= taus[k];
+      for (int i = k; i < m; ++i) Q(i, j) -= d * v[i];
+    }
+  }
+  return Q;
+}
+
+// basis.cpp:116-189: mother multiwavelets of degree p in the split basis.
+static Mat build_mother(int p) {
+  const int n = p + 1;
+  std::vector<double> qx, qw;
+  gauss_legendre(2 * p + 4, qx, qw);
+  const int nq = static_cast<int>(qx.size());
+  Mat q(2 * n, n);
+  std::vector<double> lg(n), lh(n);
+  for (int side = 0; side < 2; ++side)
+    for (int a = 0; a < nq; ++a) {
+      const double t = qx[a];
+      const double x = side == 0 ? 0.5 * (t - 1.0) : 0.5 * (t + 1.0);
+      legendre_values(p, x, lg.data());
+      legendre_values(p, t, lh.data());
+      const double w = qw[a] * std::sqrt(2.0) / 4.0;
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) q(side * n + i, j) += w * lh[i] * lg[j];
+    }
+  const Mat full = householder_q(q);
+  Mat comp(2 * n, n);
+  for (int i = 0; i < 2 * n; ++i)
+    for (int j = 0; j < n; ++j) comp(i, j) = full(i, n + j);
+  Mat moments(n, n);
+  for (int side = 0; side < 2; ++side)
+    for (int a = 0; a < nq; ++a) {
+      const double t = qx[a];
+      const double x = side == 0 ? 0.5 * (t - 1.0) : 0.5 * (t + 1.0);
+      legendre_values(p, t, lh.data());
+      const double w = qw[a] * std::sqrt(2.0) / 4.0;
+      double xpow = std::pow(x, p + 1);
+      for (int trow = 0; trow < n; ++trow) {
+        for (int i = 0; i < n; ++i) {
+          const double chi_val = w * lh[i];
+          for (int c = 0; c < n; ++c) moments(trow, c) += xpow * chi_val * comp(side * n + i, c);
+        }
+        xpow *= x;
+      }
+    }
+  Mat mt(n, n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) mt(i, j) = moments(j, i);
+  const Mat rot = householder_q(mt);
+  Mat coords(2 * n, n);
+  for (int i = 0; i < 2 * n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double v = 0.0;
+      for (int k = 0; k < n; ++k) v += comp(i, k) * rot(k, j);
+      coords(i, j) = v;
+    }
+  for (int m = 0; m < n; ++m)
+    for (int i = 2 * n - 1; i >= 0; --i)
+      if (std::abs(coords(i, m)) > 1e-10) {
+        if (coords(i, m) < 0.0)
+          for (int r = 0; r < 2 * n; ++r) coords(r, m) = -coords(r, m);
+        break;
+      }
+  return coords;
+}
+
+static const Mat& mother_wavelet(int p) {  // basis.cpp:191-198
+  static std::mutex mu;
+  static std::map<int, Mat> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(p);
+  if (it == cache.end()) it = cache.emplace(p, build_mother(p)).first;
+  return it->second;
+}
+
+static void mother_values(const Mat& mw, int p, double t, double* out) {  // :201-213
+  const int n = p + 1;
+  std::vector<double> leg(n);
+  const int side = t < 0.0 ? 0 : 1;
+  const double local = side == 0 ? 2.0 * t + 1.0 : 2.0 * t - 1.0;
+  legendre_values(p, local, leg.data());
+  const double s2 = std::sqrt(2.0);
+  for (int m = 0; m < n; ++m) {
+    double v = 0.0;
+    for (int i = 0; i < n; ++i) v += mw(side * n + i, m) * s2 * leg[i];
+    out[m] = v;
+  }
+}
+
+static void eval_basis(const BasisSpec& spec, double x, double* out) {  // :226-254
   validate(spec);
   const double t = to_reference(spec, x);
+  const int p = spec.degree;
+  const int n1 = p + 1;
   if (spec.family == 0) {
-    legendre_values(spec.degree, t, out);
+    legendre_values(p, t, out);
     return;
   }
-  // Multiwavelet branch (basis.cpp:235-253) is outside this oracle's scope
-  // (SURVEY §8f-1); BASELINE configs are Legendre-only.
-  fail(Parameter, "oracle: wavelet bases are not restated");
+  const int dim = spec.dimension();
+  std::fill(out, out + dim, 0.0);
+  legendre_values(p, t, out);
+  if (spec.resolution == 0) return;
+  const Mat& mw = mother_wavelet(p);
+  std::vector<double> psi(n1);
+  for (int level = 1; level <= spec.resolution; ++level) {
+    const std::int64_t n_int = std::int64_t(1) << (level - 1);
+    const double h = 2.0 / static_cast<double>(n_int);
+    std::int64_t i = static_cast<std::int64_t>(std::floor((t + 1.0) / h));
+    i = std::min<std::int64_t>(n_int - 1, std::max<std::int64_t>(0, i));
+    const double a = -1.0 + h * static_cast<double>(i);
+    const double local = 2.0 * (t - a) / h - 1.0;
+    mother_values(mw, p, local, psi.data());
+    const double scale = std::pow(2.0, 0.5 * (level - 1));
+    double* block = out + n1 * (std::int64_t(1) << (level - 1)) + i * n1;
+    for (int m = 0; m < n1; ++m) block[m] = scale * psi[m];
+  }
 }
 
 // ----------------------------------------------------------------- model ---
@@ -699,6 +892,20 @@ int oracle_wht(double* x, std::uint64_t n) {
 // --- basis ------------------------------------------------------------------
 int oracle_legendre_values(int p, double t, double* out) {
   return guarded([&] { legendre_values(p, t, out); });
+}
+int oracle_gauss_legendre(int n, double* nodes, double* weights) {
+  return guarded([&] {
+    std::vector<double> a, b;
+    gauss_legendre(n, a, b);
+    std::copy(a.begin(), a.end(), nodes);
+    std::copy(b.begin(), b.end(), weights);
+  });
+}
+int oracle_mother_coords(int p, double* out) {  // 2(p+1) x (p+1) column-major
+  return guarded([&] {
+    const Mat& m = mother_wavelet(p);
+    std::copy(m.a.begin(), m.a.end(), out);
+  });
 }
 int oracle_eval_basis(int family, int degree, int resolution, double lo,
                       double hi, double x, double* out) {

@@ -163,9 +163,21 @@ def legendre_values(p: int, t: float) -> np.ndarray:
 
 
 def eval_basis(degree, lo, hi, x, family=0, resolution=0):
-    out = np.zeros(degree + 1)
+    out = np.zeros((degree + 1) << (resolution if family == 1 else 0))
     _check(lib().oracle_eval_basis(C.c_int(family), C.c_int(degree), C.c_int(resolution),
                                    C.c_double(lo), C.c_double(hi), C.c_double(x), _dp(out)))
+    return out
+
+
+def gauss_legendre(n):
+    a, b = np.zeros(n), np.zeros(n)
+    _check(lib().oracle_gauss_legendre(C.c_int(n), _dp(a), _dp(b)))
+    return a, b
+
+
+def mother_coords(p):
+    out = np.zeros((2 * (p + 1), p + 1), order="F")
+    _check(lib().oracle_mother_coords(C.c_int(p), _dp(out)))
     return out
 
 

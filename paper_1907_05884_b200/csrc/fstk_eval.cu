@@ -502,63 +502,53 @@ static void launch_dense(const ModeDev& md, const double* xs, int64_t n, int64_t
   }
 }
 
+// One mode's table: wavelet-capable general kernel, dense Legendre kernel, or
+// the sparse Legendre kernel (indices not strictly increasing).
+static void launch_mode_k(const fstk_gpu_model* m, int k, const double* xs, int64_t n,
+                          int64_t n_out, const int64_t* row_src, double* tk, int64_t ldt,
+                          bool exact, unsigned long long* err_row, cudaStream_t s) {
+  if (m->modes[k].general) {
+    launch_mode_general(m->gen[k], xs, n, n_out, row_src, tk, ldt, exact, err_row, s, m->device);
+    return;
+  }
+  const ModeDev& md = m->modes_dev.m[k];
+  if (m->modes[k].sorted) {
+    if (exact)
+      launch_dense<true>(md, xs, n, n_out, row_src, tk, ldt, err_row, s, m->device);
+    else
+      launch_dense<false>(md, xs, n, n_out, row_src, tk, ldt, err_row, s, m->device);
+    return;
+  }
+  const int threads = 128;
+  Int64x8 to{};
+  to.v[k] = 0;
+  const size_t sm = mode_smem(m, k, k + 1, threads);
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n_out, threads));
+  // pts[k * ldp + src] with ldp = 0 addresses xs[src].
+  if (exact)
+    mode_tables_kernel<true><<<blocks, threads, sm, s>>>(m->modes_dev, k, k + 1, xs, 0, n, n_out,
+                                                         row_src, tk, to, ldt, err_row);
+  else
+    mode_tables_kernel<false><<<blocks, threads, sm, s>>>(m->modes_dev, k, k + 1, xs, 0, n, n_out,
+                                                          row_src, tk, to, ldt, err_row);
+  check_launch("mode_tables_kernel");
+}
+
 void launch_mode_tables(const fstk_gpu_model* m, const double* pts, int64_t ldp, int64_t n,
                         int64_t n_out, const int64_t* row_src, double* tables,
                         const int64_t* toff, int64_t ldt, bool exact,
                         unsigned long long* err_row, cudaStream_t s) {
   if (n_out <= 0) return;
   ProfScope prof(FSTK_PROF_MODE_TABLES, s);
-  if (m->dense_ok) {
-    for (int k = 0; k < m->d; ++k) {
-      const ModeDev& md = m->modes_dev.m[k];
-      if (exact)
-        launch_dense<true>(md, pts + k * ldp, n, n_out, row_src, tables + toff[k], ldt, err_row, s,
-                           m->device);
-      else
-        launch_dense<false>(md, pts + k * ldp, n, n_out, row_src, tables + toff[k], ldt, err_row, s,
-                            m->device);
-    }
-    return;
-  }
-  const int threads = 128;
-  Int64x8 to{};
-  for (int k = 0; k < m->d; ++k) to.v[k] = toff[k];
-  const size_t sm = mode_smem(m, 0, m->d, threads);
-  const unsigned blocks = static_cast<unsigned>(ceil_div(n_out, threads));
-  if (exact)
-    mode_tables_kernel<true><<<blocks, threads, sm, s>>>(m->modes_dev, 0, m->d, pts, ldp, n,
-                                                         n_out, row_src, tables, to, ldt, err_row);
-  else
-    mode_tables_kernel<false><<<blocks, threads, sm, s>>>(m->modes_dev, 0, m->d, pts, ldp, n,
-                                                          n_out, row_src, tables, to, ldt, err_row);
-  check_launch("mode_tables_kernel");
+  for (int k = 0; k < m->d; ++k)
+    launch_mode_k(m, k, pts + k * ldp, n, n_out, row_src, tables + toff[k], ldt, exact, err_row, s);
 }
 
 void launch_mode_table_one(const fstk_gpu_model* m, int mode, const double* x, int64_t n,
                            double* out, int64_t ldt, bool exact, unsigned long long* err_row,
                            cudaStream_t s) {
   if (n <= 0) return;
-  if (m->dense_ok) {
-    const ModeDev& md = m->modes_dev.m[mode];
-    if (exact)
-      launch_dense<true>(md, x, n, n, nullptr, out, ldt, err_row, s, m->device);
-    else
-      launch_dense<false>(md, x, n, n, nullptr, out, ldt, err_row, s, m->device);
-    return;
-  }
-  const int threads = 128;
-  Int64x8 to{};
-  to.v[mode] = 0;
-  const size_t sm = mode_smem(m, mode, mode + 1, threads);
-  const unsigned blocks = static_cast<unsigned>(ceil_div(n, threads));
-  const double* pts = x;  // ldp = 0 => pts[mode*0 + i]
-  if (exact)
-    mode_tables_kernel<true><<<blocks, threads, sm, s>>>(m->modes_dev, mode, mode + 1, pts, 0, n,
-                                                         n, nullptr, out, to, ldt, err_row);
-  else
-    mode_tables_kernel<false><<<blocks, threads, sm, s>>>(m->modes_dev, mode, mode + 1, pts, 0,
-                                                          n, n, nullptr, out, to, ldt, err_row);
-  check_launch("mode_tables_kernel(one)");
+  launch_mode_k(m, mode, x, n, n, nullptr, out, ldt, exact, err_row, s);
 }
 
 void eval_table_offsets(const fstk_gpu_model* m, int64_t ldt, int64_t* toff, int64_t* total) {
@@ -897,9 +887,20 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
           mh.coef.push_back(desc->coeffs[c]);
         }
         mh.rowptr.push_back(static_cast<int>(mh.idx.size()));
-        require(fam == 0, FSTK_E_PARAMETER,
-                "GPU path: multiwavelet bases are not supported yet (SURVEY 8f-1)");
         mh.pmax = std::max(mh.pmax, deg);
+        // distinct bases of the mode (mode_values evaluates each once, model.cpp:76-92)
+        int sid = -1;
+        for (size_t q2 = 0; q2 < mh.spec_family.size(); ++q2)
+          if (mh.spec_family[q2] == fam && mh.spec_p[q2] == deg && mh.spec_s[q2] == res)
+            sid = static_cast<int>(q2);
+        if (sid < 0) {
+          sid = static_cast<int>(mh.spec_family.size());
+          mh.spec_family.push_back(fam);
+          mh.spec_p.push_back(deg);
+          mh.spec_s.push_back(res);
+        }
+        mh.fn_spec.push_back(sid);
+        if (fam != 0) mh.general = true;
       }
     }
     DeviceGuard dg(device);
@@ -935,17 +936,18 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
     std::vector<int> jc(d), nch(d);
     for (int k = 0; k < d; ++k) {
       const ModeHost& mh = m->modes[k];
-      m->dense_ok = m->dense_ok && mh.sorted;
       jc[k] = static_cast<int>(std::min<int64_t>(round_up(mh.r, 8), 64));
       nch[k] = static_cast<int>(ceil_div(mh.r, jc[k]));
       const int ldc = jc[k] * nch[k];
       dense_off[k] = dense.size();
+      if (mh.general) continue;  // wavelet modes use mode_general_kernel
       dense.resize(dense.size() + static_cast<size_t>(mh.pmax + 1) * ldc, 0.0);
       double* blk = dense.data() + dense_off[k];
       for (int j = 0; j < mh.r; ++j)
         for (int s2 = mh.rowptr[j]; s2 < mh.rowptr[j + 1]; ++s2)
           blk[static_cast<size_t>(mh.idx[s2]) * ldc + j] = mh.coef[s2];
     }
+    if (dense.empty()) dense.push_back(0.0);
     m->d_dense.alloc(dense.size());
     FSTK_CUDA(cudaMemcpy(m->d_dense.p, dense.data(), dense.size() * 8, cudaMemcpyHostToDevice));
     m->modes_dev.d = d;
@@ -967,6 +969,52 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
       md.rowptr = m->d_rowptr.p + rp_off[k];
       md.idx = m->d_idx.p + ix_off[k];
       md.coef = m->d_coef.p + ix_off[k];
+    }
+    // Wavelet-capable modes.
+    {
+      std::vector<int> fs;
+      std::vector<size_t> fs_off(d);
+      for (int k = 0; k < d; ++k) {
+        fs_off[k] = fs.size();
+        fs.insert(fs.end(), m->modes[k].fn_spec.begin(), m->modes[k].fn_spec.end());
+      }
+      m->d_fn_spec.alloc(std::max<size_t>(fs.size(), 1));
+      FSTK_CUDA(cudaMemcpy(m->d_fn_spec.p, fs.data(), fs.size() * 4, cudaMemcpyHostToDevice));
+      bool any = false;
+      for (int k = 0; k < d; ++k) {
+        const ModeHost& mh = m->modes[k];
+        GenModeDev& G = m->gen[k];
+        G = GenModeDev{};
+        if (!mh.general) continue;
+        any = true;
+        const int nspec = static_cast<int>(mh.spec_family.size());
+        require(nspec <= kMaxSpec, FSTK_E_PARAMETER,
+                "GPU path: more than 8 distinct bases in one mode");
+        G.md = m->modes_dev.m[k];
+        G.nspec = nspec;
+        G.fn_spec = m->d_fn_spec.p + fs_off[k];
+        int voff = 0;
+        for (int q2 = 0; q2 < nspec; ++q2) {
+          SpecDev& sp = G.sp[q2];
+          sp.family = mh.spec_family[q2];
+          sp.p = mh.spec_p[q2];
+          sp.s = sp.family == 0 ? 0 : mh.spec_s[q2];
+          sp.voff = voff;
+          const int n1 = sp.p + 1;
+          voff += sp.family == 0 ? n1 : 2 * n1 + sp.s * (n1 + 1);
+          sp.coords = nullptr;
+          if (sp.family != 0) {
+            auto mc = mother_coords_device(device, sp.p);
+            m->mother_refs.push_back(mc);
+            sp.coords = mc->p;
+          }
+        }
+        G.vtot = voff;
+        require(static_cast<size_t>(voff) * 64 * sizeof(double) <= 200 * 1024, FSTK_E_PARAMETER,
+                "GPU path: wavelet basis too large for the per-point scratch "
+                "(needs sum over bases of (p+1)(2+s) <= 400)");
+      }
+      if (any) upload_wavelet_constants(device);
     }
     plan_layout(m.get());
     // Padded table rows beyond r_k are zero-filled by construction: the mode

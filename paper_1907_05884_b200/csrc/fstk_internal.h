@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -34,10 +35,30 @@ struct ModesDev {
   ModeDev m[kMaxOrder];
 };
 
+// Modes with wavelet bases (or several distinct bases): per-thread scratch
+// layout of each distinct basis and the function -> basis map.
+constexpr int kMaxSpec = 8;
+struct SpecDev {
+  int family;              // 0 Legendre, 1 wavelet
+  int p, s;                // degree, resolution
+  int voff;                // offset (doubles) in the per-thread scratch
+  const double* coords;    // wavelet: 2(p+1) x (p+1) mother coords * sqrt(2)
+};
+struct GenModeDev {
+  ModeDev md;
+  int nspec;               // 0 => the mode uses the Legendre fast paths
+  int vtot;                // per-thread scratch doubles
+  SpecDev sp[kMaxSpec];
+  const int* fn_spec;      // r entries
+};
+
 // Host copy of one mode.
 struct ModeHost {
   int r = 0, pmax = 0;
   bool sorted = true;  // every function's indices strictly increasing (format.md:67)
+  std::vector<int> spec_family, spec_p, spec_s;  // distinct bases, first-seen order
+  std::vector<int> fn_spec;                      // function -> distinct basis
+  bool general = false;                          // any wavelet basis in the mode
   double lo = 0, hi = 0;
   std::vector<int> rowptr;
   std::vector<uint32_t> idx;
@@ -87,6 +108,9 @@ struct fstk_gpu_model {
   fstk_gpu::DevBuf<uint32_t> d_idx;
   fstk_gpu::DevBuf<double> d_coef;
   fstk_gpu::DevBuf<double> d_dense;  // all modes' dense coefficient blocks
+  fstk_gpu::GenModeDev gen[fstk_gpu::kMaxOrder] = {};  // wavelet-capable per-mode params
+  fstk_gpu::DevBuf<int> d_fn_spec;
+  std::vector<std::shared_ptr<fstk_gpu::DevBuf<double>>> mother_refs;
   bool dense_ok = true;              // dense kernel is bit-equivalent (sorted indices)
   fstk_gpu::ModesDev modes_dev{};
 
@@ -144,5 +168,12 @@ int64_t evaluate_device_error(const fstk_gpu_model* m, int64_t n, cudaStream_t s
 [[noreturn]] void throw_domain(const fstk_gpu_model* m, int64_t row, const double* y);
 
 int device_sm_count(int device);
+
+// Wavelet support (fstk_wavelet.cu).
+std::shared_ptr<DevBuf<double>> mother_coords_device(int device, int p);
+void upload_wavelet_constants(int device);
+void launch_mode_general(const GenModeDev& G, const double* xs, int64_t n, int64_t n_out,
+                         const int64_t* row_src, double* tk, int64_t ldt, bool exact,
+                         unsigned long long* err_row, cudaStream_t s, int device);
 
 }  // namespace fstk_gpu

@@ -112,6 +112,28 @@ def random_model(ranks, degrees, nnz, seed=0, lo=0.0, hi=1.0, core_decay=1.0) ->
     return Model(np.asfortranarray(core), modes, ModelMetadata(grid_sizes=[0] * d))
 
 
+def mixed_wavelet_model(ranks, wavelets=((1, 2), (3, 1)), legendre_p=6, nnz=5, seed=0,
+                        lo=0.0, hi=1.0) -> Model:
+    """Seeded model whose modes mix Legendre and multiwavelet functions (the
+    CLI always offers a wavelet candidate, pipeline.cpp:341-343): function j
+    of mode k uses basis j % (len(wavelets)+1) (0 = Legendre p)."""
+    rng = np.random.default_rng(seed)
+    specs = [BasisSpec.legendre(legendre_p, lo, hi)] + [BasisSpec.wavelet(s_, p_, lo, hi)
+                                                        for s_, p_ in wavelets]
+    modes = []
+    for k, r in enumerate(ranks):
+        fns = []
+        for j in range(r):
+            b = specs[(j + k) % len(specs)]
+            dim = b.dimension()
+            m = min(nnz, dim)
+            idx = sorted(int(i) for i in rng.choice(dim, size=m, replace=False))
+            fns.append(ModeFunction(b, [(i, float(rng.normal())) for i in idx]))
+        modes.append(fns)
+    core = rng.normal(size=tuple(ranks))
+    return Model(np.asfortranarray(core), modes, ModelMetadata(grid_sizes=[0] * len(ranks)))
+
+
 def _legendre_matrix(p: int, t: np.ndarray) -> np.ndarray:
     out = np.zeros((t.size, p + 1))
     pm1, pm0 = np.ones_like(t), t.copy()

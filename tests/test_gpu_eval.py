@@ -142,12 +142,27 @@ def test_fstk_round_trip_evaluates_bit_identically(tmp_path):  # test_model.cpp:
     assert np.array_equal(m.evaluate_batch(pts), back.evaluate_batch(pts))
 
 
-def test_wavelet_model_rejected_loudly():
-    m = Model(np.ones(2), [[one_sparse(BasisSpec.wavelet(1, 0), 0, 1.0),
-                            one_sparse(BasisSpec.wavelet(1, 0), 1, 1.0)]])
-    with pytest.raises(ValueError) as e:
-        m.evaluate_batch(np.zeros((3, 1)))
-    assert e.value.kind == "Parameter"
+@pytest.mark.parametrize("wav", [((1, 0),), ((1, 2), (3, 1)), ((5, 3),), ((0, 4), (2, 2))])
+def test_wavelet_and_mixed_models(O, wav):
+    """Modes mixing Legendre and multiwavelet functions:
+    evaluation within 1e-12 of the oracle, mode values bit-exact."""
+    m = synth.mixed_wavelet_model((5, 4, 3), wavelets=wav, legendre_p=6, nnz=5, seed=len(wav))
+    pts = synth.uniform_points(20_000, 3, seed=7)
+    pts[0] = [0.0, 0.5, 1.0]           # interval boundaries
+    pts[1] = [0.25, 0.75, 0.125]
+    assert rel(m.evaluate_batch(pts), O.evaluate_batch(m, pts)) <= TOL
+    for k in range(3):
+        got = m.mode_values(k, pts[:300, k])
+        want = np.stack([O.mode_values(m, k, x) for x in pts[:300, k]])
+        assert np.array_equal(got, want)
+
+
+def test_haar_model_values():
+    """s=1, p=0 Haar: [1, step] (test_basis.cpp:65-72) through a 1-mode model."""
+    spec = BasisSpec.wavelet(1, 0)
+    m = Model(np.array([1.0, 1.0]), [[one_sparse(spec, 0, 1.0), one_sparse(spec, 1, 1.0)]])
+    v = m.mode_values(0, np.array([-0.5, 0.5]))
+    assert np.allclose(v, [[1.0, -1.0], [1.0, 1.0]], atol=1e-14)
 
 
 def test_native_library_is_what_ran():

@@ -203,3 +203,17 @@ def test_validation_point_out_of_domain_is_domain_error(O):
     with pytest.raises(ValueError) as e:
         F.reestimate_core(m, bad, vals, seed=17)
     assert e.value.kind == "Domain" and e.value.index == int(val_index[5])
+
+
+@pytest.mark.parametrize("t", ["dct", "wht"])
+def test_wavelet_model_refit_parity(O, t):
+    m = synth.mixed_wavelet_model((4, 3, 3), wavelets=((2, 1),), legendre_p=5, nnz=4, seed=9)
+    pts, vals = _data(O, m, 30_000, 5)
+    sess = F.RefitSession(m, pts, vals, seed=3, transform=t)
+    a, b = sess.sketched()
+    ao, bo, rows_o, _, _ = O.refit_system(m, pts, vals, seed=3, transform=t)
+    assert np.array_equal(a, ao) and np.array_equal(b, bo)
+    sess.close()
+    new, _ = F.reestimate_core(m, pts, vals, seed=3, transform=t)
+    core_o, _ = O.reestimate_core(m, pts, vals, seed=3, transform=t)
+    assert rel(new.core.reshape(-1, order="F"), core_o) <= CORE_TOL

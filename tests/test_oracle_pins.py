@@ -281,3 +281,44 @@ def test_reestimate_rejections(O):                 # :313-322
     assert e.value.kind == "Parameter"
     with pytest.raises(O.OracleError):
         O.reestimate_core(m, pts[:10], O.evaluate_batch(m, pts[:10]), sample_rows=20)
+
+
+# ------------------------------------------------ wavelet KATs (restated) ---
+def test_wavelet_kats(O):
+    v = O.eval_basis(0, -1.0, 1.0, -0.5, family=1, resolution=1)   # test_basis.cpp:65-72
+    assert np.allclose(v, [1.0, -1.0], rtol=1e-14, atol=1e-14)
+    for i in range(8):                                             # :74-90
+        x = -1.0 + (2.0 * i + 1.0) / 8.0
+        v = O.eval_basis(0, -1.0, 1.0, x, family=1, resolution=2)
+        assert v.size == 4 and int(np.sum(np.abs(v) > 1e-12)) == 3
+
+
+@pytest.mark.parametrize("s,p", [(1, 1), (3, 2), (4, 1), (0, 3)])
+def test_wavelet_orthonormality(O, s, p):                          # :92-118
+    n = (p + 1) << s
+    cells = 1 << s
+    nodes, weights = O.gauss_legendre(p + 2)
+    gram = np.zeros((n, n))
+    for c in range(cells):
+        a, b = -1.0 + 2.0 * c / cells, -1.0 + 2.0 * (c + 1) / cells
+        for xq, wq in zip(nodes, weights):
+            x = 0.5 * (a + b) + 0.5 * (b - a) * xq
+            v = O.eval_basis(p, -1.0, 1.0, x, family=1, resolution=s)
+            gram += 0.5 * wq * (b - a) / 2.0 * np.outer(v, v)
+    assert np.abs(gram - np.eye(n)).max() <= 1e-10
+
+
+def test_wavelet_spaces_nest(O):                                   # :134-155
+    p = 1
+    for s in (1, 2, 3):
+        q = 4 * ((p + 1) << s)
+        pts = -1.0 + 2.0 * (np.arange(q) + 0.5) / q
+        dc = np.array([O.eval_basis(p, -1, 1, x, family=1, resolution=s - 1) for x in pts])
+        df = np.array([O.eval_basis(p, -1, 1, x, family=1, resolution=s) for x in pts])
+        sol = np.linalg.lstsq(df, dc, rcond=None)[0]
+        assert np.abs(df @ sol - dc).max() <= 1e-10
+
+
+def test_haar_mother_is_step(O):
+    c = O.mother_coords(0)                                         # basis.cpp:177-187 signs
+    assert np.allclose(c[:, 0] * np.sqrt(2.0), [-1.0, 1.0], atol=1e-14)
