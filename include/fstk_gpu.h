@@ -213,6 +213,21 @@ int32_t fstk_gpu_refit_sketched(const fstk_gpu_refit* refit, double* a,
                                 double* b, int64_t* rows_local,
                                 fstk_gpu_error* err);
 
+/* ---- tensor-product grids --------------------------------- */
+/* All nodes of the Cartesian grid coords_0 x coords_1 x ... (coords: the
+ * sizes[k] coordinates of mode k, concatenated mode by mode); out is
+ * prod(sizes) values, mode-0 fastest (the FTEN layout).  Replaces the
+ * point-by-point evaluate_batch of reconstruct --grid (pipeline.cpp:531-569)
+ * and slice (:571-696) by a chain of mode products.  A coordinate outside its
+ * mode's domain is a Domain error whose index is the node along that mode. */
+int32_t fstk_gpu_evaluate_grid(const fstk_gpu_model* model, const double* coords,
+                               const int64_t* sizes, int32_t d, double* out,
+                               fstk_gpu_error* err);
+/* reconstruct --grid: uniform nodes lo + (hi-lo) i/(I-1) on each mode's domain
+ * (StructuredGrid::node, ingest.cpp:57-61); sizes >= 2. */
+int32_t fstk_gpu_reconstruct_grid(const fstk_gpu_model* model, const int64_t* sizes,
+                                  int32_t d, double* out, fstk_gpu_error* err);
+
 /* ---- measurement hooks (bench.py) ------------------------------------- */
 /* Kernel classes timed by the profiling hook. */
 enum {

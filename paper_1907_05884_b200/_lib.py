@@ -81,7 +81,7 @@ EXPORTS = [
     "fstk_gpu_refit_end", "fstk_gpu_refit_rows", "fstk_gpu_refit_sketched",
     "fstk_gpu_profile_enable", "fstk_gpu_profile_read", "fstk_gpu_fp64_peak",
     "fstk_gpu_refit_factor", "fstk_gpu_refit_correction", "fstk_gpu_refit_apply",
-    "fstk_gpu_refit_finish",
+    "fstk_gpu_refit_finish", "fstk_gpu_evaluate_grid", "fstk_gpu_reconstruct_grid",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -137,6 +137,10 @@ def lib():
     L.fstk_gpu_refit_end.restype = None
     L.fstk_gpu_refit_rows.argtypes = [VP, C.POINTER(C.c_uint64), C.POINTER(Err)]
     L.fstk_gpu_refit_sketched.argtypes = [VP, DP, DP, C.POINTER(C.c_int64), C.POINTER(Err)]
+    L.fstk_gpu_evaluate_grid.argtypes = [VP, DP, C.POINTER(C.c_int64), C.c_int32, DP,
+                                         C.POINTER(Err)]
+    L.fstk_gpu_reconstruct_grid.argtypes = [VP, C.POINTER(C.c_int64), C.c_int32, DP,
+                                            C.POINTER(Err)]
     L.fstk_gpu_profile_enable.argtypes = [C.c_int32]
     L.fstk_gpu_profile_enable.restype = None
     L.fstk_gpu_profile_read.argtypes = [DP, C.POINTER(C.c_uint64), C.POINTER(Err)]

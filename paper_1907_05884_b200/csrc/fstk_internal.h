@@ -1,6 +1,7 @@
 // Internal (non-ABI) declarations shared by the fstk B200 library sources.
 #pragma once
 
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <memory>
@@ -168,6 +169,7 @@ int64_t evaluate_device_error(const fstk_gpu_model* m, int64_t n, cudaStream_t s
 [[noreturn]] void throw_domain(const fstk_gpu_model* m, int64_t row, const double* y);
 
 int device_sm_count(int device);
+cublasHandle_t blas_handle(int device);
 
 // Wavelet support (fstk_wavelet.cu).
 std::shared_ptr<DevBuf<double>> mother_coords_device(int device, int p);

@@ -738,6 +738,8 @@ static Handles& handles(int device) {
   return h;
 }
 
+cublasHandle_t blas_handle(int device) { return handles(device).blas; }
+
 struct EventTimer {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t s;

@@ -274,6 +274,65 @@ class Model:
                                             points.shape[1], dptr(out), C.byref(err)), err)
         return out
 
+    def evaluate_grid(self, coords) -> np.ndarray:
+        """All nodes of the tensor grid coords[0] x coords[1] x ... as an array of
+        shape (len(coords[0]), ...), mode-0 fastest in memory (FTEN order)."""
+        if len(coords) != self.order:
+            raise make_error(1, "grid needs one size per mode")
+        cs = [np.ascontiguousarray(np.atleast_1d(np.asarray(c, dtype=np.float64))) for c in coords]
+        sizes = np.asarray([c.size for c in cs], dtype=np.int64)
+        flat = np.ascontiguousarray(np.concatenate(cs))
+        out = np.empty(int(np.prod(sizes)))
+        err = Err()
+        check(lib().fstk_gpu_evaluate_grid(self.handle(), dptr(flat),
+                                           sizes.ctypes.data_as(C.POINTER(C.c_int64)), self.order,
+                                           dptr(out), C.byref(err)), err)
+        return out.reshape(tuple(int(v) for v in sizes), order="F")
+
+    def reconstruct_grid(self, sizes) -> np.ndarray:
+        """reconstruct --grid (pipeline.cpp:531-569): uniform nodes on the domain."""
+        sz = np.asarray(sizes, dtype=np.int64)
+        if sz.size != self.order:
+            raise make_error(1, "--grid needs one size per mode")
+        out = np.empty(int(np.prod(sz)))
+        err = Err()
+        check(lib().fstk_gpu_reconstruct_grid(self.handle(),
+                                              sz.ctypes.data_as(C.POINTER(C.c_int64)), self.order,
+                                              dptr(out), C.byref(err)), err)
+        return out.reshape(tuple(int(v) for v in sz), order="F")
+
+    def slice(self, mode_x: int, mode_y: int, fixed: dict, width: int = 0, height: int = 0):
+        """slice (pipeline.cpp:571-640): values on a width x height grid over
+        (mode_x, mode_y) with the other modes fixed; returns (h, w), row i = y_i."""
+        d = self.order
+        if not (0 <= mode_x < d and 0 <= mode_y < d):
+            raise make_error(1, "slice modes must name existing modes")
+        if mode_x == mode_y:
+            raise make_error(1, "slice modes must differ")
+        gsz = self.metadata.grid_sizes
+        dflt = lambda k: gsz[k] if k < len(gsz) and gsz[k] >= 2 else 128
+        w = width if width > 0 else dflt(mode_x)
+        h = height if height > 0 else dflt(mode_y)
+        if w < 2 or h < 2:
+            raise make_error(1, "slice resolution must be at least 2 per axis")
+        coords = []
+        for k in range(d):
+            lo, hi = self.domain(k)
+            if k == mode_x:
+                coords.append(lo + (hi - lo) * np.arange(w, dtype=np.float64) / (w - 1))
+            elif k == mode_y:
+                coords.append(lo + (hi - lo) * np.arange(h, dtype=np.float64) / (h - 1))
+            else:
+                if k not in fixed:
+                    raise make_error(1, f"missing fixed value for mode {k}")
+                v = float(fixed[k])
+                if not (v >= lo - 1e-12 * (hi - lo) and v <= hi + 1e-12 * (hi - lo)):
+                    raise make_error(3, f"fixed value for mode {k} outside the model domain")
+                coords.append(np.array([v]))
+        g = self.evaluate_grid(coords)
+        g = g.reshape([g.shape[k] for k in range(d) if k in (mode_x, mode_y)], order="F")
+        return g.T if mode_x < mode_y else g
+
     def evaluate_device(self, points_t, out_t=None, stream=None):
         """Device-resident evaluation: `points_t` is a CUDA torch tensor of shape
         (d, Q) (row k = coordinate k, i.e. the column-major Q x d buffer) or a

@@ -184,3 +184,30 @@ def test_domain_error_index_in_later_device_chunk():
     with pytest.raises(ValueError) as e:
         m.evaluate_device(dp)
     assert e.value.kind == "Domain" and e.value.index == (1 << 21) + 777 and e.value.mode == 1
+
+
+def test_grid_reconstruct_and_slice(O):
+    """Separable grid evaluation equals point-wise evaluation of
+    every node (reconstruct --grid, slice) within the evaluation tolerance."""
+    m = synth.random_model((6, 5, 4), (8, 7, 6), 4, seed=11)
+    sizes = (17, 9, 5)
+    g = m.reconstruct_grid(sizes)
+    assert g.shape == sizes
+    nodes = [np.linspace(0.0, 1.0, s) for s in sizes]
+    X, Y, Z = np.meshgrid(*nodes, indexing="ij")
+    pts = np.stack([X.ravel(order="F"), Y.ravel(order="F"), Z.ravel(order="F")], axis=1)
+    want = O.evaluate_batch(m, pts)
+    assert rel(g.reshape(-1, order="F"), want) <= TOL
+    sl = m.slice(2, 0, {1: 0.3}, width=7, height=6)   # mode_x=2 (w), mode_y=0 (h)
+    ys = np.linspace(0, 1, 6)
+    xs = np.linspace(0, 1, 7)
+    ref = np.array([[O.evaluate(m, [y, 0.3, x]) for x in xs] for y in ys])
+    assert sl.shape == (6, 7) and rel(sl, ref) <= TOL
+    w = synth.mixed_wavelet_model((4, 3, 2), seed=2)
+    gw = w.evaluate_grid([np.linspace(0, 1, 9), [0.5, 0.25], np.linspace(0, 1, 4)])
+    Xw, Yw, Zw = np.meshgrid(np.linspace(0, 1, 9), [0.5, 0.25], np.linspace(0, 1, 4), indexing="ij")
+    pw = np.stack([Xw.ravel(order="F"), Yw.ravel(order="F"), Zw.ravel(order="F")], axis=1)
+    assert rel(gw.reshape(-1, order="F"), O.evaluate_batch(w, pw)) <= TOL
+    with pytest.raises(ValueError) as e:
+        m.evaluate_grid([[0.5], [0.2, 1.7], [0.1]])
+    assert e.value.kind == "Domain" and e.value.mode == 1 and e.value.index == 1
