@@ -213,6 +213,21 @@ int32_t fstk_gpu_refit_sketched(const fstk_gpu_refit* refit, double* a,
                                 double* b, int64_t* rows_local,
                                 fstk_gpu_error* err);
 
+/* ---- refit diagnostics ----------------------------------- */
+/* std::vector<std::pair<uint64_t,double>> self_convergence(const Model&,
+ * const PointCloud&, const std::vector<uint64_t>& s_values, const SketchConfig&)
+ * (randls.hpp:70-75, randls.cpp:385-413): deltas[i] = ||a_{i+1}-a_i|| / ||a_{i+1}||
+ * for i < n_s - 1 (the pair's first element is s_values[i]). */
+int32_t fstk_gpu_self_convergence(const fstk_gpu_model* model, const double* points,
+                                  const double* values, int64_t q, int32_t d,
+                                  const fstk_sketch_cfg* cfg, const uint64_t* s_values,
+                                  int32_t n_s, double* deltas, fstk_gpu_error* err);
+/* Vector leverage_scores(const Matrix& w) (randls.hpp:50, randls.cpp:227-233):
+ * w is q x r column-major (host), scores has q entries; rank_out (optional)
+ * receives the numerical rank used. */
+int32_t fstk_gpu_leverage_scores(const double* w, int64_t q, int64_t r, double* scores,
+                                 int32_t* rank_out, fstk_gpu_error* err);
+
 /* ---- tensor-product grids --------------------------------- */
 /* All nodes of the Cartesian grid coords_0 x coords_1 x ... (coords: the
  * sizes[k] coordinates of mode k, concatenated mode by mode); out is

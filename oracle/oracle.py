@@ -402,3 +402,34 @@ def reestimate_core(model, points, values, seed=0, sample_rows=0, working_subset
     info["rank_deficient"] = bool(rank_def)
     info["rows"] = rows
     return alpha, info
+
+
+def leverage_scores(w):
+    """randls.cpp:227-233 restated: thin SVD, rank by Eigen's SVDBase rule."""
+    w = np.asarray(w, dtype=np.float64)
+    q, r = w.shape
+    if q < r:
+        raise OracleError(1, "leverage scores need at least as many rows as columns")
+    u, s, _ = np.linalg.svd(w, full_matrices=False)
+    thr = min(q, r) * np.finfo(np.float64).eps * (s[0] if s.size else 0.0)
+    rank = int(np.sum(s > thr))
+    return np.sum(u[:, :rank] ** 2, axis=1)
+
+
+def self_convergence(model, points, values, s_values, seed=0, working_subset=1 << 20,
+                     transform="dct", validation_fraction=0.05):
+    """randls.cpp:385-413 restated on top of the oracle's sketched systems."""
+    s_values = [int(s) for s in s_values]
+    if len(s_values) < 2:
+        raise OracleError(1, "need at least two sample counts")
+    alphas = []
+    for s in s_values:
+        a, b, _, _, _ = refit_system(model, points, values, seed, s, working_subset, transform,
+                                     validation_fraction)
+        alphas.append(solve_system(a, b)[0])
+    out = []
+    for i in range(len(s_values) - 1):
+        den = np.linalg.norm(alphas[i + 1])
+        dl = np.linalg.norm(alphas[i + 1] - alphas[i])
+        out.append((s_values[i], dl / den if den > 0 else dl))
+    return out

@@ -9,8 +9,8 @@ in libfstk_gpu.so on the GPU; there is no CPU fallback.
 """
 from ._lib import FstkError, FstkIOError, FstkValueError, launch_count
 from .model import BasisSpec, Model, ModelMetadata, ModeFunction, load_model, save_model
-from .refit import (RefitSession, build_design_rows, mixed_matrix, reestimate_core, sketch,
-                    sketch_config)
+from .refit import (RefitSession, build_design_rows, leverage_scores, mixed_matrix,
+                    reestimate_core, self_convergence, sketch, sketch_config)
 
 
 def set_max_threads(n: int) -> None:
@@ -22,6 +22,6 @@ def set_max_threads(n: int) -> None:
 __all__ = [
     "BasisSpec", "Model", "ModelMetadata", "ModeFunction", "load_model", "save_model",
     "reestimate_core", "RefitSession", "build_design_rows", "sketch", "mixed_matrix",
-    "sketch_config", "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
+    "sketch_config", "self_convergence", "leverage_scores", "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
     "launch_count",
 ]

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 #include <cuda_runtime.h>
 
 #include <memory>
@@ -170,6 +171,7 @@ int64_t evaluate_device_error(const fstk_gpu_model* m, int64_t n, cudaStream_t s
 
 int device_sm_count(int device);
 cublasHandle_t blas_handle(int device);
+cusolverDnHandle_t solver_handle(int device);
 
 // Wavelet support (fstk_wavelet.cu).
 std::shared_ptr<DevBuf<double>> mother_coords_device(int device, int p);

@@ -739,6 +739,7 @@ static Handles& handles(int device) {
 }
 
 cublasHandle_t blas_handle(int device) { return handles(device).blas; }
+cusolverDnHandle_t solver_handle(int device) { return handles(device).solver; }
 
 struct EventTimer {
   cudaEvent_t a = nullptr, b = nullptr;

@@ -204,3 +204,31 @@ def mixed_matrix(w, seed=0, transform="dct") -> np.ndarray:
     err = Err()
     check(lib().fstk_gpu_mixed_matrix(dptr(w), q, r, C.byref(cfg), dptr(out), C.byref(err)), err)
     return out
+
+
+def self_convergence(model: Model, points, values, s_values, seed=0, working_subset=1 << 20,
+                     transform="dct", validation_fraction=0.05):
+    """randls.cpp:385-413: [(S_i, ||a_{i+1}-a_i|| / ||a_{i+1}||), ...]."""
+    require_gpu()
+    p, v = _cloud(model, points, values)
+    sv = np.ascontiguousarray(np.asarray(s_values, dtype=np.uint64))
+    cfg = sketch_config(seed, 0, working_subset, transform, validation_fraction)
+    deltas = np.zeros(max(sv.size - 1, 1))
+    err = Err()
+    check(lib().fstk_gpu_self_convergence(model.handle(), dptr(p), dptr(v), p.shape[0], p.shape[1],
+                                          C.byref(cfg), sv.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                          int(sv.size), dptr(deltas), C.byref(err)), err)
+    return [(int(sv[i]), float(deltas[i])) for i in range(sv.size - 1)]
+
+
+def leverage_scores(w) -> np.ndarray:
+    """randls.cpp:227-233."""
+    require_gpu()
+    w = np.asfortranarray(np.asarray(w, dtype=np.float64))
+    q, r = w.shape
+    out = np.zeros(q)
+    rank = C.c_int32()
+    err = Err()
+    check(lib().fstk_gpu_leverage_scores(dptr(w), q, r, dptr(out), C.byref(rank), C.byref(err)),
+          err)
+    return out

@@ -217,3 +217,53 @@ def test_wavelet_model_refit_parity(O, t):
     new, _ = F.reestimate_core(m, pts, vals, seed=3, transform=t)
     core_o, _ = O.reestimate_core(m, pts, vals, seed=3, transform=t)
     assert rel(new.core.reshape(-1, order="F"), core_o) <= CORE_TOL
+
+
+# ------------------------------------------------------ diagnostics (8f-3) ---
+def test_leverage_scores(O):                        # test_randls.cpp:208-230
+    n = 12
+    q, _ = np.linalg.qr(random_points(n, n, 59))
+    assert np.abs(F.leverage_scores(q) - 1.0).max() <= 1e-10
+    w = random_points(200, 10, 61)
+    sc = F.leverage_scores(w)
+    assert abs(sc.sum() - 10.0) <= 1e-8 * 10 and sc.min() >= 0.0
+    assert np.abs(sc - O.leverage_scores(w)).max() <= 1e-10
+    w = random_points(50, 3, 67) * 1e-6
+    w[7] = [1e6, 0, 0]
+    assert abs(F.leverage_scores(w)[7] - 1.0) <= 1e-6
+    with pytest.raises(ValueError):
+        F.leverage_scores(random_points(3, 5, 1))
+
+
+def test_mixing_spreads_leverage():                 # test_randls.cpp:232-253
+    q, r = 4096, 64
+    w = random_points(q, r, 71) * 1e-3
+    rng = np.random.default_rng(73)
+    for _ in range(10):
+        w[rng.integers(0, q)] = 100.0 * rng.normal(size=r)
+    pre = F.leverage_scores(w)
+    assert pre.max() / pre.mean() >= 50.0
+    post = F.leverage_scores(F.mixed_matrix(w, seed=7))
+    assert post.max() / post.mean() <= 5.0
+
+
+def test_self_convergence(O):                        # test_randls.cpp:324-355
+    m = legendre_model((2, 2), 131)
+    pts = random_points(1000, 2, 137)
+    vals = O.evaluate_batch(m, pts) + 0.01 * np.random.default_rng(139).normal(size=1000)
+    curve = F.self_convergence(m, pts, vals, [64, 64, 64], seed=31)
+    assert len(curve) == 2 and curve[0][1] == 0.0 and curve[1][1] == 0.0
+    m = legendre_model((2, 2, 2), 149)
+    pts = random_points(3000, 3, 151)
+    vals = O.evaluate_batch(m, pts)
+    curve = F.self_convergence(m, pts, vals, [16, 32, 64, 128], seed=37)
+    assert len(curve) == 3 and all(np.isfinite(dl) and dl <= 1e-8 for _, dl in curve)
+    noisy = vals + 0.001 * np.random.default_rng(5).normal(size=vals.size)
+    got = F.self_convergence(m, pts, noisy, [16, 40, 128], seed=3)
+    want = O.self_convergence(m, pts, noisy, [16, 40, 128], seed=3)
+    for (s1, a), (s2, b) in zip(got, want):
+        assert s1 == s2 and abs(a - b) <= 1e-8 * max(1.0, abs(b))
+    with pytest.raises(ValueError):
+        F.self_convergence(m, pts, vals, [64])
+    with pytest.raises(ValueError):
+        F.self_convergence(m, pts, vals, [64, 32])
