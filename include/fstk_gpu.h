@@ -243,6 +243,12 @@ int32_t fstk_gpu_evaluate_grid(const fstk_gpu_model* model, const double* coords
 int32_t fstk_gpu_reconstruct_grid(const fstk_gpu_model* model, const int64_t* sizes,
                                   int32_t d, double* out, fstk_gpu_error* err);
 
+/* FPTC ingest (format.md:29-44, ingest.cpp:706-742): converts the
+ * file's point-major payload (device, Q x d row-major) into the column-major
+ * SoA buffer the evaluation/refit entry points take, on `stream`. */
+int32_t fstk_gpu_point_major_to_soa(const double* in, int64_t q, int32_t d, double* out,
+                                    void* stream, fstk_gpu_error* err);
+
 /* ---- measurement hooks (bench.py) ------------------------------------- */
 /* Kernel classes timed by the profiling hook. */
 enum {

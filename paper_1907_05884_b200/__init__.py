@@ -8,6 +8,8 @@ proj/python/module.cpp): `Model.evaluate_batch`, `load_model`,
 in libfstk_gpu.so on the GPU; there is no CPU fallback.
 """
 from ._lib import FstkError, FstkIOError, FstkValueError, launch_count
+from .cloud import (PointCloud, read_cloud, read_cloud_binary, read_cloud_csv, read_cloud_device,
+                    read_points_csv, write_cloud_binary, write_cloud_csv)
 from .model import BasisSpec, Model, ModelMetadata, ModeFunction, load_model, save_model
 from .refit import (RefitSession, build_design_rows, leverage_scores, mixed_matrix,
                     reestimate_core, self_convergence, sketch, sketch_config)
@@ -23,5 +25,6 @@ __all__ = [
     "BasisSpec", "Model", "ModelMetadata", "ModeFunction", "load_model", "save_model",
     "reestimate_core", "RefitSession", "build_design_rows", "sketch", "mixed_matrix",
     "sketch_config", "self_convergence", "leverage_scores", "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
-    "launch_count",
+    "launch_count", "PointCloud", "read_cloud", "read_cloud_binary", "read_cloud_csv",
+    "read_cloud_device", "read_points_csv", "write_cloud_binary", "write_cloud_csv",
 ]

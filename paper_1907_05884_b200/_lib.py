@@ -82,7 +82,7 @@ EXPORTS = [
     "fstk_gpu_profile_enable", "fstk_gpu_profile_read", "fstk_gpu_fp64_peak",
     "fstk_gpu_refit_factor", "fstk_gpu_refit_correction", "fstk_gpu_refit_apply",
     "fstk_gpu_refit_finish", "fstk_gpu_evaluate_grid", "fstk_gpu_reconstruct_grid",
-    "fstk_gpu_self_convergence", "fstk_gpu_leverage_scores",
+    "fstk_gpu_self_convergence", "fstk_gpu_leverage_scores", "fstk_gpu_point_major_to_soa",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -147,6 +147,7 @@ def lib():
                                             DP, C.POINTER(Err)]
     L.fstk_gpu_leverage_scores.argtypes = [DP, C.c_int64, C.c_int64, DP, C.POINTER(C.c_int32),
                                            C.POINTER(Err)]
+    L.fstk_gpu_point_major_to_soa.argtypes = [VP, C.c_int64, C.c_int32, VP, VP, C.POINTER(Err)]
     L.fstk_gpu_profile_enable.argtypes = [C.c_int32]
     L.fstk_gpu_profile_enable.restype = None
     L.fstk_gpu_profile_read.argtypes = [DP, C.POINTER(C.c_uint64), C.POINTER(Err)]

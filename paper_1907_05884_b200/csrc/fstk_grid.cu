@@ -132,3 +132,32 @@ int32_t fstk_gpu_reconstruct_grid(const fstk_gpu_model* m, const int64_t* sizes,
 }
 
 }  // extern "C"
+
+// FPTC ingest: point-major (Q x d row-major, the file payload)
+// -> SoA (column-major Q x d) on the device, coalesced through shared memory.
+namespace fstk_gpu {
+__global__ void point_major_to_soa_kernel(const double* __restrict__ in, int64_t q, int d,
+                                          double* __restrict__ out) {
+  __shared__ double tile[256 * 8];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * 256;
+  const int64_t nrow = (q - base) < 256 ? (q - base) : 256;
+  for (int e = threadIdx.x; e < nrow * d; e += blockDim.x) tile[e] = in[base * d + e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < nrow * d; e += blockDim.x) {
+    const int k = e / static_cast<int>(nrow), i = e % static_cast<int>(nrow);
+    out[k * q + base + i] = tile[i * d + k];
+  }
+}
+}  // namespace fstk_gpu
+
+extern "C" int32_t fstk_gpu_point_major_to_soa(const double* in, int64_t q, int32_t d, double* out,
+                                               void* stream, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(in && out, FSTK_E_PARAMETER, "null argument");
+    require(d >= 1 && d <= kMaxOrder, FSTK_E_SHAPE, "point cloud dimension must be in [1, 8]");
+    if (q <= 0) return;
+    point_major_to_soa_kernel<<<static_cast<unsigned>(ceil_div(q, 256)), 256, 0,
+                                static_cast<cudaStream_t>(stream)>>>(in, q, d, out);
+    check_launch("point_major_to_soa_kernel");
+  });
+}
