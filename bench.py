@@ -297,7 +297,11 @@ def main():
             "step_tflops": (fc + fm) * n / (ms * 1e-3) / 1e12,
             "step_frac": (fc + fm) * n / (ms * 1e-3) / 1e12 / peak_mma,
             "mode_tables_ms_per_step": m_ms / args.steps,
-            "contract_ms_per_step": c_ms / args.steps}
+            "contract_ms_per_step": c_ms / args.steps,
+            "note": "the mode-table kernel of chunk i+1 runs concurrently with the contraction of "
+                    "chunk i on a second stream (both use the fp64 pipe), so the per-launch "
+                    "event durations overlap: `frac` is the contraction measured while sharing "
+                    "the SMs, `step_frac` is the whole evaluation step (all 73,120 flop/pt)"}
 
     # ---- e2e through the host C-ABI (pinned host buffers)
     hp = torch.from_numpy(np.ascontiguousarray(pts.T)).pin_memory()
