@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -274,10 +275,10 @@ __device__ __forceinline__ double outer_factor(const ContractParams& P, const do
   }
 }
 
-template <int NSW, int D, int TP>
-__global__ void __launch_bounds__((TP / 32 * 2 + 1) * 32) contract_kernel(const ContractParams P) {
+template <int NSW, int D, int TP, int NH>
+__global__ void __launch_bounds__((TP / 32 * NH + 1) * 32) contract_kernel(const ContractParams P) {
   constexpr int NPG = TP / 32;        // 32-point groups
-  constexpr int NCW = NPG * 2;        // consumer warps
+  constexpr int NCW = NPG * NH;       // consumer warps (NH column groups per point group)
   constexpr int U0_LD = u0_ld(TP), U1_LD = u1_ld(TP);
   extern __shared__ __align__(1024) unsigned char smem[];
   const SmemLayout L = smem_layout(P, TP);
@@ -346,9 +347,9 @@ __global__ void __launch_bounds__((TP / 32 * 2 + 1) * 32) contract_kernel(const 
 
   // ===== consumer warps =====
   const int pg = warp % NPG;  // 32-point group
-  const int nh = warp / NPG;  // column half
+  const int nh = warp / NPG;  // column group
   const int g = lane >> 2, t = lane & 3;
-  constexpr int NS = 2 * NSW;
+  constexpr int NS = NH * NSW;
   int stage = 0;
   uint32_t phase = 0;
   int it = 0;
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__((TP / 32 * 2 + 1) * 32) contract_kernel(const 
     if (nh == 0) {
       const int row = pg * 32 + lane;
       const int64_t gi = tile * TP + row;
-      if (gi < P.n) P.out[gi] = ybuf[row] + ybuf[TP + row];
+      if (gi < P.n) P.out[gi] = NH == 2 ? ybuf[row] + ybuf[TP + row] : ybuf[row];
     }
     consumer_bar<NCW>();
   }
@@ -581,36 +582,36 @@ static ContractParams make_params(const fstk_gpu_model* m, const double* tables,
   return P;
 }
 
-template <int NSW, int D, int TPL>
+template <int NSW, int D, int TPL, int NH>
 static void launch_contract_t(const fstk_gpu_model* m, const ContractParams& P, cudaStream_t s) {
   static std::once_flag once[64];
   const size_t smem = m->lay.smem;
   std::call_once(once[m->device & 63], [&] {
     int optin = 0;
     FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
-    FSTK_CUDA(cudaFuncSetAttribute(contract_kernel<NSW, D, TPL>,
+    FSTK_CUDA(cudaFuncSetAttribute(contract_kernel<NSW, D, TPL, NH>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   });
   const int64_t grid = std::min<int64_t>(P.ntiles, static_cast<int64_t>(m->num_sms) * m->lay.ctas_per_sm);
-  contract_kernel<NSW, D, TPL><<<static_cast<unsigned>(grid), (TPL / 32 * 2 + 1) * 32, smem, s>>>(P);
+  contract_kernel<NSW, D, TPL, NH><<<static_cast<unsigned>(grid), (TPL / 32 * NH + 1) * 32, smem, s>>>(P);
   check_launch("contract_kernel");
 }
 
-template <int NSW, int D>
+template <int NSW, int D, int NH>
 static void launch_contract_tp(const fstk_gpu_model* m, const ContractParams& P, cudaStream_t s) {
   if (m->lay.tp == 64)
-    launch_contract_t<NSW, D, 64>(m, P, s);
+    launch_contract_t<NSW, D, 64, NH>(m, P, s);
   else
-    launch_contract_t<NSW, D, 128>(m, P, s);
+    launch_contract_t<NSW, D, 128, NH>(m, P, s);
 }
 
-template <int NSW>
+template <int NSW, int NH>
 static void launch_contract_d(const fstk_gpu_model* m, const ContractParams& P, cudaStream_t s) {
   switch (m->d) {
-    case 2: launch_contract_tp<NSW, 2>(m, P, s); break;
-    case 3: launch_contract_tp<NSW, 3>(m, P, s); break;
-    case 4: launch_contract_tp<NSW, 4>(m, P, s); break;
-    default: launch_contract_tp<NSW, 0>(m, P, s); break;
+    case 2: launch_contract_tp<NSW, 2, NH>(m, P, s); break;
+    case 3: launch_contract_tp<NSW, 3, NH>(m, P, s); break;
+    case 4: launch_contract_tp<NSW, 4, NH>(m, P, s); break;
+    default: launch_contract_tp<NSW, 0, NH>(m, P, s); break;
   }
 }
 
@@ -632,11 +633,20 @@ void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_
   }
   ContractParams P = make_params(m, tables, toff, ldt, n, out);
   if (bpack_override) P.bpack = bpack_override;
-  switch (m->lay.nsw) {
-    case 1: launch_contract_d<1>(m, P, s); break;
-    case 2: launch_contract_d<2>(m, P, s); break;
-    case 3: launch_contract_d<3>(m, P, s); break;
-    case 4: launch_contract_d<4>(m, P, s); break;
+  if (m->lay.nh == 1) {
+    switch (m->lay.nsw) {  // NSW = N1p / 8
+      case 2: launch_contract_d<2, 1>(m, P, s); break;
+      case 4: launch_contract_d<4, 1>(m, P, s); break;
+      case 6: launch_contract_d<6, 1>(m, P, s); break;
+      default: fail(FSTK_E_COMPUTE, "internal: bad contraction layout");
+    }
+    return;
+  }
+  switch (m->lay.nsw) {  // NSW = N1p / 16
+    case 1: launch_contract_d<1, 2>(m, P, s); break;
+    case 2: launch_contract_d<2, 2>(m, P, s); break;
+    case 3: launch_contract_d<3, 2>(m, P, s); break;
+    case 4: launch_contract_d<4, 2>(m, P, s); break;
     default: fail(FSTK_E_COMPUTE, "internal: bad contraction layout");
   }
 }
@@ -657,7 +667,14 @@ static void plan_layout(fstk_gpu_model* m) {
   L.NC = static_cast<int>(ceil_div(r1, L.N1p));
   L.Mout = 1;
   for (int k = 2; k < m->d; ++k) L.Mout *= static_cast<int>(m->ranks[k]);
-  L.nsw = L.N1p / 16;
+  // Column groups per 32-point group: 1 (a warp owns all N1p/8 subtiles:
+  // more independent DMMAs, half the A-fragment loads) or 2.
+  // Measured on B200 (round 1): one group wins at N1p = 16 (C1 +7%, C4 +4%),
+  // two groups win at N1p >= 32 (register pressure of 4-6 subtiles per warp).
+  L.nh = L.N1p <= 16 ? 1 : 2;
+  if (const char* e = std::getenv("FSTK_CONTRACT_NH")) L.nh = std::atoi(e) == 1 ? 1 : 2;
+  if (L.nh == 1 && L.N1p > 48) L.nh = 2;
+  L.nsw = L.N1p / (8 * L.nh);
   L.btile_elems = static_cast<int64_t>(L.Kp) * L.N1p;
   int optin = 0, per_sm = 0;
   FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
@@ -677,7 +694,7 @@ static void plan_layout(fstk_gpu_model* m) {
       if (S.total > static_cast<uint32_t>(optin)) continue;
       const int ctas = std::min<int>(per_sm / static_cast<int>(S.total + 1024), 4);
       if (ctas < 1) continue;
-      const int warps = ctas * (tp / 32 * 2);
+      const int warps = ctas * (tp / 32 * L.nh);
       const double score =
           std::min(warps, 16) * 100.0 + std::min(ctas, 3) * 50.0 + std::min(ns, 4) * 10.0 + tp / 64.0;
       if (score > best) {

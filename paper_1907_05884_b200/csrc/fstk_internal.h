@@ -75,7 +75,8 @@ struct ContractLayout {
   int N1p = 0;         // j1 columns per B tile (multiple of 16, <= 64)
   int NC = 0;          // j1 chunks
   int Mout = 0;        // prod_{k>=2} r_k
-  int nsw = 0;         // 8-column subtiles per warp = N1p / 16
+  int nsw = 0;         // 8-column subtiles per warp = N1p / (8 nh)
+  int nh = 2;          // column groups per 32-point group
   int nstage = 0;      // B pipeline depth
   int tp = 128;        // points per CTA tile (64 or 128)
   int ctas_per_sm = 1; // resident CTAs per SM at this shared-memory footprint
