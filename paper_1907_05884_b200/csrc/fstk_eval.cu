@@ -432,6 +432,221 @@ __global__ void __launch_bounds__((TP / 32 * NH + 1) * 32) contract_kernel(const
   }
 }
 
+// ------------------------------------------------- K1b' Khatri-Rao form ---
+// For d = 3, 4: T[p, n] = sum_{j0,j1} (u0[p,j0] u1[p,j1]) G[j0, j1, n] with
+// n = (j2, j3): K = r0 * r1 (A generated per j1 as the u0 fragment times the
+// point's u1 value — one DMUL per fragment), N = r2 (r3), and a single
+// epilogue per tile y_p = sum_n T[p, n] prod_{k>=2} u_k[p, j_k(n)].  The
+// accumulators live across the whole K loop (no per-n epilogue bubbles).
+// B tiles (one per j1, Kp x Np, fragment-ordered) stream through the same
+// TMA bulk-copy / mbarrier ring; u tables arrive per tile as before.
+struct KRParams {
+  const double* tables;
+  Int64x8 toff;
+  int64_t ldt;
+  int64_t n;
+  int64_t ntiles;
+  int d;
+  int r[kMaxOrder];
+  int Kp, Nn, Np, nstage;
+  const double* bpack;  // [j1][Kp/4][Np/8][32]
+  double* out;
+};
+
+struct KRSmem {
+  uint32_t bars, u0, u1, uk, bst, ybuf, total;
+};
+
+__host__ __device__ inline KRSmem kr_smem(const KRParams& P, int tp, int nh) {
+  KRSmem L{};
+  uint32_t o = 0;
+  L.bars = o;
+  o += ((2 * P.nstage + 2) * 8 + 127) / 128 * 128;
+  L.u0 = o;
+  o += static_cast<uint32_t>(P.Kp) * u0_ld(tp) * 8;
+  L.u1 = o;
+  o += static_cast<uint32_t>(P.r[1]) * tp * 8;
+  L.uk = o;
+  for (int k = 2; k < P.d; ++k) o += static_cast<uint32_t>(P.r[k]) * tp * 8;
+  o = (o + 127) / 128 * 128;
+  L.bst = o;
+  o += static_cast<uint32_t>(P.nstage) * P.Kp * P.Np * 8;
+  L.ybuf = o;
+  o += static_cast<uint32_t>(nh) * tp * 8;
+  L.total = o;
+  return L;
+}
+
+template <int NSW, int D, int NH>
+__global__ void __launch_bounds__((64 / 32 * NH + 1) * 32) contract_kr_kernel(const KRParams P) {
+  constexpr int TP = 64;
+  constexpr int NPG = TP / 32;
+  constexpr int NCW = NPG * NH;
+  constexpr int NS = NH * NSW;
+  constexpr int U0_LD = u0_ld(TP);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const KRSmem L = kr_smem(P, TP, NH);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + P.nstage;
+  uint64_t* ufull = empty + P.nstage;
+  uint64_t* uempty = ufull + 1;
+  double* u0s = reinterpret_cast<double*>(smem + L.u0);
+  double* u1s = reinterpret_cast<double*>(smem + L.u1);
+  double* uks = reinterpret_cast<double*>(smem + L.uk);
+  double* bst = reinterpret_cast<double*>(smem + L.bst);
+  double* ybuf = reinterpret_cast<double*>(smem + L.ybuf);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r1 = P.r[1];
+  const int stage_elems = P.Kp * P.Np;
+  const uint32_t stage_bytes = static_cast<uint32_t>(stage_elems) * 8u;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P.nstage; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    mbar_init(ufull, 1);
+    mbar_init(uempty, NCW);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      uint32_t ubytes = static_cast<uint32_t>(P.Kp + r1) * TP * 8u;
+      for (int k = 2; k < P.d; ++k) ubytes += static_cast<uint32_t>(P.r[k]) * TP * 8u;
+      for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x, ++it) {
+        if (it > 0) mbar_wait(uempty, (it - 1) & 1);
+        mbar_arrive_expect_tx(ufull, ubytes);
+        const int64_t row0 = tile * TP;
+        const double* t0 = P.tables + P.toff.v[0] + row0;
+        for (int j = 0; j < P.Kp; ++j) bulk_g2s(u0s + j * U0_LD, t0 + j * P.ldt, TP * 8, ufull);
+        const double* t1 = P.tables + P.toff.v[1] + row0;
+        for (int j = 0; j < r1; ++j) bulk_g2s(u1s + j * TP, t1 + j * P.ldt, TP * 8, ufull);
+        double* dst = uks;
+        for (int k = 2; k < P.d; ++k) {
+          const double* tk = P.tables + P.toff.v[k] + row0;
+          for (int j = 0; j < P.r[k]; ++j) bulk_g2s(dst + j * TP, tk + j * P.ldt, TP * 8, ufull);
+          dst += P.r[k] * TP;
+        }
+        for (int j1 = 0; j1 < r1; ++j1) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], stage_bytes);
+          bulk_g2s(bst + static_cast<size_t>(stage) * stage_elems,
+                   P.bpack + static_cast<size_t>(j1) * stage_elems, stage_bytes, &full[stage]);
+          if (++stage == P.nstage) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  const int pg = warp % NPG;
+  const int nh = warp / NPG;
+  const int g = lane >> 2, t = lane & 3;
+  // Outer-factor offsets of this thread's 2*NSW columns (fixed across tiles).
+  int off2[NSW][2], off3[NSW][2];
+  bool nval[NSW][2];
+#pragma unroll
+  for (int b = 0; b < NSW; ++b)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int nn = (nh * NSW + b) * 8 + 2 * t + i;
+      nval[b][i] = nn < P.Nn;
+      const int nc = nval[b][i] ? nn : 0;
+      if constexpr (D == 3) {
+        off2[b][i] = nc * TP;
+        off3[b][i] = 0;
+      } else {
+        off2[b][i] = (nc % P.r[2]) * TP;
+        off3[b][i] = (P.r[2] + nc / P.r[2]) * TP;
+      }
+    }
+  int stage = 0;
+  uint32_t phase = 0;
+  int it = 0;
+  const int ksteps = P.Kp / 4;
+  for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x, ++it) {
+    mbar_wait(ufull, it & 1);
+    double acc[4][NSW][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < NSW; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const double* ua = u0s + t * U0_LD + pg * 32 + g;
+    const double* u1p = u1s + pg * 32 + g;
+    for (int j1 = 0; j1 < r1; ++j1) {
+      double u1v[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) u1v[a] = u1p[j1 * TP + a * 8];
+      mbar_wait(&full[stage], phase);
+      const double* bb = bst + static_cast<size_t>(stage) * stage_elems + (nh * NSW) * 32 + lane;
+#pragma unroll 4
+      for (int ks = 0; ks < ksteps; ++ks) {
+        double av[4], bv[NSW];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = ua[(4 * ks) * U0_LD + a * 8] * u1v[a];
+#pragma unroll
+        for (int b = 0; b < NSW; ++b) bv[b] = bb[(ks * NS + b) * 32];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < NSW; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == P.nstage) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    // Epilogue: y_p = sum_n T[p, n] prod_{k>=2} u_k[p, j_k(n)].
+    double y[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int row = pg * 32 + a * 8 + g;
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < NSW; ++b)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (!nval[b][i]) continue;
+          double o = uks[off2[b][i] + row];
+          if constexpr (D == 4) o = o * uks[off3[b][i] + row];
+          s = fma(acc[a][b][i], o, s);
+        }
+      y[a] = s;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(uempty);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      y[a] += __shfl_xor_sync(0xffffffffu, y[a], 1);
+      y[a] += __shfl_xor_sync(0xffffffffu, y[a], 2);
+      if (t == 0) ybuf[nh * TP + pg * 32 + a * 8 + g] = y[a];
+    }
+    consumer_bar<NCW>();
+    if (nh == 0) {
+      const int row = pg * 32 + lane;
+      const int64_t gi = tile * TP + row;
+      if (gi < P.n) {
+        double v = ybuf[row];
+#pragma unroll
+        for (int h = 1; h < NH; ++h) v += ybuf[h * TP + row];
+        P.out[gi] = v;
+      }
+    }
+    consumer_bar<NCW>();
+  }
+}
+
 // Generic contraction (any d <= 8, any ranks): thread per point, core read
 // through L1/L2 with incremental multi-index; used when the DMMA layout does
 // not apply (d == 1, or shared-memory budget exceeded).
@@ -615,6 +830,47 @@ static void launch_contract_d(const fstk_gpu_model* m, const ContractParams& P, 
   }
 }
 
+template <int NSW, int D, int NH>
+static void launch_kr_t(const fstk_gpu_model* m, const KRParams& P, cudaStream_t s) {
+  static std::once_flag once[64];
+  std::call_once(once[m->device & 63], [&] {
+    int optin = 0;
+    FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+    FSTK_CUDA(cudaFuncSetAttribute(contract_kr_kernel<NSW, D, NH>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  });
+  const int64_t grid = std::min<int64_t>(P.ntiles, static_cast<int64_t>(m->num_sms) * m->lay.ctas_per_sm);
+  contract_kr_kernel<NSW, D, NH><<<static_cast<unsigned>(grid), (2 * NH + 1) * 32, m->lay.smem, s>>>(P);
+  check_launch("contract_kr_kernel");
+}
+
+template <int D, int NH>
+static void launch_kr_n(const fstk_gpu_model* m, const KRParams& P, cudaStream_t s) {
+  switch (m->lay.nsw) {
+    case 2: launch_kr_t<2, D, NH>(m, P, s); break;
+    case 3: launch_kr_t<3, D, NH>(m, P, s); break;
+    case 4: launch_kr_t<4, D, NH>(m, P, s); break;
+    default: fail(FSTK_E_COMPUTE, "internal: bad KR layout");
+  }
+}
+
+template <int D>
+static void launch_kr_h(const fstk_gpu_model* m, const KRParams& P, cudaStream_t s) {
+  switch (m->lay.nh) {
+    case 1: launch_kr_n<D, 1>(m, P, s); break;
+    case 2: launch_kr_n<D, 2>(m, P, s); break;
+    case 4: launch_kr_n<D, 4>(m, P, s); break;
+    default: fail(FSTK_E_COMPUTE, "internal: bad KR layout");
+  }
+}
+
+static void launch_kr(const fstk_gpu_model* m, const KRParams& P, cudaStream_t s) {
+  if (m->d == 3)
+    launch_kr_h<3>(m, P, s);
+  else
+    launch_kr_h<4>(m, P, s);
+}
+
 void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_t* toff,
                      int64_t ldt, int64_t n, double* out, cudaStream_t s,
                      const double* bpack_override, const double* core_override) {
@@ -629,6 +885,26 @@ void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_
     contract_generic_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, s>>>(
         tables, to, ldt, n, m->d, rk, core_override ? core_override : m->d_core.p, m->R, out);
     check_launch("contract_generic_kernel");
+    return;
+  }
+  if (m->lay.kr) {
+    KRParams P{};
+    P.tables = tables;
+    for (int k = 0; k < m->d; ++k) {
+      P.toff.v[k] = toff[k];
+      P.r[k] = static_cast<int>(m->ranks[k]);
+    }
+    P.ldt = ldt;
+    P.n = n;
+    P.ntiles = ceil_div(n, 64);
+    P.d = m->d;
+    P.Kp = m->lay.Kp;
+    P.Nn = m->lay.Mout;
+    P.Np = m->lay.kr_np;
+    P.nstage = m->lay.nstage;
+    P.bpack = bpack_override ? bpack_override : m->d_bpack.p;
+    P.out = out;
+    launch_kr(m, P, s);
     return;
   }
   ContractParams P = make_params(m, tables, toff, ldt, n, out);
@@ -655,11 +931,87 @@ void launch_contract(const fstk_gpu_model* m, const double* tables, const int64_
 // Chooses the tile (TP = 64 or 128 points) and ring depth that maximise
 // resident consumer warps per SM (so one CTA's u-table prologue overlaps the
 // other CTAs' DMMA work), preferring deeper rings at equal residency.
+// Khatri-Rao form (d = 3, 4): K = r0 r1, N = prod_{k>=2} r_k <= 128 split over
+// NH warps of NSW 8-column subtiles; TP = 64 points; ring depth and residency
+// as for the classic layout.
+static bool plan_kr(fstk_gpu_model* m) {
+  ContractLayout& L = m->lay;
+  if (!(m->d == 3 || m->d == 4)) return false;
+  // Measured on B200 (round 1): the KR form wins for d = 4 (C4 +4%) and loses
+  // for d = 3 (C1 -12%, C2 -4%, C3 -3%: the per-fragment DMUL sits on the
+  // A-operand path); FSTK_CONTRACT_KR=0/1 overrides.
+  bool want = m->d == 4;
+  if (const char* e = std::getenv("FSTK_CONTRACT_KR")) want = std::atoi(e) != 0;
+  if (!want) return false;
+  int Nn = 1;
+  for (int k = 2; k < m->d; ++k) Nn *= static_cast<int>(m->ranks[k]);
+  int best_np = 1 << 30, bnh = 0, bnsw = 0;
+  for (int nh : {2, 1, 4})
+    for (int nsw : {2, 3, 4}) {
+      const int np = nh * nsw * 8;
+      if (np >= Nn && np < best_np) {
+        best_np = np;
+        bnh = nh;
+        bnsw = nsw;
+      }
+    }
+  if (const char* e = std::getenv("FSTK_KR_NH")) {
+    const int nh = std::atoi(e);
+    for (int nsw : {2, 3, 4})
+      if ((nh == 1 || nh == 2 || nh == 4) && nh * nsw * 8 >= Nn) {
+        bnh = nh;
+        bnsw = nsw;
+        best_np = nh * nsw * 8;
+        break;
+      }
+  }
+  if (!bnh) return false;
+  L.Kp = static_cast<int>(round_up(m->ranks[0], 4));
+  L.Mout = Nn;
+  L.kr_np = best_np;
+  L.nh = bnh;
+  L.nsw = bnsw;
+  int optin = 0, per_sm = 0;
+  FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  FSTK_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device));
+  double best = -1;
+  for (int ns = 2; ns <= 6; ++ns) {
+    KRParams P{};
+    P.d = m->d;
+    for (int k = 0; k < m->d; ++k) P.r[k] = static_cast<int>(m->ranks[k]);
+    P.Kp = L.Kp;
+    P.Np = L.kr_np;
+    P.nstage = ns;
+    const KRSmem S = kr_smem(P, 64, L.nh);
+    if (S.total > static_cast<uint32_t>(optin)) continue;
+    const int ctas = std::min<int>(per_sm / static_cast<int>(S.total + 1024), 4);
+    if (ctas < 1) continue;
+    const int warps = ctas * 2 * L.nh;
+    const double score =
+        std::min(warps, 16) * 100.0 + std::min(ctas, 3) * 50.0 + std::min(ns, 4) * 10.0;
+    if (score > best) {
+      best = score;
+      L.nstage = ns;
+      L.smem = S.total;
+      L.ctas_per_sm = ctas;
+    }
+  }
+  if (best < 0) return false;
+  L.kr = true;
+  L.fast = true;
+  L.tp = 64;
+  m->rp[0] = L.Kp;
+  m->rp[1] = static_cast<int>(m->ranks[1]);
+  return true;
+}
+
 static void plan_layout(fstk_gpu_model* m) {
   ContractLayout& L = m->lay;
   L = ContractLayout{};
   for (int k = 0; k < m->d; ++k) m->rp[k] = static_cast<int>(m->ranks[k]);
   if (m->d < 2) return;
+  if (plan_kr(m)) return;
+  L = ContractLayout{};
   const int r0 = static_cast<int>(m->ranks[0]), r1 = static_cast<int>(m->ranks[1]);
   L.Kp = static_cast<int>(round_up(r0, 4));
   const int r1p = static_cast<int>(round_up(r1, 16));
@@ -717,6 +1069,26 @@ static void pack_core_into(const fstk_gpu_model* m, const double* core, DevBuf<d
   const ContractLayout& L = m->lay;
   if (!L.fast) return;
   const int r0 = static_cast<int>(m->ranks[0]), r1 = static_cast<int>(m->ranks[1]);
+  if (L.kr) {
+    // [j1][ks][nsub][lane]: G[k = 4 ks + lane%4, j1, n = 8 nsub + lane/4]
+    const int NSB = L.kr_np / 8;
+    const int64_t tile = static_cast<int64_t>(L.Kp) * L.kr_np;
+    std::vector<double> bp(static_cast<size_t>(r1 * tile), 0.0);
+    for (int j1 = 0; j1 < r1; ++j1)
+      for (int ks = 0; ks < L.Kp / 4; ++ks)
+        for (int ns = 0; ns < NSB; ++ns)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int k = 4 * ks + (lane & 3);
+            const int nn = 8 * ns + (lane >> 2);
+            double v = 0.0;
+            if (k < r0 && nn < L.Mout)
+              v = core[static_cast<size_t>(k + static_cast<int64_t>(r0) * (j1 + static_cast<int64_t>(r1) * nn))];
+            bp[static_cast<size_t>(j1 * tile + (ks * NSB + ns) * 32 + lane)] = v;
+          }
+    out.alloc(bp.size());
+    FSTK_CUDA(cudaMemcpy(out.p, bp.data(), bp.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return;
+  }
   const int NS = L.N1p / 8;
   const int64_t NT = static_cast<int64_t>(L.NC) * L.Mout;
   std::vector<double> bp(static_cast<size_t>(NT * L.btile_elems), 0.0);

@@ -77,6 +77,8 @@ struct ContractLayout {
   int Mout = 0;        // prod_{k>=2} r_k
   int nsw = 0;         // 8-column subtiles per warp = N1p / (8 nh)
   int nh = 2;          // column groups per 32-point group
+  bool kr = false;     // Khatri-Rao form (K = r0 r1, one epilogue per tile)
+  int kr_np = 0;       // padded N = prod_{k>=2} r_k of the KR form
   int nstage = 0;      // B pipeline depth
   int tp = 128;        // points per CTA tile (64 or 128)
   int ctas_per_sm = 1; // resident CTAs per SM at this shared-memory footprint
