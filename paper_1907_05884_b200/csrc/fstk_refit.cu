@@ -299,7 +299,7 @@ __device__ __forceinline__ void radix_round(typename std::conditional<REAL, doub
   }
 }
 
-template <bool REAL, int G>
+template <bool REAL, int G, int DT>  // DT: mode count when known at compile time (0 = runtime)
 __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParams P, int ncols_batch) {
   using T = typename std::conditional<REAL, double, double2>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
     __syncthreads();
     // ---- load (generate the design column on the fly in the first pass)
     if (P.src == SRC_BUFFER) {
+#pragma unroll 4
       for (int e = threadIdx.x; e < nel; e += blockDim.x) {
         const int64_t p = base + (e % G) + static_cast<int64_t>(e / G) * stride;
         if constexpr (REAL)
@@ -335,19 +336,21 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
           x[spad(e)] = P.cbuf[static_cast<int64_t>(cc) * P.n + p];
       }
     } else {
-      const double* tc[kMaxOrder];
+      constexpr int NTC = DT > 0 ? DT : kMaxOrder;
+      const double* tc[NTC];
       const bool design = col < P.R;
       if (design && P.src == SRC_TABLES) {
         int64_t rem = col;
 #pragma unroll
-        for (int k = 0; k < kMaxOrder; ++k) {
-          if (k < P.d) {
+        for (int k = 0; k < NTC; ++k) {
+          if (DT > 0 || k < P.d) {
             const int64_t jk = rem % P.r[k];
             rem /= P.r[k];
             tc[k] = P.tables + P.toff.v[k] + jk * P.ldt;
           }
         }
       }
+#pragma unroll 4
       for (int e = threadIdx.x; e < nel; e += blockDim.x) {
         const int64_t p = base + (e % G) + static_cast<int64_t>(e / G) * stride;
         double v = 0.0;
@@ -357,8 +360,8 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
           // three independent loads, no gather.
           v = tc[0][p];
 #pragma unroll
-          for (int k = 1; k < kMaxOrder; ++k)
-            if (k < P.d) v = xmul(v, tc[k][p]);
+          for (int k = 1; k < NTC; ++k)
+            if (DT > 0 || k < P.d) v = xmul(v, tc[k][p]);
         } else {
           const int64_t src = P.row_src[p];
           if (src >= 0) v = xmul(P.sgn[p], design ? P.dense[src + P.ldd * col] : P.rhs[src]);
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
       __syncthreads();
     }
     // ---- store
+#pragma unroll 4
     for (int e = threadIdx.x; e < nel; e += blockDim.x) {
       const int64_t p = base + (e % G) + static_cast<int64_t>(e / G) * stride;
       if (!P.last) {
@@ -499,14 +503,17 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
   }
   static std::once_flag attr_once[64];
   std::call_once(attr_once[device & 63], [&] {
-    FSTK_CUDA(cudaFuncSetAttribute(transform_pass2_kernel<false, 1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
-    FSTK_CUDA(cudaFuncSetAttribute(transform_pass2_kernel<true, 1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
-    FSTK_CUDA(cudaFuncSetAttribute(transform_pass2_kernel<false, 2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
-    FSTK_CUDA(cudaFuncSetAttribute(transform_pass2_kernel<true, 2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+    auto attr = [](const void* f) {
+      FSTK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+    };
+    attr(reinterpret_cast<const void*>(transform_pass2_kernel<false, 1, 0>));
+    attr(reinterpret_cast<const void*>(transform_pass2_kernel<true, 1, 0>));
+    attr(reinterpret_cast<const void*>(transform_pass2_kernel<false, 1, 3>));
+    attr(reinterpret_cast<const void*>(transform_pass2_kernel<true, 1, 3>));
+    attr(reinterpret_cast<const void*>(transform_pass2_kernel<false, 1, 4>));
+    attr(reinterpret_cast<const void*>(transform_pass2_kernel<true, 1, 4>));
+    attr(reinterpret_cast<const void*>(transform_pass2_kernel<false, 2, 0>));
+    attr(reinterpret_cast<const void*>(transform_pass2_kernel<true, 2, 0>));
   });
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -564,14 +571,29 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
                                                                     ceil_div(bc, cpc), ceil_div(int64_t(sms) * 8, sets))));
       dim3 grid(static_cast<unsigned>(sets), static_cast<unsigned>(gy));
       ProfScope prof(FSTK_PROF_TRANSFORM, s);
-      if (real && P.G == 1)
-        transform_pass2_kernel<true, 1><<<grid, 256, smem, s>>>(P, static_cast<int>(bc));
-      else if (real)
-        transform_pass2_kernel<true, 2><<<grid, 256, smem, s>>>(P, static_cast<int>(bc));
-      else if (P.G == 1)
-        transform_pass2_kernel<false, 1><<<grid, 256, smem, s>>>(P, static_cast<int>(bc));
-      else
-        transform_pass2_kernel<false, 2><<<grid, 256, smem, s>>>(P, static_cast<int>(bc));
+      const int dt = (P.src == SRC_TABLES && (J.d == 3 || J.d == 4)) ? J.d : 0;
+      const int nb = static_cast<int>(bc);
+      if (P.G == 2) {
+        if (real)
+          transform_pass2_kernel<true, 2, 0><<<grid, 256, smem, s>>>(P, nb);
+        else
+          transform_pass2_kernel<false, 2, 0><<<grid, 256, smem, s>>>(P, nb);
+      } else if (dt == 3) {
+        if (real)
+          transform_pass2_kernel<true, 1, 3><<<grid, 256, smem, s>>>(P, nb);
+        else
+          transform_pass2_kernel<false, 1, 3><<<grid, 256, smem, s>>>(P, nb);
+      } else if (dt == 4) {
+        if (real)
+          transform_pass2_kernel<true, 1, 4><<<grid, 256, smem, s>>>(P, nb);
+        else
+          transform_pass2_kernel<false, 1, 4><<<grid, 256, smem, s>>>(P, nb);
+      } else {
+        if (real)
+          transform_pass2_kernel<true, 1, 0><<<grid, 256, smem, s>>>(P, nb);
+        else
+          transform_pass2_kernel<false, 1, 0><<<grid, 256, smem, s>>>(P, nb);
+      }
       check_launch("transform_pass2_kernel");
     }
   }
