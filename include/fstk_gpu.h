@@ -38,8 +38,14 @@ enum {
   FSTK_E_COMPUTE = 7
 };
 
-/* Mixing transforms, fstk::MixingTransform (randls.hpp:13). */
-enum { FSTK_TRANSFORM_DCT = 0, FSTK_TRANSFORM_WHT = 1, FSTK_TRANSFORM_FFT = 2 };
+/* Mixing transforms, fstk::MixingTransform (randls.hpp:13), plus NONE: the
+ * north_star's literal estimator (extension, not in the reference): S of the
+ * Q_w working rows sampled uniformly without replacement from the sketch RNG
+ * stream, scaled by sqrt(Q_w/S), no mixing; A^T A is accumulated from design
+ * rows generated block by block so A is never materialised.  reestimate_core /
+ * refit_* only. */
+enum { FSTK_TRANSFORM_DCT = 0, FSTK_TRANSFORM_WHT = 1, FSTK_TRANSFORM_FFT = 2,
+       FSTK_TRANSFORM_NONE = 3 };
 
 typedef struct fstk_gpu_error {
   int32_t kind;     /* FSTK_E_* or 0 */

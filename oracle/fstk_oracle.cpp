@@ -620,7 +620,7 @@ static constexpr std::uint64_t kValidationTag = 0x76616c69ull;  // :16
 static constexpr std::uint64_t kSubsetTag = 0x73756273ull;      // :17
 static constexpr std::uint64_t kSketchTag = 0x736b6574ull;      // :18
 
-enum Transform { Dct = 0, Wht = 1, Fft = 2 };  // randls.hpp:13
+enum Transform { Dct = 0, Wht = 1, Fft = 2, None = 3 };  // randls.hpp:13 (+ None: extension)
 
 // :21-41. Tables are Q x r_k column-major.
 static std::vector<std::vector<double>> mode_value_tables(const Model& m,
@@ -677,11 +677,31 @@ static SketchPlan make_plan(std::uint64_t q_w, std::uint64_t s,
   return plan;
 }
 
+// Extension (not in the reference; the north_star's literal estimator):
+// transform None samples S of the Q_w working rows uniformly without
+// replacement from Rng(mix_seed(seed, kSketchTag)) and scales them by
+// sqrt(Q_w / S); no mixing.
+static SketchPlan make_plan_none(std::uint64_t q_w, std::uint64_t s, std::uint64_t seed) {
+  SketchPlan plan;
+  plan.q_pad = q_w;
+  require(s >= 1, Parameter, "sample rows must be positive");
+  require(s <= q_w, Parameter, "sample rows exceed the working subset");
+  Rng rng(seed);
+  plan.rows = rng.sample_without_replacement(q_w, s);
+  plan.scale = std::sqrt(static_cast<double>(q_w) / static_cast<double>(s));
+  return plan;
+}
+
 template <typename Getter>
 static void sketch_column(const SketchPlan& plan, int transform,
                           std::uint64_t q_w, Getter&& getter,
                           std::vector<double>& scratch, std::vector<cd>& cscratch,
                           double* out_re, double* out_im) {  // :79-105
+  if (transform == None) {
+    for (std::size_t s = 0; s < plan.rows.size(); ++s)
+      out_re[s] = plan.scale * getter(plan.rows[s]);
+    return;
+  }
   const std::size_t n = plan.q_pad;
   if (transform == Fft) {
     cscratch.assign(n, {0.0, 0.0});
@@ -1063,7 +1083,7 @@ int oracle_refit_sizes(MODEL_ARGS, std::int64_t q, std::uint64_t seed,
         working_subset == 0 ? train : std::min<std::uint64_t>(working_subset, train);
     out->sample_rows = s;
     out->working_rows = q_w;
-    out->padded_rows = next_pow2(q_w);
+    out->padded_rows = transform == None ? q_w : next_pow2(q_w);
     out->n_val = held ? n_val : train;
     out->system_rows = transform == Fft ? 2 * static_cast<std::int64_t>(s)
                                         : static_cast<std::int64_t>(s);
@@ -1093,7 +1113,9 @@ int oracle_refit_system(MODEL_ARGS, const double* pts, const double* vals,
     const auto tables = mode_value_tables(m, ws.train_points.data(),
                                           static_cast<std::int64_t>(ws.q_w));
     // solve_sketched (:315-348)
-    const SketchPlan plan = make_plan(ws.q_w, s, mix_seed(seed, kSketchTag));
+    const SketchPlan plan = transform == None
+                                ? make_plan_none(ws.q_w, s, mix_seed(seed, kSketchTag))
+                                : make_plan(ws.q_w, s, mix_seed(seed, kSketchTag));
     const bool fft = transform == Fft;
     const std::int64_t s_rows = static_cast<std::int64_t>(plan.rows.size());
     const std::int64_t lda = fft ? 2 * s_rows : s_rows;

@@ -27,7 +27,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 _REF = None
 
-TRANSFORMS = {"dct": 0, "wht": 1, "fft": 2}
+TRANSFORMS = {"dct": 0, "wht": 1, "fft": 2, "none": 3}
 KINDS = ["Parameter", "Shape", "Domain", "Data", "Io", "Decode", "Compute"]
 
 

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfstk_gpu.so")
 
 KINDS = ["Parameter", "Shape", "Domain", "Data", "Io", "Decode", "Compute"]
-TRANSFORMS = {"dct": 0, "wht": 1, "fft": 2}
+TRANSFORMS = {"dct": 0, "wht": 1, "fft": 2, "none": 3}
 
 
 class FstkError(Exception):

@@ -123,6 +123,20 @@ static Plan make_plan(uint64_t q_w, uint64_t s, uint64_t seed, bool sample = tru
   return plan;
 }
 
+// Extension (north_star literal estimator, not in the reference): S of the Q_w
+// working rows sampled uniformly without replacement from the sketch stream,
+// scaled by sqrt(Q_w / S), no mixing.  Bit-identical to oracle/fstk_oracle.cpp.
+static Plan make_plan_none(uint64_t q_w, uint64_t s, uint64_t seed) {
+  Plan plan;
+  plan.q_pad = q_w;
+  require(s >= 1, FSTK_E_PARAMETER, "sample rows must be positive");
+  require(s <= q_w, FSTK_E_PARAMETER, "sample rows exceed the working subset");
+  Rng rng(seed);
+  plan.rows = rng.sample_without_replacement(q_w, s);
+  plan.scale = std::sqrt(static_cast<double>(q_w) / static_cast<double>(s));
+  return plan;
+}
+
 // ------------------------------------------------------ twiddle replay ---
 // For stage len = 2^(s+1) the reference forms wlen = (cos, sin)(-2 pi / len)
 // and multiplies w *= wlen once per butterfly (transforms.cpp:36-46).  The
@@ -423,6 +437,39 @@ __global__ void fold_sign_kernel(double* __restrict__ t0, int64_t ldt, int r0,
   if (i >= n) return;
   const double s = sgn[i];
   for (int j = 0; j < r0; ++j) t0[j * ldt + i] = xmul(s, t0[j * ldt + i]);
+}
+
+// transform = none (north_star K5): rows of A generated on the fly from the
+// mode tables of the sampled points, block by block, so A never exists whole.
+// W[i, ell] = scale * ((u0 u1) u2 ...)[row0 + i] (design_column order,
+// randls.cpp:44-52, then plan.scale as sketch_column applies it).
+template <int DT>
+__global__ void __launch_bounds__(256) design_block_kernel(
+    const double* __restrict__ tables, Int64x8 toff, int64_t ldt, int d, Int64x8 ranks,
+    int64_t row0, int64_t nrows, int64_t R, double scale, double* __restrict__ W, int64_t ldw) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  constexpr int NTC = DT > 0 ? DT : kMaxOrder;
+  for (int64_t ell = blockIdx.y; ell < R; ell += gridDim.y) {
+    if (i >= nrows) continue;
+    int64_t rem = ell;
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < NTC; ++k) {
+      if (DT > 0 || k < d) {
+        const int64_t jk = rem % ranks.v[k];
+        rem /= ranks.v[k];
+        const double u = tables[toff.v[k] + jk * ldt + row0 + i];
+        v = k == 0 ? u : xmul(v, u);
+      }
+    }
+    W[ell * ldw + i] = xmul(scale, v);
+  }
+}
+
+__global__ void scaled_gather_kernel(const double* __restrict__ vals, const int64_t* __restrict__ src,
+                                     int64_t n, double scale, double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = xmul(scale, vals[src[i]]);
 }
 
 __global__ void finite_check_kernel(const double* __restrict__ a, int64_t n, int* flag) {
@@ -815,6 +862,11 @@ struct fstk_gpu_refit {
   bool factored = false;
   bool rank_def = false;
   DevBuf<double> tmp_r;   // local residual rows
+  // transform = none: mode tables of this shard's sampled rows (A generated on demand)
+  bool none = false;
+  DevBuf<double> tables;
+  int64_t toff[kMaxOrder] = {0};
+  int64_t ldt = 0;
   ~fstk_gpu_refit() {
     if (stream) cudaStreamDestroy(stream);
   }
@@ -846,8 +898,8 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     require(m && points && values && cfg && out, FSTK_E_PARAMETER, "null argument");
     *out = nullptr;
     require(shards >= 1 && shard >= 0 && shard < shards, FSTK_E_PARAMETER, "bad shard");
-    require(cfg->transform >= 0 && cfg->transform <= 2, FSTK_E_PARAMETER,
-            "transform must be dct, wht, or fft");
+    require(cfg->transform >= 0 && cfg->transform <= 3, FSTK_E_PARAMETER,
+            "transform must be dct, wht, fft or none");
     // PointCloud::from_data (ingest.cpp:19-31) validation happens first.
     require(d >= 1 && d <= kMaxOrder, FSTK_E_SHAPE, "point cloud dimension must be in [1, 8]");
     require(q >= 1, FSTK_E_DATA, "point cloud is empty");
@@ -926,8 +978,10 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     }
     rf->q_w = q_w;
     rf->S = S;
+    rf->none = cfg->transform == FSTK_TRANSFORM_NONE;
     // solve_sketched (randls.cpp:318): plan seeded with mix_seed(seed, kSketchTag).
-    rf->plan = make_plan(q_w, S, mix_seed(cfg->seed, kSketchTag));
+    rf->plan = rf->none ? make_plan_none(q_w, S, mix_seed(cfg->seed, kSketchTag))
+                        : make_plan(q_w, S, mix_seed(cfg->seed, kSketchTag));
     rf->q_pad = rf->plan.q_pad;
     require(rf->q_pad < (uint64_t(1) << 31), FSTK_E_PARAMETER, "working subset too large");
     // Validation points/values on the device.
@@ -950,12 +1004,56 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
                                 cudaMemcpyDeviceToHost, s));
       FSTK_CUDA(cudaStreamSynchronize(s));
     }
-    // Inputs in transform order; destination rows in last-pass visit order.
-    build_inputs(cfg->transform, rf->q_pad, q_w, rf->plan.signs, rf->plan.rows, false, subset,
-                 true, rf->in, s);
     rf->row_lo = static_cast<int64_t>(S) * shard / shards;
     rf->row_hi = static_cast<int64_t>(S) * (shard + 1) / shards;
     rf->local_rows = rf->row_hi - rf->row_lo;
+    if (rf->none) {
+      // Tables and rhs of this shard's sampled rows only; A is generated on demand.
+      const int64_t nl = rf->local_rows;
+      std::vector<int64_t> src(static_cast<size_t>(std::max<int64_t>(nl, 1)));
+      for (int64_t i = 0; i < nl; ++i) src[i] = subset[rf->plan.rows[rf->row_lo + i]];
+      DevBuf<int64_t> dsrc(src.size());
+      FSTK_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), src.size() * 8, cudaMemcpyHostToDevice, s));
+      rf->ldt = round_up(std::max<int64_t>(nl, 1), 128);
+      int64_t tot = 0;
+      for (int k = 0; k < d; ++k) {
+        rf->toff[k] = tot;
+        tot += m->ranks[k] * rf->ldt;
+      }
+      rf->tables.alloc(static_cast<size_t>(tot));
+      DevBuf<unsigned long long> derr(1);
+      FSTK_CUDA(cudaMemsetAsync(derr.p, 0xff, 8, s));
+      launch_mode_tables(m, rf->d_points.p, q, nl, rf->ldt, dsrc.p, rf->tables.p, rf->toff,
+                         rf->ldt, true, derr.p, s);
+      rf->b.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)));
+      if (nl > 0) {
+        scaled_gather_kernel<<<static_cast<unsigned>(ceil_div(nl, 256)), 256, 0, s>>>(
+            rf->d_values.p, dsrc.p, nl, rf->plan.scale, rf->b.p);
+        check_launch("scaled_gather_kernel");
+      }
+      unsigned long long bad = 0;
+      FSTK_CUDA(cudaMemcpyAsync(&bad, derr.p, 8, cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));
+      if (bad != ULLONG_MAX) {
+        const int64_t row = src[bad];
+        std::vector<double> y(d);
+        for (int k = 0; k < d; ++k) y[k] = points[k * q + row];
+        throw_domain(m, row, y.data());
+      }
+      if (info) {
+        info->t_prepare = tprep.seconds();
+        info->t_sketch = 0.0;
+        info->sample_rows = S;
+        info->working_rows = q_w;
+        info->padded_rows = rf->q_pad;
+        info->held_out = rf->held_out ? 1 : 0;
+      }
+      *out = rf.release();
+      return;
+    }
+    // Inputs in transform order; destination rows in last-pass visit order.
+    build_inputs(cfg->transform, rf->q_pad, q_w, rf->plan.signs, rf->plan.rows, false, subset,
+                 true, rf->in, s);
     // Mode tables over the padded positions, bit-exact (mode_value_tables, randls.cpp:21-41).
     int64_t toff[kMaxOrder], tot = 0;
     const int64_t ldt = static_cast<int64_t>(rf->q_pad);
@@ -1036,6 +1134,63 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
   });
 }
 
+namespace fstk_gpu {
+
+// gram(lower) = beta * gram + A^T A for A (rows x n, lda): column-blocked
+// DSYRK on the diagonal blocks + one DGEMM per block row below it.
+static void gram_accumulate(cublasHandle_t h, const double* A, int lda, int rows, int n,
+                            double* gram, double beta) {
+  const double one = 1.0;
+  const int nb = n >= 4096 ? 8 : 1;
+  for (int bi = 0; bi < nb; ++bi) {
+    const int i0 = static_cast<int>(static_cast<int64_t>(n) * bi / nb);
+    const int i1 = static_cast<int>(static_cast<int64_t>(n) * (bi + 1) / nb);
+    if (cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, i1 - i0, rows, &one,
+                    A + static_cast<int64_t>(lda) * i0, lda, &beta,
+                    gram + static_cast<int64_t>(n) * i0 + i0, n) != CUBLAS_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "cublasDsyrk failed");
+    count_launch();
+    if (i0 > 0) {
+      if (cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, i1 - i0, i0, rows, &one,
+                      A + static_cast<int64_t>(lda) * i0, lda, A, lda, &beta, gram + i0,
+                      n) != CUBLAS_STATUS_SUCCESS)
+        fail(FSTK_E_COMPUTE, "cublasDgemm failed");
+      count_launch();
+    }
+  }
+}
+
+// Rows per generated block of A for transform = none (about 1 GB of fp64).
+static int64_t none_block_rows(const fstk_gpu_refit* rf) {
+  const int64_t cap = std::max<int64_t>(1024, (int64_t(1) << 27) / std::max<int64_t>(rf->R, 1));
+  return std::min<int64_t>(round_up(cap, 128), std::max<int64_t>(rf->local_rows, 1));
+}
+
+static void generate_design_block(const fstk_gpu_refit* rf, int64_t row0, int64_t nrows,
+                                  double* W, int64_t ldw, cudaStream_t s) {
+  const fstk_gpu_model* m = rf->model;
+  Int64x8 to{}, rk{};
+  for (int k = 0; k < m->d; ++k) {
+    to.v[k] = rf->toff[k];
+    rk.v[k] = m->ranks[k];
+  }
+  dim3 grid(static_cast<unsigned>(ceil_div(nrows, 256)),
+            static_cast<unsigned>(std::min<int64_t>(rf->R, 4096)));
+  ProfScope prof(FSTK_PROF_TRANSFORM, s);
+  if (m->d == 3)
+    design_block_kernel<3><<<grid, 256, 0, s>>>(rf->tables.p, to, rf->ldt, m->d, rk, row0, nrows,
+                                                rf->R, rf->plan.scale, W, ldw);
+  else if (m->d == 4)
+    design_block_kernel<4><<<grid, 256, 0, s>>>(rf->tables.p, to, rf->ldt, m->d, rk, row0, nrows,
+                                                rf->R, rf->plan.scale, W, ldw);
+  else
+    design_block_kernel<0><<<grid, 256, 0, s>>>(rf->tables.p, to, rf->ldt, m->d, rk, row0, nrows,
+                                                rf->R, rf->plan.scale, W, ldw);
+  check_launch("design_block_kernel");
+}
+
+}  // namespace fstk_gpu
+
 int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
                                         fstk_reestimate_info* info, fstk_gpu_error* err) {
   return guarded(err, [&] {
@@ -1057,30 +1212,32 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double
       // is split into nb column blocks: block row i below the diagonal is one
       // DGEMM A_i^T [A_0 .. A_{i-1}] and each diagonal block one DSYRK, so
       // (nb-1)/nb of the flops run in large GEMMs.
-      ProfScope prof(FSTK_PROF_GRAM, s);
-      const int nb = n >= 4096 ? 8 : 1;
-      const int lda = static_cast<int>(arows);
-      for (int bi = 0; bi < nb; ++bi) {
-        const int i0 = static_cast<int>(static_cast<int64_t>(n) * bi / nb);
-        const int i1 = static_cast<int>(static_cast<int64_t>(n) * (bi + 1) / nb);
-        if (cublasDsyrk(h.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, i1 - i0, lda, &one,
-                        rf->A.p + static_cast<int64_t>(lda) * i0, lda, &zero,
-                        gram + static_cast<int64_t>(n) * i0 + i0, n) != CUBLAS_STATUS_SUCCESS)
-          fail(FSTK_E_COMPUTE, "cublasDsyrk failed");
-        count_launch();
-        if (i0 > 0) {
-          // G[i0:i1, 0:i0] = A[:, i0:i1]^T A[:, 0:i0]
-          if (cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, i1 - i0, i0, lda, &one,
-                          rf->A.p + static_cast<int64_t>(lda) * i0, lda, rf->A.p, lda, &zero,
-                          gram + i0, n) != CUBLAS_STATUS_SUCCESS)
-            fail(FSTK_E_COMPUTE, "cublasDgemm failed");
+      if (rf->none) {
+        // A^T A accumulated over generated row blocks (A never materialised).
+        const int64_t BS = none_block_rows(rf);
+        DevBuf<double> W(static_cast<size_t>(BS) * rf->R);
+        for (int64_t r0 = 0; r0 < arows; r0 += BS) {
+          const int64_t nb_rows = std::min(BS, arows - r0);
+          generate_design_block(rf, r0, nb_rows, W.p, BS, s);
+          ProfScope prof(FSTK_PROF_GRAM, s);
+          const double beta = r0 == 0 ? 0.0 : 1.0;
+          gram_accumulate(h.blas, W.p, static_cast<int>(BS), static_cast<int>(nb_rows), n, gram, beta);
+          if (cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(nb_rows), n, &one, W.p,
+                          static_cast<int>(BS), rf->b.p + r0, 1, &beta, rhs, 1) !=
+              CUBLAS_STATUS_SUCCESS)
+            fail(FSTK_E_COMPUTE, "cublasDgemv failed");
           count_launch();
         }
+        FSTK_CUDA(cudaStreamSynchronize(s));
+      } else {
+        ProfScope prof(FSTK_PROF_GRAM, s);
+        gram_accumulate(h.blas, rf->A.p, static_cast<int>(arows), static_cast<int>(arows), n, gram,
+                        0.0);
+        if (cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(arows), n, &one, rf->A.p,
+                        static_cast<int>(arows), rf->b.p, 1, &zero, rhs, 1) != CUBLAS_STATUS_SUCCESS)
+          fail(FSTK_E_COMPUTE, "cublasDgemv failed");
+        count_launch();
       }
-      if (cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(arows), n, &one, rf->A.p,
-                      static_cast<int>(arows), rf->b.p, 1, &zero, rhs, 1) != CUBLAS_STATUS_SUCCESS)
-        fail(FSTK_E_COMPUTE, "cublasDgemv failed");
-      count_launch();
     }
     const double t = tg.seconds();
     if (info) info->t_gram = t;
@@ -1216,6 +1373,26 @@ int32_t fstk_gpu_refit_correction(fstk_gpu_refit* rf, const double* x_dev, doubl
     rf->tmp_r.ensure(static_cast<size_t>(arows));
     FSTK_CUDA(cudaMemcpyAsync(rf->tmp_r.p, rf->b.p, arows * 8, cudaMemcpyDeviceToDevice, s));
     const double one = 1.0, mone = -1.0, zero = 0.0;
+    if (rf->none) {
+      const int64_t BS = none_block_rows(rf);
+      DevBuf<double> W(static_cast<size_t>(BS) * rf->R);
+      for (int64_t r0 = 0; r0 < arows; r0 += BS) {
+        const int64_t nb_rows = std::min(BS, arows - r0);
+        generate_design_block(rf, r0, nb_rows, W.p, BS, s);
+        ProfScope prof(FSTK_PROF_SOLVE, s);
+        const double beta = r0 == 0 ? 0.0 : 1.0;
+        if (cublasDgemv(h.blas, CUBLAS_OP_N, static_cast<int>(nb_rows), n, &mone, W.p,
+                        static_cast<int>(BS), x_dev, 1, &one, rf->tmp_r.p + r0, 1) !=
+                CUBLAS_STATUS_SUCCESS ||
+            cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(nb_rows), n, &one, W.p,
+                        static_cast<int>(BS), rf->tmp_r.p + r0, 1, &beta, s_dev, 1) !=
+                CUBLAS_STATUS_SUCCESS)
+          fail(FSTK_E_COMPUTE, "cublasDgemv failed");
+        count_launch(2);
+      }
+      FSTK_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
     ProfScope prof(FSTK_PROF_SOLVE, s);
     if (cublasDgemv(h.blas, CUBLAS_OP_N, static_cast<int>(arows), n, &mone, rf->A.p,
                     static_cast<int>(arows), x_dev, 1, &one, rf->tmp_r.p, 1) != CUBLAS_STATUS_SUCCESS)
@@ -1359,6 +1536,15 @@ int32_t fstk_gpu_refit_sketched(const fstk_gpu_refit* rf, double* a, double* b, 
     if (rows_local) *rows_local = arows;
     if (!a && !b) return;
     DeviceGuard dg(rf->device);
+    if (rf->none) {
+      // Rows are already in plan order (sorted sampled rows of this shard).
+      DevBuf<double> W(static_cast<size_t>(std::max<int64_t>(arows, 1)) * rf->R);
+      if (arows > 0) generate_design_block(rf, 0, arows, W.p, arows, rf->stream);
+      FSTK_CUDA(cudaStreamSynchronize(rf->stream));
+      if (a) FSTK_CUDA(cudaMemcpy(a, W.p, static_cast<size_t>(arows) * rf->R * 8, cudaMemcpyDeviceToHost));
+      if (b) FSTK_CUDA(cudaMemcpy(b, rf->b.p, arows * 8, cudaMemcpyDeviceToHost));
+      return;
+    }
     std::vector<double> ha(static_cast<size_t>(arows) * rf->R), hb(arows);
     FSTK_CUDA(cudaMemcpy(ha.data(), rf->A.p, ha.size() * 8, cudaMemcpyDeviceToHost));
     FSTK_CUDA(cudaMemcpy(hb.data(), rf->b.p, hb.size() * 8, cudaMemcpyDeviceToHost));
@@ -1460,7 +1646,7 @@ static int32_t sketch_dense(const double* w, const double* u, int64_t q, int64_t
     require(w && cfg, FSTK_E_PARAMETER, "null argument");
     require(q >= 1, FSTK_E_PARAMETER, mixed ? "empty matrix" : "empty system");
     require(cfg->transform >= 0 && cfg->transform <= 2, FSTK_E_PARAMETER,
-            "transform must be dct, wht, or fft");
+            "transform must be dct, wht, or fft");  // 'none' is a reestimate_core option only
     int dev = 0;
     FSTK_CUDA(cudaGetDevice(&dev));
     const uint64_t S = mixed ? 0 : resolve_sample_rows(cfg->sample_rows, r);

@@ -19,7 +19,7 @@ def sketch_config(seed=0, sample_rows=0, working_subset=1 << 20, transform="dct"
                   validation_fraction=0.05) -> SketchCfg:
     """module.cpp:83-102 (sketch_from_kwargs)."""
     if transform not in TRANSFORMS:
-        raise make_error(1, "transform must be dct, wht, or fft")
+        raise make_error(1, "transform must be dct, wht, fft or none")
     return SketchCfg(int(seed), int(working_subset), int(sample_rows), TRANSFORMS[transform],
                      float(validation_fraction))
 

@@ -267,3 +267,39 @@ def test_self_convergence(O):                        # test_randls.cpp:324-355
         F.self_convergence(m, pts, vals, [64])
     with pytest.raises(ValueError):
         F.self_convergence(m, pts, vals, [64, 32])
+
+
+# --------------------------------------- transform = none (north_star K5) ---
+@pytest.mark.parametrize("q,ranks,wsub,s", [(20_000, (4, 3, 2), 1 << 20, 0), (9_000, (3, 3, 2, 2), 6000, 500),
+                                            (50_000, (6, 5, 4), 30_000, 4000)])
+def test_none_transform_parity(O, q, ranks, wsub, s):
+    """Uniformly sampled design rows (no mixing), A generated block by block:
+    sampled rows and A/b bit-exact against the oracle extension, core 1e-9."""
+    m = synth.random_model(ranks, [6] * len(ranks), 4, seed=3)
+    pts, vals = _data(O, m, q, 4)
+    sess = F.RefitSession(m, pts, vals, seed=17, transform="none", working_subset=wsub,
+                          sample_rows=s)
+    a, b = sess.sketched()
+    ao, bo, rows_o, _, _ = O.refit_system(m, pts, vals, seed=17, transform="none",
+                                          working_subset=wsub, sample_rows=s)
+    assert np.array_equal(sess.rows(), rows_o)
+    assert np.array_equal(a, ao) and np.array_equal(b, bo)
+    sess.close()
+    new, info = F.reestimate_core(m, pts, vals, seed=17, transform="none", working_subset=wsub,
+                                  sample_rows=s)
+    core_o, info_o = O.reestimate_core(m, pts, vals, seed=17, transform="none",
+                                       working_subset=wsub, sample_rows=s)
+    assert rel(new.core.reshape(-1, order="F"), core_o) <= CORE_TOL
+    assert info["padded_rows"] == info_o["padded_rows"]
+
+
+def test_none_transform_recovers_planted_core(O):
+    m = legendre_model((2, 3, 2), 89)
+    planted = m.core + 0.5 * np.random.default_rng(97).normal(size=m.core.shape)
+    pts = random_points(4000, 3, 101)
+    new, _ = F.reestimate_core(m, pts, O.evaluate_batch(m.with_core(planted), pts), seed=23,
+                               sample_rows=48, transform="none")
+    assert rel(new.core, planted) <= 1e-10
+    with pytest.raises(ValueError):   # S > Q_w
+        F.reestimate_core(m, pts[:100], O.evaluate_batch(m, pts[:100]), sample_rows=99,
+                          transform="none")
