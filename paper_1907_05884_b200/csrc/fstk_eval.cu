@@ -1032,8 +1032,11 @@ static void plan_layout(fstk_gpu_model* m) {
   FSTK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   FSTK_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device));
   double best = -1;
+  const int force_ns = std::getenv("FSTK_CONTRACT_NSTAGE") ? std::atoi(std::getenv("FSTK_CONTRACT_NSTAGE")) : 0;
+  const int force_ctas = std::getenv("FSTK_CONTRACT_CTAS") ? std::atoi(std::getenv("FSTK_CONTRACT_CTAS")) : 0;
   for (int tp : {64, 128}) {
     for (int ns = 2; ns <= 6; ++ns) {
+      if (force_ns && ns != force_ns) continue;
       ContractParams P{};
       P.d = m->d;
       for (int k = 0; k < m->d; ++k) P.r[k] = static_cast<int>(m->ranks[k]);
@@ -1044,7 +1047,8 @@ static void plan_layout(fstk_gpu_model* m) {
       P.nstage = ns;
       const SmemLayout S = smem_layout(P, tp);
       if (S.total > static_cast<uint32_t>(optin)) continue;
-      const int ctas = std::min<int>(per_sm / static_cast<int>(S.total + 1024), 4);
+      int ctas = std::min<int>(per_sm / static_cast<int>(S.total + 1024), 4);
+      if (force_ctas) ctas = std::min(ctas, force_ctas);
       if (ctas < 1) continue;
       const int warps = ctas * (tp / 32 * L.nh);
       const double score =
@@ -1063,6 +1067,9 @@ static void plan_layout(fstk_gpu_model* m) {
     m->rp[0] = L.Kp;
     m->rp[1] = L.NC * L.N1p;
   }
+  if (std::getenv("FSTK_DEBUG_LAYOUT"))
+    std::fprintf(stderr, "fstk layout: tp=%d nstage=%d ctas/sm=%d nh=%d nsw=%d smem=%zu kr=%d\n",
+                 L.tp, L.nstage, L.ctas_per_sm, L.nh, L.nsw, L.smem, L.kr ? 1 : 0);
 }
 
 static void pack_core_into(const fstk_gpu_model* m, const double* core, DevBuf<double>& out) {
