@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfstk_gpu.so")
+LIB_PATH = os.environ.get("FSTK_GPU_LIB") or os.path.join(HERE, "libfstk_gpu.so")
 
 KINDS = ["Parameter", "Shape", "Domain", "Data", "Io", "Decode", "Compute"]
 TRANSFORMS = {"dct": 0, "wht": 1, "fft": 2, "none": 3}

@@ -128,72 +128,116 @@ __global__ void __launch_bounds__(128) mode_tables_kernel(
 // leaves every partial sum unchanged, so with EXACT (separate multiply/add)
 // this reproduces the reference's sparse dot (model.cpp:86-88) bit for bit
 // whenever the indices are strictly increasing (format.md:67).
+// PPT points per thread (rows i and i + 128): one broadcast coefficient load
+// then feeds 2*PPT independent FMAs, which keeps the shared-memory (MIO) queue
+// off the critical path.
+template <bool EXACT, int JC>
+struct DensePPT {
+  static constexpr int value = JC <= 32 ? 2 : 1;
+};
+
 template <bool EXACT, int JC>
 __global__ void __launch_bounds__(128) mode_dense_kernel(
     ModeDev md, const double* __restrict__ xs, int64_t n, int64_t n_out,
     const int64_t* __restrict__ row_src, double* __restrict__ tk, int64_t ldt,
     unsigned long long* err_row) {
+  constexpr int PPT = DensePPT<EXACT, JC>::value;
   extern __shared__ __align__(16) double Cs[];  // (pmax+1) x JC
   const int j0 = blockIdx.y * JC;
   const int p = md.pmax;
   for (int e = threadIdx.x; e < (p + 1) * JC; e += blockDim.x)
     Cs[e] = md.dense[(e / JC) * md.ldc + j0 + (e % JC)];
   __syncthreads();
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n_out) return;
-  int64_t src = i;
-  bool valid = i < n;
-  if (row_src) {
-    src = i < n ? row_src[i] : -1;
-    valid = src >= 0;
-  }
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * (128 * PPT) + threadIdx.x;
   const int jn = min(JC, md.r - j0);
-  if (!valid) {
+  double t[PPT];
+  bool live[PPT];
 #pragma unroll
-    for (int j = 0; j < JC; ++j)
-      if (j < jn) tk[(j0 + j) * ldt + i] = 0.0;
-    return;
-  }
-  const double x = xs[src];
-  double t;
-  if (!(x >= md.lo - md.slack && x <= md.hi + md.slack)) {
-    atomicMin(err_row, static_cast<unsigned long long>(i));
-    t = 0.0;
-  } else {
-    const double cl = fmin(md.hi, fmax(md.lo, x));
-    t = xadd(-1.0, __ddiv_rn(xmul(2.0, xsub(cl, md.lo)), md.span));
-  }
-  double acc[JC];
+  for (int u = 0; u < PPT; ++u) {
+    const int64_t i = base + u * 128;
+    live[u] = i < n_out;
+    t[u] = 0.0;
+    if (!live[u]) continue;
+    int64_t src = i;
+    bool valid = i < n;
+    if (row_src) {
+      src = i < n ? row_src[i] : -1;
+      valid = src >= 0;
+    }
+    if (!valid) {
 #pragma unroll
-  for (int j = 0; j < JC; ++j) acc[j] = 0.0;
-  auto apply = [&](const double* row, double L) {
+      for (int j = 0; j < JC; ++j)
+        if (j < jn) tk[(j0 + j) * ldt + i] = 0.0;
+      live[u] = false;
+      continue;
+    }
+    const double x = xs[src];
+    if (!(x >= md.lo - md.slack && x <= md.hi + md.slack)) {
+      atomicMin(err_row, static_cast<unsigned long long>(i));
+    } else {
+      const double cl = fmin(md.hi, fmax(md.lo, x));
+      t[u] = xadd(-1.0, __ddiv_rn(xmul(2.0, xsub(cl, md.lo)), md.span));
+    }
+  }
+  if (PPT == 1 ? !live[0] : !(live[0] || live[PPT - 1])) return;
+  double acc[PPT][JC];
+#pragma unroll
+  for (int u = 0; u < PPT; ++u)
+#pragma unroll
+    for (int j = 0; j < JC; ++j) acc[u][j] = 0.0;
+  auto apply = [&](const double* row, const double (&L)[PPT]) {
     const double2* r2 = reinterpret_cast<const double2*>(row);
 #pragma unroll
     for (int j = 0; j < JC / 2; ++j) {
       const double2 c = r2[j];
-      if (EXACT) {
-        acc[2 * j] = xadd(acc[2 * j], xmul(c.x, L));
-        acc[2 * j + 1] = xadd(acc[2 * j + 1], xmul(c.y, L));
-      } else {
-        acc[2 * j] = fma(c.x, L, acc[2 * j]);
-        acc[2 * j + 1] = fma(c.y, L, acc[2 * j + 1]);
+#pragma unroll
+      for (int u = 0; u < PPT; ++u) {
+        if (EXACT) {
+          acc[u][2 * j] = xadd(acc[u][2 * j], xmul(c.x, L[u]));
+          acc[u][2 * j + 1] = xadd(acc[u][2 * j + 1], xmul(c.y, L[u]));
+        } else {
+          acc[u][2 * j] = fma(c.x, L[u], acc[u][2 * j]);
+          acc[u][2 * j + 1] = fma(c.y, L[u], acc[u][2 * j + 1]);
+        }
       }
     }
   };
   // legendre_values (basis.cpp:49-61), same rounding sequence.
-  apply(Cs, 1.0);
-  if (p >= 1) apply(Cs + JC, xmul(c_leg.norm[1], t));
-  double pm1 = 1.0, pm0 = t;
-  for (int q = 1; q < p; ++q) {
-    const double num = xsub(xmul(xmul(c_leg.a[q], t), pm0), xmul(c_leg.b[q], pm1));
-    const double pn1 = xdiv_small(num, c_leg.c[q], c_leg.rc[q]);
-    pm1 = pm0;
-    pm0 = pn1;
-    apply(Cs + (q + 1) * JC, xmul(c_leg.norm[q + 1], pn1));
+  double L[PPT], pm1[PPT], pm0[PPT];
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) L[u] = 1.0;
+  apply(Cs, L);
+  if (p >= 1) {
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) L[u] = xmul(c_leg.norm[1], t[u]);
+    apply(Cs + JC, L);
   }
 #pragma unroll
-  for (int j = 0; j < JC; ++j)
-    if (j < jn) tk[(j0 + j) * ldt + i] = acc[j];
+  for (int u = 0; u < PPT; ++u) {
+    pm1[u] = 1.0;
+    pm0[u] = t[u];
+  }
+  for (int q = 1; q < p; ++q) {
+    const double a = c_leg.a[q], b = c_leg.b[q], c = c_leg.c[q], rc = c_leg.rc[q];
+    const double nq = c_leg.norm[q + 1];
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+      const double num = xsub(xmul(xmul(a, t[u]), pm0[u]), xmul(b, pm1[u]));
+      const double pn1 = xdiv_small(num, c, rc);
+      pm1[u] = pm0[u];
+      pm0[u] = pn1;
+      L[u] = xmul(nq, pn1);
+    }
+    apply(Cs + (q + 1) * JC, L);
+  }
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    if (!live[u]) continue;
+    const int64_t i = base + u * 128;
+#pragma unroll
+    for (int j = 0; j < JC; ++j)
+      if (j < jn) tk[(j0 + j) * ldt + i] = acc[u][j];
+  }
 }
 
 // ------------------------------------------------------- K1b contract ---
@@ -700,7 +744,8 @@ static void launch_dense_t(const ModeDev& md, const double* xs, int64_t n, int64
                                    (kMaxDegree + 1) * JC * static_cast<int>(sizeof(double))));
   });
   const size_t sm = static_cast<size_t>(md.pmax + 1) * JC * sizeof(double);
-  dim3 grid(static_cast<unsigned>(ceil_div(n_out, 128)), static_cast<unsigned>(md.nchunk));
+  constexpr int rows_per_cta = 128 * DensePPT<EXACT, JC>::value;
+  dim3 grid(static_cast<unsigned>(ceil_div(n_out, rows_per_cta)), static_cast<unsigned>(md.nchunk));
   mode_dense_kernel<EXACT, JC><<<grid, 128, sm, s>>>(md, xs, n, n_out, row_src, tk, ldt, err_row);
   check_launch("mode_dense_kernel");
 }
