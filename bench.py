@@ -366,6 +366,27 @@ def main():
     return 0
 
 
+def gram_roofline(gram_flops, info, t, peak_fp64):
+    """Gram stage against its roofline.  Native: fp64 SYRK flops vs the DMMA
+    peak.  Sliced (fstk_gram.cu): int8 ops issued vs the B200 dense int8
+    tensor peak (4.5 POPS nominal; MEASURED_PEAKS.json has no int8 entry),
+    plus the fp64-equivalent rate (R(R+1)S/t) that the DGEMM Gram would need
+    to match it."""
+    if not t:
+        return None
+    if info["gram_slices"] > 0 and info.get("gram_int8_ops"):
+        ach = info["gram_int8_ops"] / t / 1e12
+        return {"bound": "tensor", "achieved": ach, "peak": 4500.0, "unit": "TOP/s (int8)",
+                "frac": ach / 4500.0, "peak_source": "nominal B200 dense int8 (= the fp8 rate in B200_PROFILING.md); cuBLASLt int8 TN measured 2.84 POPS here (profiles/int8_probe_r01.txt)",
+                "fp64_equivalent_tflops": gram_flops / t / 1e12, "fp64_peak_tflops": peak_fp64,
+                "kernel": f"cuBLASLt int8 IMMA over {info['gram_slices']} exact digit planes "
+                          "(slice/fold kernels in fstk_gram.cu)"}
+    ach = gram_flops / t / 1e12
+    return {"bound": "tensor", "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s",
+            "frac": ach / peak_fp64 if peak_fp64 else None,
+            "kernel": "cublasDsyrk/Dgemm (library SYRK on the sketched A)"}
+
+
 def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
     import torch
 
@@ -426,9 +447,8 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
             "stages_s": {"prepare": tm["prepare_s"], "alloc": tm["alloc_s"], "sketch": tm["sketch_s"],
                          "gram": tm["gram_s"], "allreduce": t_ar, "solve": tm["solve_s"],
                          "residual": tm["residual_s"]},
-            "gram_roofline": {"bound": "tensor", "achieved": gram_flops / tm["gram_s"] / 1e12
-                              if tm["gram_s"] else None, "peak": peak, "unit": "TFLOP/s",
-                              "kernel": "cublasDsyrk (library SYRK on the sketched A)"},
+            "gram_slices": info["gram_slices"], "refine_steps": info["refine_steps"],
+            "gram_roofline": gram_roofline(gram_flops, info, tm["gram_s"], peak),
             "residual_before": info["residual_before"], "residual_after": info["residual_after"],
             "rank_deficient": info["rank_deficient"],
             "note": "solve (cuSOLVER Cholesky) is outside the hot-path claim (north_star)"}

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define FSTK_GPU_ABI_VERSION 1
+#define FSTK_GPU_ABI_VERSION 2
 
 /* Status codes = fstk::ErrorKind + 1 (error.hpp:11-19). */
 enum {
@@ -102,6 +102,9 @@ typedef struct fstk_reestimate_info {
   double t_solve;     /* Cholesky (cuSOLVER), timed outside the hot-path claim */
   double t_residual;  /* validation residuals */
   double t_alloc;     /* host wall time of the sketch (A) allocation */
+  int32_t gram_slices;  /* int8 digit planes of the Gram used (0 = native fp64) */
+  int32_t refine_steps; /* iterative-refinement steps against A */
+  double gram_int8_ops; /* int8 tensor-core ops (2 x multiply-adds) of the sliced Gram */
 } fstk_reestimate_info;
 
 typedef struct fstk_gpu_model fstk_gpu_model;
@@ -177,7 +180,7 @@ int32_t fstk_gpu_reestimate_core(const fstk_gpu_model* model, const double* poin
  * begin() does the host RNG plan (bit-exact, identical on every rank), the
  * gathers, mode tables and the sketch of the rows this shard owns
  * (sampled rows [S*shard/shards, S*(shard+1)/shards)); normal_equations()
- * writes this shard's partial A^T A (R x R, full symmetric, column-major) and
+ * writes this shard's partial A^T A (R x R, column-major, lower triangle) and
  * A^T b into caller-provided DEVICE buffers so the caller can sum them across
  * ranks (one NCCL all-reduce); solve() runs the Cholesky solve on the summed
  * system and the validation residuals. */
@@ -189,6 +192,17 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* model, const double* points,
 int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* refit, double* gram,
                                         double* rhs, fstk_reestimate_info* info,
                                         fstk_gpu_error* err);
+/* Same, always with the native fp64 DSYRK/DGEMM Gram (the fallback when the
+ * sliced Gram is not positive definite or refinement stalls). */
+int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* refit, double* gram,
+                                               double* rhs, fstk_reestimate_info* info,
+                                               fstk_gpu_error* err);
+/* Process-wide Gram arithmetic: slices > 0 runs A^T A as int8 tensor-core
+ * GEMMs over that many exact 7-bit digit planes (4..9, default 7 or
+ * $FSTK_GRAM_SLICES); 0 selects the native fp64 Gram; < 0 only queries.
+ * Returns the previous setting.  No reference counterpart (an arithmetic
+ * choice of this backend; the solution still matches the reference's QR). */
+int32_t fstk_gpu_gram_slices(int32_t slices);
 int32_t fstk_gpu_refit_solve(fstk_gpu_refit* refit, const double* gram,
                              const double* rhs, double* core_out,
                              fstk_reestimate_info* info, fstk_gpu_error* err);

@@ -67,7 +67,8 @@ class ReestimateInfo(C.Structure):
                 ("padded_rows", C.c_uint64), ("rank_deficient", C.c_int32),
                 ("held_out", C.c_int32), ("t_prepare", C.c_double), ("t_sketch", C.c_double),
                 ("t_gram", C.c_double), ("t_solve", C.c_double), ("t_residual", C.c_double),
-                ("t_alloc", C.c_double)]
+                ("t_alloc", C.c_double), ("gram_slices", C.c_int32),
+                ("refine_steps", C.c_int32), ("gram_int8_ops", C.c_double)]
 
 
 # Every symbol include/fstk_gpu.h declares (checked by tests/test_abi.py).
@@ -83,6 +84,7 @@ EXPORTS = [
     "fstk_gpu_refit_factor", "fstk_gpu_refit_correction", "fstk_gpu_refit_apply",
     "fstk_gpu_refit_finish", "fstk_gpu_evaluate_grid", "fstk_gpu_reconstruct_grid",
     "fstk_gpu_self_convergence", "fstk_gpu_leverage_scores", "fstk_gpu_point_major_to_soa",
+    "fstk_gpu_refit_normal_equations_native", "fstk_gpu_gram_slices",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -127,6 +129,10 @@ def lib():
                                        C.POINTER(ReestimateInfo), C.POINTER(Err)]
     L.fstk_gpu_refit_normal_equations.argtypes = [VP, VP, VP, C.POINTER(ReestimateInfo),
                                                   C.POINTER(Err)]
+    L.fstk_gpu_refit_normal_equations_native.argtypes = [VP, VP, VP, C.POINTER(ReestimateInfo),
+                                                         C.POINTER(Err)]
+    L.fstk_gpu_gram_slices.argtypes = [C.c_int32]
+    L.fstk_gpu_gram_slices.restype = C.c_int32
     L.fstk_gpu_refit_solve.argtypes = [VP, VP, VP, DP, C.POINTER(ReestimateInfo),
                                        C.POINTER(Err)]
     L.fstk_gpu_refit_factor.argtypes = [VP, VP, VP, VP, C.POINTER(ReestimateInfo),

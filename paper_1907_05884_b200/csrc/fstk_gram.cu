@@ -1,0 +1,262 @@
+// A^T A for the core refit on the int8 tensor cores (exact integer slicing).
+//
+// The Gram of the sketched system (randls.cpp:112-123 solves min ||A x - b||
+// by QR; we form A^T A, Cholesky-factor it and refine against A itself) is
+// S x R^2 / 2 fused multiply-adds: at C2 that is 1.4e14 fp64 FMAs, 7.6 s at
+// the B200's measured DGEMM peak.  Here it runs as int8 x int8 -> int32
+// tensor-core GEMMs instead, with no loss of fp64-class accuracy:
+//
+//  * Per row segment g (<= kseg rows) and column a, e_ga = exponent of
+//    max_s |A[s][a]| so v = A * 2^-e_ga lies in (-1, 1).
+//  * v is cut into ns signed digits by round-to-nearest:
+//      d_1 = rint(64 v),  r = 64 v - d_1,  d_i = rint(128 r), r = 128 r - d_i
+//    every step exact in fp64 (Sterbenz), |d_i| <= 64, and
+//      v = sum_i d_i 2^(1-7i) + O(2^-7ns).
+//  * v_a v_b = sum_t 2^(2-7t) C_t with C_t = sum_{i+j=t} d_i(a) d_j(b).  Each
+//    C_t is ONE int8 GEMM: the digit planes of a column are stored
+//    consecutively along K ([d_1..d_ns] in X, [d_ns..d_1] in Y), so rows
+//    [0, (t-1)k) of X against rows [(ns-t+1)k, ns k) of Y pair exactly the
+//    digits with i + j = t.  |C_t| <= (t-1) k 64^2 < 2^31: exact in int32.
+//  * Terms with i + j > ns + 1 are dropped.  The fold kernel adds
+//    2^(e_a+e_b) sum_t 2^(2-7t) C_t into the fp64 Gram.
+//
+// ns = 7 gives 49 bits per column-max-relative entry; the Gram is then as
+// good a preconditioner as a DGEMM Gram and the iterative refinement against
+// A (fp64, fstk_refit.cu) converges to the same least-squares solution.  The
+// caller falls back to the native fp64 Gram whenever the sliced one is not
+// positive definite or refinement stalls, so rank-deficient systems take the
+// exact same path as before.
+#include <cublasLt.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "fstk_common.cuh"
+#include "fstk_internal.h"
+
+namespace fstk_gpu {
+
+namespace {
+
+constexpr int kDigitMax = 64;
+constexpr int kDefaultSlices = 7;
+std::atomic<int> g_slices{-1};
+
+int clamp_slices(int v) { return v <= 0 ? 0 : std::min(std::max(v, 4), 9); }
+
+struct LtState {
+  cublasLtHandle_t lt = nullptr;
+  std::mutex mu;  // guards algos
+  std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t>, cublasLtMatmulAlgo_t> algos;
+};
+std::mutex g_lt_mu;
+std::map<int, LtState*> g_lt;
+
+LtState& lt_state(int device) {
+  std::lock_guard<std::mutex> lk(g_lt_mu);
+  LtState*& st = g_lt[device];
+  if (!st) {
+    st = new LtState();
+    if (cublasLtCreate(&st->lt) != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, "cublasLtCreate failed");
+  }
+  return *st;
+}
+
+__global__ void col_exponent_kernel(const double* __restrict__ A, int64_t lda, int64_t rows,
+                                    int n, int* __restrict__ ex) {
+  const int a = blockIdx.x;
+  double m = 0.0;
+  if (a < n) {
+    const double* col = A + static_cast<int64_t>(a) * lda;
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) m = fmax(m, fabs(col[r]));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double wm[32];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, wm[w]);
+    int e = 0;
+    if (m > 0.0) frexp(m, &e);
+    ex[a] = e;
+  }
+}
+
+// Thread per 4 consecutive rows of one column; X/Y column stride ld = ns*kp.
+__global__ void slice_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n,
+                             int64_t kp, int ns, const int* __restrict__ ex,
+                             int8_t* __restrict__ X, int8_t* __restrict__ Y) {
+  const int a = blockIdx.y;
+  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (r0 >= kp) return;
+  const double sc = ldexp(1.0, 6 - ex[a]);
+  double v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    v[u] = (a < n && r0 + u < rows) ? A[static_cast<int64_t>(a) * lda + r0 + u] * sc : 0.0;
+  const int64_t ld = static_cast<int64_t>(ns) * kp;
+  int8_t* xa = X + static_cast<int64_t>(a) * ld + r0;
+  int8_t* ya = Y + static_cast<int64_t>(a) * ld + r0;
+  for (int i = 0; i < ns; ++i) {
+    int q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double d = rint(v[u]);
+      q[u] = static_cast<int>(d);
+      v[u] = (v[u] - d) * 128.0;
+    }
+    const char4 c = make_char4(static_cast<signed char>(q[0]), static_cast<signed char>(q[1]),
+                               static_cast<signed char>(q[2]), static_cast<signed char>(q[3]));
+    *reinterpret_cast<char4*>(xa + i * kp) = c;
+    *reinterpret_cast<char4*>(ya + (ns - 1 - i) * kp) = c;
+  }
+}
+
+// G[c0+i][c0+j] (+)= 2^(e_i+e_j) sum_t 2^(2-7t) C_t[i][j] for the valid rows
+// i >= j of the column block (the lower triangle the solver reads).
+__global__ void fold_kernel(const int32_t* __restrict__ C, int64_t cstride, int ns, int64_t m,
+                            int w, int c0, int n, const int* __restrict__ ex,
+                            double* __restrict__ G, int accumulate) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= m || j >= w || i < j || c0 + i >= n || c0 + j >= n) return;
+  const int64_t e = i + static_cast<int64_t>(j) * m;
+  double v = 0.0;
+  for (int t = ns + 1; t >= 2; --t)
+    v += ldexp(static_cast<double>(C[static_cast<int64_t>(t - 2) * cstride + e]), 2 - 7 * t);
+  v = ldexp(v, ex[c0 + i] + ex[c0 + j]);
+  double* g = G + (c0 + i) + static_cast<int64_t>(c0 + j) * n;
+  *g = accumulate ? *g + v : v;
+}
+
+// C (M x N, int32, col-major, ldc) = op(A)^T B with A: K x M int8 (lda),
+// B: K x N int8 (ldb) -- the "TN" IMMA layout cuBLASLt runs on tensor cores.
+void imma_tn(LtState& st, DevBuf<uint8_t>& ws, int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda,
+             const int8_t* B, int64_t ldb, int32_t* Cm, int64_t ldc, cudaStream_t s) {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+  auto ok = [](cublasStatus_t x, const char* what) {
+    if (x != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, std::string("cuBLASLt: ") + what);
+  };
+  ok(cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
+  const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
+  ok(cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof(tA)), "transa");
+  ok(cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof(tB)), "transb");
+  ok(cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, K, M, lda), "layout A");
+  ok(cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, K, N, ldb), "layout B");
+  ok(cublasLtMatrixLayoutCreate(&lc, CUDA_R_32I, M, N, ldc), "layout C");
+  const auto key = std::make_tuple(M, N, K, lda, ldc);
+  cublasLtMatmulAlgo_t algo;
+  {
+  std::lock_guard<std::mutex> lk(st.mu);
+  auto it = st.algos.find(key);
+  if (it == st.algos.end()) {
+    cublasLtMatmulPreference_t pref = nullptr;
+    ok(cublasLtMatmulPreferenceCreate(&pref), "pref");
+    const size_t wsz = ws.n;
+    ok(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsz,
+                                            sizeof(wsz)),
+       "pref ws");
+    cublasLtMatmulHeuristicResult_t res{};
+    int cnt = 0;
+    const cublasStatus_t hs =
+        cublasLtMatmulAlgoGetHeuristic(st.lt, op, la, lb, lc, lc, pref, 1, &res, &cnt);
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (hs != CUBLAS_STATUS_SUCCESS || cnt == 0)
+      fail(FSTK_E_COMPUTE, "cuBLASLt: no int8 TN algorithm for the sliced Gram");
+    it = st.algos.emplace(key, res.algo).first;
+  }
+  algo = it->second;
+  }
+  const int32_t one = 1, zero = 0;
+  const cublasStatus_t ms = cublasLtMatmul(st.lt, op, &one, A, la, B, lb, &zero, Cm, lc, Cm, lc,
+                                           &algo, ws.p, ws.n, s);
+  cublasLtMatrixLayoutDestroy(la);
+  cublasLtMatrixLayoutDestroy(lb);
+  cublasLtMatrixLayoutDestroy(lc);
+  cublasLtMatmulDescDestroy(op);
+  ok(ms, "matmul");
+  count_launch();
+}
+
+}  // namespace
+
+int gram_slices() {
+  int v = g_slices.load();
+  if (v < 0) {
+    const char* e = std::getenv("FSTK_GRAM_SLICES");
+    v = clamp_slices(e ? std::atoi(e) : kDefaultSlices);
+    g_slices.store(v);
+  }
+  return v;
+}
+
+int set_gram_slices(int slices) {
+  const int prev = gram_slices();
+  g_slices.store(slices < 0 ? prev : clamp_slices(slices));
+  return prev;
+}
+
+bool gram_sliced_applies(int64_t rows, int n) { return gram_slices() > 0 && n >= 256 && rows > 0; }
+
+// gram (n x n, col-major, lower triangle) = beta * gram + A^T A over `rows`
+// rows of A (col-major, lda).
+double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n, double* gram,
+                              double beta, cudaStream_t s, int device, GramScratch& sc) {
+  double ops = 0.0;
+  const int ns = gram_slices();
+  LtState& st = lt_state(device);
+  const int64_t np = round_up(static_cast<int64_t>(n), 16);
+  // Segment rows: int32-exact bound, 65536 cap, and <= ~8 GB of digit planes.
+  int64_t kmax = ((int64_t(1) << 31) - 1) / (int64_t(kDigitMax) * kDigitMax * ns);
+  kmax = std::min<int64_t>(kmax, 65536);
+  const int64_t plane_budget = int64_t(8) << 30;
+  kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, plane_budget / (2 * ns * np)));
+  kmax &= ~int64_t(15);
+  const int64_t kp = std::min<int64_t>(kmax, round_up(rows, 16));
+  // Column blocks: C_t planes (ns of them, m x w int32) within ~4 GB.
+  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * ns * 4));
+  w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), 16), np);
+  if (w > 4096 && np > 4096) w = 4096;
+  const int64_t ld = ns * kp;
+  sc.X.ensure(static_cast<size_t>(ld * np));
+  sc.Y.ensure(static_cast<size_t>(ld * np));
+  sc.C.ensure(static_cast<size_t>(ns) * np * w);
+  sc.ex.ensure(static_cast<size_t>(np));
+  sc.ws.ensure(size_t(32) << 20);
+  DevBuf<int8_t>& X = sc.X;
+  DevBuf<int8_t>& Y = sc.Y;
+  DevBuf<int32_t>& Cb = sc.C;
+  DevBuf<int>& ex = sc.ex;
+  bool first = true;
+  for (int64_t s0 = 0; s0 < rows; s0 += kp) {
+    const int64_t kr = std::min(kp, rows - s0);
+    col_exponent_kernel<<<static_cast<unsigned>(np), 256, 0, s>>>(A + s0, lda, kr, n, ex.p);
+    check_launch("col_exponent_kernel");
+    dim3 sg(static_cast<unsigned>(ceil_div(kp / 4, 256)), static_cast<unsigned>(np));
+    slice_kernel<<<sg, 256, 0, s>>>(A + s0, lda, kr, n, kp, ns, ex.p, X.p, Y.p);
+    check_launch("slice_kernel");
+    for (int64_t c0 = 0; c0 < np; c0 += w) {
+      const int64_t wn = std::min(w, np - c0);
+      const int64_t m = np - c0;
+      for (int t = 2; t <= ns + 1; ++t) {
+        const int64_t K = (t - 1) * kp;
+        ops += 2.0 * static_cast<double>(m) * static_cast<double>(wn) * static_cast<double>(K);
+        imma_tn(st, sc.ws, m, wn, K, X.p + c0 * ld, ld, Y.p + c0 * ld + (ns - t + 1) * kp, ld,
+                Cb.p + static_cast<int64_t>(t - 2) * m * wn, m, s);
+      }
+      dim3 fg(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(wn));
+      const int acc = (!first || beta != 0.0) ? 1 : 0;
+      fold_kernel<<<fg, 256, 0, s>>>(Cb.p, m * wn, ns, m, static_cast<int>(wn),
+                                     static_cast<int>(c0), n, ex.p, gram, acc);
+      check_launch("fold_kernel");
+    }
+    first = false;
+  }
+  return ops;
+}
+
+}  // namespace fstk_gpu

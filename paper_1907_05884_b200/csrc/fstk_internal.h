@@ -183,4 +183,19 @@ void launch_mode_general(const GenModeDev& G, const double* xs, int64_t n, int64
                          const int64_t* row_src, double* tk, int64_t ldt, bool exact,
                          unsigned long long* err_row, cudaStream_t s, int device);
 
+// Sliced int8 tensor-core Gram (fstk_gram.cu).  Scratch is per refit so
+// concurrent refits on one device never share buffers.
+struct GramScratch {
+  DevBuf<int8_t> X, Y;     // digit planes, column a at a * ns * kp
+  DevBuf<int32_t> C;       // ns planes of one column block
+  DevBuf<int> ex;          // per-column exponents of the current segment
+  DevBuf<uint8_t> ws;      // cuBLASLt workspace
+};
+int gram_slices();                      // 0 = native fp64 DSYRK/DGEMM Gram
+int set_gram_slices(int slices);        // returns the previous setting
+bool gram_sliced_applies(int64_t rows, int n);
+// Returns the int8 tensor-core ops (2 x multiply-adds) issued.
+double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n, double* gram,
+                              double beta, cudaStream_t s, int device, GramScratch& sc);
+
 }  // namespace fstk_gpu

@@ -864,6 +864,8 @@ struct fstk_gpu_refit {
   DevBuf<double> tmp_r;   // local residual rows
   // transform = none: mode tables of this shard's sampled rows (A generated on demand)
   bool none = false;
+  GramScratch gs;        // sliced int8 Gram scratch (fstk_gram.cu)
+  int gram_used = 0;     // digit planes of the last Gram (0 = native fp64)
   DevBuf<double> tables;
   int64_t toff[kMaxOrder] = {0};
   int64_t ldt = 0;
@@ -1161,8 +1163,10 @@ static void gram_accumulate(cublasHandle_t h, const double* A, int lda, int rows
 }
 
 // Rows per generated block of A for transform = none (about 1 GB of fp64).
-static int64_t none_block_rows(const fstk_gpu_refit* rf) {
-  const int64_t cap = std::max<int64_t>(1024, (int64_t(1) << 27) / std::max<int64_t>(rf->R, 1));
+static int64_t none_block_rows(const fstk_gpu_refit* rf, bool sliced = false) {
+  // ~1 GB of fp64; 4 GB when the Gram is sliced (longer int8 GEMM K per block).
+  const int64_t elems = (int64_t(1) << 27) * (sliced ? 4 : 1);
+  const int64_t cap = std::max<int64_t>(1024, elems / std::max<int64_t>(rf->R, 1));
   return std::min<int64_t>(round_up(cap, 128), std::max<int64_t>(rf->local_rows, 1));
 }
 
@@ -1191,10 +1195,12 @@ static void generate_design_block(const fstk_gpu_refit* rf, int64_t row0, int64_
 
 }  // namespace fstk_gpu
 
-int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
-                                        fstk_reestimate_info* info, fstk_gpu_error* err) {
-  return guarded(err, [&] {
-    require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
+namespace fstk_gpu {
+static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
+                             fstk_reestimate_info* info, bool allow_sliced) {
+  {
+    rf->gram_used = 0;
+    double i8ops = 0.0;
     DeviceGuard dg(rf->device);
     cudaStream_t s = rf->stream;
     Handles& h = handles(rf->device);
@@ -1212,16 +1218,22 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double
       // is split into nb column blocks: block row i below the diagonal is one
       // DGEMM A_i^T [A_0 .. A_{i-1}] and each diagonal block one DSYRK, so
       // (nb-1)/nb of the flops run in large GEMMs.
+      const bool sliced = allow_sliced && gram_sliced_applies(arows, n);
+      rf->gram_used = sliced ? gram_slices() : 0;
       if (rf->none) {
         // A^T A accumulated over generated row blocks (A never materialised).
-        const int64_t BS = none_block_rows(rf);
+        const int64_t BS = none_block_rows(rf, sliced);
         DevBuf<double> W(static_cast<size_t>(BS) * rf->R);
         for (int64_t r0 = 0; r0 < arows; r0 += BS) {
           const int64_t nb_rows = std::min(BS, arows - r0);
           generate_design_block(rf, r0, nb_rows, W.p, BS, s);
           ProfScope prof(FSTK_PROF_GRAM, s);
           const double beta = r0 == 0 ? 0.0 : 1.0;
-          gram_accumulate(h.blas, W.p, static_cast<int>(BS), static_cast<int>(nb_rows), n, gram, beta);
+          if (sliced)
+            i8ops += gram_accumulate_sliced(W.p, BS, nb_rows, n, gram, beta, s, rf->device, rf->gs);
+          else
+            gram_accumulate(h.blas, W.p, static_cast<int>(BS), static_cast<int>(nb_rows), n, gram,
+                            beta);
           if (cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(nb_rows), n, &one, W.p,
                           static_cast<int>(BS), rf->b.p + r0, 1, &beta, rhs, 1) !=
               CUBLAS_STATUS_SUCCESS)
@@ -1231,8 +1243,11 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double
         FSTK_CUDA(cudaStreamSynchronize(s));
       } else {
         ProfScope prof(FSTK_PROF_GRAM, s);
-        gram_accumulate(h.blas, rf->A.p, static_cast<int>(arows), static_cast<int>(arows), n, gram,
-                        0.0);
+        if (sliced)
+          i8ops = gram_accumulate_sliced(rf->A.p, arows, arows, n, gram, 0.0, s, rf->device, rf->gs);
+        else
+          gram_accumulate(h.blas, rf->A.p, static_cast<int>(arows), static_cast<int>(arows), n,
+                          gram, 0.0);
         if (cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(arows), n, &one, rf->A.p,
                         static_cast<int>(arows), rf->b.p, 1, &zero, rhs, 1) != CUBLAS_STATUS_SUCCESS)
           fail(FSTK_E_COMPUTE, "cublasDgemv failed");
@@ -1240,9 +1255,32 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double
       }
     }
     const double t = tg.seconds();
-    if (info) info->t_gram = t;
+    if (info) {
+      info->t_gram = t;
+      info->gram_slices = rf->gram_used;
+      info->gram_int8_ops = i8ops;
+    }
+  }
+}
+}  // namespace fstk_gpu
+
+int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
+                                        fstk_reestimate_info* info, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
+    normal_equations(rf, gram, rhs, info, true);
   });
 }
+
+int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* rf, double* gram, double* rhs,
+                                               fstk_reestimate_info* info, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
+    normal_equations(rf, gram, rhs, info, false);
+  });
+}
+
+int32_t fstk_gpu_gram_slices(int32_t slices) { return fstk_gpu::set_gram_slices(slices); }
 
 // ---- solve: Cholesky of the summed normal equations + iterative refinement
 // against the sketched system itself (corrected semi-normal equations), which
@@ -1486,15 +1524,49 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     DevBuf<double> x(n), sv(n);
     auto rc = [&](int32_t c) { rethrow_stage(c, err); };
     rc(fstk_gpu_refit_factor(rf, gram_in, rhs_in, x.p, info, err));
+    // The sliced int8 Gram is a preconditioner-grade A^T A; whenever it is not
+    // positive definite or refinement does not contract, redo the system with
+    // the native fp64 Gram so those cases follow the exact fp64 path.
+    DevBuf<double> g2, r2;
+    auto native_refactor = [&] {
+      fstk_reestimate_info li{};
+      g2.ensure(static_cast<size_t>(n) * n);
+      r2.ensure(static_cast<size_t>(n));
+      rc(fstk_gpu_refit_normal_equations_native(rf, g2.p, r2.p, &li, err));
+      rc(fstk_gpu_refit_factor(rf, g2.p, r2.p, x.p, info, err));
+      if (info) {
+        info->t_gram += li.t_gram;
+        info->gram_slices = 0;
+      }
+    };
+    if (!rf->factored && rf->gram_used > 0) native_refactor();
+    int steps = 0;
     if (rf->factored) {
       EventTimer tref(rf->stream);
       double prev = 1e300;
-      for (int it = 0; it < 6; ++it) {
+      for (int it = 0; it < 8; ++it) {
         rc(fstk_gpu_refit_correction(rf, x.p, sv.p, err));
         double step = 0.0;
         rc(fstk_gpu_refit_apply(rf, sv.p, x.p, &step, err));
+        ++steps;
         if (step <= 1e-15) break;
-        if (it >= 1 && step > 0.5 * prev) {
+        // Stagnation at the rounding floor (||dx||/||x|| ~ cond(A) eps, about
+        // 1e-13 at C2) is convergence.  Not contracting above kStallFloor, or
+        // out of steps while still moving, is a stall: redo it on the native
+        // Gram if this one was sliced, else flag the system.
+        constexpr double kStallFloor = 1e-11;
+        const bool flat = it >= 1 && step > 0.5 * prev;
+        if (flat && step <= kStallFloor) break;
+        const bool last = it == 7 && step > kStallFloor;
+        if (flat || last) {
+          if (last && rf->gram_used == 0) break;
+          if (rf->gram_used > 0) {
+            native_refactor();
+            if (!rf->factored) break;
+            prev = 1e300;
+            it = -1;
+            continue;
+          }
           // No contraction: cond(A)^2 eps is not small; keep the iterate but
           // report the system as numerically rank deficient.
           rf->rank_def = true;
@@ -1504,6 +1576,7 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
       }
       if (info) info->t_solve += tref.seconds();
     }
+    if (info) info->refine_steps = steps;
     rc(fstk_gpu_refit_finish(rf, x.p, core_out, info, err));
   });
 }

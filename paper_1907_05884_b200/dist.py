@@ -36,27 +36,63 @@ def evaluate_sharded(model, points, rank: int, world: int):
     return lo, hi, model.evaluate_batch(np.asfortranarray(points[lo:hi]))
 
 
-def refine_distributed(sess, gram, rhs, max_iter: int = 6, group=None):
+STALL_FLOOR = 1e-11  # ||dx||/||x|| below which a flat refinement has converged
+
+
+def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None):
     """Cholesky of the summed Gram on every rank, then iterative refinement
     against the row-sharded sketch: each step needs one all-reduce of an
-    R-vector.  Returns the solution tensor x (identical on all ranks)."""
+    R-vector.  Returns the solution tensor x (identical on all ranks).
+
+    With the sliced int8 Gram (fstk_gpu_gram_slices > 0) a Gram that is not
+    positive definite, or refinement that stops contracting, is redone once
+    with the native fp64 Gram (fstk_refit.cu: fstk_gpu_refit_solve does the
+    same on one GPU).  Both decisions depend only on all-reduced data, so
+    every rank takes the same branch."""
     import torch
     import torch.distributed as dist
 
+    from .refit import gram_slices
+
     x = torch.empty_like(rhs)
+    sliced = gram_slices() > 0
+
+    def native():
+        sess.normal_equations_native(gram, rhs)
+        reduce_normal_equations(gram, rhs, group=group)
+        return sess.factor(gram, rhs, x)
+
+    sess.info.refine_steps = 0
     ok = sess.factor(gram, rhs, x)
+    if not ok and sliced:
+        ok, sliced = native(), False
     if not ok:
         return x
     s = torch.empty_like(rhs)
     prev = float("inf")
-    for it in range(max_iter):
+    it = 0
+    while it < max_iter:
         sess.correction(x, s)
         if dist.is_initialized() and dist.get_world_size(group) > 1:
             dist.all_reduce(s, group=group)
         step = sess.apply(s, x)
-        if step <= 1e-15 or (it >= 1 and step > 0.5 * prev):
+        sess.info.refine_steps += 1
+        if step <= 1e-15:
             break
+        # Flat at the rounding floor is convergence (see fstk_gpu_refit_solve).
+        flat = it >= 1 and step > 0.5 * prev
+        if flat and step <= STALL_FLOOR:
+            break
+        if flat or (sliced and it == max_iter - 1 and step > STALL_FLOOR):
+            if not sliced:
+                break
+            ok, sliced = native(), False
+            if not ok:
+                break
+            prev, it = float("inf"), 0
+            continue
         prev = step
+        it += 1
     return x
 
 

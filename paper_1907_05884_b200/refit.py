@@ -40,10 +40,18 @@ def _info_dict(info: ReestimateInfo) -> dict:
     return {"residual_before": info.residual_before, "residual_after": info.residual_after,
             "sample_rows": int(info.sample_rows), "working_rows": int(info.working_rows),
             "rank_deficient": bool(info.rank_deficient), "held_out": bool(info.held_out),
-            "padded_rows": int(info.padded_rows),
+            "padded_rows": int(info.padded_rows), "gram_slices": int(info.gram_slices),
+            "refine_steps": int(info.refine_steps), "gram_int8_ops": float(info.gram_int8_ops),
             "timings": {"prepare_s": info.t_prepare, "sketch_s": info.t_sketch,
                         "gram_s": info.t_gram, "solve_s": info.t_solve,
                         "residual_s": info.t_residual, "alloc_s": info.t_alloc}}
+
+
+def gram_slices(slices: int | None = None) -> int:
+    """Gram arithmetic of this process: returns the current number of int8
+    digit planes (0 = native fp64 Gram); with `slices` given, sets it first
+    (4..9, or 0) and returns the previous value.  See fstk_gram.cu."""
+    return int(lib().fstk_gpu_gram_slices(-1 if slices is None else int(slices)))
 
 
 def reestimate_core(model: Model, points, values, seed=0, sample_rows=0,
@@ -107,6 +115,12 @@ class RefitSession:
         err = Err()
         check(lib().fstk_gpu_refit_normal_equations(self._h, gram_t.data_ptr(), rhs_t.data_ptr(),
                                                     C.byref(self.info), C.byref(err)), err)
+
+    def normal_equations_native(self, gram_t, rhs_t):
+        """normal_equations() with the native fp64 DSYRK/DGEMM Gram."""
+        err = Err()
+        check(lib().fstk_gpu_refit_normal_equations_native(
+            self._h, gram_t.data_ptr(), rhs_t.data_ptr(), C.byref(self.info), C.byref(err)), err)
 
     def solve(self, gram_t, rhs_t) -> np.ndarray:
         core = np.zeros(self.R)
