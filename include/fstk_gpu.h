@@ -203,6 +203,14 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* refit, double* gr
  * Returns the previous setting.  No reference counterpart (an arithmetic
  * choice of this backend; the solution still matches the reference's QR). */
 int32_t fstk_gpu_gram_slices(int32_t slices);
+/* gram (n x n, column-major, lower triangle written) = A^T A for a DEVICE
+ * matrix A (rows x n, column-major, lda), with `slices` digit planes
+ * (0 = native fp64 DSYRK/DGEMM), on `stream` (cudaStream_t, NULL = default).
+ * The Gram stage of normal_equations() on its own, for tests and callers
+ * that build their own design matrices. */
+int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t n,
+                             double* gram, int32_t slices, int32_t device, void* stream,
+                             fstk_gpu_error* err);
 int32_t fstk_gpu_refit_solve(fstk_gpu_refit* refit, const double* gram,
                              const double* rhs, double* core_out,
                              fstk_reestimate_info* info, fstk_gpu_error* err);

@@ -11,7 +11,7 @@ from ._lib import FstkError, FstkIOError, FstkValueError, launch_count
 from .cloud import (PointCloud, read_cloud, read_cloud_binary, read_cloud_csv, read_cloud_device,
                     read_points_csv, write_cloud_binary, write_cloud_csv)
 from .model import BasisSpec, Model, ModelMetadata, ModeFunction, load_model, save_model
-from .refit import (RefitSession, build_design_rows, gram_slices, leverage_scores, mixed_matrix,
+from .refit import (RefitSession, build_design_rows, gram, gram_slices, leverage_scores, mixed_matrix,
                     reestimate_core, self_convergence, sketch, sketch_config)
 
 
@@ -24,7 +24,7 @@ def set_max_threads(n: int) -> None:
 __all__ = [
     "BasisSpec", "Model", "ModelMetadata", "ModeFunction", "load_model", "save_model",
     "reestimate_core", "RefitSession", "build_design_rows", "sketch", "mixed_matrix",
-    "sketch_config", "self_convergence", "leverage_scores", "gram_slices", "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
+    "sketch_config", "self_convergence", "leverage_scores", "gram_slices", "gram", "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
     "launch_count", "PointCloud", "read_cloud", "read_cloud_binary", "read_cloud_csv",
     "read_cloud_device", "read_points_csv", "write_cloud_binary", "write_cloud_csv",
 ]

@@ -205,9 +205,9 @@ bool gram_sliced_applies(int64_t rows, int n) { return gram_slices() > 0 && n >=
 // gram (n x n, col-major, lower triangle) = beta * gram + A^T A over `rows`
 // rows of A (col-major, lda).
 double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n, double* gram,
-                              double beta, cudaStream_t s, int device, GramScratch& sc) {
+                              double beta, int ns, cudaStream_t s, int device, GramScratch& sc) {
   double ops = 0.0;
-  const int ns = gram_slices();
+  require(ns >= 4 && ns <= 9, FSTK_E_PARAMETER, "sliced Gram: 4..9 digit planes");
   LtState& st = lt_state(device);
   const int64_t np = round_up(static_cast<int64_t>(n), 16);
   // Segment rows: int32-exact bound, 65536 cap, and <= ~8 GB of digit planes.

@@ -196,6 +196,6 @@ int set_gram_slices(int slices);        // returns the previous setting
 bool gram_sliced_applies(int64_t rows, int n);
 // Returns the int8 tensor-core ops (2 x multiply-adds) issued.
 double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n, double* gram,
-                              double beta, cudaStream_t s, int device, GramScratch& sc);
+                              double beta, int slices, cudaStream_t s, int device, GramScratch& sc);
 
 }  // namespace fstk_gpu

@@ -1230,7 +1230,8 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
           ProfScope prof(FSTK_PROF_GRAM, s);
           const double beta = r0 == 0 ? 0.0 : 1.0;
           if (sliced)
-            i8ops += gram_accumulate_sliced(W.p, BS, nb_rows, n, gram, beta, s, rf->device, rf->gs);
+            i8ops += gram_accumulate_sliced(W.p, BS, nb_rows, n, gram, beta, rf->gram_used, s,
+                                            rf->device, rf->gs);
           else
             gram_accumulate(h.blas, W.p, static_cast<int>(BS), static_cast<int>(nb_rows), n, gram,
                             beta);
@@ -1244,7 +1245,8 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
       } else {
         ProfScope prof(FSTK_PROF_GRAM, s);
         if (sliced)
-          i8ops = gram_accumulate_sliced(rf->A.p, arows, arows, n, gram, 0.0, s, rf->device, rf->gs);
+          i8ops = gram_accumulate_sliced(rf->A.p, arows, arows, n, gram, 0.0, rf->gram_used, s,
+                                         rf->device, rf->gs);
         else
           gram_accumulate(h.blas, rf->A.p, static_cast<int>(arows), static_cast<int>(arows), n,
                           gram, 0.0);
@@ -1281,6 +1283,31 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* rf, double* gram,
 }
 
 int32_t fstk_gpu_gram_slices(int32_t slices) { return fstk_gpu::set_gram_slices(slices); }
+
+int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t n, double* gram,
+                             int32_t slices, int32_t device, void* stream, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    require(a && gram, FSTK_E_PARAMETER, "null argument");
+    require(n > 0 && rows > 0 && lda >= rows, FSTK_E_SHAPE, "gram: need n > 0, rows > 0, lda >= rows");
+    require(slices == 0 || (slices >= 4 && slices <= 9), FSTK_E_PARAMETER,
+            "gram: slices must be 0 (native fp64) or 4..9");
+    require((rows <= INT32_MAX && lda <= INT32_MAX) || slices > 0, FSTK_E_SHAPE,
+            "gram: native path needs rows, lda < 2^31");
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (slices > 0) {
+      GramScratch sc;
+      gram_accumulate_sliced(a, lda, rows, n, gram, 0.0, slices, s, device, sc);
+      FSTK_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    Handles& h = handles(device);
+    cublasSetStream(h.blas, s);
+    gram_accumulate(h.blas, a, static_cast<int>(lda), static_cast<int>(rows), n, gram, 0.0);
+    FSTK_CUDA(cudaStreamSynchronize(s));
+  });
+}
 
 // ---- solve: Cholesky of the summed normal equations + iterative refinement
 // against the sketched system itself (corrected semi-normal equations), which

@@ -39,7 +39,7 @@ def evaluate_sharded(model, points, rank: int, world: int):
 STALL_FLOOR = 1e-11  # ||dx||/||x|| below which a flat refinement has converged
 
 
-def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None):
+def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, sliced=None):
     """Cholesky of the summed Gram on every rank, then iterative refinement
     against the row-sharded sketch: each step needs one all-reduce of an
     R-vector.  Returns the solution tensor x (identical on all ranks).
@@ -52,10 +52,11 @@ def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None):
     import torch
     import torch.distributed as dist
 
-    from .refit import gram_slices
-
     x = torch.empty_like(rhs)
-    sliced = gram_slices() > 0
+    if sliced is None:
+        from .refit import gram_slices
+
+        sliced = gram_slices() > 0
 
     def native():
         sess.normal_equations_native(gram, rhs)

@@ -54,6 +54,26 @@ def gram_slices(slices: int | None = None) -> int:
     return int(lib().fstk_gpu_gram_slices(-1 if slices is None else int(slices)))
 
 
+def gram(a, slices: int | None = None):
+    """Lower triangle of A^T A for a CUDA float64 tensor A (rows x n) through
+    fstk_gpu_gram_device; `slices` digit planes (default: the process
+    setting, 0 = native fp64).  Returns an n x n CUDA tensor (upper triangle
+    of the column-major result left zero)."""
+    import torch
+
+    if not (isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == torch.float64 and a.dim() == 2):
+        raise TypeError("gram: expected a 2-D CUDA float64 tensor")
+    rows, n = a.shape
+    at = a.t().contiguous()  # column-major A: column j at j * rows
+    g = torch.zeros(n * n, dtype=torch.float64, device=a.device)
+    ns = gram_slices() if slices is None else int(slices)
+    err = Err()
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    check(lib().fstk_gpu_gram_device(at.data_ptr(), rows, rows, n, g.data_ptr(), ns,
+                                     a.device.index, stream, C.byref(err)), err)
+    return g.view(n, n).t()  # [row, col]
+
+
 def reestimate_core(model: Model, points, values, seed=0, sample_rows=0,
                     working_subset=1 << 20, transform="dct", validation_fraction=0.05,
                     device=None):

@@ -65,3 +65,72 @@ def test_gloo_world2_normal_equations_allreduce(O):
     alpha = np.linalg.solve(out[0][0], out[0][1])
     want, _ = O.solve_system(a, b)
     assert np.linalg.norm(alpha - want) <= 1e-9 * np.linalg.norm(want)
+
+
+# ---- refine_distributed control flow (sliced-Gram fallback), CPU-only -------
+class _ScriptedSession:
+    """Stands in for RefitSession: factor() outcomes and refinement step sizes
+    follow a script, and every call is logged, so the fallback logic of
+    dist.refine_distributed can be checked without a GPU."""
+
+    def __init__(self, factor_ok, steps):
+        import types
+
+        self.factor_ok = list(factor_ok)
+        self.steps = list(steps)
+        self.calls = []
+        self.info = types.SimpleNamespace(refine_steps=0)
+
+    def factor(self, gram, rhs, x):
+        self.calls.append("factor")
+        return self.factor_ok.pop(0)
+
+    def normal_equations_native(self, gram, rhs):
+        self.calls.append("native")
+
+    def correction(self, x, s):
+        self.calls.append("correction")
+
+    def apply(self, s, x):
+        self.calls.append("apply")
+        return self.steps.pop(0)
+
+
+def _refine(sess, sliced):
+    import torch
+
+    from paper_1907_05884_b200 import dist
+
+    g, r = torch.zeros(4), torch.zeros(2)
+    return dist.refine_distributed(sess, g, r, sliced=sliced)
+
+
+def test_refine_converges_at_rounding_floor_without_fallback():
+    s = _ScriptedSession([True], [1e-9, 2e-13, 1.5e-13])
+    _refine(s, sliced=True)
+    assert "native" not in s.calls and s.info.refine_steps == 3
+
+
+def test_refine_not_pd_sliced_falls_back_once():
+    s = _ScriptedSession([False, True], [1e-9, 1e-16])
+    _refine(s, sliced=True)
+    assert s.calls[:3] == ["factor", "native", "factor"] and s.calls.count("native") == 1
+
+
+def test_refine_stall_above_floor_falls_back_then_stops():
+    s = _ScriptedSession([True, True], [1e-3, 9e-4, 1e-9, 1e-16])
+    _refine(s, sliced=True)
+    assert s.calls.count("native") == 1 and s.calls.count("apply") == 4
+
+
+def test_refine_native_stall_does_not_loop():
+    s = _ScriptedSession([True], [1e-3, 9e-4])
+    _refine(s, sliced=False)
+    assert "native" not in s.calls and s.calls.count("apply") == 2
+
+
+def test_refine_slow_sliced_contraction_falls_back():
+    steps = [1e-2 * 0.4 ** k for k in range(8)] + [1e-16]
+    s = _ScriptedSession([True, True], steps)
+    _refine(s, sliced=True)
+    assert s.calls.count("native") == 1

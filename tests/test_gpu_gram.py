@@ -1,0 +1,213 @@
+"""The sliced int8 tensor-core Gram (fstk_gram.cu) through the C-ABI
+(fstk_gpu_gram_device / the refit stages).
+
+Bars: every entry within the rigorous digit-plane bound
+    |G - A^T A|_ab <= 4 (ns + 3) 2^(-7 ns) rows max|A_a| max|A_b|
+(+ the fp64 reference's own rounding); bit-exact when the entries need no
+more bits than the planes hold; the refit core with the sliced Gram equal to
+the native-Gram core to 1e-12 and to the oracle's QR core to the north-star
+1e-9; systems the sliced Gram cannot precondition fall back to the native
+Gram (reported as gram_slices == 0) with the same answer."""
+import numpy as np
+import pytest
+
+import paper_1907_05884_b200 as F
+from conftest import rel
+from paper_1907_05884_b200 import synth
+
+pytestmark = pytest.mark.gpu
+CORE_TOL = 1e-9
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _check_bound(a, g, ns):
+    torch = _torch()
+    ref = a.t() @ a
+    rows = a.shape[0]
+    mx = a.abs().amax(dim=0)
+    bound = 4 * (ns + 3) * 2.0 ** (-7 * ns) * rows * (mx[:, None] * mx[None, :])
+    nrm = torch.linalg.norm(a, dim=0)
+    bound = bound + 4 * rows * 2.0 ** -53 * (nrm[:, None] * nrm[None, :])
+    low = torch.tril(torch.ones_like(ref, dtype=torch.bool))
+    err = (g - ref).abs()
+    assert bool((err[low] <= bound[low]).all()), float((err - bound)[low].max())
+    assert bool((g[~low] == 0).all())  # upper triangle untouched
+    return err, ref, low
+
+
+@pytest.mark.parametrize("rows,n", [(1000, 300), (70_000, 257), (333, 4000), (500, 5000),
+                                    (17, 263), (4099, 1024)])
+@pytest.mark.parametrize("ns", [7, 5])
+def test_gram_within_digit_plane_bound(rows, n, ns):
+    torch = _torch()
+    gen = torch.Generator(device="cuda").manual_seed(rows * 7 + n)
+    a = torch.randn(rows, n, dtype=torch.float64, device="cuda", generator=gen)
+    g = F.gram(a, slices=ns)
+    err, ref, low = _check_bound(a, g, ns)
+    if ns == 7:
+        assert float(torch.linalg.norm(err[low]) / torch.linalg.norm(ref[low])) < 1e-13
+
+
+def test_gram_native_matches_torch():
+    torch = _torch()
+    a = torch.randn(3000, 700, dtype=torch.float64, device="cuda")
+    g = F.gram(a, slices=0)
+    ref = a.t() @ a
+    low = torch.tril(torch.ones_like(ref, dtype=torch.bool))
+    assert float((g - ref).abs()[low].max() / ref.abs().max()) < 1e-13
+
+
+def test_gram_wild_column_scales_and_zero_columns():
+    torch = _torch()
+    rng = np.random.default_rng(5)
+    rows, n = 20_000, 600
+    a = torch.randn(rows, n, dtype=torch.float64, device="cuda")
+    scales = torch.tensor(2.0 ** rng.integers(-40, 41, n), dtype=torch.float64, device="cuda")
+    a = a * scales[None, :]
+    a[:, 7] = 0.0
+    a[:, 300] = 0.0
+    a[123, 55] = 1e9  # one outlier dominating its column
+    for ns in (7, 9, 4):
+        g = F.gram(a, slices=ns)
+        _check_bound(a, g, ns)
+        assert bool((g[7, :] == 0).all()) and bool((g[:, 300] == 0).all())
+
+
+def test_gram_bitexact_when_entries_fit_the_planes():
+    # Integers below 2^11 need only the first two digit planes (6 + 7 bits):
+    # every C_t is exact, no dropped term is nonzero, and the fp64 fold of
+    # integer sums < 2^53 is exact.
+    torch = _torch()
+    rng = np.random.default_rng(9)
+    rows, n = 40_000, 320
+    ai = rng.integers(-2047, 2048, size=(rows, n))
+    ai[:, 0] = 2047  # pin every column max to the same exponent ...
+    ai[:, 1] = 0
+    ai[0, :] = 2047  # ... then the planes hold every entry exactly
+    a = torch.tensor(ai, dtype=torch.float64, device="cuda")
+    exact = ai.T.astype(np.int64) @ ai.astype(np.int64)
+    g = F.gram(a, slices=7).cpu().numpy()
+    low = np.tril(np.ones((n, n), dtype=bool))
+    assert np.array_equal(g[low], exact[low].astype(np.float64))
+
+
+def test_gram_rejects_bad_arguments():
+    torch = _torch()
+    a = torch.randn(10, 300, dtype=torch.float64, device="cuda")
+    with pytest.raises(F.FstkValueError):
+        F.gram(a, slices=3)
+    with pytest.raises(F.FstkValueError):
+        F.gram(a, slices=10)
+
+
+def _problem(ranks, q, seed, degree=8, nnz=5):
+    m = synth.random_model(ranks, [degree] * len(ranks), nnz, seed=seed)
+    pts = synth.uniform_points(q, len(ranks), seed + 1)
+    vals = synth.flame_field(pts, seed=seed + 2) if len(ranks) == 3 else np.sin(pts.sum(axis=1))
+    return m, pts, vals
+
+
+@pytest.mark.parametrize("t", ["dct", "wht", "fft", "none"])
+def test_sliced_refit_matches_native_and_oracle(O, t):
+    m, pts, vals = _problem((8, 8, 6), 60_000, 11)
+    prev = F.gram_slices(7)
+    try:
+        new_s, info_s = F.reestimate_core(m, pts, vals, seed=5, transform=t)
+        F.gram_slices(0)
+        new_n, info_n = F.reestimate_core(m, pts, vals, seed=5, transform=t)
+    finally:
+        F.gram_slices(prev)
+    assert info_s["gram_slices"] == 7 and info_n["gram_slices"] == 0
+    assert info_s["gram_int8_ops"] > 0 and info_n["gram_int8_ops"] == 0
+    cs, cn = new_s.core.reshape(-1, order="F"), new_n.core.reshape(-1, order="F")
+    assert rel(cs, cn) <= 1e-12
+    core_o, _ = O.reestimate_core(m, pts, vals, seed=5, transform=t)
+    assert rel(cs, core_o) <= CORE_TOL
+    assert not info_s["rank_deficient"]
+
+
+def test_sliced_refit_sharded_matches_oracle(O):
+    # Two row shards on one GPU with the all-reduces done by hand: the
+    # dist.py algorithm (summed sliced Grams, refinement with summed
+    # corrections) lands on the oracle's QR core.
+    torch = _torch()
+    m, pts, vals = _problem((8, 8, 6), 60_000, 13)
+    R = 8 * 8 * 6
+    prev = F.gram_slices(7)
+    sessions = []
+    try:
+        sessions = [F.RefitSession(m, pts, vals, seed=3, shard=k, shards=2) for k in range(2)]
+        gs = [torch.empty(R * R, dtype=torch.float64, device="cuda") for _ in range(2)]
+        rs = [torch.empty(R, dtype=torch.float64, device="cuda") for _ in range(2)]
+        for s, g, r in zip(sessions, gs, rs):
+            s.normal_equations(g, r)
+            assert s.info.gram_slices == 7
+        gsum, rsum = gs[0] + gs[1], rs[0] + rs[1]
+        xs = [torch.empty_like(rsum) for _ in range(2)]
+        for s, x in zip(sessions, xs):
+            assert s.factor(gsum, rsum, x)
+        for _ in range(4):
+            parts = [torch.empty_like(rsum) for _ in range(2)]
+            for s, x, p in zip(sessions, xs, parts):
+                s.correction(x, p)
+            tot = parts[0] + parts[1]
+            for s, x in zip(sessions, xs):
+                s.apply(tot, x)
+        assert torch.equal(xs[0], xs[1])
+        core = sessions[0].finish(xs[0])
+        core_o, _ = O.reestimate_core(m, pts, vals, seed=3)
+        assert rel(core, core_o) <= CORE_TOL
+    finally:
+        for s in sessions:
+            s.close()
+        F.gram_slices(prev)
+
+
+def _ill_conditioned_model(seed=21):
+    """Mode functions 0 and 1 nearly collinear in every mode: the design
+    columns then have cond ~1e6 or worse."""
+    m = synth.random_model((8, 8, 6), (8, 8, 8), 9, seed=seed)  # R = 384: sliced path
+    modes = [list(mk) for mk in m.modes]
+    for k in range(3):
+        base = modes[k][0]
+        coeffs = [(i, c * (1.0 + 1e-6 * (j + 1))) for j, (i, c) in enumerate(base.coeffs)]
+        modes[k][1] = F.ModeFunction(base.basis, coeffs)
+    return F.Model(m.core, modes, m.metadata)
+
+
+def test_sliced_gram_falls_back_when_it_cannot_precondition(O):
+    m = _ill_conditioned_model()
+    pts = synth.uniform_points(40_000, 3, 2)
+    vals = synth.flame_field(pts, seed=4)
+    prev = F.gram_slices(4)
+    try:
+        new_s, info_s = F.reestimate_core(m, pts, vals, seed=8)
+        F.gram_slices(0)
+        new_n, info_n = F.reestimate_core(m, pts, vals, seed=8)
+    finally:
+        F.gram_slices(prev)
+    # 4 planes (28 bits) cannot precondition cond(A)^2 ~ 1e12: the solve
+    # redoes the system on the native Gram and lands on the native answer.
+    assert info_s["gram_slices"] == 0
+    assert info_s["rank_deficient"] == info_n["rank_deficient"]
+    assert rel(new_s.core.reshape(-1, order="F"), new_n.core.reshape(-1, order="F")) <= 1e-9
+
+
+def test_gram_slices_setting_roundtrip():
+    prev = F.gram_slices()
+    try:
+        assert F.gram_slices(5) == prev
+        assert F.gram_slices() == 5
+        F.gram_slices(12)
+        assert F.gram_slices() == 9  # clamped to 4..9
+        F.gram_slices(2)
+        assert F.gram_slices() == 4
+        F.gram_slices(0)
+        assert F.gram_slices() == 0
+    finally:
+        F.gram_slices(prev)
