@@ -198,11 +198,19 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* refit, double* gr
                                                double* rhs, fstk_reestimate_info* info,
                                                fstk_gpu_error* err);
 /* Process-wide Gram arithmetic: slices > 0 runs A^T A as int8 tensor-core
- * GEMMs over that many exact 7-bit digit planes (4..9, default 7 or
+ * GEMMs over that many exact 7-bit digit planes (4..9, default 5 or
  * $FSTK_GRAM_SLICES); 0 selects the native fp64 Gram; < 0 only queries.
- * Returns the previous setting.  No reference counterpart (an arithmetic
- * choice of this backend; the solution still matches the reference's QR). */
+ * Returns the previous setting.  solve() escalates a sliced Gram that cannot
+ * precondition the system: upgrade to 7 planes, then the native Gram.  No
+ * reference counterpart (an arithmetic choice of this backend; the solution
+ * still matches the reference's QR). */
 int32_t fstk_gpu_gram_slices(int32_t slices);
+/* Writes into delta (device, R x R, lower triangle, rest zero) the plane sums
+ * that turn this shard's current sliced Gram into the `slices`-plane Gram
+ * (digits are a prefix code: exact).  Sharded runs all-reduce delta and add
+ * it to the summed Gram, then factor() again. */
+int32_t fstk_gpu_refit_gram_upgrade(fstk_gpu_refit* refit, int32_t slices, double* delta,
+                                    fstk_reestimate_info* info, fstk_gpu_error* err);
 /* gram (n x n, column-major, lower triangle written) = A^T A for a DEVICE
  * matrix A (rows x n, column-major, lda), with `slices` digit planes
  * (0 = native fp64 DSYRK/DGEMM), on `stream` (cudaStream_t, NULL = default).

@@ -42,10 +42,11 @@ namespace fstk_gpu {
 namespace {
 
 constexpr int kDigitMax = 64;
-constexpr int kDefaultSlices = 7;
+constexpr int kDefaultSlices = 5;
+constexpr int kMaxSlices = 9;
 std::atomic<int> g_slices{-1};
 
-int clamp_slices(int v) { return v <= 0 ? 0 : std::min(std::max(v, 4), 9); }
+int clamp_slices(int v) { return v <= 0 ? 0 : std::min(std::max(v, 4), kMaxSlices); }
 
 struct LtState {
   cublasLtHandle_t lt = nullptr;
@@ -115,19 +116,29 @@ __global__ void slice_kernel(const double* __restrict__ A, int64_t lda, int64_t 
   }
 }
 
-// G[c0+i][c0+j] (+)= 2^(e_i+e_j) sum_t 2^(2-7t) C_t[i][j] for the valid rows
-// i >= j of the column block (the lower triangle the solver reads).
-__global__ void fold_kernel(const int32_t* __restrict__ C, int64_t cstride, int ns, int64_t m,
-                            int w, int c0, int n, const int* __restrict__ ex,
-                            double* __restrict__ G, int accumulate) {
+// 2^e as a double for |e| <= 1022 (exact; built from the exponent field).
+__device__ __forceinline__ double pow2(int e) {
+  return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+}
+
+// G[c0+i][c0+j] (+)= 2^(e_i+e_j) sum_{t>=t_lo} 2^(2-7t) C_t[i][j] for the valid rows
+// i >= j of the column block (the lower triangle the solver reads).  The
+// plane weights are exact powers of two, applied smallest first.
+__global__ void __launch_bounds__(256) fold_kernel(const int32_t* __restrict__ C, int64_t cstride,
+                                                   int ns, int t_lo, int64_t m, int w, int c0, int n,
+                                                   const int* __restrict__ ex,
+                                                   double* __restrict__ G, int accumulate) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   if (i >= m || j >= w || i < j || c0 + i >= n || c0 + j >= n) return;
   const int64_t e = i + static_cast<int64_t>(j) * m;
+  const int32_t* c = C + e;
   double v = 0.0;
-  for (int t = ns + 1; t >= 2; --t)
-    v += ldexp(static_cast<double>(C[static_cast<int64_t>(t - 2) * cstride + e]), 2 - 7 * t);
-  v = ldexp(v, ex[c0 + i] + ex[c0 + j]);
+  for (int t = ns + 1; t >= t_lo; --t)
+    v += static_cast<double>(__ldg(c + static_cast<int64_t>(t - t_lo) * cstride)) * pow2(2 - 7 * t);
+  // e_i + e_j may leave the normal range only for absurd column scales.
+  const int sc = ex[c0 + i] + ex[c0 + j];
+  v = (sc > -1000 && sc < 1000) ? v * pow2(sc) : ldexp(v, sc);
   double* g = G + (c0 + i) + static_cast<int64_t>(c0 + j) * n;
   *g = accumulate ? *g + v : v;
 }
@@ -205,26 +216,53 @@ bool gram_sliced_applies(int64_t rows, int n) { return gram_slices() > 0 && n >=
 // gram (n x n, col-major, lower triangle) = beta * gram + A^T A over `rows`
 // rows of A (col-major, lda).
 double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n, double* gram,
-                              double beta, int ns, cudaStream_t s, int device, GramScratch& sc) {
+                              double beta, int ns, int t_lo, cudaStream_t s, int device,
+                              GramScratch& sc) {
   double ops = 0.0;
-  require(ns >= 4 && ns <= 9, FSTK_E_PARAMETER, "sliced Gram: 4..9 digit planes");
+  require(ns >= 4 && ns <= kMaxSlices, FSTK_E_PARAMETER, "sliced Gram: 4..9 digit planes");
+  require(t_lo >= 2 && t_lo <= ns + 1, FSTK_E_PARAMETER, "sliced Gram: bad plane range");
+  const int nt = ns + 2 - t_lo;  // plane sums t_lo..ns+1
   LtState& st = lt_state(device);
   const int64_t np = round_up(static_cast<int64_t>(n), 16);
-  // Segment rows: int32-exact bound, 65536 cap, and <= ~8 GB of digit planes.
-  int64_t kmax = ((int64_t(1) << 31) - 1) / (int64_t(kDigitMax) * kDigitMax * ns);
-  kmax = std::min<int64_t>(kmax, 65536);
-  const int64_t plane_budget = int64_t(8) << 30;
-  kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, plane_budget / (2 * ns * np)));
-  kmax &= ~int64_t(15);
-  const int64_t kp = std::min<int64_t>(kmax, round_up(rows, 16));
-  // Column blocks: C_t planes (ns of them, m x w int32) within ~4 GB.
-  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * ns * 4));
+  // Column blocks: C_t planes (ns of them, m x w int32) within ~4 GB; 2048
+  // wide by default, so the wasted upper half of each diagonal block (the
+  // GEMMs compute full m x w tiles) stays ~6% of the triangle.
+  static const int64_t block_cap = [] {
+    const char* e = std::getenv("FSTK_GRAM_BLOCK");
+    return e ? std::max<int64_t>(256, std::atoll(e)) : int64_t(2048);
+  }();
+  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nt * 4));
   w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), 16), np);
-  if (w > 4096 && np > 4096) w = 4096;
+  if (w > block_cap && np > block_cap) w = round_up(block_cap, 16);
+  // Segment rows: int32-exact for any plane count, digit planes (X and Y)
+  // within a third of the free memory (at most 24 GB), 16384 by default
+  // (measured best at C2: longer K makes cuBLASLt pick slower kernels).  The
+  // first call on a scratch fixes the segment length: the per-segment column
+  // exponents, hence the digits, must be the same when a later call adds
+  // more plane sums (the progressive upgrade in fstk_refit.cu).
+  int64_t kmax = ((int64_t(1) << 31) - 1) / (int64_t(kDigitMax) * kDigitMax * kMaxSlices);
+  kmax = std::min<int64_t>(kmax, 65536);
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    free_b = size_t(24) << 30;
+  }
+  const int64_t have = static_cast<int64_t>(sc.X.n + sc.Y.n);  // reusable scratch
+  const int64_t plane_budget =
+      std::min<int64_t>(int64_t(24) << 30, (static_cast<int64_t>(free_b) + have) / 3);
+  kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, plane_budget / (2 * ns * np)));
+  static const int64_t seg_cap = [] {
+    const char* e = std::getenv("FSTK_GRAM_SEG");
+    return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(16384);
+  }();
+  kmax = std::min(kmax, seg_cap);
+  kmax &= ~int64_t(15);
+  if (sc.kp == 0) sc.kp = kmax;
+  const int64_t kp = std::min<int64_t>(sc.kp, round_up(rows, 16));
   const int64_t ld = ns * kp;
   sc.X.ensure(static_cast<size_t>(ld * np));
   sc.Y.ensure(static_cast<size_t>(ld * np));
-  sc.C.ensure(static_cast<size_t>(ns) * np * w);
+  sc.C.ensure(static_cast<size_t>(nt) * np * w);
   sc.ex.ensure(static_cast<size_t>(np));
   sc.ws.ensure(size_t(32) << 20);
   DevBuf<int8_t>& X = sc.X;
@@ -242,15 +280,15 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
     for (int64_t c0 = 0; c0 < np; c0 += w) {
       const int64_t wn = std::min(w, np - c0);
       const int64_t m = np - c0;
-      for (int t = 2; t <= ns + 1; ++t) {
+      for (int t = t_lo; t <= ns + 1; ++t) {
         const int64_t K = (t - 1) * kp;
         ops += 2.0 * static_cast<double>(m) * static_cast<double>(wn) * static_cast<double>(K);
         imma_tn(st, sc.ws, m, wn, K, X.p + c0 * ld, ld, Y.p + c0 * ld + (ns - t + 1) * kp, ld,
-                Cb.p + static_cast<int64_t>(t - 2) * m * wn, m, s);
+                Cb.p + static_cast<int64_t>(t - t_lo) * m * wn, m, s);
       }
       dim3 fg(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(wn));
       const int acc = (!first || beta != 0.0) ? 1 : 0;
-      fold_kernel<<<fg, 256, 0, s>>>(Cb.p, m * wn, ns, m, static_cast<int>(wn),
+      fold_kernel<<<fg, 256, 0, s>>>(Cb.p, m * wn, ns, t_lo, m, static_cast<int>(wn),
                                      static_cast<int>(c0), n, ex.p, gram, acc);
       check_launch("fold_kernel");
     }

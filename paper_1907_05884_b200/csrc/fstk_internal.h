@@ -190,12 +190,17 @@ struct GramScratch {
   DevBuf<int32_t> C;       // ns planes of one column block
   DevBuf<int> ex;          // per-column exponents of the current segment
   DevBuf<uint8_t> ws;      // cuBLASLt workspace
+  int64_t kp = 0;          // segment rows, fixed by the first call
 };
 int gram_slices();                      // 0 = native fp64 DSYRK/DGEMM Gram
 int set_gram_slices(int slices);        // returns the previous setting
 bool gram_sliced_applies(int64_t rows, int n);
-// Returns the int8 tensor-core ops (2 x multiply-adds) issued.
+// gram = beta * gram + the plane sums t_lo..slices+1 of A^T A (t_lo = 2:
+// the whole sliced Gram; t_lo = s0 + 2 upgrades an s0-plane Gram to
+// `slices` planes exactly).  Returns the int8 tensor-core ops issued.
 double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n, double* gram,
-                              double beta, int slices, cudaStream_t s, int device, GramScratch& sc);
+                              double beta, int slices, int t_lo, cudaStream_t s, int device,
+                              GramScratch& sc);
+constexpr int kGramUpgradeSlices = 7;   // escalation target before the native Gram
 
 }  // namespace fstk_gpu

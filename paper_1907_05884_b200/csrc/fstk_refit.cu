@@ -1230,7 +1230,7 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
           ProfScope prof(FSTK_PROF_GRAM, s);
           const double beta = r0 == 0 ? 0.0 : 1.0;
           if (sliced)
-            i8ops += gram_accumulate_sliced(W.p, BS, nb_rows, n, gram, beta, rf->gram_used, s,
+            i8ops += gram_accumulate_sliced(W.p, BS, nb_rows, n, gram, beta, rf->gram_used, 2, s,
                                             rf->device, rf->gs);
           else
             gram_accumulate(h.blas, W.p, static_cast<int>(BS), static_cast<int>(nb_rows), n, gram,
@@ -1245,7 +1245,7 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
       } else {
         ProfScope prof(FSTK_PROF_GRAM, s);
         if (sliced)
-          i8ops = gram_accumulate_sliced(rf->A.p, arows, arows, n, gram, 0.0, rf->gram_used, s,
+          i8ops = gram_accumulate_sliced(rf->A.p, arows, arows, n, gram, 0.0, rf->gram_used, 2, s,
                                          rf->device, rf->gs);
         else
           gram_accumulate(h.blas, rf->A.p, static_cast<int>(arows), static_cast<int>(arows), n,
@@ -1264,7 +1264,77 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
     }
   }
 }
+
+// delta = the plane sums (from+2 .. to+1) of this shard's A^T A, lower
+// triangle (rest zero).  The digits are a prefix code, so a `from`-plane Gram
+// plus delta is exactly the `to`-plane Gram (same segments, same exponents).
+static double gram_upgrade_delta(fstk_gpu_refit* rf, int to, double* delta) {
+  DeviceGuard dg(rf->device);
+  cudaStream_t s = rf->stream;
+  const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
+  const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
+  const int n = static_cast<int>(rf->R);
+  const int from = rf->gram_used;
+  FSTK_CUDA(cudaMemsetAsync(delta, 0, static_cast<size_t>(n) * n * 8, s));
+  double ops = 0.0;
+  if (arows > 0) {
+    if (rf->none) {
+      const int64_t BS = none_block_rows(rf, true);
+      DevBuf<double> W(static_cast<size_t>(BS) * rf->R);
+      for (int64_t r0 = 0; r0 < arows; r0 += BS) {
+        const int64_t nb_rows = std::min(BS, arows - r0);
+        generate_design_block(rf, r0, nb_rows, W.p, BS, s);
+        ProfScope prof(FSTK_PROF_GRAM, s);
+        ops += gram_accumulate_sliced(W.p, BS, nb_rows, n, delta, 1.0, to, from + 2, s,
+                                      rf->device, rf->gs);
+      }
+    } else {
+      ProfScope prof(FSTK_PROF_GRAM, s);
+      ops = gram_accumulate_sliced(rf->A.p, arows, arows, n, delta, 1.0, to, from + 2, s,
+                                   rf->device, rf->gs);
+    }
+  }
+  FSTK_CUDA(cudaStreamSynchronize(s));
+  rf->gram_used = to;
+  return ops;
+}
+
+__global__ void add_inplace_kernel(double* __restrict__ y, const double* __restrict__ x,
+                                   int64_t count) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] += x[i];
+}
 }  // namespace fstk_gpu
+
+int32_t fstk_gpu_refit_gram_upgrade(fstk_gpu_refit* rf, int32_t slices, double* delta,
+                                    fstk_reestimate_info* info, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    require(rf && delta, FSTK_E_PARAMETER, "null argument");
+    const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
+    const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
+    require(rf->gram_used > 0 || arows == 0 || rf->R < 256, FSTK_E_PARAMETER,
+            "gram_upgrade: the last Gram of this refit was not sliced");
+    require(slices > rf->gram_used && slices <= 9, FSTK_E_PARAMETER,
+            "gram_upgrade: slices must exceed the current planes (at most 9)");
+    EventTimer tg(rf->stream);
+    if (rf->gram_used == 0) {  // empty shard or tiny system: nothing to add
+      DeviceGuard dg(rf->device);
+      FSTK_CUDA(cudaMemsetAsync(delta, 0, static_cast<size_t>(rf->R) * rf->R * 8, rf->stream));
+      FSTK_CUDA(cudaStreamSynchronize(rf->stream));
+      rf->gram_used = slices;
+      if (info) info->gram_slices = slices;
+      return;
+    }
+    const double ops = gram_upgrade_delta(rf, slices, delta);
+    if (info) {
+      info->t_gram += tg.seconds();
+      info->gram_slices = slices;
+      info->gram_int8_ops += ops;
+    }
+  });
+}
 
 int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
                                         fstk_reestimate_info* info, fstk_gpu_error* err) {
@@ -1298,7 +1368,7 @@ int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (slices > 0) {
       GramScratch sc;
-      gram_accumulate_sliced(a, lda, rows, n, gram, 0.0, slices, s, device, sc);
+      gram_accumulate_sliced(a, lda, rows, n, gram, 0.0, slices, 2, s, device, sc);
       FSTK_CUDA(cudaStreamSynchronize(s));
       return;
     }
@@ -1551,22 +1621,55 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     DevBuf<double> x(n), sv(n);
     auto rc = [&](int32_t c) { rethrow_stage(c, err); };
     rc(fstk_gpu_refit_factor(rf, gram_in, rhs_in, x.p, info, err));
-    // The sliced int8 Gram is a preconditioner-grade A^T A; whenever it is not
-    // positive definite or refinement does not contract, redo the system with
-    // the native fp64 Gram so those cases follow the exact fp64 path.
-    DevBuf<double> g2, r2;
-    auto native_refactor = [&] {
+    // Escalation ladder for the sliced int8 Gram (a preconditioner-grade
+    // A^T A): when it is not positive definite or refinement contracts slowly
+    // or stalls, add the missing plane sums up to kGramUpgradeSlices (exactly
+    // the higher-precision Gram), then fall back to the native fp64 Gram, so
+    // hard systems end on the exact fp64 path.
+    DevBuf<double> g2, r2, delta;
+    const double* gcur = gram_in;
+    const double* rcur = rhs_in;
+    auto escalate = [&]() -> bool {
+      if (rf->gram_used == 0) return false;
       fstk_reestimate_info li{};
-      g2.ensure(static_cast<size_t>(n) * n);
-      r2.ensure(static_cast<size_t>(n));
-      rc(fstk_gpu_refit_normal_equations_native(rf, g2.p, r2.p, &li, err));
-      rc(fstk_gpu_refit_factor(rf, g2.p, r2.p, x.p, info, err));
-      if (info) {
-        info->t_gram += li.t_gram;
-        info->gram_slices = 0;
+      if (rf->gram_used < kGramUpgradeSlices) {
+        delta.ensure(static_cast<size_t>(n) * n);
+        rc(fstk_gpu_refit_gram_upgrade(rf, kGramUpgradeSlices, delta.p, &li, err));
+        if (gcur != g2.p) {
+          g2.ensure(static_cast<size_t>(n) * n);
+          FSTK_CUDA(cudaMemcpyAsync(g2.p, gcur, static_cast<size_t>(n) * n * 8,
+                                    cudaMemcpyDeviceToDevice, rf->stream));
+          gcur = g2.p;
+        }
+        add_inplace_kernel<<<4 * 148, 256, 0, rf->stream>>>(g2.p, delta.p,
+                                                             static_cast<int64_t>(n) * n);
+        check_launch("add_inplace_kernel");
+        if (info) {
+          info->t_gram += li.t_gram;
+          info->gram_int8_ops += li.gram_int8_ops;
+          info->gram_slices = rf->gram_used;
+        }
+      } else {
+        g2.ensure(static_cast<size_t>(n) * n);
+        r2.ensure(static_cast<size_t>(n));
+        rc(fstk_gpu_refit_normal_equations_native(rf, g2.p, r2.p, &li, err));
+        gcur = g2.p;
+        rcur = r2.p;
+        if (info) {
+          info->t_gram += li.t_gram;
+          info->gram_slices = 0;
+        }
       }
+      rc(fstk_gpu_refit_factor(rf, gcur, rcur, x.p, info, err));
+      return true;
     };
-    if (!rf->factored && rf->gram_used > 0) native_refactor();
+    auto escalate_until_factored = [&]() -> bool {
+      do {
+        if (!escalate()) return false;
+      } while (!rf->factored);
+      return true;
+    };
+    if (!rf->factored) escalate_until_factored();
     int steps = 0;
     if (rf->factored) {
       EventTimer tref(rf->stream);
@@ -1578,24 +1681,24 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
         ++steps;
         if (step <= 1e-15) break;
         // Stagnation at the rounding floor (||dx||/||x|| ~ cond(A) eps, about
-        // 1e-13 at C2) is convergence.  Not contracting above kStallFloor, or
-        // out of steps while still moving, is a stall: redo it on the native
-        // Gram if this one was sliced, else flag the system.
+        // 1e-13 at C2) is convergence.  Above kStallFloor: not contracting,
+        // contracting slower than 10x per step on a sliced Gram, or out of
+        // steps while still moving, escalates (or flags a native system).
         constexpr double kStallFloor = 1e-11;
         const bool flat = it >= 1 && step > 0.5 * prev;
         if (flat && step <= kStallFloor) break;
+        const bool slow = rf->gram_used > 0 && it >= 1 && step > kStallFloor && step > 0.1 * prev;
         const bool last = it == 7 && step > kStallFloor;
-        if (flat || last) {
-          if (last && rf->gram_used == 0) break;
+        if (flat || slow || last) {
           if (rf->gram_used > 0) {
-            native_refactor();
-            if (!rf->factored) break;
+            if (!escalate_until_factored()) break;
             prev = 1e300;
             it = -1;
             continue;
           }
-          // No contraction: cond(A)^2 eps is not small; keep the iterate but
-          // report the system as numerically rank deficient.
+          if (last) break;
+          // No contraction on the native Gram: cond(A)^2 eps is not small;
+          // keep the iterate but report the system as numerically rank deficient.
           rf->rank_def = true;
           break;
         }

@@ -37,36 +37,67 @@ def evaluate_sharded(model, points, rank: int, world: int):
 
 
 STALL_FLOOR = 1e-11  # ||dx||/||x|| below which a flat refinement has converged
+UPGRADE_SLICES = 7   # escalation target of a sliced Gram before the native one
 
 
-def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, sliced=None):
+def _max_over_ranks(v: int, group=None) -> int:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return int(v)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([int(v)], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return int(t.item())
+
+
+def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, used=None):
     """Cholesky of the summed Gram on every rank, then iterative refinement
     against the row-sharded sketch: each step needs one all-reduce of an
     R-vector.  Returns the solution tensor x (identical on all ranks).
 
-    With the sliced int8 Gram (fstk_gpu_gram_slices > 0) a Gram that is not
-    positive definite, or refinement that stops contracting, is redone once
-    with the native fp64 Gram (fstk_refit.cu: fstk_gpu_refit_solve does the
-    same on one GPU).  Both decisions depend only on all-reduced data, so
-    every rank takes the same branch."""
+    `used` = digit planes of the summed Gram (None: the max over ranks of
+    sess.info.gram_slices).  A sliced Gram that is not positive definite, or
+    whose refinement contracts slower than 10x per step or stalls, escalates
+    like fstk_gpu_refit_solve: first to UPGRADE_SLICES planes (all-reduced
+    exact delta), then to the native fp64 Gram.  Every decision depends only
+    on all-reduced data, so all ranks take the same branch."""
     import torch
     import torch.distributed as dist
 
     x = torch.empty_like(rhs)
-    if sliced is None:
-        from .refit import gram_slices
+    if used is None:
+        used = _max_over_ranks(sess.info.gram_slices, group)
 
-        sliced = gram_slices() > 0
+    def escalate():
+        nonlocal used
+        if used == 0:
+            return False
+        if used < UPGRADE_SLICES:
+            delta = torch.empty_like(gram)
+            sess.gram_upgrade(UPGRADE_SLICES, delta)
+            reduce_normal_equations(delta, torch.zeros(1, dtype=rhs.dtype, device=rhs.device),
+                                    group=group)
+            gram.add_(delta)
+            used = UPGRADE_SLICES
+        else:
+            sess.normal_equations_native(gram, rhs)
+            reduce_normal_equations(gram, rhs, group=group)
+            used = 0
+        return True
 
-    def native():
-        sess.normal_equations_native(gram, rhs)
-        reduce_normal_equations(gram, rhs, group=group)
-        return sess.factor(gram, rhs, x)
+    def escalate_until_factored():
+        while True:
+            if not escalate():
+                return False
+            if sess.factor(gram, rhs, x):
+                return True
 
     sess.info.refine_steps = 0
     ok = sess.factor(gram, rhs, x)
-    if not ok and sliced:
-        ok, sliced = native(), False
+    if not ok:
+        ok = escalate_until_factored()
     if not ok:
         return x
     s = torch.empty_like(rhs)
@@ -84,11 +115,10 @@ def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, sliced=No
         flat = it >= 1 and step > 0.5 * prev
         if flat and step <= STALL_FLOOR:
             break
-        if flat or (sliced and it == max_iter - 1 and step > STALL_FLOOR):
-            if not sliced:
-                break
-            ok, sliced = native(), False
-            if not ok:
+        slow = used > 0 and it >= 1 and step > STALL_FLOOR and step > 0.1 * prev
+        last = it == max_iter - 1 and step > STALL_FLOOR
+        if flat or slow or last:
+            if used == 0 or not escalate_until_factored():
                 break
             prev, it = float("inf"), 0
             continue

@@ -142,6 +142,13 @@ class RefitSession:
         check(lib().fstk_gpu_refit_normal_equations_native(
             self._h, gram_t.data_ptr(), rhs_t.data_ptr(), C.byref(self.info), C.byref(err)), err)
 
+    def gram_upgrade(self, slices, delta_t):
+        """Writes the plane sums that raise this shard's sliced Gram to
+        `slices` planes into delta_t (CUDA float64, R*R)."""
+        err = Err()
+        check(lib().fstk_gpu_refit_gram_upgrade(self._h, int(slices), delta_t.data_ptr(),
+                                                C.byref(self.info), C.byref(err)), err)
+
     def solve(self, gram_t, rhs_t) -> np.ndarray:
         core = np.zeros(self.R)
         err = Err()

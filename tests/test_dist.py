@@ -70,20 +70,24 @@ def test_gloo_world2_normal_equations_allreduce(O):
 # ---- refine_distributed control flow (sliced-Gram fallback), CPU-only -------
 class _ScriptedSession:
     """Stands in for RefitSession: factor() outcomes and refinement step sizes
-    follow a script, and every call is logged, so the fallback logic of
+    follow a script, and every call is logged, so the escalation logic of
     dist.refine_distributed can be checked without a GPU."""
 
-    def __init__(self, factor_ok, steps):
+    def __init__(self, factor_ok, steps, slices=5):
         import types
 
         self.factor_ok = list(factor_ok)
         self.steps = list(steps)
         self.calls = []
-        self.info = types.SimpleNamespace(refine_steps=0)
+        self.info = types.SimpleNamespace(refine_steps=0, gram_slices=slices)
 
     def factor(self, gram, rhs, x):
         self.calls.append("factor")
         return self.factor_ok.pop(0)
+
+    def gram_upgrade(self, slices, delta):
+        self.calls.append(f"upgrade{slices}")
+        delta.zero_()
 
     def normal_equations_native(self, gram, rhs):
         self.calls.append("native")
@@ -96,41 +100,82 @@ class _ScriptedSession:
         return self.steps.pop(0)
 
 
-def _refine(sess, sliced):
+def _refine(sess, used=None):
     import torch
 
     from paper_1907_05884_b200 import dist
 
-    g, r = torch.zeros(4), torch.zeros(2)
-    return dist.refine_distributed(sess, g, r, sliced=sliced)
+    g, r = torch.zeros(4, dtype=torch.float64), torch.zeros(2, dtype=torch.float64)
+    return dist.refine_distributed(sess, g, r, used=used)
 
 
-def test_refine_converges_at_rounding_floor_without_fallback():
+def test_refine_converges_at_rounding_floor_without_escalation():
     s = _ScriptedSession([True], [1e-9, 2e-13, 1.5e-13])
-    _refine(s, sliced=True)
-    assert "native" not in s.calls and s.info.refine_steps == 3
+    _refine(s)
+    assert "native" not in s.calls and "upgrade7" not in s.calls and s.info.refine_steps == 3
 
 
-def test_refine_not_pd_sliced_falls_back_once():
-    s = _ScriptedSession([False, True], [1e-9, 1e-16])
-    _refine(s, sliced=True)
-    assert s.calls[:3] == ["factor", "native", "factor"] and s.calls.count("native") == 1
+def test_refine_not_pd_escalates_upgrade_then_native():
+    s = _ScriptedSession([False, False, True], [1e-9, 1e-16])
+    _refine(s)
+    assert s.calls[:5] == ["factor", "upgrade7", "factor", "native", "factor"]
 
 
-def test_refine_stall_above_floor_falls_back_then_stops():
-    s = _ScriptedSession([True, True], [1e-3, 9e-4, 1e-9, 1e-16])
-    _refine(s, sliced=True)
-    assert s.calls.count("native") == 1 and s.calls.count("apply") == 4
+def test_refine_slow_contraction_upgrades_once():
+    s = _ScriptedSession([True, True], [1e-3, 5e-4, 1e-9, 1e-16])
+    _refine(s)
+    assert s.calls.count("upgrade7") == 1 and "native" not in s.calls
+    assert s.calls.count("apply") == 4
+
+
+def test_refine_seven_planes_go_straight_to_native():
+    s = _ScriptedSession([True, True], [1e-3, 9e-4, 1e-9, 1e-16], slices=7)
+    _refine(s)
+    assert "upgrade7" not in s.calls and s.calls.count("native") == 1
 
 
 def test_refine_native_stall_does_not_loop():
     s = _ScriptedSession([True], [1e-3, 9e-4])
-    _refine(s, sliced=False)
+    _refine(s, used=0)
     assert "native" not in s.calls and s.calls.count("apply") == 2
 
 
-def test_refine_slow_sliced_contraction_falls_back():
-    steps = [1e-2 * 0.4 ** k for k in range(8)] + [1e-16]
-    s = _ScriptedSession([True, True], steps)
-    _refine(s, sliced=True)
-    assert s.calls.count("native") == 1
+def test_refine_fast_contraction_keeps_five_planes():
+    s = _ScriptedSession([True], [1e-6, 1e-11 * 0.5, 1e-16])
+    _refine(s)
+    assert s.calls.count("apply") == 3 and "upgrade7" not in s.calls
+
+
+def _gloo_refine_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # Rank 1 holds no sampled rows (gram_slices 0); the max over ranks
+        # still selects the sliced ladder on both ranks.
+        s = _ScriptedSession([False, True], [1e-9, 1e-16], slices=5 if rank == 0 else 0)
+        _refine(s)
+        q.put((rank, s.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_refine_escalation_agrees_across_gloo_ranks():
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_gloo_refine_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert out[0] == out[1] and out[0][:3] == ["factor", "upgrade7", "factor"]

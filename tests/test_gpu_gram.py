@@ -6,8 +6,9 @@ Bars: every entry within the rigorous digit-plane bound
 (+ the fp64 reference's own rounding); bit-exact when the entries need no
 more bits than the planes hold; the refit core with the sliced Gram equal to
 the native-Gram core to 1e-12 and to the oracle's QR core to the north-star
-1e-9; systems the sliced Gram cannot precondition fall back to the native
-Gram (reported as gram_slices == 0) with the same answer."""
+1e-9; systems the sliced Gram cannot precondition escalate (more planes, then the
+native Gram) and land on the native answer; a Gram upgraded by the extra
+plane sums equals the higher-precision Gram."""
 import numpy as np
 import pytest
 
@@ -180,7 +181,7 @@ def _ill_conditioned_model(seed=21):
     return F.Model(m.core, modes, m.metadata)
 
 
-def test_sliced_gram_falls_back_when_it_cannot_precondition(O):
+def test_sliced_gram_escalates_when_it_cannot_precondition(O):
     m = _ill_conditioned_model()
     pts = synth.uniform_points(40_000, 3, 2)
     vals = synth.flame_field(pts, seed=4)
@@ -192,10 +193,64 @@ def test_sliced_gram_falls_back_when_it_cannot_precondition(O):
     finally:
         F.gram_slices(prev)
     # 4 planes (28 bits) cannot precondition cond(A)^2 ~ 1e12: the solve
-    # redoes the system on the native Gram and lands on the native answer.
-    assert info_s["gram_slices"] == 0
+    # escalates (7 planes, then the native Gram) and lands on the native answer.
+    assert info_s["gram_slices"] in (0, 7)
     assert info_s["rank_deficient"] == info_n["rank_deficient"]
     assert rel(new_s.core.reshape(-1, order="F"), new_n.core.reshape(-1, order="F")) <= 1e-9
+
+
+def test_gram_upgrade_is_the_higher_precision_gram():
+    # Digits are a prefix code: G(5 planes) + delta(5 -> 7) == G(7 planes)
+    # up to the fp64 rounding of the two folds.
+    torch = _torch()
+    m, pts, vals = _problem((8, 8, 6), 60_000, 17)
+    R = 384
+    prev = F.gram_slices(5)
+    try:
+        s5 = F.RefitSession(m, pts, vals, seed=2)
+        g5, r5 = (torch.empty(R * R, dtype=torch.float64, device="cuda"),
+                  torch.empty(R, dtype=torch.float64, device="cuda"))
+        s5.normal_equations(g5, r5)
+        assert s5.info.gram_slices == 5
+        delta = torch.empty_like(g5)
+        s5.gram_upgrade(7, delta)
+        assert s5.info.gram_slices == 7
+        with pytest.raises(F.FstkValueError):
+            s5.gram_upgrade(7, delta)  # already at 7 planes
+        F.gram_slices(7)
+        s7 = F.RefitSession(m, pts, vals, seed=2)
+        g7, r7 = torch.empty_like(g5), torch.empty_like(r5)
+        s7.normal_equations(g7, r7)
+        F.gram_slices(0)
+        sn = F.RefitSession(m, pts, vals, seed=2)
+        gn, rn = torch.empty_like(g5), torch.empty_like(r5)
+        sn.normal_equations(gn, rn)
+    finally:
+        F.gram_slices(prev)
+    low = torch.tril(torch.ones(R, R, dtype=torch.bool, device="cuda"))
+    up = (g5 + delta).view(R, R).t()
+    G7, GN, G5 = g7.view(R, R).t(), gn.view(R, R).t(), g5.view(R, R).t()
+    d = torch.sqrt(torch.diagonal(GN))
+    sc = d[:, None] * d[None, :]
+    assert float(((up - G7).abs() / sc)[low].max()) <= 1e-15
+    e7 = float(((G7 - GN).abs() / sc)[low].max())
+    e5 = float(((G5 - GN).abs() / sc)[low].max())
+    assert e7 < 1e-13 and e5 < 1e-9 and e7 < e5
+    assert torch.equal(r5, rn) and torch.equal(r7, rn)  # A^T b is always fp64
+    for s in (s5, s7, sn):
+        s.close()
+
+
+def test_default_five_planes_refit_matches_oracle(O):
+    m, pts, vals = _problem((8, 8, 6), 60_000, 19)
+    prev = F.gram_slices(5)
+    try:
+        new, info = F.reestimate_core(m, pts, vals, seed=4)
+    finally:
+        F.gram_slices(prev)
+    assert info["gram_slices"] in (5, 7)
+    core_o, _ = O.reestimate_core(m, pts, vals, seed=4)
+    assert rel(new.core.reshape(-1, order="F"), core_o) <= CORE_TOL
 
 
 def test_gram_slices_setting_roundtrip():
