@@ -36,6 +36,7 @@
 #include <mutex>
 #include <numeric>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "fstk_internal.h"
@@ -59,21 +60,54 @@ struct Rng {
     return x % n;
   }
   double sign() { return (next_u64() & 1ull) ? -1.0 : 1.0; }
+  // rng.cpp sample_without_replacement: a partial Fisher-Yates shuffle of
+  // [0, n) (swap i with i + uniform_index(n - i) for i < k), first k sorted.
+  // Replayed with O(k) state -- positions [0, k) in a dense array, displaced
+  // positions >= k in an open-addressing map -- so the same draws give the
+  // same sample without materialising n indices; sorted by a bitmap over
+  // [0, n) when that is cheaper than a comparison sort.
   std::vector<uint64_t> sample_without_replacement(uint64_t n, uint64_t k) {
     if (k >= n) {
       std::vector<uint64_t> all(n);
       std::iota(all.begin(), all.end(), 0);
       return all;
     }
-    std::vector<uint64_t> idx(n);
-    std::iota(idx.begin(), idx.end(), 0);
+    std::vector<uint64_t> pre(k);
+    std::iota(pre.begin(), pre.end(), 0);
+    int bits = 4;
+    while ((uint64_t(1) << bits) < 2 * k) ++bits;
+    const uint64_t cap = uint64_t(1) << bits, mask = cap - 1;
+    constexpr uint64_t kEmpty = ~uint64_t(0);
+    std::vector<std::pair<uint64_t, uint64_t>> tab(cap, {kEmpty, 0});
+    auto slot = [&](uint64_t key) -> std::pair<uint64_t, uint64_t>& {
+      uint64_t h = (key * 0x9e3779b97f4a7c15ull) >> (64 - bits);
+      while (tab[h].first != kEmpty && tab[h].first != key) h = (h + 1) & mask;
+      return tab[h];
+    };
     for (uint64_t i = 0; i < k; ++i) {
       const uint64_t j = i + uniform_index(n - i);
-      std::swap(idx[i], idx[j]);
+      const uint64_t vi = pre[i];
+      uint64_t vj;
+      if (j < k) {
+        vj = pre[j];
+        pre[j] = vi;
+      } else {
+        auto& e = slot(j);
+        vj = e.first == kEmpty ? j : e.second;
+        e = {j, vi};
+      }
+      pre[i] = vj;
     }
-    idx.resize(k);
-    std::sort(idx.begin(), idx.end());
-    return idx;
+    if (n / 64 <= 16 * k) {
+      std::vector<uint64_t> bm((n + 63) / 64, 0);
+      for (const uint64_t v : pre) bm[v >> 6] |= uint64_t(1) << (v & 63);
+      uint64_t o = 0;
+      for (uint64_t w = 0; w < bm.size(); ++w)
+        for (uint64_t b = bm[w]; b; b &= b - 1) pre[o++] = (w << 6) + __builtin_ctzll(b);
+    } else {
+      std::sort(pre.begin(), pre.end());
+    }
+    return pre;
   }
 };
 
@@ -472,6 +506,28 @@ __global__ void scaled_gather_kernel(const double* __restrict__ vals, const int6
   if (i < n) out[i] = xmul(scale, vals[src[i]]);
 }
 
+// True when no entry is Inf/NaN (exponent field all ones); host threads.
+static bool all_finite(const double* a, size_t n) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const size_t per = std::max<size_t>(size_t(1) << 20, (n + hw - 1) / hw);
+  const size_t nt = (n + per - 1) / per;
+  std::vector<char> bad(nt, 0);
+  auto work = [&](size_t t) {
+    const uint64_t* u = reinterpret_cast<const uint64_t*>(a);
+    const size_t lo = t * per, hi = std::min(n, lo + per);
+    uint64_t acc = 0;
+    for (size_t i = lo; i < hi; ++i) acc |= static_cast<uint64_t>(((u[i] >> 52) & 0x7ff) == 0x7ff);
+    bad[t] = acc != 0;
+  };
+  std::vector<std::thread> th;
+  for (size_t t = 1; t < nt; ++t) th.emplace_back(work, t);
+  if (nt > 0) work(0);
+  for (auto& x : th) x.join();
+  for (char b : bad)
+    if (b) return false;
+  return true;
+}
+
 __global__ void finite_check_kernel(const double* __restrict__ a, int64_t n, int* flag) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -852,7 +908,8 @@ struct fstk_gpu_refit {
   int64_t row_lo = 0, row_hi = 0, local_rows = 0;  // destination rows of this shard
   DevBuf<double> A;      // local_rows(x2 for FFT) x R, column-major
   DevBuf<double> b;
-  DevBuf<double> d_points, d_values;  // full dataset on device
+  DevBuf<double> d_points, d_values;  // working-subset rows (subset order) on device
+  std::vector<int64_t> subset;         // dataset row of each working-subset row
   DevBuf<double> val_points, val_values;
   int64_t n_val = 0;
   std::vector<double> h_val_values;
@@ -918,26 +975,27 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     FSTK_CUDA(cudaStreamCreateWithFlags(&rf->stream, cudaStreamNonBlocking));
     cudaStream_t s = rf->stream;
     EventTimer tprep(s);
-    // Upload the dataset and check finiteness on the device.
-    rf->d_points.alloc(static_cast<size_t>(q) * d);
-    rf->d_values.alloc(static_cast<size_t>(q));
-    FSTK_CUDA(cudaMemcpyAsync(rf->d_points.p, points, static_cast<size_t>(q) * d * 8,
-                              cudaMemcpyHostToDevice, s));
-    FSTK_CUDA(cudaMemcpyAsync(rf->d_values.p, values, static_cast<size_t>(q) * 8,
-                              cudaMemcpyHostToDevice, s));
+    // FSTK_DEBUG_TIMING=1: host wall time per prepare phase (stream synced).
+    static const bool dbg_timing = std::getenv("FSTK_DEBUG_TIMING") != nullptr;
+    auto tmark = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+      if (!dbg_timing) return;
+      cudaStreamSynchronize(s);
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "fstk prepare: %-22s %8.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - tmark).count());
+      tmark = now;
+    };
+    // PointCloud::from_data (ingest.cpp:19-31): every coordinate and value
+    // must be finite -- checked on the host (all cores) so that only the
+    // rows the refit reads (working subset + validation) travel to the GPU.
     {
-      DevBuf<int> flag(2);
-      FSTK_CUDA(cudaMemsetAsync(flag.p, 0, 8, s));
-      finite_check_kernel<<<592, 256, 0, s>>>(rf->d_points.p, q * d, flag.p);
-      check_launch("finite_check_kernel");
-      finite_check_kernel<<<592, 256, 0, s>>>(rf->d_values.p, q, flag.p + 1);
-      check_launch("finite_check_kernel");
-      int hf[2] = {0, 0};
-      FSTK_CUDA(cudaMemcpyAsync(hf, flag.p, 8, cudaMemcpyDeviceToHost, s));
-      FSTK_CUDA(cudaStreamSynchronize(s));
-      require(hf[0] == 0, FSTK_E_DATA, "point coordinates must be finite");
-      require(hf[1] == 0, FSTK_E_DATA, "sample values must be finite");
+      const bool ok_p = all_finite(points, static_cast<size_t>(q) * d);
+      const bool ok_v = all_finite(values, static_cast<size_t>(q));
+      require(ok_p, FSTK_E_DATA, "point coordinates must be finite");
+      require(ok_v, FSTK_E_DATA, "sample values must be finite");
     }
+    mark("finite check");
     // reestimate_core (randls.cpp:363-368)
     const uint64_t S = resolve_sample_rows(cfg->sample_rows, m->R);
     require(S > static_cast<uint64_t>(m->R), FSTK_E_PARAMETER,
@@ -952,32 +1010,45 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
       n_val = static_cast<uint64_t>(std::llround(cfg->validation_fraction * static_cast<double>(uq)));
       n_val = std::min<uint64_t>(std::min(n_val, uq - 1), 100000);
     }
-    std::vector<char> in_val(uq, 0);
-    rf->held_out = true;
-    if (n_val >= 1) {
+    // Validation rows (sorted) and the training rows = their complement in
+    // ascending order, never materialised: train_at() maps sorted positions
+    // into the complement by one merge against `val`.
+    std::vector<uint64_t> val;
+    rf->held_out = n_val >= 1;
+    if (rf->held_out) {
       Rng rng(mix_seed(cfg->seed, kValidationTag));
-      for (const auto i : rng.sample_without_replacement(uq, n_val)) in_val[i] = 1;
-    } else {
-      rf->held_out = false;
+      val = rng.sample_without_replacement(uq, n_val);
     }
-    std::vector<uint64_t> train, val;
-    train.reserve(uq - n_val);
-    val.reserve(n_val);
-    for (uint64_t i = 0; i < uq; ++i) (in_val[i] ? val : train).push_back(i);
-    if (!rf->held_out) val = train;
+    const uint64_t n_train = uq - val.size();
+    auto complement_of = [&](const std::vector<uint64_t>& pos) {
+      std::vector<int64_t> outv(pos.size());
+      uint64_t vi = 0;
+      for (size_t t = 0; t < pos.size(); ++t) {
+        uint64_t x = pos[t] + vi;
+        while (vi < val.size() && val[vi] <= x) x = pos[t] + ++vi;
+        outv[t] = static_cast<int64_t>(x);
+      }
+      return outv;
+    };
+    mark("validation split");
     const uint64_t q_w = cfg->working_subset == 0
-                             ? train.size()
-                             : std::min<uint64_t>(cfg->working_subset, train.size());
+                             ? n_train
+                             : std::min<uint64_t>(cfg->working_subset, n_train);
     require(q_w >= 1, FSTK_E_PARAMETER, "no training points left");
-    std::vector<int64_t> subset;
-    subset.reserve(q_w);
-    if (q_w == train.size()) {
-      for (auto i : train) subset.push_back(static_cast<int64_t>(i));
+    std::vector<int64_t> subset;  // dataset rows of the working subset, ascending
+    if (q_w == n_train) {
+      std::vector<uint64_t> all(n_train);
+      std::iota(all.begin(), all.end(), 0);
+      subset = complement_of(all);
     } else {
       Rng rng(mix_seed(cfg->seed, kSubsetTag));
-      for (const auto i : rng.sample_without_replacement(train.size(), q_w))
-        subset.push_back(static_cast<int64_t>(train[i]));
+      subset = complement_of(rng.sample_without_replacement(n_train, q_w));
     }
+    if (!rf->held_out) {  // no held-out points: validate on the training rows
+      val.resize(n_train);  // == q: every row
+      std::iota(val.begin(), val.end(), 0);
+    }
+    mark("working subset");
     rf->q_w = q_w;
     rf->S = S;
     rf->none = cfg->transform == FSTK_TRANSFORM_NONE;
@@ -986,26 +1057,42 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
                         : make_plan(q_w, S, mix_seed(cfg->seed, kSketchTag));
     rf->q_pad = rf->plan.q_pad;
     require(rf->q_pad < (uint64_t(1) << 31), FSTK_E_PARAMETER, "working subset too large");
-    // Validation points/values on the device.
+    mark("sketch plan");
+    // Compact upload: subset rows (in subset order) and validation rows.
+    rf->subset = subset;
+    rf->d_points.alloc(static_cast<size_t>(q_w) * d);
+    rf->d_values.alloc(static_cast<size_t>(q_w));
     rf->n_val = static_cast<int64_t>(val.size());
+    rf->val_points.alloc(static_cast<size_t>(std::max<int64_t>(rf->n_val, 1)) * d);
+    rf->val_values.alloc(static_cast<size_t>(std::max<int64_t>(rf->n_val, 1)));
     {
-      std::vector<int64_t> vi(val.begin(), val.end());
-      rf->h_val_index = vi;
-      DevBuf<int64_t> dvi(std::max<size_t>(vi.size(), 1));
-      FSTK_CUDA(cudaMemcpyAsync(dvi.p, vi.data(), vi.size() * 8, cudaMemcpyHostToDevice, s));
-      rf->val_points.alloc(static_cast<size_t>(std::max<int64_t>(rf->n_val, 1)) * d);
-      rf->val_values.alloc(static_cast<size_t>(std::max<int64_t>(rf->n_val, 1)));
-      if (rf->n_val > 0) {
-        gather_points_kernel<<<static_cast<unsigned>(ceil_div(rf->n_val, 256)), 256, 0, s>>>(
-            rf->d_points.p, q, d, dvi.p, rf->n_val, rf->val_points.p, rf->n_val,
-            rf->d_values.p, rf->val_values.p);
-        check_launch("gather_points_kernel");
+      const int64_t nv = rf->n_val;
+      std::vector<double> hp(static_cast<size_t>(q_w) * d), hv(q_w), vp(static_cast<size_t>(nv) * d);
+      rf->h_val_values.resize(nv);
+      rf->h_val_index.resize(nv);
+      for (int k = 0; k < d; ++k) {
+        const double* col = points + static_cast<int64_t>(k) * q;
+        double* dst = hp.data() + static_cast<size_t>(k) * q_w;
+        for (uint64_t t = 0; t < q_w; ++t) dst[t] = col[subset[t]];
+        double* vdst = vp.data() + static_cast<size_t>(k) * nv;
+        for (int64_t t = 0; t < nv; ++t) vdst[t] = col[val[t]];
       }
-      rf->h_val_values.resize(rf->n_val);
-      FSTK_CUDA(cudaMemcpyAsync(rf->h_val_values.data(), rf->val_values.p, rf->n_val * 8,
-                                cudaMemcpyDeviceToHost, s));
+      for (uint64_t t = 0; t < q_w; ++t) hv[t] = values[subset[t]];
+      for (int64_t t = 0; t < nv; ++t) {
+        rf->h_val_index[t] = static_cast<int64_t>(val[t]);
+        rf->h_val_values[t] = values[val[t]];
+      }
+      FSTK_CUDA(cudaMemcpyAsync(rf->d_points.p, hp.data(), hp.size() * 8, cudaMemcpyHostToDevice, s));
+      FSTK_CUDA(cudaMemcpyAsync(rf->d_values.p, hv.data(), hv.size() * 8, cudaMemcpyHostToDevice, s));
+      if (nv > 0) {
+        FSTK_CUDA(cudaMemcpyAsync(rf->val_points.p, vp.data(), vp.size() * 8,
+                                  cudaMemcpyHostToDevice, s));
+        FSTK_CUDA(cudaMemcpyAsync(rf->val_values.p, rf->h_val_values.data(), nv * 8,
+                                  cudaMemcpyHostToDevice, s));
+      }
       FSTK_CUDA(cudaStreamSynchronize(s));
     }
+    mark("compact upload");
     rf->row_lo = static_cast<int64_t>(S) * shard / shards;
     rf->row_hi = static_cast<int64_t>(S) * (shard + 1) / shards;
     rf->local_rows = rf->row_hi - rf->row_lo;
@@ -1013,7 +1100,7 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
       // Tables and rhs of this shard's sampled rows only; A is generated on demand.
       const int64_t nl = rf->local_rows;
       std::vector<int64_t> src(static_cast<size_t>(std::max<int64_t>(nl, 1)));
-      for (int64_t i = 0; i < nl; ++i) src[i] = subset[rf->plan.rows[rf->row_lo + i]];
+      for (int64_t i = 0; i < nl; ++i) src[i] = static_cast<int64_t>(rf->plan.rows[rf->row_lo + i]);
       DevBuf<int64_t> dsrc(src.size());
       FSTK_CUDA(cudaMemcpyAsync(dsrc.p, src.data(), src.size() * 8, cudaMemcpyHostToDevice, s));
       rf->ldt = round_up(std::max<int64_t>(nl, 1), 128);
@@ -1025,7 +1112,7 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
       rf->tables.alloc(static_cast<size_t>(tot));
       DevBuf<unsigned long long> derr(1);
       FSTK_CUDA(cudaMemsetAsync(derr.p, 0xff, 8, s));
-      launch_mode_tables(m, rf->d_points.p, q, nl, rf->ldt, dsrc.p, rf->tables.p, rf->toff,
+      launch_mode_tables(m, rf->d_points.p, static_cast<int64_t>(q_w), nl, rf->ldt, dsrc.p, rf->tables.p, rf->toff,
                          rf->ldt, true, derr.p, s);
       rf->b.alloc(static_cast<size_t>(std::max<int64_t>(nl, 1)));
       if (nl > 0) {
@@ -1037,7 +1124,7 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
       FSTK_CUDA(cudaMemcpyAsync(&bad, derr.p, 8, cudaMemcpyDeviceToHost, s));
       FSTK_CUDA(cudaStreamSynchronize(s));
       if (bad != ULLONG_MAX) {
-        const int64_t row = src[bad];
+        const int64_t row = subset[src[bad]];
         std::vector<double> y(d);
         for (int k = 0; k < d; ++k) y[k] = points[k * q + row];
         throw_domain(m, row, y.data());
@@ -1054,8 +1141,9 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
       return;
     }
     // Inputs in transform order; destination rows in last-pass visit order.
-    build_inputs(cfg->transform, rf->q_pad, q_w, rf->plan.signs, rf->plan.rows, false, subset,
+    build_inputs(cfg->transform, rf->q_pad, q_w, rf->plan.signs, rf->plan.rows, false, {},
                  true, rf->in, s);
+    mark("build inputs");
     // Mode tables over the padded positions, bit-exact (mode_value_tables, randls.cpp:21-41).
     int64_t toff[kMaxOrder], tot = 0;
     const int64_t ldt = static_cast<int64_t>(rf->q_pad);
@@ -1066,7 +1154,7 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     DevBuf<double> tables(static_cast<size_t>(tot));
     DevBuf<unsigned long long> derr(1);
     FSTK_CUDA(cudaMemsetAsync(derr.p, 0xff, 8, s));
-    launch_mode_tables(m, rf->d_points.p, q, static_cast<int64_t>(rf->q_pad),
+    launch_mode_tables(m, rf->d_points.p, static_cast<int64_t>(q_w), static_cast<int64_t>(rf->q_pad),
                        static_cast<int64_t>(rf->q_pad), rf->in.row_src.p, tables.p, toff, ldt,
                        true, derr.p, s);
     fold_sign_kernel<<<static_cast<unsigned>(ceil_div(ldt, 256)), 256, 0, s>>>(
@@ -1079,10 +1167,12 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
       // Map the failing table row back to the dataset row.
       int64_t src = -1;
       FSTK_CUDA(cudaMemcpy(&src, rf->in.row_src.p + bad, 8, cudaMemcpyDeviceToHost));
+      src = subset[src];
       std::vector<double> y(d);
       for (int k = 0; k < d; ++k) y[k] = points[k * q + src];
       throw_domain(m, src, y.data());
     }
+    mark("mode tables");
     if (info) info->t_prepare = tprep.seconds();
     // Sketch: all R design columns plus the rhs; this shard keeps its rows.
     const bool fft = cfg->transform == FSTK_TRANSFORM_FFT;
@@ -1591,7 +1681,8 @@ int32_t fstk_gpu_refit_finish(fstk_gpu_refit* rf, const double* x_dev, double* c
         const int64_t row = rf->h_val_index[bad];
         std::vector<double> y(rf->d);
         for (int k = 0; k < rf->d; ++k)
-          FSTK_CUDA(cudaMemcpy(&y[k], rf->d_points.p + k * rf->q + row, 8, cudaMemcpyDeviceToHost));
+          FSTK_CUDA(cudaMemcpy(&y[k], rf->val_points.p + k * rf->n_val + bad, 8,
+                               cudaMemcpyDeviceToHost));
         throw_domain(rf->model, row, y.data());
       }
       FSTK_CUDA(cudaMemcpyAsync(pred.data(), dp.p, rf->n_val * 8, cudaMemcpyDeviceToHost, s));
