@@ -256,7 +256,18 @@ struct PassParams {
   double* A;
   int64_t lda;
   double* b;
+  int prefetch;             // stage the next column with cp.async (see kernel)
+  int stg_off;              // byte offset of the staging buffer in shared memory
+  int compact;              // last pass: destination rows consecutive per CTA
+  int list_off;             // byte offset of the per-CTA sampled-element list
 };
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __device__ __forceinline__ double2 cmul_x(double2 x, double2 w) {
   // (a + ib)(c + id) = (ac - bd) + i(ad + bc), separately rounded (GCC's
@@ -370,11 +381,107 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
       tws[e] = P.tw[(int64_t(1) << (P.s0 + j)) - 1 + k];
     }
   }
+  // Prefetch (P.prefetch): the next column's inputs -- the intermediate's
+  // 16-byte element pairs, or the DT mode-table segments of a design column
+  // -- are copied into a shared staging buffer with cp.async while this
+  // column's butterflies run, so the strided global reads no longer stall
+  // the stages.  Data movement only: the arithmetic is unchanged.
+  unsigned char* stg = smem_raw + P.stg_off;
+  auto staged = [&](int cc) {
+    return P.prefetch && cc < ncols_batch && (P.src == SRC_BUFFER || P.col0 + cc < P.R);
+  };
+  auto prefetch = [&](int cc) {
+    if (!staged(cc)) return;
+    if (P.src == SRC_BUFFER) {
+      // G == 2: element pairs (e, e+1) are adjacent in global memory.
+      const int nch = REAL ? nel / 2 : nel;
+      for (int ch = threadIdx.x; ch < nch; ch += blockDim.x) {
+        const int e = REAL ? 2 * ch : ch;
+        const int64_t p = base + (e % G) + static_cast<int64_t>(e / G) * stride;
+        const void* src = REAL ? static_cast<const void*>(P.rbuf + static_cast<int64_t>(cc) * P.n + p)
+                               : static_cast<const void*>(P.cbuf + static_cast<int64_t>(cc) * P.n + p);
+        cp_async16(stg + static_cast<size_t>(ch) * 16, src);
+      }
+    } else if constexpr (DT > 0) {
+      // G == 1, stride 1: the CTA's positions are base .. base + nel - 1.
+      int64_t rem = P.col0 + cc;
+#pragma unroll
+      for (int k = 0; k < DT; ++k) {
+        const int64_t jk = rem % P.r[k];
+        rem /= P.r[k];
+        const double* t = P.tables + P.toff.v[k] + jk * P.ldt + base;
+        for (int ch = threadIdx.x; ch < nel / 2; ch += blockDim.x)
+          cp_async16(stg + (static_cast<size_t>(k) * nel + 2 * ch) * 8, t + 2 * ch);
+      }
+    }
+    cp_async_commit();
+  };
+  // Compact last pass: destination rows are assigned in last-pass visit
+  // order (build_inputs), so this CTA's sampled elements, in ascending e,
+  // own the consecutive rows first, first + 1, ...  Collect their e once;
+  // every column then stores only those (~S / q_pad of the elements) with
+  // coalesced post-factor reads and A writes, instead of reloading slot[]
+  // for all elements per column.
+  uint16_t* elist = reinterpret_cast<uint16_t*>(smem_raw + P.list_off);
+  __shared__ int s_wcnt[32];
+  __shared__ int s_cnt;
+  __shared__ int s_first;
+  const bool use_list = P.last && P.compact;
+  if (use_list) {
+    if (threadIdx.x == 0) {
+      s_cnt = 0;
+      s_first = 0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i0 = 0; i0 < nel; i0 += blockDim.x) {
+      const int e = i0 + threadIdx.x;
+      int sl = -1;
+      if (e < nel) sl = P.slot[base + (e % G) + static_cast<int64_t>(e / G) * stride];
+      const unsigned bal = __ballot_sync(0xffffffffu, sl >= 0);
+      if (lane == 0) s_wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int off = s_cnt;
+      for (int w = 0; w < warp; ++w) off += s_wcnt[w];
+      if (sl >= 0) {
+        const int pos = off + __popc(bal & ((1u << lane) - 1));
+        elist[pos] = static_cast<uint16_t>(e);
+        if (pos == 0) s_first = sl;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int tot = s_cnt;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_wcnt[w];
+        s_cnt = tot;
+      }
+      __syncthreads();
+    }
+  }
+  prefetch(blockIdx.y);
   for (int cc = blockIdx.y; cc < ncols_batch; cc += gridDim.y) {
     const int64_t col = P.col0 + cc;
     __syncthreads();
     // ---- load (generate the design column on the fly in the first pass)
-    if (P.src == SRC_BUFFER) {
+    if (staged(cc)) {
+      cp_async_wait_all();
+      __syncthreads();
+      if (P.src == SRC_BUFFER) {
+        const T* sv = reinterpret_cast<const T*>(stg);
+        for (int e = threadIdx.x; e < nel; e += blockDim.x) x[spad(e)] = sv[e];
+      } else if constexpr (DT > 0) {
+        const double* sv = reinterpret_cast<const double*>(stg);
+        for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+          // design_column (randls.cpp:44-52): ((u0 * u1) * u2) * ..., sign in u0.
+          double v = sv[e];
+#pragma unroll
+          for (int k = 1; k < DT; ++k) v = xmul(v, sv[k * nel + e]);
+          if constexpr (REAL)
+            x[spad(e)] = v;
+          else
+            x[spad(e)] = make_double2(v, 0.0);
+        }
+      }
+    } else if (P.src == SRC_BUFFER) {
 #pragma unroll 4
       for (int e = threadIdx.x; e < nel; e += blockDim.x) {
         const int64_t p = base + (e % G) + static_cast<int64_t>(e / G) * stride;
@@ -421,6 +528,7 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
       }
     }
     __syncthreads();
+    prefetch(cc + gridDim.y);  // staging is free: this column now lives in x
     // ---- stages, three per register round
     for (int j = 0; j < L; j += 3) {
       const int ns = min(3, L - j);
@@ -433,6 +541,29 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
       __syncthreads();
     }
     // ---- store
+    if (use_list) {
+      double* out = (col == P.R) ? P.b : P.A + P.lda * col;
+      const int cnt = s_cnt;
+      const int64_t first = s_first;
+      for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+        const int e = elist[idx];
+        const int64_t sl = first + idx;
+        if (sl < P.row_lo || sl >= P.row_hi) continue;
+        const int64_t dst = sl - P.row_lo;
+        if constexpr (REAL) {
+          out[dst] = xmul(P.scale, xmul(x[spad(e)], P.inv_sqrt_n));
+        } else if (P.kind == FSTK_TRANSFORM_DCT) {
+          const double2 V = x[spad(e)];
+          const double val = xsub(xmul(__ldg(P.post_re + sl), V.x), xmul(__ldg(P.post_im + sl), V.y));
+          out[dst] = xmul(P.scale, xmul(__ldg(P.post_c + sl), val));
+        } else {
+          const double2 V = x[spad(e)];
+          out[dst] = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
+          out[P.im_off + dst] = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
+        }
+      }
+      continue;
+    }
 #pragma unroll 4
     for (int e = threadIdx.x; e < nel; e += blockDim.x) {
       const int64_t p = base + (e % G) + static_cast<int64_t>(e / G) * stride;
@@ -573,6 +704,7 @@ struct SketchJob {
   double* A;
   int64_t lda;
   double* b;
+  bool compact = false;  // slot = last-pass visit order (build_inputs compact)
 };
 
 static int ilog2(uint64_t n) {
@@ -607,7 +739,10 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
   static std::once_flag attr_once[64];
   std::call_once(attr_once[device & 63], [&] {
     auto attr = [](const void* f) {
-      FSTK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+      FSTK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      // One carveout for every pass kernel: the passes alternate hundreds of
+      // times per sketch and must not trigger L1/shared reconfiguration.
+      FSTK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     };
     attr(reinterpret_cast<const void*>(transform_pass2_kernel<false, 1, 0>));
     attr(reinterpret_cast<const void*>(transform_pass2_kernel<true, 1, 0>));
@@ -662,8 +797,27 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       P.b = J.b;
       const int64_t E = int64_t(1) << P.L;
       const int64_t sets = static_cast<int64_t>(J.n) / (E * P.G);
-      const size_t smem = static_cast<size_t>(E * P.G + E * P.G / 8) * elem +
-                          (real ? 0 : static_cast<size_t>((E - 1) * P.G) * 16);
+      size_t smem = static_cast<size_t>(E * P.G + E * P.G / 8) * elem +
+                    (real ? 0 : static_cast<size_t>((E - 1) * P.G) * 16);
+      // cp.async staging of the next column (FSTK_SKETCH_PREFETCH=0 disables).
+      static const bool pf_on = [] {
+        const char* e = std::getenv("FSTK_SKETCH_PREFETCH");
+        return !(e && std::atoi(e) == 0);
+      }();
+      const int dtp = (P.src == SRC_TABLES && (J.d == 3 || J.d == 4)) ? J.d : 0;
+      size_t stg = 0;
+      if (pf_on && P.src == SRC_BUFFER && P.G == 2)
+        stg = static_cast<size_t>(E * P.G) * elem;
+      else if (pf_on && dtp > 0 && P.G == 1 && P.s0 == 0 && E * P.G >= 2)
+        stg = static_cast<size_t>(dtp) * E * P.G * 8;
+      smem = round_up(static_cast<int64_t>(smem), 16);
+      P.prefetch = stg > 0 ? 1 : 0;
+      P.stg_off = static_cast<int>(smem);
+      smem += stg;
+      P.compact = (J.compact && P.last && E * P.G <= 65536) ? 1 : 0;
+      smem = round_up(static_cast<int64_t>(smem), 16);
+      P.list_off = static_cast<int>(smem);
+      if (P.compact) smem += static_cast<size_t>(E * P.G) * sizeof(uint16_t);
       // ~4 columns per CTA: many short CTAs (small tail wave), twiddles still
       // amortised over several columns.
       static const int64_t cpc = [] {
@@ -1203,6 +1357,7 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     J.sgn = rf->in.sgn.p;
     J.row_src = rf->in.row_src.p;
     J.slot = rf->in.slot.p;
+    J.compact = true;
     J.post_re = rf->in.post_re.p;
     J.post_im = rf->in.post_im.p;
     J.post_c = rf->in.post_c.p;
