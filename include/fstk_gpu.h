@@ -197,23 +197,25 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* refit, double* gram,
 int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* refit, double* gram,
                                                double* rhs, fstk_reestimate_info* info,
                                                fstk_gpu_error* err);
-/* Process-wide Gram arithmetic: slices > 0 runs A^T A as int8 tensor-core
- * GEMMs over that many exact 7-bit digit planes (4..9, default 5 or
- * $FSTK_GRAM_SLICES); 0 selects the native fp64 Gram; < 0 only queries.
- * Returns the previous setting.  solve() escalates a sliced Gram that cannot
- * precondition the system: upgrade to 7 planes, then the native Gram.  No
- * reference counterpart (an arithmetic choice of this backend; the solution
- * still matches the reference's QR). */
+/* Process-wide Gram arithmetic: slices > 0 runs A^T A on the int8 tensor
+ * cores at the accuracy of that many 7-bit planes (4..7, default 4 or
+ * $FSTK_GRAM_SLICES): entries rounded to (7 slices - 1)-bit integers per
+ * column and segment, products exact (CRT over int8 residues; the
+ * digit-plane split with FSTK_GRAM_SCHEME=digits); 0 selects the native fp64
+ * Gram; < 0 only queries.  Returns the previous setting.  No reference
+ * counterpart (an arithmetic choice of this backend; the solution still
+ * matches the reference's QR). */
 int32_t fstk_gpu_gram_slices(int32_t slices);
-/* Writes into delta (device, R x R, lower triangle, rest zero) the plane sums
- * that turn this shard's current sliced Gram into the `slices`-plane Gram
- * (digits are a prefix code: exact).  Sharded runs all-reduce delta and add
- * it to the summed Gram, then factor() again. */
-int32_t fstk_gpu_refit_gram_upgrade(fstk_gpu_refit* refit, int32_t slices, double* delta,
-                                    fstk_reestimate_info* info, fstk_gpu_error* err);
+/* normal_equations() at an explicit Gram precision: slices 4..7 (sliced,
+ * int8 tensor cores) or 0 (native fp64).  solve() and dist.refine_distributed
+ * escalate with it: a sliced Gram that cannot precondition the system is
+ * recomputed at 7, then at 0. */
+int32_t fstk_gpu_refit_normal_equations_level(fstk_gpu_refit* refit, int32_t slices,
+                                              double* gram, double* rhs,
+                                              fstk_reestimate_info* info, fstk_gpu_error* err);
 /* gram (n x n, column-major, lower triangle written) = A^T A for a DEVICE
- * matrix A (rows x n, column-major, lda), with `slices` digit planes
- * (0 = native fp64 DSYRK/DGEMM), on `stream` (cudaStream_t, NULL = default).
+ * matrix A (rows x n, column-major, lda), at `slices` plane-accuracy (4..7)
+ * or native fp64 DSYRK/DGEMM (0), on `stream` (cudaStream_t, NULL = default).
  * The Gram stage of normal_equations() on its own, for tests and callers
  * that build their own design matrices. */
 int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t n,

@@ -85,7 +85,7 @@ EXPORTS = [
     "fstk_gpu_refit_finish", "fstk_gpu_evaluate_grid", "fstk_gpu_reconstruct_grid",
     "fstk_gpu_self_convergence", "fstk_gpu_leverage_scores", "fstk_gpu_point_major_to_soa",
     "fstk_gpu_refit_normal_equations_native", "fstk_gpu_gram_slices", "fstk_gpu_gram_device",
-    "fstk_gpu_refit_gram_upgrade",
+    "fstk_gpu_refit_normal_equations_level",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -134,8 +134,8 @@ def lib():
                                                          C.POINTER(Err)]
     L.fstk_gpu_gram_slices.argtypes = [C.c_int32]
     L.fstk_gpu_gram_slices.restype = C.c_int32
-    L.fstk_gpu_refit_gram_upgrade.argtypes = [VP, C.c_int32, VP, C.POINTER(ReestimateInfo),
-                                              C.POINTER(Err)]
+    L.fstk_gpu_refit_normal_equations_level.argtypes = [VP, C.c_int32, VP, VP,
+                                                        C.POINTER(ReestimateInfo), C.POINTER(Err)]
     L.fstk_gpu_gram_device.argtypes = [VP, C.c_int64, C.c_int64, C.c_int32, VP, C.c_int32,
                                        C.c_int32, VP, C.POINTER(Err)]
     L.fstk_gpu_refit_solve.argtypes = [VP, VP, VP, DP, C.POINTER(ReestimateInfo),

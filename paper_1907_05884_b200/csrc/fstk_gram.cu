@@ -29,6 +29,8 @@
 #include <cublasLt.h>
 
 #include <atomic>
+#include <cmath>
+#include <string>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -42,8 +44,8 @@ namespace fstk_gpu {
 namespace {
 
 constexpr int kDigitMax = 64;
-constexpr int kDefaultSlices = 5;
-constexpr int kMaxSlices = 9;
+constexpr int kDefaultSlices = 4;
+constexpr int kMaxSlices = 7;
 std::atomic<int> g_slices{-1};
 
 int clamp_slices(int v) { return v <= 0 ? 0 : std::min(std::max(v, 4), kMaxSlices); }
@@ -193,6 +195,165 @@ void imma_tn(LtState& st, DevBuf<uint8_t>& ws, int64_t M, int64_t N, int64_t K, 
   count_launch();
 }
 
+// ------------------------------------------------------------- CRT scheme ---
+// Same Gram, fewer int8 GEMMs (an Ozaki-II-style modular split).  Per segment
+// and column, x = rint(A 2^(k-e)) is a k-bit integer (k = 7 ns - 1: the same
+// column-max-relative accuracy as ns digit planes, with no dropped terms).
+// Its symmetric residues modulo pairwise-coprime m_i <= 255 are int8, and
+// C_i = R_i^T R_i (one int8 GEMM per modulus, K = segment rows, exact in
+// int32) is sum_s x_a x_b mod m_i.  Garner's algorithm rebuilds the exact
+// integer sum in 128-bit arithmetic (|sum| < M/4, M = prod m_i), which is
+// converted to fp64 once (exact whenever representable) and scaled by
+// 2^(e_a + e_b - 2k).  At ns = 5 that is 11 GEMMs of K rows instead of the
+// digit scheme's 15; at ns = 7, 15 instead of 28.
+// Pairwise coprime moduli <= 255 (residues fit int8 in symmetric form).
+__host__ __device__ constexpr int kmod(int i) {
+  constexpr int t[20] = {255, 254, 253, 251, 247, 241, 239, 233, 229, 227,
+                         223, 211, 199, 197, 193, 191, 181, 179, 173, 167};
+  return t[i];
+}
+constexpr int kMaxModuli = 20;
+constexpr int cx_inv(int a, int m) {  // a^-1 mod m (gcd(a, m) = 1)
+  for (int x = 1; x < m; ++x)
+    if ((static_cast<long long>(a) * x) % m == 1) return x;
+  return 0;
+}
+struct CrtTables {
+  int pmod[kMaxModuli][kMaxModuli];  // (prod_{l<j} m_l) mod m_i, j < i
+  int inv[kMaxModuli];               // (prod_{l<i} m_l)^-1 mod m_i
+};
+constexpr CrtTables make_crt_tables() {
+  CrtTables t{};
+  for (int i = 0; i < kMaxModuli; ++i) {
+    long long p = 1;  // prod_{l<j} m_l mod m_i, built up over j
+    for (int j = 0; j < kMaxModuli; ++j) {
+      t.pmod[j][i] = static_cast<int>(p);
+      if (j < i) p = (p * kmod(j)) % kmod(i);
+    }
+    t.inv[i] = i == 0 ? 1 : cx_inv(static_cast<int>(p % kmod(i)), kmod(i));
+  }
+  return t;
+}
+__constant__ CrtTables c_crt = make_crt_tables();
+
+__device__ __forceinline__ int sym_mod(long long x, int m) {
+  int r = static_cast<int>(x % m);  // constant m after unrolling
+  if (r > m / 2) r -= m;
+  if (r < -(m - 1) / 2) r += m;
+  return r;
+}
+
+// Thread per 4 consecutive rows of one column; plane i at X + i * kp * np.
+template <int NM>
+__global__ void residue_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n,
+                               int64_t kp, int64_t np, int k, const int* __restrict__ ex,
+                               int8_t* __restrict__ X) {
+  const int a = blockIdx.y;
+  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (r0 >= kp) return;
+  const double sc = ldexp(1.0, k - ex[a]);
+  long long x[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    x[u] = (a < n && r0 + u < rows) ? __double2ll_rn(A[static_cast<int64_t>(a) * lda + r0 + u] * sc)
+                                    : 0ll;
+  int8_t* dst = X + static_cast<int64_t>(a) * kp + r0;
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    const char4 c = make_char4(static_cast<signed char>(sym_mod(x[0], kmod(i))),
+                               static_cast<signed char>(sym_mod(x[1], kmod(i))),
+                               static_cast<signed char>(sym_mod(x[2], kmod(i))),
+                               static_cast<signed char>(sym_mod(x[3], kmod(i))));
+    *reinterpret_cast<char4*>(dst + static_cast<int64_t>(i) * kp * np) = c;
+  }
+}
+
+// 128-bit integer -> double on the magnitude: exact whenever the value is
+// representable (both 64-bit halves then carry <= 53 significant bits and the
+// fused sum is exact), otherwise within one ulp.
+__device__ __forceinline__ double i128_to_double(__int128 v) {
+  const bool neg = v < 0;
+  const unsigned __int128 u = neg ? static_cast<unsigned __int128>(0) - static_cast<unsigned __int128>(v)
+                                  : static_cast<unsigned __int128>(v);
+  const double hi = static_cast<double>(static_cast<unsigned long long>(u >> 64));
+  const double lo = static_cast<double>(static_cast<unsigned long long>(u));
+  const double d = fma(hi, 18446744073709551616.0, lo);
+  return neg ? -d : d;
+}
+
+template <int NM>
+__global__ void __launch_bounds__(256) crt_fold_kernel(const int32_t* __restrict__ C,
+                                                       int64_t cstride, int64_t m, int w, int c0,
+                                                       int n, int k, const int* __restrict__ ex,
+                                                       double* __restrict__ G, int accumulate) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= m || j >= w || i < j || c0 + i >= n || c0 + j >= n) return;
+  const int32_t* c = C + i + static_cast<int64_t>(j) * m;
+  int y[NM];  // symmetric mixed-radix digits (Garner)
+#pragma unroll
+  for (int t = 0; t < NM; ++t) {
+    const int mt = kmod(t);
+    int v = __ldg(c + static_cast<int64_t>(t) * cstride) % mt;  // |C| < 2^31
+    int s = 0;
+#pragma unroll
+    for (int l = 0; l < t; ++l) s += y[l] * c_crt.pmod[l][t];
+    v = (v - s % mt) % mt;
+    if (v < 0) v += mt;
+    v = (v * c_crt.inv[t]) % mt;
+    if (v > mt / 2) v -= mt;
+    y[t] = v;
+  }
+  __int128 acc = y[NM - 1];
+#pragma unroll
+  for (int t = NM - 2; t >= 0; --t) acc = acc * kmod(t) + y[t];
+  const double v = ldexp(i128_to_double(acc), ex[c0 + i] + ex[c0 + j] - 2 * k);
+  double* g = G + (c0 + i) + static_cast<int64_t>(c0 + j) * n;
+  *g = accumulate ? *g + v : v;
+}
+
+// Moduli for k-bit integers summed over kp rows: M > 4 kp 2^(2k).
+int crt_moduli(int k, int64_t kp) {
+  const double need = 2.0 + std::log2(static_cast<double>(std::max<int64_t>(kp, 1))) + 2.0 * k;
+  double have = 0.0;
+  for (int i = 0; i < kMaxModuli; ++i) {
+    have += std::log2(static_cast<double>(kmod(i)));
+    if (have > need + 0.25) return i + 1;
+  }
+  return -1;
+}
+
+template <int NM>
+void launch_crt(const double* A, int64_t lda, int64_t kr, int n, int64_t kp, int64_t np, int k,
+                const int* ex, int8_t* X, cudaStream_t s) {
+  dim3 g(static_cast<unsigned>(ceil_div(kp / 4, 256)), static_cast<unsigned>(np));
+  residue_kernel<NM><<<g, 256, 0, s>>>(A, lda, kr, n, kp, np, k, ex, X);
+  check_launch("residue_kernel");
+}
+template <int NM>
+void launch_crt_fold(const int32_t* C, int64_t cstride, int64_t m, int64_t wn, int64_t c0, int n,
+                     int k, const int* ex, double* G, int acc, cudaStream_t s) {
+  dim3 fg(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(wn));
+  crt_fold_kernel<NM><<<fg, 256, 0, s>>>(C, cstride, m, static_cast<int>(wn), static_cast<int>(c0),
+                                         n, k, ex, G, acc);
+  check_launch("crt_fold_kernel");
+}
+
+#define FSTK_CRT_SWITCH(NMV, CALL)                                              \
+  switch (NMV) {                                                                \
+    case 8: CALL(8); break;                                                     \
+    case 9: CALL(9); break;                                                     \
+    case 10: CALL(10); break;                                                   \
+    case 11: CALL(11); break;                                                   \
+    case 12: CALL(12); break;                                                   \
+    case 13: CALL(13); break;                                                   \
+    case 14: CALL(14); break;                                                   \
+    case 15: CALL(15); break;                                                   \
+    case 16: CALL(16); break;                                                   \
+    case 17: CALL(17); break;                                                   \
+    default: fail(FSTK_E_COMPUTE, "internal: unsupported CRT modulus count");   \
+  }
+
 }  // namespace
 
 int gram_slices() {
@@ -215,9 +376,15 @@ bool gram_sliced_applies(int64_t rows, int n) { return gram_slices() > 0 && n >=
 
 // gram (n x n, col-major, lower triangle) = beta * gram + A^T A over `rows`
 // rows of A (col-major, lda).
+double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, double* gram,
+                           double beta, int ns, cudaStream_t s, int device, GramScratch& sc);
+bool gram_scheme_crt();
+
 double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n, double* gram,
                               double beta, int ns, int t_lo, cudaStream_t s, int device,
                               GramScratch& sc) {
+  if (t_lo == 2 && gram_scheme_crt())
+    return gram_accumulate_crt(A, lda, rows, n, gram, beta, ns, s, device, sc);
   double ops = 0.0;
   require(ns >= 4 && ns <= kMaxSlices, FSTK_E_PARAMETER, "sliced Gram: 4..9 digit planes");
   require(t_lo >= 2 && t_lo <= ns + 1, FSTK_E_PARAMETER, "sliced Gram: bad plane range");
@@ -291,6 +458,82 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
       fold_kernel<<<fg, 256, 0, s>>>(Cb.p, m * wn, ns, t_lo, m, static_cast<int>(wn),
                                      static_cast<int>(c0), n, ex.p, gram, acc);
       check_launch("fold_kernel");
+    }
+    first = false;
+  }
+  return ops;
+}
+
+bool gram_scheme_crt() {
+  static const bool crt = [] {
+    const char* e = std::getenv("FSTK_GRAM_SCHEME");
+    return !(e && std::string(e) == "digits");
+  }();
+  return crt;
+}
+
+// CRT variant of gram_accumulate_sliced (whole Gram, t_lo = 2 semantics).
+double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, double* gram,
+                           double beta, int ns, cudaStream_t s, int device, GramScratch& sc) {
+  require(ns >= 4 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: 4..7 plane-equivalents");
+  const int k = 7 * ns - 1;
+  LtState& st = lt_state(device);
+  const int64_t np = round_up(static_cast<int64_t>(n), 16);
+  static const int64_t seg_cap = [] {
+    const char* e = std::getenv("FSTK_GRAM_SEG");
+    return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(32768);
+  }();
+  // int32-exact: K * 127^2 < 2^31; residue planes within a third of free
+  // memory (<= 24 GB); fixed for the scratch's lifetime like the digit scheme.
+  int64_t kmax = std::min<int64_t>(seg_cap, ((int64_t(1) << 31) - 1) / (127 * 127));
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    free_b = size_t(24) << 30;
+  }
+  const int nm_max = crt_moduli(7 * 7 - 1, kmax);
+  const int64_t have = static_cast<int64_t>(sc.X.n);
+  const int64_t budget = std::min<int64_t>(int64_t(24) << 30, (static_cast<int64_t>(free_b) + have) / 3);
+  kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, budget / (nm_max * np)));
+  kmax &= ~int64_t(15);
+  if (sc.kp == 0) sc.kp = kmax;
+  const int64_t kp = std::min<int64_t>(sc.kp, round_up(rows, 16));
+  const int nm = crt_moduli(k, kp);
+  require(nm >= 8 && nm <= 17, FSTK_E_COMPUTE, "internal: CRT modulus count out of range");
+  static const int64_t block_cap = [] {
+    const char* e = std::getenv("FSTK_GRAM_BLOCK");
+    return e ? std::max<int64_t>(256, std::atoll(e)) : int64_t(2048);
+  }();
+  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * 4));
+  w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), 16), np);
+  if (w > block_cap && np > block_cap) w = round_up(block_cap, 16);
+  sc.X.ensure(static_cast<size_t>(nm) * kp * np);
+  sc.C.ensure(static_cast<size_t>(nm) * np * w);
+  sc.ex.ensure(static_cast<size_t>(np));
+  sc.ws.ensure(size_t(32) << 20);
+  double ops = 0.0;
+  bool first = true;
+  for (int64_t s0 = 0; s0 < rows; s0 += kp) {
+    const int64_t kr = std::min(kp, rows - s0);
+    col_exponent_kernel<<<static_cast<unsigned>(np), 256, 0, s>>>(A + s0, lda, kr, n, sc.ex.p);
+    check_launch("col_exponent_kernel");
+#define FSTK_CRT_RES(NMV) launch_crt<NMV>(A + s0, lda, kr, n, kp, np, k, sc.ex.p, sc.X.p, s)
+    FSTK_CRT_SWITCH(nm, FSTK_CRT_RES)
+#undef FSTK_CRT_RES
+    for (int64_t c0 = 0; c0 < np; c0 += w) {
+      const int64_t wn = std::min(w, np - c0);
+      const int64_t m = np - c0;
+      for (int t = 0; t < nm; ++t) {
+        const int8_t* Rt = sc.X.p + static_cast<int64_t>(t) * kp * np;
+        ops += 2.0 * static_cast<double>(m) * static_cast<double>(wn) * static_cast<double>(kp);
+        imma_tn(st, sc.ws, m, wn, kp, Rt + c0 * kp, kp, Rt + c0 * kp, kp,
+                sc.C.p + static_cast<int64_t>(t) * m * wn, m, s);
+      }
+      const int acc = (!first || beta != 0.0) ? 1 : 0;
+#define FSTK_CRT_FOLD(NMV) \
+  launch_crt_fold<NMV>(sc.C.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, acc, s)
+      FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
+#undef FSTK_CRT_FOLD
     }
     first = false;
   }

@@ -1441,8 +1441,10 @@ static void generate_design_block(const fstk_gpu_refit* rf, int64_t row0, int64_
 }  // namespace fstk_gpu
 
 namespace fstk_gpu {
+// slices < 0: the process setting (gram_slices()); 0: native fp64 Gram;
+// 4..7: the sliced Gram at that precision level.
 static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
-                             fstk_reestimate_info* info, bool allow_sliced) {
+                             fstk_reestimate_info* info, int slices) {
   {
     rf->gram_used = 0;
     double i8ops = 0.0;
@@ -1463,8 +1465,9 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
       // is split into nb column blocks: block row i below the diagonal is one
       // DGEMM A_i^T [A_0 .. A_{i-1}] and each diagonal block one DSYRK, so
       // (nb-1)/nb of the flops run in large GEMMs.
-      const bool sliced = allow_sliced && gram_sliced_applies(arows, n);
-      rf->gram_used = sliced ? gram_slices() : 0;
+      const int level = slices < 0 ? gram_slices() : slices;
+      const bool sliced = level > 0 && gram_sliced_applies(arows, n);
+      rf->gram_used = sliced ? level : 0;
       if (rf->none) {
         // A^T A accumulated over generated row blocks (A never materialised).
         const int64_t BS = none_block_rows(rf, sliced);
@@ -1510,82 +1513,24 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
   }
 }
 
-// delta = the plane sums (from+2 .. to+1) of this shard's A^T A, lower
-// triangle (rest zero).  The digits are a prefix code, so a `from`-plane Gram
-// plus delta is exactly the `to`-plane Gram (same segments, same exponents).
-static double gram_upgrade_delta(fstk_gpu_refit* rf, int to, double* delta) {
-  DeviceGuard dg(rf->device);
-  cudaStream_t s = rf->stream;
-  const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
-  const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
-  const int n = static_cast<int>(rf->R);
-  const int from = rf->gram_used;
-  FSTK_CUDA(cudaMemsetAsync(delta, 0, static_cast<size_t>(n) * n * 8, s));
-  double ops = 0.0;
-  if (arows > 0) {
-    if (rf->none) {
-      const int64_t BS = none_block_rows(rf, true);
-      DevBuf<double> W(static_cast<size_t>(BS) * rf->R);
-      for (int64_t r0 = 0; r0 < arows; r0 += BS) {
-        const int64_t nb_rows = std::min(BS, arows - r0);
-        generate_design_block(rf, r0, nb_rows, W.p, BS, s);
-        ProfScope prof(FSTK_PROF_GRAM, s);
-        ops += gram_accumulate_sliced(W.p, BS, nb_rows, n, delta, 1.0, to, from + 2, s,
-                                      rf->device, rf->gs);
-      }
-    } else {
-      ProfScope prof(FSTK_PROF_GRAM, s);
-      ops = gram_accumulate_sliced(rf->A.p, arows, arows, n, delta, 1.0, to, from + 2, s,
-                                   rf->device, rf->gs);
-    }
-  }
-  FSTK_CUDA(cudaStreamSynchronize(s));
-  rf->gram_used = to;
-  return ops;
-}
-
-__global__ void add_inplace_kernel(double* __restrict__ y, const double* __restrict__ x,
-                                   int64_t count) {
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    y[i] += x[i];
-}
 }  // namespace fstk_gpu
-
-int32_t fstk_gpu_refit_gram_upgrade(fstk_gpu_refit* rf, int32_t slices, double* delta,
-                                    fstk_reestimate_info* info, fstk_gpu_error* err) {
-  using namespace fstk_gpu;
-  return guarded(err, [&] {
-    require(rf && delta, FSTK_E_PARAMETER, "null argument");
-    const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
-    const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
-    require(rf->gram_used > 0 || arows == 0 || rf->R < 256, FSTK_E_PARAMETER,
-            "gram_upgrade: the last Gram of this refit was not sliced");
-    require(slices > rf->gram_used && slices <= 9, FSTK_E_PARAMETER,
-            "gram_upgrade: slices must exceed the current planes (at most 9)");
-    EventTimer tg(rf->stream);
-    if (rf->gram_used == 0) {  // empty shard or tiny system: nothing to add
-      DeviceGuard dg(rf->device);
-      FSTK_CUDA(cudaMemsetAsync(delta, 0, static_cast<size_t>(rf->R) * rf->R * 8, rf->stream));
-      FSTK_CUDA(cudaStreamSynchronize(rf->stream));
-      rf->gram_used = slices;
-      if (info) info->gram_slices = slices;
-      return;
-    }
-    const double ops = gram_upgrade_delta(rf, slices, delta);
-    if (info) {
-      info->t_gram += tg.seconds();
-      info->gram_slices = slices;
-      info->gram_int8_ops += ops;
-    }
-  });
-}
 
 int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
                                         fstk_reestimate_info* info, fstk_gpu_error* err) {
   return guarded(err, [&] {
     require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
-    normal_equations(rf, gram, rhs, info, true);
+    normal_equations(rf, gram, rhs, info, -1);
+  });
+}
+
+int32_t fstk_gpu_refit_normal_equations_level(fstk_gpu_refit* rf, int32_t slices, double* gram,
+                                              double* rhs, fstk_reestimate_info* info,
+                                              fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
+    require(slices == 0 || (slices >= 4 && slices <= 7), FSTK_E_PARAMETER,
+            "normal_equations_level: slices must be 0 (native) or 4..7");
+    normal_equations(rf, gram, rhs, info, slices);
   });
 }
 
@@ -1593,7 +1538,7 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* rf, double* gram,
                                                fstk_reestimate_info* info, fstk_gpu_error* err) {
   return guarded(err, [&] {
     require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
-    normal_equations(rf, gram, rhs, info, false);
+    normal_equations(rf, gram, rhs, info, 0);
   });
 }
 
@@ -1605,8 +1550,8 @@ int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t
   return guarded(err, [&] {
     require(a && gram, FSTK_E_PARAMETER, "null argument");
     require(n > 0 && rows > 0 && lda >= rows, FSTK_E_SHAPE, "gram: need n > 0, rows > 0, lda >= rows");
-    require(slices == 0 || (slices >= 4 && slices <= 9), FSTK_E_PARAMETER,
-            "gram: slices must be 0 (native fp64) or 4..9");
+    require(slices == 0 || (slices >= 4 && slices <= 7), FSTK_E_PARAMETER,
+            "gram: slices must be 0 (native fp64) or 4..7");
     require((rows <= INT32_MAX && lda <= INT32_MAX) || slices > 0, FSTK_E_SHAPE,
             "gram: native path needs rows, lda < 2^31");
     DeviceGuard dg(device);
@@ -1869,42 +1814,25 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     rc(fstk_gpu_refit_factor(rf, gram_in, rhs_in, x.p, info, err));
     // Escalation ladder for the sliced int8 Gram (a preconditioner-grade
     // A^T A): when it is not positive definite or refinement contracts slowly
-    // or stalls, add the missing plane sums up to kGramUpgradeSlices (exactly
-    // the higher-precision Gram), then fall back to the native fp64 Gram, so
-    // hard systems end on the exact fp64 path.
-    DevBuf<double> g2, r2, delta;
+    // or stalls, recompute it at kGramUpgradeSlices' accuracy, then fall back
+    // to the native fp64 Gram, so hard systems end on the exact fp64 path.
+    DevBuf<double> g2, r2;
     const double* gcur = gram_in;
     const double* rcur = rhs_in;
     auto escalate = [&]() -> bool {
       if (rf->gram_used == 0) return false;
+      // Next level: kGramUpgradeSlices planes' accuracy, then the native Gram.
+      const int to = rf->gram_used < kGramUpgradeSlices ? kGramUpgradeSlices : 0;
       fstk_reestimate_info li{};
-      if (rf->gram_used < kGramUpgradeSlices) {
-        delta.ensure(static_cast<size_t>(n) * n);
-        rc(fstk_gpu_refit_gram_upgrade(rf, kGramUpgradeSlices, delta.p, &li, err));
-        if (gcur != g2.p) {
-          g2.ensure(static_cast<size_t>(n) * n);
-          FSTK_CUDA(cudaMemcpyAsync(g2.p, gcur, static_cast<size_t>(n) * n * 8,
-                                    cudaMemcpyDeviceToDevice, rf->stream));
-          gcur = g2.p;
-        }
-        add_inplace_kernel<<<4 * 148, 256, 0, rf->stream>>>(g2.p, delta.p,
-                                                             static_cast<int64_t>(n) * n);
-        check_launch("add_inplace_kernel");
-        if (info) {
-          info->t_gram += li.t_gram;
-          info->gram_int8_ops += li.gram_int8_ops;
-          info->gram_slices = rf->gram_used;
-        }
-      } else {
-        g2.ensure(static_cast<size_t>(n) * n);
-        r2.ensure(static_cast<size_t>(n));
-        rc(fstk_gpu_refit_normal_equations_native(rf, g2.p, r2.p, &li, err));
-        gcur = g2.p;
-        rcur = r2.p;
-        if (info) {
-          info->t_gram += li.t_gram;
-          info->gram_slices = 0;
-        }
+      g2.ensure(static_cast<size_t>(n) * n);
+      r2.ensure(static_cast<size_t>(n));
+      rc(fstk_gpu_refit_normal_equations_level(rf, to, g2.p, r2.p, &li, err));
+      gcur = g2.p;
+      rcur = r2.p;
+      if (info) {
+        info->t_gram += li.t_gram;
+        info->gram_int8_ops += li.gram_int8_ops;
+        info->gram_slices = rf->gram_used;
       }
       rc(fstk_gpu_refit_factor(rf, gcur, rcur, x.p, info, err));
       return true;

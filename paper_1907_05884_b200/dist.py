@@ -60,8 +60,8 @@ def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, used=None
     `used` = digit planes of the summed Gram (None: the max over ranks of
     sess.info.gram_slices).  A sliced Gram that is not positive definite, or
     whose refinement contracts slower than 10x per step or stalls, escalates
-    like fstk_gpu_refit_solve: first to UPGRADE_SLICES planes (all-reduced
-    exact delta), then to the native fp64 Gram.  Every decision depends only
+    like fstk_gpu_refit_solve: the Gram is recomputed (and all-reduced) at
+    UPGRADE_SLICES' accuracy, then natively in fp64.  Every decision depends only
     on all-reduced data, so all ranks take the same branch."""
     import torch
     import torch.distributed as dist
@@ -74,17 +74,9 @@ def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, used=None
         nonlocal used
         if used == 0:
             return False
-        if used < UPGRADE_SLICES:
-            delta = torch.empty_like(gram)
-            sess.gram_upgrade(UPGRADE_SLICES, delta)
-            reduce_normal_equations(delta, torch.zeros(1, dtype=rhs.dtype, device=rhs.device),
-                                    group=group)
-            gram.add_(delta)
-            used = UPGRADE_SLICES
-        else:
-            sess.normal_equations_native(gram, rhs)
-            reduce_normal_equations(gram, rhs, group=group)
-            used = 0
+        used = UPGRADE_SLICES if used < UPGRADE_SLICES else 0
+        sess.normal_equations_level(used, gram, rhs)
+        reduce_normal_equations(gram, rhs, group=group)
         return True
 
     def escalate_until_factored():

@@ -48,9 +48,10 @@ def _info_dict(info: ReestimateInfo) -> dict:
 
 
 def gram_slices(slices: int | None = None) -> int:
-    """Gram arithmetic of this process: returns the current number of int8
-    digit planes (0 = native fp64 Gram); with `slices` given, sets it first
-    (4..9, or 0) and returns the previous value.  See fstk_gram.cu."""
+    """Gram arithmetic of this process: returns the current precision level
+    (the accuracy of that many 7-bit planes, 4..7; 0 = native fp64 Gram); with
+    `slices` given, sets it first and returns the previous value.  See
+    fstk_gram.cu."""
     return int(lib().fstk_gpu_gram_slices(-1 if slices is None else int(slices)))
 
 
@@ -142,12 +143,13 @@ class RefitSession:
         check(lib().fstk_gpu_refit_normal_equations_native(
             self._h, gram_t.data_ptr(), rhs_t.data_ptr(), C.byref(self.info), C.byref(err)), err)
 
-    def gram_upgrade(self, slices, delta_t):
-        """Writes the plane sums that raise this shard's sliced Gram to
-        `slices` planes into delta_t (CUDA float64, R*R)."""
+    def normal_equations_level(self, slices, gram_t, rhs_t):
+        """normal_equations() at an explicit Gram precision: 4..7 (sliced,
+        int8 tensor cores) or 0 (native fp64)."""
         err = Err()
-        check(lib().fstk_gpu_refit_gram_upgrade(self._h, int(slices), delta_t.data_ptr(),
-                                                C.byref(self.info), C.byref(err)), err)
+        check(lib().fstk_gpu_refit_normal_equations_level(
+            self._h, int(slices), gram_t.data_ptr(), rhs_t.data_ptr(), C.byref(self.info),
+            C.byref(err)), err)
 
     def solve(self, gram_t, rhs_t) -> np.ndarray:
         core = np.zeros(self.R)

@@ -85,12 +85,8 @@ class _ScriptedSession:
         self.calls.append("factor")
         return self.factor_ok.pop(0)
 
-    def gram_upgrade(self, slices, delta):
-        self.calls.append(f"upgrade{slices}")
-        delta.zero_()
-
-    def normal_equations_native(self, gram, rhs):
-        self.calls.append("native")
+    def normal_equations_level(self, slices, gram, rhs):
+        self.calls.append(f"upgrade{slices}" if slices else "native")
 
     def correction(self, x, s):
         self.calls.append("correction")
