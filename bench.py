@@ -411,7 +411,14 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
             torch.distributed.barrier()
         t0 = time.perf_counter()
         sess = F.RefitSession(model, pts, vals, seed=0, sample_rows=S, transform=args.transform,
-                              shard=rank, shards=world)
+                              shard=rank, shards=world, layout="columns" if world > 1 else "rows")
+        t_x = 0.0
+        if world > 1:
+            from paper_1907_05884_b200.dist import exchange_columns
+
+            tx = time.perf_counter()
+            exchange_columns(sess)
+            t_x = time.perf_counter() - tx
         gram = torch.empty(R * R, dtype=torch.float64, device=dev)
         rhs = torch.empty(R, dtype=torch.float64, device=dev)
         sess.normal_equations(gram, rhs)
@@ -432,6 +439,7 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
         info = sess.info_dict()
         sess.close()
         del gram
+        info["exchange_s"] = t_x
         return t_hot, t_all, t_ar, info
 
     from paper_1907_05884_b200 import _lib
@@ -455,6 +463,7 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
             "kernel_ms": {k: v[0] for k, v in kprof.items() if v[1]},
             "kernel_launches": {k: v[1] for k, v in kprof.items() if v[1]},
             "stages_s": {"prepare": tm["prepare_s"], "alloc": tm["alloc_s"], "sketch": tm["sketch_s"],
+                         "exchange": info.get("exchange_s", 0.0),
                          "gram": tm["gram_s"], "allreduce": t_ar, "solve": tm["solve_s"],
                          "residual": tm["residual_s"]},
             "gram_slices": info["gram_slices"], "refine_steps": info["refine_steps"],

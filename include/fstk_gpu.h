@@ -189,6 +189,26 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* model, const double* points,
                              const fstk_sketch_cfg* cfg, int32_t shard,
                              int32_t shards, fstk_gpu_refit** out,
                              fstk_reestimate_info* info, fstk_gpu_error* err);
+/* Column-sharded begin: the sketch transform -- replicated by
+ * refit_begin's row sharding -- is split instead: this shard transforms
+ * columns [(R+1) shard / shards, (R+1)(shard+1) / shards) of the R design
+ * columns + rhs, for all S sample rows, written straight into a send buffer
+ * packed per destination rank.  exchange_layout() then returns that buffer,
+ * the receive buffer (this shard's S/shards-row slab, column-major, the
+ * blocks of source g at its columns) and the per-peer element counts of one
+ * all-to-all (ncclAllToAll / torch all_to_all_single); adopt_rows() finishes
+ * the switch, after which the refit continues exactly as a row-sharded one
+ * (normal_equations, factor, ...).  The rows are bit-identical to
+ * refit_begin's.  transform = none (no transform) behaves like refit_begin. */
+int32_t fstk_gpu_refit_begin_columns(const fstk_gpu_model* model, const double* points,
+                                     const double* values, int64_t q, int32_t d,
+                                     const fstk_sketch_cfg* cfg, int32_t shard,
+                                     int32_t shards, fstk_gpu_refit** out,
+                                     fstk_reestimate_info* info, fstk_gpu_error* err);
+int32_t fstk_gpu_refit_exchange_layout(fstk_gpu_refit* refit, double** send,
+                                       int64_t* send_counts, double** recv,
+                                       int64_t* recv_counts, fstk_gpu_error* err);
+int32_t fstk_gpu_refit_adopt_rows(fstk_gpu_refit* refit, fstk_gpu_error* err);
 int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* refit, double* gram,
                                         double* rhs, fstk_reestimate_info* info,
                                         fstk_gpu_error* err);

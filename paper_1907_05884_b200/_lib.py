@@ -85,7 +85,8 @@ EXPORTS = [
     "fstk_gpu_refit_finish", "fstk_gpu_evaluate_grid", "fstk_gpu_reconstruct_grid",
     "fstk_gpu_self_convergence", "fstk_gpu_leverage_scores", "fstk_gpu_point_major_to_soa",
     "fstk_gpu_refit_normal_equations_native", "fstk_gpu_gram_slices", "fstk_gpu_gram_device",
-    "fstk_gpu_refit_normal_equations_level",
+    "fstk_gpu_refit_normal_equations_level", "fstk_gpu_refit_begin_columns",
+    "fstk_gpu_refit_exchange_layout", "fstk_gpu_refit_adopt_rows",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -134,6 +135,14 @@ def lib():
                                                          C.POINTER(Err)]
     L.fstk_gpu_gram_slices.argtypes = [C.c_int32]
     L.fstk_gpu_gram_slices.restype = C.c_int32
+    L.fstk_gpu_refit_begin_columns.argtypes = [VP, DP, DP, C.c_int64, C.c_int32,
+                                               C.POINTER(SketchCfg), C.c_int32, C.c_int32,
+                                               C.POINTER(VP), C.POINTER(ReestimateInfo),
+                                               C.POINTER(Err)]
+    L.fstk_gpu_refit_exchange_layout.argtypes = [VP, C.POINTER(VP), C.POINTER(C.c_int64),
+                                                 C.POINTER(VP), C.POINTER(C.c_int64),
+                                                 C.POINTER(Err)]
+    L.fstk_gpu_refit_adopt_rows.argtypes = [VP, C.POINTER(Err)]
     L.fstk_gpu_refit_normal_equations_level.argtypes = [VP, C.c_int32, VP, VP,
                                                         C.POINTER(ReestimateInfo), C.POINTER(Err)]
     L.fstk_gpu_gram_device.argtypes = [VP, C.c_int64, C.c_int64, C.c_int32, VP, C.c_int32,

@@ -13,7 +13,8 @@
 
 namespace fstk_gpu {
 
-constexpr int kMaxOrder = 8;   // proj/include/fstk/tensor.hpp:16
+constexpr int kMaxOrder = 8;
+constexpr int kMaxShards = 32;  // ranks of a column-sharded refit (fstk_gpu_refit_begin_columns)   // proj/include/fstk/tensor.hpp:16
 struct Int64x8 {
   int64_t v[8];
 };

@@ -260,7 +260,32 @@ struct PassParams {
   int stg_off;              // byte offset of the staging buffer in shared memory
   int compact;              // last pass: destination rows consecutive per CTA
   int list_off;             // byte offset of the per-CTA sampled-element list
+  // Column-sharded sketch (fstk_gpu_refit_begin_columns): the last pass
+  // writes sample row sl of column col straight into the all-to-all send
+  // buffer A, packed per destination rank h (the owner of sl):
+  // A[pk_base[h] + (col - c_lo) * ld_h + (sl - shard_lo[h]) (+ rows_h for Im)],
+  // ld_h = fft2 * rows_h.
+  int packed;
+  int nshards;
+  int fft2;
+  int64_t S;
+  int64_t c_lo;
+  int64_t shard_lo[kMaxShards + 1];
+  int64_t pk_base[kMaxShards];
 };
+
+__device__ __forceinline__ double* store_ptr(const PassParams& P, int64_t col, int64_t sl, bool im) {
+  if (!P.packed) {
+    double* out = (col == P.R) ? P.b : P.A + P.lda * col;
+    return out + (sl - P.row_lo) + (im ? P.im_off : 0);
+  }
+  int h = static_cast<int>((sl * P.nshards) / P.S);
+  while (h + 1 < P.nshards && P.shard_lo[h + 1] <= sl) ++h;
+  while (h > 0 && P.shard_lo[h] > sl) --h;
+  const int64_t rows_h = P.shard_lo[h + 1] - P.shard_lo[h];
+  return P.A + P.pk_base[h] + (col - P.c_lo) * (P.fft2 * rows_h) + (sl - P.shard_lo[h]) +
+         (im ? rows_h : 0);
+}
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
@@ -542,24 +567,22 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
     }
     // ---- store
     if (use_list) {
-      double* out = (col == P.R) ? P.b : P.A + P.lda * col;
       const int cnt = s_cnt;
       const int64_t first = s_first;
       for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
         const int e = elist[idx];
         const int64_t sl = first + idx;
         if (sl < P.row_lo || sl >= P.row_hi) continue;
-        const int64_t dst = sl - P.row_lo;
         if constexpr (REAL) {
-          out[dst] = xmul(P.scale, xmul(x[spad(e)], P.inv_sqrt_n));
+          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(x[spad(e)], P.inv_sqrt_n));
         } else if (P.kind == FSTK_TRANSFORM_DCT) {
           const double2 V = x[spad(e)];
           const double val = xsub(xmul(__ldg(P.post_re + sl), V.x), xmul(__ldg(P.post_im + sl), V.y));
-          out[dst] = xmul(P.scale, xmul(__ldg(P.post_c + sl), val));
+          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(__ldg(P.post_c + sl), val));
         } else {
           const double2 V = x[spad(e)];
-          out[dst] = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
-          out[P.im_off + dst] = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
+          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
+          *store_ptr(P, col, sl, true) = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
         }
       }
       continue;
@@ -576,18 +599,16 @@ __global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParam
       }
       const int32_t sl = P.slot[p];
       if (sl < 0 || sl < P.row_lo || sl >= P.row_hi) continue;
-      const int64_t dst = sl - P.row_lo;
-      double* out = (col == P.R) ? P.b : P.A + P.lda * col;
       if constexpr (REAL) {
-        out[dst] = xmul(P.scale, xmul(x[spad(e)], P.inv_sqrt_n));
+        *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(x[spad(e)], P.inv_sqrt_n));
       } else if (P.kind == FSTK_TRANSFORM_DCT) {
         const double2 V = x[spad(e)];
         const double val = xsub(xmul(P.post_re[sl], V.x), xmul(P.post_im[sl], V.y));
-        out[dst] = xmul(P.scale, xmul(P.post_c[sl], val));
+        *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(P.post_c[sl], val));
       } else {
         const double2 V = x[spad(e)];
-        out[dst] = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
-        out[P.im_off + dst] = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
+        *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
+        *store_ptr(P, col, sl, true) = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
       }
     }
   }
@@ -705,6 +726,14 @@ struct SketchJob {
   int64_t lda;
   double* b;
   bool compact = false;  // slot = last-pass visit order (build_inputs compact)
+  // Column range [col_lo, col_hi) of the R (+rhs) columns (col_hi < 0: all)
+  // and the packed all-to-all layout (see PassParams::packed).
+  int64_t col_lo = 0, col_hi = -1;
+  bool packed = false;
+  int nshards = 1;
+  int64_t S = 0;
+  int64_t shard_lo[kMaxShards + 1] = {0};
+  int64_t pk_base[kMaxShards] = {0};
 };
 
 static int ilog2(uint64_t n) {
@@ -755,8 +784,9 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
   });
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  for (int64_t c0 = 0; c0 < ncols; c0 += nb) {
-    const int64_t bc = std::min(nb, ncols - c0);
+  const int64_t cbeg = J.col_lo, cend = J.col_hi < 0 ? ncols : std::min(ncols, J.col_hi);
+  for (int64_t c0 = cbeg; c0 < cend; c0 += nb) {
+    const int64_t bc = std::min(nb, cend - c0);
     for (int pass = 0; pass < npass; ++pass) {
       PassParams P{};
       P.n = static_cast<int64_t>(J.n);
@@ -795,6 +825,13 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       P.A = J.A;
       P.lda = J.lda;
       P.b = J.b;
+      P.packed = J.packed ? 1 : 0;
+      P.nshards = J.nshards;
+      P.fft2 = J.kind == FSTK_TRANSFORM_FFT ? 2 : 1;
+      P.S = J.S;
+      P.c_lo = J.col_lo;
+      for (int h = 0; h <= J.nshards && h <= kMaxShards; ++h) P.shard_lo[h] = J.shard_lo[h];
+      for (int h = 0; h < J.nshards && h < kMaxShards; ++h) P.pk_base[h] = J.pk_base[h];
       const int64_t E = int64_t(1) << P.L;
       const int64_t sets = static_cast<int64_t>(J.n) / (E * P.G);
       size_t smem = static_cast<size_t>(E * P.G + E * P.G / 8) * elem +
@@ -1075,6 +1112,13 @@ struct fstk_gpu_refit {
   DevBuf<double> tmp_r;   // local residual rows
   // transform = none: mode tables of this shard's sampled rows (A generated on demand)
   bool none = false;
+  // Column-sharded sketch: this shard's columns [c_lo, c_hi) of the R + 1,
+  // packed per destination rank in `send` until the all-to-all lands the row
+  // slab in A (then exchanged = true and the refit continues row-sharded).
+  bool columns = false, exchanged = false;
+  int64_t c_lo = 0, c_hi = 0;
+  int64_t pk_base[kMaxShards] = {0};
+  DevBuf<double> send;
   GramScratch gs;        // sliced int8 Gram scratch (fstk_gram.cu)
   int gram_used = 0;     // digit planes of the last Gram (0 = native fp64)
   DevBuf<double> tables;
@@ -1103,10 +1147,12 @@ static double rel_residual(const std::vector<double>& pred, const std::vector<do
 
 extern "C" {
 
-int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, const double* values,
-                             int64_t q, int32_t d, const fstk_sketch_cfg* cfg, int32_t shard,
-                             int32_t shards, fstk_gpu_refit** out, fstk_reestimate_info* info,
-                             fstk_gpu_error* err) {
+namespace fstk_gpu {
+static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
+                                const double* values, int64_t q, int32_t d,
+                                const fstk_sketch_cfg* cfg, int32_t shard, int32_t shards,
+                                bool columns, fstk_gpu_refit** out, fstk_reestimate_info* info,
+                                fstk_gpu_error* err) {
   return guarded(err, [&] {
     require(m && points && values && cfg && out, FSTK_E_PARAMETER, "null argument");
     *out = nullptr;
@@ -1328,10 +1374,30 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     }
     mark("mode tables");
     if (info) info->t_prepare = tprep.seconds();
-    // Sketch: all R design columns plus the rhs; this shard keeps its rows.
+    // Sketch.  Row-sharded: all R design columns plus the rhs, this shard
+    // keeps its rows.  Column-sharded: this shard's columns of the R + 1
+    // (rhs last), every sample row, written packed per destination rank for
+    // one all-to-all (exchange_layout / adopt_rows).
     const bool fft = cfg->transform == FSTK_TRANSFORM_FFT;
     const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
-    {
+    const int fft2 = fft ? 2 : 1;
+    rf->columns = columns;
+    if (columns) {
+      require(shards <= kMaxShards, FSTK_E_PARAMETER, "column-sharded refit: at most 32 shards");
+      const int64_t nc = m->R + 1;
+      rf->c_lo = nc * shard / shards;
+      rf->c_hi = nc * (shard + 1) / shards;
+      int64_t off = 0;
+      for (int h = 0; h < shards; ++h) {
+        const int64_t lo = static_cast<int64_t>(S) * h / shards, hi = static_cast<int64_t>(S) * (h + 1) / shards;
+        rf->pk_base[h] = off;
+        off += (rf->c_hi - rf->c_lo) * fft2 * (hi - lo);
+      }
+      const auto ta = std::chrono::steady_clock::now();
+      rf->send.alloc(static_cast<size_t>(std::max<int64_t>(off, 1)));
+      if (info)
+        info->t_alloc = std::chrono::duration<double>(std::chrono::steady_clock::now() - ta).count();
+    } else {
       const auto ta = std::chrono::steady_clock::now();
       rf->A.alloc(static_cast<size_t>(std::max<int64_t>(arows, 1)) * m->R);
       rf->b.alloc(static_cast<size_t>(std::max<int64_t>(arows, 1)));
@@ -1368,6 +1434,18 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
     J.A = rf->A.p;
     J.lda = arows;
     J.b = rf->b.p;
+    if (columns) {
+      J.col_lo = rf->c_lo;
+      J.col_hi = rf->c_hi;
+      J.packed = true;
+      J.nshards = shards;
+      J.S = static_cast<int64_t>(S);
+      for (int h = 0; h <= shards; ++h) J.shard_lo[h] = static_cast<int64_t>(S) * h / shards;
+      for (int h = 0; h < shards; ++h) J.pk_base[h] = rf->pk_base[h];
+      J.A = rf->send.p;
+      J.row_lo = 0;
+      J.row_hi = static_cast<int64_t>(S);
+    }
     run_sketch(m->device, J, s);
     if (info) info->t_sketch = tsk.seconds();
     FSTK_CUDA(cudaStreamSynchronize(s));
@@ -1378,6 +1456,70 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
       info->held_out = rf->held_out ? 1 : 0;
     }
     *out = rf.release();
+  });
+}
+}  // namespace fstk_gpu
+
+int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, const double* values,
+                             int64_t q, int32_t d, const fstk_sketch_cfg* cfg, int32_t shard,
+                             int32_t shards, fstk_gpu_refit** out, fstk_reestimate_info* info,
+                             fstk_gpu_error* err) {
+  return fstk_gpu::refit_begin_impl(m, points, values, q, d, cfg, shard, shards, false, out, info,
+                                    err);
+}
+
+int32_t fstk_gpu_refit_begin_columns(const fstk_gpu_model* m, const double* points,
+                                     const double* values, int64_t q, int32_t d,
+                                     const fstk_sketch_cfg* cfg, int32_t shard, int32_t shards,
+                                     fstk_gpu_refit** out, fstk_reestimate_info* info,
+                                     fstk_gpu_error* err) {
+  // transform = none has no transform to shard: its rows are generated locally.
+  const bool cols = cfg && cfg->transform != FSTK_TRANSFORM_NONE;
+  return fstk_gpu::refit_begin_impl(m, points, values, q, d, cfg, shard, shards, cols, out, info,
+                                    err);
+}
+
+int32_t fstk_gpu_refit_exchange_layout(fstk_gpu_refit* rf, double** send, int64_t* send_counts,
+                                       double** recv, int64_t* recv_counts, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    require(rf && send && send_counts && recv && recv_counts, FSTK_E_PARAMETER, "null argument");
+    require(rf->columns && !rf->exchanged, FSTK_E_PARAMETER,
+            "exchange_layout: not a column-sharded refit awaiting its exchange");
+    DeviceGuard dg(rf->device);
+    const int fft2 = rf->cfg.transform == FSTK_TRANSFORM_FFT ? 2 : 1;
+    const int64_t arows = fft2 * rf->local_rows;
+    const int G = rf->shards;
+    const int64_t nc = rf->R + 1;
+    rf->A.alloc(static_cast<size_t>(std::max<int64_t>(arows, 1)) * nc);
+    for (int h = 0; h < G; ++h) {
+      const int64_t lo = static_cast<int64_t>(rf->S) * h / G, hi = static_cast<int64_t>(rf->S) * (h + 1) / G;
+      send_counts[h] = (rf->c_hi - rf->c_lo) * fft2 * (hi - lo);
+      // Column block of source g lands at columns [c_lo_g, c_hi_g) of the row
+      // slab (column-major, ld = arows): contiguous, in rank order.
+      recv_counts[h] = (nc * (h + 1) / G - nc * h / G) * arows;
+    }
+    *send = rf->send.p;
+    *recv = rf->A.p;
+  });
+}
+
+int32_t fstk_gpu_refit_adopt_rows(fstk_gpu_refit* rf, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    require(rf, FSTK_E_PARAMETER, "null argument");
+    require(rf->columns && !rf->exchanged && rf->A.p, FSTK_E_PARAMETER,
+            "adopt_rows: call exchange_layout and complete the all-to-all first");
+    DeviceGuard dg(rf->device);
+    const int fft2 = rf->cfg.transform == FSTK_TRANSFORM_FFT ? 2 : 1;
+    const int64_t arows = fft2 * rf->local_rows;
+    rf->b.alloc(static_cast<size_t>(std::max<int64_t>(arows, 1)));
+    if (arows > 0)
+      FSTK_CUDA(cudaMemcpyAsync(rf->b.p, rf->A.p + rf->R * arows, arows * 8, cudaMemcpyDeviceToDevice,
+                                rf->stream));
+    FSTK_CUDA(cudaStreamSynchronize(rf->stream));
+    rf->send.release();
+    rf->exchanged = true;
   });
 }
 
@@ -1446,6 +1588,8 @@ namespace fstk_gpu {
 static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
                              fstk_reestimate_info* info, int slices) {
   {
+    require(!rf->columns || rf->exchanged, FSTK_E_PARAMETER,
+            "column-sharded refit: exchange_layout, the all-to-all and adopt_rows come first");
     rf->gram_used = 0;
     double i8ops = 0.0;
     DeviceGuard dg(rf->device);
@@ -1683,6 +1827,8 @@ int32_t fstk_gpu_refit_correction(fstk_gpu_refit* rf, const double* x_dev, doubl
                                   fstk_gpu_error* err) {
   return guarded(err, [&] {
     require(rf && x_dev && s_dev, FSTK_E_PARAMETER, "null argument");
+    require(!rf->columns || rf->exchanged, FSTK_E_PARAMETER,
+            "column-sharded refit: exchange_layout, the all-to-all and adopt_rows come first");
     DeviceGuard dg(rf->device);
     cudaStream_t s = rf->stream;
     Handles& h = handles(rf->device);
@@ -1907,6 +2053,8 @@ int32_t fstk_gpu_refit_sketched(const fstk_gpu_refit* rf, double* a, double* b, 
                                 fstk_gpu_error* err) {
   return guarded(err, [&] {
     require(rf, FSTK_E_PARAMETER, "null argument");
+    require(!rf->columns || rf->exchanged, FSTK_E_PARAMETER,
+            "column-sharded refit: exchange_layout, the all-to-all and adopt_rows come first");
     const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
     const int64_t lr = rf->local_rows;
     const int64_t arows = fft ? 2 * lr : lr;

@@ -119,15 +119,50 @@ def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, used=None
     return x
 
 
-def refit_distributed(model, points, values, rank: int, world: int, device=None, **kw):
-    """Row-sharded refit: returns (new_model, info) on rank 0, (None, info) elsewhere."""
+def exchange_columns(sess, group=None):
+    """Column-to-row all-to-all of a layout='columns' RefitSession (SURVEY
+    8e): every rank sent its transformed columns for every row slab; after
+    this each rank holds its row slab and the refit continues row-sharded.
+    NCCL moves device tensors directly; other backends stage through host
+    memory."""
+    import torch
+    import torch.distributed as dist
+
+    bufs = sess.exchange_buffers()
+    if bufs is None:  # transform="none": rows are generated locally
+        return
+    send, sc, recv, rc = bufs
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        if dist.get_backend(group) == "nccl":
+            dist.all_to_all_single(recv, send, output_split_sizes=rc, input_split_sizes=sc,
+                                   group=group)
+        else:
+            hr = torch.empty(recv.numel(), dtype=recv.dtype)
+            dist.all_to_all_single(hr, send.cpu(), output_split_sizes=rc, input_split_sizes=sc,
+                                   group=group)
+            recv.copy_(hr)
+    else:
+        recv.copy_(send)  # one shard: the packed and row layouts coincide
+    torch.cuda.synchronize(recv.device)
+    sess.adopt_rows()
+
+
+def refit_distributed(model, points, values, rank: int, world: int, device=None,
+                      layout: str = "columns", **kw):
+    """Sharded refit: returns (new_model, info) on rank 0, (None, info) elsewhere.
+    layout="columns" (default) shards the sketch transform by columns and
+    exchanges once (exchange_columns); layout="rows" replicates the transform
+    and keeps each rank's rows."""
     import torch
     import torch.distributed as dist
 
     from .refit import RefitSession
 
     R = int(np.prod(model.ranks))
-    sess = RefitSession(model, points, values, shard=rank, shards=world, device=device, **kw)
+    sess = RefitSession(model, points, values, shard=rank, shards=world, device=device,
+                        layout=layout, **kw)
+    if layout == "columns":
+        exchange_columns(sess)
     dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
     gram = torch.empty(R * R, dtype=torch.float64, device=dev)
     rhs = torch.empty(R, dtype=torch.float64, device=dev)

@@ -91,27 +91,72 @@ def reestimate_core(model: Model, points, values, seed=0, sample_rows=0,
     return model.with_core(core.reshape(model.ranks, order="F")), _info_dict(info)
 
 
+class _DeviceArray:
+    """Zero-copy view of library-owned device memory for torch.as_tensor."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
 class RefitSession:
-    """Staged refit (fstk_gpu_refit_*): used for row-sharded multi-GPU runs and
-    for parity tests that inspect the sampled rows / sketched system."""
+    """Staged refit (fstk_gpu_refit_*): used for sharded multi-GPU runs and
+    for parity tests that inspect the sampled rows / sketched system.
+
+    layout="rows" (fstk_gpu_refit_begin): every shard transforms all columns
+    and keeps its rows.  layout="columns" (fstk_gpu_refit_begin_columns): each
+    shard transforms its columns; exchange_buffers() + one all-to-all +
+    adopt_rows() then leave the same row slabs."""
 
     def __init__(self, model: Model, points, values, seed=0, sample_rows=0,
                  working_subset=1 << 20, transform="dct", validation_fraction=0.05,
-                 shard=0, shards=1, device=None):
+                 shard=0, shards=1, device=None, layout="rows"):
         require_gpu()
+        if layout not in ("rows", "columns"):
+            raise ValueError("layout must be 'rows' or 'columns'")
         self.model = model
         self.device = device
+        self.shards = shards
+        self.layout = layout
         p, v = _cloud(model, points, values)
         self.cfg = sketch_config(seed, sample_rows, working_subset, transform,
                                  validation_fraction)
         self.info = ReestimateInfo()
         out = C.c_void_p()
         err = Err()
-        check(lib().fstk_gpu_refit_begin(model.handle(device), dptr(p), dptr(v), p.shape[0],
-                                         p.shape[1], C.byref(self.cfg), shard, shards,
-                                         C.byref(out), C.byref(self.info), C.byref(err)), err)
+        begin = lib().fstk_gpu_refit_begin_columns if layout == "columns" else \
+            lib().fstk_gpu_refit_begin
+        check(begin(model.handle(device), dptr(p), dptr(v), p.shape[0], p.shape[1],
+                    C.byref(self.cfg), shard, shards, C.byref(out), C.byref(self.info),
+                    C.byref(err)), err)
         self._h = out.value
         self.R = int(np.prod(model.ranks))
+
+    def exchange_buffers(self):
+        """(send, send_counts, recv, recv_counts) of the column-to-row
+        all-to-all: CUDA float64 views of the library's buffers and the
+        per-peer element counts (rank order).  transform="none" has nothing to
+        exchange and returns None."""
+        import torch
+
+        if self.layout != "columns" or self.cfg.transform == TRANSFORMS["none"]:
+            return None
+        sp, rp = C.c_void_p(), C.c_void_p()
+        sc = (C.c_int64 * self.shards)()
+        rc = (C.c_int64 * self.shards)()
+        err = Err()
+        check(lib().fstk_gpu_refit_exchange_layout(self._h, C.byref(sp), sc, C.byref(rp), rc,
+                                                   C.byref(err)), err)
+        dev = torch.device("cuda", self.device if self.device is not None
+                           else torch.cuda.current_device())
+        send = torch.as_tensor(_DeviceArray(sp.value, sum(sc)), device=dev)
+        recv = torch.as_tensor(_DeviceArray(rp.value, sum(rc)), device=dev)
+        return send, list(sc), recv, list(rc)
+
+    def adopt_rows(self):
+        err = Err()
+        check(lib().fstk_gpu_refit_adopt_rows(self._h, C.byref(err)), err)
 
     def rows(self) -> np.ndarray:
         out = np.zeros(int(self.info.sample_rows), dtype=np.uint64)
