@@ -180,6 +180,44 @@ def cpu_eval_baseline(model, pts, budget_s: float = 12.0) -> dict:
                       f"(restated model.cpp:208-227, parallel_for over {cores} threads), {dt:.1f} s"}
 
 
+def cpu_refit_estimate(model, pts, vals, S: int, transform: str = "dct") -> dict:
+    """Reference refit on the host, EXTRAPOLATED (A alone is 68.7 GB
+    at C2 and the QR 5.4e14 flop, infeasible on the host): prepare timed in
+    full; the sketch (design column + the reference's DCT, pinned bit-exact to
+    its own transforms.cpp, + sampling; parallel over columns like
+    solve_sketched) timed on k columns and scaled by (R+1)/k; the QR flop count
+    2 m R^2 - 2/3 R^3 at the host's measured pivoted-QR rate (scipy dgeqp3 on
+    all threads -- conservative: the reference's Eigen QR is single-threaded)."""
+    import scipy.linalg as sla
+
+    from oracle import oracle as O
+
+    cores = O.max_threads()
+    R = int(np.prod(model.ranks))
+    t0 = time.perf_counter()
+    O.refit_columns(model, pts, vals, 0, 0, seed=0, sample_rows=S, transform=transform)
+    t_prep = time.perf_counter() - t0
+    k = max(2 * cores, 16)
+    t0 = time.perf_counter()
+    O.refit_columns(model, pts, vals, 0, k, seed=0, sample_rows=S, transform=transform)
+    t_k = max(time.perf_counter() - t0 - t_prep, 1e-6)
+    t_sketch = t_k / k * (R + 1)
+    m_, n_ = 4096, 1024
+    a = np.random.default_rng(0).standard_normal((m_, n_))
+    sla.qr(a[:512, :128], mode="economic", pivoting=True)
+    t0 = time.perf_counter()
+    sla.qr(a, mode="economic", pivoting=True)
+    rate = (2.0 * m_ * n_ ** 2 - 2.0 / 3.0 * n_ ** 3) / (time.perf_counter() - t0)
+    m_rows = 2 * S if transform == "fft" else S
+    t_qr = (2.0 * m_rows * R ** 2 - 2.0 / 3.0 * R ** 3) / rate
+    return {"seconds": t_prep + t_sketch + t_qr, "extrapolated": True, "kind": "port",
+            "cores": cores, "prepare_s": t_prep, "sketch_s": t_sketch, "qr_s": t_qr,
+            "qr_gflops_measured": rate / 1e9,
+            "sample": f"prepare in full; sketch of {k} of {R + 1} columns scaled; QR "
+                      f"{m_rows}x{R} by flop count at the measured {rate / 1e9:.0f} GFLOP/s "
+                      f"(dgeqp3 4096x1024, {cores} threads)"}
+
+
 def traffic_from_profile(cfg: str):
     """dram bytes per contraction launch from the committed ncu capture, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_contract_summary.json")
@@ -230,6 +268,9 @@ def run_reference(args):
                                        "Eigen absent), all host threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if vals is not None and not args.no_refit:
+        line["refit"] = cpu_refit_estimate(model, pts, vals, c["m_factor"] * int(np.prod(model.ranks)),
+                                           args.transform)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -363,6 +404,9 @@ def main():
 
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_eval_baseline(model, pts)
+        if vals is not None and not args.no_refit:
+            line["cpu_baseline"]["refit"] = cpu_refit_estimate(
+                model, pts, vals, cfgd["m_factor"] * int(np.prod(model.ranks)), args.transform)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
