@@ -463,10 +463,13 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
             tx = time.perf_counter()
             exchange_columns(sess)
             t_x = time.perf_counter() - tx
+        t_b = time.perf_counter() - t0
         gram = torch.empty(R * R, dtype=torch.float64, device=dev)
         rhs = torch.empty(R, dtype=torch.float64, device=dev)
+        tn = time.perf_counter()
         sess.normal_equations(gram, rhs)
         torch.cuda.synchronize()
+        t_n = time.perf_counter() - tn
         t_ar = 0.0
         if world > 1:
             ta = time.perf_counter()
@@ -477,13 +480,19 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
         t_hot = time.perf_counter() - t0
         from paper_1907_05884_b200.dist import refine_distributed
 
+        tr = time.perf_counter()
         x = refine_distributed(sess, gram, rhs)
+        torch.cuda.synchronize()
+        t_r = time.perf_counter() - tr
+        tf = time.perf_counter()
         core = sess.finish(x) if rank == 0 else None
+        t_f = time.perf_counter() - tf
         t_all = time.perf_counter() - t0
         info = sess.info_dict()
         sess.close()
         del gram
         info["exchange_s"] = t_x
+        info["wall_s"] = {"begin": t_b, "normal_equations": t_n, "refine": t_r, "finish": t_f}
         return t_hot, t_all, t_ar, info
 
     from paper_1907_05884_b200 import _lib
@@ -510,6 +519,7 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
                          "exchange": info.get("exchange_s", 0.0),
                          "gram": tm["gram_s"], "allreduce": t_ar, "solve": tm["solve_s"],
                          "residual": tm["residual_s"]},
+            "host_wall_s": info.get("wall_s"),
             "gram_slices": info["gram_slices"], "refine_steps": info["refine_steps"],
             "gram_roofline": gram_roofline(gram_flops, info, tm["gram_s"], peak),
             "residual_before": info["residual_before"], "residual_after": info["residual_after"],

@@ -680,6 +680,22 @@ static bool all_finite(const double* a, size_t n) {
   return true;
 }
 
+// fn(lo, hi) over [0, n) in contiguous chunks on the host cores (independent
+// per element; results do not depend on the split).
+template <class F>
+static void parallel_chunks(uint64_t n, F&& fn, uint64_t min_chunk = uint64_t(1) << 15) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const uint64_t nt = std::max<uint64_t>(1, std::min<uint64_t>(hw, n / std::max<uint64_t>(min_chunk, 1)));
+  if (nt <= 1) {
+    fn(uint64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (uint64_t t = 1; t < nt; ++t) th.emplace_back([&, t] { fn(n * t / nt, n * (t + 1) / nt); });
+  fn(uint64_t(0), n / nt);
+  for (auto& x : th) x.join();
+}
+
 __global__ void finite_check_kernel(const double* __restrict__ a, int64_t n, int* flag) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -904,7 +920,8 @@ static uint64_t bitrev(uint64_t v, int bits) {
 static void input_order(int kind, uint64_t n, std::vector<uint64_t>& pos2i) {
   const int LOG = ilog2(n);
   pos2i.resize(n);
-  for (uint64_t p = 0; p < n; ++p) {
+  parallel_chunks(n, [&](uint64_t lo, uint64_t hi) {
+  for (uint64_t p = lo; p < hi; ++p) {
     if (kind == FSTK_TRANSFORM_WHT) {
       pos2i[p] = p;
       continue;
@@ -919,6 +936,7 @@ static void input_order(int kind, uint64_t n, std::vector<uint64_t>& pos2i) {
       pos2i[p] = m < n / 2 ? 2 * m : 2 * (n - 1 - m) + 1;
     }
   }
+  });
 }
 
 #pragma GCC push_options
@@ -955,16 +973,18 @@ static void build_inputs(int kind, uint64_t n, uint64_t q_w, const std::vector<d
   input_order(kind, n, pos2i);
   std::vector<double> sg(n);
   std::vector<int64_t> rs(n);
-  for (uint64_t p = 0; p < n; ++p) {
-    const uint64_t i = pos2i[p];
-    if (i < q_w) {
-      rs[p] = src_of_i.empty() ? static_cast<int64_t>(i) : src_of_i[i];
-      sg[p] = signs[i];
-    } else {
-      rs[p] = -1;
-      sg[p] = 0.0;
+  parallel_chunks(n, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t p = lo; p < hi; ++p) {
+      const uint64_t i = pos2i[p];
+      if (i < q_w) {
+        rs[p] = src_of_i.empty() ? static_cast<int64_t>(i) : src_of_i[i];
+        sg[p] = signs[i];
+      } else {
+        rs[p] = -1;
+        sg[p] = 0.0;
+      }
     }
-  }
+  });
   // Destination rows.
   std::vector<int32_t> slot(n, -1);
   const uint64_t nrows = all_rows ? n : rows.size();
@@ -995,22 +1015,29 @@ static void build_inputs(int kind, uint64_t n, uint64_t q_w, const std::vector<d
       return (cta << 32) | (t * G + c);
     };
     std::vector<std::pair<uint64_t, uint64_t>> keyed(nrows);
-    for (uint64_t sidx = 0; sidx < nrows; ++sidx) {
-      const uint64_t k = all_rows ? sidx : rows[sidx];
-      keyed[sidx] = {order_key(k), sidx};
-    }
+    parallel_chunks(nrows, [&](uint64_t lo, uint64_t hi) {
+      for (uint64_t sidx = lo; sidx < hi; ++sidx) {
+        const uint64_t k = all_rows ? sidx : rows[sidx];
+        keyed[sidx] = {order_key(k), sidx};
+      }
+    });
     std::sort(keyed.begin(), keyed.end());
-    for (uint64_t dst = 0; dst < nrows; ++dst) {
-      const uint64_t sidx = keyed[dst].second;
-      const uint64_t k = all_rows ? sidx : rows[sidx];
-      slot[k] = static_cast<int32_t>(dst);
-      pos_of_dest[dst] = k;
-      S.dest_of_sample[sidx] = static_cast<int64_t>(dst);
-    }
+    parallel_chunks(nrows, [&](uint64_t lo, uint64_t hi) {
+      for (uint64_t dst = lo; dst < hi; ++dst) {
+        const uint64_t sidx = keyed[dst].second;
+        const uint64_t k = all_rows ? sidx : rows[sidx];
+        slot[k] = static_cast<int32_t>(dst);
+        pos_of_dest[dst] = k;
+        S.dest_of_sample[sidx] = static_cast<int64_t>(dst);
+      }
+    });
   }
   std::vector<double> pre(nrows), pim(nrows), pc(nrows);
   if (kind == FSTK_TRANSFORM_DCT) {
-    for (uint64_t dst = 0; dst < nrows; ++dst) dct_post(pos_of_dest[dst], n, &pre[dst], &pim[dst], &pc[dst]);
+    parallel_chunks(nrows, [&](uint64_t lo, uint64_t hi) {
+      for (uint64_t dst = lo; dst < hi; ++dst)
+        dct_post(pos_of_dest[dst], n, &pre[dst], &pim[dst], &pc[dst]);
+    });
     if (n == 1) {  // dct2_orthonormal returns early for n == 1 (identity)
       pre[0] = 1.0;
       pim[0] = 0.0;
@@ -1270,14 +1297,19 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
       std::vector<double> hp(static_cast<size_t>(q_w) * d), hv(q_w), vp(static_cast<size_t>(nv) * d);
       rf->h_val_values.resize(nv);
       rf->h_val_index.resize(nv);
+      parallel_chunks(q_w, [&](uint64_t lo, uint64_t hi) {
+        for (int k = 0; k < d; ++k) {
+          const double* col = points + static_cast<int64_t>(k) * q;
+          double* dst = hp.data() + static_cast<size_t>(k) * q_w;
+          for (uint64_t t = lo; t < hi; ++t) dst[t] = col[subset[t]];
+        }
+        for (uint64_t t = lo; t < hi; ++t) hv[t] = values[subset[t]];
+      });
       for (int k = 0; k < d; ++k) {
         const double* col = points + static_cast<int64_t>(k) * q;
-        double* dst = hp.data() + static_cast<size_t>(k) * q_w;
-        for (uint64_t t = 0; t < q_w; ++t) dst[t] = col[subset[t]];
         double* vdst = vp.data() + static_cast<size_t>(k) * nv;
         for (int64_t t = 0; t < nv; ++t) vdst[t] = col[val[t]];
       }
-      for (uint64_t t = 0; t < q_w; ++t) hv[t] = values[subset[t]];
       for (int64_t t = 0; t < nv; ++t) {
         rf->h_val_index[t] = static_cast<int64_t>(val[t]);
         rf->h_val_values[t] = values[val[t]];
