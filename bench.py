@@ -72,6 +72,17 @@ def workload(cfg_name: str, n_override: int, rank: int):
         pts = synth.uniform_points(n, 3, seed + 1000 * rank)
         model = synth.fitted_model(c["grid"], c["ranks"], c["degrees"][0], c["nnz"], seed=seed)
         vals = synth.flame_field(pts, seed=seed, noise=1e-2)
+    elif cfg_name == "C4":
+        # 4D space-time: x, y, z uniform, t on 64 uniform snapshots; the
+        # travelling front of BASELINE configs[3]; refit with M = 16R.
+        n = n_override or min(c["n"], 1 << 24)
+        rng = np.random.default_rng(seed + 1000 * rank)
+        pts = rng.random((n, 4))
+        pts[:, 3] = rng.integers(0, 64, n) / 63.0
+        x, y, z, t = pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]
+        vals = np.tanh((z - 0.3 - 0.4 * t - 0.05 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y))
+                       / 0.02)
+        model = synth.random_model(c["ranks"], c["degrees"], c["nnz"], seed=seed)
     else:
         n = n_override or min(c["n"], 1 << 24)
         d = c["d"]

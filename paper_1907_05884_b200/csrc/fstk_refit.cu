@@ -327,7 +327,14 @@ __device__ __forceinline__ double source_value(const PassParams& P, int64_t col,
 // stride 2^s0), keeps that set's replayed twiddles in shared memory and loops
 // over columns; stages run three at a time in registers (radix-2^3 rounds of
 // the very same radix-2 butterflies, so the result stays bit-identical).
-__host__ __device__ inline int pass_group(int s0) { return s0 == 0 ? 1 : 2; }
+static int pass_group(int s0) {
+  // Groups per CTA in passes after the first (FSTK_SKETCH_G: 1 or 2).
+  static const int g_later = [] {
+    const char* e = std::getenv("FSTK_SKETCH_G");
+    return (e && std::atoi(e) == 1) ? 1 : 2;
+  }();
+  return s0 == 0 ? 1 : g_later;
+}
 // Shared-memory slot of element e: one pad slot per 8 elements, so the 8
 // consecutive elements a thread owns in the first radix round fall in
 // distinct 16-byte bank groups.
@@ -859,7 +866,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       }();
       const int dtp = (P.src == SRC_TABLES && (J.d == 3 || J.d == 4)) ? J.d : 0;
       size_t stg = 0;
-      if (pf_on && P.src == SRC_BUFFER && P.G == 2)
+      if (pf_on && P.src == SRC_BUFFER && (P.G == 2 || !real))
         stg = static_cast<size_t>(E * P.G) * elem;
       else if (pf_on && dtp > 0 && P.G == 1 && P.s0 == 0 && E * P.G >= 2)
         stg = static_cast<size_t>(dtp) * E * P.G * 8;
