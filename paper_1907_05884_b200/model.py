@@ -436,6 +436,30 @@ def _header_json(model: Model) -> str:
                       allow_nan=True)
 
 
+def evaluate_fields(models, points, device=None) -> np.ndarray:
+    """Several models at one shared point set (BASELINE C5's visualisation
+    stream): the points travel to the GPU once and every field is evaluated
+    from HBM through fstk_gpu_evaluate_batch_device.  Returns (Q, n_fields),
+    column f bit-identical to models[f].evaluate_batch(points)."""
+    import torch
+
+    models = list(models)
+    if not models:
+        raise make_error(1, "no models")
+    d = models[0].order
+    if any(m.order != d for m in models):
+        raise make_error(2, "models of different order")
+    p = np.asarray(points, dtype=np.float64)
+    if p.ndim != 2 or p.shape[1] != d:
+        raise make_error(1, "points must be Q x d")
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+    pt = torch.from_numpy(np.ascontiguousarray(p.T)).to(dev)  # (d, Q): the Q x d col-major buffer
+    out = torch.empty((len(models), p.shape[0]), dtype=torch.float64, device=dev)
+    for f, m in enumerate(models):
+        m.evaluate_device(pt, out[f])
+    return out.cpu().numpy().T
+
+
 def save_model(model: Model, path: str):
     """model.cpp:280-333 / format.md:56-69."""
     header = _header_json(model).encode("utf-8")

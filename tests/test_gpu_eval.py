@@ -211,3 +211,15 @@ def test_grid_reconstruct_and_slice(O):
     with pytest.raises(ValueError) as e:
         m.evaluate_grid([[0.5], [0.2, 1.7], [0.1]])
     assert e.value.kind == "Domain" and e.value.mode == 1 and e.value.index == 1
+
+
+def test_evaluate_fields_shared_points(O):
+    # BASELINE C5 shape in small: 8 seeded fields, one shared point set,
+    # points uploaded once; each column equals the per-model batch bit for bit.
+    models = [synth.random_model((6, 5, 4), (10, 10, 10), 5, seed=40 + f) for f in range(8)]
+    pts = synth.uniform_points(50_000, 3, seed=41)
+    out = F.evaluate_fields(models, pts)
+    assert out.shape == (50_000, 8)
+    for f, m in enumerate(models):
+        assert np.array_equal(out[:, f], m.evaluate_batch(pts))
+        assert rel(out[:, f], O.evaluate_batch(m, pts)) <= 1e-12
