@@ -391,7 +391,7 @@ __device__ __forceinline__ void radix_round(typename std::conditional<REAL, doub
 }
 
 template <bool REAL, int G, int DT>  // DT: mode count when known at compile time (0 = runtime)
-__global__ void __launch_bounds__(256, 3) transform_pass2_kernel(const PassParams P, int ncols_batch) {
+__global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(const PassParams P, int ncols_batch) {
   using T = typename std::conditional<REAL, double, double2>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = P.L, E = 1 << L, nel = E * G;
