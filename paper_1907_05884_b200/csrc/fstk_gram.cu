@@ -236,15 +236,27 @@ constexpr CrtTables make_crt_tables() {
 }
 __constant__ CrtTables c_crt = make_crt_tables();
 
+// Symmetric residue of x modulo a compile-time m (unrolled callers), in
+// 32-bit arithmetic: x itself when it fits (k <= 30), else two 31-bit halves
+// x = hi 2^31 + lo with |hi| < 2^31.
+template <bool X32>
 __device__ __forceinline__ int sym_mod(long long x, int m) {
-  int r = static_cast<int>(x % m);  // constant m after unrolling
+  int r;
+  if constexpr (X32) {
+    r = static_cast<int>(x) % m;
+  } else {
+    const int hi = static_cast<int>(x >> 31);
+    const int lo = static_cast<int>(x & 0x7fffffffll);
+    const int p31 = static_cast<int>((1ll << 31) % m);
+    r = ((hi % m) * p31 + lo % m) % m;
+  }
   if (r > m / 2) r -= m;
   if (r < -(m - 1) / 2) r += m;
   return r;
 }
 
 // Thread per 4 consecutive rows of one column; plane i at X + i * kp * np.
-template <int NM>
+template <int NM, bool X32>
 __global__ void residue_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n,
                                int64_t kp, int64_t np, int k, const int* __restrict__ ex,
                                int8_t* __restrict__ X) {
@@ -260,10 +272,10 @@ __global__ void residue_kernel(const double* __restrict__ A, int64_t lda, int64_
   int8_t* dst = X + static_cast<int64_t>(a) * kp + r0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
-    const char4 c = make_char4(static_cast<signed char>(sym_mod(x[0], kmod(i))),
-                               static_cast<signed char>(sym_mod(x[1], kmod(i))),
-                               static_cast<signed char>(sym_mod(x[2], kmod(i))),
-                               static_cast<signed char>(sym_mod(x[3], kmod(i))));
+    const char4 c = make_char4(static_cast<signed char>(sym_mod<X32>(x[0], kmod(i))),
+                               static_cast<signed char>(sym_mod<X32>(x[1], kmod(i))),
+                               static_cast<signed char>(sym_mod<X32>(x[2], kmod(i))),
+                               static_cast<signed char>(sym_mod<X32>(x[3], kmod(i))));
     *reinterpret_cast<char4*>(dst + static_cast<int64_t>(i) * kp * np) = c;
   }
 }
@@ -327,7 +339,10 @@ template <int NM>
 void launch_crt(const double* A, int64_t lda, int64_t kr, int n, int64_t kp, int64_t np, int k,
                 const int* ex, int8_t* X, cudaStream_t s) {
   dim3 g(static_cast<unsigned>(ceil_div(kp / 4, 256)), static_cast<unsigned>(np));
-  residue_kernel<NM><<<g, 256, 0, s>>>(A, lda, kr, n, kp, np, k, ex, X);
+  if (k <= 30)
+    residue_kernel<NM, true><<<g, 256, 0, s>>>(A, lda, kr, n, kp, np, k, ex, X);
+  else
+    residue_kernel<NM, false><<<g, 256, 0, s>>>(A, lda, kr, n, kp, np, k, ex, X);
   check_launch("residue_kernel");
 }
 template <int NM>
