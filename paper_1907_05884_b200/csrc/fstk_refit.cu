@@ -772,9 +772,10 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
   const int64_t ncols = J.R + (J.with_rhs ? 1 : 0);
   const size_t elem = real ? 8 : 16;
   const int npass = LOG == 0 ? 1 : (LOG + 9) / 10;
-  // Column batch: the inter-pass intermediate is sized to stay L2-resident
-  // (pass 1 reads it in 32-byte segments at a 16 KB stride, which is
-  // latency-bound from DRAM but cheap from L2).  FSTK_SKETCH_BATCH_MB overrides.
+  // Column batches of ~FSTK_SKETCH_BATCH_MB (default 2 GB) of inter-pass
+  // intermediate: big enough that each pass's grid fills the GPU many times
+  // over (smaller batches measured slower; running consecutive batches on two
+  // streams gained nothing, since full grids only overlap at their tails).
   int64_t batch_mb = 2048;
   if (const char* e = std::getenv("FSTK_SKETCH_BATCH_MB")) batch_mb = std::max(1, std::atoi(e));
   int64_t nb = ncols;
