@@ -54,23 +54,21 @@ def parse():
 
 
 # ------------------------------------------------------------- workload ---
-def workload(cfg_name: str, n_override: int, rank: int):
+def dataset(cfg_name: str, n_override: int, rank: int):
+    """Seeded points (Q x d, column-major) and values (or None) of a config;
+    `rank` offsets the seed (each rank's own weak-scaling slab)."""
     from paper_1907_05884_b200 import synth
 
     c = synth.CONFIGS[cfg_name]
     seed = 0
     if cfg_name == "C2":
         n = n_override or 256 ** 3
-        m = round(n ** (1 / 3)) if not n_override else None
         pts = synth.jittered_mesh(256, seed=seed + 1000 * rank) if not n_override else \
             synth.uniform_points(n, 3, seed + 1000 * rank)
-        model = synth.fitted_model(256, c["ranks"], c["degrees"][0], c["nnz"], seed=seed,
-                                   n_gauss=8)
         vals = synth.flame_field(pts, seed=seed, n_gauss=8, noise=1e-2)
     elif cfg_name == "C1":
         n = n_override or c["n"]
         pts = synth.uniform_points(n, 3, seed + 1000 * rank)
-        model = synth.fitted_model(c["grid"], c["ranks"], c["degrees"][0], c["nnz"], seed=seed)
         vals = synth.flame_field(pts, seed=seed, noise=1e-2)
     elif cfg_name == "C4":
         # 4D space-time: x, y, z uniform, t on 64 uniform snapshots; the
@@ -82,15 +80,29 @@ def workload(cfg_name: str, n_override: int, rank: int):
         x, y, z, t = pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]
         vals = np.tanh((z - 0.3 - 0.4 * t - 0.05 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y))
                        / 0.02)
-        model = synth.random_model(c["ranks"], c["degrees"], c["nnz"], seed=seed)
     else:
         n = n_override or min(c["n"], 1 << 24)
         d = c["d"]
         pts = synth.uniform_points(n, d, seed + 1000 * rank) if d == 4 else \
             synth.flame_surface_mixture(n, seed + 1000 * rank)
-        model = synth.random_model(c["ranks"], c["degrees"], c["nnz"], seed=seed)
         vals = None
-    return model, np.asfortranarray(pts), vals, c
+    return np.asfortranarray(pts), vals
+
+
+def workload(cfg_name: str, n_override: int, rank: int):
+    from paper_1907_05884_b200 import synth
+
+    c = synth.CONFIGS[cfg_name]
+    seed = 0
+    if cfg_name == "C2":
+        model = synth.fitted_model(256, c["ranks"], c["degrees"][0], c["nnz"], seed=seed,
+                                   n_gauss=8)
+    elif cfg_name == "C1":
+        model = synth.fitted_model(c["grid"], c["ranks"], c["degrees"][0], c["nnz"], seed=seed)
+    else:
+        model = synth.random_model(c["ranks"], c["degrees"], c["nnz"], seed=seed)
+    pts, vals = dataset(cfg_name, n_override, rank)
+    return model, pts, vals, c
 
 
 def flops_per_point(model) -> tuple[float, float]:
@@ -411,7 +423,9 @@ def main():
 
     # ---- refit (one problem; rows sharded across ranks; one all-reduce)
     if not args.no_refit and vals is not None:
-        line["refit"] = run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak_mma)
+        # The refit is ONE problem: every rank passes the same (rank-0) cloud.
+        rpts, rvals = (pts, vals) if rank == 0 else dataset(args.config, args.points, 0)
+        line["refit"] = run_refit(model, rpts, rvals, cfgd, args, rank, world, dev, peak_mma)
 
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_eval_baseline(model, pts)

@@ -147,9 +147,34 @@ def exchange_columns(sess, group=None):
     sess.adopt_rows()
 
 
+def _check_same_dataset(points, values, device=None, group=None):
+    """The sharded refit is ONE least-squares problem: every rank must pass
+    the same cloud (the host plan indexes it identically on all ranks).  A
+    fingerprint of the size and a strided sample is compared across ranks."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return
+    p = np.asarray(points, dtype=np.float64)
+    v = np.asarray(values, dtype=np.float64)
+    step = max(1, p.shape[0] // 4096)
+    fp = np.array([p.shape[0], p.shape[1], float(np.sum(p[::step])), float(np.sum(v[::step]))])
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = torch.tensor(fp, dtype=torch.float64, device=dev)
+    lo, hi = t.clone(), t.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    if not torch.equal(lo, hi):
+        raise ValueError("refit_distributed: ranks hold different point clouds; the sharded "
+                         "refit needs the same dataset on every rank")
+
+
 def refit_distributed(model, points, values, rank: int, world: int, device=None,
                       layout: str = "columns", **kw):
-    """Sharded refit: returns (new_model, info) on rank 0, (None, info) elsewhere.
+    """Sharded refit of ONE dataset (identical `points`/`values` on every rank):
+    returns (new_model, info) on rank 0, (None, info) elsewhere.
     layout="columns" (default) shards the sketch transform by columns and
     exchanges once (exchange_columns); layout="rows" replicates the transform
     and keeps each rank's rows."""
@@ -159,6 +184,7 @@ def refit_distributed(model, points, values, rank: int, world: int, device=None,
     from .refit import RefitSession
 
     R = int(np.prod(model.ranks))
+    _check_same_dataset(points, values, device)
     sess = RefitSession(model, points, values, shard=rank, shards=world, device=device,
                         layout=layout, **kw)
     if layout == "columns":
