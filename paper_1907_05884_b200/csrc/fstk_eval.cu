@@ -136,12 +136,11 @@ struct DensePPT {
   static constexpr int value = JC <= 32 ? 2 : 1;
 };
 
-template <bool EXACT, int JC>
+template <bool EXACT, int JC, int PPT>
 __global__ void __launch_bounds__(128) mode_dense_kernel(
     ModeDev md, const double* __restrict__ xs, int64_t n, int64_t n_out,
     const int64_t* __restrict__ row_src, double* __restrict__ tk, int64_t ldt,
     unsigned long long* err_row) {
-  constexpr int PPT = DensePPT<EXACT, JC>::value;
   extern __shared__ __align__(16) double Cs[];  // (pmax+1) x JC
   const int j0 = blockIdx.y * JC;
   const int p = md.pmax;
@@ -738,15 +737,27 @@ static void launch_dense_t(const ModeDev& md, const double* xs, int64_t n, int64
                            const int64_t* row_src, double* tk, int64_t ldt,
                            unsigned long long* err_row, cudaStream_t s, int device) {
   static std::once_flag once[64];
+  constexpr int smax = (kMaxDegree + 1) * JC * static_cast<int>(sizeof(double));
   std::call_once(once[device & 63], [&] {
-    FSTK_CUDA(cudaFuncSetAttribute(mode_dense_kernel<EXACT, JC>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (kMaxDegree + 1) * JC * static_cast<int>(sizeof(double))));
+    FSTK_CUDA(cudaFuncSetAttribute(mode_dense_kernel<EXACT, JC, 1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+    FSTK_CUDA(cudaFuncSetAttribute(mode_dense_kernel<EXACT, JC, DensePPT<EXACT, JC>::value>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
   });
+  // FSTK_MODE_PPT=1: one point per thread (fewer registers, so mode CTAs can
+  // co-reside with the contraction of the other stream).
+  static const bool one = [] {
+    const char* e = std::getenv("FSTK_MODE_PPT");
+    return e && std::atoi(e) == 1;
+  }();
   const size_t sm = static_cast<size_t>(md.pmax + 1) * JC * sizeof(double);
-  constexpr int rows_per_cta = 128 * DensePPT<EXACT, JC>::value;
+  constexpr int ppt = DensePPT<EXACT, JC>::value;
+  const int rows_per_cta = 128 * (one ? 1 : ppt);
   dim3 grid(static_cast<unsigned>(ceil_div(n_out, rows_per_cta)), static_cast<unsigned>(md.nchunk));
-  mode_dense_kernel<EXACT, JC><<<grid, 128, sm, s>>>(md, xs, n, n_out, row_src, tk, ldt, err_row);
+  if (one || ppt == 1)
+    mode_dense_kernel<EXACT, JC, 1><<<grid, 128, sm, s>>>(md, xs, n, n_out, row_src, tk, ldt, err_row);
+  else
+    mode_dense_kernel<EXACT, JC, ppt><<<grid, 128, sm, s>>>(md, xs, n, n_out, row_src, tk, ldt, err_row);
   check_launch("mode_dense_kernel");
 }
 
