@@ -68,6 +68,18 @@ LtState& lt_state(int device) {
   return *st;
 }
 
+// a * 2^s exactly for any column exponent: one power-of-two factor when it is
+// a normal double, else two (a column max below ~2^-996 needs 2^s > 2^1023).
+struct Pow2Scale {
+  double f1, f2;
+  __device__ explicit Pow2Scale(int s) {
+    const int h = s / 2;
+    f1 = (s > -1000 && s < 1000) ? ldexp(1.0, s) : ldexp(1.0, h);
+    f2 = (s > -1000 && s < 1000) ? 1.0 : ldexp(1.0, s - h);
+  }
+  __device__ double operator()(double a) const { return (a * f1) * f2; }
+};
+
 __global__ void col_exponent_kernel(const double* __restrict__ A, int64_t lda, int64_t rows,
                                     int n, int* __restrict__ ex) {
   const int a = blockIdx.x;
@@ -95,11 +107,11 @@ __global__ void slice_kernel(const double* __restrict__ A, int64_t lda, int64_t 
   const int a = blockIdx.y;
   const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   if (r0 >= kp) return;
-  const double sc = ldexp(1.0, 6 - ex[a]);
+  const Pow2Scale sc(6 - ex[a]);
   double v[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u)
-    v[u] = (a < n && r0 + u < rows) ? A[static_cast<int64_t>(a) * lda + r0 + u] * sc : 0.0;
+    v[u] = (a < n && r0 + u < rows) ? sc(A[static_cast<int64_t>(a) * lda + r0 + u]) : 0.0;
   const int64_t ld = static_cast<int64_t>(ns) * kp;
   int8_t* xa = X + static_cast<int64_t>(a) * ld + r0;
   int8_t* ya = Y + static_cast<int64_t>(a) * ld + r0;
@@ -263,11 +275,11 @@ __global__ void residue_kernel(const double* __restrict__ A, int64_t lda, int64_
   const int a = blockIdx.y;
   const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   if (r0 >= kp) return;
-  const double sc = ldexp(1.0, k - ex[a]);
+  const Pow2Scale sc(k - ex[a]);
   long long x[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u)
-    x[u] = (a < n && r0 + u < rows) ? __double2ll_rn(A[static_cast<int64_t>(a) * lda + r0 + u] * sc)
+    x[u] = (a < n && r0 + u < rows) ? __double2ll_rn(sc(A[static_cast<int64_t>(a) * lda + r0 + u]))
                                     : 0ll;
   int8_t* dst = X + static_cast<int64_t>(a) * kp + r0;
 #pragma unroll

@@ -34,6 +34,7 @@ def _check_bound(a, g, ns):
     bound = 4 * (ns + 3) * 2.0 ** (-7 * ns) * rows * (mx[:, None] * mx[None, :])
     nrm = torch.linalg.norm(a, dim=0)
     bound = bound + 4 * rows * 2.0 ** -53 * (nrm[:, None] * nrm[None, :])
+    bound = bound + 4 * rows * 2.0 ** -1074  # products in the subnormal range round absolutely
     low = torch.tril(torch.ones_like(ref, dtype=torch.bool))
     err = (g - ref).abs()
     assert bool((err[low] <= bound[low]).all()), float((err - bound)[low].max())
@@ -253,3 +254,20 @@ def test_gram_slices_setting_roundtrip():
         assert F.gram_slices() == 0
     finally:
         F.gram_slices(prev)
+
+
+def test_gram_tiny_and_huge_column_scales_stay_finite():
+    # Column maxima near the bottom of the double range (1e-305: the scale
+    # 2^(k - e) alone would overflow) and large ones: every entry stays
+    # within the bound, and no NaN/Inf appears where the true Gram is finite.
+    torch = _torch()
+    rows, n = 5000, 300
+    a = torch.randn(rows, n, dtype=torch.float64, device="cuda")
+    a[:, 3] *= 1e-305
+    a[:, 4] *= 1e-160
+    a[:, 5] *= 1e150
+    a[:, 6] = 0.0
+    for ns in (4, 7):
+        g = F.gram(a, slices=ns)
+        assert bool(torch.isfinite(g).all())
+        _check_bound(a, g, ns)
