@@ -80,13 +80,55 @@ struct Pow2Scale {
   __device__ double operator()(double a) const { return (a * f1) * f2; }
 };
 
-__global__ void col_exponent_kernel(const double* __restrict__ A, int64_t lda, int64_t rows,
-                                    int n, int* __restrict__ ex) {
+// Column sources of the sliced Gram.  DenseSrc: a column-major fp64 matrix.
+// DesignSrc: the rows of the transform="none" design matrix generated from
+// the mode tables, A[r][a] = scale ((u0 u1) u2 ...)(row0 + r) -- the same
+// product order as design_block_kernel (fstk_refit.cu), so the values are
+// bit-identical and no fp64 A is ever written.
+struct DenseSrc {
+  const double* A;
+  int64_t lda;
+  struct Col {
+    const double* p;
+    __device__ double operator()(int64_t r) const { return p[r]; }
+  };
+  __device__ Col col(int a) const { return Col{A + static_cast<int64_t>(a) * lda}; }
+};
+
+struct DesignSrc {
+  DesignSpec s;
+  struct Col {
+    const double* u[kMaxOrder];
+    int d;
+    double scale;
+    __device__ double operator()(int64_t r) const {
+      double v = u[0][r];
+      for (int k = 1; k < d; ++k) v = xmul(v, u[k][r]);
+      return xmul(scale, v);
+    }
+  };
+  __device__ Col col(int a) const {
+    Col c;
+    c.d = s.d;
+    c.scale = s.scale;
+    int64_t rem = a;
+    for (int k = 0; k < s.d; ++k) {
+      const int64_t jk = rem % s.ranks.v[k];
+      rem /= s.ranks.v[k];
+      c.u[k] = s.tables + s.toff.v[k] + jk * s.ldt + s.row0;
+    }
+    return c;
+  }
+};
+
+template <class SRC>
+__global__ void col_exponent_kernel(const SRC src, int64_t s0, int64_t rows, int n,
+                                    int* __restrict__ ex) {
   const int a = blockIdx.x;
   double m = 0.0;
   if (a < n) {
-    const double* col = A + static_cast<int64_t>(a) * lda;
-    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) m = fmax(m, fabs(col[r]));
+    const auto col = src.col(a);
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) m = fmax(m, fabs(col(s0 + r)));
   }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   __shared__ double wm[32];
@@ -268,19 +310,21 @@ __device__ __forceinline__ int sym_mod(long long x, int m) {
 }
 
 // Thread per 4 consecutive rows of one column; plane i at X + i * kp * np.
-template <int NM, bool X32>
-__global__ void residue_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n,
-                               int64_t kp, int64_t np, int k, const int* __restrict__ ex,
+template <int NM, bool X32, class SRC>
+__global__ void residue_kernel(const SRC src, int64_t s0, int64_t rows, int n, int64_t kp,
+                               int64_t np, int k, const int* __restrict__ ex,
                                int8_t* __restrict__ X) {
   const int a = blockIdx.y;
   const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   if (r0 >= kp) return;
   const Pow2Scale sc(k - ex[a]);
-  long long x[4];
+  long long x[4] = {0ll, 0ll, 0ll, 0ll};
+  if (a < n) {
+    const auto col = src.col(a);
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
-    x[u] = (a < n && r0 + u < rows) ? __double2ll_rn(sc(A[static_cast<int64_t>(a) * lda + r0 + u]))
-                                    : 0ll;
+    for (int u = 0; u < 4; ++u)
+      if (r0 + u < rows) x[u] = __double2ll_rn(sc(col(s0 + r0 + u)));
+  }
   int8_t* dst = X + static_cast<int64_t>(a) * kp + r0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
@@ -347,14 +391,14 @@ int crt_moduli(int k, int64_t kp) {
   return -1;
 }
 
-template <int NM>
-void launch_crt(const double* A, int64_t lda, int64_t kr, int n, int64_t kp, int64_t np, int k,
+template <int NM, class SRC>
+void launch_crt(const SRC& src, int64_t s0, int64_t kr, int n, int64_t kp, int64_t np, int k,
                 const int* ex, int8_t* X, cudaStream_t s) {
   dim3 g(static_cast<unsigned>(ceil_div(kp / 4, 256)), static_cast<unsigned>(np));
   if (k <= 30)
-    residue_kernel<NM, true><<<g, 256, 0, s>>>(A, lda, kr, n, kp, np, k, ex, X);
+    residue_kernel<NM, true, SRC><<<g, 256, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
   else
-    residue_kernel<NM, false><<<g, 256, 0, s>>>(A, lda, kr, n, kp, np, k, ex, X);
+    residue_kernel<NM, false, SRC><<<g, 256, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
   check_launch("residue_kernel");
 }
 template <int NM>
@@ -466,7 +510,8 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
   bool first = true;
   for (int64_t s0 = 0; s0 < rows; s0 += kp) {
     const int64_t kr = std::min(kp, rows - s0);
-    col_exponent_kernel<<<static_cast<unsigned>(np), 256, 0, s>>>(A + s0, lda, kr, n, ex.p);
+    col_exponent_kernel<DenseSrc><<<static_cast<unsigned>(np), 256, 0, s>>>(DenseSrc{A, lda}, s0, kr, n,
+                                                                           ex.p);
     check_launch("col_exponent_kernel");
     dim3 sg(static_cast<unsigned>(ceil_div(kp / 4, 256)), static_cast<unsigned>(np));
     slice_kernel<<<sg, 256, 0, s>>>(A + s0, lda, kr, n, kp, ns, ex.p, X.p, Y.p);
@@ -500,8 +545,10 @@ bool gram_scheme_crt() {
 }
 
 // CRT variant of gram_accumulate_sliced (whole Gram, t_lo = 2 semantics).
-double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, double* gram,
-                           double beta, int ns, cudaStream_t s, int device, GramScratch& sc) {
+template <class SRC>
+static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, double* gram,
+                                      double beta, int ns, cudaStream_t s, int device,
+                                      GramScratch& sc) {
   require(ns >= 4 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: 4..7 plane-equivalents");
   const int k = 7 * ns - 1;
   LtState& st = lt_state(device);
@@ -542,9 +589,9 @@ double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, do
   bool first = true;
   for (int64_t s0 = 0; s0 < rows; s0 += kp) {
     const int64_t kr = std::min(kp, rows - s0);
-    col_exponent_kernel<<<static_cast<unsigned>(np), 256, 0, s>>>(A + s0, lda, kr, n, sc.ex.p);
+    col_exponent_kernel<SRC><<<static_cast<unsigned>(np), 256, 0, s>>>(src, s0, kr, n, sc.ex.p);
     check_launch("col_exponent_kernel");
-#define FSTK_CRT_RES(NMV) launch_crt<NMV>(A + s0, lda, kr, n, kp, np, k, sc.ex.p, sc.X.p, s)
+#define FSTK_CRT_RES(NMV) launch_crt<NMV, SRC>(src, s0, kr, n, kp, np, k, sc.ex.p, sc.X.p, s)
     FSTK_CRT_SWITCH(nm, FSTK_CRT_RES)
 #undef FSTK_CRT_RES
     for (int64_t c0 = 0; c0 < np; c0 += w) {
@@ -565,6 +612,17 @@ double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, do
     first = false;
   }
   return ops;
+}
+
+double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, double* gram,
+                           double beta, int ns, cudaStream_t s, int device, GramScratch& sc) {
+  return gram_accumulate_crt_src(DenseSrc{A, lda}, rows, n, gram, beta, ns, s, device, sc);
+}
+
+double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n, double* gram,
+                                     double beta, int ns, cudaStream_t s, int device,
+                                     GramScratch& sc) {
+  return gram_accumulate_crt_src(DesignSrc{spec}, rows, n, gram, beta, ns, s, device, sc);
 }
 
 }  // namespace fstk_gpu

@@ -203,5 +203,21 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
                               double beta, int slices, int t_lo, cudaStream_t s, int device,
                               GramScratch& sc);
 constexpr int kGramUpgradeSlices = 7;   // escalation target before the native Gram
+// transform = "none" design rows A[r][ell] = scale ((u0 u1) u2 ...)(row0 + r)
+// generated from mode tables (column j_k of mode k at toff[k] + j_k ldt).
+struct DesignSpec {
+  const double* tables;
+  Int64x8 toff;
+  int64_t ldt;
+  int d;
+  Int64x8 ranks;
+  int64_t row0;
+  double scale;
+};
+// The sliced (CRT) Gram of those rows without materialising them.
+bool gram_scheme_crt();
+double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n, double* gram,
+                                     double beta, int slices, cudaStream_t s, int device,
+                                     GramScratch& sc);
 
 }  // namespace fstk_gpu

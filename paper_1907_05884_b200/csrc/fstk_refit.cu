@@ -1157,6 +1157,7 @@ struct fstk_gpu_refit {
   GramScratch gs;        // sliced int8 Gram scratch (fstk_gram.cu)
   int gram_used = 0;     // digit planes of the last Gram (0 = native fp64)
   DevBuf<double> tables;
+  DevBuf<double> kr;     // transform = none: Khatri-Rao of modes 1..d-1 (ldt x R/r0), lazily
   int64_t toff[kMaxOrder] = {0};
   int64_t ldt = 0;
   ~fstk_gpu_refit() {
@@ -1597,6 +1598,124 @@ static int64_t none_block_rows(const fstk_gpu_refit* rf, bool sliced = false) {
   return std::min<int64_t>(round_up(cap, 128), std::max<int64_t>(rf->local_rows, 1));
 }
 
+// ---- transform = none through the Kronecker structure (north_star: A is
+// never materialised).  Row i of A is scale * u0(i) (x) KR(i), KR(i) = the
+// Khatri-Rao row of modes 1..d-1, so with X = x as an r0 x R/r0 matrix
+//   A x  = scale * rowdot(U0, KR X^T)           (one DGEMM + a row dot)
+//   A^T y = scale * (diag(y) U0)^T KR           (one DGEMM)
+// -- 2 S R flops each instead of regenerating S x R values.  These feed the
+// normal equations' rhs and the refinement, which need fp64 accuracy, not the
+// design's bit pattern (the Gram's residues use the bit-exact generator).
+__global__ void khatri_rao_kernel(const double* __restrict__ tables, Int64x8 toff, int64_t ldt,
+                                  int d, Int64x8 ranks, int64_t rows, int64_t Rr,
+                                  double* __restrict__ kr) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  for (int64_t m = blockIdx.y; m < Rr; m += gridDim.y) {
+    int64_t rem = m;
+    double v = 1.0;
+    for (int k = 1; k < d; ++k) {
+      const int64_t jk = rem % ranks.v[k];
+      rem /= ranks.v[k];
+      v *= tables[toff.v[k] + jk * ldt + i];
+    }
+    kr[m * ldt + i] = v;
+  }
+}
+
+__global__ void scale_rows_kernel(const double* __restrict__ u0, int64_t ldt, int r0,
+                                  const double* __restrict__ y, int64_t rows,
+                                  double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const double yi = y[i];
+  for (int j = 0; j < r0; ++j) out[j * ldt + i] = u0[j * ldt + i] * yi;
+}
+
+__global__ void row_dot_kernel(const double* __restrict__ u0, const double* __restrict__ Y,
+                               int64_t ldt, int r0, int64_t rows, double scale,
+                               const double* __restrict__ b, double* __restrict__ out) {
+  // out_i = b_i - scale * sum_j U0[i, j] Y[i, j]  (b may be null: out_i = scale * dot)
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  double acc = 0.0;
+  for (int j = 0; j < r0; ++j) acc = fma(u0[j * ldt + i], Y[j * ldt + i], acc);
+  out[i] = b ? b[i] - scale * acc : scale * acc;
+}
+
+static const double* none_kr(fstk_gpu_refit* rf) {
+  const fstk_gpu_model* m = rf->model;
+  const int64_t rows = rf->local_rows;
+  const int64_t Rr = rf->R / m->ranks[0];
+  if (!rf->kr.p) {
+    rf->kr.alloc(static_cast<size_t>(std::max<int64_t>(rf->ldt, 1)) * Rr);
+    FSTK_CUDA(cudaMemsetAsync(rf->kr.p, 0, rf->kr.n * 8, rf->stream));
+    if (rows > 0) {
+      Int64x8 to{}, rk{};
+      for (int k = 0; k < m->d; ++k) {
+        to.v[k] = rf->toff[k];
+        rk.v[k] = m->ranks[k];
+      }
+      dim3 g(static_cast<unsigned>(ceil_div(rows, 256)), static_cast<unsigned>(std::min<int64_t>(Rr, 4096)));
+      khatri_rao_kernel<<<g, 256, 0, rf->stream>>>(rf->tables.p, to, rf->ldt, m->d, rk, rows, Rr,
+                                                   rf->kr.p);
+      check_launch("khatri_rao_kernel");
+    }
+  }
+  return rf->kr.p;
+}
+
+// out (R) = A_local^T y (y: local rows); beta = 0 overwrite.
+static void none_At(fstk_gpu_refit* rf, const double* y, double* out) {
+  const fstk_gpu_model* m = rf->model;
+  const int64_t rows = rf->local_rows;
+  const int r0 = static_cast<int>(m->ranks[0]);
+  const int64_t Rr = rf->R / r0;
+  cudaStream_t s = rf->stream;
+  if (rows == 0) {
+    FSTK_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(rf->R) * 8, s));
+    return;
+  }
+  const double* kr = none_kr(rf);
+  DevBuf<double> uy(static_cast<size_t>(rf->ldt) * r0);
+  FSTK_CUDA(cudaMemsetAsync(uy.p, 0, uy.n * 8, s));
+  scale_rows_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, s>>>(
+      rf->tables.p + rf->toff[0], rf->ldt, r0, y, rows, uy.p);
+  check_launch("scale_rows_kernel");
+  Handles& h = handles(rf->device);
+  cublasSetStream(h.blas, s);
+  const double sc = rf->plan.scale, zero = 0.0;
+  if (cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, r0, static_cast<int>(Rr), static_cast<int>(rows),
+                  &sc, uy.p, static_cast<int>(rf->ldt), kr, static_cast<int>(rf->ldt), &zero, out,
+                  r0) != CUBLAS_STATUS_SUCCESS)
+    fail(FSTK_E_COMPUTE, "cublasDgemm failed (none A^T y)");
+  count_launch();
+}
+
+// r (local rows) = b - A_local x.
+static void none_residual(fstk_gpu_refit* rf, const double* x, double* r) {
+  const fstk_gpu_model* m = rf->model;
+  const int64_t rows = rf->local_rows;
+  const int r0 = static_cast<int>(m->ranks[0]);
+  const int64_t Rr = rf->R / r0;
+  cudaStream_t s = rf->stream;
+  if (rows == 0) return;
+  const double* kr = none_kr(rf);
+  DevBuf<double> Y(static_cast<size_t>(rf->ldt) * r0);
+  Handles& h = handles(rf->device);
+  cublasSetStream(h.blas, s);
+  const double one = 1.0, zero = 0.0;
+  // Y (rows x r0) = KR (rows x Rr) * X^T, X = x as r0 x Rr (column-major).
+  if (cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_T, static_cast<int>(rows), r0, static_cast<int>(Rr),
+                  &one, kr, static_cast<int>(rf->ldt), x, r0, &zero, Y.p,
+                  static_cast<int>(rf->ldt)) != CUBLAS_STATUS_SUCCESS)
+    fail(FSTK_E_COMPUTE, "cublasDgemm failed (none A x)");
+  count_launch();
+  row_dot_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, s>>>(
+      rf->tables.p + rf->toff[0], Y.p, rf->ldt, r0, rows, rf->plan.scale, rf->b.p, r);
+  check_launch("row_dot_kernel");
+}
+
 static void generate_design_block(const fstk_gpu_refit* rf, int64_t row0, int64_t nrows,
                                   double* W, int64_t ldw, cudaStream_t s) {
   const fstk_gpu_model* m = rf->model;
@@ -1652,7 +1771,25 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
       const int level = slices < 0 ? gram_slices() : slices;
       const bool sliced = level > 0 && gram_sliced_applies(arows, n);
       rf->gram_used = sliced ? level : 0;
-      if (rf->none) {
+      if (rf->none && sliced && gram_scheme_crt()) {
+        // A never materialised: CRT residues straight from the mode tables,
+        // A^T b through the Kronecker structure.
+        ProfScope prof(FSTK_PROF_GRAM, s);
+        DesignSpec spec{};
+        spec.tables = rf->tables.p;
+        for (int k = 0; k < rf->model->d; ++k) {
+          spec.toff.v[k] = rf->toff[k];
+          spec.ranks.v[k] = rf->model->ranks[k];
+        }
+        spec.ldt = rf->ldt;
+        spec.d = rf->model->d;
+        spec.row0 = 0;
+        spec.scale = rf->plan.scale;
+        i8ops = gram_accumulate_sliced_design(spec, arows, n, gram, 0.0, rf->gram_used, s,
+                                              rf->device, rf->gs);
+        none_At(rf, rf->b.p, rhs);
+        FSTK_CUDA(cudaStreamSynchronize(s));
+      } else if (rf->none) {
         // A^T A accumulated over generated row blocks (A never materialised).
         const int64_t BS = none_block_rows(rf, sliced);
         DevBuf<double> W(static_cast<size_t>(BS) * rf->R);
@@ -1885,22 +2022,10 @@ int32_t fstk_gpu_refit_correction(fstk_gpu_refit* rf, const double* x_dev, doubl
     FSTK_CUDA(cudaMemcpyAsync(rf->tmp_r.p, rf->b.p, arows * 8, cudaMemcpyDeviceToDevice, s));
     const double one = 1.0, mone = -1.0, zero = 0.0;
     if (rf->none) {
-      const int64_t BS = none_block_rows(rf);
-      DevBuf<double> W(static_cast<size_t>(BS) * rf->R);
-      for (int64_t r0 = 0; r0 < arows; r0 += BS) {
-        const int64_t nb_rows = std::min(BS, arows - r0);
-        generate_design_block(rf, r0, nb_rows, W.p, BS, s);
-        ProfScope prof(FSTK_PROF_SOLVE, s);
-        const double beta = r0 == 0 ? 0.0 : 1.0;
-        if (cublasDgemv(h.blas, CUBLAS_OP_N, static_cast<int>(nb_rows), n, &mone, W.p,
-                        static_cast<int>(BS), x_dev, 1, &one, rf->tmp_r.p + r0, 1) !=
-                CUBLAS_STATUS_SUCCESS ||
-            cublasDgemv(h.blas, CUBLAS_OP_T, static_cast<int>(nb_rows), n, &one, W.p,
-                        static_cast<int>(BS), rf->tmp_r.p + r0, 1, &beta, s_dev, 1) !=
-                CUBLAS_STATUS_SUCCESS)
-          fail(FSTK_E_COMPUTE, "cublasDgemv failed");
-        count_launch(2);
-      }
+      // s = A^T (b - A x) through the Kronecker structure (no rows generated).
+      ProfScope prof(FSTK_PROF_SOLVE, s);
+      none_residual(rf, x_dev, rf->tmp_r.p);
+      none_At(rf, rf->tmp_r.p, s_dev);
       FSTK_CUDA(cudaStreamSynchronize(s));
       return;
     }
