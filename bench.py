@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-refit", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--transform", default="dct")
+    ap.add_argument("--no-refit-none", action="store_true",
+                    help="skip the transform='none' refit reported as refit_none")
     ap.add_argument("--refit-warmup", type=int, default=1,
                     help="untimed full-size refits before the timed one (cuBLASLt algorithm "
                          "choice per Gram shape, lazy kernel loading)")
@@ -426,6 +428,11 @@ def main():
         # The refit is ONE problem: every rank passes the same (rank-0) cloud.
         rpts, rvals = (pts, vals) if rank == 0 else dataset(args.config, args.points, 0)
         line["refit"] = run_refit(model, rpts, rvals, cfgd, args, rank, world, dev, peak_mma)
+        if args.transform != "none" and not args.no_refit_none:
+            # The north star's literal estimator (sampled Kronecker rows, no
+            # mixing; A never materialised), measured beside the reference's.
+            line["refit_none"] = run_refit(model, rpts, rvals, cfgd, args, rank, world, dev,
+                                           peak_mma, transform="none")
 
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_eval_baseline(model, pts)
@@ -461,25 +468,26 @@ def gram_roofline(gram_flops, info, t, peak_fp64):
             "kernel": "cublasDsyrk/Dgemm (library SYRK on the sketched A)"}
 
 
-def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
+def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=None):
     import torch
 
     import paper_1907_05884_b200 as F
     from paper_1907_05884_b200 import synth
 
+    tform = transform or args.transform
     R = int(np.prod(model.ranks))
     S = cfgd["m_factor"] * R
     # warm-up on a small problem (cuBLAS/cuSOLVER handles, twiddle cache)
     wm = synth.random_model((4, 4, 4), (6, 6, 6), 4, seed=1)
     wp = synth.uniform_points(4096, 3, 2)
-    F.reestimate_core(wm, wp, np.sin(wp[:, 0]), seed=1, transform=args.transform)
+    F.reestimate_core(wm, wp, np.sin(wp[:, 0]), seed=1, transform=tform)
 
     def one():
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        sess = F.RefitSession(model, pts, vals, seed=0, sample_rows=S, transform=args.transform,
+        sess = F.RefitSession(model, pts, vals, seed=0, sample_rows=S, transform=tform,
                               shard=rank, shards=world, layout="columns" if world > 1 else "rows")
         t_x = 0.0
         if world > 1:
@@ -537,7 +545,7 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak):
     return {"seconds": t_all, "hot_path_seconds": t_hot, "warmup_refits": args.refit_warmup,
             "cold": cold,
             "scaling": "strong", "sample_rows": S, "working_rows": info["working_rows"],
-            "padded_rows": info["padded_rows"], "transform": args.transform,
+            "padded_rows": info["padded_rows"], "transform": tform,
             "kernel_ms": {k: v[0] for k, v in kprof.items() if v[1]},
             "kernel_launches": {k: v[1] for k, v in kprof.items() if v[1]},
             "stages_s": {"prepare": tm["prepare_s"], "alloc": tm["alloc_s"], "sketch": tm["sketch_s"],
