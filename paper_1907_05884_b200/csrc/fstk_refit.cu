@@ -1075,12 +1075,14 @@ struct Handles {
   cublasHandle_t blas = nullptr;
   cusolverDnHandle_t solver = nullptr;
 };
-static std::mutex g_h_mu;
-static std::map<int, Handles> g_handles;
-
+// One cuBLAS/cuSOLVER handle pair per (host thread, device): a handle must
+// not be driven from two threads at once (cublasSetStream + calls), and the
+// C-ABI is callable from many threads (refits of different models on one
+// device run concurrently).  Created on first use with the device current;
+// left to the process teardown.
 static Handles& handles(int device) {
-  std::lock_guard<std::mutex> lk(g_h_mu);
-  Handles& h = g_handles[device];
+  static thread_local std::map<int, Handles> tl_handles;
+  Handles& h = tl_handles[device];
   if (!h.blas) {
     if (cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, "cublasCreate failed");
     if (cusolverDnCreate(&h.solver) != CUSOLVER_STATUS_SUCCESS)
