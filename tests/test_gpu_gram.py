@@ -182,15 +182,16 @@ def _ill_conditioned_model(seed=21):
     return F.Model(m.core, modes, m.metadata)
 
 
-def test_sliced_gram_escalates_when_it_cannot_precondition(O):
+@pytest.mark.parametrize("t", ["dct", "none"])
+def test_sliced_gram_escalates_when_it_cannot_precondition(O, t):
     m = _ill_conditioned_model()
     pts = synth.uniform_points(40_000, 3, 2)
     vals = synth.flame_field(pts, seed=4)
     prev = F.gram_slices(4)
     try:
-        new_s, info_s = F.reestimate_core(m, pts, vals, seed=8)
+        new_s, info_s = F.reestimate_core(m, pts, vals, seed=8, transform=t)
         F.gram_slices(0)
-        new_n, info_n = F.reestimate_core(m, pts, vals, seed=8)
+        new_n, info_n = F.reestimate_core(m, pts, vals, seed=8, transform=t)
     finally:
         F.gram_slices(prev)
     # 4 planes (28 bits) cannot precondition cond(A)^2 ~ 1e12: the solve
