@@ -732,6 +732,140 @@ static size_t mode_smem(const fstk_gpu_model* m, int k0, int k1, int threads) {
   return static_cast<size_t>(pm + 1) * threads * sizeof(double);
 }
 
+// Coefficients as a by-value kernel parameter (CUDA >= 12.1: up to 32 KB):
+// with the degree loop unrolled for a compile-time pmax, every coefficient is
+// a constant-bank operand of its FMA -- no shared-memory loads (the MIO stall
+// of mode_dense_kernel), no shared memory at all, ~50 registers per thread,
+// so these CTAs co-reside with the contraction of the other stream.  The
+// arithmetic is mode_dense_kernel's, step for step (bit-identical results).
+template <int NQ, int JC>
+struct CoefParam {
+  double c[NQ][JC];
+};
+
+template <bool EXACT, int JC, int P>
+__global__ void __launch_bounds__(128) mode_param_kernel(
+    const ModeDev md, const CoefParam<P + 1, JC> cp, int j0, const double* __restrict__ xs,
+    int64_t n, int64_t n_out, const int64_t* __restrict__ row_src, double* __restrict__ tk,
+    int64_t ldt, unsigned long long* err_row) {
+  constexpr int PPT = 2;  // rows i and i + 128: each constant operand feeds two FMAs
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * (128 * PPT) + threadIdx.x;
+  const int jn = min(JC, md.r - j0);
+  double t[PPT];
+  bool live[PPT];
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    const int64_t i = base + u * 128;
+    live[u] = i < n_out;
+    t[u] = 0.0;
+    if (!live[u]) continue;
+    int64_t src = i;
+    bool valid = i < n;
+    if (row_src) {
+      src = i < n ? row_src[i] : -1;
+      valid = src >= 0;
+    }
+    if (!valid) {
+#pragma unroll
+      for (int j = 0; j < JC; ++j)
+        if (j < jn) tk[(j0 + j) * ldt + i] = 0.0;
+      live[u] = false;
+      continue;
+    }
+    const double x = xs[src];
+    if (!(x >= md.lo - md.slack && x <= md.hi + md.slack)) {
+      atomicMin(err_row, static_cast<unsigned long long>(i));
+    } else {
+      const double cl = fmin(md.hi, fmax(md.lo, x));
+      t[u] = xadd(-1.0, __ddiv_rn(xmul(2.0, xsub(cl, md.lo)), md.span));
+    }
+  }
+  if (!(live[0] || live[1])) return;
+  double acc[PPT][JC];
+#pragma unroll
+  for (int u = 0; u < PPT; ++u)
+#pragma unroll
+    for (int j = 0; j < JC; ++j) acc[u][j] = 0.0;
+  auto apply = [&](const double (&row)[JC], const double (&L)[PPT]) {
+#pragma unroll
+    for (int j = 0; j < JC; ++j)
+#pragma unroll
+      for (int u = 0; u < PPT; ++u)
+        acc[u][j] = EXACT ? xadd(acc[u][j], xmul(row[j], L[u])) : fma(row[j], L[u], acc[u][j]);
+  };
+  // legendre_values (basis.cpp:49-61), same rounding sequence.
+  double L[PPT], pm1[PPT], pm0[PPT];
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) L[u] = 1.0;
+  apply(cp.c[0], L);
+  if (P >= 1) {
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) L[u] = xmul(c_leg.norm[1], t[u]);
+    apply(cp.c[1], L);
+  }
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    pm1[u] = 1.0;
+    pm0[u] = t[u];
+  }
+#pragma unroll
+  for (int q = 1; q < P; ++q) {
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+      const double num = xsub(xmul(xmul(c_leg.a[q], t[u]), pm0[u]), xmul(c_leg.b[q], pm1[u]));
+      const double pn1 = xdiv_small(num, c_leg.c[q], c_leg.rc[q]);
+      pm1[u] = pm0[u];
+      pm0[u] = pn1;
+      L[u] = xmul(c_leg.norm[q + 1], pn1);
+    }
+    apply(cp.c[q + 1], L);
+  }
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    if (!live[u]) continue;
+    const int64_t i = base + u * 128;
+#pragma unroll
+    for (int j = 0; j < JC; ++j)
+      if (j < jn) tk[(j0 + j) * ldt + i] = acc[u][j];
+  }
+}
+
+template <bool EXACT, int JC, int P>
+static void launch_param_t(const ModeDev& md, const double* xs, int64_t n, int64_t n_out,
+                           const int64_t* row_src, double* tk, int64_t ldt,
+                           unsigned long long* err_row, cudaStream_t s) {
+  for (int c = 0; c < md.nchunk; ++c) {
+    CoefParam<P + 1, JC> cp;
+    for (int q = 0; q <= P; ++q)
+      for (int j = 0; j < JC; ++j) cp.c[q][j] = md.h_dense[static_cast<size_t>(q) * md.ldc + c * JC + j];
+    mode_param_kernel<EXACT, JC, P><<<static_cast<unsigned>(ceil_div(n_out, 256)), 128, 0, s>>>(
+        md, cp, c * JC, xs, n, n_out, row_src, tk, ldt, err_row);
+    check_launch("mode_param_kernel");
+  }
+}
+
+// The parameter kernel for the (pmax, jc) pairs it is instantiated for.
+template <bool EXACT>
+static bool launch_param(const ModeDev& md, const double* xs, int64_t n, int64_t n_out,
+                         const int64_t* row_src, double* tk, int64_t ldt,
+                         unsigned long long* err_row, cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = std::getenv("FSTK_MODE_PARAM");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!on || !md.h_dense) return false;
+#define FSTK_PJ(P, J)                                                                 \
+  if (md.pmax == P && md.jc == J) {                                                    \
+    launch_param_t<EXACT, J, P>(md, xs, n, n_out, row_src, tk, ldt, err_row, s);       \
+    return true;                                                                       \
+  }
+#define FSTK_P(P) FSTK_PJ(P, 8) FSTK_PJ(P, 16) FSTK_PJ(P, 32)
+  FSTK_P(16) FSTK_P(20) FSTK_P(32) FSTK_P(48) FSTK_P(64)
+#undef FSTK_P
+#undef FSTK_PJ
+  return false;
+}
+
 template <bool EXACT, int JC>
 static void launch_dense_t(const ModeDev& md, const double* xs, int64_t n, int64_t n_out,
                            const int64_t* row_src, double* tk, int64_t ldt,
@@ -785,10 +919,12 @@ static void launch_mode_k(const fstk_gpu_model* m, int k, const double* xs, int6
   }
   const ModeDev& md = m->modes_dev.m[k];
   if (m->modes[k].sorted) {
-    if (exact)
-      launch_dense<true>(md, xs, n, n_out, row_src, tk, ldt, err_row, s, m->device);
-    else
+    if (exact) {
+      if (!launch_param<true>(md, xs, n, n_out, row_src, tk, ldt, err_row, s))
+        launch_dense<true>(md, xs, n, n_out, row_src, tk, ldt, err_row, s, m->device);
+    } else if (!launch_param<false>(md, xs, n, n_out, row_src, tk, ldt, err_row, s)) {
       launch_dense<false>(md, xs, n, n_out, row_src, tk, ldt, err_row, s, m->device);
+    }
     return;
   }
   const int threads = 128;
@@ -1402,9 +1538,11 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
     if (dense.empty()) dense.push_back(0.0);
     m->d_dense.alloc(dense.size());
     FSTK_CUDA(cudaMemcpy(m->d_dense.p, dense.data(), dense.size() * 8, cudaMemcpyHostToDevice));
+    m->h_dense = dense;
     m->modes_dev.d = d;
     for (int k = 0; k < d; ++k) {
       m->modes_dev.m[k].dense = m->d_dense.p + dense_off[k];
+      m->modes_dev.m[k].h_dense = m->h_dense.data() + dense_off[k];
       m->modes_dev.m[k].jc = jc[k];
       m->modes_dev.m[k].nchunk = nch[k];
       m->modes_dev.m[k].ldc = jc[k] * nch[k];

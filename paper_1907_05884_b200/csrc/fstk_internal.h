@@ -32,6 +32,7 @@ struct ModeDev {
   int ldc;                     // nchunk * jc
   int jc;                      // functions per dense-kernel thread (multiple of 8, <= 64)
   int nchunk;
+  const double* h_dense;       // host copy of `dense` (builds the kernel-parameter blocks)
 };
 struct ModesDev {
   int d;
@@ -114,6 +115,7 @@ struct fstk_gpu_model {
   fstk_gpu::DevBuf<uint32_t> d_idx;
   fstk_gpu::DevBuf<double> d_coef;
   fstk_gpu::DevBuf<double> d_dense;  // all modes' dense coefficient blocks
+  std::vector<double> h_dense;       // host copy (kernel-parameter coefficient blocks)
   fstk_gpu::GenModeDev gen[fstk_gpu::kMaxOrder] = {};  // wavelet-capable per-mode params
   fstk_gpu::DevBuf<int> d_fn_spec;
   std::vector<std::shared_ptr<fstk_gpu::DevBuf<double>>> mother_refs;
