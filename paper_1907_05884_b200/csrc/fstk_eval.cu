@@ -1615,7 +1615,11 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
     for (int k = 0; k < d; ++k) per_pt += m->rp[k];
     // Chunks large enough that the last wave of tiles is a small fraction
     // (>= ~100 tiles per SM), capped near 2 GB of table workspace.
-    m->chunk_points = std::min<int64_t>(int64_t(1) << 21,
+    static const int chunk_log2 = [] {
+      const char* e = std::getenv("FSTK_EVAL_CHUNK_LOG2");
+      return e ? std::min(24, std::max(16, std::atoi(e))) : 21;
+    }();
+    m->chunk_points = std::min<int64_t>(int64_t(1) << chunk_log2,
                                         std::max<int64_t>(int64_t(1) << 16,
                                                           (int64_t(1) << 31) / (per_pt * 8)));
     m->chunk_points = round_up(m->chunk_points, 128);
