@@ -1160,6 +1160,9 @@ struct fstk_gpu_refit {
   int gram_used = 0;     // digit planes of the last Gram (0 = native fp64)
   DevBuf<double> tables;
   DevBuf<double> kr;     // transform = none: Khatri-Rao of modes 1..d-1 (ldt x R/r0), lazily
+  DevBuf<double> kr_tmp; // transform = none: ldt x r0 scratch of the structured products
+  DevBuf<double> apply_dx;  // refinement scratch (no per-step allocations)
+  DevBuf<int> apply_info;
   int64_t toff[kMaxOrder] = {0};
   int64_t ldt = 0;
   ~fstk_gpu_refit() {
@@ -1679,7 +1682,8 @@ static void none_At(fstk_gpu_refit* rf, const double* y, double* out) {
     return;
   }
   const double* kr = none_kr(rf);
-  DevBuf<double> uy(static_cast<size_t>(rf->ldt) * r0);
+  rf->kr_tmp.ensure(static_cast<size_t>(rf->ldt) * r0);
+  DevBuf<double>& uy = rf->kr_tmp;
   FSTK_CUDA(cudaMemsetAsync(uy.p, 0, uy.n * 8, s));
   scale_rows_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, s>>>(
       rf->tables.p + rf->toff[0], rf->ldt, r0, y, rows, uy.p);
@@ -1703,7 +1707,8 @@ static void none_residual(fstk_gpu_refit* rf, const double* x, double* r) {
   cudaStream_t s = rf->stream;
   if (rows == 0) return;
   const double* kr = none_kr(rf);
-  DevBuf<double> Y(static_cast<size_t>(rf->ldt) * r0);
+  rf->kr_tmp.ensure(static_cast<size_t>(rf->ldt) * r0);
+  DevBuf<double>& Y = rf->kr_tmp;
   Handles& h = handles(rf->device);
   cublasSetStream(h.blas, s);
   const double one = 1.0, zero = 0.0;
@@ -2088,8 +2093,10 @@ int32_t fstk_gpu_refit_apply(fstk_gpu_refit* rf, const double* s_dev, double* x_
     cusolverDnSetStream(h.solver, s);
     cublasSetStream(h.blas, s);
     const int n = static_cast<int>(rf->R);
-    DevBuf<double> dx(n);
-    DevBuf<int> dinfo(1);
+    rf->apply_dx.ensure(static_cast<size_t>(n));
+    rf->apply_info.ensure(1);
+    DevBuf<double>& dx = rf->apply_dx;
+    DevBuf<int>& dinfo = rf->apply_info;
     FSTK_CUDA(cudaMemcpyAsync(dx.p, s_dev, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
     ProfScope prof(FSTK_PROF_SOLVE, s);
     if (n >= 4096) {
