@@ -184,6 +184,15 @@ int32_t fstk_gpu_reestimate_core(const fstk_gpu_model* model, const double* poin
  * A^T b into caller-provided DEVICE buffers so the caller can sum them across
  * ranks (one NCCL all-reduce); solve() runs the Cholesky solve on the summed
  * system and the validation residuals. */
+/* Host-only diagnostics of the bit-exact RNG replay (no device work, callable
+ * without a GPU): rng.cpp sample_without_replacement of Rng(seed) (sorted,
+ * min(n, k) values; the library replays the partial Fisher-Yates with O(k)
+ * state) and make_plan (randls.cpp:54-75: signs[q_pad], rows[s], scale,
+ * q_pad = next_pow2(q_w)). */
+int32_t fstk_gpu_sample_without_replacement(uint64_t seed, uint64_t n, uint64_t k,
+                                            uint64_t* out, fstk_gpu_error* err);
+int32_t fstk_gpu_make_plan(uint64_t q_w, uint64_t s, uint64_t seed, double* signs,
+                           uint64_t* rows, double* scale, uint64_t* q_pad, fstk_gpu_error* err);
 int32_t fstk_gpu_refit_begin(const fstk_gpu_model* model, const double* points,
                              const double* values, int64_t q, int32_t d,
                              const fstk_sketch_cfg* cfg, int32_t shard,

@@ -87,6 +87,7 @@ EXPORTS = [
     "fstk_gpu_refit_normal_equations_native", "fstk_gpu_gram_slices", "fstk_gpu_gram_device",
     "fstk_gpu_refit_normal_equations_level", "fstk_gpu_refit_begin_columns",
     "fstk_gpu_refit_exchange_layout", "fstk_gpu_refit_adopt_rows",
+    "fstk_gpu_sample_without_replacement", "fstk_gpu_make_plan",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -143,6 +144,11 @@ def lib():
                                                  C.POINTER(VP), C.POINTER(C.c_int64),
                                                  C.POINTER(Err)]
     L.fstk_gpu_refit_adopt_rows.argtypes = [VP, C.POINTER(Err)]
+    L.fstk_gpu_sample_without_replacement.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64,
+                                                      C.POINTER(C.c_uint64), C.POINTER(Err)]
+    L.fstk_gpu_make_plan.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, DP,
+                                     C.POINTER(C.c_uint64), DP, C.POINTER(C.c_uint64),
+                                     C.POINTER(Err)]
     L.fstk_gpu_refit_normal_equations_level.argtypes = [VP, C.c_int32, VP, VP,
                                                         C.POINTER(ReestimateInfo), C.POINTER(Err)]
     L.fstk_gpu_gram_device.argtypes = [VP, C.c_int64, C.c_int64, C.c_int32, VP, C.c_int32,

@@ -1506,6 +1506,32 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
 }
 }  // namespace fstk_gpu
 
+// Host-only diagnostics of the bit-exact RNG replay (no device work; callable
+// without a GPU): rng.cpp sample_without_replacement seeded like
+// Rng(seed), and make_plan (randls.cpp:54-75).
+int32_t fstk_gpu_sample_without_replacement(uint64_t seed, uint64_t n, uint64_t k,
+                                            uint64_t* out, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    require(out || std::min(n, k) == 0, FSTK_E_PARAMETER, "null argument");
+    Rng rng(seed);
+    const auto v = rng.sample_without_replacement(n, k);
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
+int32_t fstk_gpu_make_plan(uint64_t q_w, uint64_t s, uint64_t seed, double* signs,
+                           uint64_t* rows, double* scale, uint64_t* q_pad, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    const Plan p = make_plan(q_w, s, seed);
+    if (q_pad) *q_pad = p.q_pad;
+    if (scale) *scale = p.scale;
+    if (signs) std::copy(p.signs.begin(), p.signs.end(), signs);
+    if (rows) std::copy(p.rows.begin(), p.rows.end(), rows);
+  });
+}
+
 int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, const double* values,
                              int64_t q, int32_t d, const fstk_sketch_cfg* cfg, int32_t shard,
                              int32_t shards, fstk_gpu_refit** out, fstk_reestimate_info* info,
