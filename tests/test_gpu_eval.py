@@ -26,6 +26,13 @@ SHAPES = {
     "ragged": ((5, 13, 3), (9, 17, 4), 6),
     "wide_r1": ((8, 80, 3), (10, 64, 5), 7),
     "d5": ((3, 2, 4, 2, 3), (4, 4, 4, 4, 4), 3),
+    "d6": ((3, 2, 2, 2, 2, 2), (4, 3, 3, 3, 3, 3), 3),
+    "d7": ((2, 2, 2, 2, 2, 2, 2), (3, 3, 3, 3, 3, 3, 3), 2),
+    "d8_max_order": ((2, 2, 2, 2, 2, 2, 2, 2), (3, 3, 2, 2, 2, 2, 2, 2), 2),
+    "p64_cap_degree": ((4, 3, 2), (64, 64, 64), 24),
+    "jc48_shared_kernel": ((48, 8, 2), (48, 8, 8), 12),
+    "jc40": ((40, 6, 3), (20, 20, 20), 8),
+    "p48_param_kernel_jc8": ((8, 8, 8), (48, 48, 48), 12),
 }
 
 
@@ -223,3 +230,28 @@ def test_evaluate_fields_shared_points(O):
     for f, m in enumerate(models):
         assert np.array_equal(out[:, f], m.evaluate_batch(pts))
         assert rel(out[:, f], O.evaluate_batch(m, pts)) <= 1e-12
+
+
+def test_boundary_and_slack_points_evaluate(O):
+    # basis.cpp:215-222: points exactly on lo/hi and within +-1e-12 span are
+    # clamped and evaluate like the boundary; the GPU agrees with the oracle.
+    m = synth.random_model((6, 5, 4), (12, 12, 12), 5, seed=70)
+    eps = 1e-12 * 0.999
+    edge = np.array([[0.0, 1.0, 0.5], [1.0, 0.0, 0.0], [-eps, 1.0 + eps, 0.25],
+                     [1.0 + eps, -eps, 1.0], [0.5, 0.5, 0.5]])
+    got = m.evaluate_batch(np.asfortranarray(edge))
+    want = O.evaluate_batch(m, np.asfortranarray(edge))
+    assert rel(got, want) <= 1e-12
+    clamped = np.clip(edge, 0.0, 1.0)
+    assert np.array_equal(got, m.evaluate_batch(np.asfortranarray(clamped)))
+
+
+def test_refit_d2_and_d4_parity(O):
+    for ranks in ((6, 5), (3, 3, 2, 2)):
+        m = synth.random_model(ranks, [6] * len(ranks), 4, seed=71)
+        q = 20_000
+        pts = synth.uniform_points(q, len(ranks), 72)
+        vals = O.evaluate_batch(m, pts) + 1e-2 * np.random.default_rng(73).normal(size=q)
+        new, _ = F.reestimate_core(m, pts, vals, seed=5)
+        core_o, _ = O.reestimate_core(m, pts, vals, seed=5)
+        assert rel(new.core.reshape(-1, order="F"), core_o) <= 1e-9
