@@ -374,7 +374,11 @@ def main():
     per_launch_pts = n * args.steps / max(c_n, 1)
     achieved = fc * n * args.steps / (c_ms * 1e-3) / 1e12 if c_ms > 0 else None
     traffic, tpts = traffic_from_profile(args.config)
-    roof = {"bound": "tensor", "kernel": "contract_kernel (fp64 DMMA m8n8k4)",
+    kr = os.environ.get("FSTK_CONTRACT_KR")
+    use_kr = (kr != "0") if kr is not None and model.order in (3, 4) else model.order == 4
+    kname = ("contract_kr_kernel (fp64 DMMA m8n8k4, Khatri-Rao K = r0 r1)" if use_kr
+             else "contract_kernel (fp64 DMMA m8n8k4)")
+    roof = {"bound": "tensor", "kernel": kname,
             "achieved": achieved, "peak": peak_mma, "unit": "TFLOP/s",
             "frac": (achieved / peak_mma) if achieved else None,
             "traffic": (traffic * per_launch_pts / tpts) if traffic and tpts else None,
