@@ -119,6 +119,12 @@ uint64_t fstk_gpu_launch_count(void);
  * (model.cpp:22-53): Shape on count/domain mismatch, Parameter on invalid
  * bases.  Wavelet bases are accepted by the format but not by this GPU path
  * (FSTK_E_PARAMETER). */
+/* The devices of this process: a model created with device = -1
+ * lives on ids[0] with replicas on the others, and a host evaluate_batch on it
+ * splits the points into contiguous slabs, one per device, concurrently (the
+ * reference's single-process call, spread over several GPUs).  n = 0 resets
+ * to the current device.  Other entry points use the first device. */
+int32_t fstk_gpu_set_devices(int32_t n, const int32_t* ids, fstk_gpu_error* err);
 int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device,
                               fstk_gpu_model** out, fstk_gpu_error* err);
 void fstk_gpu_model_destroy(fstk_gpu_model* model);

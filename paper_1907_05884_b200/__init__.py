@@ -7,7 +7,7 @@ proj/python/module.cpp): `Model.evaluate_batch`, `load_model`,
 `reestimate_core`, `BasisSpec`, plus the refit diagnostics.  All compute runs
 in libfstk_gpu.so on the GPU; there is no CPU fallback.
 """
-from ._lib import FstkError, FstkIOError, FstkValueError, launch_count
+from ._lib import FstkError, FstkIOError, FstkValueError, launch_count, set_devices
 from .cloud import (PointCloud, read_cloud, read_cloud_binary, read_cloud_csv, read_cloud_device,
                     read_points_csv, write_cloud_binary, write_cloud_csv)
 from .model import (BasisSpec, Model, ModelMetadata, ModeFunction, evaluate_fields, load_model,
@@ -27,6 +27,6 @@ __all__ = [
     "evaluate_fields",
     "reestimate_core", "RefitSession", "build_design_rows", "sketch", "mixed_matrix",
     "sketch_config", "self_convergence", "leverage_scores", "gram_slices", "gram", "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
-    "launch_count", "PointCloud", "read_cloud", "read_cloud_binary", "read_cloud_csv",
+    "launch_count", "set_devices", "PointCloud", "read_cloud", "read_cloud_binary", "read_cloud_csv",
     "read_cloud_device", "read_points_csv", "write_cloud_binary", "write_cloud_csv",
 ]

@@ -87,7 +87,7 @@ EXPORTS = [
     "fstk_gpu_refit_normal_equations_native", "fstk_gpu_gram_slices", "fstk_gpu_gram_device",
     "fstk_gpu_refit_normal_equations_level", "fstk_gpu_refit_begin_columns",
     "fstk_gpu_refit_exchange_layout", "fstk_gpu_refit_adopt_rows",
-    "fstk_gpu_sample_without_replacement", "fstk_gpu_make_plan",
+    "fstk_gpu_sample_without_replacement", "fstk_gpu_make_plan", "fstk_gpu_set_devices",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -144,6 +144,7 @@ def lib():
                                                  C.POINTER(VP), C.POINTER(C.c_int64),
                                                  C.POINTER(Err)]
     L.fstk_gpu_refit_adopt_rows.argtypes = [VP, C.POINTER(Err)]
+    L.fstk_gpu_set_devices.argtypes = [C.c_int32, C.POINTER(C.c_int32), C.POINTER(Err)]
     L.fstk_gpu_sample_without_replacement.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64,
                                                       C.POINTER(C.c_uint64), C.POINTER(Err)]
     L.fstk_gpu_make_plan.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, DP,
@@ -226,3 +227,16 @@ def fp64_peak(device: int = 0):
     err = Err()
     check(lib().fstk_gpu_fp64_peak(device, C.byref(a), C.byref(b), C.byref(err)), err)
     return a.value, b.value
+
+
+DEVICE_LIST: list = []  # fstk_gpu_set_devices (empty: one device per model handle)
+
+
+def set_devices(ids) -> None:
+    """fstk_gpu_set_devices: models created afterwards through Model.handle()
+    replicate on these devices and a host evaluate_batch splits across them."""
+    ids = [int(i) for i in ids]
+    arr = (C.c_int32 * max(len(ids), 1))(*ids)
+    err = Err()
+    check(lib().fstk_gpu_set_devices(len(ids), arr, C.byref(err)), err)
+    DEVICE_LIST[:] = ids

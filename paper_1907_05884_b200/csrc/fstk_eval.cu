@@ -20,6 +20,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "fstk_internal.h"
@@ -1425,8 +1426,61 @@ int32_t fstk_gpu_device_count(void) {
 
 uint64_t fstk_gpu_launch_count(void) { return g_launches.load(); }
 
+namespace fstk_gpu {
+static void rethrow_stage_code(int32_t c, const fstk_gpu_error* err) {
+  if (!c) return;
+  Error e{c, err ? err->message : "stage failed"};
+  throw e;
+}
+static std::mutex g_dev_mu;
+static std::vector<int> g_devices;  // fstk_gpu_set_devices; empty = the current device
+}  // namespace fstk_gpu
+
+int32_t fstk_gpu_set_devices(int32_t n, const int32_t* ids, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    require(n >= 0 && (n == 0 || ids), FSTK_E_PARAMETER, "set_devices: bad device list");
+    int count = 0;
+    FSTK_CUDA(cudaGetDeviceCount(&count));
+    std::vector<int> v;
+    for (int i = 0; i < n; ++i) {
+      require(ids[i] >= 0 && ids[i] < count, FSTK_E_PARAMETER, "set_devices: no such device");
+      v.push_back(ids[i]);
+    }
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    g_devices = v;
+  });
+}
+
 int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_gpu_model** out,
                               fstk_gpu_error* err) {
+  if (device < 0) {
+    // The device list of fstk_gpu_set_devices: the model on the first device,
+    // replicas on the others (a host evaluate_batch then splits across all).
+    std::vector<int> ids;
+    {
+      std::lock_guard<std::mutex> lk(fstk_gpu::g_dev_mu);
+      ids = fstk_gpu::g_devices;
+    }
+    if (ids.empty()) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      ids.push_back(cur);
+    }
+    const int32_t rc = fstk_gpu_model_create(desc, ids[0], out, err);
+    if (rc) return rc;
+    for (size_t i = 1; i < ids.size(); ++i) {
+      fstk_gpu_model* r = nullptr;
+      const int32_t rc2 = fstk_gpu_model_create(desc, ids[i], &r, err);
+      if (rc2) {
+        fstk_gpu_model_destroy(*out);
+        *out = nullptr;
+        return rc2;
+      }
+      (*out)->replicas.push_back(r);
+    }
+    return 0;
+  }
   return guarded(err, [&] {
     require(desc != nullptr && out != nullptr, FSTK_E_PARAMETER, "null argument");
     *out = nullptr;
@@ -1648,6 +1702,8 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
 
 void fstk_gpu_model_destroy(fstk_gpu_model* model) {
   if (!model) return;
+  for (auto* r : model->replicas) fstk_gpu_model_destroy(r);
+  model->replicas.clear();
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(model->device);
@@ -1659,6 +1715,7 @@ void fstk_gpu_model_destroy(fstk_gpu_model* model) {
 int32_t fstk_gpu_model_set_core(fstk_gpu_model* m, const double* core, fstk_gpu_error* err) {
   return guarded(err, [&] {
     require(m && core, FSTK_E_PARAMETER, "null argument");
+    for (auto* r : m->replicas) rethrow_stage_code(fstk_gpu_model_set_core(r, core, err), err);
     std::lock_guard<std::mutex> lk(m->mu);
     DeviceGuard dg(m->device);
     FSTK_CUDA(cudaDeviceSynchronize());
@@ -1700,6 +1757,54 @@ int32_t fstk_gpu_evaluate_batch_device(const fstk_gpu_model* m, const double* po
 // chunk i+1 and the D2H copy of chunk i-1 overlap the kernels of chunk i.
 // Each chunk records its lowest failing row in its own device slot; one
 // read-back at the end reports the globally lowest (deterministic) Domain error.
+namespace fstk_gpu {
+// Rows [r0, r0 + q) of a column-major points buffer with leading dimension
+// ldp, on this model's device (chunked, two streams).  A Domain error reports
+// the global row index.
+static void eval_host_slab(const fstk_gpu_model* m, const double* points, int64_t ldp,
+                           int64_t r0, int64_t q, int d, double* out) {
+  if (q == 0) return;
+  std::lock_guard<std::mutex> lk(m->mu);
+  DeviceGuard dg(m->device);
+  const int64_t CH = m->chunk_points;
+  const int64_t ldt = round_up(CH, 128);
+  int64_t toff[kMaxOrder], tot = 0;
+  eval_table_offsets(m, ldt, toff, &tot);
+  const int64_t nchunks = ceil_div(q, CH);
+  m->chunk_err.ensure(static_cast<size_t>(nchunks));
+  FSTK_CUDA(cudaMemsetAsync(m->chunk_err.p, 0xff, nchunks * sizeof(unsigned long long),
+                            m->chunk[0].stream));
+  FSTK_CUDA(cudaEventRecord(m->chunk[0].done, m->chunk[0].stream));
+  FSTK_CUDA(cudaStreamWaitEvent(m->chunk[1].stream, m->chunk[0].done, 0));
+  for (int64_t c = 0; c < nchunks; ++c) {
+    Chunk& ck = m->chunk[c & 1];
+    const int64_t b = c * CH;
+    const int64_t nb = std::min(CH, q - b);
+    for (int k = 0; k < d; ++k)
+      FSTK_CUDA(cudaMemcpyAsync(ck.points.p + k * CH, points + k * ldp + r0 + b,
+                                nb * sizeof(double), cudaMemcpyHostToDevice, ck.stream));
+    launch_mode_tables(m, ck.points.p, CH, nb, round_up(nb, 128), nullptr, ck.tables.p, toff,
+                       ldt, false, m->chunk_err.p + c, ck.stream);
+    launch_contract(m, ck.tables.p, toff, ldt, nb, ck.out.p, ck.stream, nullptr, nullptr);
+    FSTK_CUDA(cudaMemcpyAsync(out + r0 + b, ck.out.p, nb * sizeof(double),
+                              cudaMemcpyDeviceToHost, ck.stream));
+  }
+  FSTK_CUDA(cudaStreamSynchronize(m->chunk[1].stream));
+  std::vector<unsigned long long> bad(static_cast<size_t>(nchunks));
+  FSTK_CUDA(cudaMemcpyAsync(bad.data(), m->chunk_err.p, nchunks * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, m->chunk[0].stream));
+  FSTK_CUDA(cudaStreamSynchronize(m->chunk[0].stream));
+  for (int64_t c = 0; c < nchunks; ++c) {
+    if (bad[c] != ULLONG_MAX) {
+      const int64_t row = r0 + c * CH + static_cast<int64_t>(bad[c]);
+      std::vector<double> y(d);
+      for (int k = 0; k < d; ++k) y[k] = points[k * ldp + row];
+      throw_domain(m, row, y.data());
+    }
+  }
+}
+}  // namespace fstk_gpu
+
 int32_t fstk_gpu_evaluate_batch(const fstk_gpu_model* m, const double* points, int64_t q,
                                 int32_t d, double* out, fstk_gpu_error* err) {
   return guarded(err, [&] {
@@ -1708,44 +1813,40 @@ int32_t fstk_gpu_evaluate_batch(const fstk_gpu_model* m, const double* points, i
     require(q >= 0, FSTK_E_PARAMETER, "negative point count");
     if (q == 0) return;
     require(points && out, FSTK_E_PARAMETER, "null buffer");
-    std::lock_guard<std::mutex> lk(m->mu);
-    DeviceGuard dg(m->device);
-    const int64_t CH = m->chunk_points;
-    const int64_t ldt = round_up(CH, 128);
-    int64_t toff[kMaxOrder], tot = 0;
-    eval_table_offsets(m, ldt, toff, &tot);
-    const int64_t nchunks = ceil_div(q, CH);
-    m->chunk_err.ensure(static_cast<size_t>(nchunks));
-    FSTK_CUDA(cudaMemsetAsync(m->chunk_err.p, 0xff, nchunks * sizeof(unsigned long long),
-                              m->chunk[0].stream));
-    FSTK_CUDA(cudaEventRecord(m->chunk[0].done, m->chunk[0].stream));
-    FSTK_CUDA(cudaStreamWaitEvent(m->chunk[1].stream, m->chunk[0].done, 0));
-    for (int64_t c = 0; c < nchunks; ++c) {
-      Chunk& ck = m->chunk[c & 1];
-      const int64_t b = c * CH;
-      const int64_t nb = std::min(CH, q - b);
-      for (int k = 0; k < d; ++k)
-        FSTK_CUDA(cudaMemcpyAsync(ck.points.p + k * CH, points + k * q + b, nb * sizeof(double),
-                                  cudaMemcpyHostToDevice, ck.stream));
-      launch_mode_tables(m, ck.points.p, CH, nb, round_up(nb, 128), nullptr, ck.tables.p, toff,
-                         ldt, false, m->chunk_err.p + c, ck.stream);
-      launch_contract(m, ck.tables.p, toff, ldt, nb, ck.out.p, ck.stream, nullptr, nullptr);
-      FSTK_CUDA(cudaMemcpyAsync(out + b, ck.out.p, nb * sizeof(double), cudaMemcpyDeviceToHost,
-                                ck.stream));
+    if (m->replicas.empty()) {
+      eval_host_slab(m, points, q, 0, q, d, out);
+      return;
     }
-    FSTK_CUDA(cudaStreamSynchronize(m->chunk[1].stream));
-    std::vector<unsigned long long> bad(static_cast<size_t>(nchunks));
-    FSTK_CUDA(cudaMemcpyAsync(bad.data(), m->chunk_err.p, nchunks * sizeof(unsigned long long),
-                              cudaMemcpyDeviceToHost, m->chunk[0].stream));
-    FSTK_CUDA(cudaStreamSynchronize(m->chunk[0].stream));
-    for (int64_t c = 0; c < nchunks; ++c) {
-      if (bad[c] != ULLONG_MAX) {
-        const int64_t row = c * CH + static_cast<int64_t>(bad[c]);
-        std::vector<double> y(d);
-        for (int k = 0; k < d; ++k) y[k] = points[k * q + row];
-        throw_domain(m, row, y.data());
-      }
+    // One host thread per device: contiguous slabs, concurrently.  Errors
+    // are the reference's: the Domain error with the lowest point index wins.
+    std::vector<const fstk_gpu_model*> dev{m};
+    for (const auto* r : m->replicas) dev.push_back(r);
+    const int64_t G = static_cast<int64_t>(dev.size());
+    std::vector<Error> errs(dev.size());
+    std::vector<char> failed(dev.size(), 0);
+    std::vector<std::thread> th;
+    for (int64_t g = 0; g < G; ++g) {
+      th.emplace_back([&, g] {
+        try {
+          eval_host_slab(dev[g], points, q, q * g / G, q * (g + 1) / G - q * g / G, d, out);
+        } catch (const Error& e) {
+          errs[g] = e;
+          failed[g] = 1;
+        } catch (const std::exception& e) {
+          errs[g] = Error{FSTK_E_COMPUTE, e.what()};
+          failed[g] = 1;
+        }
+      });
     }
+    for (auto& t : th) t.join();
+    int first = -1;
+    for (int64_t g = 0; g < G; ++g) {
+      if (!failed[g]) continue;
+      if (first < 0) first = static_cast<int>(g);
+      const bool dom = errs[g].code == FSTK_E_DOMAIN, fdom = errs[first].code == FSTK_E_DOMAIN;
+      if (dom && (!fdom || errs[g].index < errs[first].index)) first = static_cast<int>(g);
+    }
+    if (first >= 0) throw errs[first];
   });
 }
 

@@ -103,6 +103,9 @@ struct Chunk {
 
 struct fstk_gpu_model {
   int device = 0;
+  // fstk_gpu_set_devices: replicas on the other listed devices; a host
+  // evaluate_batch splits its points across this model and the replicas.
+  std::vector<fstk_gpu_model*> replicas;
   int d = 0;
   std::vector<int64_t> ranks;
   int64_t R = 0;

@@ -202,9 +202,11 @@ class Model:
 
     # -- device handle ---------------------------------------------------------
     def handle(self, device: int | None = None):
-        """The fstk_gpu_model* for `device` (default: current torch/CUDA device 0)."""
+        """The fstk_gpu_model* for `device` (default: current torch/CUDA device
+        0, or -- after set_devices(ids) -- a model replicated on those devices,
+        whose host evaluate_batch splits the points across them)."""
         if device is None:
-            device = _current_device()
+            device = -1 if _lib.DEVICE_LIST else _current_device()
         with self._lock:
             h = self._handles.get(device)
             if h is None:

@@ -255,3 +255,28 @@ def test_refit_d2_and_d4_parity(O):
         new, _ = F.reestimate_core(m, pts, vals, seed=5)
         core_o, _ = O.reestimate_core(m, pts, vals, seed=5)
         assert rel(new.core.reshape(-1, order="F"), core_o) <= 1e-9
+
+
+def test_set_devices_splits_host_evaluation():
+    # Two replicas on the one GPU of this box exercise the multi-device path:
+    # slabs evaluated concurrently give the single-device bits, and a domain
+    # error reports the lowest offending index across slabs.
+    m = synth.random_model((10, 8, 6), (16, 16, 16), 6, seed=80)
+    pts = synth.uniform_points(500_001, 3, seed=81)
+    one = m.evaluate_batch(pts)
+    try:
+        F.set_devices([0, 0, 0])
+        m2 = synth.random_model((10, 8, 6), (16, 16, 16), 6, seed=80)
+        assert np.array_equal(m2.evaluate_batch(pts), one)
+        bad = pts.copy(order="F")
+        bad[400_000, 1] = 2.0   # in the last slab
+        bad[200_000, 2] = -3.0  # in the middle slab: the lower index wins
+        with pytest.raises(F.FstkValueError) as ei:
+            m2.evaluate_batch(bad)
+        assert ei.value.index == 200_000 and ei.value.mode == 2
+        m3 = m2.with_core(m2.core * 2.0)
+        assert np.allclose(m3.evaluate_batch(pts[:1000]), 2.0 * one[:1000], rtol=1e-14, atol=0)
+        with pytest.raises(F.FstkValueError):
+            F.set_devices([99])
+    finally:
+        F.set_devices([])
