@@ -1406,6 +1406,8 @@ fstk_gpu_model::~fstk_gpu_model() {
   for (auto& c : chunk) {
     if (c.stream) cudaStreamDestroy(c.stream);
     if (c.done) cudaEventDestroy(c.done);
+    if (c.host_done) cudaEventDestroy(c.host_done);
+    if (c.h_stage) cudaFreeHost(c.h_stage);
   }
   if (fork_ev) cudaEventDestroy(fork_ev);
 }
@@ -1684,6 +1686,7 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
     for (auto& ck : m->chunk) {
       FSTK_CUDA(cudaStreamCreateWithFlags(&ck.stream, cudaStreamNonBlocking));
       FSTK_CUDA(cudaEventCreateWithFlags(&ck.done, cudaEventDisableTiming));
+      FSTK_CUDA(cudaEventCreateWithFlags(&ck.host_done, cudaEventDisableTiming));
     }
     // Allocate and zero the padded table workspaces once (padding rows stay 0).
     for (auto& ck : m->chunk) {
@@ -1761,12 +1764,58 @@ namespace fstk_gpu {
 // Rows [r0, r0 + q) of a column-major points buffer with leading dimension
 // ldp, on this model's device (chunked, two streams).  A Domain error reports
 // the global row index.
+// dst <- src (bytes) on up to 8 host threads (pageable <-> pinned staging).
+static void host_copy(void* dst, const void* src, size_t bytes) {
+  const size_t per = size_t(4) << 20;
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const size_t nt = std::min<size_t>(hw, (bytes + per - 1) / per);
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (size_t t = 1; t < nt; ++t)
+    th.emplace_back([=] {
+      const size_t lo = bytes * t / nt, hi = bytes * (t + 1) / nt;
+      std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+    });
+  std::memcpy(dst, src, bytes / nt);
+  for (auto& x : th) x.join();
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess;
+  cudaGetLastError();
+  return ok && a.type != cudaMemoryTypeUnregistered;
+}
+
 static void eval_host_slab(const fstk_gpu_model* m, const double* points, int64_t ldp,
                            int64_t r0, int64_t q, int d, double* out) {
   if (q == 0) return;
   std::lock_guard<std::mutex> lk(m->mu);
   DeviceGuard dg(m->device);
   const int64_t CH = m->chunk_points;
+  // Pageable caller buffers (the reference's Eigen/numpy arrays): stage each
+  // chunk through a pinned double buffer, the host copies of chunk c+1 (and
+  // the results of c-1) overlapping the GPU work of chunk c.  Pinned buffers
+  // go straight to the DMA engines.
+  const bool stage = q >= (int64_t(1) << 16) && !(is_pinned(points) && is_pinned(out));
+  if (stage)
+    for (auto& ck : m->chunk)
+      if (!ck.h_stage)
+        FSTK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ck.h_stage),
+                                static_cast<size_t>(d + 1) * CH * sizeof(double),
+                                cudaHostAllocDefault));
+  int64_t pend[2] = {-1, -1};  // chunk whose outputs wait in each staging slot
+  auto drain = [&](int slot) {
+    if (pend[slot] < 0) return;
+    Chunk& ck = m->chunk[slot];
+    FSTK_CUDA(cudaEventSynchronize(ck.host_done));
+    const int64_t b = pend[slot] * CH, nb = std::min(CH, q - b);
+    host_copy(out + r0 + b, ck.h_stage + static_cast<int64_t>(d) * CH, nb * sizeof(double));
+    pend[slot] = -1;
+  };
   const int64_t ldt = round_up(CH, 128);
   int64_t toff[kMaxOrder], tot = 0;
   eval_table_offsets(m, ldt, toff, &tot);
@@ -1777,19 +1826,41 @@ static void eval_host_slab(const fstk_gpu_model* m, const double* points, int64_
   FSTK_CUDA(cudaEventRecord(m->chunk[0].done, m->chunk[0].stream));
   FSTK_CUDA(cudaStreamWaitEvent(m->chunk[1].stream, m->chunk[0].done, 0));
   for (int64_t c = 0; c < nchunks; ++c) {
-    Chunk& ck = m->chunk[c & 1];
+    const int slot = static_cast<int>(c & 1);
+    Chunk& ck = m->chunk[slot];
     const int64_t b = c * CH;
     const int64_t nb = std::min(CH, q - b);
-    for (int k = 0; k < d; ++k)
-      FSTK_CUDA(cudaMemcpyAsync(ck.points.p + k * CH, points + k * ldp + r0 + b,
-                                nb * sizeof(double), cudaMemcpyHostToDevice, ck.stream));
+    if (stage) {
+      drain(slot);  // chunk c-2 is done with this slot: its outputs go to the caller
+      for (int k = 0; k < d; ++k)
+        host_copy(ck.h_stage + static_cast<int64_t>(k) * CH, points + k * ldp + r0 + b,
+                  nb * sizeof(double));
+      FSTK_CUDA(cudaMemcpyAsync(ck.points.p, ck.h_stage, static_cast<size_t>(d) * CH * sizeof(double),
+                                cudaMemcpyHostToDevice, ck.stream));
+    } else {
+      for (int k = 0; k < d; ++k)
+        FSTK_CUDA(cudaMemcpyAsync(ck.points.p + k * CH, points + k * ldp + r0 + b,
+                                  nb * sizeof(double), cudaMemcpyHostToDevice, ck.stream));
+    }
     launch_mode_tables(m, ck.points.p, CH, nb, round_up(nb, 128), nullptr, ck.tables.p, toff,
                        ldt, false, m->chunk_err.p + c, ck.stream);
     launch_contract(m, ck.tables.p, toff, ldt, nb, ck.out.p, ck.stream, nullptr, nullptr);
-    FSTK_CUDA(cudaMemcpyAsync(out + r0 + b, ck.out.p, nb * sizeof(double),
-                              cudaMemcpyDeviceToHost, ck.stream));
+    if (stage) {
+      FSTK_CUDA(cudaMemcpyAsync(ck.h_stage + static_cast<int64_t>(d) * CH, ck.out.p,
+                                nb * sizeof(double), cudaMemcpyDeviceToHost, ck.stream));
+      FSTK_CUDA(cudaEventRecord(ck.host_done, ck.stream));
+      pend[slot] = c;
+    } else {
+      FSTK_CUDA(cudaMemcpyAsync(out + r0 + b, ck.out.p, nb * sizeof(double),
+                                cudaMemcpyDeviceToHost, ck.stream));
+    }
+  }
+  if (stage) {
+    drain(static_cast<int>((nchunks - 2) & 1));
+    drain(static_cast<int>((nchunks - 1) & 1));
   }
   FSTK_CUDA(cudaStreamSynchronize(m->chunk[1].stream));
+  FSTK_CUDA(cudaStreamSynchronize(m->chunk[0].stream));
   std::vector<unsigned long long> bad(static_cast<size_t>(nchunks));
   FSTK_CUDA(cudaMemcpyAsync(bad.data(), m->chunk_err.p, nchunks * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, m->chunk[0].stream));

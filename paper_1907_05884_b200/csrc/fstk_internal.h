@@ -97,6 +97,8 @@ struct Chunk {
   std::vector<unsigned long long> err_host;
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
+  cudaEvent_t host_done = nullptr;  // pageable staging: this slot's D2H landed
+  double* h_stage = nullptr;        // pageable staging: pinned d x CH points + CH outputs
 };
 
 }  // namespace fstk_gpu

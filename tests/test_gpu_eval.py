@@ -280,3 +280,25 @@ def test_set_devices_splits_host_evaluation():
             F.set_devices([99])
     finally:
         F.set_devices([])
+
+
+def test_pageable_staging_matches_pinned_and_reports_domain_index():
+    # Host buffers that are not pinned are staged through the library's pinned
+    # double buffer (several chunks here): bit-identical to the pinned path,
+    # and a domain error in the third chunk keeps its global index.
+    import torch
+
+    m = synth.random_model((8, 6, 5), (12, 12, 12), 5, seed=90)
+    n = 5_000_000
+    pts = synth.uniform_points(n, 3, seed=91)
+    got = m.evaluate_batch(pts)
+    pin = torch.empty((3, n), dtype=torch.float64).pin_memory()
+    pin.numpy()[:] = pts.T
+    po = torch.empty(n, dtype=torch.float64).pin_memory()
+    m.evaluate_batch_into(pin.numpy().T, po.numpy())
+    assert np.array_equal(got, po.numpy())
+    bad = pts.copy(order="F")
+    bad[4_500_001, 0] = -0.5
+    with pytest.raises(F.FstkValueError) as ei:
+        m.evaluate_batch(bad)
+    assert ei.value.index == 4_500_001 and ei.value.mode == 0
