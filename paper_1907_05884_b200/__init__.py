@@ -10,8 +10,8 @@ in libfstk_gpu.so on the GPU; there is no CPU fallback.
 from ._lib import FstkError, FstkIOError, FstkValueError, launch_count, set_devices
 from .cloud import (PointCloud, read_cloud, read_cloud_binary, read_cloud_csv, read_cloud_device,
                     read_points_csv, write_cloud_binary, write_cloud_csv)
-from .model import (BasisSpec, Model, ModelMetadata, ModeFunction, evaluate_fields, load_model,
-                    save_model)
+from .model import (BasisSpec, Model, ModelMetadata, ModeFunction, eval_basis, evaluate_fields,
+                    load_model, save_model)
 from .refit import (RefitSession, build_design_rows, gram, gram_slices, leverage_scores, mixed_matrix,
                     reestimate_core, self_convergence, sketch, sketch_config)
 
@@ -24,7 +24,7 @@ def set_max_threads(n: int) -> None:
 
 __all__ = [
     "BasisSpec", "Model", "ModelMetadata", "ModeFunction", "load_model", "save_model",
-    "evaluate_fields",
+    "evaluate_fields", "eval_basis",
     "reestimate_core", "RefitSession", "build_design_rows", "sketch", "mixed_matrix",
     "sketch_config", "self_convergence", "leverage_scores", "gram_slices", "gram", "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
     "launch_count", "set_devices", "PointCloud", "read_cloud", "read_cloud_binary", "read_cloud_csv",

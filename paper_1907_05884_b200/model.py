@@ -438,6 +438,26 @@ def _header_json(model: Model) -> str:
                       allow_nan=True)
 
 
+_BASIS_MODELS: dict = {}
+
+
+def eval_basis(spec: "BasisSpec", x):
+    """fstk.eval_basis (basis.cpp:226-234, module.cpp:152-156): the
+    spec.dimension() basis values at x (scalar -> vector, array -> (n, dim)).
+    Runs on the GPU through the C-ABI: a cached one-mode model whose function
+    j is basis element j with coefficient 1.0, read out with mode_values
+    (bit-exact: 0 + 1.0 * phi_j = phi_j).  Domain errors as the reference."""
+    key = (spec.family, spec.degree, spec.resolution, spec.lo, spec.hi)
+    m = _BASIS_MODELS.get(key)
+    if m is None:
+        spec.validate()
+        n = spec.dimension()
+        fns = [ModeFunction(spec, [(j, 1.0)]) for j in range(n)]
+        m = Model(np.ones(n), [fns], ModelMetadata(grid_sizes=[0]))
+        _BASIS_MODELS[key] = m
+    return m.mode_values(0, x)
+
+
 def evaluate_fields(models, points, device=None) -> np.ndarray:
     """Several models at one shared point set (BASELINE C5's visualisation
     stream): the points travel to the GPU once and every field is evaluated

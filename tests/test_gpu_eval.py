@@ -302,3 +302,20 @@ def test_pageable_staging_matches_pinned_and_reports_domain_index():
     with pytest.raises(F.FstkValueError) as ei:
         m.evaluate_batch(bad)
     assert ei.value.index == 4_500_001 and ei.value.mode == 0
+
+
+@pytest.mark.parametrize("fam,p,res", [(0, 0, 0), (0, 7, 0), (0, 48, 0), (0, 64, 0), (1, 2, 1),
+                                       (1, 3, 3), (1, 0, 4)])
+def test_eval_basis_bitexact(O, fam, p, res):
+    # fstk.eval_basis (module.cpp:152-156) on the GPU, bit-exact against the
+    # oracle restatement of basis.cpp:226-234, scalar and vector x.
+    spec = BasisSpec.legendre(p, 0.0, 2.0) if fam == 0 else BasisSpec.wavelet(res, p, 0.0, 2.0)
+    xs = np.concatenate([[0.0, 2.0, 1.0, 1e-13, 2.0 - 1e-13],
+                         np.random.default_rng(p + res).uniform(0, 2, 50)])
+    got = F.eval_basis(spec, xs)
+    for i, x in enumerate(xs):
+        want = O.eval_basis(p, 0.0, 2.0, x, family=fam, resolution=res)
+        assert np.array_equal(got[i], want)
+    assert np.array_equal(F.eval_basis(spec, 0.5), got[0] * 0 + F.eval_basis(spec, np.array([0.5]))[0])
+    with pytest.raises(F.FstkValueError):
+        F.eval_basis(spec, 2.5)
