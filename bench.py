@@ -451,6 +451,33 @@ def main():
     return 0
 
 
+def sketch_roofline(model, info, t, transform, world):
+    """The sketch (design columns -> DCT/WHT/FFT -> sampled rows) against HBM:
+    algorithmic bytes = the mode tables read once + per column the complex
+    (real for WHT) q_pad intermediate written and read once between the two
+    passes + the S sampled rows written, over this rank's (R+1)/world columns.
+    Peak: MEASURED_PEAKS.json hbm_gbs (the driver's copy bandwidth)."""
+    if not t or transform == "none":
+        return None
+    R = int(np.prod(model.ranks))
+    q_pad, S = info["padded_rows"], info["sample_rows"]
+    elem = 8 if transform == "wht" else 16
+    cols = (R + 1) / max(world, 1)
+    tables = 8.0 * q_pad * sum(model.ranks)
+    per_col = 2.0 * elem * q_pad + 8.0 * S * (2 if transform == "fft" else 1)
+    algo = tables + cols * per_col
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak, src = float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        peak, src = 7700.0, "B200_PROFILING.md nominal (MEASURED_PEAKS.json absent)"
+    ach = algo / t / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "algorithmic_bytes": algo, "peak_source": src,
+            "kernel": "transform_pass2_kernel (pass 1: design columns + 10 stages; pass 2: 10 "
+                      "stages + post-rotation + sampled rows)"}
+
+
 def gram_roofline(gram_flops, info, t, peak_fp64):
     """Gram stage against its roofline.  Native: fp64 SYRK flops vs the DMMA
     peak.  Sliced (fstk_gram.cu): int8 ops issued vs the B200 dense int8
@@ -559,6 +586,7 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=No
             "host_wall_s": info.get("wall_s"),
             "gram_slices": info["gram_slices"], "refine_steps": info["refine_steps"],
             "gram_roofline": gram_roofline(gram_flops, info, tm["gram_s"], peak),
+            "sketch_roofline": sketch_roofline(model, info, tm["sketch_s"], tform, world),
             "residual_before": info["residual_before"], "residual_after": info["residual_after"],
             "rank_deficient": info["rank_deficient"],
             "note": "solve (cuSOLVER Cholesky) is outside the hot-path claim (north_star)"}
