@@ -118,3 +118,41 @@ def test_none_transform_columns_layout_is_row_local(O):
     assert np.array_equal(a1, a2) and np.array_equal(b1, b2)
     s.close()
     r.close()
+
+
+@pytest.mark.parametrize("t", ["dct", "fft"])
+def test_column_layout_with_thin_shards(O, t):
+    # R + 1 = 7 columns and S = 8 sample rows over 5 shards: shards own one or
+    # two columns and one or two rows; the exchange still lands bit-exactly.
+    m = synth.random_model((3, 2, 1), [4, 4, 4], 3, seed=11)
+    pts, vals = _data(O, m, 5_000, 12)
+    G = 5
+    cols = [F.RefitSession(m, pts, vals, seed=4, transform=t, sample_rows=8, shard=g, shards=G,
+                           layout="columns") for g in range(G)]
+    _exchange_in_process(cols)
+    for g in range(G):
+        r = F.RefitSession(m, pts, vals, seed=4, transform=t, sample_rows=8, shard=g, shards=G)
+        ac, bc = cols[g].sketched()
+        ar, br = r.sketched()
+        assert np.array_equal(ac, ar) and np.array_equal(bc, br)
+        r.close()
+    for s in cols:
+        s.close()
+
+
+def test_column_layout_more_shards_than_columns(O):
+    # 9 shards for R + 1 = 7 columns: two shards transform nothing.
+    m = synth.random_model((3, 2, 1), [4, 4, 4], 3, seed=13)
+    pts, vals = _data(O, m, 5_000, 14)
+    G = 9
+    cols = [F.RefitSession(m, pts, vals, seed=4, sample_rows=18, shard=g, shards=G,
+                           layout="columns") for g in range(G)]
+    _exchange_in_process(cols)
+    for g in range(G):
+        r = F.RefitSession(m, pts, vals, seed=4, sample_rows=18, shard=g, shards=G)
+        ac, bc = cols[g].sketched()
+        ar, br = r.sketched()
+        assert np.array_equal(ac, ar) and np.array_equal(bc, br)
+        r.close()
+    for s in cols:
+        s.close()
