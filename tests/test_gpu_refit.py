@@ -303,3 +303,20 @@ def test_none_transform_recovers_planted_core(O):
     with pytest.raises(ValueError):   # S > Q_w
         F.reestimate_core(m, pts[:100], O.evaluate_batch(m, pts[:100]), sample_rows=99,
                           transform="none")
+
+
+@pytest.mark.parametrize("t", ["dct", "fft", "wht"])
+def test_three_pass_sketch_bitexact(O, t):
+    # working_subset above 2^20 makes q_pad = 2^21: the sketch takes three
+    # transform passes (a middle pass reads and writes the intermediate).
+    m = synth.random_model((3, 2, 2), [5, 5, 5], 3, seed=31)
+    q = (1 << 21) + 50_000  # q_w = q - 100,000 validation rows < 2^21
+    pts, vals = _data(O, m, q, 32)
+    sess = F.RefitSession(m, pts, vals, seed=6, transform=t, working_subset=0, sample_rows=64)
+    assert sess.info_dict()["padded_rows"] == 1 << 21
+    a, b = sess.sketched()
+    ao, bo, rows_o, _, _ = O.refit_system(m, pts, vals, seed=6, transform=t, working_subset=0,
+                                          sample_rows=64)
+    assert np.array_equal(sess.rows(), rows_o)
+    assert np.array_equal(a, ao) and np.array_equal(b, bo)
+    sess.close()
