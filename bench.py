@@ -408,9 +408,21 @@ def main():
         model.evaluate_batch_into(hp_np, hout.numpy())
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = maxreduce(float(np.median(e2e_times)), world, dev)
+    # Same call with plain (pageable) numpy buffers, as a reference caller
+    # passes them: the library stages them through pinned memory.
+    pg_times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        model.evaluate_batch(pts)
+        pg_times.append(time.perf_counter() - t0)
+    pg_s = maxreduce(float(np.median(pg_times)), world, dev)
     e2e = {"value": world * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(n * d * 8),
            "d2h_bytes_per_step": int(n * 8), "ms_per_step": e2e_s * 1e3,
-           "path": "fstk_gpu_evaluate_batch (host C-ABI), pinned host buffers"}
+           "path": "fstk_gpu_evaluate_batch (host C-ABI), pinned host buffers",
+           "pageable": {"value": world * n / pg_s, "ms_per_step": pg_s * 1e3,
+                        "path": "the same call with pageable numpy buffers (staged by the "
+                                "library through pinned memory)"}}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
