@@ -260,6 +260,7 @@ struct PassParams {
   int stg_off;              // byte offset of the staging buffer in shared memory
   int compact;              // last pass: destination rows consecutive per CTA
   int list_off;             // byte offset of the per-CTA sampled-element list
+  int ct_rounds;            // L == 10: compile-time stage rounds (radix_round_ct)
   // Column-sharded sketch (fstk_gpu_refit_begin_columns): the last pass
   // writes sample row sl of column col straight into the all-to-all send
   // buffer A, packed per destination rank h (the owner of sl):
@@ -390,6 +391,62 @@ __device__ __forceinline__ void radix_round(typename std::conditional<REAL, doub
   }
 }
 
+// radix_round with the stage index J and the element count NEL known at
+// compile time (the L = 10 passes of every q_pad >= 2^10): the NV shared
+// addresses and the twiddle addresses of a block become one base plus
+// immediate offsets, instead of an IMAD chain per access.  Same butterflies
+// in the same order, so bit-identical to radix_round.
+//   spad(e0 + m jstep) - spad(e0) == spad(m jstep) here: jstep is a multiple
+//   of 8, or (J = 0) e0 mod 8 < G = jstep with m jstep < 8 G.
+template <bool REAL, int NS, int G, int J, int NEL>
+__device__ __forceinline__ void radix_round_ct(typename std::conditional<REAL, double, double2>::type* x,
+                                               const double2* tws) {
+  using T = typename std::conditional<REAL, double, double2>::type;
+  constexpr int NV = 1 << NS;
+  constexpr int jstep = (1 << J) * G;
+  constexpr int jmask = (1 << J) - 1;
+  static_assert(jstep % 8 == 0 || J == 0, "offset identity needs jstep % 8 == 0 or J == 0");
+  for (int blk = threadIdx.x; blk < (NEL >> NS); blk += blockDim.x) {
+    const int c = blk % G, q = blk / G;
+    const int tb = ((q >> J) << (J + NS)) | (q & jmask);
+    const int e0 = tb * G + c;
+    T* xb = x + spad(e0);
+    T v[NV];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) v[m] = xb[spad(m * jstep)];
+    if constexpr (REAL) {
+#pragma unroll
+      for (int jj = 0; jj < NS; ++jj) {
+        const int half = 1 << jj;
+#pragma unroll
+        for (int a = 0; a < NV; ++a) {
+          if (a & half) continue;
+          const double u = v[a], w2 = v[a + half];
+          v[a] = xadd(u, w2);
+          v[a + half] = xsub(u, w2);
+        }
+      }
+    } else {
+      const double2* twb = tws + (tb & jmask) * G + c;
+#pragma unroll
+      for (int jj = 0; jj < NS; ++jj) {
+        const int half = 1 << jj;
+#pragma unroll
+        for (int a = 0; a < NV; ++a) {
+          if (a & half) continue;
+          const double2 w = twb[((1 << (J + jj)) - 1) * G + (a & (half - 1)) * jstep];
+          const double2 u = v[a];
+          const double2 t2 = cmul_x(v[a + half], w);
+          v[a] = make_double2(xadd(u.x, t2.x), xadd(u.y, t2.y));
+          v[a + half] = make_double2(xsub(u.x, t2.x), xsub(u.y, t2.y));
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < NV; ++m) xb[spad(m * jstep)] = v[m];
+  }
+}
+
 template <bool REAL, int G, int DT>  // DT: mode count when known at compile time (0 = runtime)
 __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(const PassParams P, int ncols_batch) {
   using T = typename std::conditional<REAL, double, double2>::type;
@@ -436,11 +493,14 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
       }
     } else if constexpr (DT > 0) {
       // G == 1, stride 1: the CTA's positions are base .. base + nel - 1.
-      int64_t rem = P.col0 + cc;
+      // Mixed-radix digits in 32-bit arithmetic (columns < 2^31): a 64-bit
+      // division per digit per column per thread was the pass's top cost.
+      uint32_t rem = static_cast<uint32_t>(P.col0 + cc);
 #pragma unroll
       for (int k = 0; k < DT; ++k) {
-        const int64_t jk = rem % P.r[k];
-        rem /= P.r[k];
+        const uint32_t rk = static_cast<uint32_t>(P.r[k]);
+        const int64_t jk = rem % rk;
+        rem /= rk;
         const double* t = P.tables + P.toff.v[k] + jk * P.ldt + base;
         for (int ch = threadIdx.x; ch < nel / 2; ch += blockDim.x)
           cp_async16(stg + (static_cast<size_t>(k) * nel + 2 * ch) * 8, t + 2 * ch);
@@ -527,12 +587,13 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
       const double* tc[NTC];
       const bool design = col < P.R;
       if (design && P.src == SRC_TABLES) {
-        int64_t rem = col;
+        uint32_t rem = static_cast<uint32_t>(col);
 #pragma unroll
         for (int k = 0; k < NTC; ++k) {
           if (DT > 0 || k < P.d) {
-            const int64_t jk = rem % P.r[k];
-            rem /= P.r[k];
+            const uint32_t rk = static_cast<uint32_t>(P.r[k]);
+            const int64_t jk = rem % rk;
+            rem /= rk;
             tc[k] = P.tables + P.toff.v[k] + jk * P.ldt;
           }
         }
@@ -562,6 +623,17 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
     __syncthreads();
     prefetch(cc + gridDim.y);  // staging is free: this column now lives in x
     // ---- stages, three per register round
+    if (L == 10 && P.ct_rounds) {
+      constexpr int NE = 1024 * G;
+      radix_round_ct<REAL, 3, G, 0, NE>(x, tws);
+      __syncthreads();
+      radix_round_ct<REAL, 3, G, 3, NE>(x, tws);
+      __syncthreads();
+      radix_round_ct<REAL, 3, G, 6, NE>(x, tws);
+      __syncthreads();
+      radix_round_ct<REAL, 1, G, 9, NE>(x, tws);
+      __syncthreads();
+    } else
     for (int j = 0; j < L; j += 3) {
       const int ns = min(3, L - j);
       if (ns == 3)
@@ -618,6 +690,152 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
         *store_ptr(P, col, sl, true) = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
       }
     }
+  }
+}
+
+// ------------------------------------------- warp-level first pass (K3a) ---
+// Stages 0..9 of a q_pad >= 2^11 complex (DCT/FFT) sketch, one 1024-point
+// block of one design column per warp, held in registers: no CTA barrier.
+// Lane a first owns elements 32a + b (b = 0..31, register index) and runs
+// stages 0..4 (len 2..32) in registers; one warp-private shared-memory
+// exchange (33-element rows: conflict-free both ways) gives lane b' the
+// elements 32a + b' for stages 5..9 (len 64..1024); the block is stored as
+// 32 coalesced 512-byte rows.  The butterflies are transforms.cpp:36-46's,
+// each a separately rounded (ac - bd, ad + bc) product and sum, with two
+// value-preserving shortcuts: the k = 0 twiddle of every stage is the exact
+// (1, 0) the recurrence starts from, and a product by it returns its operand
+// (up to the sign of an exact zero), so it is skipped; stage 0's inputs are
+// real, so its imaginary sums (+0 +- +0 = +0) are written directly.
+// Stages 0..4 use twiddles 0..30, passed by value (constant-bank operands);
+// stages 5..9 read twiddles 31..1022 from one shared copy per CTA.  The
+// twiddles of these stages do not depend on q_pad.
+struct WarpPass1Params {
+  int64_t n;          // q_pad
+  int nblk;           // n / 1024
+  int ncols;          // columns in this batch
+  int64_t col0;       // first global column of the batch
+  int64_t R;          // columns < R: design; == R: rhs
+  const double* tables;
+  Int64x8 toff;
+  int64_t ldt;
+  int r[kMaxOrder];
+  const double* sgn;
+  const int64_t* row_src;
+  const double* rhs;
+  const double2* tw;  // replayed twiddles (global)
+  double2* cbuf;      // complex intermediate, n per batch column
+  double2 tw5[31];    // twiddles of stages 0..4
+};
+
+constexpr int kWp1Row = 33;                    // padded 32-element row
+constexpr int kWp1Buf = 32 * kWp1Row;          // double2 per warp
+constexpr int kWp1Tw = 992;                    // twiddles 31..1022
+
+template <int DT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPass1Params P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* tws = reinterpret_cast<double2*>(smem_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* X = tws + kWp1Tw + warp * kWp1Buf;
+  for (int i = threadIdx.x; i < kWp1Tw; i += blockDim.x) tws[i] = P.tw[31 + i];
+  __syncthreads();
+  const int64_t units = static_cast<int64_t>(P.ncols) * P.nblk;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * WARPS;
+  for (int64_t u = static_cast<int64_t>(blockIdx.x) * WARPS + warp; u < units; u += nw) {
+    const int cc = static_cast<int>(u / P.nblk);
+    const int64_t base = (u - static_cast<int64_t>(cc) * P.nblk) * 1024;
+    const int64_t col = P.col0 + cc;
+    // ---- inputs: design column x_p = ((s u0) u1) u2 ... (randls.cpp:44-52,
+    // sign folded into u0), coalesced pairs, into the warp's buffer.
+    __syncwarp();
+    if (col < P.R) {
+      const double* tc[DT];
+      uint32_t rem = static_cast<uint32_t>(col);
+#pragma unroll
+      for (int k = 0; k < DT; ++k) {
+        const uint32_t rk = static_cast<uint32_t>(P.r[k]);
+        tc[k] = P.tables + P.toff.v[k] + static_cast<int64_t>(rem % rk) * P.ldt + base;
+        rem /= rk;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 t[DT][8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int k = 0; k < DT; ++k)
+            t[k][j] = __ldg(reinterpret_cast<const double2*>(tc[k] + 64 * (8 * h + j) + 2 * lane));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          double v0 = t[0][j].x, v1 = t[0][j].y;
+#pragma unroll
+          for (int k = 1; k < DT; ++k) {
+            v0 = xmul(v0, t[k][j].x);
+            v1 = xmul(v1, t[k][j].y);
+          }
+          const int e = 64 * (8 * h + j) + 2 * lane;
+          X[e + (e >> 5)] = make_double2(v0, 0.0);
+          X[e + 1 + (e >> 5)] = make_double2(v1, 0.0);
+        }
+      }
+    } else {
+      for (int e = lane; e < 1024; e += 32) {
+        const int64_t p = base + e;
+        const int64_t src = P.row_src[p];
+        X[e + (e >> 5)] = make_double2(src < 0 ? 0.0 : xmul(P.sgn[p], P.rhs[src]), 0.0);
+      }
+    }
+    __syncwarp();
+    double2 v[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) v[b] = X[lane * kWp1Row + b];
+    // ---- stage 0 (len 2, twiddle (1, 0)): real inputs
+#pragma unroll
+    for (int b = 0; b < 32; b += 2) {
+      const double a0 = v[b].x, a1 = v[b + 1].x;
+      v[b] = make_double2(xadd(a0, a1), 0.0);
+      v[b + 1] = make_double2(xsub(a0, a1), 0.0);
+    }
+    // ---- stages 1..4 (len 4..32)
+#pragma unroll
+    for (int s = 1; s < 5; ++s) {
+      const int half = 1 << s;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        if (b & half) continue;
+        const int k = b & (half - 1);
+        const double2 uu = v[b];
+        const double2 t2 = k == 0 ? v[b + half] : cmul_x(v[b + half], P.tw5[half - 1 + k]);
+        v[b] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
+        v[b + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
+      }
+    }
+    // ---- exchange: lane b' gets elements 32 a + b'
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < 32; ++b) X[lane * kWp1Row + b] = v[b];
+    __syncwarp();
+#pragma unroll
+    for (int a = 0; a < 32; ++a) v[a] = X[a * kWp1Row + lane];
+    // ---- stages 5..9 (len 64..1024): k = b' + 32 (a mod 2^i)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const int half = 1 << i;  // in rows of 32
+#pragma unroll
+      for (int m = 0; m < half; ++m) {
+        const double2 w = tws[32 * half - 32 + lane + 32 * m];
+#pragma unroll
+        for (int a = m; a < 32; a += 2 * half) {
+          const double2 uu = v[a];
+          const double2 t2 = cmul_x(v[a + half], w);
+          v[a] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
+          v[a + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
+        }
+      }
+    }
+    double2* out = P.cbuf + static_cast<int64_t>(cc) * P.n + base + lane;
+#pragma unroll
+    for (int a = 0; a < 32; ++a) __stcg(out + 32 * a, v[a]);
   }
 }
 
@@ -769,7 +987,16 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
   const int LOG = ilog2(J.n);
   const bool real = J.kind == FSTK_TRANSFORM_WHT;
   auto tw = real ? nullptr : twiddles(device, J.n);
+  // Twiddles 0..30 (stages 0..4; independent of n) for warp_pass1_kernel.
+  double2 tw_host[31];
+  if (!real && J.n >= 32) {
+    std::vector<double2> h;
+    replay_twiddles(32, h);
+    for (int i = 0; i < 31; ++i) tw_host[i] = h[i];
+  }
   const int64_t ncols = J.R + (J.with_rhs ? 1 : 0);
+  // The pass kernels decompose column indices in 32-bit arithmetic.
+  require(ncols < (int64_t(1) << 31), FSTK_E_PARAMETER, "too many design columns");
   const size_t elem = real ? 8 : 16;
   const int npass = LOG == 0 ? 1 : (LOG + 9) / 10;
   // Column batches of ~FSTK_SKETCH_BATCH_MB (default 4 GB) of inter-pass
@@ -816,6 +1043,14 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
     attr(reinterpret_cast<const void*>(transform_pass2_kernel<true, 1, 4>));
     attr(reinterpret_cast<const void*>(transform_pass2_kernel<false, 2, 0>));
     attr(reinterpret_cast<const void*>(transform_pass2_kernel<true, 2, 0>));
+    auto attr_w = [](const void* f) {
+      FSTK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      FSTK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    };
+    attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<3, 8>));
+    attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<3, 12>));
+    attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<4, 8>));
+    attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<4, 12>));
   });
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -887,6 +1122,11 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       P.stg_off = static_cast<int>(smem);
       smem += stg;
       P.compact = (J.compact && P.last && E * P.G <= 65536) ? 1 : 0;
+      static const int ct_on = [] {
+        const char* e = std::getenv("FSTK_SKETCH_CT");
+        return (e && std::atoi(e) == 0) ? 0 : 1;
+      }();
+      P.ct_rounds = ct_on;
       smem = round_up(static_cast<int64_t>(smem), 16);
       P.list_off = static_cast<int>(smem);
       if (P.compact) smem += static_cast<size_t>(E * P.G) * sizeof(uint16_t);
@@ -902,6 +1142,52 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       ProfScope prof(FSTK_PROF_TRANSFORM, s);
       const int dt = (P.src == SRC_TABLES && (J.d == 3 || J.d == 4)) ? J.d : 0;
       const int nb = static_cast<int>(bc);
+      // Warp-level first pass (warp_pass1_kernel): complex transforms with
+      // a design-table source and a later pass (FSTK_SKETCH_WARP=0 disables;
+      // FSTK_SKETCH_WARP=12 runs 12 warps per CTA instead of 8).
+      static const int warp_mode = [] {
+        const char* e = std::getenv("FSTK_SKETCH_WARP");
+        return e ? std::atoi(e) : 8;
+      }();
+      if (warp_mode != 0 && !real && pass == 0 && !P.last && P.L == 10 && dt > 0) {
+        WarpPass1Params W{};
+        W.n = P.n;
+        W.nblk = static_cast<int>(J.n / 1024);
+        W.ncols = nb;
+        W.col0 = c0;
+        W.R = J.R;
+        W.tables = J.tables;
+        W.toff = P.toff;
+        W.ldt = J.ldt;
+        for (int k = 0; k < J.d; ++k) W.r[k] = J.r[k];
+        W.sgn = J.sgn;
+        W.row_src = J.row_src;
+        W.rhs = J.rhs;
+        W.tw = tw->p;
+        W.cbuf = cbuf.p;
+        for (int i = 0; i < 31; ++i) W.tw5[i] = tw_host[i];
+        const int wpc = warp_mode == 12 ? 12 : 8;
+        const size_t wsm = static_cast<size_t>(kWp1Tw + wpc * kWp1Buf) * sizeof(double2);
+        const unsigned wgrid = static_cast<unsigned>(std::min<int64_t>(
+            sms, ceil_div(static_cast<int64_t>(nb) * W.nblk, static_cast<int64_t>(wpc))));
+        if (dt == 3 && wpc == 8)
+          warp_pass1_kernel<3, 8><<<wgrid, 8 * 32, wsm, s>>>(W);
+        else if (dt == 3)
+          warp_pass1_kernel<3, 12><<<wgrid, 12 * 32, wsm, s>>>(W);
+        else if (wpc == 8)
+          warp_pass1_kernel<4, 8><<<wgrid, 8 * 32, wsm, s>>>(W);
+        else
+          warp_pass1_kernel<4, 12><<<wgrid, 12 * 32, wsm, s>>>(W);
+        check_launch("warp_pass1_kernel");
+        continue;
+      }
+      // G = 1 passes: a radix-2^3 round has E / 8 = 128 butterfly blocks, so
+      // FSTK_SKETCH_G1_THREADS=128 keeps every thread busy in the rounds.
+      static const int g1_threads = [] {
+        const char* e = std::getenv("FSTK_SKETCH_G1_THREADS");
+        return (e && std::atoi(e) == 128) ? 128 : 256;
+      }();
+      const int nt1 = g1_threads;
       if (P.G == 2) {
         if (real)
           transform_pass2_kernel<true, 2, 0><<<grid, 256, smem, s>>>(P, nb);
@@ -909,19 +1195,19 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
           transform_pass2_kernel<false, 2, 0><<<grid, 256, smem, s>>>(P, nb);
       } else if (dt == 3) {
         if (real)
-          transform_pass2_kernel<true, 1, 3><<<grid, 256, smem, s>>>(P, nb);
+          transform_pass2_kernel<true, 1, 3><<<grid, nt1, smem, s>>>(P, nb);
         else
-          transform_pass2_kernel<false, 1, 3><<<grid, 256, smem, s>>>(P, nb);
+          transform_pass2_kernel<false, 1, 3><<<grid, nt1, smem, s>>>(P, nb);
       } else if (dt == 4) {
         if (real)
-          transform_pass2_kernel<true, 1, 4><<<grid, 256, smem, s>>>(P, nb);
+          transform_pass2_kernel<true, 1, 4><<<grid, nt1, smem, s>>>(P, nb);
         else
-          transform_pass2_kernel<false, 1, 4><<<grid, 256, smem, s>>>(P, nb);
+          transform_pass2_kernel<false, 1, 4><<<grid, nt1, smem, s>>>(P, nb);
       } else {
         if (real)
-          transform_pass2_kernel<true, 1, 0><<<grid, 256, smem, s>>>(P, nb);
+          transform_pass2_kernel<true, 1, 0><<<grid, nt1, smem, s>>>(P, nb);
         else
-          transform_pass2_kernel<false, 1, 0><<<grid, 256, smem, s>>>(P, nb);
+          transform_pass2_kernel<false, 1, 0><<<grid, nt1, smem, s>>>(P, nb);
       }
       check_launch("transform_pass2_kernel");
     }
