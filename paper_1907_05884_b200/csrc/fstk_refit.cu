@@ -219,6 +219,40 @@ static std::shared_ptr<DevBuf<double2>> twiddles(int device, uint64_t n) {
   return buf;
 }
 
+// Twiddle rows of warp_pass2_kernel for n = 2^20: row lo holds, at local
+// index (2^J - 1) + t' (J = 0..9, t' < 2^J), the replayed twiddle of stage
+// 10 + J for k = lo + 1024 t', i.e. tw[(2^(10+J) - 1) + lo + 1024 t'].
+static std::map<TwiddleKey, std::shared_ptr<DevBuf<double2>>> g_tw2;
+static std::shared_ptr<DevBuf<double2>> warp_pass2_twiddles(int device, uint64_t n) {
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto it = g_tw2.find({device, n});
+  if (it != g_tw2.end()) return it->second;
+  std::vector<double2> h, rows(static_cast<size_t>(1024) * 1023);
+  replay_twiddles(n, h);
+  for (uint64_t lo = 0; lo < 1024; ++lo)
+    for (int J = 0; J < 10; ++J)
+      for (uint64_t t = 0; t < (uint64_t(1) << J); ++t)
+        rows[lo * 1023 + (uint64_t(1) << J) - 1 + t] = h[(uint64_t(1) << (10 + J)) - 1 + lo + 1024 * t];
+  auto buf = std::make_shared<DevBuf<double2>>(rows.size());
+  FSTK_CUDA(cudaMemcpy(buf->p, rows.data(), rows.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  g_tw2[{device, n}] = buf;
+  return buf;
+}
+
+// Whether the last pass of a sketch runs warp_pass2_kernel: complex
+// transforms with q_pad = 2^20 (two passes of 10 stages), when
+// FSTK_SKETCH_WARP2=1 (off by default: at C2 it measured 3.1-3.4 ms per 256
+// columns against 2.8 ms for transform_pass2_kernel -- every column re-reads
+// 16 MB of class twiddle rows, or, class-group major, over-fetches the
+// intermediate).  build_inputs orders destination rows to match.
+static bool warp_last_pass(int kind, uint64_t n) {
+  static const bool on = [] {
+    const char* e = std::getenv("FSTK_SKETCH_WARP2");
+    return e && std::atoi(e) == 1;
+  }();
+  return on && kind != FSTK_TRANSFORM_WHT && n == (uint64_t(1) << 20);
+}
+
 // ------------------------------------------------------ transform pass ---
 enum SrcKind { SRC_TABLES = 0, SRC_DENSE = 1, SRC_BUFFER = 2 };
 
@@ -261,6 +295,11 @@ struct PassParams {
   int compact;              // last pass: destination rows consecutive per CTA
   int list_off;             // byte offset of the per-CTA sampled-element list
   int ct_rounds;            // L == 10: compile-time stage rounds (radix_round_ct)
+  // warp_pass2_kernel (last pass of q_pad = 2^20): per-position-class twiddle
+  // rows and the sampled elements of each class in destination-row order.
+  const double2* tw2;       // 1024 rows of 1023 twiddles (warp_pass2_twiddles)
+  const int32_t* lo_start;  // class lo owns destination rows [lo_start[lo], lo_start[lo+1])
+  const uint16_t* t_list;   // per destination row: its element t (position t 1024 + lo)
   // Column-sharded sketch (fstk_gpu_refit_begin_columns): the last pass
   // writes sample row sl of column col straight into the all-to-all send
   // buffer A, packed per destination rank h (the owner of sl):
@@ -742,8 +781,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
   const int64_t units = static_cast<int64_t>(P.ncols) * P.nblk;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * WARPS;
   for (int64_t u = static_cast<int64_t>(blockIdx.x) * WARPS + warp; u < units; u += nw) {
-    const int cc = static_cast<int>(u / P.nblk);
-    const int64_t base = (u - static_cast<int64_t>(cc) * P.nblk) * 1024;
+    // Column fastest: concurrently running warps share the block's u1, u2
+    // segments across consecutive columns (mode-0 digit fastest).
+    const int64_t hb = u / P.ncols;
+    const int cc = static_cast<int>(u - hb * P.ncols);
+    const int64_t base = hb * 1024;
     const int64_t col = P.col0 + cc;
     // ---- inputs: design column x_p = ((s u0) u1) u2 ... (randls.cpp:44-52,
     // sign folded into u0), coalesced pairs, into the warp's buffer.
@@ -836,6 +878,109 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
     double2* out = P.cbuf + static_cast<int64_t>(cc) * P.n + base + lane;
 #pragma unroll
     for (int a = 0; a < 32; ++a) __stcg(out + 32 * a, v[a]);
+  }
+}
+
+// ------------------------------------------- warp-level last pass (K3b) ---
+// Stages 10..19 of a q_pad = 2^20 complex sketch.  A CTA of 4 warps owns 4
+// adjacent position classes lo0..lo0+3 (positions t 1024 + lo, t < 1024) of
+// one column, so every 64-byte run t 1024 + lo0 .. lo0+3 of the intermediate
+// is read whole.  Phase A: lane (a_sub, c) of warp w loads t = 32 a + b
+// (a = 8 w + a_sub, b = 0..31) of class lo0 + c -- coalesced 64-byte runs --
+// and runs stages 10..14 (len 2^11..2^15) in registers.  One CTA exchange
+// (per-class rows of 33, class stride 1058: conflict-free both ways) gives
+// warp w class lo0 + w with lane b' holding t = 32 a + b', a = 0..31, for
+// stages 15..19; twiddle rows are per class (warp_pass2_twiddles).  The
+// class's sampled elements (destination rows lo_start[lo] ..) are then
+// post-rotated (DCT) or split (FFT) and stored row-contiguously.  Same
+// butterflies and epilogue as transform_pass2_kernel, in the same order.
+constexpr int kWp2Cls = 4;                     // classes (warps) per CTA
+constexpr int kWp2Stride = 32 * kWp1Row + 2;   // double2 per class row block
+
+__global__ void __launch_bounds__(kWp2Cls * 32, 3) warp_pass2_kernel(const PassParams P, int ncols_batch) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* Xc = reinterpret_cast<double2*>(smem_raw);
+  double2* tA = Xc + kWp2Cls * kWp2Stride;  // [class][31]
+  const int c = lane & 3, a = 8 * warp + (lane >> 2);
+  const int64_t groups = static_cast<int64_t>(ncols_batch) * (1024 / kWp2Cls);
+  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+    // Class-group major, column fastest: CTAs running together share the
+    // twiddle rows of one or two class groups (L1/L2 hits); the other half
+    // of each 128-byte run is read by the next class group from L2.
+    const int64_t lg = g / ncols_batch;
+    const int cc = static_cast<int>(g - lg * ncols_batch);
+    const int lo0 = static_cast<int>(lg) * kWp2Cls;
+    const int64_t col = P.col0 + cc;
+    const double2* src = P.cbuf + static_cast<int64_t>(cc) * P.n + lo0 + c;
+    double2 v[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) v[b] = __ldcg(src + static_cast<int64_t>(32 * a + b) * 1024);
+    __syncthreads();  // previous group done with Xc and tA
+    for (int i = threadIdx.x; i < kWp2Cls * 31; i += blockDim.x)
+      tA[i] = P.tw2[static_cast<int64_t>(lo0 + i / 31) * 1023 + i % 31];
+    __syncthreads();
+    // ---- stages 10..14: k = lo + 1024 (b mod 2^j)
+    const double2* tc = tA + 31 * c;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int half = 1 << j;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        if (b & half) continue;
+        const double2 w = tc[half - 1 + (b & (half - 1))];
+        const double2 uu = v[b];
+        const double2 t2 = cmul_x(v[b + half], w);
+        v[b] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
+        v[b + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
+      }
+    }
+    // ---- exchange: warp w takes class lo0 + w, lane b' the elements 32 a + b'
+    double2* xo = Xc + c * kWp2Stride + a * kWp1Row;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) xo[b] = v[b];
+    __syncthreads();
+    double2* xw = Xc + warp * kWp2Stride;
+#pragma unroll
+    for (int aa = 0; aa < 32; ++aa) v[aa] = xw[aa * kWp1Row + lane];
+    // ---- stages 15..19: k = lo + 1024 (b' + 32 (a mod 2^i))
+    const int lo = lo0 + warp;
+    const double2* twr = P.tw2 + static_cast<int64_t>(lo) * 1023;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const int half = 1 << i;
+      const double2* twi = twr + (32 << i) - 1 + lane;
+#pragma unroll
+      for (int m = 0; m < half; ++m) {
+        const double2 w = __ldg(twi + 32 * m);
+#pragma unroll
+        for (int aa = m; aa < 32; aa += 2 * half) {
+          const double2 uu = v[aa];
+          const double2 t2 = cmul_x(v[aa + half], w);
+          v[aa] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
+          v[aa + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int aa = 0; aa < 32; ++aa) xw[aa * kWp1Row + lane] = v[aa];
+    __syncwarp();
+    // ---- sampled rows of this class (consecutive destination rows)
+    const int first = P.lo_start[lo], cnt = P.lo_start[lo + 1] - first;
+    for (int i = lane; i < cnt; i += 32) {
+      const int64_t sl = first + i;
+      if (sl < P.row_lo || sl >= P.row_hi) continue;
+      const int t = P.t_list[sl];
+      const double2 V = xw[(t >> 5) * kWp1Row + (t & 31)];
+      if (P.kind == FSTK_TRANSFORM_DCT) {
+        const double val = xsub(xmul(__ldg(P.post_re + sl), V.x), xmul(__ldg(P.post_im + sl), V.y));
+        *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(__ldg(P.post_c + sl), val));
+      } else {
+        *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
+        *store_ptr(P, col, sl, true) = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
+      }
+    }
   }
 }
 
@@ -967,6 +1112,8 @@ struct SketchJob {
   int64_t lda;
   double* b;
   bool compact = false;  // slot = last-pass visit order (build_inputs compact)
+  const int32_t* lo_start = nullptr;  // warp_last_pass order (build_inputs)
+  const uint16_t* t_list = nullptr;
   // Column range [col_lo, col_hi) of the R (+rhs) columns (col_hi < 0: all)
   // and the packed all-to-all layout (see PassParams::packed).
   int64_t col_lo = 0, col_hi = -1;
@@ -1051,6 +1198,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<3, 12>));
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<4, 8>));
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<4, 12>));
+    attr_w(reinterpret_cast<const void*>(warp_pass2_kernel));
   });
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1143,12 +1291,25 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       const int dt = (P.src == SRC_TABLES && (J.d == 3 || J.d == 4)) ? J.d : 0;
       const int nb = static_cast<int>(bc);
       // Warp-level first pass (warp_pass1_kernel): complex transforms with
-      // a design-table source and a later pass (FSTK_SKETCH_WARP=0 disables;
-      // FSTK_SKETCH_WARP=12 runs 12 warps per CTA instead of 8).
+      // a design-table source and a later pass, and warp_pass2_kernel for
+      // the last pass of q_pad = 2^20 (FSTK_SKETCH_WARP=0 disables both;
+      // FSTK_SKETCH_WARP=8 runs 8 warps per CTA instead of 12).
       static const int warp_mode = [] {
         const char* e = std::getenv("FSTK_SKETCH_WARP");
-        return e ? std::atoi(e) : 8;
+        return e ? std::atoi(e) : 12;
       }();
+      if (P.last && J.compact && J.lo_start && warp_last_pass(J.kind, J.n) && npass == 2) {
+        auto tw2 = warp_pass2_twiddles(device, J.n);
+        P.tw2 = tw2->p;
+        P.lo_start = J.lo_start;
+        P.t_list = J.t_list;
+        const size_t wsm = static_cast<size_t>(kWp2Cls * kWp2Stride + kWp2Cls * 31) * sizeof(double2);
+        const unsigned wgrid = static_cast<unsigned>(std::min<int64_t>(
+            int64_t(sms) * 3, static_cast<int64_t>(nb) * (1024 / kWp2Cls)));
+        warp_pass2_kernel<<<wgrid, kWp2Cls * 32, wsm, s>>>(P, nb);
+        check_launch("warp_pass2_kernel");
+        continue;
+      }
       if (warp_mode != 0 && !real && pass == 0 && !P.last && P.L == 10 && dt > 0) {
         WarpPass1Params W{};
         W.n = P.n;
@@ -1166,7 +1327,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
         W.tw = tw->p;
         W.cbuf = cbuf.p;
         for (int i = 0; i < 31; ++i) W.tw5[i] = tw_host[i];
-        const int wpc = warp_mode == 12 ? 12 : 8;
+        const int wpc = warp_mode == 8 ? 8 : 12;
         const size_t wsm = static_cast<size_t>(kWp1Tw + wpc * kWp1Buf) * sizeof(double2);
         const unsigned wgrid = static_cast<unsigned>(std::min<int64_t>(
             sms, ceil_div(static_cast<int64_t>(nb) * W.nblk, static_cast<int64_t>(wpc))));
@@ -1263,6 +1424,8 @@ struct SketchInputs {
   DevBuf<int64_t> row_src;
   DevBuf<int32_t> slot;
   DevBuf<double> post_re, post_im, post_c;
+  DevBuf<int32_t> lo_start;  // warp_last_pass order: 1025 class starts
+  DevBuf<uint16_t> t_list;   // warp_last_pass order: element t per destination row
   int64_t rows_total = 0;  // destination rows (S, or q_pad for mixed_matrix)
   std::vector<int64_t> dest_of_sample;  // sample s (plan order) -> destination row
 };
@@ -1311,7 +1474,9 @@ static void build_inputs(int kind, uint64_t n, uint64_t q_w, const std::vector<d
     const uint64_t stride = uint64_t(1) << s0;
     const uint64_t G = std::min<uint64_t>(static_cast<uint64_t>(pass_group(s0)), stride);
     const uint64_t lo_blocks = stride / G;
+    const bool wl = warp_last_pass(kind, n);  // warp_pass2_kernel: class lo, then t
     auto order_key = [&](uint64_t k) {
+      if (wl) return ((k & 1023) << 32) | (k >> 10);
       const uint64_t low = k & (stride - 1);
       const uint64_t hi = k >> (s0 + L);
       const uint64_t cta = hi * lo_blocks + low / G;
@@ -1336,6 +1501,21 @@ static void build_inputs(int kind, uint64_t n, uint64_t q_w, const std::vector<d
         S.dest_of_sample[sidx] = static_cast<int64_t>(dst);
       }
     });
+    if (wl) {
+      std::vector<int32_t> ls(1025, 0);
+      std::vector<uint16_t> tl(std::max<uint64_t>(nrows, 1));
+      for (uint64_t dst = 0; dst < nrows; ++dst) {
+        const uint64_t k = pos_of_dest[dst];
+        ++ls[(k & 1023) + 1];
+        tl[dst] = static_cast<uint16_t>(k >> 10);
+      }
+      for (int i = 0; i < 1024; ++i) ls[i + 1] += ls[i];
+      S.lo_start.alloc(1025);
+      S.t_list.alloc(tl.size());
+      FSTK_CUDA(cudaMemcpyAsync(S.lo_start.p, ls.data(), ls.size() * 4, cudaMemcpyHostToDevice, s));
+      FSTK_CUDA(cudaMemcpyAsync(S.t_list.p, tl.data(), tl.size() * 2, cudaMemcpyHostToDevice, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));  // host vectors go out of scope
+    }
   }
   std::vector<double> pre(nrows), pim(nrows), pc(nrows);
   if (kind == FSTK_TRANSFORM_DCT) {
@@ -1767,6 +1947,8 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
     J.row_src = rf->in.row_src.p;
     J.slot = rf->in.slot.p;
     J.compact = true;
+    J.lo_start = rf->in.lo_start.p;
+    J.t_list = rf->in.t_list.p;
     J.post_re = rf->in.post_re.p;
     J.post_im = rf->in.post_im.p;
     J.post_c = rf->in.post_c.p;

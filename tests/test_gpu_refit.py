@@ -320,3 +320,19 @@ def test_three_pass_sketch_bitexact(O, t):
     assert np.array_equal(sess.rows(), rows_o)
     assert np.array_equal(a, ao) and np.array_equal(b, bo)
     sess.close()
+
+
+@pytest.mark.parametrize("t,q,s", [("dct", 1_200_000, 4096), ("fft", 1_200_000, 4096),
+                                   ("dct", 700_000, 600_000), ("fft", 700_000, 30)])
+def test_two_pass_1m_sketch_bitexact(O, t, q, s):
+    # q_pad = 2^20: both warp-level transform passes (the C2/C4/C5 shape),
+    # with a full working subset (q = 1.2M) and with 383k zero-padded rows.
+    m = synth.random_model((3, 2, 2), [6, 6, 6], 3, seed=41)
+    pts, vals = _data(O, m, q, 42)
+    sess = F.RefitSession(m, pts, vals, seed=8, transform=t, sample_rows=s)
+    assert sess.info_dict()["padded_rows"] == 1 << 20
+    a, b = sess.sketched()
+    ao, bo, rows_o, _, _ = O.refit_system(m, pts, vals, seed=8, transform=t, sample_rows=s)
+    assert np.array_equal(sess.rows(), rows_o)
+    assert np.array_equal(a, ao) and np.array_equal(b, bo)
+    sess.close()
