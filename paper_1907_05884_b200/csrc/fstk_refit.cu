@@ -241,10 +241,14 @@ static std::shared_ptr<DevBuf<double2>> warp_pass2_twiddles(int device, uint64_t
 
 // Whether the last pass of a sketch runs warp_pass2_kernel: complex
 // transforms with q_pad = 2^20 (two passes of 10 stages), when
-// FSTK_SKETCH_WARP2=1 (off by default: at C2 it measured 3.1-3.4 ms per 256
-// columns against 2.8 ms for transform_pass2_kernel -- every column re-reads
-// 16 MB of class twiddle rows, or, class-group major, over-fetches the
-// intermediate).  build_inputs orders destination rows to match.
+// FSTK_SKETCH_WARP2=1.  Off by default: at C2 it reads the intermediate once
+// (4.3 GB per 256 columns) but takes 4.4 ms against 2.8 ms for
+// transform_pass2_kernel -- 8 warps per SM (255 registers with the stage
+// 15..19 twiddles resident) cannot hide the load latency.  Measured and
+// dropped on the way: one class per warp (3.1 ms; each column re-reads the
+// 16 MB of class twiddle rows), 4-class CTAs class-group major (3.4 ms) or
+// two per SM (5.0 ms; 64-byte runs over-fetch the intermediate 1.5x).
+// build_inputs orders destination rows to match.
 static bool warp_last_pass(int kind, uint64_t n) {
   static const bool on = [] {
     const char* e = std::getenv("FSTK_SKETCH_WARP2");
@@ -295,6 +299,7 @@ struct PassParams {
   int compact;              // last pass: destination rows consecutive per CTA
   int list_off;             // byte offset of the per-CTA sampled-element list
   int ct_rounds;            // L == 10: compile-time stage rounds (radix_round_ct)
+  int swap;                 // staging in x's layout, alternating with x (see kernel)
   // warp_pass2_kernel (last pass of q_pad = 2^20): per-position-class twiddle
   // rows and the sampled elements of each class in destination-row order.
   const double2* tw2;       // 1024 rows of 1023 twiddles (warp_pass2_twiddles)
@@ -493,6 +498,12 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
   const int L = P.L, E = 1 << L, nel = E * G;
   T* x = reinterpret_cast<T*>(smem_raw);
   double2* tws = reinterpret_cast<double2*>(smem_raw + static_cast<size_t>(nel + nel / 8) * sizeof(T));
+  // P.swap (complex intermediate source): the staging buffer has x's padded
+  // layout, and the two alternate as the working buffer column by column.
+  const bool swap = !REAL && P.src == SRC_BUFFER && P.prefetch && P.swap;
+  T* const buf0 = x;
+  T* const buf1 = reinterpret_cast<T*>(smem_raw + P.stg_off);
+  int cur = 0;
   const int64_t stride = int64_t(1) << P.s0;
   const int64_t lo_blocks = stride / G;
   const int64_t bidx = blockIdx.x;
@@ -518,9 +529,14 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
   auto staged = [&](int cc) {
     return P.prefetch && cc < ncols_batch && (P.src == SRC_BUFFER || P.col0 + cc < P.R);
   };
-  auto prefetch = [&](int cc) {
+  auto prefetch = [&](int cc, int into) {
     if (!staged(cc)) return;
-    if (P.src == SRC_BUFFER) {
+    if (swap) {
+      for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+        const int64_t p = base + (e % G) + static_cast<int64_t>(e / G) * stride;
+        cp_async16((into ? buf1 : buf0) + spad(e), P.cbuf + static_cast<int64_t>(cc) * P.n + p);
+      }
+    } else if (P.src == SRC_BUFFER) {
       // G == 2: element pairs (e, e+1) are adjacent in global memory.
       const int nch = REAL ? nel / 2 : nel;
       for (int ch = threadIdx.x; ch < nch; ch += blockDim.x) {
@@ -588,7 +604,7 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
       __syncthreads();
     }
   }
-  prefetch(blockIdx.y);
+  prefetch(blockIdx.y, 0);
   for (int cc = blockIdx.y; cc < ncols_batch; cc += gridDim.y) {
     const int64_t col = P.col0 + cc;
     __syncthreads();
@@ -596,7 +612,9 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
     if (staged(cc)) {
       cp_async_wait_all();
       __syncthreads();
-      if (P.src == SRC_BUFFER) {
+      if (swap) {
+        x = cur ? buf1 : buf0;
+      } else if (P.src == SRC_BUFFER) {
         const T* sv = reinterpret_cast<const T*>(stg);
         for (int e = threadIdx.x; e < nel; e += blockDim.x) x[spad(e)] = sv[e];
       } else if constexpr (DT > 0) {
@@ -660,7 +678,8 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
       }
     }
     __syncthreads();
-    prefetch(cc + gridDim.y);  // staging is free: this column now lives in x
+    prefetch(cc + gridDim.y, cur ^ 1);  // staging is free: this column now lives in x
+    cur ^= 1;
     // ---- stages, three per register round
     if (L == 10 && P.ct_rounds) {
       constexpr int NE = 1024 * G;
@@ -882,103 +901,114 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
 }
 
 // ------------------------------------------- warp-level last pass (K3b) ---
-// Stages 10..19 of a q_pad = 2^20 complex sketch.  A CTA of 4 warps owns 4
-// adjacent position classes lo0..lo0+3 (positions t 1024 + lo, t < 1024) of
-// one column, so every 64-byte run t 1024 + lo0 .. lo0+3 of the intermediate
-// is read whole.  Phase A: lane (a_sub, c) of warp w loads t = 32 a + b
-// (a = 8 w + a_sub, b = 0..31) of class lo0 + c -- coalesced 64-byte runs --
-// and runs stages 10..14 (len 2^11..2^15) in registers.  One CTA exchange
-// (per-class rows of 33, class stride 1058: conflict-free both ways) gives
-// warp w class lo0 + w with lane b' holding t = 32 a + b', a = 0..31, for
-// stages 15..19; twiddle rows are per class (warp_pass2_twiddles).  The
-// class's sampled elements (destination rows lo_start[lo] ..) are then
-// post-rotated (DCT) or split (FFT) and stored row-contiguously.  Same
-// butterflies and epilogue as transform_pass2_kernel, in the same order.
-constexpr int kWp2Cls = 4;                     // classes (warps) per CTA
-constexpr int kWp2Stride = 32 * kWp1Row + 2;   // double2 per class row block
+// Stages 10..19 of a q_pad = 2^20 complex sketch.  A CTA of 8 warps owns the
+// 8 adjacent position classes lo0..lo0+7 (positions t 1024 + lo, t < 1024),
+// i.e. whole 128-byte runs of the intermediate, and loops over the batch's
+// columns, so each class's twiddles are fetched once per launch: stages
+// 10..14 from a shared copy, stages 15..19 held in registers.
+// Phase A: lane (a_sub, c) of warp w loads t = 32 a + b (a = 4 w + a_sub,
+// b = 0..31) of class lo0 + c -- four full lines per load -- and runs stages
+// 10..14 (len 2^11..2^15) in registers.  One CTA exchange (per-class rows of
+// 33, class stride 1057: conflict-free both ways) gives warp w class lo0 + w
+// with lane b' holding t = 32 a + b', a = 0..31, for stages 15..19.  The
+// result is parked in the warp's class rows while the next column's loads
+// are in flight, and the class's sampled elements (destination rows
+// lo_start[lo] ..) are post-rotated (DCT) or split (FFT) and stored
+// row-contiguously.  Same butterflies and epilogue as transform_pass2_kernel,
+// in the same order.
+constexpr int kWp2Cls = 8;                     // classes (warps) per CTA
+constexpr int kWp2Stride = 32 * kWp1Row + 1;   // double2 per class row block
 
-__global__ void __launch_bounds__(kWp2Cls * 32, 3) warp_pass2_kernel(const PassParams P, int ncols_batch) {
+__device__ __forceinline__ void wp2_load(double2 (&v)[32], const double2* src) {
+#pragma unroll
+  for (int b = 0; b < 32; ++b) v[b] = __ldcs(src + static_cast<int64_t>(b) * 1024);
+}
+
+__global__ void __launch_bounds__(kWp2Cls * 32, 1) warp_pass2_kernel(const PassParams P, int ncols_batch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* Xc = reinterpret_cast<double2*>(smem_raw);
   double2* tA = Xc + kWp2Cls * kWp2Stride;  // [class][31]
-  const int c = lane & 3, a = 8 * warp + (lane >> 2);
-  const int64_t groups = static_cast<int64_t>(ncols_batch) * (1024 / kWp2Cls);
-  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
-    // Class-group major, column fastest: CTAs running together share the
-    // twiddle rows of one or two class groups (L1/L2 hits); the other half
-    // of each 128-byte run is read by the next class group from L2.
-    const int64_t lg = g / ncols_batch;
-    const int cc = static_cast<int>(g - lg * ncols_batch);
-    const int lo0 = static_cast<int>(lg) * kWp2Cls;
-    const int64_t col = P.col0 + cc;
-    const double2* src = P.cbuf + static_cast<int64_t>(cc) * P.n + lo0 + c;
-    double2 v[32];
-#pragma unroll
-    for (int b = 0; b < 32; ++b) v[b] = __ldcg(src + static_cast<int64_t>(32 * a + b) * 1024);
-    __syncthreads();  // previous group done with Xc and tA
+  const int c = lane & 7, a = 4 * warp + (lane >> 3);
+  double2* xo = Xc + c * kWp2Stride + a * kWp1Row;
+  double2* xw = Xc + warp * kWp2Stride;
+  for (int lg = blockIdx.x; lg < 1024 / kWp2Cls; lg += gridDim.x) {
+    const int lo0 = lg * kWp2Cls, lo = lo0 + warp;
+    __syncthreads();  // previous class group done with tA
     for (int i = threadIdx.x; i < kWp2Cls * 31; i += blockDim.x)
       tA[i] = P.tw2[static_cast<int64_t>(lo0 + i / 31) * 1023 + i % 31];
-    __syncthreads();
-    // ---- stages 10..14: k = lo + 1024 (b mod 2^j)
-    const double2* tc = tA + 31 * c;
+    // stages 15..19 twiddles of class lo for this lane: k = lo + 1024 (b' + 32 m)
+    double2 twB[31];
+    {
+      const double2* twr = P.tw2 + static_cast<int64_t>(lo) * 1023 + lane;
 #pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      const int half = 1 << j;
+      for (int i = 0; i < 5; ++i)
 #pragma unroll
-      for (int b = 0; b < 32; ++b) {
-        if (b & half) continue;
-        const double2 w = tc[half - 1 + (b & (half - 1))];
-        const double2 uu = v[b];
-        const double2 t2 = cmul_x(v[b + half], w);
-        v[b] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
-        v[b + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
-      }
+        for (int m = 0; m < (1 << i); ++m) twB[(1 << i) - 1 + m] = __ldg(twr + (32 << i) - 1 + 32 * m);
     }
-    // ---- exchange: warp w takes class lo0 + w, lane b' the elements 32 a + b'
-    double2* xo = Xc + c * kWp2Stride + a * kWp1Row;
+    const double2* tc = tA + 31 * c;
+    const int first = P.lo_start[lo], cnt = P.lo_start[lo + 1] - first;
+    const double2* src0 = P.cbuf + lo0 + c + static_cast<int64_t>(32 * a) * 1024;
+    double2 v[32];
+    wp2_load(v, src0);
+    __syncthreads();  // tA ready
+    for (int cc = 0; cc < ncols_batch; ++cc) {
+      const int64_t col = P.col0 + cc;
+      // ---- stages 10..14: k = lo + 1024 (b mod 2^j)
 #pragma unroll
-    for (int b = 0; b < 32; ++b) xo[b] = v[b];
-    __syncthreads();
-    double2* xw = Xc + warp * kWp2Stride;
+      for (int j = 0; j < 5; ++j) {
+        const int half = 1 << j;
 #pragma unroll
-    for (int aa = 0; aa < 32; ++aa) v[aa] = xw[aa * kWp1Row + lane];
-    // ---- stages 15..19: k = lo + 1024 (b' + 32 (a mod 2^i))
-    const int lo = lo0 + warp;
-    const double2* twr = P.tw2 + static_cast<int64_t>(lo) * 1023;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const int half = 1 << i;
-      const double2* twi = twr + (32 << i) - 1 + lane;
-#pragma unroll
-      for (int m = 0; m < half; ++m) {
-        const double2 w = __ldg(twi + 32 * m);
-#pragma unroll
-        for (int aa = m; aa < 32; aa += 2 * half) {
-          const double2 uu = v[aa];
-          const double2 t2 = cmul_x(v[aa + half], w);
-          v[aa] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
-          v[aa + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
+        for (int b = 0; b < 32; ++b) {
+          if (b & half) continue;
+          const double2 w = tc[half - 1 + (b & (half - 1))];
+          const double2 uu = v[b];
+          const double2 t2 = cmul_x(v[b + half], w);
+          v[b] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
+          v[b + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
         }
       }
-    }
-    __syncwarp();
+      // ---- exchange: warp w takes class lo0 + w, lane b' the elements 32 a + b'
+      __syncthreads();  // previous column's output reads done
 #pragma unroll
-    for (int aa = 0; aa < 32; ++aa) xw[aa * kWp1Row + lane] = v[aa];
-    __syncwarp();
-    // ---- sampled rows of this class (consecutive destination rows)
-    const int first = P.lo_start[lo], cnt = P.lo_start[lo + 1] - first;
-    for (int i = lane; i < cnt; i += 32) {
-      const int64_t sl = first + i;
-      if (sl < P.row_lo || sl >= P.row_hi) continue;
-      const int t = P.t_list[sl];
-      const double2 V = xw[(t >> 5) * kWp1Row + (t & 31)];
-      if (P.kind == FSTK_TRANSFORM_DCT) {
-        const double val = xsub(xmul(__ldg(P.post_re + sl), V.x), xmul(__ldg(P.post_im + sl), V.y));
-        *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(__ldg(P.post_c + sl), val));
-      } else {
-        *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
-        *store_ptr(P, col, sl, true) = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
+      for (int b = 0; b < 32; ++b) xo[b] = v[b];
+      __syncthreads();
+#pragma unroll
+      for (int aa = 0; aa < 32; ++aa) v[aa] = xw[aa * kWp1Row + lane];
+      // ---- stages 15..19: k = lo + 1024 (b' + 32 (a mod 2^i))
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int half = 1 << i;
+#pragma unroll
+        for (int m = 0; m < half; ++m) {
+          const double2 w = twB[half - 1 + m];
+#pragma unroll
+          for (int aa = m; aa < 32; aa += 2 * half) {
+            const double2 uu = v[aa];
+            const double2 t2 = cmul_x(v[aa + half], w);
+            v[aa] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
+            v[aa + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int aa = 0; aa < 32; ++aa) xw[aa * kWp1Row + lane] = v[aa];
+      __syncwarp();
+      if (cc + 1 < ncols_batch) wp2_load(v, src0 + static_cast<int64_t>(cc + 1) * P.n);
+      // ---- sampled rows of this class (consecutive destination rows)
+      for (int i = lane; i < cnt; i += 32) {
+        const int64_t sl = first + i;
+        if (sl < P.row_lo || sl >= P.row_hi) continue;
+        const int t = P.t_list[sl];
+        const double2 V = xw[(t >> 5) * kWp1Row + (t & 31)];
+        if (P.kind == FSTK_TRANSFORM_DCT) {
+          const double val = xsub(xmul(__ldg(P.post_re + sl), V.x), xmul(__ldg(P.post_im + sl), V.y));
+          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(__ldg(P.post_c + sl), val));
+        } else {
+          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
+          *store_ptr(P, col, sl, true) = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
+        }
       }
     }
   }
@@ -1261,7 +1291,14 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       }();
       const int dtp = (P.src == SRC_TABLES && (J.d == 3 || J.d == 4)) ? J.d : 0;
       size_t stg = 0;
-      if (pf_on && P.src == SRC_BUFFER && (P.G == 2 || !real))
+      static const bool swap_on = [] {
+        const char* e = std::getenv("FSTK_SKETCH_SWAP");
+        return !(e && std::atoi(e) == 0);
+      }();
+      P.swap = (swap_on && pf_on && P.src == SRC_BUFFER && !real) ? 1 : 0;
+      if (P.swap)
+        stg = static_cast<size_t>(E * P.G + E * P.G / 8) * elem;
+      else if (pf_on && P.src == SRC_BUFFER && (P.G == 2 || !real))
         stg = static_cast<size_t>(E * P.G) * elem;
       else if (pf_on && dtp > 0 && P.G == 1 && P.s0 == 0 && E * P.G >= 2)
         stg = static_cast<size_t>(dtp) * E * P.G * 8;
@@ -1304,8 +1341,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
         P.lo_start = J.lo_start;
         P.t_list = J.t_list;
         const size_t wsm = static_cast<size_t>(kWp2Cls * kWp2Stride + kWp2Cls * 31) * sizeof(double2);
-        const unsigned wgrid = static_cast<unsigned>(std::min<int64_t>(
-            int64_t(sms) * 3, static_cast<int64_t>(nb) * (1024 / kWp2Cls)));
+        const unsigned wgrid = static_cast<unsigned>(std::min<int64_t>(sms, 1024 / kWp2Cls));
         warp_pass2_kernel<<<wgrid, kWp2Cls * 32, wsm, s>>>(P, nb);
         check_launch("warp_pass2_kernel");
         continue;
