@@ -1767,13 +1767,47 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
     // Validation rows (sorted) and the training rows = their complement in
     // ascending order, never materialised: train_at() maps sorted positions
     // into the complement by one merge against `val`.
-    std::vector<uint64_t> val;
     rf->held_out = n_val >= 1;
+    const uint64_t n_train = uq - n_val;  // sample_without_replacement returns n_val < q rows
+    const uint64_t q_w = cfg->working_subset == 0
+                             ? n_train
+                             : std::min<uint64_t>(cfg->working_subset, n_train);
+    require(q_w >= 1, FSTK_E_PARAMETER, "no training points left");
+    rf->q_w = q_w;
+    rf->S = S;
+    rf->none = cfg->transform == FSTK_TRANSFORM_NONE;
+    // The three host RNG streams are independent (mix_seed tags), so the
+    // sketch plan and the transform-order inputs built from it (solve_sketched,
+    // randls.cpp:318: plan seeded with mix_seed(seed, kSketchTag)) are made on
+    // a second host thread while this one draws the validation rows and the
+    // working subset and uploads them.  Same draws, same results; a plan error
+    // is rethrown after the join.
+    std::exception_ptr plan_err;
+    std::thread planner([&, dev = m->device] {
+      try {
+        FSTK_CUDA(cudaSetDevice(dev));
+        rf->plan = rf->none ? make_plan_none(q_w, S, mix_seed(cfg->seed, kSketchTag))
+                            : make_plan(q_w, S, mix_seed(cfg->seed, kSketchTag));
+        require(rf->plan.q_pad < (uint64_t(1) << 31), FSTK_E_PARAMETER, "working subset too large");
+        // Inputs in transform order; destination rows in last-pass visit order.
+        if (!rf->none)
+          build_inputs(cfg->transform, rf->plan.q_pad, q_w, rf->plan.signs, rf->plan.rows, false, {},
+                       true, rf->in, s);
+      } catch (...) {
+        plan_err = std::current_exception();
+      }
+    });
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } joiner{planner};
+    std::vector<uint64_t> val;
     if (rf->held_out) {
       Rng rng(mix_seed(cfg->seed, kValidationTag));
       val = rng.sample_without_replacement(uq, n_val);
     }
-    const uint64_t n_train = uq - val.size();
     auto complement_of = [&](const std::vector<uint64_t>& pos) {
       std::vector<int64_t> outv(pos.size());
       uint64_t vi = 0;
@@ -1785,10 +1819,6 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
       return outv;
     };
     mark("validation split");
-    const uint64_t q_w = cfg->working_subset == 0
-                             ? n_train
-                             : std::min<uint64_t>(cfg->working_subset, n_train);
-    require(q_w >= 1, FSTK_E_PARAMETER, "no training points left");
     std::vector<int64_t> subset;  // dataset rows of the working subset, ascending
     if (q_w == n_train) {
       std::vector<uint64_t> all(n_train);
@@ -1803,15 +1833,6 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
       std::iota(val.begin(), val.end(), 0);
     }
     mark("working subset");
-    rf->q_w = q_w;
-    rf->S = S;
-    rf->none = cfg->transform == FSTK_TRANSFORM_NONE;
-    // solve_sketched (randls.cpp:318): plan seeded with mix_seed(seed, kSketchTag).
-    rf->plan = rf->none ? make_plan_none(q_w, S, mix_seed(cfg->seed, kSketchTag))
-                        : make_plan(q_w, S, mix_seed(cfg->seed, kSketchTag));
-    rf->q_pad = rf->plan.q_pad;
-    require(rf->q_pad < (uint64_t(1) << 31), FSTK_E_PARAMETER, "working subset too large");
-    mark("sketch plan");
     // Compact upload: subset rows (in subset order) and validation rows.
     rf->subset = subset;
     rf->d_points.alloc(static_cast<size_t>(q_w) * d);
@@ -1852,6 +1873,10 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
       FSTK_CUDA(cudaStreamSynchronize(s));
     }
     mark("compact upload");
+    planner.join();
+    if (plan_err) std::rethrow_exception(plan_err);
+    rf->q_pad = rf->plan.q_pad;
+    mark("sketch plan + inputs");
     rf->row_lo = static_cast<int64_t>(S) * shard / shards;
     rf->row_hi = static_cast<int64_t>(S) * (shard + 1) / shards;
     rf->local_rows = rf->row_hi - rf->row_lo;
@@ -1899,10 +1924,6 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
       *out = rf.release();
       return;
     }
-    // Inputs in transform order; destination rows in last-pass visit order.
-    build_inputs(cfg->transform, rf->q_pad, q_w, rf->plan.signs, rf->plan.rows, false, {},
-                 true, rf->in, s);
-    mark("build inputs");
     // Mode tables over the padded positions, bit-exact (mode_value_tables, randls.cpp:21-41).
     int64_t toff[kMaxOrder], tot = 0;
     const int64_t ldt = static_cast<int64_t>(rf->q_pad);
