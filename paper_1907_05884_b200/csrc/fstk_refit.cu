@@ -242,9 +242,10 @@ static std::shared_ptr<DevBuf<double2>> warp_pass2_twiddles(int device, uint64_t
 // Whether the last pass of a sketch runs warp_pass2_kernel: complex
 // transforms with q_pad = 2^20 (two passes of 10 stages), when
 // FSTK_SKETCH_WARP2=1.  Off by default: at C2 it reads the intermediate once
-// (4.3 GB per 256 columns) but takes 4.4 ms against 2.8 ms for
+// (4.3 GB per 256 columns) but takes 2.67 ms against ~2.5 ms for
 // transform_pass2_kernel -- 8 warps per SM (255 registers with the stage
-// 15..19 twiddles resident) cannot hide the load latency.  Measured and
+// 15..19 twiddles resident, some spilled) leave shared-memory latency
+// exposed (4.4 ms before the per-class sampled-row cache).  Measured and
 // dropped on the way: one class per warp (3.1 ms; each column re-reads the
 // 16 MB of class twiddle rows), 4-class CTAs class-group major (3.4 ms) or
 // two per SM (5.0 ms; 64-byte runs over-fetch the intermediate 1.5x).
@@ -288,6 +289,7 @@ struct PassParams {
   const double* post_im;    // per destination row (DCT: sin)
   const double* post_c;     // per destination row (DCT: c_k)
   double scale;             // plan.scale (sqrt(q_pad/S)) or 1
+  double post_c0, post_ck;  // DCT normalisation c_0, c_k (dct_post; warp_pass2_kernel)
   double inv_sqrt_n;        // 1/sqrt(n) (FFT, WHT)
   int64_t row_lo, row_hi;   // destination rows owned by this shard
   int64_t im_off;           // FFT: rows of the Re block in A (Im block follows)
@@ -918,6 +920,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
 // in the same order.
 constexpr int kWp2Cls = 8;                     // classes (warps) per CTA
 constexpr int kWp2Stride = 32 * kWp1Row + 1;   // double2 per class row block
+constexpr int kWp2Cap = 512;                   // sampled elements per class cached in shared memory
+constexpr size_t kWp2Smem = (kWp2Cls * kWp2Stride + kWp2Cls * 31) * sizeof(double2) +
+                            kWp2Cls * kWp2Cap * (2 * sizeof(double) + sizeof(uint16_t));
 
 __device__ __forceinline__ void wp2_load(double2 (&v)[32], const double2* src) {
 #pragma unroll
@@ -929,6 +934,12 @@ __global__ void __launch_bounds__(kWp2Cls * 32, 1) warp_pass2_kernel(const PassP
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* Xc = reinterpret_cast<double2*>(smem_raw);
   double2* tA = Xc + kWp2Cls * kWp2Stride;  // [class][31]
+  // Per class, the first kWp2Cap sampled elements: t and the DCT rotation,
+  // the same for every column (loaded once per class group).
+  double* cre = reinterpret_cast<double*>(tA + kWp2Cls * 31) + warp * kWp2Cap;
+  double* cim = reinterpret_cast<double*>(tA + kWp2Cls * 31) + (kWp2Cls + warp) * kWp2Cap;
+  uint16_t* ct = reinterpret_cast<uint16_t*>(reinterpret_cast<double*>(tA + kWp2Cls * 31) +
+                                             2 * kWp2Cls * kWp2Cap) + warp * kWp2Cap;
   const int c = lane & 7, a = 4 * warp + (lane >> 3);
   double2* xo = Xc + c * kWp2Stride + a * kWp1Row;
   double2* xw = Xc + warp * kWp2Stride;
@@ -948,6 +959,14 @@ __global__ void __launch_bounds__(kWp2Cls * 32, 1) warp_pass2_kernel(const PassP
     }
     const double2* tc = tA + 31 * c;
     const int first = P.lo_start[lo], cnt = P.lo_start[lo + 1] - first;
+    const bool dct = P.kind == FSTK_TRANSFORM_DCT;
+    for (int i = lane; i < min(cnt, kWp2Cap); i += 32) {
+      ct[i] = P.t_list[first + i];
+      if (dct) {
+        cre[i] = P.post_re[first + i];
+        cim[i] = P.post_im[first + i];
+      }
+    }
     const double2* src0 = P.cbuf + lo0 + c + static_cast<int64_t>(32 * a) * 1024;
     double2 v[32];
     wp2_load(v, src0);
@@ -1000,11 +1019,15 @@ __global__ void __launch_bounds__(kWp2Cls * 32, 1) warp_pass2_kernel(const PassP
       for (int i = lane; i < cnt; i += 32) {
         const int64_t sl = first + i;
         if (sl < P.row_lo || sl >= P.row_hi) continue;
-        const int t = P.t_list[sl];
+        const bool cached = i < kWp2Cap;
+        const int t = cached ? ct[i] : P.t_list[sl];
         const double2 V = xw[(t >> 5) * kWp1Row + (t & 31)];
-        if (P.kind == FSTK_TRANSFORM_DCT) {
-          const double val = xsub(xmul(__ldg(P.post_re + sl), V.x), xmul(__ldg(P.post_im + sl), V.y));
-          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(__ldg(P.post_c + sl), val));
+        if (dct) {
+          const double re = cached ? cre[i] : __ldg(P.post_re + sl);
+          const double im = cached ? cim[i] : __ldg(P.post_im + sl);
+          const double val = xsub(xmul(re, V.x), xmul(im, V.y));
+          const double cf = (t == 0 && lo == 0) ? P.post_c0 : P.post_ck;  // dct_post(k = t 1024 + lo)
+          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(cf, val));
         } else {
           *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
           *store_ptr(P, col, sl, true) = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
@@ -1160,6 +1183,8 @@ static int ilog2(uint64_t n) {
   return l;
 }
 
+static void dct_post(uint64_t k, uint64_t n, double* re, double* im, double* c);
+
 static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
   const int LOG = ilog2(J.n);
   const bool real = J.kind == FSTK_TRANSFORM_WHT;
@@ -1267,6 +1292,11 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       P.post_c = J.post_c;
       P.scale = J.scale;
       P.inv_sqrt_n = 1.0 / std::sqrt(static_cast<double>(J.n));
+      {
+        double re, im;
+        dct_post(0, J.n, &re, &im, &P.post_c0);
+        dct_post(1, J.n, &re, &im, &P.post_ck);
+      }
       P.row_lo = J.row_lo;
       P.row_hi = J.row_hi;
       P.im_off = J.im_off;
@@ -1340,7 +1370,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
         P.tw2 = tw2->p;
         P.lo_start = J.lo_start;
         P.t_list = J.t_list;
-        const size_t wsm = static_cast<size_t>(kWp2Cls * kWp2Stride + kWp2Cls * 31) * sizeof(double2);
+        const size_t wsm = kWp2Smem;
         const unsigned wgrid = static_cast<unsigned>(std::min<int64_t>(sms, 1024 / kWp2Cls));
         warp_pass2_kernel<<<wgrid, kWp2Cls * 32, wsm, s>>>(P, nb);
         check_launch("warp_pass2_kernel");
