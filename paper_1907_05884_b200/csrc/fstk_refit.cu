@@ -606,6 +606,21 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
       __syncthreads();
     }
   }
+  // The DCT rotation of this CTA's first two sampled elements per thread,
+  // the same for every column: kept in registers.
+  double cre0 = 0.0, cim0 = 0.0, cre1 = 0.0, cim1 = 0.0;
+  if (!REAL && use_list && P.kind == FSTK_TRANSFORM_DCT) {
+    const int cnt = s_cnt;
+    const int64_t first = s_first;
+    if (static_cast<int>(threadIdx.x) < cnt) {
+      cre0 = __ldg(P.post_re + first + threadIdx.x);
+      cim0 = __ldg(P.post_im + first + threadIdx.x);
+    }
+    if (static_cast<int>(threadIdx.x + blockDim.x) < cnt) {
+      cre1 = __ldg(P.post_re + first + threadIdx.x + blockDim.x);
+      cim1 = __ldg(P.post_im + first + threadIdx.x + blockDim.x);
+    }
+  }
   prefetch(blockIdx.y, 0);
   for (int cc = blockIdx.y; cc < ncols_batch; cc += gridDim.y) {
     const int64_t col = P.col0 + cc;
@@ -716,8 +731,13 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
           *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(x[spad(e)], P.inv_sqrt_n));
         } else if (P.kind == FSTK_TRANSFORM_DCT) {
           const double2 V = x[spad(e)];
-          const double val = xsub(xmul(__ldg(P.post_re + sl), V.x), xmul(__ldg(P.post_im + sl), V.y));
-          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(__ldg(P.post_c + sl), val));
+          const bool k0 = idx == static_cast<int>(threadIdx.x), k1 = idx == static_cast<int>(threadIdx.x + blockDim.x);
+          const double re = k0 ? cre0 : (k1 ? cre1 : __ldg(P.post_re + sl));
+          const double im = k0 ? cim0 : (k1 ? cim1 : __ldg(P.post_im + sl));
+          const double val = xsub(xmul(re, V.x), xmul(im, V.y));
+          // dct_post: c_0 at output position 0, c_k elsewhere
+          const bool pos0 = base + (e % G) + static_cast<int64_t>(e / G) * stride == 0;
+          *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(pos0 ? P.post_c0 : P.post_ck, val));
         } else {
           const double2 V = x[spad(e)];
           *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
