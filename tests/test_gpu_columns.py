@@ -156,3 +156,23 @@ def test_column_layout_more_shards_than_columns(O):
         r.close()
     for s in cols:
         s.close()
+
+
+@pytest.mark.parametrize("t", ["dct", "fft"])
+def test_column_sharded_rows_bitexact_at_1m(O, t):
+    # q_pad = 2^20 (the warp-level first pass) with packed per-shard stores.
+    m = synth.random_model((3, 2, 2), [5, 5, 5], 3, seed=13)
+    pts, vals = _data(O, m, 1_150_000, 14)
+    G = 2
+    cols = [F.RefitSession(m, pts, vals, seed=5, transform=t, shard=g, shards=G, sample_rows=4096,
+                           layout="columns") for g in range(G)]
+    _exchange_in_process(cols)
+    for g in range(G):
+        r = F.RefitSession(m, pts, vals, seed=5, transform=t, shard=g, shards=G, sample_rows=4096)
+        assert r.info_dict()["padded_rows"] == 1 << 20
+        ac, bc = cols[g].sketched()
+        ar, br = r.sketched()
+        assert np.array_equal(ac, ar) and np.array_equal(bc, br)
+        r.close()
+    for s in cols:
+        s.close()

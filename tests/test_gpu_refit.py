@@ -336,3 +336,18 @@ def test_two_pass_1m_sketch_bitexact(O, t, q, s):
     assert np.array_equal(sess.rows(), rows_o)
     assert np.array_equal(a, ao) and np.array_equal(b, bo)
     sess.close()
+
+
+@pytest.mark.parametrize("t,ranks", [("dct", (2, 2, 2, 2)), ("wht", (3, 2, 2))])
+def test_two_pass_1m_order4_and_wht_bitexact(O, t, ranks):
+    # q_pad = 2^20 for a 4-mode model (warp first pass with four tables) and
+    # for the real WHT (shared-memory passes only).
+    m = synth.random_model(ranks, [5] * len(ranks), 3, seed=43)
+    pts, vals = _data(O, m, 1_150_000, 44)
+    sess = F.RefitSession(m, pts, vals, seed=9, transform=t, sample_rows=2048)
+    assert sess.info_dict()["padded_rows"] == 1 << 20
+    a, b = sess.sketched()
+    ao, bo, rows_o, _, _ = O.refit_system(m, pts, vals, seed=9, transform=t, sample_rows=2048)
+    assert np.array_equal(sess.rows(), rows_o)
+    assert np.array_equal(a, ao) and np.array_equal(b, bo)
+    sess.close()

@@ -1,5 +1,4 @@
-# scratch experiment driver (gpurun): parity subset + sketch timing
-K="sketch_rows or three_pass or c1_refit or two_pass_1m or sharded or columns"
-python -m pytest tests/test_gpu_refit.py tests/test_gpu_columns.py -x -q -k "$K" > gpurun_out/exp_tests.log 2>&1; tail -n 2 gpurun_out/exp_tests.log
-python tools/sketch_time.py 4 > gpurun_out/exp_time.log 2>&1
-cat gpurun_out/exp_time.log
+# scratch experiment driver (gpurun): new 2^20 parity tests + bench
+python -m pytest tests/test_gpu_refit.py tests/test_gpu_columns.py -x -q -k "1m" > gpurun_out/exp_tests.log 2>&1; tail -n 2 gpurun_out/exp_tests.log
+FSTK_SKETCH_WARP2=1 python -m pytest tests/test_gpu_refit.py tests/test_gpu_columns.py -x -q -k "1m" > gpurun_out/exp_tests2.log 2>&1; tail -n 2 gpurun_out/exp_tests2.log
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -n 2 gpurun_out/bench.err
