@@ -1428,13 +1428,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
         check_launch("warp_pass1_kernel");
         continue;
       }
-      // G = 1 passes: a radix-2^3 round has E / 8 = 128 butterfly blocks, so
-      // FSTK_SKETCH_G1_THREADS=128 keeps every thread busy in the rounds.
-      static const int g1_threads = [] {
-        const char* e = std::getenv("FSTK_SKETCH_G1_THREADS");
-        return (e && std::atoi(e) == 128) ? 128 : 256;
-      }();
-      const int nt1 = g1_threads;
+      const int nt1 = 256;  // 128-thread CTAs for G = 1 measured no faster
       if (P.G == 2) {
         if (real)
           transform_pass2_kernel<true, 2, 0><<<grid, 256, smem, s>>>(P, nb);
