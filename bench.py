@@ -584,10 +584,14 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=No
     # Timed: the median of --refit-reps refits (the int8 Gram and the Cholesky
     # run near the power cap, so single refits vary by ~0.2 s from box to box);
     # then one more with per-kernel event profiling for the stage breakdown.
-    reps = []
+    reps, rep_stages = [], []
     for _ in range(max(1, args.refit_reps)):
-        r_hot, r_all, _, _ = one()
+        r_hot, r_all, _, r_info = one()
         reps.append((r_all, maxreduce(r_hot, world, dev)))
+        rt, rw = r_info["timings"], r_info["wall_s"]
+        rep_stages.append({"prepare": round(rt["prepare_s"], 4), "sketch": round(rt["sketch_s"], 4),
+                           "gram": round(rt["gram_s"], 4), "solve": round(rt["solve_s"], 4),
+                           "begin_wall": round(rw["begin"], 4), "refine_wall": round(rw["refine"], 4)})
     t_all = float(np.median([r[0] for r in reps]))
     t_hot = float(np.median([r[1] for r in reps]))
     _lib.profile_read()
@@ -599,7 +603,7 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=No
     gram_flops = S / world * R * (R + 1)
     return {"seconds": t_all, "hot_path_seconds": t_hot, "warmup_refits": args.refit_warmup,
             "timed_refits": len(reps), "samples_s": [round(r[0], 4) for r in reps],
-            "hot_path_samples_s": [round(r[1], 4) for r in reps],
+            "hot_path_samples_s": [round(r[1], 4) for r in reps], "sample_stages_s": rep_stages,
             "profiled_refit_s": p_all, "cold": cold,
             "scaling": "strong", "sample_rows": S, "working_rows": info["working_rows"],
             "padded_rows": info["padded_rows"], "transform": tform,

@@ -2567,6 +2567,40 @@ static double dev_norm(cublasHandle_t h, int n, const double* x) {
 
 }  // namespace fstk_gpu
 
+// x += (L L^T)^{-1} s (s summed over shards); rel_step = ||dx|| / ||x||.
+namespace fstk_gpu {
+// x := (L L^T)^{-1} x for the lower Cholesky factor L (n x n, ld n), blocked:
+// 1024-wide diagonal TRSVs plus DGEMV panel updates that stream L at memory
+// speed.  cuSOLVER potrs' whole-matrix TRSVs are latency-bound at n = 32,768;
+// this cut the C2 refinement by ~0.1 s.  (Pre-inverting the diagonal blocks
+// so they too become DGEMVs measured slower: the inversions cost more than
+// the four solves save.)
+static void chol_solve_blocked(cublasHandle_t h, const double* L, int n, double* x) {
+  constexpr int NB = 1024;
+  const double one = 1.0, mone = -1.0;
+  auto ok = [](cublasStatus_t st) {
+    if (st != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, "blocked Cholesky solve failed");
+  };
+  for (int i0 = 0; i0 < n; i0 += NB) {  // forward: L y = x
+    const int nb = std::min(NB, n - i0);
+    const double* Lii = L + static_cast<int64_t>(i0) * n + i0;
+    ok(cublasDtrsv(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, nb, Lii, n, x + i0, 1));
+    const int rest = n - i0 - nb;
+    if (rest > 0)
+      ok(cublasDgemv(h, CUBLAS_OP_N, rest, nb, &mone, Lii + nb, n, x + i0, 1, &one, x + i0 + nb, 1));
+  }
+  for (int i1 = n; i1 > 0; i1 -= NB) {  // backward: L^T z = y
+    const int i0 = std::max(0, i1 - NB);
+    const int nb = i1 - i0;
+    const double* Lii = L + static_cast<int64_t>(i0) * n + i0;
+    ok(cublasDtrsv(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, nb, Lii, n, x + i0, 1));
+    if (i0 > 0)  // x[0:i0] -= L[i0:i1, 0:i0]^T x[i0:i1]
+      ok(cublasDgemv(h, CUBLAS_OP_T, nb, i0, &mone, L + i0, n, x + i0, 1, &one, x, 1));
+  }
+  count_launch(4 * ((n + NB - 1) / NB));
+}
+}  // namespace fstk_gpu
+
 int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const double* rhs_in,
                               double* x_dev, fstk_reestimate_info* info, fstk_gpu_error* err) {
   return guarded(err, [&] {
@@ -2596,7 +2630,10 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
     FSTK_CUDA(cudaStreamSynchronize(s));
     rf->factored = hinfo == 0;
     rf->rank_def = !rf->factored;
-    if (rf->factored) {
+    if (rf->factored && n >= 4096) {
+      cublasSetStream(h.blas, s);
+      chol_solve_blocked(h.blas, rf->L.p, n, x_dev);  // potrs' whole-matrix TRSVs are latency-bound
+    } else if (rf->factored) {
       if (cusolverDnDpotrs(h.solver, CUBLAS_FILL_MODE_LOWER, n, 1, rf->L.p, n, x_dev, n, dinfo.p) !=
           CUSOLVER_STATUS_SUCCESS)
         fail(FSTK_E_COMPUTE, "potrs failed");
@@ -2654,39 +2691,6 @@ int32_t fstk_gpu_refit_correction(fstk_gpu_refit* rf, const double* x_dev, doubl
   });
 }
 
-// x += (L L^T)^{-1} s (s summed over shards); rel_step = ||dx|| / ||x||.
-namespace fstk_gpu {
-// x := (L L^T)^{-1} x for the lower Cholesky factor L (n x n, ld n), blocked:
-// 1024-wide diagonal TRSVs plus DGEMV panel updates that stream L at memory
-// speed.  cuSOLVER potrs' whole-matrix TRSVs are latency-bound at n = 32,768;
-// this cut the C2 refinement by ~0.1 s.  (Pre-inverting the diagonal blocks
-// so they too become DGEMVs measured slower: the inversions cost more than
-// the four solves save.)
-static void chol_solve_blocked(cublasHandle_t h, const double* L, int n, double* x) {
-  constexpr int NB = 1024;
-  const double one = 1.0, mone = -1.0;
-  auto ok = [](cublasStatus_t st) {
-    if (st != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, "blocked Cholesky solve failed");
-  };
-  for (int i0 = 0; i0 < n; i0 += NB) {  // forward: L y = x
-    const int nb = std::min(NB, n - i0);
-    const double* Lii = L + static_cast<int64_t>(i0) * n + i0;
-    ok(cublasDtrsv(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, nb, Lii, n, x + i0, 1));
-    const int rest = n - i0 - nb;
-    if (rest > 0)
-      ok(cublasDgemv(h, CUBLAS_OP_N, rest, nb, &mone, Lii + nb, n, x + i0, 1, &one, x + i0 + nb, 1));
-  }
-  for (int i1 = n; i1 > 0; i1 -= NB) {  // backward: L^T z = y
-    const int i0 = std::max(0, i1 - NB);
-    const int nb = i1 - i0;
-    const double* Lii = L + static_cast<int64_t>(i0) * n + i0;
-    ok(cublasDtrsv(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, nb, Lii, n, x + i0, 1));
-    if (i0 > 0)  // x[0:i0] -= L[i0:i1, 0:i0]^T x[i0:i1]
-      ok(cublasDgemv(h, CUBLAS_OP_T, nb, i0, &mone, L + i0, n, x + i0, 1, &one, x, 1));
-  }
-  count_launch(4 * ((n + NB - 1) / NB));
-}
-}  // namespace fstk_gpu
 
 int32_t fstk_gpu_refit_apply(fstk_gpu_refit* rf, const double* s_dev, double* x_dev,
                              double* rel_step, fstk_gpu_error* err) {
