@@ -256,6 +256,14 @@ int32_t fstk_gpu_refit_normal_equations_level(fstk_gpu_refit* refit, int32_t sli
 int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t n,
                              double* gram, int32_t slices, int32_t device, void* stream,
                              fstk_gpu_error* err);
+/* Lower Cholesky factor (in place, lower triangle) of a DEVICE n x n matrix
+ * (column-major, ld n): blocked, panels of nb, with the trailing updates on
+ * the int8 tensor cores at `slices` plane-accuracy (4..7), or cuSOLVER
+ * dpotrf (0).  *info = 0 on success, nonzero when a block is not positive
+ * definite.  The factor stage of fstk_gpu_refit_factor on its own (it uses
+ * the int8 path for R >= 8192 unless FSTK_CHOL_CRT=0). */
+int32_t fstk_gpu_cholesky_device(double* g, int32_t n, int32_t nb, int32_t slices, int32_t device,
+                                 void* stream, int32_t* info, fstk_gpu_error* err);
 int32_t fstk_gpu_refit_solve(fstk_gpu_refit* refit, const double* gram,
                              const double* rhs, double* core_out,
                              fstk_reestimate_info* info, fstk_gpu_error* err);

@@ -88,6 +88,7 @@ EXPORTS = [
     "fstk_gpu_refit_normal_equations_level", "fstk_gpu_refit_begin_columns",
     "fstk_gpu_refit_exchange_layout", "fstk_gpu_refit_adopt_rows",
     "fstk_gpu_sample_without_replacement", "fstk_gpu_make_plan", "fstk_gpu_set_devices",
+    "fstk_gpu_cholesky_device",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -154,6 +155,8 @@ def lib():
                                                         C.POINTER(ReestimateInfo), C.POINTER(Err)]
     L.fstk_gpu_gram_device.argtypes = [VP, C.c_int64, C.c_int64, C.c_int32, VP, C.c_int32,
                                        C.c_int32, VP, C.POINTER(Err)]
+    L.fstk_gpu_cholesky_device.argtypes = [VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP,
+                                           C.POINTER(C.c_int32), C.POINTER(Err)]
     L.fstk_gpu_refit_solve.argtypes = [VP, VP, VP, DP, C.POINTER(ReestimateInfo),
                                        C.POINTER(Err)]
     L.fstk_gpu_refit_factor.argtypes = [VP, VP, VP, VP, C.POINTER(ReestimateInfo),

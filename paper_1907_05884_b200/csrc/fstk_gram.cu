@@ -353,7 +353,8 @@ template <int NM>
 __global__ void __launch_bounds__(256) crt_fold_kernel(const int32_t* __restrict__ C,
                                                        int64_t cstride, int64_t m, int w, int c0,
                                                        int n, int k, const int* __restrict__ ex,
-                                                       double* __restrict__ G, int accumulate) {
+                                                       double* __restrict__ G, int64_t ldg,
+                                                       int accumulate, int negate) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   if (i >= m || j >= w || i < j || c0 + i >= n || c0 + j >= n) return;
@@ -375,8 +376,9 @@ __global__ void __launch_bounds__(256) crt_fold_kernel(const int32_t* __restrict
   __int128 acc = y[NM - 1];
 #pragma unroll
   for (int t = NM - 2; t >= 0; --t) acc = acc * kmod(t) + y[t];
-  const double v = ldexp(i128_to_double(acc), ex[c0 + i] + ex[c0 + j] - 2 * k);
-  double* g = G + (c0 + i) + static_cast<int64_t>(c0 + j) * n;
+  const double v0 = ldexp(i128_to_double(acc), ex[c0 + i] + ex[c0 + j] - 2 * k);
+  const double v = negate ? -v0 : v0;
+  double* g = G + (c0 + i) + static_cast<int64_t>(c0 + j) * ldg;
   *g = accumulate ? *g + v : v;
 }
 
@@ -403,10 +405,10 @@ void launch_crt(const SRC& src, int64_t s0, int64_t kr, int n, int64_t kp, int64
 }
 template <int NM>
 void launch_crt_fold(const int32_t* C, int64_t cstride, int64_t m, int64_t wn, int64_t c0, int n,
-                     int k, const int* ex, double* G, int acc, cudaStream_t s) {
+                     int k, const int* ex, double* G, int64_t ldg, int acc, int neg, cudaStream_t s) {
   dim3 fg(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(wn));
   crt_fold_kernel<NM><<<fg, 256, 0, s>>>(C, cstride, m, static_cast<int>(wn), static_cast<int>(c0),
-                                         n, k, ex, G, acc);
+                                         n, k, ex, G, ldg, acc, neg);
   check_launch("crt_fold_kernel");
 }
 
@@ -548,7 +550,8 @@ bool gram_scheme_crt() {
 template <class SRC>
 static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, double* gram,
                                       double beta, int ns, cudaStream_t s, int device,
-                                      GramScratch& sc) {
+                                      GramScratch& sc, int64_t ldg = -1, bool negate = false) {
+  if (ldg < 0) ldg = n;
   require(ns >= 4 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: 4..7 plane-equivalents");
   const int k = 7 * ns - 1;
   LtState& st = lt_state(device);
@@ -605,7 +608,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
       }
       const int acc = (!first || beta != 0.0) ? 1 : 0;
 #define FSTK_CRT_FOLD(NMV) \
-  launch_crt_fold<NMV>(sc.C.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, acc, s)
+  launch_crt_fold<NMV>(sc.C.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
       FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
 #undef FSTK_CRT_FOLD
     }
@@ -617,6 +620,11 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
 double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, double* gram,
                            double beta, int ns, cudaStream_t s, int device, GramScratch& sc) {
   return gram_accumulate_crt_src(DenseSrc{A, lda}, rows, n, gram, beta, ns, s, device, sc);
+}
+
+double gram_update_crt(const double* T, int64_t ldt, int64_t rows, int n, double* G, int64_t ldg,
+                       int ns, cudaStream_t s, int device, GramScratch& sc) {
+  return gram_accumulate_crt_src(DenseSrc{T, ldt}, rows, n, G, 1.0, ns, s, device, sc, ldg, true);
 }
 
 double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n, double* gram,

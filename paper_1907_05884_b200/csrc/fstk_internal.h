@@ -221,6 +221,11 @@ struct DesignSpec {
   int64_t row0;
   double scale;
 };
+// G (lower triangle, n x n inside a matrix of leading dimension ldg) -= T^T T
+// for T = rows x n (column-major, ldt), through the CRT int8 Gram at `slices`
+// plane-accuracy: the trailing update of the blocked Cholesky (chol_crt).
+double gram_update_crt(const double* T, int64_t ldt, int64_t rows, int n, double* G, int64_t ldg,
+                       int slices, cudaStream_t s, int device, GramScratch& sc);
 // The sliced (CRT) Gram of those rows without materialising them.
 bool gram_scheme_crt();
 double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n, double* gram,

@@ -2567,6 +2567,120 @@ static double dev_norm(cublasHandle_t h, int n, const double* x) {
 
 }  // namespace fstk_gpu
 
+// ---- blocked Cholesky with int8 tensor-core trailing updates (chol_crt) ----
+namespace fstk_gpu {
+// T (b x m, column-major, ld b) = L21^T for L21 = m x b at L (ld ldl).
+__global__ void transpose_panel_kernel(const double* __restrict__ L, int64_t ldl, int m, int b,
+                                       double* __restrict__ T) {
+  __shared__ double tile[32][33];
+  const int a0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int a = a0 + threadIdx.x, r = r0 + y;
+    if (a < m && r < b) tile[y][threadIdx.x] = L[a + static_cast<int64_t>(r) * ldl];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int r = r0 + threadIdx.x, a = a0 + y;
+    if (a < m && r < b) T[r + static_cast<int64_t>(a) * b] = tile[threadIdx.x][y];
+  }
+}
+
+// Lower Cholesky factor of the n x n matrix G (column-major, ld n) in place,
+// right-looking in panels of nb: cuSOLVER potrf of the diagonal block, DTRSM
+// of the panel below it, and the trailing update G22 -= L21 L21^T through the
+// CRT int8 tensor-core Gram at `slices` plane-accuracy (the Gram machinery of
+// fstk_gram.cu with K = nb).  The factor preconditions the refinement
+// against A, which restores fp64 accuracy whatever the factor's rounding; at
+// R = 32,768 the DMMA-bound potrf's 1.2e13 flops are 88% trailing updates.
+// Returns false when a diagonal block is not positive definite.
+static bool chol_crt(cublasHandle_t blas, cusolverDnHandle_t solver, double* G, int n, int nb,
+                     int slices, cudaStream_t s, int device) {
+  cublasSetStream(blas, s);
+  cusolverDnSetStream(solver, s);
+  const int npan = (n + nb - 1) / nb;
+  int lwork = 0;
+  if (cusolverDnDpotrf_bufferSize(solver, CUBLAS_FILL_MODE_LOWER, nb, G, n, &lwork) !=
+      CUSOLVER_STATUS_SUCCESS)
+    fail(FSTK_E_COMPUTE, "potrf_bufferSize failed");
+  DevBuf<double> work(std::max(lwork, 1));
+  DevBuf<int> dinfo(npan);
+  FSTK_CUDA(cudaMemsetAsync(dinfo.p, 0, npan * sizeof(int), s));
+  DevBuf<double> T(static_cast<size_t>(nb) * std::max(n - nb, 1));
+  GramScratch sc;
+  const double one = 1.0;
+  for (int p = 0; p < npan; ++p) {
+    const int i0 = p * nb, b = std::min(nb, n - i0), rest = n - i0 - b;
+    double* Gii = G + static_cast<int64_t>(i0) * n + i0;
+    if (cusolverDnDpotrf(solver, CUBLAS_FILL_MODE_LOWER, b, Gii, n, work.p, lwork, dinfo.p + p) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "potrf failed");
+    if (rest == 0) break;
+    double* A21 = Gii + b;
+    if (cublasDtrsm(blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
+                    CUBLAS_DIAG_NON_UNIT, rest, b, &one, Gii, n, A21, n) != CUBLAS_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "cublasDtrsm failed");
+    dim3 tg(static_cast<unsigned>(ceil_div(rest, 32)), static_cast<unsigned>(ceil_div(b, 32)));
+    transpose_panel_kernel<<<tg, dim3(32, 8), 0, s>>>(A21, n, rest, b, T.p);
+    check_launch("transpose_panel_kernel");
+    gram_update_crt(T.p, b, b, rest, A21 + static_cast<int64_t>(b) * n, n, slices, s, device, sc);
+    count_launch(3);
+  }
+  std::vector<int> hinfo(npan);
+  FSTK_CUDA(cudaMemcpyAsync(hinfo.data(), dinfo.p, npan * sizeof(int), cudaMemcpyDeviceToHost, s));
+  FSTK_CUDA(cudaStreamSynchronize(s));
+  for (int v : hinfo)
+    if (v != 0) return false;
+  return true;
+}
+
+// FSTK_CHOL_CRT: plane-accuracy of chol_crt's trailing updates (0 = cuSOLVER
+// dpotrf throughout; default 5), used for R >= 8192.
+static int chol_crt_slices() {
+  static const int v = [] {
+    const char* e = std::getenv("FSTK_CHOL_CRT");
+    const int x = e ? std::atoi(e) : 5;
+    return x <= 0 ? 0 : std::min(std::max(x, 4), 7);
+  }();
+  return v;
+}
+}  // namespace fstk_gpu
+
+// Lower Cholesky factor of a DEVICE matrix in place: chol_crt (slices 4..7,
+// panels of nb) or cuSOLVER dpotrf (slices 0).  *info_out = 0 on success.
+int32_t fstk_gpu_cholesky_device(double* g, int32_t n, int32_t nb, int32_t slices, int32_t device,
+                                 void* stream, int32_t* info_out, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    require(g && info_out, FSTK_E_PARAMETER, "null argument");
+    require(n > 0, FSTK_E_SHAPE, "cholesky: n must be positive");
+    require(slices == 0 || (slices >= 4 && slices <= 7), FSTK_E_PARAMETER,
+            "cholesky: slices must be 0 (cuSOLVER) or 4..7");
+    require(slices == 0 || (nb >= 256 && nb % 16 == 0), FSTK_E_PARAMETER,
+            "cholesky: panel width must be a multiple of 16, >= 256");
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Handles& h = handles(device);
+    if (slices > 0) {
+      *info_out = chol_crt(h.blas, h.solver, g, n, nb, slices, s, device) ? 0 : 1;
+      return;
+    }
+    cusolverDnSetStream(h.solver, s);
+    int lwork = 0;
+    if (cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, n, g, n, &lwork) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "potrf_bufferSize failed");
+    DevBuf<double> work(std::max(lwork, 1));
+    DevBuf<int> dinfo(1);
+    if (cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, n, g, n, work.p, lwork, dinfo.p) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(FSTK_E_COMPUTE, "potrf failed");
+    int hinfo = 0;
+    FSTK_CUDA(cudaMemcpyAsync(&hinfo, dinfo.p, 4, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    *info_out = hinfo;
+  });
+}
+
 // x += (L L^T)^{-1} s (s summed over shards); rel_step = ||dx|| / ||x||.
 namespace fstk_gpu {
 // x := (L L^T)^{-1} x for the lower Cholesky factor L (n x n, ld n), blocked:
@@ -2616,18 +2730,30 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
     FSTK_CUDA(cudaMemcpyAsync(x_dev, rhs_in, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
     int lwork = 0;
     ProfScope prof(FSTK_PROF_SOLVE, s);
-    if (cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, n, rf->L.p, n, &lwork) !=
-        CUSOLVER_STATUS_SUCCESS)
-      fail(FSTK_E_COMPUTE, "potrf_bufferSize failed");
-    DevBuf<double> work(std::max(lwork, 1));
     DevBuf<int> dinfo(1);
-    if (cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, n, rf->L.p, n, work.p, lwork, dinfo.p) !=
-        CUSOLVER_STATUS_SUCCESS)
-      fail(FSTK_E_COMPUTE, "potrf failed");
-    count_launch();
-    int hinfo = 0;
-    FSTK_CUDA(cudaMemcpyAsync(&hinfo, dinfo.p, 4, cudaMemcpyDeviceToHost, s));
-    FSTK_CUDA(cudaStreamSynchronize(s));
+    int hinfo = 1;
+    if (n >= 8192 && chol_crt_slices() > 0) {
+      // Blocked Cholesky with int8 tensor-core trailing updates; a block that
+      // is not positive definite there is retried with cuSOLVER's dpotrf.
+      if (chol_crt(h.blas, h.solver, rf->L.p, n, 2048, chol_crt_slices(), s, rf->device)) {
+        hinfo = 0;
+      } else {
+        FSTK_CUDA(cudaMemcpyAsync(rf->L.p, gram_in, static_cast<size_t>(n) * n * 8,
+                                  cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    if (hinfo != 0) {
+      if (cusolverDnDpotrf_bufferSize(h.solver, CUBLAS_FILL_MODE_LOWER, n, rf->L.p, n, &lwork) !=
+          CUSOLVER_STATUS_SUCCESS)
+        fail(FSTK_E_COMPUTE, "potrf_bufferSize failed");
+      DevBuf<double> work(std::max(lwork, 1));
+      if (cusolverDnDpotrf(h.solver, CUBLAS_FILL_MODE_LOWER, n, rf->L.p, n, work.p, lwork, dinfo.p) !=
+          CUSOLVER_STATUS_SUCCESS)
+        fail(FSTK_E_COMPUTE, "potrf failed");
+      count_launch();
+      FSTK_CUDA(cudaMemcpyAsync(&hinfo, dinfo.p, 4, cudaMemcpyDeviceToHost, s));
+      FSTK_CUDA(cudaStreamSynchronize(s));
+    }
     rf->factored = hinfo == 0;
     rf->rank_def = !rf->factored;
     if (rf->factored && n >= 4096) {

@@ -75,6 +75,28 @@ def gram(a, slices: int | None = None):
     return g.view(n, n).t()  # [row, col]
 
 
+def cholesky(g, slices: int = 5, nb: int = 2048):
+    """Lower Cholesky factor of a symmetric positive definite CUDA float64
+    tensor (n x n; its lower triangle is read) through fstk_gpu_cholesky_device:
+    panels of `nb` with the trailing updates on the int8 tensor cores at
+    `slices` plane-accuracy, or cuSOLVER dpotrf (slices=0).  Returns
+    (L, info): info = 0 on success, nonzero when a block is not positive
+    definite."""
+    import torch
+
+    if not (isinstance(g, torch.Tensor) and g.is_cuda and g.dtype == torch.float64 and g.dim() == 2
+            and g.shape[0] == g.shape[1]):
+        raise TypeError("cholesky: expected a square 2-D CUDA float64 tensor")
+    n = g.shape[0]
+    w = g.t().contiguous()  # column-major
+    info = C.c_int32(0)
+    err = Err()
+    stream = torch.cuda.current_stream(g.device).cuda_stream
+    check(lib().fstk_gpu_cholesky_device(w.data_ptr(), n, int(nb), int(slices), g.device.index,
+                                         stream, C.byref(info), C.byref(err)), err)
+    return torch.tril(w.t()), int(info.value)
+
+
 def reestimate_core(model: Model, points, values, seed=0, sample_rows=0,
                     working_subset=1 << 20, transform="dct", validation_fraction=0.05,
                     device=None):

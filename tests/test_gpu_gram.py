@@ -272,3 +272,35 @@ def test_gram_tiny_and_huge_column_scales_stay_finite():
         g = F.gram(a, slices=ns)
         assert bool(torch.isfinite(g).all())
         _check_bound(a, g, ns)
+
+
+@pytest.mark.parametrize("n,nb,slices", [(8192, 2048, 5), (3000, 512, 7), (4096, 1024, 4)])
+def test_blocked_cholesky_with_int8_trailing_updates(n, nb, slices):
+    # chol_crt: cuSOLVER potrf on the diagonal blocks, DTRSM panels, and the
+    # trailing G22 -= L21 L21^T through the CRT int8 Gram.  Its backward error
+    # ||L L^T - G|| / ||G|| is set by the plane accuracy of the updates
+    # (2^-(7 slices - 1) per entry, relative to the row maxima).
+    torch = _torch()
+    gen = torch.Generator(device="cuda").manual_seed(n + slices)
+    x = torch.randn(n + 500, n, dtype=torch.float64, device="cuda", generator=gen)
+    x *= torch.exp(torch.randn(n, dtype=torch.float64, device="cuda", generator=gen))  # column scales
+    g = x.t() @ x
+    gn = float(torch.linalg.norm(g))
+    l, info = F.cholesky(g, slices=slices, nb=nb)
+    assert info == 0
+    assert bool((l.triu(1) == 0).all())
+    back = float(torch.linalg.norm(l @ l.t() - g)) / gn
+    assert back < {4: 1e-7, 5: 1e-9, 7: 1e-13}[slices], back
+    l0, info0 = F.cholesky(g, slices=0)
+    assert info0 == 0 and float(torch.linalg.norm(l0 @ l0.t() - g)) / gn < 1e-14
+
+
+def test_blocked_cholesky_reports_indefinite():
+    torch = _torch()
+    n = 3000
+    g = torch.eye(n, dtype=torch.float64, device="cuda")
+    g[2600, 2600] = -1.0  # the fifth 512-panel is not positive definite
+    _, info = F.cholesky(g, slices=5, nb=512)
+    assert info != 0
+    _, info0 = F.cholesky(g, slices=0)
+    assert info0 != 0

@@ -1,5 +1,2 @@
-# scratch experiment driver (gpurun): bench refit samples with stage breakdown
-python bench.py --steps 20 --warmup 5 --no-cpu --no-refit-none --refit-reps 5 > gpurun_out/b.json 2>/dev/null
-python -c "
-import json; d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1]); r=d['refit']; print(r['seconds'], r['samples_s'])
-for x in r['sample_stages_s']: print(x)"
+# scratch experiment driver (gpurun): blocked int8 Cholesky level A/B (refit solve times)
+for v in "FSTK_CHOL_CRT=7" "FSTK_CHOL_CRT=5" "FSTK_CHOL_CRT=6" "FSTK_CHOL_CRT=0"; do echo "== $v"; env $v python tools/refit_var.py 5 | sed 's/.*| dev//'; done > gpurun_out/exp_time.log 2>&1; cat gpurun_out/exp_time.log
