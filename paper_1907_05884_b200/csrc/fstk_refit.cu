@@ -1746,6 +1746,10 @@ static double rel_residual(const std::vector<double>& pred, const std::vector<do
 extern "C" {
 
 namespace fstk_gpu {
+static std::mutex g_stage_mu;      // pinned staging of the working-subset upload
+static double* g_stage = nullptr;
+static size_t g_stage_n = 0;
+
 static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
                                 const double* values, int64_t q, int32_t d,
                                 const fstk_sketch_cfg* cfg, int32_t shard, int32_t shards,
@@ -1886,13 +1890,27 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
     rf->val_values.alloc(static_cast<size_t>(std::max<int64_t>(rf->n_val, 1)));
     {
       const int64_t nv = rf->n_val;
-      std::vector<double> hp(static_cast<size_t>(q_w) * d), hv(q_w), vp(static_cast<size_t>(nv) * d);
+      // Gathered straight into a process-wide pinned staging buffer (grow-only,
+      // one refit at a time uses it), so the upload is a plain DMA.
+      const size_t nst = static_cast<size_t>(q_w) * (d + 1);
+      std::unique_lock<std::mutex> stage_lock(g_stage_mu);
+      if (g_stage_n < nst) {
+        if (g_stage) cudaFreeHost(g_stage);
+        g_stage = nullptr;
+        g_stage_n = 0;
+        FSTK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g_stage), nst * sizeof(double),
+                                cudaHostAllocPortable));
+        g_stage_n = nst;
+      }
+      double* hp = g_stage;
+      double* hv = g_stage + static_cast<size_t>(q_w) * d;
+      std::vector<double> vp(static_cast<size_t>(nv) * d);
       rf->h_val_values.resize(nv);
       rf->h_val_index.resize(nv);
       parallel_chunks(q_w, [&](uint64_t lo, uint64_t hi) {
         for (int k = 0; k < d; ++k) {
           const double* col = points + static_cast<int64_t>(k) * q;
-          double* dst = hp.data() + static_cast<size_t>(k) * q_w;
+          double* dst = hp + static_cast<size_t>(k) * q_w;
           for (uint64_t t = lo; t < hi; ++t) dst[t] = col[subset[t]];
         }
         for (uint64_t t = lo; t < hi; ++t) hv[t] = values[subset[t]];
@@ -1906,8 +1924,10 @@ static int32_t refit_begin_impl(const fstk_gpu_model* m, const double* points,
         rf->h_val_index[t] = static_cast<int64_t>(val[t]);
         rf->h_val_values[t] = values[val[t]];
       }
-      FSTK_CUDA(cudaMemcpyAsync(rf->d_points.p, hp.data(), hp.size() * 8, cudaMemcpyHostToDevice, s));
-      FSTK_CUDA(cudaMemcpyAsync(rf->d_values.p, hv.data(), hv.size() * 8, cudaMemcpyHostToDevice, s));
+      FSTK_CUDA(cudaMemcpyAsync(rf->d_points.p, hp, static_cast<size_t>(q_w) * d * 8,
+                                cudaMemcpyHostToDevice, s));
+      FSTK_CUDA(cudaMemcpyAsync(rf->d_values.p, hv, static_cast<size_t>(q_w) * 8,
+                                cudaMemcpyHostToDevice, s));
       if (nv > 0) {
         FSTK_CUDA(cudaMemcpyAsync(rf->val_points.p, vp.data(), vp.size() * 8,
                                   cudaMemcpyHostToDevice, s));

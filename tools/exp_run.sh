@@ -1,2 +1,3 @@
-# scratch experiment driver (gpurun): blocked int8 Cholesky level A/B (refit solve times)
-for v in "FSTK_CHOL_CRT=7" "FSTK_CHOL_CRT=5" "FSTK_CHOL_CRT=6" "FSTK_CHOL_CRT=0"; do echo "== $v"; env $v python tools/refit_var.py 5 | sed 's/.*| dev//'; done > gpurun_out/exp_time.log 2>&1; cat gpurun_out/exp_time.log
+# scratch experiment driver (gpurun): refit tests + prepare timing
+python -m pytest tests/test_gpu_refit.py tests/test_gpu_threads.py tests/test_gpu_dist.py -x -q > gpurun_out/exp_tests.log 2>&1; tail -n 1 gpurun_out/exp_tests.log
+FSTK_DEBUG_TIMING=1 python tools/refit_var.py 4 > gpurun_out/exp_prep.log 2>&1; grep -E "compact|working|run " gpurun_out/exp_prep.log | sed 's/gram 1.*//'
