@@ -2755,7 +2755,13 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
     if (n >= 8192 && chol_crt_slices() > 0) {
       // Blocked Cholesky with int8 tensor-core trailing updates; a block that
       // is not positive definite there is retried with cuSOLVER's dpotrf.
-      if (chol_crt(h.blas, h.solver, rf->L.p, n, 2048, chol_crt_slices(), s, rf->device)) {
+      static const bool dbg = std::getenv("FSTK_DEBUG_TIMING") != nullptr;
+      const auto tc0 = std::chrono::steady_clock::now();
+      const bool chol_ok = chol_crt(h.blas, h.solver, rf->L.p, n, 2048, chol_crt_slices(), s, rf->device);
+      if (dbg)
+        std::fprintf(stderr, "fstk factor: chol_crt %8.2f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count());
+      if (chol_ok) {
         hinfo = 0;
       } else {
         FSTK_CUDA(cudaMemcpyAsync(rf->L.p, gram_in, static_cast<size_t>(n) * n * 8,
