@@ -817,6 +817,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
   double2* tws = reinterpret_cast<double2*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* X = tws + kWp1Tw + warp * kWp1Buf;
+  double* Xr = reinterpret_cast<double*>(X);  // real inputs, rows of 33 doubles
   for (int i = threadIdx.x; i < kWp1Tw; i += blockDim.x) tws[i] = P.tw[31 + i];
   __syncthreads();
   const int64_t units = static_cast<int64_t>(P.ncols) * P.nblk;
@@ -857,25 +858,23 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
             v1 = xmul(v1, t[k][j].y);
           }
           const int e = 64 * (8 * h + j) + 2 * lane;
-          X[e + (e >> 5)] = make_double2(v0, 0.0);
-          X[e + 1 + (e >> 5)] = make_double2(v1, 0.0);
+          Xr[e + (e >> 5)] = v0;
+          Xr[e + 1 + (e >> 5)] = v1;
         }
       }
     } else {
       for (int e = lane; e < 1024; e += 32) {
         const int64_t p = base + e;
         const int64_t src = P.row_src[p];
-        X[e + (e >> 5)] = make_double2(src < 0 ? 0.0 : xmul(P.sgn[p], P.rhs[src]), 0.0);
+        Xr[e + (e >> 5)] = src < 0 ? 0.0 : xmul(P.sgn[p], P.rhs[src]);
       }
     }
     __syncwarp();
     double2 v[32];
-#pragma unroll
-    for (int b = 0; b < 32; ++b) v[b] = X[lane * kWp1Row + b];
-    // ---- stage 0 (len 2, twiddle (1, 0)): real inputs
+    // ---- stage 0 (len 2, twiddle (1, 0)): real inputs, staged as doubles
 #pragma unroll
     for (int b = 0; b < 32; b += 2) {
-      const double a0 = v[b].x, a1 = v[b + 1].x;
+      const double a0 = Xr[lane * kWp1Row + b], a1 = Xr[lane * kWp1Row + b + 1];
       v[b] = make_double2(xadd(a0, a1), 0.0);
       v[b + 1] = make_double2(xsub(a0, a1), 0.0);
     }
