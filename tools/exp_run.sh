@@ -1,5 +1,4 @@
-# scratch experiment driver (gpurun): parity subset + sketch timing
-K="sketch_rows or three_pass or c1_refit or 1m"
-python -m pytest tests/test_gpu_refit.py tests/test_gpu_columns.py -x -q -k "$K" > gpurun_out/exp_tests.log 2>&1; tail -n 1 gpurun_out/exp_tests.log
-python tools/sketch_time.py 5 > gpurun_out/exp_time.log 2>&1; cat gpurun_out/exp_time.log
-ncu --set full --clock-control none -k regex:"warp_pass1" -s 2 -c 1 -o gpurun_out/wp1r python tools/sketch_time.py 1 > /dev/null 2>&1
+# scratch experiment driver (gpurun): parity + sketch timing A/B (pass-1 register twiddles, 8 warps)
+K="sketch_rows or three_pass or 1m"
+FSTK_SKETCH_WARP=8 FSTK_SKETCH_W1RT=1 python -m pytest tests/test_gpu_refit.py -x -q -k "$K" > gpurun_out/exp_tests.log 2>&1; tail -n 1 gpurun_out/exp_tests.log
+for r in 1 2; do for v in "FSTK_SKETCH_WARP=8 FSTK_SKETCH_W1RT=1" "FSTK_SKETCH_WARP=12" "FSTK_SKETCH_WARP=8"; do echo "== $v"; env $v python tools/sketch_time.py 3; done; done > gpurun_out/exp_time.log 2>&1; cat gpurun_out/exp_time.log
