@@ -2756,7 +2756,15 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
       // is not positive definite there is retried with cuSOLVER's dpotrf.
       static const bool dbg = std::getenv("FSTK_DEBUG_TIMING") != nullptr;
       const auto tc0 = std::chrono::steady_clock::now();
-      const bool chol_ok = chol_crt(h.blas, h.solver, rf->L.p, n, 2048, chol_crt_slices(), s, rf->device);
+      bool chol_ok = false;
+      try {
+        chol_ok = chol_crt(h.blas, h.solver, rf->L.p, n, 2048, chol_crt_slices(), s, rf->device);
+      } catch (const Error& e) {
+        // e.g. no room for the int8 scratch next to a large sketch: dpotrf needs none.
+        if (e.code != FSTK_E_COMPUTE) throw;
+        cudaGetLastError();
+        FSTK_CUDA(cudaStreamSynchronize(s));
+      }
       if (dbg)
         std::fprintf(stderr, "fstk factor: chol_crt %8.2f ms\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count());
