@@ -255,10 +255,10 @@ void imma_tn(LtState& st, DevBuf<uint8_t>& ws, int64_t M, int64_t N, int64_t K, 
 // column-max-relative accuracy as ns digit planes, with no dropped terms).
 // Its symmetric residues modulo pairwise-coprime m_i <= 255 are int8, and
 // C_i = R_i^T R_i (one int8 GEMM per modulus, K = segment rows, exact in
-// int32) is sum_s x_a x_b mod m_i.  Garner's algorithm rebuilds the exact
-// integer sum in 128-bit arithmetic (|sum| < M/4, M = prod m_i), which is
-// converted to fp64 once (exact whenever representable) and scaled by
-// 2^(e_a + e_b - 2k).  At ns = 5 that is 11 GEMMs of K rows instead of the
+// int32) is sum_s x_a x_b mod m_i.  Garner's algorithm (one reduction per
+// digit) rebuilds the exact integer sum in 128-bit arithmetic (|sum| < M/4,
+// M = prod m_i), which is converted to fp64 once (exact whenever
+// representable) and scaled by 2^(e_a + e_b - 2k).  At ns = 5 that is 11 GEMMs of K rows instead of the
 // digit scheme's 15; at ns = 7, 15 instead of 28.
 // Pairwise coprime moduli <= 255 (residues fit int8 in symmetric form).
 __host__ __device__ constexpr int kmod(int i) {
@@ -275,6 +275,7 @@ constexpr int cx_inv(int a, int m) {  // a^-1 mod m (gcd(a, m) = 1)
 struct CrtTables {
   int pmod[kMaxModuli][kMaxModuli];  // (prod_{l<j} m_l) mod m_i, j < i
   int inv[kMaxModuli];               // (prod_{l<i} m_l)^-1 mod m_i
+  int q[kMaxModuli][kMaxModuli];     // pmod[l][i] inv[i] mod m_i (Garner, one reduction per digit)
 };
 constexpr CrtTables make_crt_tables() {
   CrtTables t{};
@@ -285,6 +286,8 @@ constexpr CrtTables make_crt_tables() {
       if (j < i) p = (p * kmod(j)) % kmod(i);
     }
     t.inv[i] = i == 0 ? 1 : cx_inv(static_cast<int>(p % kmod(i)), kmod(i));
+    for (int j = 0; j < kMaxModuli; ++j)
+      t.q[j][i] = static_cast<int>((static_cast<long long>(t.pmod[j][i]) * t.inv[i]) % kmod(i));
   }
   return t;
 }
@@ -362,21 +365,22 @@ __global__ void __launch_bounds__(256) crt_fold_kernel(const int32_t* __restrict
   int y[NM];  // symmetric mixed-radix digits (Garner)
 #pragma unroll
   for (int t = 0; t < NM; ++t) {
+    // y_t = (C_t - sum_{l<t} y_l P_{l,t}) P_t^-1 mod m_t, as one reduction of
+    // c' inv_t - sum_{l<t} y_l q_{l,t} (|.| < 2^19: no overflow).
     const int mt = kmod(t);
-    int v = __ldg(c + static_cast<int64_t>(t) * cstride) % mt;  // |C| < 2^31
-    int s = 0;
+    int a = (__ldg(c + static_cast<int64_t>(t) * cstride) % mt) * c_crt.inv[t];  // |C| < 2^31
 #pragma unroll
-    for (int l = 0; l < t; ++l) s += y[l] * c_crt.pmod[l][t];
-    v = (v - s % mt) % mt;
+    for (int l = 0; l < t; ++l) a -= y[l] * c_crt.q[l][t];
+    int v = a % mt;
     if (v < 0) v += mt;
-    v = (v * c_crt.inv[t]) % mt;
     if (v > mt / 2) v -= mt;
     y[t] = v;
   }
   __int128 acc = y[NM - 1];
 #pragma unroll
   for (int t = NM - 2; t >= 0; --t) acc = acc * kmod(t) + y[t];
-  const double v0 = ldexp(i128_to_double(acc), ex[c0 + i] + ex[c0 + j] - 2 * k);
+  const double accd = i128_to_double(acc);
+  const double v0 = ldexp(accd, ex[c0 + i] + ex[c0 + j] - 2 * k);
   const double v = negate ? -v0 : v0;
   double* g = G + (c0 + i) + static_cast<int64_t>(c0 + j) * ldg;
   *g = accumulate ? *g + v : v;
