@@ -507,8 +507,8 @@ def gram_roofline(gram_flops, info, t, peak_fp64):
         return {"bound": "tensor", "achieved": ach, "peak": 4500.0, "unit": "TOP/s (int8)",
                 "frac": ach / 4500.0, "peak_source": "nominal B200 dense int8 (= the fp8 rate in B200_PROFILING.md); cuBLASLt int8 TN measured 2.84 POPS here (profiles/int8_probe_r01.txt)",
                 "fp64_equivalent_tflops": gram_flops / t / 1e12, "fp64_peak_tflops": peak_fp64,
-                "kernel": f"cuBLASLt int8 IMMA over {info['gram_slices']} exact digit planes "
-                          "(slice/fold kernels in fstk_gram.cu)"}
+                "kernel": f"cuBLASLt int8 IMMA GEMMs, one per CRT modulus, at plane-accuracy level "
+                          f"{info['gram_slices']} (residue/fold kernels in fstk_gram.cu)"}
     ach = gram_flops / t / 1e12
     return {"bound": "tensor", "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s",
             "frac": ach / peak_fp64 if peak_fp64 else None,
@@ -619,7 +619,9 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=No
             "sketch_roofline": sketch_roofline(model, info, tm["sketch_s"], tform, world),
             "residual_before": info["residual_before"], "residual_after": info["residual_after"],
             "rank_deficient": info["rank_deficient"],
-            "note": "solve (cuSOLVER Cholesky) is outside the hot-path claim (north_star)"}
+            "note": "solve (blocked Cholesky: cuSOLVER diagonal blocks, DTRSM panels, int8 "
+                    "tensor-core trailing updates; then refinement against A) is outside the "
+                    "hot-path claim (north_star)"}
 
 
 if __name__ == "__main__":
