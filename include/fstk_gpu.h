@@ -114,6 +114,11 @@ int32_t fstk_gpu_abi_version(void);
 int32_t fstk_gpu_device_count(void);
 /* Kernel launches issued by this process so far (evidence counter). */
 uint64_t fstk_gpu_launch_count(void);
+/* Returns the library's cached device blocks (>= 256 MB, kept after release
+ * for the next refit session of the same size; see fstk_common.cuh) to the
+ * driver: one device, or all when device < 0.  Returns the bytes released.
+ * No reference counterpart (the reference has no device memory). */
+uint64_t fstk_gpu_trim_device_cache(int32_t device);
 
 /* Builds the device-resident model.  Validates like the reference ctor
  * (model.cpp:22-53): Shape on count/domain mismatch, Parameter on invalid

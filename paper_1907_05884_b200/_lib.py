@@ -74,6 +74,7 @@ class ReestimateInfo(C.Structure):
 # Every symbol include/fstk_gpu.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "fstk_gpu_abi_version", "fstk_gpu_device_count", "fstk_gpu_launch_count",
+    "fstk_gpu_trim_device_cache",
     "fstk_gpu_model_create", "fstk_gpu_model_destroy", "fstk_gpu_model_set_core",
     "fstk_gpu_model_get_core", "fstk_gpu_evaluate_batch", "fstk_gpu_evaluate",
     "fstk_gpu_evaluate_batch_device", "fstk_gpu_mode_values", "fstk_gpu_build_design_rows",
@@ -109,6 +110,8 @@ def lib():
     L.fstk_gpu_abi_version.restype = C.c_int32
     L.fstk_gpu_device_count.restype = C.c_int32
     L.fstk_gpu_launch_count.restype = C.c_uint64
+    L.fstk_gpu_trim_device_cache.argtypes = [C.c_int32]
+    L.fstk_gpu_trim_device_cache.restype = C.c_uint64
     L.fstk_gpu_model_create.argtypes = [C.POINTER(ModelDesc), C.c_int32, C.POINTER(VP),
                                         C.POINTER(Err)]
     L.fstk_gpu_model_destroy.argtypes = [VP]
@@ -197,6 +200,12 @@ def dptr(a):
 
 def launch_count() -> int:
     return int(lib().fstk_gpu_launch_count())
+
+
+def trim_device_cache(device: int = -1) -> int:
+    """Hand the library's cached large device blocks back to the driver
+    (bytes released).  Refit sessions reuse them otherwise."""
+    return int(lib().fstk_gpu_trim_device_cache(device))
 
 
 def device_count() -> int:

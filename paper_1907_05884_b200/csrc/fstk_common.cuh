@@ -5,6 +5,9 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -96,24 +99,150 @@ struct DeviceGuard {
   }
 };
 
+// ------------------------------------------------ large-block device cache ---
+// Refit sessions allocate ~80 GB at C2 (A alone is 68.7 GB) and used to hand
+// it back to the driver on close.  Re-mapping that much memory every session
+// left some refits' HBM-bound stages (sketch, blocked Cholesky) up to 1.8x
+// slower at full SM clocks (tools/refit_clocks.py).  Blocks of >= 256 MB are
+// therefore kept per device after release and reused by the next request of
+// the same size class (<= 1/8 larger), up to half of the device's memory
+// (least recently released blocks are freed first).
+// A failed cudaMalloc first returns every cached block to the driver and
+// retries; fstk_gpu_trim_device_cache() does the same on demand.
+// FSTK_DEVICE_CACHE=0 disables caching.
+struct CachedBlock {
+  void* p;
+  size_t bytes;
+  int device;
+};
+struct DeviceCache {
+  std::mutex mu;
+  std::vector<CachedBlock> free_blocks;
+  size_t cached = 0;
+};
+inline DeviceCache& device_cache() {
+  static DeviceCache* c = new DeviceCache();  // leaked: no teardown-order hazards at exit
+  return *c;
+}
+constexpr size_t kCacheMinBytes = size_t(256) << 20;
+inline bool device_cache_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FSTK_DEVICE_CACHE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// Frees the cached blocks of `device` (all devices when < 0).
+inline void device_cache_trim(int device) {
+  DeviceCache& c = device_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  int prev = -1;
+  cudaGetDevice(&prev);
+  for (size_t i = 0; i < c.free_blocks.size();) {
+    CachedBlock& b = c.free_blocks[i];
+    if (device >= 0 && b.device != device) {
+      ++i;
+      continue;
+    }
+    cudaSetDevice(b.device);
+    cudaFree(b.p);
+    c.cached -= b.bytes;
+    c.free_blocks.erase(c.free_blocks.begin() + i);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+}
+inline cudaError_t device_alloc(void** p, size_t bytes, size_t* got) {
+  *got = bytes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (bytes >= kCacheMinBytes && device_cache_enabled()) {
+    DeviceCache& c = device_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    int best = -1;
+    for (size_t i = 0; i < c.free_blocks.size(); ++i) {
+      const CachedBlock& b = c.free_blocks[i];
+      if (b.device == dev && b.bytes >= bytes && b.bytes - bytes <= bytes / 8 &&
+          (best < 0 || b.bytes < c.free_blocks[best].bytes))
+        best = static_cast<int>(i);
+    }
+    if (best >= 0) {
+      *p = c.free_blocks[best].p;
+      *got = c.free_blocks[best].bytes;
+      c.cached -= c.free_blocks[best].bytes;
+      c.free_blocks.erase(c.free_blocks.begin() + best);  // keep release order (oldest first)
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    device_cache_trim(dev);
+    e = cudaMalloc(p, bytes);
+  }
+  return e;
+}
+inline void device_free(void* p, size_t bytes) {
+  if (!p) return;
+  cudaPointerAttributes at{};
+  if (bytes >= kCacheMinBytes && device_cache_enabled() &&
+      cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != at.device) cudaSetDevice(at.device);
+    size_t total = 0, freeb = 0;
+    cudaMemGetInfo(&freeb, &total);
+    DeviceCache& c = device_cache();
+    std::unique_lock<std::mutex> lk(c.mu);
+    const bool keep = bytes <= total / 2;
+    if (keep) {
+      // cudaFree would have synchronised the device; a cached block must
+      // likewise be idle before the next owner's stream touches it.
+      cudaDeviceSynchronize();
+      // Least recently released blocks go first, so the latest session's
+      // working set is what stays cached.
+      size_t on_dev = 0;
+      for (const CachedBlock& b : c.free_blocks)
+        if (b.device == at.device) on_dev += b.bytes;
+      for (size_t i = 0; on_dev + bytes > total / 2 && i < c.free_blocks.size();) {
+        if (c.free_blocks[i].device != at.device) {
+          ++i;
+          continue;
+        }
+        cudaFree(c.free_blocks[i].p);
+        on_dev -= c.free_blocks[i].bytes;
+        c.cached -= c.free_blocks[i].bytes;
+        c.free_blocks.erase(c.free_blocks.begin() + i);
+      }
+      c.free_blocks.push_back({p, bytes, at.device});
+      c.cached += bytes;
+    }
+    lk.unlock();
+    if (prev >= 0 && prev != at.device) cudaSetDevice(prev);
+    if (keep) return;
+  }
+  cudaGetLastError();
+  cudaFree(p);
+}
+
 // RAII device buffer.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t bytes = 0;  // of the block actually held (a cached block may be larger)
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), bytes(o.bytes) { o.p = nullptr; o.n = 0; o.bytes = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; bytes = o.bytes; o.p = nullptr; o.n = 0; o.bytes = 0; }
     return *this;
   }
   void alloc(size_t count) {
     release();
     if (count == 0) return;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    cudaError_t e = device_alloc(reinterpret_cast<void**>(&p), count * sizeof(T), &bytes);
     if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();
@@ -126,9 +255,10 @@ struct DevBuf {
     if (count > n) alloc(count);
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) device_free(p, bytes);
     p = nullptr;
     n = 0;
+    bytes = 0;
   }
   ~DevBuf() { release(); }
 };

@@ -1428,6 +1428,18 @@ int32_t fstk_gpu_device_count(void) {
 
 uint64_t fstk_gpu_launch_count(void) { return g_launches.load(); }
 
+uint64_t fstk_gpu_trim_device_cache(int32_t device) {
+  DeviceCache& c = device_cache();
+  size_t before;
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    before = c.cached;
+  }
+  device_cache_trim(device);
+  std::lock_guard<std::mutex> lk(c.mu);
+  return before - c.cached;
+}
+
 namespace fstk_gpu {
 static void rethrow_stage_code(int32_t c, const fstk_gpu_error* err) {
   if (!c) return;

@@ -31,3 +31,14 @@ def rel(a, b):
     b = np.asarray(b, dtype=np.float64).ravel()
     nb = np.linalg.norm(b)
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _trim_library_device_cache():
+    """The library keeps large device blocks between refit sessions; hand
+    them back after each module so torch allocations in later modules (and
+    their memory-size assumptions) see a clean device."""
+    yield
+    mod = sys.modules.get("paper_1907_05884_b200._lib")
+    if mod is not None and getattr(mod, "_LIB", None) is not None:
+        mod.trim_device_cache(-1)

@@ -351,3 +351,21 @@ def test_two_pass_1m_order4_and_wht_bitexact(O, t, ranks):
     assert np.array_equal(sess.rows(), rows_o)
     assert np.array_equal(a, ao) and np.array_equal(b, bo)
     sess.close()
+
+
+def test_cached_device_blocks_reused_bit_identically():
+    # A sketched system >= 256 MB (S x R = 131,072 x 512 fp64) goes through
+    # the library's large-block cache: the second refit reuses the first's
+    # blocks and must return the same core bit for bit; trimming hands them back.
+    from paper_1907_05884_b200 import _lib
+
+    _lib.trim_device_cache(-1)
+    m = synth.random_model((8, 8, 8), (8, 8, 8), 5, seed=51)
+    pts = synth.uniform_points(400_000, 3, seed=52)
+    vals = m.evaluate_batch(pts) + 1e-3 * np.random.default_rng(53).normal(size=400_000)
+    a, ia = F.reestimate_core(m, pts, vals, seed=54, sample_rows=131_072)
+    b, ib = F.reestimate_core(m, pts, vals, seed=54, sample_rows=131_072)
+    assert np.array_equal(a.core, b.core)
+    assert ia["residual_after"] == ib["residual_after"]
+    assert _lib.trim_device_cache(-1) >= 256 << 20
+    assert _lib.trim_device_cache(-1) == 0
