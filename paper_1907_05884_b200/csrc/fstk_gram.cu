@@ -321,6 +321,34 @@ __global__ void residue_kernel(const SRC src, int64_t s0, int64_t rows, int n, i
   const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   if (r0 >= kp) return;
   const Pow2Scale sc(k - ex[a]);
+  int8_t* dst = X + static_cast<int64_t>(a) * kp + r0;
+  if constexpr (X32) {
+    // |x| <= 2^30: 32-bit conversion, and each residue as an unsigned
+    // remainder of x + (a multiple of m above 2^30) -- no signed-division
+    // fix-ups.  Same symmetric residues as sym_mod.
+    int x[4] = {0, 0, 0, 0};
+    if (a < n) {
+      const auto col = src.col(a);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r0 + u < rows) x[u] = __double2int_rn(sc(col(s0 + r0 + u)));
+    }
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      const unsigned m = static_cast<unsigned>(kmod(i));
+      const unsigned off = ((1u << 30) / m + 1u) * m;
+      signed char r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int v = static_cast<int>((static_cast<unsigned>(x[u]) + off) % m);
+        if (v > static_cast<int>(m / 2)) v -= static_cast<int>(m);
+        r[u] = static_cast<signed char>(v);
+      }
+      *reinterpret_cast<char4*>(dst + static_cast<int64_t>(i) * kp * np) =
+          make_char4(r[0], r[1], r[2], r[3]);
+    }
+    return;
+  }
   long long x[4] = {0ll, 0ll, 0ll, 0ll};
   if (a < n) {
     const auto col = src.col(a);
@@ -328,7 +356,6 @@ __global__ void residue_kernel(const SRC src, int64_t s0, int64_t rows, int n, i
     for (int u = 0; u < 4; ++u)
       if (r0 + u < rows) x[u] = __double2ll_rn(sc(col(s0 + r0 + u)));
   }
-  int8_t* dst = X + static_cast<int64_t>(a) * kp + r0;
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const char4 c = make_char4(static_cast<signed char>(sym_mod<X32>(x[0], kmod(i))),
