@@ -544,7 +544,9 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=No
             exchange_columns(sess)
             t_x = time.perf_counter() - tx
         t_b = time.perf_counter() - t0
-        gram = torch.empty(R * R, dtype=torch.float64, device=dev)
+        from paper_1907_05884_b200 import _lib as L
+
+        gram = L.device_tensor(R * R, dev)
         rhs = torch.empty(R, dtype=torch.float64, device=dev)
         tn = time.perf_counter()
         sess.normal_equations(gram, rhs)

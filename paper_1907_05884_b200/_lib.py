@@ -208,6 +208,21 @@ def trim_device_cache(device: int = -1) -> int:
     return int(lib().fstk_gpu_trim_device_cache(device))
 
 
+def device_tensor(n: int, device, zero: bool = False):
+    """A float64 CUDA tensor of n elements for Gram-sized buffers.  On a torch
+    out-of-memory error the library's cached device blocks are handed back and
+    the allocation is retried once (torch's allocator does not know about them)."""
+    import torch
+
+    make = torch.zeros if zero else torch.empty
+    try:
+        return make(n, dtype=torch.float64, device=device)
+    except torch.OutOfMemoryError:
+        d = torch.device(device)
+        trim_device_cache(d.index if d.index is not None else torch.cuda.current_device())
+        return make(n, dtype=torch.float64, device=device)
+
+
 def device_count() -> int:
     return int(lib().fstk_gpu_device_count())
 

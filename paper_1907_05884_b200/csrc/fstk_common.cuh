@@ -105,10 +105,10 @@ struct DeviceGuard {
 // left some refits' HBM-bound stages (sketch, blocked Cholesky) up to 1.8x
 // slower at full SM clocks (tools/refit_clocks.py).  Blocks of >= 256 MB are
 // therefore kept per device after release and reused by the next request of
-// the same size class (<= 1/8 larger), up to half of the device's memory
-// (least recently released blocks are freed first).
-// A failed cudaMalloc first returns every cached block to the driver and
-// retries; fstk_gpu_trim_device_cache() does the same on demand.
+// the same size class (<= 1/8 larger), up to 3/4 of the device's memory
+// (least recently released blocks are freed first; C2's ~97 GB session fits).
+// A failed cudaMalloc returns cached blocks, oldest first, until the request
+// fits; fstk_gpu_trim_device_cache() returns all of them on demand.
 // FSTK_DEVICE_CACHE=0 disables caching.
 struct CachedBlock {
   void* p;
@@ -173,12 +173,49 @@ inline cudaError_t device_alloc(void** p, size_t bytes, size_t* got) {
       return cudaSuccess;
     }
   }
-  cudaError_t e = cudaMalloc(p, bytes);
-  if (e == cudaErrorMemoryAllocation) {
+  if (bytes >= kCacheMinBytes && device_cache_enabled()) {
+    // A block beyond the cache's cap (C4's 137 GB sketch) means this
+    // session's working set cannot stay cached: return everything now, once,
+    // rather than evicting block by block inside the timed stages later.
+    size_t fb = 0, tb = 0;
+    if (cudaMemGetInfo(&fb, &tb) == cudaSuccess && bytes > tb / 4 * 3) device_cache_trim(dev);
     cudaGetLastError();
-    device_cache_trim(dev);
+  }
+  cudaError_t e = cudaMalloc(p, bytes);
+  // Out of memory: return cached blocks of this device to the driver, least
+  // recently released first, one at a time until the request fits.
+  while (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    bool freed = false;
+    {
+      DeviceCache& c = device_cache();
+      std::lock_guard<std::mutex> lk(c.mu);
+      for (size_t i = 0; i < c.free_blocks.size(); ++i) {
+        if (c.free_blocks[i].device != dev) continue;
+        cudaFree(c.free_blocks[i].p);
+        c.cached -= c.free_blocks[i].bytes;
+        c.free_blocks.erase(c.free_blocks.begin() + i);
+        freed = true;
+        break;
+      }
+    }
+    if (!freed) break;
     e = cudaMalloc(p, bytes);
   }
+  return e;
+}
+// cudaMemGetInfo for sizing decisions: the current device's cached blocks
+// count as free (an allocation that needs them trims the cache and retries),
+// so cached memory never shrinks a later session's segment or batch sizes.
+inline cudaError_t device_mem_info(size_t* free_b, size_t* total_b) {
+  const cudaError_t e = cudaMemGetInfo(free_b, total_b);
+  if (e != cudaSuccess) return e;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DeviceCache& c = device_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  for (const CachedBlock& b : c.free_blocks)
+    if (b.device == dev) *free_b += b.bytes;
   return e;
 }
 inline void device_free(void* p, size_t bytes) {
@@ -193,7 +230,8 @@ inline void device_free(void* p, size_t bytes) {
     cudaMemGetInfo(&freeb, &total);
     DeviceCache& c = device_cache();
     std::unique_lock<std::mutex> lk(c.mu);
-    const bool keep = bytes <= total / 2;
+    const size_t cap = total / 4 * 3;
+    const bool keep = bytes <= cap;
     if (keep) {
       // cudaFree would have synchronised the device; a cached block must
       // likewise be idle before the next owner's stream touches it.
@@ -203,7 +241,7 @@ inline void device_free(void* p, size_t bytes) {
       size_t on_dev = 0;
       for (const CachedBlock& b : c.free_blocks)
         if (b.device == at.device) on_dev += b.bytes;
-      for (size_t i = 0; on_dev + bytes > total / 2 && i < c.free_blocks.size();) {
+      for (size_t i = 0; on_dev + bytes > cap && i < c.free_blocks.size();) {
         if (c.free_blocks[i].device != at.device) {
           ++i;
           continue;

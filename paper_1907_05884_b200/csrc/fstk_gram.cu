@@ -514,7 +514,7 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
   int64_t kmax = ((int64_t(1) << 31) - 1) / (int64_t(kDigitMax) * kDigitMax * kMaxSlices);
   kmax = std::min<int64_t>(kmax, 65536);
   size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+  if (device_mem_info(&free_b, &total_b) != cudaSuccess) {
     cudaGetLastError();
     free_b = size_t(24) << 30;
   }
@@ -592,20 +592,24 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
     return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(32768);
   }();
   // int32-exact: K * 127^2 < 2^31; residue planes within a third of free
-  // memory (<= 24 GB); fixed for the scratch's lifetime like the digit scheme.
+  // memory (<= 24 GB).
   int64_t kmax = std::min<int64_t>(seg_cap, ((int64_t(1) << 31) - 1) / (127 * 127));
   size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+  if (device_mem_info(&free_b, &total_b) != cudaSuccess) {
     cudaGetLastError();
     free_b = size_t(24) << 30;
   }
-  const int nm_max = crt_moduli(7 * 7 - 1, kmax);
+  // Sized per call for this call's modulus count (an escalation to a higher
+  // level re-sizes; the CRT sums are exact per segment, so the segment length
+  // does not change what a call computes beyond fp64 accumulation order).
+  // Sizing for the level-7 count on every call shrank C4's segments to ~20k
+  // rows next to its 137 GB sketch (Gram 2.8 s instead of 2.3 s).
+  const int nm_need = crt_moduli(k, kmax);
   const int64_t have = static_cast<int64_t>(sc.X.n);
   const int64_t budget = std::min<int64_t>(int64_t(24) << 30, (static_cast<int64_t>(free_b) + have) / 3);
-  kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, budget / (nm_max * np)));
+  kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, budget / (nm_need * np)));
   kmax &= ~int64_t(15);
-  if (sc.kp == 0) sc.kp = kmax;
-  const int64_t kp = std::min<int64_t>(sc.kp, round_up(rows, 16));
+  const int64_t kp = std::min<int64_t>(kmax, round_up(rows, 16));
   const int nm = crt_moduli(k, kp);
   require(nm >= 8 && nm <= 17, FSTK_E_COMPUTE, "internal: CRT modulus count out of range");
   static const int64_t block_cap = [] {

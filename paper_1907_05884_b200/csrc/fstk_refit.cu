@@ -1231,7 +1231,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
   int64_t batch_mb = 4096;
   {
     size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+    if (device_mem_info(&fr, &tot) == cudaSuccess)
       batch_mb = std::max<int64_t>(64, std::min<int64_t>(batch_mb, static_cast<int64_t>(fr >> 22)));
     else
       cudaGetLastError();

@@ -11,6 +11,8 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _lib
+
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous block [lo, hi) of n items owned by `rank` (same rule the
@@ -190,7 +192,7 @@ def refit_distributed(model, points, values, rank: int, world: int, device=None,
     if layout == "columns":
         exchange_columns(sess)
     dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
-    gram = torch.empty(R * R, dtype=torch.float64, device=dev)
+    gram = _lib.device_tensor(R * R, dev)
     rhs = torch.empty(R, dtype=torch.float64, device=dev)
     sess.normal_equations(gram, rhs)
     reduce_normal_equations(gram, rhs)

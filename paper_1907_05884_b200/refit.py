@@ -10,6 +10,7 @@ import ctypes as C
 
 import numpy as np
 
+from . import _lib
 from ._lib import (TRANSFORMS, Err, ReestimateInfo, SketchCfg, check, dptr, lib, make_error,
                    require_gpu)
 from .model import Model
@@ -66,7 +67,7 @@ def gram(a, slices: int | None = None):
         raise TypeError("gram: expected a 2-D CUDA float64 tensor")
     rows, n = a.shape
     at = a.t().contiguous()  # column-major A: column j at j * rows
-    g = torch.zeros(n * n, dtype=torch.float64, device=a.device)
+    g = _lib.device_tensor(n * n, a.device, zero=True)
     ns = gram_slices() if slices is None else int(slices)
     err = Err()
     stream = torch.cuda.current_stream(a.device).cuda_stream

@@ -1,6 +1,6 @@
 """Dev tool: bench-style C2 refits with nvidia-smi sampled every 50 ms, to
 correlate slow stages with SM clock / power / throttle reasons.
-usage: FSTK_DEBUG_TIMING=1 python tools/refit_clocks.py [runs] > gpurun_out/refit_clocks.log"""
+usage: FSTK_DEBUG_TIMING=1 python tools/refit_clocks.py [runs] [config] > gpurun_out/refit_clocks.log"""
 import os
 import subprocess
 import sys
@@ -16,10 +16,12 @@ from paper_1907_05884_b200.dist import refine_distributed
 
 FIELDS = ("timestamp,clocks.sm,clocks.mem,power.draw,temperature.gpu,memory.used,"
           "clocks_event_reasons.active")
-log = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "smi_refit.csv")
+log = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out",
+                   f"smi_refit_{os.getpid()}.csv")
 smi = subprocess.Popen(["nvidia-smi", f"--query-gpu={FIELDS}", "--format=csv,noheader",
                         "-lms", "50"], stdout=open(log, "w"), stderr=subprocess.DEVNULL)
-model, pts, vals, c = workload("C2", 0, 0)
+CFG = sys.argv[2] if len(sys.argv) > 2 else "C2"
+model, pts, vals, c = workload(CFG, 0, 0)
 R = int(np.prod(model.ranks))
 t_origin = time.time()
 
