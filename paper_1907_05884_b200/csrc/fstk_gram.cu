@@ -366,6 +366,29 @@ __global__ void residue_kernel(const SRC src, int64_t s0, int64_t rows, int n, i
   }
 }
 
+// P_s = prod_{t<s} m_t, and the split of an NM-digit Garner value into two
+// halves that are exact in fp64: the smallest s with prod_{s<=t<NM} m_t and
+// P_s both below 2^53 (0 = none; then the 128-bit path).
+__host__ __device__ constexpr unsigned long long crt_prefix(int s) {
+  unsigned long long p = 1;
+  for (int t = 0; t < s; ++t) p *= static_cast<unsigned long long>(kmod(t));
+  return p;
+}
+__host__ __device__ constexpr int crt_split(int nm) {
+  constexpr unsigned long long lim = 1ull << 53;
+  for (int s = 1; s < nm; ++s) {
+    unsigned long long q = 1;
+    bool ok = true;
+    for (int t = s; t < nm; ++t) {
+      if (q > lim / static_cast<unsigned long long>(kmod(t))) { ok = false; break; }
+      q *= static_cast<unsigned long long>(kmod(t));
+    }
+    if (ok && q < lim && crt_prefix(s) < lim) return s;
+  }
+  return 0;
+}
+static_assert(crt_split(9) > 0 && crt_split(11) > 0 && crt_split(12) > 0, "CRT split");
+
 // 128-bit integer -> double on the magnitude: exact whenever the value is
 // representable (both 64-bit halves then carry <= 53 significant bits and the
 // fused sum is exact), otherwise within one ulp.
@@ -403,10 +426,25 @@ __global__ void __launch_bounds__(256) crt_fold_kernel(const int32_t* __restrict
     if (v > mt / 2) v -= mt;
     y[t] = v;
   }
-  __int128 acc = y[NM - 1];
+  double accd;
+  constexpr int SPLIT = crt_split(NM);
+  if constexpr (SPLIT > 0) {
+    // V = V_lo + P_s V_hi with both halves and P_s below 2^53 (exact int64
+    // Horner, exact doubles); one fma rounds V once: correctly rounded, so
+    // exact whenever V is representable, like the 128-bit evaluation.
+    long long hi = y[NM - 1];
 #pragma unroll
-  for (int t = NM - 2; t >= 0; --t) acc = acc * kmod(t) + y[t];
-  const double accd = i128_to_double(acc);
+    for (int t = NM - 2; t >= SPLIT; --t) hi = hi * kmod(t) + y[t];
+    long long lo = y[SPLIT - 1];
+#pragma unroll
+    for (int t = SPLIT - 2; t >= 0; --t) lo = lo * kmod(t) + y[t];
+    accd = fma(static_cast<double>(hi), static_cast<double>(crt_prefix(SPLIT)), static_cast<double>(lo));
+  } else {
+    __int128 acc = y[NM - 1];
+#pragma unroll
+    for (int t = NM - 2; t >= 0; --t) acc = acc * kmod(t) + y[t];
+    accd = i128_to_double(acc);
+  }
   const double v0 = ldexp(accd, ex[c0 + i] + ex[c0 + j] - 2 * k);
   const double v = negate ? -v0 : v0;
   double* g = G + (c0 + i) + static_cast<int64_t>(c0 + j) * ldg;
