@@ -316,6 +316,10 @@ def main():
     # exercises the multi-rank code path on a single GPU (host-mediated
     # collectives, no kernels waiting on each other).
     backend = os.environ.get("FSTK_BENCH_BACKEND", "nccl")
+    if backend != "nccl" and world > 1:
+        # several ranks share one GPU here: a per-process device cache could
+        # hold memory another rank needs (each can only trim its own).
+        os.environ.setdefault("FSTK_DEVICE_CACHE", "0")
     ndev = torch.cuda.device_count()
     local = local % max(ndev, 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
