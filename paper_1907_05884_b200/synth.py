@@ -168,7 +168,21 @@ def _omp(phi: np.ndarray, z: np.ndarray, max_nnz: int):
 def fitted_model(grid: int, ranks, degree: int, max_nnz: int, seed: int = 0,
                  n_gauss: int = 0) -> Model:
     """Upstream stand-in (NOT the hot path): sample the noise-free field on a
-    node-centred grid^3 over [0,1]^3, fixed-rank HOSVD, sparse Legendre fits."""
+    node-centred grid^3 over [0,1]^3, fixed-rank HOSVD, sparse Legendre fits.
+    Runs with single-threaded BLAS: the greedy sparse fits pick different
+    indices when the eigen/least-squares rounding changes with the thread
+    count, and every launch (plain python, torchrun's OMP_NUM_THREADS=1) must
+    build the same model from the same seed."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover - the image ships threadpoolctl
+        return _fitted_model(grid, ranks, degree, max_nnz, seed, n_gauss)
+    with threadpool_limits(1):
+        return _fitted_model(grid, ranks, degree, max_nnz, seed, n_gauss)
+
+
+def _fitted_model(grid: int, ranks, degree: int, max_nnz: int, seed: int,
+                  n_gauss: int) -> Model:
     g = np.linspace(0.0, 1.0, grid)
     x, y, z = np.meshgrid(g, g, g, indexing="ij")
     pts = np.stack([x.ravel(order="F"), y.ravel(order="F"), z.ravel(order="F")], axis=1)
