@@ -108,3 +108,27 @@ def test_flop_accounting_matches_survey():
     m = synth.random_model((16, 16, 16, 8), (32, 32, 32, 16), 12, seed=0)
     fc, _ = bench.flops_per_point(m)
     assert fc == 74272                                # C4
+
+
+def test_device_tensor_trims_library_cache_on_torch_oom(monkeypatch):
+    # Gram-sized torch buffers: a torch out-of-memory error hands the
+    # library's cached device blocks back (fstk_gpu_trim_device_cache) and
+    # retries once.
+    import torch
+
+    from paper_1907_05884_b200 import _lib
+
+    calls = {"empty": 0, "trim": []}
+    real_empty = torch.empty
+
+    def flaky_empty(*a, **k):
+        calls["empty"] += 1
+        if calls["empty"] == 1:
+            raise torch.OutOfMemoryError("simulated")
+        return real_empty(*a, **k)
+
+    monkeypatch.setattr(torch, "empty", flaky_empty)
+    monkeypatch.setattr(_lib, "trim_device_cache", lambda dev=-1: calls["trim"].append(dev) or 0)
+    t = _lib.device_tensor(16, torch.device("cpu", 0))
+    assert t.numel() == 16 and t.dtype == torch.float64
+    assert calls["empty"] == 2 and len(calls["trim"]) == 1
