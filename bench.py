@@ -38,6 +38,20 @@ METRIC = "FST eval points/s (fp64) + randomized-LS core refit s, at 1/2/4/8 B200
 UNIT = "points/s"
 
 
+DATA_DESC = {
+    "C1": "synthetic (seeded uniform points in [0,1]^3, analytic flame field; model fitted from "
+          "seed by the upstream stand-in on a 64^3 grid)",
+    "C2": "synthetic (seeded jittered 256^3 mesh, analytic flame field; model fitted from seed by "
+          "the upstream stand-in)",
+    "C3": "synthetic (seeded points, 50% uniform and 50% within 0.03 of the flame surface; seeded "
+          "random model of the config's shape)",
+    "C4": "synthetic (seeded 4D points, t on 64 snapshots, travelling-front field; seeded random "
+          "model of the config's shape)",
+    "C5": "synthetic (seeded uniform points shared by 8 seeded random models of the config's "
+          "shape)",
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -89,7 +103,7 @@ def dataset(cfg_name: str, n_override: int, rank: int):
     else:
         n = n_override or min(c["n"], 1 << 24)
         d = c["d"]
-        pts = synth.uniform_points(n, d, seed + 1000 * rank) if d == 4 else \
+        pts = synth.uniform_points(n, d, seed + 1000 * rank) if d == 4 or cfg_name == "C5" else \
             synth.flame_surface_mixture(n, seed + 1000 * rank)
         vals = None
     return np.asfortranarray(pts), vals
@@ -342,9 +356,23 @@ def main():
 
     # ---- device-resident inputs for `value`
     dpts = torch.from_numpy(np.ascontiguousarray(pts.T)).to(dev)  # (d, N): column-major N x d
-    dout = torch.empty(n, dtype=torch.float64, device=dev)
+    # C5 (BASELINE configs[4]): 8 seeded fields sharing one point set, the
+    # visualisation stream; every other config evaluates one model.
+    models = [model]
+    if args.config == "C5":
+        from paper_1907_05884_b200 import synth as _s
+
+        models += [_s.random_model(cfgd["ranks"], cfgd["degrees"], cfgd["nnz"], seed=f)
+                   for f in range(1, 8)]
+    NF = len(models)
+    dout = torch.empty((NF, n), dtype=torch.float64, device=dev)
+
+    def eval_step():
+        for f, m in enumerate(models):
+            m.evaluate_device(dpts, dout[f])
+
     for _ in range(max(args.warmup, 3)):
-        model.evaluate_device(dpts, dout)
+        eval_step()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -365,7 +393,7 @@ def main():
         if flush is not None:
             flush.fill_(1.0)
         e0.record(stream)
-        model.evaluate_device(dpts, dout)
+        eval_step()
         e1.record(stream)
     torch.cuda.synchronize()
     _lib.profile_enable(False)
@@ -374,13 +402,13 @@ def main():
     prof = _lib.profile_read()
     ms = sum(e0.elapsed_time(e1) for e0, e1 in ev) / args.steps
     ms = maxreduce(ms, world, dev)
-    value = world * n / (ms * 1e-3)
+    value = world * n * NF / (ms * 1e-3)
 
     # ---- roofline of the dominant kernel (the DMMA contraction)
     c_ms, c_n = prof["contract"]
     m_ms, m_n = prof["mode_tables"]
-    per_launch_pts = n * args.steps / max(c_n, 1)
-    achieved = fc * n * args.steps / (c_ms * 1e-3) / 1e12 if c_ms > 0 else None
+    per_launch_pts = n * NF * args.steps / max(c_n, 1)
+    achieved = fc * n * NF * args.steps / (c_ms * 1e-3) / 1e12 if c_ms > 0 else None
     traffic, tpts = traffic_from_profile(args.config)
     kr = os.environ.get("FSTK_CONTRACT_KR")
     use_kr = (kr != "0") if kr is not None and model.order in (3, 4) else model.order == 4
@@ -394,8 +422,8 @@ def main():
                            "(MEASURED_PEAKS.json has no fp64 entry); DFMA measured %.1f" % peak_fma,
             "algorithmic_flops_per_point": fc,
             "share_of_step": c_ms / (c_ms + m_ms) if c_ms + m_ms > 0 else None,
-            "step_tflops": (fc + fm) * n / (ms * 1e-3) / 1e12,
-            "step_frac": (fc + fm) * n / (ms * 1e-3) / 1e12 / peak_mma,
+            "step_tflops": (fc + fm) * n * NF / (ms * 1e-3) / 1e12,
+            "step_frac": (fc + fm) * n * NF / (ms * 1e-3) / 1e12 / peak_mma,
             "mode_tables_ms_per_step": m_ms / args.steps,
             "contract_ms_per_step": c_ms / args.steps,
             "note": "the mode-table kernel of chunk i+1 runs concurrently with the contraction of "
@@ -404,6 +432,23 @@ def main():
                     "the SMs, `step_frac` is the whole evaluation step (all 73,120 flop/pt)"}
 
     # ---- e2e through the host C-ABI (pinned host buffers)
+    if NF > 1:
+        # C5: the public multi-field call, points uploaded once per step,
+        # every field's values read back.
+        from paper_1907_05884_b200.model import evaluate_fields
+
+        evaluate_fields(models, pts)
+        ef_times = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            evaluate_fields(models, pts)
+            ef_times.append(time.perf_counter() - t0)
+        ef_s = maxreduce(float(np.median(ef_times)), world, dev)
+        e2e = {"value": world * n * NF / ef_s, "unit": UNIT, "h2d_bytes_per_step": int(n * d * 8),
+               "d2h_bytes_per_step": int(NF * n * 8), "ms_per_step": ef_s * 1e3,
+               "path": "evaluate_fields (pageable numpy points uploaded once, %d fields "
+                       "evaluated from HBM through fstk_gpu_evaluate_batch_device, read back)" % NF}
     hp = torch.from_numpy(np.ascontiguousarray(pts.T)).pin_memory()
     hout = torch.empty(n, dtype=torch.float64).pin_memory()
     hp_np = hp.numpy().T  # (N, d) view, column-major
@@ -425,19 +470,24 @@ def main():
         model.evaluate_batch(pts)
         pg_times.append(time.perf_counter() - t0)
     pg_s = maxreduce(float(np.median(pg_times)), world, dev)
-    e2e = {"value": world * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(n * d * 8),
+    e2e_one = {"value": world * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(n * d * 8),
            "d2h_bytes_per_step": int(n * 8), "ms_per_step": e2e_s * 1e3,
            "path": "fstk_gpu_evaluate_batch (host C-ABI), pinned host buffers",
            "pageable": {"value": world * n / pg_s, "ms_per_step": pg_s * 1e3,
                         "path": "the same call with pageable numpy buffers (staged by the "
                                 "library through pinned memory)"}}
+    if NF == 1:
+        e2e = e2e_one
+    else:
+        e2e["single_field"] = e2e_one
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded jittered 256^3 mesh, analytic flame field; model fitted "
-                    "from seed by the upstream stand-in)",
-            "config": {"workload": f"{args.config}: evaluate {n} points per rank, ranks "
+            "data": DATA_DESC.get(args.config, "synthetic"),
+            "config": {"workload": f"{args.config}: evaluate {n} points per rank"
+                                   + (f" x {NF} fields (value counts field-points)" if NF > 1 else "")
+                                   + f", ranks "
                                    f"{tuple(model.ranks)}, Legendre p={cfgd['degrees'][0]}, "
                                    f"<= {cfgd['nnz']} nnz",
                        "points_per_rank": n, "flops_per_point": fc + fm,

@@ -476,10 +476,22 @@ def evaluate_fields(models, points, device=None) -> np.ndarray:
         raise make_error(1, "points must be Q x d")
     dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
     pt = torch.from_numpy(np.ascontiguousarray(p.T)).to(dev)  # (d, Q): the Q x d col-major buffer
-    out = torch.empty((len(models), p.shape[0]), dtype=torch.float64, device=dev)
+    nf, q = len(models), p.shape[0]
+    out = torch.empty((nf, q), dtype=torch.float64, device=dev)
+    # Field f's values stream back to pinned host memory on a copy stream
+    # while field f+1 is evaluated; only the last field's read-back is exposed.
+    host = torch.empty((nf, q), dtype=torch.float64, pin_memory=True)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
     for f, m in enumerate(models):
         m.evaluate_device(pt, out[f])
-    return out.cpu().numpy().T
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        copy.wait_event(ev)
+        with torch.cuda.stream(copy):
+            host[f].copy_(out[f], non_blocking=True)
+    copy.synchronize()
+    return host.numpy().T
 
 
 def save_model(model: Model, path: str):
