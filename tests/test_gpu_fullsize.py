@@ -73,3 +73,31 @@ def test_c3_full_128m_parity(O):
     idx = _sample_index(pts.shape[0], 43)
     assert (idx < (1 << 26)).any() and (idx >= (1 << 26)).any()
     del full
+
+
+def test_ramped_chunk_schedule_errors_and_values():
+    # Pinned host slabs of >= 4 chunks ramp their first and last chunks (CH/8,
+    # CH/4, CH/2): values equal the pageable (uniformly chunked) path bit for
+    # bit and small batches, and a Domain error in a ramped chunk reports the
+    # right point.
+    import torch
+
+    import paper_1907_05884_b200 as F
+
+    m = synth.random_model((8, 8, 8), (10, 10, 10), 5, seed=61)
+    n = 9 * CHUNK + 12345
+    pts = synth.uniform_points(n, 3, seed=62)
+    pin = torch.empty((3, n), dtype=torch.float64).pin_memory()
+    pin.numpy()[:] = pts.T
+    po = torch.empty(n, dtype=torch.float64).pin_memory()
+    m.evaluate_batch_into(pin.numpy().T, po.numpy())
+    full = po.numpy().copy()
+    assert np.array_equal(full, m.evaluate_batch(pts))
+    for lo, hi in ((0, 300_000), (CHUNK // 8 - 5, CHUNK // 8 + 5), (n - 300_000, n)):
+        assert np.array_equal(m.evaluate_batch(pts[lo:hi]), full[lo:hi])
+    for bad in (CHUNK // 8 + 3, 3 * CHUNK // 8 + 1, n - 1000, n - CHUNK // 2 - 7):
+        pin.numpy()[2, bad] = 2.0
+        with pytest.raises(F.FstkError) as e:
+            m.evaluate_batch_into(pin.numpy().T, po.numpy())
+        assert e.value.kind == "Domain" and e.value.index == bad and e.value.mode == 2
+        pin.numpy()[2, bad] = pts[bad, 2]
