@@ -1345,6 +1345,28 @@ static void upload_core(fstk_gpu_model* m) {
 // (both are fp64-pipe bound with complementary stalls).  Chunk c records its
 // lowest failing row in m->chunk_err[c]; the caller's stream `s` is joined
 // at the end.
+// Chunk begins of a q-point evaluation (the last entry is q): full chunks of
+// CH, except that with `ramp` slabs of >= 4 chunks ramp their first and last
+// chunks (CH/8, CH/4, CH/2 and back), so the work that cannot overlap
+// another chunk -- the first upload or mode-table pass, the last read-back --
+// is small.  Chunking never changes a point's value (position independence).
+static std::vector<int64_t> chunk_begins(int64_t q, int64_t CH, bool ramp) {
+  std::vector<int64_t> cb{0};
+  const int64_t r8 = round_up(std::max<int64_t>(CH / 8, 128), 128);
+  if (ramp && q >= 4 * CH && CH >= 1024) {
+    const int64_t steps[3] = {r8, 2 * r8, 4 * r8};
+    for (int64_t x : steps) cb.push_back(cb.back() + x);
+    const int64_t mid_end = q - 7 * r8;
+    while (cb.back() + CH <= mid_end) cb.push_back(cb.back() + CH);
+    if (cb.back() < mid_end) cb.push_back(mid_end);
+    for (int i = 2; i >= 0; --i) cb.push_back(cb.back() + steps[i]);
+  } else {
+    for (int64_t b = CH; b < q; b += CH) cb.push_back(b);
+    cb.push_back(std::max<int64_t>(q, 0));
+  }
+  return cb;
+}
+
 void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, const double* pts,
                           int64_t ldp, int64_t n, double* out, cudaStream_t s) {
   const int64_t CH = m->chunk_points;
@@ -1357,15 +1379,18 @@ void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, cons
     craw.alloc(m->R);
     FSTK_CUDA(cudaMemcpy(craw.p, core_host, m->R * 8, cudaMemcpyHostToDevice));
   }
-  const int64_t nchunks = std::max<int64_t>(1, ceil_div(n, CH));
+  // Device-resident inputs: uniform chunks (a ramp measured no faster here;
+  // the first two chunks' mode passes already run concurrently).
+  const std::vector<int64_t> cb = chunk_begins(n, CH, false);
+  const int64_t nchunks = std::max<int64_t>(1, static_cast<int64_t>(cb.size()) - 1);
   m->chunk_err.ensure(static_cast<size_t>(nchunks));
   FSTK_CUDA(cudaMemsetAsync(m->chunk_err.p, 0xff, nchunks * sizeof(unsigned long long), s));
   FSTK_CUDA(cudaEventRecord(m->fork_ev, s));
   for (auto& ck : m->chunk) FSTK_CUDA(cudaStreamWaitEvent(ck.stream, m->fork_ev, 0));
-  for (int64_t c = 0; c * CH < n; ++c) {
+  for (int64_t c = 0; c + 1 < static_cast<int64_t>(cb.size()) && cb[c] < n; ++c) {
     Chunk& ck = m->chunk[c & 1];
-    const int64_t b = c * CH;
-    const int64_t nb = std::min(CH, n - b);
+    const int64_t b = cb[c];
+    const int64_t nb = cb[c + 1] - b;
     const int64_t nout = round_up(nb, 128);
     launch_mode_tables(m, pts + b, ldp, nb, nout, nullptr, ck.tables.p, toff, ldt, false,
                        m->chunk_err.p + c, ck.stream);
@@ -1382,14 +1407,14 @@ void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, cons
 // Lowest failing row over the chunks of the last evaluate_device call (or -1);
 // synchronises `s`.
 int64_t evaluate_device_error(const fstk_gpu_model* m, int64_t n, cudaStream_t s) {
-  const int64_t CH = m->chunk_points;
-  const int64_t nchunks = std::max<int64_t>(1, ceil_div(n, CH));
+  const std::vector<int64_t> cb = chunk_begins(n, m->chunk_points, false);
+  const int64_t nchunks = std::max<int64_t>(1, static_cast<int64_t>(cb.size()) - 1);
   std::vector<unsigned long long> bad(static_cast<size_t>(nchunks));
   FSTK_CUDA(cudaMemcpyAsync(bad.data(), m->chunk_err.p, nchunks * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, s));
   FSTK_CUDA(cudaStreamSynchronize(s));
   for (int64_t c = 0; c < nchunks; ++c)
-    if (bad[c] != ULLONG_MAX) return c * CH + static_cast<int64_t>(bad[c]);
+    if (bad[c] != ULLONG_MAX) return cb[c] + static_cast<int64_t>(bad[c]);
   return -1;
 }
 
@@ -1819,28 +1844,10 @@ static void eval_host_slab(const fstk_gpu_model* m, const double* points, int64_
         FSTK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ck.h_stage),
                                 static_cast<size_t>(d + 1) * CH * sizeof(double),
                                 cudaHostAllocDefault));
-  // Chunk schedule: full chunks, except that long pinned slabs ramp up (CH/8,
-  // CH/4, CH/2) and down (CH/2, CH/4, CH/8) at the ends, so only a small first
-  // upload and a small last read-back are not hidden behind another chunk's
-  // compute.  Chunking never changes a point's value (position independence).
-  std::vector<int64_t> cb{0};  // chunk begins; cb.back() == q at the end
-  {
-    const int64_t r8 = round_up(std::max<int64_t>(CH / 8, 128), 128);
-    // Pinned buffers only: the staged (pageable) path is bound by its host
-    // copies, and the small end chunks measured slower there (3.2e8 -> 2.8e8
-    // pts/s at C2) while the pinned path gained (3.70e8 -> 3.74e8).
-    if (!stage && q >= 4 * CH && CH >= 1024) {
-      const int64_t ramp[3] = {r8, 2 * r8, 4 * r8};
-      for (int64_t x : ramp) cb.push_back(cb.back() + x);
-      const int64_t mid_end = q - 7 * r8;
-      while (cb.back() + CH <= mid_end) cb.push_back(cb.back() + CH);
-      if (cb.back() < mid_end) cb.push_back(mid_end);
-      for (int i = 2; i >= 0; --i) cb.push_back(cb.back() + ramp[i]);
-    } else {
-      for (int64_t b = CH; b < q; b += CH) cb.push_back(b);
-      cb.push_back(q);
-    }
-  }
+  // Long pinned slabs ramp their end chunks; the staged (pageable) path is
+  // bound by its host copies, where small end chunks measured slower (3.2e8
+  // -> 2.8e8 pts/s at C2) while the pinned path gained (3.70e8 -> 3.74e8).
+  const std::vector<int64_t> cb = chunk_begins(q, CH, !stage);
   int64_t pend[2] = {-1, -1};  // chunk whose outputs wait in each staging slot
   auto drain = [&](int slot) {
     if (pend[slot] < 0) return;

@@ -101,3 +101,24 @@ def test_ramped_chunk_schedule_errors_and_values():
             m.evaluate_batch_into(pin.numpy().T, po.numpy())
         assert e.value.kind == "Domain" and e.value.index == bad and e.value.mode == 2
         pin.numpy()[2, bad] = pts[bad, 2]
+
+
+def test_device_schedule_matches_ramped_host_and_reports_domain_index():
+    # Device-resident evaluation (uniform chunks) gives the values of the
+    # ramped pinned host path bit for bit, and the right error index.
+    import torch
+
+    import paper_1907_05884_b200 as F
+
+    m = synth.random_model((8, 8, 8), (10, 10, 10), 5, seed=63)
+    n = 9 * CHUNK + 777
+    pts = synth.uniform_points(n, 3, seed=64)
+    host = m.evaluate_batch(pts)
+    dp = torch.from_numpy(np.ascontiguousarray(pts.T)).cuda()
+    assert np.array_equal(m.evaluate_device(dp).cpu().numpy(), host)
+    for bad in (5, CHUNK // 8 + 9, n - 3 * CHUNK // 8 - 1):
+        dp[1, bad] = -1.0
+        with pytest.raises(F.FstkError) as e:
+            m.evaluate_device(dp)
+        assert e.value.kind == "Domain" and e.value.index == bad and e.value.mode == 1
+        dp[1, bad] = float(pts[bad, 1])
