@@ -20,6 +20,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <condition_variable>
 #include <thread>
 #include <vector>
 
@@ -1802,22 +1803,86 @@ namespace fstk_gpu {
 // ldp, on this model's device (chunked, two streams).  A Domain error reports
 // the global row index.
 // dst <- src (bytes) on up to 8 host threads (pageable <-> pinned staging).
-static void host_copy(void* dst, const void* src, size_t bytes) {
-  const size_t per = size_t(4) << 20;
-  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  const size_t nt = std::min<size_t>(hw, (bytes + per - 1) / per);
-  if (nt <= 1) {
-    std::memcpy(dst, src, bytes);
-    return;
+// Host staging copies run on a persistent pool (up to 8 threads): spawning
+// threads per copy cost several milliseconds per C2 evaluation.  A job is a
+// list of segments whose concatenation is split into equal byte ranges.
+struct CopySeg {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+class CopyPool {
+ public:
+  explicit CopyPool(int n) : nparts_(n) {
+    for (int i = 1; i < n; ++i) std::thread([this, i] { worker(i); }).detach();
   }
-  std::vector<std::thread> th;
-  for (size_t t = 1; t < nt; ++t)
-    th.emplace_back([=] {
-      const size_t lo = bytes * t / nt, hi = bytes * (t + 1) / nt;
-      std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
-    });
-  std::memcpy(dst, src, bytes / nt);
-  for (auto& x : th) x.join();
+  void run(const CopySeg* segs, int nseg) {
+    size_t total = 0;
+    for (int k = 0; k < nseg; ++k) total += segs[k].bytes;
+    if (nparts_ <= 1 || total < (size_t(4) << 20)) {
+      for (int k = 0; k < nseg; ++k) std::memcpy(segs[k].dst, segs[k].src, segs[k].bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> one(run_mu_);  // one job at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      segs_ = segs;
+      nseg_ = nseg;
+      total_ = total;
+      remaining_ = nparts_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    part(segs, nseg, total, 0, nparts_);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return remaining_ == 0; });
+  }
+
+ private:
+  static void part(const CopySeg* segs, int nseg, size_t total, int i, int np) {
+    size_t lo = total * i / np, hi = total * (i + 1) / np, base = 0;
+    for (int k = 0; k < nseg && lo < hi; ++k) {
+      const size_t b = segs[k].bytes;
+      if (lo < base + b) {
+        const size_t off = lo - base, n = std::min(hi, base + b) - lo;
+        std::memcpy(static_cast<char*>(segs[k].dst) + off, static_cast<const char*>(segs[k].src) + off, n);
+        lo += n;
+      }
+      base += b;
+    }
+  }
+  void worker(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      const CopySeg* segs = segs_;
+      const int nseg = nseg_;
+      const size_t total = total_;
+      lk.unlock();
+      part(segs, nseg, total, i, nparts_);
+      lk.lock();
+      if (--remaining_ == 0) done_.notify_one();
+    }
+  }
+  const int nparts_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const CopySeg* segs_ = nullptr;
+  int nseg_ = 0;
+  size_t total_ = 0;
+  int remaining_ = 0;
+  uint64_t gen_ = 0;
+};
+static CopyPool& copy_pool() {
+  static CopyPool* p = new CopyPool(
+      static_cast<int>(std::max(1u, std::min(8u, std::thread::hardware_concurrency()))));
+  return *p;  // leaked: its detached workers live for the process
+}
+static void host_copy(void* dst, const void* src, size_t bytes) {
+  const CopySeg seg{dst, src, bytes};
+  copy_pool().run(&seg, 1);
 }
 
 static bool is_pinned(const void* p) {
@@ -1873,9 +1938,11 @@ static void eval_host_slab(const fstk_gpu_model* m, const double* points, int64_
     const int64_t nb = cb[c + 1] - b;
     if (stage) {
       drain(slot);  // chunk c-2 is done with this slot: its outputs go to the caller
+      CopySeg segs[kMaxOrder];
       for (int k = 0; k < d; ++k)
-        host_copy(ck.h_stage + static_cast<int64_t>(k) * CH, points + k * ldp + r0 + b,
-                  nb * sizeof(double));
+        segs[k] = {ck.h_stage + static_cast<int64_t>(k) * CH, points + k * ldp + r0 + b,
+                   static_cast<size_t>(nb) * sizeof(double)};
+      copy_pool().run(segs, d);
       FSTK_CUDA(cudaMemcpyAsync(ck.points.p, ck.h_stage, static_cast<size_t>(d) * CH * sizeof(double),
                                 cudaMemcpyHostToDevice, ck.stream));
     } else {
