@@ -578,6 +578,13 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=No
     tform = transform or args.transform
     R = int(np.prod(model.ranks))
     S = cfgd["m_factor"] * R
+    # Repeated refits of one size: keep the library's large device blocks
+    # between sessions (policy 2) unless FSTK_DEVICE_CACHE chose otherwise;
+    # the default policy returns them to the driver after every refit.
+    from paper_1907_05884_b200 import _lib as _L
+
+    if "FSTK_DEVICE_CACHE" not in os.environ:
+        _L.set_device_cache(2)
     # warm-up on a small problem (cuBLAS/cuSOLVER handles, twiddle cache)
     wm = synth.random_model((4, 4, 4), (6, 6, 6), 4, seed=1)
     wp = synth.uniform_points(4096, 3, 2)

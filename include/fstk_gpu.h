@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define FSTK_GPU_ABI_VERSION 2
+#define FSTK_GPU_ABI_VERSION 3
 
 /* Status codes = fstk::ErrorKind + 1 (error.hpp:11-19). */
 enum {
@@ -105,6 +105,13 @@ typedef struct fstk_reestimate_info {
   int32_t gram_slices;  /* int8 digit planes of the Gram used (0 = native fp64) */
   int32_t refine_steps; /* iterative-refinement steps against A */
   double gram_int8_ops; /* int8 tensor-core ops (2 x multiply-adds) of the sliced Gram */
+  /* Rank decision (randls.cpp:112-123).  The Cholesky route certifies full
+   * rank when sigma_min(A) / max column norm > 100 R eps (sigma_ratio, its
+   * estimate); otherwise qr_path = 1: streaming TSQR + pivoted QR of A with
+   * Eigen's threshold decides, and a deficient system gets the COD's
+   * minimum-norm solution. */
+  int32_t qr_path;
+  double sigma_ratio;
 } fstk_reestimate_info;
 
 typedef struct fstk_gpu_model fstk_gpu_model;
@@ -114,16 +121,23 @@ int32_t fstk_gpu_abi_version(void);
 int32_t fstk_gpu_device_count(void);
 /* Kernel launches issued by this process so far (evidence counter). */
 uint64_t fstk_gpu_launch_count(void);
-/* Returns the library's cached device blocks (>= 256 MB, kept after release
- * for the next refit session of the same size; see fstk_common.cuh) to the
- * driver: one device, or all when device < 0.  Returns the bytes released.
- * No reference counterpart (the reference has no device memory). */
+/* Large-block device cache (blocks >= 256 MB; see fstk_common.cuh).  policy
+ * 0 = off; 1 = per session (default): blocks are reused only while a refit
+ * session is open and all go back to the driver when the last one ends, so
+ * reestimate_core returns holding no idle HBM; 2 = persistent across
+ * sessions (repeated refits of one size) until trimmed.  Returns the previous
+ * policy.  FSTK_DEVICE_CACHE=0/1/2 sets the initial policy.  No reference
+ * counterpart (the reference has no device memory). */
+int32_t fstk_gpu_set_device_cache(int32_t policy);
+/* Returns the cached blocks to the driver: one device, or all when
+ * device < 0.  Returns the bytes released. */
 uint64_t fstk_gpu_trim_device_cache(int32_t device);
 
 /* Builds the device-resident model.  Validates like the reference ctor
  * (model.cpp:22-53): Shape on count/domain mismatch, Parameter on invalid
- * bases.  Wavelet bases are accepted by the format but not by this GPU path
- * (FSTK_E_PARAMETER). */
+ * bases.  Legendre and Alpert multiwavelet bases are both evaluated on the
+ * GPU (basis.cpp:226-253); the evaluation workspaces are
+ * allocated on the first evaluate call, not here. */
 /* The devices of this process: a model created with device = -1
  * lives on ids[0] with replicas on the others, and a host evaluate_batch on it
  * splits the points into contiguous slabs, one per device, concurrently (the
@@ -280,9 +294,38 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* refit, const double* gram,
  * (iterative refinement = corrected semi-normal equations, converging to the
  * reference's QR least-squares solution); finish() copies x to the host core
  * and computes the validation residuals. */
+/* factor(): info->rank_deficient = 1 means the Gram was not positive
+ * definite (x = 0); the rank question then goes to the pivoted-QR stages
+ * below.  */
 int32_t fstk_gpu_refit_factor(fstk_gpu_refit* refit, const double* gram,
                               const double* rhs, double* x, fstk_reestimate_info* info,
                               fstk_gpu_error* err);
+/* Rank decision of a sharded refit (randls.cpp:112-123), in stages:
+ * certify() after the refinement has converged: estimates sigma_min(A) from
+ * the Cholesky factor and the summed Gram's diagonal; *certified = 1 when
+ * sigma_min / max column norm > 100 R eps, i.e. Eigen's ColPivHouseholderQR
+ * would report full rank.  Otherwise, or when the Gram cannot be factored:
+ * local_qr() writes the (R+1) x (R+1) upper R of this shard's [A b] (device,
+ * column-major, streaming TSQR; A is left intact); the caller stacks the
+ * shards' factors with fstk_gpu_qr_stack on one rank and calls qr_solve():
+ * pivoted QR, Eigen's rank rule (threshold min(rows, R) eps max|R_ii|), the
+ * QR solution or the COD minimum-norm solution into x, and
+ * info->rank_deficient. */
+int32_t fstk_gpu_refit_certify(fstk_gpu_refit* refit, const double* gram, double* sigma_ratio,
+                               int32_t* certified, fstk_gpu_error* err);
+int32_t fstk_gpu_refit_local_qr(fstk_gpu_refit* refit, double* raug, fstk_gpu_error* err);
+int32_t fstk_gpu_refit_qr_solve(fstk_gpu_refit* refit, const double* raug, double* x,
+                                fstk_reestimate_info* info, fstk_gpu_error* err);
+/* top := R of [top; other] for two (n1 x n1) upper-triangular device
+ * factors (column-major, ld n1): the stacking step of a sharded TSQR. */
+int32_t fstk_gpu_qr_stack(double* top, const double* other, int64_t n1, int32_t device,
+                          void* stream, fstk_gpu_error* err);
+/* solve_system (randls.cpp:112-123) on the GPU for a host system a (m x n,
+ * column-major) and b: ColPivHouseholderQR's rank with Eigen's default
+ * threshold; x = the QR solution when rank == n, else the
+ * CompleteOrthogonalDecomposition minimum-norm solution (*rank_deficient = 1). */
+int32_t fstk_gpu_solve_system(const double* a, int64_t m, int64_t n, const double* b, double* x,
+                              int32_t* rank, int32_t* rank_deficient, fstk_gpu_error* err);
 int32_t fstk_gpu_refit_correction(fstk_gpu_refit* refit, const double* x, double* s,
                                   fstk_gpu_error* err);
 int32_t fstk_gpu_refit_apply(fstk_gpu_refit* refit, const double* s, double* x,

@@ -298,10 +298,13 @@ def mixed_matrix(w, seed=0, transform="dct"):
 
 
 # ------------------------------------------------------- QR solve (Eigen) ---
-def solve_system(a, b):
-    """Restates randls.cpp:112-123 with LAPACK: ColPivHouseholderQR; rank by
-    Eigen's default threshold |R_ii| > diagSize*eps*|R_00|; min-norm (COD)
-    fallback when rank-deficient.  Returns (alpha, rank_deficient)."""
+def solve_system_rank(a, b):
+    """Restates randls.cpp:112-123 with LAPACK: ColPivHouseholderQR (dgeqp3);
+    rank = #{|R_ii| > min(m,n) eps max|R_ii|} (Eigen's default threshold,
+    ColPivHouseholderQR::rank()); full rank -> the QR solution; otherwise the
+    CompleteOrthogonalDecomposition minimum-norm solution, i.e. the min-norm
+    solution of the rank-k system [R11 R12] P^T x = (Q^T b)_k, computed from
+    the QR of [R11 R12]^T.  Returns (alpha, rank_deficient, rank)."""
     import scipy.linalg as sla
 
     a = np.asarray(a, dtype=np.float64)
@@ -310,15 +313,24 @@ def solve_system(a, b):
     q, r, piv = sla.qr(a, mode="economic", pivoting=True, check_finite=False)
     diag = np.abs(np.diag(r))
     thresh = min(m, n) * np.finfo(np.float64).eps
-    maxp = diag[0] if diag.size else 0.0
+    maxp = float(diag.max()) if diag.size else 0.0
     rank = int(np.sum(diag > thresh * maxp)) if maxp > 0 else 0
+    c = q.T @ b
+    alpha = np.zeros(n)
     if rank == n:
-        y = sla.solve_triangular(r, q.T @ b, check_finite=False)
-        alpha = np.empty(n)
-        alpha[piv] = y
-        return alpha, False
-    alpha = np.linalg.lstsq(a, b, rcond=thresh)[0]
-    return alpha, True
+        alpha[piv] = sla.solve_triangular(r, c, check_finite=False)
+        return alpha, False, rank
+    if rank > 0:
+        q3, u = np.linalg.qr(r[:rank, :].T)  # [R11 R12]^T = Q3 U
+        z = sla.solve_triangular(u, c[:rank], trans="T", check_finite=False)
+        alpha[piv] = q3 @ z
+    return alpha, True, rank
+
+
+def solve_system(a, b):
+    """(alpha, rank_deficient) of solve_system_rank."""
+    alpha, deficient, _ = solve_system_rank(a, b)
+    return alpha, deficient
 
 
 # ------------------------------------------------------- reestimate_core ---

@@ -68,13 +68,15 @@ class ReestimateInfo(C.Structure):
                 ("held_out", C.c_int32), ("t_prepare", C.c_double), ("t_sketch", C.c_double),
                 ("t_gram", C.c_double), ("t_solve", C.c_double), ("t_residual", C.c_double),
                 ("t_alloc", C.c_double), ("gram_slices", C.c_int32),
-                ("refine_steps", C.c_int32), ("gram_int8_ops", C.c_double)]
+                ("refine_steps", C.c_int32), ("gram_int8_ops", C.c_double),
+                ("qr_path", C.c_int32), ("sigma_ratio", C.c_double)]
 
 
 # Every symbol include/fstk_gpu.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "fstk_gpu_abi_version", "fstk_gpu_device_count", "fstk_gpu_launch_count",
     "fstk_gpu_trim_device_cache",
+    "fstk_gpu_set_device_cache",
     "fstk_gpu_model_create", "fstk_gpu_model_destroy", "fstk_gpu_model_set_core",
     "fstk_gpu_model_get_core", "fstk_gpu_evaluate_batch", "fstk_gpu_evaluate",
     "fstk_gpu_evaluate_batch_device", "fstk_gpu_mode_values", "fstk_gpu_build_design_rows",
@@ -89,7 +91,8 @@ EXPORTS = [
     "fstk_gpu_refit_normal_equations_level", "fstk_gpu_refit_begin_columns",
     "fstk_gpu_refit_exchange_layout", "fstk_gpu_refit_adopt_rows",
     "fstk_gpu_sample_without_replacement", "fstk_gpu_make_plan", "fstk_gpu_set_devices",
-    "fstk_gpu_cholesky_device",
+    "fstk_gpu_cholesky_device", "fstk_gpu_refit_certify", "fstk_gpu_refit_local_qr",
+    "fstk_gpu_refit_qr_solve", "fstk_gpu_qr_stack", "fstk_gpu_solve_system",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -110,6 +113,8 @@ def lib():
     L.fstk_gpu_abi_version.restype = C.c_int32
     L.fstk_gpu_device_count.restype = C.c_int32
     L.fstk_gpu_launch_count.restype = C.c_uint64
+    L.fstk_gpu_set_device_cache.argtypes = [C.c_int32]
+    L.fstk_gpu_set_device_cache.restype = C.c_int32
     L.fstk_gpu_trim_device_cache.argtypes = [C.c_int32]
     L.fstk_gpu_trim_device_cache.restype = C.c_uint64
     L.fstk_gpu_model_create.argtypes = [C.POINTER(ModelDesc), C.c_int32, C.POINTER(VP),
@@ -167,6 +172,12 @@ def lib():
     L.fstk_gpu_refit_correction.argtypes = [VP, VP, VP, C.POINTER(Err)]
     L.fstk_gpu_refit_apply.argtypes = [VP, VP, VP, DP, C.POINTER(Err)]
     L.fstk_gpu_refit_finish.argtypes = [VP, VP, DP, C.POINTER(ReestimateInfo), C.POINTER(Err)]
+    L.fstk_gpu_refit_certify.argtypes = [VP, VP, DP, C.POINTER(C.c_int32), C.POINTER(Err)]
+    L.fstk_gpu_refit_local_qr.argtypes = [VP, VP, C.POINTER(Err)]
+    L.fstk_gpu_refit_qr_solve.argtypes = [VP, VP, VP, C.POINTER(ReestimateInfo), C.POINTER(Err)]
+    L.fstk_gpu_qr_stack.argtypes = [VP, VP, C.c_int64, C.c_int32, VP, C.POINTER(Err)]
+    L.fstk_gpu_solve_system.argtypes = [DP, C.c_int64, C.c_int64, DP, DP, C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_int32), C.POINTER(Err)]
     L.fstk_gpu_refit_end.argtypes = [VP]
     L.fstk_gpu_refit_end.restype = None
     L.fstk_gpu_refit_rows.argtypes = [VP, C.POINTER(C.c_uint64), C.POINTER(Err)]
@@ -200,6 +211,12 @@ def dptr(a):
 
 def launch_count() -> int:
     return int(lib().fstk_gpu_launch_count())
+
+
+def set_device_cache(policy: int) -> int:
+    """Device-cache policy (0 off, 1 per refit session [default], 2
+    persistent); returns the previous one.  See fstk_gpu_set_device_cache."""
+    return int(lib().fstk_gpu_set_device_cache(int(policy)))
 
 
 def trim_device_cache(device: int = -1) -> int:

@@ -109,7 +109,14 @@ struct DeviceGuard {
 // (least recently released blocks are freed first; C2's ~97 GB session fits).
 // A failed cudaMalloc returns cached blocks, oldest first, until the request
 // fits; fstk_gpu_trim_device_cache() returns all of them on demand.
-// FSTK_DEVICE_CACHE=0 disables caching.
+//
+// Policy (fstk_gpu_set_device_cache, or FSTK_DEVICE_CACHE=0/1/2):
+//   0 off: plain cudaMalloc/cudaFree;
+//   1 session (default): blocks are cached only while a refit session is
+//     open; when the last one ends, every cached block goes back to the
+//     driver, so reestimate_core returns holding no idle HBM;
+//   2 persistent: blocks stay cached across sessions (repeated refits of the
+//     same size, e.g. bench.py) until trimmed.
 struct CachedBlock {
   void* p;
   size_t bytes;
@@ -125,12 +132,24 @@ inline DeviceCache& device_cache() {
   return *c;
 }
 constexpr size_t kCacheMinBytes = size_t(256) << 20;
-inline bool device_cache_enabled() {
-  static const bool on = [] {
+inline std::atomic<int>& device_cache_policy() {
+  static std::atomic<int> pol{[] {
     const char* e = std::getenv("FSTK_DEVICE_CACHE");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+    if (!e || !e[0]) return 1;
+    const int v = std::atoi(e);
+    return v <= 0 ? 0 : (v >= 2 ? 2 : 1);
+  }()};
+  return pol;
+}
+// Open refit sessions (policy 1 keeps released blocks only while > 0).
+inline std::atomic<int>& device_cache_sessions() {
+  static std::atomic<int> n{0};
+  return n;
+}
+inline bool device_cache_enabled() { return device_cache_policy().load() != 0; }
+inline bool device_cache_keeps() {
+  const int p = device_cache_policy().load();
+  return p == 2 || (p == 1 && device_cache_sessions().load() > 0);
 }
 // Frees the cached blocks of `device` (all devices when < 0).
 inline void device_cache_trim(int device) {
@@ -151,6 +170,17 @@ inline void device_cache_trim(int device) {
   }
   if (prev >= 0) cudaSetDevice(prev);
 }
+// RAII marker of an open refit session; the last one to close under policy
+// 1 returns the session's cached blocks to the driver.
+struct DeviceCacheSession {
+  DeviceCacheSession() { device_cache_sessions().fetch_add(1); }
+  ~DeviceCacheSession() {
+    if (device_cache_sessions().fetch_sub(1) == 1 && device_cache_policy().load() == 1)
+      device_cache_trim(-1);
+  }
+  DeviceCacheSession(const DeviceCacheSession&) = delete;
+  DeviceCacheSession& operator=(const DeviceCacheSession&) = delete;
+};
 inline cudaError_t device_alloc(void** p, size_t bytes, size_t* got) {
   *got = bytes;
   int dev = 0;
@@ -221,7 +251,7 @@ inline cudaError_t device_mem_info(size_t* free_b, size_t* total_b) {
 inline void device_free(void* p, size_t bytes) {
   if (!p) return;
   cudaPointerAttributes at{};
-  if (bytes >= kCacheMinBytes && device_cache_enabled() &&
+  if (bytes >= kCacheMinBytes && device_cache_keeps() &&
       cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice) {
     int prev = -1;
     cudaGetDevice(&prev);

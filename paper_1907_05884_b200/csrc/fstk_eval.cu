@@ -1368,8 +1368,25 @@ static std::vector<int64_t> chunk_begins(int64_t q, int64_t CH, bool ramp) {
   return cb;
 }
 
+// Allocates and zeroes the padded table workspaces of both chunk slots on
+// first use (padding rows stay 0 afterwards).  Caller holds m->mu.
+void ensure_chunk_workspace(const fstk_gpu_model* m) {
+  for (auto& ck : m->chunk) {
+    if (ck.tables.p) continue;
+    int64_t toff[kMaxOrder], tot = 0;
+    eval_table_offsets(m, round_up(m->chunk_points, 128), toff, &tot);
+    ck.tables.alloc(static_cast<size_t>(tot));
+    FSTK_CUDA(cudaMemsetAsync(ck.tables.p, 0, static_cast<size_t>(tot) * 8, ck.stream));
+    ck.err.alloc(1);
+    ck.points.alloc(static_cast<size_t>(m->d) * m->chunk_points);
+    ck.out.alloc(static_cast<size_t>(m->chunk_points));
+    FSTK_CUDA(cudaStreamSynchronize(ck.stream));
+  }
+}
+
 void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, const double* pts,
                           int64_t ldp, int64_t n, double* out, cudaStream_t s) {
+  ensure_chunk_workspace(m);
   const int64_t CH = m->chunk_points;
   int64_t toff[kMaxOrder], tot = 0;
   const int64_t ldt = round_up(CH, 128);
@@ -1453,6 +1470,12 @@ int32_t fstk_gpu_device_count(void) {
 }
 
 uint64_t fstk_gpu_launch_count(void) { return g_launches.load(); }
+
+int32_t fstk_gpu_set_device_cache(int32_t policy) {
+  const int prev = device_cache_policy().exchange(policy <= 0 ? 0 : (policy >= 2 ? 2 : 1));
+  if (policy <= 0 || (policy == 1 && device_cache_sessions().load() == 0)) device_cache_trim(-1);
+  return prev;
+}
 
 uint64_t fstk_gpu_trim_device_cache(int32_t device) {
   DeviceCache& c = device_cache();
@@ -1726,16 +1749,9 @@ int32_t fstk_gpu_model_create(const fstk_model_desc* desc, int32_t device, fstk_
       FSTK_CUDA(cudaEventCreateWithFlags(&ck.done, cudaEventDisableTiming));
       FSTK_CUDA(cudaEventCreateWithFlags(&ck.host_done, cudaEventDisableTiming));
     }
-    // Allocate and zero the padded table workspaces once (padding rows stay 0).
-    for (auto& ck : m->chunk) {
-      int64_t toff[kMaxOrder], tot = 0;
-      eval_table_offsets(m.get(), round_up(m->chunk_points, 128), toff, &tot);
-      ck.tables.alloc(static_cast<size_t>(tot));
-      FSTK_CUDA(cudaMemset(ck.tables.p, 0, static_cast<size_t>(tot) * 8));
-      ck.err.alloc(1);
-      ck.points.alloc(static_cast<size_t>(d) * m->chunk_points);
-      ck.out.alloc(static_cast<size_t>(m->chunk_points));
-    }
+    // The chunk workspaces (up to ~2 GB of tables each) are allocated on the
+    // first evaluation (ensure_chunk_workspace): a model used only for
+    // mode_values / eval_basis / grids never holds them.
     FSTK_CUDA(cudaDeviceSynchronize());
     *out = m.release();
   });
@@ -1897,6 +1913,7 @@ static void eval_host_slab(const fstk_gpu_model* m, const double* points, int64_
   if (q == 0) return;
   std::lock_guard<std::mutex> lk(m->mu);
   DeviceGuard dg(m->device);
+  ensure_chunk_workspace(m);
   const int64_t CH = m->chunk_points;
   // Pageable caller buffers (the reference's Eigen/numpy arrays): stage each
   // chunk through a pinned double buffer, the host copies of chunk c+1 (and

@@ -103,7 +103,7 @@ int32_t fstk_gpu_evaluate_grid(const fstk_gpu_model* m, const double* coords, co
           fail(FSTK_E_COMPUTE, "cublasDgemmStridedBatched failed");
       }
       count_launch();
-      std::swap(A.p, B.p);
+      std::swap(A, B);  // whole buffers (pointer, count and block size) trade places
       P *= Ik;
     }
     FSTK_CUDA(cudaMemcpyAsync(out, A.p, total * 8, cudaMemcpyDeviceToHost, s));

@@ -232,4 +232,41 @@ double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n
                                      double beta, int slices, cudaStream_t s, int device,
                                      GramScratch& sc);
 
+
+// ---- rank decision (fstk_rank.cu; randls.cpp:112-123) ----
+// Streaming TSQR of a tall matrix with n1 columns, fed in row blocks of at
+// most bmax rows: after fold(), the leading n1 x n1 block of W (ld ldw) is
+// the upper-triangular R of everything folded so far (zeros below).
+struct QrStream {
+  int n1 = 0;
+  int64_t bmax = 0, ldw = 0;
+  DevBuf<double> W, tau;
+  DevBuf<uint8_t> work;
+  size_t work_bytes = 0;
+  std::vector<uint8_t> host_work;
+  DevBuf<int> info;
+  cusolverDnParams_t params = nullptr;
+  bool has_r = false;
+  cudaStream_t s = nullptr;
+  int device = 0;
+  QrStream() = default;
+  QrStream(const QrStream&) = delete;
+  QrStream& operator=(const QrStream&) = delete;
+  ~QrStream();
+  void init(int n1, int64_t bmax, cudaStream_t s, int device);
+  double* block() { return W.p + n1; }  // rows [n1, n1 + rows) of W, ld = ldw
+  void fold(int64_t rows);              // R := R of [R; block rows]
+  void fold_upper(const double* R2, int64_t ld2);  // R := R of [R; R2] (n1 x n1)
+  void get_r(double* dst, int64_t ld) const;
+};
+// Pivoted QR of the (n+1) x (n+1) upper R of [A b] (ld ldr), Eigen's rank
+// rule with diag_size = min(rows of A, n), then the QR solution (full rank)
+// or the COD minimum-norm solution.  Returns the rank; x is device memory.
+int cpqr_solve(const double* Raug, int64_t ldr, int n, int64_t diag_size, double* x,
+               bool* deficient, cudaStream_t s, int device);
+// X := (L L^T)^{-1} X (nrhs columns, ld ldx) for a lower factor L (ld n).
+void chol_solve_blocked_multi(cublasHandle_t h, const double* L, int n, double* X, int64_t ldx,
+                              int nrhs);
+// Upper estimate of lambda_min(L L^T) (block power iteration on the inverse).
+double chol_lambda_min_estimate(const double* L, int n, int iters, cudaStream_t s, int device);
 }  // namespace fstk_gpu

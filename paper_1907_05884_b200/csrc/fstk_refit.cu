@@ -1677,6 +1677,10 @@ struct EventTimer {
 using namespace fstk_gpu;
 
 struct fstk_gpu_refit {
+  // Declared first, so destroyed last: the members below release their
+  // blocks into the device cache, and under the default policy (1) the last
+  // open session's end then hands every cached block back to the driver.
+  DeviceCacheSession cache_session;
   const fstk_gpu_model* model = nullptr;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -1702,6 +1706,7 @@ struct fstk_gpu_refit {
   DevBuf<double> L;       // R x R, lower Cholesky factor
   bool factored = false;
   bool rank_def = false;
+  double sigma_ratio = 0.0;  // certificate sigma_min(A) / max column norm (0 = not computed)
   DevBuf<double> tmp_r;   // local residual rows
   // transform = none: mode tables of this shard's sampled rows (A generated on demand)
   bool none = false;
@@ -2528,42 +2533,69 @@ int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t
 // (randls.cpp:112-123) with O(cond(A) eps) instead of O(cond(A)^2 eps) error.
 namespace fstk_gpu {
 
-static void minnorm_solve(fstk_gpu_refit* rf, const double* gram_in, const double* rhs_in,
-                          double* x_dev) {
-  // Not positive definite: minimum-norm solution on the numerical range of
-  // the Gram (stands in for the COD fallback, randls.cpp:117-121).
-  Handles& h = handles(rf->device);
+// R of [A b] over this shard's sketched rows (streaming TSQR, fstk_rank.cu):
+// A is copied block by block into the fold scratch (or, for transform =
+// none, generated there), so the sketch itself is left intact.
+static void refit_local_qr(fstk_gpu_refit* rf, QrStream& qs) {
   cudaStream_t s = rf->stream;
-  const int n = static_cast<int>(rf->R);
-  DevBuf<double> G(static_cast<size_t>(n) * n), wv(n);
-  DevBuf<int> dinfo(1);
-  FSTK_CUDA(cudaMemcpyAsync(G.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
-  int lw2 = 0;
-  if (cusolverDnDsyevd_bufferSize(h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
-                                  G.p, n, wv.p, &lw2) != CUSOLVER_STATUS_SUCCESS)
-    fail(FSTK_E_COMPUTE, "syevd_bufferSize failed");
-  DevBuf<double> w2(std::max(lw2, 1));
-  if (cusolverDnDsyevd(h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, G.p, n,
-                       wv.p, w2.p, lw2, dinfo.p) != CUSOLVER_STATUS_SUCCESS)
-    fail(FSTK_E_COMPUTE, "syevd failed");
-  count_launch();
-  std::vector<double> ev(n), V(static_cast<size_t>(n) * n), rhs(n);
-  FSTK_CUDA(cudaMemcpyAsync(ev.data(), wv.p, n * 8, cudaMemcpyDeviceToHost, s));
-  FSTK_CUDA(cudaMemcpyAsync(V.data(), G.p, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToHost, s));
-  FSTK_CUDA(cudaMemcpyAsync(rhs.data(), rhs_in, n * 8, cudaMemcpyDeviceToHost, s));
-  FSTK_CUDA(cudaStreamSynchronize(s));
-  const double lmax = std::max(std::fabs(ev[n - 1]), std::fabs(ev[0]));
-  const double thr = lmax * static_cast<double>(n) * 2.220446049250313e-16;
-  std::vector<double> sol(n, 0.0);
-  for (int j = 0; j < n; ++j) {
-    if (ev[j] <= thr) continue;
-    double c = 0.0;
-    for (int i = 0; i < n; ++i) c += V[static_cast<size_t>(j) * n + i] * rhs[i];
-    c /= ev[j];
-    for (int i = 0; i < n; ++i) sol[i] += c * V[static_cast<size_t>(j) * n + i];
+  const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
+  const int64_t arows = fft ? 2 * rf->local_rows : rf->local_rows;
+  const int n = static_cast<int>(rf->R), n1 = n + 1;
+  size_t freeb = 0, totb = 0;
+  FSTK_CUDA(device_mem_info(&freeb, &totb));
+  // Row blocks of at least n1 rows, the scratch within a quarter of the free memory.
+  const int64_t budget_rows = static_cast<int64_t>(freeb / 4 / (static_cast<size_t>(n1) * 8)) - n1;
+  const int64_t bmax = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(arows, 1),
+                                                              std::max<int64_t>(n1, budget_rows)));
+  qs.init(n1, bmax, s, rf->device);
+  for (int64_t r0 = 0; r0 < arows; r0 += bmax) {
+    const int64_t rows = std::min(bmax, arows - r0);
+    if (rf->none)
+      generate_design_block(rf, r0, rows, qs.block(), qs.ldw, s);
+    else
+      FSTK_CUDA(cudaMemcpy2DAsync(qs.block(), qs.ldw * 8, rf->A.p + r0, arows * 8, rows * 8, n,
+                                  cudaMemcpyDeviceToDevice, s));
+    FSTK_CUDA(cudaMemcpyAsync(qs.block() + static_cast<int64_t>(n) * qs.ldw, rf->b.p + r0, rows * 8,
+                              cudaMemcpyDeviceToDevice, s));
+    qs.fold(rows);
   }
-  FSTK_CUDA(cudaMemcpyAsync(x_dev, sol.data(), n * 8, cudaMemcpyHostToDevice, s));
   FSTK_CUDA(cudaStreamSynchronize(s));
+}
+
+// Gram-side certificate of full rank in the reference's sense.  After the
+// refinement x += (L L^T)^{-1} A^T (b - A x) has converged, the eigenvalues of
+// (L L^T)^{-1} A^T A lie in [1 - q, 1 + q] with q <= 1/2 (a flatter step ratio
+// is not accepted as convergence), so sigma_min(A)^2 >= lambda_min(L L^T) / 2.
+// Every |R_ii| of a pivoted QR of A is >= sigma_min(A), and its largest pivot
+// |R_00| is the largest column norm sqrt(max_j G_jj); so sigma_min(A) >
+// R eps max_j ||A_j|| (with a 100x margin for the power-iteration estimate)
+// means ColPivHouseholderQR::rank() == R.  Returns sigma_min / max col norm.
+static double refit_sigma_ratio(fstk_gpu_refit* rf, const double* gram) {
+  const int n = static_cast<int>(rf->R);
+  cudaStream_t s = rf->stream;
+  const double lam = chol_lambda_min_estimate(rf->L.p, n, 4, s, rf->device);
+  std::vector<double> diag(n);
+  FSTK_CUDA(cudaMemcpy2DAsync(diag.data(), 8, gram, static_cast<size_t>(n + 1) * 8, 8, n,
+                              cudaMemcpyDeviceToHost, s));
+  FSTK_CUDA(cudaStreamSynchronize(s));
+  double mx = 0.0;
+  for (double v : diag) mx = std::max(mx, v);
+  if (!(mx > 0.0) || !(lam > 0.0)) return 0.0;
+  return std::sqrt(0.5 * lam / mx);
+}
+static bool certified_full_rank(const fstk_gpu_refit* rf, double ratio) {
+  return ratio > 100.0 * static_cast<double>(rf->R) * 2.220446049250313e-16;
+}
+
+// The reference's own decision (randls.cpp:112-123) on this shard's rows:
+// TSQR, pivoted QR, Eigen's rank rule, QR or COD solution.  One shard only;
+// sharded refits stack their factors first (fstk_gpu_qr_stack).
+static void exact_solve(fstk_gpu_refit* rf, double* x_dev) {
+  QrStream qs;
+  refit_local_qr(rf, qs);
+  bool def = false;
+  cpqr_solve(qs.W.p, qs.ldw, static_cast<int>(rf->R), rf->R, x_dev, &def, rf->stream, rf->device);
+  rf->rank_def = def;
 }
 
 // Re-raises a failed nested C-ABI stage with its full error record.
@@ -2788,6 +2820,8 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
       FSTK_CUDA(cudaStreamSynchronize(s));
     }
     rf->factored = hinfo == 0;
+    // Not positive definite: the rank question goes to the pivoted-QR path
+    // (refit_solve / fstk_gpu_refit_qr_solve); until then x = 0.
     rf->rank_def = !rf->factored;
     if (rf->factored && n >= 4096) {
       cublasSetStream(h.blas, s);
@@ -2798,7 +2832,7 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
         fail(FSTK_E_COMPUTE, "potrs failed");
       count_launch();
     } else {
-      minnorm_solve(rf, gram_in, rhs_in, x_dev);
+      FSTK_CUDA(cudaMemsetAsync(x_dev, 0, static_cast<size_t>(n) * 8, s));
     }
     FSTK_CUDA(cudaStreamSynchronize(s));
     if (info) {
@@ -2881,6 +2915,50 @@ int32_t fstk_gpu_refit_apply(fstk_gpu_refit* rf, const double* s_dev, double* x_
     const double ndx = dev_norm(h.blas, n, dx.p), nx = dev_norm(h.blas, n, x_dev);
     FSTK_CUDA(cudaStreamSynchronize(s));
     if (rel_step) *rel_step = nx > 0 ? ndx / nx : ndx;
+  });
+}
+
+int32_t fstk_gpu_refit_certify(fstk_gpu_refit* rf, const double* gram_in, double* sigma_ratio,
+                               int32_t* certified, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && gram_in && certified, FSTK_E_PARAMETER, "null argument");
+    require(rf->factored, FSTK_E_PARAMETER, "refit_certify: no Cholesky factor");
+    DeviceGuard dg(rf->device);
+    rf->sigma_ratio = refit_sigma_ratio(rf, gram_in);
+    if (sigma_ratio) *sigma_ratio = rf->sigma_ratio;
+    *certified = certified_full_rank(rf, rf->sigma_ratio) ? 1 : 0;
+    if (*certified) rf->rank_def = false;
+  });
+}
+
+int32_t fstk_gpu_refit_local_qr(fstk_gpu_refit* rf, double* raug, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && raug, FSTK_E_PARAMETER, "null argument");
+    require(!rf->columns || rf->exchanged, FSTK_E_PARAMETER,
+            "column-sharded refit: exchange_layout, the all-to-all and adopt_rows come first");
+    DeviceGuard dg(rf->device);
+    QrStream qs;
+    refit_local_qr(rf, qs);
+    qs.get_r(raug, rf->R + 1);
+    FSTK_CUDA(cudaStreamSynchronize(rf->stream));
+  });
+}
+
+int32_t fstk_gpu_refit_qr_solve(fstk_gpu_refit* rf, const double* raug, double* x_dev,
+                                fstk_reestimate_info* info, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && raug && x_dev, FSTK_E_PARAMETER, "null argument");
+    DeviceGuard dg(rf->device);
+    EventTimer tq(rf->stream);
+    bool def = false;
+    cpqr_solve(raug, rf->R + 1, static_cast<int>(rf->R), rf->R, x_dev, &def, rf->stream,
+               rf->device);
+    rf->rank_def = def;
+    if (info) {
+      info->t_solve += tq.seconds();
+      info->rank_deficient = def ? 1 : 0;
+      info->qr_path = 1;
+    }
   });
 }
 
@@ -2970,6 +3048,9 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     };
     if (!rf->factored) escalate_until_factored();
     int steps = 0;
+    // Whether the Cholesky route can answer the reference's rank question;
+    // otherwise the pivoted QR of A itself decides (exact_solve).
+    bool need_qr = !rf->factored;
     if (rf->factored) {
       EventTimer tref(rf->stream);
       double prev = 1e300;
@@ -2995,17 +3076,32 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
             it = -1;
             continue;
           }
-          if (last) break;
-          // No contraction on the native Gram: cond(A)^2 eps is not small;
-          // keep the iterate but report the system as numerically rank deficient.
-          rf->rank_def = true;
+          // No (or too slow) contraction on the native Gram: cond(A)^2 eps
+          // is not small, and only the pivoted QR can decide the rank.
+          need_qr = true;
           break;
         }
         prev = step;
       }
+      if (!need_qr) {
+        rf->sigma_ratio = refit_sigma_ratio(rf, gcur);
+        need_qr = !certified_full_rank(rf, rf->sigma_ratio);
+      }
       if (info) info->t_solve += tref.seconds();
     }
-    if (info) info->refine_steps = steps;
+    if (need_qr) {
+      EventTimer tq(rf->stream);
+      exact_solve(rf, x.p);
+      if (info) info->t_solve += tq.seconds();
+    } else {
+      rf->rank_def = false;
+    }
+    if (info) {
+      info->refine_steps = steps;
+      info->rank_deficient = rf->rank_def ? 1 : 0;
+      info->qr_path = need_qr ? 1 : 0;
+      info->sigma_ratio = rf->sigma_ratio;
+    }
     rc(fstk_gpu_refit_finish(rf, x.p, core_out, info, err));
   });
 }

@@ -54,6 +54,72 @@ def _max_over_ranks(v: int, group=None) -> int:
     return int(t.item())
 
 
+def _max_over_ranks_f(v: float, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return float(v)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def _to_backend(t, group=None):
+    """Tensor as the backend moves it (NCCL: the CUDA tensor; gloo: a host copy)."""
+    import torch.distributed as dist
+
+    return t if dist.get_backend(group) == "nccl" else t.cpu()
+
+
+def qr_decide_distributed(sess, x, group=None):
+    """The reference's rank decision (randls.cpp:112-123) for a row-sharded
+    sketch: every rank folds its rows into R of [A b] (streaming TSQR), rank 0
+    stacks the factors in rank order (fstk_gpu_qr_stack), runs the pivoted QR
+    with Eigen's threshold and solves (QR or COD), and broadcasts x and the
+    flag.  Returns rank_deficient (same on every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    n1 = sess.R + 1
+    raug = _lib.device_tensor(n1 * n1, x.device)
+    sess.local_qr(raug)
+    multi = dist.is_initialized() and dist.get_world_size(group) > 1
+    rank = dist.get_rank(group) if multi else 0
+    if multi:
+        world = dist.get_world_size(group)
+        if rank == 0:
+            other = _lib.device_tensor(n1 * n1, x.device)
+            for src in range(1, world):
+                buf = _to_backend(other, group)
+                dist.recv(buf, src=src, group=group)
+                if buf is not other:
+                    other.copy_(buf)
+                refit_qr_stack(raug, other)
+        else:
+            dist.send(_to_backend(raug, group), dst=0, group=group)
+    flag = torch.zeros(1, dtype=torch.float64, device=x.device)
+    if rank == 0:
+        flag[0] = 1.0 if sess.qr_solve(raug, x) else 0.0
+    if multi:
+        for t in (x, flag):
+            buf = _to_backend(t, group)
+            dist.broadcast(buf, src=0, group=group)
+            if buf is not t:
+                t.copy_(buf)
+    deficient = bool(flag.item() != 0.0)
+    sess.info.rank_deficient = int(deficient)
+    sess.info.qr_path = 1
+    return deficient
+
+
+def refit_qr_stack(top, other):
+    from .refit import qr_stack
+
+    qr_stack(top, other)
+
+
 def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, used=None):
     """Cholesky of the summed Gram on every rank, then iterative refinement
     against the row-sharded sketch: each step needs one all-reduce of an
@@ -81,27 +147,34 @@ def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, used=None
         reduce_normal_equations(gram, rhs, group=group)
         return True
 
+    def factor():
+        # A rank whose int8 Cholesky fell back to dpotrf (or failed) must not
+        # branch alone: the factored flag is the minimum over ranks.
+        ok_local = sess.factor(gram, rhs, x)
+        return not bool(_max_over_ranks(int(not ok_local), group))
+
     def escalate_until_factored():
         while True:
             if not escalate():
                 return False
-            if sess.factor(gram, rhs, x):
+            if factor():
                 return True
 
     sess.info.refine_steps = 0
-    ok = sess.factor(gram, rhs, x)
+    ok = factor()
     if not ok:
         ok = escalate_until_factored()
-    if not ok:
-        return x
+    need_qr = not ok
     s = torch.empty_like(rhs)
     prev = float("inf")
     it = 0
-    while it < max_iter:
+    while ok and it < max_iter:
         sess.correction(x, s)
         if dist.is_initialized() and dist.get_world_size(group) > 1:
             dist.all_reduce(s, group=group)
-        step = sess.apply(s, x)
+        # Steps are computed from all-reduced data, but each rank's factor
+        # can round differently: branch on the largest.
+        step = _max_over_ranks_f(sess.apply(s, x), group)
         sess.info.refine_steps += 1
         if step <= 1e-15:
             break
@@ -113,11 +186,18 @@ def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, used=None
         last = it == max_iter - 1 and step > STALL_FLOOR
         if flat or slow or last:
             if used == 0 or not escalate_until_factored():
+                need_qr = True  # no contraction on the native Gram
                 break
             prev, it = float("inf"), 0
             continue
         prev = step
         it += 1
+    if not need_qr:
+        need_qr = not sess.certify(gram)
+    if _max_over_ranks(int(need_qr), group):
+        qr_decide_distributed(sess, x, group)
+    else:
+        sess.info.rank_deficient = 0
     return x
 
 

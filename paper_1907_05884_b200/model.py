@@ -10,6 +10,7 @@ proj/docs/format.md:56-92.
 from __future__ import annotations
 
 import ctypes as C
+import collections
 import json
 import struct
 import threading
@@ -438,7 +439,11 @@ def _header_json(model: Model) -> str:
                       allow_nan=True)
 
 
-_BASIS_MODELS: dict = {}
+# eval_basis models, least recently used last out.  Each is a one-mode
+# model holding only its coefficient tables (the evaluation workspaces are
+# allocated on a model's first evaluate call, which eval_basis never makes).
+_BASIS_MODELS: "collections.OrderedDict" = collections.OrderedDict()
+_BASIS_MODELS_MAX = 32
 
 
 def eval_basis(spec: "BasisSpec", x):
@@ -455,6 +460,10 @@ def eval_basis(spec: "BasisSpec", x):
         fns = [ModeFunction(spec, [(j, 1.0)]) for j in range(n)]
         m = Model(np.ones(n), [fns], ModelMetadata(grid_sizes=[0]))
         _BASIS_MODELS[key] = m
+        while len(_BASIS_MODELS) > _BASIS_MODELS_MAX:
+            _BASIS_MODELS.popitem(last=False)
+    else:
+        _BASIS_MODELS.move_to_end(key)
     return m.mode_values(0, x)
 
 

@@ -43,6 +43,7 @@ def _info_dict(info: ReestimateInfo) -> dict:
             "rank_deficient": bool(info.rank_deficient), "held_out": bool(info.held_out),
             "padded_rows": int(info.padded_rows), "gram_slices": int(info.gram_slices),
             "refine_steps": int(info.refine_steps), "gram_int8_ops": float(info.gram_int8_ops),
+            "qr_path": bool(info.qr_path), "sigma_ratio": float(info.sigma_ratio),
             "timings": {"prepare_s": info.t_prepare, "sketch_s": info.t_sketch,
                         "gram_s": info.t_gram, "solve_s": info.t_solve,
                         "residual_s": info.t_residual, "alloc_s": info.t_alloc}}
@@ -245,6 +246,33 @@ class RefitSession:
                                          C.byref(err)), err)
         return step.value
 
+    def certify(self, gram_t) -> bool:
+        """After the refinement converged: True when the Cholesky route
+        certifies full rank in the reference's sense (fstk_gpu_refit_certify)."""
+        ratio = C.c_double()
+        ok = C.c_int32()
+        err = Err()
+        check(lib().fstk_gpu_refit_certify(self._h, gram_t.data_ptr(), C.byref(ratio),
+                                           C.byref(ok), C.byref(err)), err)
+        self.info.sigma_ratio = ratio.value
+        if ok.value:
+            self.info.rank_deficient = 0
+        return bool(ok.value)
+
+    def local_qr(self, raug_t):
+        """(R+1)^2 CUDA float64 tensor <- upper R of this shard's [A b]
+        (column-major; fstk_gpu_refit_local_qr)."""
+        err = Err()
+        check(lib().fstk_gpu_refit_local_qr(self._h, raug_t.data_ptr(), C.byref(err)), err)
+
+    def qr_solve(self, raug_t, x_t) -> bool:
+        """Pivoted QR of the stacked factor, Eigen's rank rule, QR or COD
+        solution into x_t.  Returns rank_deficient."""
+        err = Err()
+        check(lib().fstk_gpu_refit_qr_solve(self._h, raug_t.data_ptr(), x_t.data_ptr(),
+                                            C.byref(self.info), C.byref(err)), err)
+        return bool(self.info.rank_deficient)
+
     def finish(self, x_t) -> np.ndarray:
         core = np.zeros(self.R)
         err = Err()
@@ -265,6 +293,36 @@ class RefitSession:
             self.close()
         except Exception:
             pass
+
+
+def qr_stack(top_t, other_t):
+    """top := R of [top; other] for two (n1 x n1) column-major upper factors
+    (CUDA float64 tensors of n1*n1 elements)."""
+    import torch
+
+    n1 = int(round(top_t.numel() ** 0.5))
+    err = Err()
+    stream = torch.cuda.current_stream(top_t.device).cuda_stream
+    check(lib().fstk_gpu_qr_stack(top_t.data_ptr(), other_t.data_ptr(), n1, top_t.device.index,
+                                  stream, C.byref(err)), err)
+
+
+def solve_system(a, b):
+    """randls.cpp:112-123 on the GPU: (alpha, rank_deficient, rank) of the
+    least-squares system a x = b (ColPivHouseholderQR rank with Eigen's
+    threshold; COD minimum-norm solution when deficient)."""
+    require_gpu()
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    if a.ndim != 2 or b.shape != (a.shape[0],):
+        raise make_error(2, "solve_system: a must be m x n and b of length m")
+    m, n = a.shape
+    x = np.zeros(n)
+    rank, deficient = C.c_int32(), C.c_int32()
+    err = Err()
+    check(lib().fstk_gpu_solve_system(dptr(a), m, n, dptr(b), dptr(x), C.byref(rank),
+                                      C.byref(deficient), C.byref(err)), err)
+    return x, bool(deficient.value), int(rank.value)
 
 
 def build_design_rows(model: Model, points) -> np.ndarray:

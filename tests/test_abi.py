@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert sorted(_lib.EXPORTS) == _declared()
     _lib.lib()  # the binding itself resolves every symbol
-    assert L.fstk_gpu_abi_version() == 2
+    assert L.fstk_gpu_abi_version() == 3
 
 
 def test_library_is_sm100a():

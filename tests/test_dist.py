@@ -73,13 +73,30 @@ class _ScriptedSession:
     follow a script, and every call is logged, so the escalation logic of
     dist.refine_distributed can be checked without a GPU."""
 
-    def __init__(self, factor_ok, steps, slices=5):
+    def __init__(self, factor_ok, steps, slices=5, certified=True, deficient=False):
         import types
 
         self.factor_ok = list(factor_ok)
         self.steps = list(steps)
         self.calls = []
-        self.info = types.SimpleNamespace(refine_steps=0, gram_slices=slices)
+        self.certified = certified
+        self.deficient = deficient
+        self.R = 1
+        self.info = types.SimpleNamespace(refine_steps=0, gram_slices=slices, rank_deficient=0,
+                                          qr_path=0)
+
+    def certify(self, gram):
+        self.calls.append("certify")
+        return self.certified
+
+    def local_qr(self, raug):
+        self.calls.append("local_qr")
+        raug.fill_(float(len(self.calls)))
+
+    def qr_solve(self, raug, x):
+        self.calls.append("qr_solve")
+        x.fill_(7.0)
+        return self.deficient
 
     def factor(self, gram, rhs, x):
         self.calls.append("factor")
@@ -131,9 +148,31 @@ def test_refine_seven_planes_go_straight_to_native():
 
 
 def test_refine_native_stall_does_not_loop():
-    s = _ScriptedSession([True], [1e-3, 9e-4])
-    _refine(s, used=0)
+    # No contraction on the native Gram: only the pivoted QR can decide.
+    s = _ScriptedSession([True], [1e-3, 9e-4], deficient=True)
+    x = _refine(s, used=0)
     assert "native" not in s.calls and s.calls.count("apply") == 2
+    assert s.calls[-2:] == ["local_qr", "qr_solve"] and "certify" not in s.calls
+    assert s.info.rank_deficient == 1 and float(x[0]) == 7.0
+
+
+def test_refine_converged_certified_skips_qr():
+    s = _ScriptedSession([True], [1e-9, 1e-16])
+    _refine(s)
+    assert s.calls[-1] == "certify" and "local_qr" not in s.calls
+    assert s.info.rank_deficient == 0
+
+
+def test_refine_converged_uncertified_goes_to_qr():
+    s = _ScriptedSession([True], [1e-9, 1e-16], certified=False)
+    _refine(s)
+    assert s.calls[-3:] == ["certify", "local_qr", "qr_solve"] and s.info.qr_path == 1
+
+
+def test_refine_native_not_pd_goes_to_qr():
+    s = _ScriptedSession([False], [], slices=0)
+    _refine(s, used=0)
+    assert s.calls == ["factor", "local_qr", "qr_solve"]
 
 
 def test_refine_fast_contraction_keeps_five_planes():
@@ -157,6 +196,50 @@ def _gloo_refine_worker(rank, world, port, q):
         q.put((rank, s.calls))
     finally:
         dist.destroy_process_group()
+
+
+def _gloo_qr_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1907_05884_b200 import dist as D
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    stacked = []
+    D.refit_qr_stack = lambda top, other: stacked.append(float(other[0]))
+    try:
+        # Only rank 1 fails the certificate: every rank still takes the QR
+        # path, rank 0 stacks rank 1's factor, and x / the flag come from rank 0.
+        s = _ScriptedSession([True], [1e-9, 1e-16], certified=(rank == 0), deficient=True)
+        x = _refine(s)
+        q.put((rank, s.calls, stacked, float(x[0]), s.info.rank_deficient))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_refine_qr_decision_agrees_across_gloo_ranks():
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_gloo_qr_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = {r: rest for r, *rest in (q.get(timeout=120) for _ in ps)}
+    for p in ps:
+        p.join(timeout=60)
+    calls0, st0, x0, d0 = out[0]
+    calls1, st1, x1, d1 = out[1]
+    assert calls0[-3:] == ["certify", "local_qr", "qr_solve"]
+    assert calls1[-2:] == ["certify", "local_qr"]  # rank 1 only contributes its factor
+    assert len(st0) == 1 and st1 == []
+    assert x0 == x1 == 7.0 and d0 == d1 == 1
 
 
 def test_refine_escalation_agrees_across_gloo_ranks():

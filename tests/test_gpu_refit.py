@@ -363,9 +363,19 @@ def test_cached_device_blocks_reused_bit_identically():
     m = synth.random_model((8, 8, 8), (8, 8, 8), 5, seed=51)
     pts = synth.uniform_points(400_000, 3, seed=52)
     vals = m.evaluate_batch(pts) + 1e-3 * np.random.default_rng(53).normal(size=400_000)
-    a, ia = F.reestimate_core(m, pts, vals, seed=54, sample_rows=131_072)
-    b, ib = F.reestimate_core(m, pts, vals, seed=54, sample_rows=131_072)
-    assert np.array_equal(a.core, b.core)
-    assert ia["residual_after"] == ib["residual_after"]
-    assert _lib.trim_device_cache(-1) >= 256 << 20
+    prev = _lib.set_device_cache(2)  # persistent: blocks survive between sessions
+    try:
+        a, ia = F.reestimate_core(m, pts, vals, seed=54, sample_rows=131_072)
+        b, ib = F.reestimate_core(m, pts, vals, seed=54, sample_rows=131_072)
+        assert np.array_equal(a.core, b.core)
+        assert ia["residual_after"] == ib["residual_after"]
+        assert _lib.trim_device_cache(-1) >= 256 << 20
+        assert _lib.trim_device_cache(-1) == 0
+    finally:
+        _lib.set_device_cache(prev)
+    # Default policy (per session): reestimate_core returns holding no cached
+    # blocks, and the result is the same bits as on reused blocks.
+    _lib.set_device_cache(1)
+    c, _ = F.reestimate_core(m, pts, vals, seed=54, sample_rows=131_072)
+    assert np.array_equal(a.core, c.core)
     assert _lib.trim_device_cache(-1) == 0
