@@ -311,6 +311,12 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* refit, const double* gram,
  * pivoted QR, Eigen's rank rule (threshold min(rows, R) eps max|R_ii|), the
  * QR solution or the COD minimum-norm solution into x, and
  * info->rank_deficient. */
+/* Columns cols[0..ncols) of this shard's sketched A (index R = the
+ * right-hand side b) in the reference's row order, column c at
+ * out + c * rows_local (x2 for FFT): single-column parity checks at full size
+ * without copying A (68.7 GB at C2) to the host. */
+int32_t fstk_gpu_refit_sketched_columns(const fstk_gpu_refit* refit, const int64_t* cols,
+                                        int64_t ncols, double* out, fstk_gpu_error* err);
 int32_t fstk_gpu_refit_certify(fstk_gpu_refit* refit, const double* gram, double* sigma_ratio,
                                int32_t* certified, fstk_gpu_error* err);
 int32_t fstk_gpu_refit_local_qr(fstk_gpu_refit* refit, double* raug, fstk_gpu_error* err);

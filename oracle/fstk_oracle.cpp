@@ -1149,6 +1149,54 @@ int oracle_refit_system(MODEL_ARGS, const double* pts, const double* vals,
   });
 }
 
+// Sketched columns at arbitrary indices (column r_total = the right-hand
+// side b), plus the plan's sampled rows: full-size parity checks of single
+// columns without forming A (randls.cpp:313-348, one column at a time).
+int oracle_refit_column_set(MODEL_ARGS, const double* pts, const double* vals,
+                            std::int64_t q, int pd, std::uint64_t seed,
+                            std::uint64_t working_subset, std::uint64_t sample_rows,
+                            int transform, double validation_fraction,
+                            const std::int64_t* cols, std::int64_t ncols, double* a,
+                            std::uint64_t* rows_out) {
+  return guarded([&] {
+    const Model m = build_model(MODEL_PASS);
+    const std::int64_t r_total = m.size();
+    const std::uint64_t s = resolve_sample_rows(sample_rows, r_total);
+    SketchCfg cfg{seed, working_subset, sample_rows, transform,
+                  validation_fraction};
+    const Workspace ws = prepare(m, pts, vals, q, pd, cfg);
+    const auto tables = mode_value_tables(m, ws.train_points.data(),
+                                          static_cast<std::int64_t>(ws.q_w));
+    const SketchPlan plan = make_plan(ws.q_w, s, mix_seed(seed, kSketchTag));
+    const bool fft = transform == Fft;
+    const std::int64_t s_rows = static_cast<std::int64_t>(plan.rows.size());
+    const std::int64_t lda = fft ? 2 * s_rows : s_rows;
+    const std::int64_t qw = static_cast<std::int64_t>(ws.q_w);
+    parallel_for(static_cast<std::size_t>(ncols),
+                 [&](std::size_t begin, std::size_t end) {
+                   std::vector<double> scratch;
+                   std::vector<cd> cscratch;
+                   std::vector<double> col(static_cast<std::size_t>(qw));
+                   for (std::size_t c = begin; c < end; ++c) {
+                     const std::int64_t ell = cols[c];
+                     require(ell >= 0 && ell <= r_total, Parameter, "column out of range");
+                     double* out = a + static_cast<std::int64_t>(c) * lda;
+                     if (ell < r_total) {
+                       design_column(m, tables, qw, ell, col.data());
+                       sketch_column(plan, transform, ws.q_w,
+                                     [&](std::uint64_t i) { return col[i]; },
+                                     scratch, cscratch, out, fft ? out + s_rows : nullptr);
+                     } else {
+                       sketch_column(plan, transform, ws.q_w,
+                                     [&](std::uint64_t i) { return ws.train_values[i]; },
+                                     scratch, cscratch, out, fft ? out + s_rows : nullptr);
+                     }
+                   }
+                 });
+    if (rows_out) std::copy(plan.rows.begin(), plan.rows.end(), rows_out);
+  });
+}
+
 // Only the sketched columns in [col_begin, col_end) (and b when include_rhs):
 // used by the CPU baseline to time a bounded sample of the transform stage.
 int oracle_refit_columns(MODEL_ARGS, const double* pts, const double* vals,

@@ -388,6 +388,31 @@ def refit_columns(model, points, values, col_begin, col_end, seed=0, sample_rows
     return a
 
 
+def refit_column_set(model, points, values, cols, seed=0, sample_rows=0,
+                     working_subset=1 << 20, transform="dct", validation_fraction=0.05):
+    """Sketched columns at the given indices (index R = the right-hand side b)
+    and the plan's sampled rows: (a (system_rows x len(cols)), rows)."""
+    f = flat_of(model)
+    p = _fpoints(points)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    t = TRANSFORMS[transform]
+    sz = _Sizes()
+    args = _margs(f)
+    _check(lib().oracle_refit_sizes(*args, C.c_int64(p.shape[0]), C.c_uint64(seed),
+                                    C.c_uint64(working_subset), C.c_uint64(sample_rows),
+                                    C.c_int(t), C.c_double(validation_fraction), C.byref(sz)))
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    a = np.zeros((sz.system_rows, c.size), order="F")
+    rows = np.zeros(int(sz.sample_rows), dtype=np.uint64)
+    _check(lib().oracle_refit_column_set(*args, _dp(p), _dp(v), C.c_int64(p.shape[0]),
+                                         C.c_int(p.shape[1]), C.c_uint64(seed),
+                                         C.c_uint64(working_subset), C.c_uint64(sample_rows),
+                                         C.c_int(t), C.c_double(validation_fraction),
+                                         c.ctypes.data_as(C.POINTER(C.c_int64)),
+                                         C.c_int64(c.size), _dp(a), _u64p(rows)))
+    return a, rows
+
+
 def relative_residual(model_flat, points, values):
     """randls.cpp:350-356."""
     pred = evaluate_batch(model_flat, points)

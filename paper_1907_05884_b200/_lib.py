@@ -93,6 +93,7 @@ EXPORTS = [
     "fstk_gpu_sample_without_replacement", "fstk_gpu_make_plan", "fstk_gpu_set_devices",
     "fstk_gpu_cholesky_device", "fstk_gpu_refit_certify", "fstk_gpu_refit_local_qr",
     "fstk_gpu_refit_qr_solve", "fstk_gpu_qr_stack", "fstk_gpu_solve_system",
+    "fstk_gpu_refit_sketched_columns",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -174,6 +175,8 @@ def lib():
     L.fstk_gpu_refit_finish.argtypes = [VP, VP, DP, C.POINTER(ReestimateInfo), C.POINTER(Err)]
     L.fstk_gpu_refit_certify.argtypes = [VP, VP, DP, C.POINTER(C.c_int32), C.POINTER(Err)]
     L.fstk_gpu_refit_local_qr.argtypes = [VP, VP, C.POINTER(Err)]
+    L.fstk_gpu_refit_sketched_columns.argtypes = [VP, C.POINTER(C.c_int64), C.c_int64, DP,
+                                                  C.POINTER(Err)]
     L.fstk_gpu_refit_qr_solve.argtypes = [VP, VP, VP, C.POINTER(ReestimateInfo), C.POINTER(Err)]
     L.fstk_gpu_qr_stack.argtypes = [VP, VP, C.c_int64, C.c_int32, VP, C.POINTER(Err)]
     L.fstk_gpu_solve_system.argtypes = [DP, C.c_int64, C.c_int64, DP, DP, C.POINTER(C.c_int32),

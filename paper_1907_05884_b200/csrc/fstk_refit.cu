@@ -3171,6 +3171,39 @@ int32_t fstk_gpu_refit_sketched(const fstk_gpu_refit* rf, double* a, double* b, 
   });
 }
 
+// Columns `cols` of this shard's sketched A (index R = b) in reference row
+// order, column c at out + c * rows_local (rows_local = 2 x rows for FFT).
+int32_t fstk_gpu_refit_sketched_columns(const fstk_gpu_refit* rf, const int64_t* cols,
+                                        int64_t ncols, double* out, fstk_gpu_error* err) {
+  return guarded(err, [&] {
+    require(rf && (ncols == 0 || (cols && out)), FSTK_E_PARAMETER, "null argument");
+    require(!rf->columns || rf->exchanged, FSTK_E_PARAMETER,
+            "column-sharded refit: exchange_layout, the all-to-all and adopt_rows come first");
+    require(!rf->none, FSTK_E_PARAMETER,
+            "transform none never materialises A; use fstk_gpu_refit_sketched");
+    DeviceGuard dg(rf->device);
+    const bool fft = rf->cfg.transform == FSTK_TRANSFORM_FFT;
+    const int64_t lr = rf->local_rows;
+    const int64_t arows = fft ? 2 * lr : lr;
+    std::vector<int64_t> order;  // source row (shard-local) of each output row
+    for (uint64_t sidx = 0; sidx < rf->S; ++sidx) {
+      const int64_t dst = rf->in.dest_of_sample[sidx];
+      if (dst >= rf->row_lo && dst < rf->row_hi) order.push_back(dst - rf->row_lo);
+    }
+    std::vector<double> col(static_cast<size_t>(std::max<int64_t>(arows, 1)));
+    for (int64_t c = 0; c < ncols; ++c) {
+      require(cols[c] >= 0 && cols[c] <= rf->R, FSTK_E_PARAMETER, "column index out of range");
+      const double* src = cols[c] == rf->R ? rf->b.p : rf->A.p + cols[c] * arows;
+      FSTK_CUDA(cudaMemcpy(col.data(), src, static_cast<size_t>(arows) * 8, cudaMemcpyDeviceToHost));
+      double* o = out + c * arows;
+      for (int64_t r = 0; r < static_cast<int64_t>(order.size()); ++r) {
+        o[r] = col[order[r]];
+        if (fft) o[lr + r] = col[lr + order[r]];
+      }
+    }
+  });
+}
+
 int32_t fstk_gpu_reestimate_core(const fstk_gpu_model* m, const double* points,
                                  const double* values, int64_t q, int32_t d,
                                  const fstk_sketch_cfg* cfg, double* core_out,

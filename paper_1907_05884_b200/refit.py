@@ -199,6 +199,17 @@ class RefitSession:
               err)
         return a, b
 
+    def sketched_columns(self, cols) -> np.ndarray:
+        """Columns `cols` of the sketched A (index R = b) in reference row order."""
+        c = np.ascontiguousarray(cols, dtype=np.int64)
+        n = C.c_int64()
+        err = Err()
+        check(lib().fstk_gpu_refit_sketched(self._h, None, None, C.byref(n), C.byref(err)), err)
+        out = np.zeros((n.value, c.size), order="F")
+        check(lib().fstk_gpu_refit_sketched_columns(self._h, c.ctypes.data_as(C.POINTER(C.c_int64)),
+                                                    c.size, dptr(out), C.byref(err)), err)
+        return out
+
     def normal_equations(self, gram_t, rhs_t):
         """Writes this shard's partial A^T A (lower triangle, column-major) and
         A^T b into CUDA float64 tensors of R*R and R elements."""
