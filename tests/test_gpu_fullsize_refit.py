@@ -8,12 +8,13 @@ CPU oracle, so each run is checked through properties that hold at any size:
   * 64 seeded columns of A, plus b, equal the oracle's per-column sketch
     (design_column + sign + DCT + sampling, randls.cpp:44-105) bit for bit;
   * the returned core is the least-squares solution of that bit-exact A:
-    - C2: against the QR solution of the same A (streaming TSQR on the GPU,
-      then R x = Q^T b), within 1e-9 relative;
-    - everywhere: the a-posteriori bound ||x - x*|| <= ||A^T (b - A x)|| /
-      sigma_min(A)^2, with sigma_min from the Cholesky-side certificate (a
-      100x margin on sigma^2 for the estimate), within 1e-9 of ||x||;
-  * the reference's rank decision: full rank, certified, no QR path needed.
+    within 1e-9 relative of the QR solution of the same A (a second session
+    re-sketches A bit for bit -- the first one's Gram and Cholesky factor are
+    gone, so even C4's 137 GB A leaves room -- then streaming TSQR on the GPU
+    and R x = Q^T b), with a normal-equation residual ||A^T (b - A x)|| at the
+    QR solution's level;
+  * the reference's rank decision: full rank, certified by the Cholesky
+    route, no QR path needed.
 C2 is the bench's own workload (bench.workload: the fitted model and the
 jittered-mesh flame field); C4 and C5 use seeded models of their shapes with
 BASELINE's fields plus noise."""
@@ -27,7 +28,7 @@ from paper_1907_05884_b200.dist import refine_distributed
 pytestmark = pytest.mark.gpu
 
 
-def _refit_parity(O, model, pts, vals, S, seed=0, qr_check=False, ncols=64):
+def _refit_parity(O, model, pts, vals, S, seed=0, ncols=64):
     import torch
 
     R = int(np.prod(model.ranks))
@@ -46,35 +47,35 @@ def _refit_parity(O, model, pts, vals, S, seed=0, qr_check=False, ncols=64):
         rhs = torch.empty(R, dtype=torch.float64, device=dev)
         sess.normal_equations(gram, rhs)
         x = refine_distributed(sess, gram, rhs)
+        del gram, rhs
+        core = sess.finish(x)
         info = sess.info_dict()
         assert not info["rank_deficient"] and not info["qr_path"]
-        maxcol2 = float(gram.view(R, R).diagonal().max())
-        del gram, rhs
+        assert np.isfinite(core).all()
         s = torch.empty_like(x)
         sess.correction(x, s)
-        sigma2 = info["sigma_ratio"] ** 2 * maxcol2 / 100.0  # 100x margin on the estimate
-        bound = float(torch.linalg.norm(s)) / sigma2 / float(torch.linalg.norm(x))
-        assert bound <= 1e-9, f"a-posteriori LS error bound {bound:.3e}"
-        if qr_check:
-            torch.cuda.empty_cache()
-            n1 = R + 1
-            raug = _lib.device_tensor(n1 * n1, dev)
-            sess.local_qr(raug)
-            rq = raug.view(n1, n1).t()  # column-major storage -> [row, col]
-            x_qr = torch.linalg.solve_triangular(rq[:R, :R].contiguous(), rq[:R, R:].contiguous(),
-                                                 upper=True)[:, 0]
-            del raug, rq
-            rel = float(torch.linalg.norm(x - x_qr) / torch.linalg.norm(x_qr))
-            assert rel <= 1e-9, f"core vs QR solution of the same A: {rel:.3e}"
-            # the refined core reaches the QR solution's normal-equation residual level
-            s_qr = torch.empty_like(x)
-            sess.correction(x_qr, s_qr)
-            assert float(torch.linalg.norm(s)) <= 10 * float(torch.linalg.norm(s_qr)) + 1e-300
-        core = sess.finish(x)
-        assert np.isfinite(core).all()
-        return core, sess.info_dict()
     finally:
         sess.close()
+    torch.cuda.empty_cache()
+    # The QR solution of the same (bit-exact, re-sketched) A.
+    n1 = R + 1
+    sess = F.RefitSession(model, pts, vals, seed=seed, sample_rows=S)
+    try:
+        raug = _lib.device_tensor(n1 * n1, dev)
+        sess.local_qr(raug)
+        rq = raug.view(n1, n1).t()  # column-major storage -> [row, col]
+        x_qr = torch.linalg.solve_triangular(rq[:R, :R].contiguous(), rq[:R, R:].contiguous(),
+                                             upper=True)[:, 0]
+        del raug, rq
+        torch.cuda.empty_cache()
+        rel = float(torch.linalg.norm(x - x_qr) / torch.linalg.norm(x_qr))
+        assert rel <= 1e-9, f"core vs QR solution of the same A: {rel:.3e}"
+        s_qr = torch.empty_like(x)
+        sess.correction(x_qr, s_qr)
+        assert float(torch.linalg.norm(s)) <= 10 * float(torch.linalg.norm(s_qr))
+    finally:
+        sess.close()
+    return core, info, rel
 
 
 def test_c2_fullsize_noisy_refit_parity(O):
@@ -82,7 +83,7 @@ def test_c2_fullsize_noisy_refit_parity(O):
 
     model, pts, vals, c = bench.workload("C2", 0, 0)
     R = int(np.prod(model.ranks))
-    _, info = _refit_parity(O, model, pts, vals, c["m_factor"] * R, seed=0, qr_check=True)
+    _, info, _ = _refit_parity(O, model, pts, vals, c["m_factor"] * R, seed=0)
     assert info["sample_rows"] == 262_144 and info["padded_rows"] == 1 << 20
 
 
@@ -97,7 +98,7 @@ def test_c4_fullsize_noisy_refit_parity(O):
     vals = np.tanh((z - 0.3 - 0.4 * t - 0.05 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y)) / 0.02)
     vals = vals + 1e-2 * rng.normal(size=n)
     R = int(np.prod(model.ranks))
-    _, info = _refit_parity(O, model, np.asfortranarray(pts), vals, c["m_factor"] * R, seed=4)
+    _, info, _ = _refit_parity(O, model, np.asfortranarray(pts), vals, c["m_factor"] * R, seed=4)
     assert info["sample_rows"] == 524_288
 
 
@@ -107,5 +108,5 @@ def test_c5_field_fullsize_noisy_refit_parity(O):
     pts = synth.uniform_points(1 << 22, 3, seed=51)
     vals = synth.flame_field(pts, seed=52, n_gauss=8)
     R = int(np.prod(model.ranks))
-    _, info = _refit_parity(O, model, pts, vals, c["m_factor"] * R, seed=5)
+    _, info, _ = _refit_parity(O, model, pts, vals, c["m_factor"] * R, seed=5)
     assert info["sample_rows"] == 262_144
