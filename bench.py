@@ -274,6 +274,48 @@ def traffic_from_profile(cfg: str):
     return None, None
 
 
+L2_BYTES = 126 << 20
+
+
+def arm_config(args, model, cfgd, n: int, nf: int, world: int) -> dict:
+    """The `config` of both arms (ours and --impl reference): the workload one
+    step processes on each rank, whatever sample the host arm times."""
+    in_bytes = n * model.order * 8 + n * 8
+    return {"workload": f"{args.config}: evaluate {n} points per rank"
+                        + (f" x {nf} fields (value counts field-points)" if nf > 1 else "")
+                        + f", ranks {tuple(model.ranks)}, Legendre p={cfgd['degrees'][0]}, "
+                          f"<= {cfgd['nnz']} nnz",
+            "points_per_rank": n,
+            "l2": ("inputs (%d MB) exceed 2x the 126 MB L2; no flush needed" % (in_bytes >> 20))
+                  if in_bytes > 2 * L2_BYTES else
+                  "L2 flushed between steps (512 MB buffer write, untimed)",
+            "parallelism": f"point-sharded x{world}"}
+
+
+def int8_peak(dev) -> dict:
+    """Live int8 x int8 -> int32 GEMM ceiling of this GPU (cuBLASLt through
+    torch._int_mm, TN 8192 x 8192 x 16384, best of 5 after warm-up): the
+    denominator of the sliced Gram's roofline."""
+    import torch
+
+    a = torch.randint(-127, 128, (8192, 16384), dtype=torch.int8, device=dev)
+    b = torch.randint(-127, 128, (8192, 16384), dtype=torch.int8, device=dev).t()
+    for _ in range(3):
+        torch._int_mm(a, b)
+    best = float("inf")
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return {"tops": 2.0 * 8192 * 8192 * 16384 / (best * 1e-3) / 1e12,
+            "source": "live cuBLASLt int8 TN GEMM 8192x8192x16384 via torch._int_mm, best of 5 "
+                      "(burst; MEASURED_PEAKS.json has no int8 entry)"}
+
+
 # ------------------------------------------------------------ reference arm ---
 def run_reference(args):
     rank, world, _ = dist_env()
@@ -298,17 +340,22 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.mean(times))
     value = n / (ms * 1e-3)
+    nfull = pts.shape[0]
+    nf = 8 if args.config == "C5" else 1
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config}: eval of {pts.shape[0]} points (bounded sample "
-                                   f"of {n} per step on the host)",
-                       "ranks": model.ranks},
+            "data": DATA_DESC.get(args.config, "synthetic"), "impl": "reference",
+            "config": arm_config(args, model, c, nfull, nf, world),
+            "sample": {"points_per_step": n, "points_in_config": nfull,
+                       "full_step_seconds_extrapolated": nfull * nf / value,
+                       "note": "each step times the first %d of the %d points of this config "
+                               "(per-point cost does not depend on position); a full step "
+                               "would take %.1f s on these cores" % (n, nfull, nfull * nf / value)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{n} points per step of the {args.config} workload; oracle "
-                                       "restatement of evaluate_batch (reference cannot build: "
-                                       "Eigen absent), all host threads"},
+                             "sample": f"{n} of {nfull} points per step of the {args.config} "
+                                       "workload; oracle restatement of evaluate_batch (the "
+                                       "reference cannot build: Eigen absent), all host threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     if vals is not None and not args.no_refit:
@@ -379,8 +426,7 @@ def main():
     # Between timed steps: inputs larger than L2 need no flush; otherwise a
     # 512 MB buffer is overwritten (outside the per-step event pairs).
     in_bytes = n * d * 8 + n * 8
-    l2_bytes = 126 << 20
-    flush = None if in_bytes > 2 * l2_bytes else torch.empty(64 << 20, dtype=torch.float64,
+    flush = None if in_bytes > 2 * L2_BYTES else torch.empty(64 << 20, dtype=torch.float64,
                                                             device=dev)
     launches0 = F.launch_count()
     clocks = Clocks(local)
@@ -404,11 +450,33 @@ def main():
     ms = maxreduce(ms, world, dev)
     value = world * n * NF / (ms * 1e-3)
 
-    # ---- roofline of the dominant kernel (the DMMA contraction)
-    c_ms, c_n = prof["contract"]
-    m_ms, m_n = prof["mode_tables"]
-    per_launch_pts = n * NF * args.steps / max(c_n, 1)
-    achieved = fc * n * NF * args.steps / (c_ms * 1e-3) / 1e12 if c_ms > 0 else None
+    # ---- roofline of the dominant kernel (the DMMA contraction).  In the
+    # timed steps the mode-table kernel of chunk i+1 overlaps the contraction
+    # of chunk i on a second stream, so their event durations overlap.  The
+    # kernel's own duration comes from an isolated pass of the same chunks on
+    # one stream (fstk_gpu_eval_serialize; values unchanged).
+    conc = {k: prof[k] for k in ("contract", "mode_tables")}
+    iso_steps = 3
+    _lib.eval_serialize(True)
+    eval_step()
+    torch.cuda.synchronize()
+    _lib.profile_read()
+    _lib.profile_enable(True)
+    e_iso = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    e_iso[0].record(stream)
+    for _ in range(iso_steps):
+        eval_step()
+    e_iso[1].record(stream)
+    torch.cuda.synchronize()
+    _lib.profile_enable(False)
+    _lib.eval_serialize(False)
+    iso = _lib.profile_read()
+    iso_step_ms = e_iso[0].elapsed_time(e_iso[1]) / iso_steps
+    c_ms, c_n = iso["contract"]
+    m_ms, m_n = iso["mode_tables"]
+    assert c_ms / iso_steps <= iso_step_ms * 1.001, "contraction time exceeds its step"
+    per_launch_pts = n * NF * iso_steps / max(c_n, 1)
+    achieved = fc * n * NF * iso_steps / (c_ms * 1e-3) / 1e12 if c_ms > 0 else None
     traffic, tpts = traffic_from_profile(args.config)
     kr = os.environ.get("FSTK_CONTRACT_KR")
     use_kr = (kr != "0") if kr is not None and model.order in (3, 4) else model.order == 4
@@ -421,15 +489,20 @@ def main():
             "peak_source": "fp64 DMMA throughput measured live on this GPU by fstk_gpu_fp64_peak "
                            "(MEASURED_PEAKS.json has no fp64 entry); DFMA measured %.1f" % peak_fma,
             "algorithmic_flops_per_point": fc,
+            "ms_per_launch": c_ms / max(c_n, 1), "launches_per_step": c_n / iso_steps,
+            "points_per_launch": per_launch_pts,
             "share_of_step": c_ms / (c_ms + m_ms) if c_ms + m_ms > 0 else None,
+            "isolated_step_ms": iso_step_ms,
+            "contract_ms_per_step": c_ms / iso_steps,
+            "mode_tables_ms_per_step": m_ms / iso_steps,
             "step_tflops": (fc + fm) * n * NF / (ms * 1e-3) / 1e12,
             "step_frac": (fc + fm) * n * NF / (ms * 1e-3) / 1e12 / peak_mma,
-            "mode_tables_ms_per_step": m_ms / args.steps,
-            "contract_ms_per_step": c_ms / args.steps,
-            "note": "the mode-table kernel of chunk i+1 runs concurrently with the contraction of "
-                    "chunk i on a second stream (both use the fp64 pipe), so the per-launch "
-                    "event durations overlap: `frac` is the contraction measured while sharing "
-                    "the SMs, `step_frac` is the whole evaluation step (all 73,120 flop/pt)"}
+            "concurrent_event_ms_per_step": {k: v[0] / args.steps for k, v in conc.items()},
+            "note": "achieved/frac: the contraction kernel's algorithmic flops over its own "
+                    "event-timed duration in an isolated pass of the same chunks on one stream "
+                    "(%d steps). The timed steps overlap it with the next chunk's mode-table "
+                    "kernel on a second stream; step_frac is the whole evaluation step "
+                    "(all %d flop/pt) at ms_per_step" % (iso_steps, int(fc + fm))}
 
     # ---- e2e through the host C-ABI (pinned host buffers)
     if NF > 1:
@@ -485,16 +558,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": DATA_DESC.get(args.config, "synthetic"),
-            "config": {"workload": f"{args.config}: evaluate {n} points per rank"
-                                   + (f" x {NF} fields (value counts field-points)" if NF > 1 else "")
-                                   + f", ranks "
-                                   f"{tuple(model.ranks)}, Legendre p={cfgd['degrees'][0]}, "
-                                   f"<= {cfgd['nnz']} nnz",
-                       "points_per_rank": n, "flops_per_point": fc + fm,
-                       "l2": ("inputs (%d MB) exceed 2x the 126 MB L2; no flush needed"
-                              % (in_bytes >> 20)) if flush is None else
-                             "L2 flushed between steps (512 MB buffer write, untimed)",
-                       "parallelism": f"point-sharded x{world}"},
+            "config": arm_config(args, model, cfgd, n, NF, world),
+            "flops_per_point": fc + fm,
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": ck}
 
     # ---- refit (one problem; rows sharded across ranks; one all-reduce)
@@ -548,18 +613,20 @@ def sketch_roofline(model, info, t, transform, world):
                       "stages + post-rotation + sampled rows)"}
 
 
-def gram_roofline(gram_flops, info, t, peak_fp64):
+def gram_roofline(gram_flops, info, t, peak_fp64, i8=None):
     """Gram stage against its roofline.  Native: fp64 SYRK flops vs the DMMA
-    peak.  Sliced (fstk_gram.cu): int8 ops issued vs the B200 dense int8
-    tensor peak (4.5 POPS nominal; MEASURED_PEAKS.json has no int8 entry),
-    plus the fp64-equivalent rate (R(R+1)S/t) that the DGEMM Gram would need
-    to match it."""
+    peak.  Sliced (fstk_gram.cu): int8 ops issued vs the int8 GEMM ceiling
+    measured live on this GPU (int8_peak; MEASURED_PEAKS.json has no int8
+    entry), plus the fp64-equivalent rate (R(R+1)S/t) that the DGEMM Gram
+    would need to match it."""
     if not t:
         return None
     if info["gram_slices"] > 0 and info.get("gram_int8_ops"):
         ach = info["gram_int8_ops"] / t / 1e12
-        return {"bound": "tensor", "achieved": ach, "peak": 4500.0, "unit": "TOP/s (int8)",
-                "frac": ach / 4500.0, "peak_source": "nominal B200 dense int8 (= the fp8 rate in B200_PROFILING.md); cuBLASLt int8 TN measured 2.84 POPS here (profiles/int8_probe_r01.txt)",
+        pk = i8["tops"] if i8 else 4500.0
+        src = i8["source"] if i8 else "nominal B200 dense int8 (live probe unavailable)"
+        return {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TOP/s (int8)",
+                "frac": ach / pk, "peak_source": src,
                 "fp64_equivalent_tflops": gram_flops / t / 1e12, "fp64_peak_tflops": peak_fp64,
                 "kernel": f"cuBLASLt int8 IMMA GEMMs, one per CRT modulus, at plane-accuracy level "
                           f"{info['gram_slices']} (residue/fold kernels in fstk_gram.cu)"}
@@ -678,7 +745,8 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=No
                          "residual": tm["residual_s"]},
             "host_wall_s": info.get("wall_s"),
             "gram_slices": info["gram_slices"], "refine_steps": info["refine_steps"],
-            "gram_roofline": gram_roofline(gram_flops, info, tm["gram_s"], peak),
+            "gram_roofline": gram_roofline(gram_flops, info, tm["gram_s"], peak,
+                                           int8_peak(dev) if info["gram_slices"] > 0 else None),
             "sketch_roofline": sketch_roofline(model, info, tm["sketch_s"], tform, world),
             "residual_before": info["residual_before"], "residual_after": info["residual_after"],
             "rank_deficient": info["rank_deficient"],

@@ -129,6 +129,11 @@ uint64_t fstk_gpu_launch_count(void);
  * policy.  FSTK_DEVICE_CACHE=0/1/2 sets the initial policy.  No reference
  * counterpart (the reference has no device memory). */
 int32_t fstk_gpu_set_device_cache(int32_t policy);
+/* Measurement mode (no reference counterpart): on != 0 runs every chunk of a
+ * device-resident evaluation on one stream, so the mode-table and DMMA
+ * contraction kernels do not overlap and their profiled durations are their
+ * own (bench.py's roofline).  Values are unchanged.  Returns the previous. */
+int32_t fstk_gpu_eval_serialize(int32_t on);
 /* Returns the cached blocks to the driver: one device, or all when
  * device < 0.  Returns the bytes released. */
 uint64_t fstk_gpu_trim_device_cache(int32_t device);

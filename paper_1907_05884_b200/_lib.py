@@ -93,7 +93,7 @@ EXPORTS = [
     "fstk_gpu_sample_without_replacement", "fstk_gpu_make_plan", "fstk_gpu_set_devices",
     "fstk_gpu_cholesky_device", "fstk_gpu_refit_certify", "fstk_gpu_refit_local_qr",
     "fstk_gpu_refit_qr_solve", "fstk_gpu_qr_stack", "fstk_gpu_solve_system",
-    "fstk_gpu_refit_sketched_columns",
+    "fstk_gpu_refit_sketched_columns", "fstk_gpu_eval_serialize",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -114,6 +114,8 @@ def lib():
     L.fstk_gpu_abi_version.restype = C.c_int32
     L.fstk_gpu_device_count.restype = C.c_int32
     L.fstk_gpu_launch_count.restype = C.c_uint64
+    L.fstk_gpu_eval_serialize.argtypes = [C.c_int32]
+    L.fstk_gpu_eval_serialize.restype = C.c_int32
     L.fstk_gpu_set_device_cache.argtypes = [C.c_int32]
     L.fstk_gpu_set_device_cache.restype = C.c_int32
     L.fstk_gpu_trim_device_cache.argtypes = [C.c_int32]
@@ -214,6 +216,12 @@ def dptr(a):
 
 def launch_count() -> int:
     return int(lib().fstk_gpu_launch_count())
+
+
+def eval_serialize(on: bool) -> bool:
+    """Measurement mode: chunks of a device evaluation on one stream (no
+    mode/contraction overlap).  Returns the previous setting."""
+    return bool(lib().fstk_gpu_eval_serialize(1 if on else 0))
 
 
 def set_device_cache(policy: int) -> int:

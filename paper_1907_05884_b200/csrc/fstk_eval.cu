@@ -1384,9 +1384,15 @@ void ensure_chunk_workspace(const fstk_gpu_model* m) {
   }
 }
 
+// fstk_gpu_eval_serialize: every chunk on the first workspace stream, so the
+// mode-table and contraction kernels never overlap (a measurement mode: their
+// event durations are then the kernels' own, for the roofline).
+static std::atomic<int> g_eval_serial{0};
+
 void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, const double* pts,
                           int64_t ldp, int64_t n, double* out, cudaStream_t s) {
   ensure_chunk_workspace(m);
+  const int lanes = g_eval_serial.load() ? 1 : 2;
   const int64_t CH = m->chunk_points;
   int64_t toff[kMaxOrder], tot = 0;
   const int64_t ldt = round_up(CH, 128);
@@ -1407,12 +1413,13 @@ void evaluate_device_core(const fstk_gpu_model* m, const double* core_host, cons
   for (auto& ck : m->chunk) FSTK_CUDA(cudaStreamWaitEvent(ck.stream, m->fork_ev, 0));
   for (int64_t c = 0; c + 1 < static_cast<int64_t>(cb.size()) && cb[c] < n; ++c) {
     Chunk& ck = m->chunk[c & 1];
+    cudaStream_t cs = m->chunk[lanes == 1 ? 0 : (c & 1)].stream;
     const int64_t b = cb[c];
     const int64_t nb = cb[c + 1] - b;
     const int64_t nout = round_up(nb, 128);
     launch_mode_tables(m, pts + b, ldp, nb, nout, nullptr, ck.tables.p, toff, ldt, false,
-                       m->chunk_err.p + c, ck.stream);
-    launch_contract(m, ck.tables.p, toff, ldt, nb, out + b, ck.stream,
+                       m->chunk_err.p + c, cs);
+    launch_contract(m, ck.tables.p, toff, ldt, nb, out + b, cs,
                     core_host ? bp.p : nullptr, core_host ? craw.p : nullptr);
   }
   for (auto& ck : m->chunk) {
@@ -1470,6 +1477,8 @@ int32_t fstk_gpu_device_count(void) {
 }
 
 uint64_t fstk_gpu_launch_count(void) { return g_launches.load(); }
+
+int32_t fstk_gpu_eval_serialize(int32_t on) { return g_eval_serial.exchange(on ? 1 : 0); }
 
 int32_t fstk_gpu_set_device_cache(int32_t policy) {
   const int prev = device_cache_policy().exchange(policy <= 0 ? 0 : (policy >= 2 ? 2 : 1));
