@@ -182,6 +182,7 @@ int64_t evaluate_device_error(const fstk_gpu_model* m, int64_t n, cudaStream_t s
 
 int device_sm_count(int device);
 cublasHandle_t blas_handle(int device);
+cublasHandle_t blas_side_handle(int device);
 cusolverDnHandle_t solver_handle(int device);
 
 // Wavelet support (fstk_wavelet.cu).
@@ -267,6 +268,17 @@ int cpqr_solve(const double* Raug, int64_t ldr, int n, int64_t diag_size, double
 // X := (L L^T)^{-1} X (nrhs columns, ld ldx) for a lower factor L (ld n).
 void chol_solve_blocked_multi(cublasHandle_t h, const double* L, int n, double* X, int64_t ldx,
                               int nrhs);
-// Upper estimate of lambda_min(L L^T) (block power iteration on the inverse).
+// Upper estimate of lambda_min(L L^T) (block power iteration on the inverse),
+// enqueued without host synchronisation (start) and read back (result), so
+// it can overlap other work on another stream.
+struct LambdaMinEstimate {
+  static constexpr int kVectors = 4;
+  DevBuf<double> X, norms;
+  int n = 0, device = 0;
+  cudaStream_t s = nullptr;
+  bool started = false;
+  void start(const double* L, int n, int iters, cudaStream_t s, int device);
+  double result();
+};
 double chol_lambda_min_estimate(const double* L, int n, int iters, cudaStream_t s, int device);
 }  // namespace fstk_gpu

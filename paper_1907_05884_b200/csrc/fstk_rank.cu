@@ -434,12 +434,38 @@ void chol_solve_blocked_multi(cublasHandle_t h, const double* L, int n, double* 
   count_launch(4 * ((n + NB - 1) / NB));
 }
 
-// Estimate of lambda_min(L L^T) by block power iteration on (L L^T)^{-1}
-// (4 seeded vectors, `iters` steps): the largest growth factor is a lower
-// bound of lambda_max((L L^T)^{-1}), so the returned value is an UPPER
-// estimate of lambda_min; callers apply a safety factor.
-double chol_lambda_min_estimate(const double* L, int n, int iters, cudaStream_t s, int device) {
-  constexpr int NV = 4;
+// Column c of X (n x nv, ld n): norms[c] = ||X_c||, then X_c /= norms[c].
+// One CTA per column; no host round trip, so a whole power iteration can be
+// enqueued at once on a side stream.
+__global__ void colnorm_scale_kernel(double* __restrict__ X, int n, double* __restrict__ norms) {
+  __shared__ double red[32];
+  double* x = X + static_cast<int64_t>(blockIdx.x) * n;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(x[i], x[i], s);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) red[0] = sqrt(s);
+  }
+  __syncthreads();
+  const double nrm = red[0];
+  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] *= inv;
+  if (threadIdx.x == 0) norms[blockIdx.x] = nrm;
+}
+
+// Block power iteration on (L L^T)^{-1} (4 seeded vectors, `iters` steps),
+// enqueued on stream s without host synchronisation; result() returns an
+// UPPER estimate of lambda_min(L L^T) (the largest growth factor is a lower
+// bound of lambda_max((L L^T)^{-1})); callers apply a safety factor.
+void LambdaMinEstimate::start(const double* L, int n_, int iters, cudaStream_t s_, int device_) {
+  constexpr int NV = kVectors;
+  n = n_;
+  s = s_;
+  device = device_;
   std::vector<double> h(static_cast<size_t>(n) * NV);
   uint64_t st = 0x9e3779b97f4a7c15ull;
   for (double& v : h) {  // splitmix64 -> uniform(-1, 1)
@@ -450,35 +476,36 @@ double chol_lambda_min_estimate(const double* L, int n, int iters, cudaStream_t 
     z ^= z >> 31;
     v = static_cast<double>(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
   }
-  DevBuf<double> X(h.size());
+  X.alloc(h.size());
+  norms.alloc(NV);
   FSTK_CUDA(cudaMemcpyAsync(X.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s));
-  cublasHandle_t blas = blas_handle(device);
+  FSTK_CUDA(cudaStreamSynchronize(s));  // h is a host temporary
+  cublasHandle_t blas = blas_side_handle(device);
   cublasSetStream(blas, s);
-  double growth = 0.0;
-  std::vector<double> nrm(NV);
   for (int it = 0; it < iters; ++it) {
-    for (int c = 0; c < NV; ++c) {
-      if (cublasDnrm2(blas, n, X.p + static_cast<int64_t>(c) * n, 1, &nrm[c]) != CUBLAS_STATUS_SUCCESS)
-        fail(FSTK_E_COMPUTE, "cublasDnrm2 failed");
-    }
-    FSTK_CUDA(cudaStreamSynchronize(s));
-    for (int c = 0; c < NV; ++c) {
-      const double inv = nrm[c] > 0 ? 1.0 / nrm[c] : 0.0;
-      if (cublasDscal(blas, n, &inv, X.p + static_cast<int64_t>(c) * n, 1) != CUBLAS_STATUS_SUCCESS)
-        fail(FSTK_E_COMPUTE, "cublasDscal failed");
-    }
+    colnorm_scale_kernel<<<NV, 256, 0, s>>>(X.p, n, norms.p);
+    check_launch("colnorm_scale_kernel");
     chol_solve_blocked_multi(blas, L, n, X.p, n, NV);
-    growth = 0.0;
-    for (int c = 0; c < NV; ++c) {
-      double g = 0.0;
-      if (cublasDnrm2(blas, n, X.p + static_cast<int64_t>(c) * n, 1, &g) != CUBLAS_STATUS_SUCCESS)
-        fail(FSTK_E_COMPUTE, "cublasDnrm2 failed");
-      growth = std::max(growth, g);
-    }
-    count_launch(3 * NV);
   }
+  colnorm_scale_kernel<<<NV, 256, 0, s>>>(X.p, n, norms.p);  // growth of the last step
+  check_launch("colnorm_scale_kernel");
+  started = true;
+}
+
+double LambdaMinEstimate::result() {
+  if (!started) return 0.0;
+  double hn[kVectors];
+  FSTK_CUDA(cudaMemcpyAsync(hn, norms.p, sizeof(hn), cudaMemcpyDeviceToHost, s));
   FSTK_CUDA(cudaStreamSynchronize(s));
+  double growth = 0.0;
+  for (double g : hn) growth = std::max(growth, g);
   return growth > 0 ? 1.0 / growth : 0.0;
+}
+
+double chol_lambda_min_estimate(const double* L, int n, int iters, cudaStream_t s, int device) {
+  LambdaMinEstimate e;
+  e.start(L, n, iters, s, device);
+  return e.result();
 }
 
 }  // namespace fstk_gpu

@@ -1648,6 +1648,14 @@ static Handles& handles(int device) {
 }
 
 cublasHandle_t blas_handle(int device) { return handles(device).blas; }
+// A second cuBLAS handle per (thread, device) for work enqueued on a side
+// stream while the first handle drives the main stream (separate workspaces).
+cublasHandle_t blas_side_handle(int device) {
+  static thread_local std::map<int, cublasHandle_t> tl_side;
+  cublasHandle_t& h = tl_side[device];
+  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(FSTK_E_COMPUTE, "cublasCreate failed");
+  return h;
+}
 cusolverDnHandle_t solver_handle(int device) { return handles(device).solver; }
 
 struct EventTimer {
@@ -2570,10 +2578,11 @@ static void refit_local_qr(fstk_gpu_refit* rf, QrStream& qs) {
 // |R_00| is the largest column norm sqrt(max_j G_jj); so sigma_min(A) >
 // R eps max_j ||A_j|| (with a 100x margin for the power-iteration estimate)
 // means ColPivHouseholderQR::rank() == R.  Returns sigma_min / max col norm.
-static double refit_sigma_ratio(fstk_gpu_refit* rf, const double* gram) {
+// lam: the lambda_min(L L^T) estimate (< 0: computed here, synchronously).
+static double refit_sigma_ratio(fstk_gpu_refit* rf, const double* gram, double lam = -1.0) {
   const int n = static_cast<int>(rf->R);
   cudaStream_t s = rf->stream;
-  const double lam = chol_lambda_min_estimate(rf->L.p, n, 4, s, rf->device);
+  if (lam < 0.0) lam = chol_lambda_min_estimate(rf->L.p, n, 3, s, rf->device);
   std::vector<double> diag(n);
   FSTK_CUDA(cudaMemcpy2DAsync(diag.data(), 8, gram, static_cast<size_t>(n + 1) * 8, 8, n,
                               cudaMemcpyDeviceToHost, s));
@@ -3022,8 +3031,36 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     DevBuf<double> g2, r2;
     const double* gcur = gram_in;
     const double* rcur = rhs_in;
+    // The certificate's power iteration reads the Cholesky factor on a side
+    // stream while the refinement streams A on the main one (latency-bound
+    // triangular solves beside HBM-bound GEMVs).
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_l = nullptr;
+    FSTK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    FSTK_CUDA(cudaEventCreateWithFlags(&ev_l, cudaEventDisableTiming));
+    struct SideGuard {
+      cudaStream_t s;
+      cudaEvent_t e;
+      ~SideGuard() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+        cudaEventDestroy(e);
+      }
+    } side_guard{side, ev_l};
+    LambdaMinEstimate est;
+    bool est_fresh = false;
+    auto start_estimate = [&]() {
+      FSTK_CUDA(cudaEventRecord(ev_l, rf->stream));
+      FSTK_CUDA(cudaStreamWaitEvent(side, ev_l, 0));
+      est = LambdaMinEstimate();
+      est.start(rf->L.p, n, 3, side, rf->device);
+      est_fresh = true;
+    };
     auto escalate = [&]() -> bool {
       if (rf->gram_used == 0) return false;
+      // The factor is about to be overwritten: the estimate must be done with it.
+      FSTK_CUDA(cudaStreamSynchronize(side));
+      est_fresh = false;
       // Next level: kGramUpgradeSlices planes' accuracy, then the native Gram.
       const int to = rf->gram_used < kGramUpgradeSlices ? kGramUpgradeSlices : 0;
       fstk_reestimate_info li{};
@@ -3053,6 +3090,7 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     bool need_qr = !rf->factored;
     if (rf->factored) {
       EventTimer tref(rf->stream);
+      start_estimate();
       double prev = 1e300;
       for (int it = 0; it < 8; ++it) {
         rc(fstk_gpu_refit_correction(rf, x.p, sv.p, err));
@@ -3072,6 +3110,7 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
         if (flat || slow || last) {
           if (rf->gram_used > 0) {
             if (!escalate_until_factored()) break;
+            start_estimate();
             prev = 1e300;
             it = -1;
             continue;
@@ -3083,9 +3122,12 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
         }
         prev = step;
       }
-      if (!need_qr) {
-        rf->sigma_ratio = refit_sigma_ratio(rf, gcur);
+      if (!need_qr && rf->factored) {
+        const double lam = est_fresh ? est.result() : -1.0;
+        rf->sigma_ratio = refit_sigma_ratio(rf, gcur, lam);
         need_qr = !certified_full_rank(rf, rf->sigma_ratio);
+      } else if (!rf->factored) {
+        need_qr = true;
       }
       if (info) info->t_solve += tref.seconds();
     }
