@@ -265,6 +265,12 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* refit, double* gr
  * counterpart (an arithmetic choice of this backend; the solution still
  * matches the reference's QR). */
 int32_t fstk_gpu_gram_slices(int32_t slices);
+/* The int8 GEMM engine of the CRT Gram: 1 = the hand-written sm_100a
+ * tcgen05 SYRK (default: lower-triangle 256x256 tiles of all moduli in one
+ * persistent launch, residues reduced in the epilogue), 2 = cuBLASLt IMMA
+ * GEMMs (kept for comparison; $FSTK_GRAM_GEMM=cublaslt).  Both produce the
+ * identical Gram bit for bit.  0 only queries.  Returns the previous setting. */
+int32_t fstk_gpu_gram_engine(int32_t engine);
 /* normal_equations() at an explicit Gram precision: slices 4..7 (sliced,
  * int8 tensor cores) or 0 (native fp64).  solve() and dist.refine_distributed
  * escalate with it: a sliced Gram that cannot precondition the system is

@@ -12,7 +12,7 @@ from .cloud import (PointCloud, read_cloud, read_cloud_binary, read_cloud_csv, r
                     read_points_csv, write_cloud_binary, write_cloud_csv)
 from .model import (BasisSpec, Model, ModelMetadata, ModeFunction, eval_basis, evaluate_fields,
                     load_model, save_model)
-from .refit import (RefitSession, build_design_rows, cholesky, gram, gram_slices, leverage_scores, mixed_matrix,
+from .refit import (RefitSession, build_design_rows, cholesky, gram, gram_engine, gram_slices, leverage_scores, mixed_matrix,
                     reestimate_core, self_convergence, sketch, sketch_config)
 
 
@@ -26,7 +26,7 @@ __all__ = [
     "BasisSpec", "Model", "ModelMetadata", "ModeFunction", "load_model", "save_model",
     "evaluate_fields", "eval_basis",
     "reestimate_core", "RefitSession", "build_design_rows", "sketch", "mixed_matrix",
-    "sketch_config", "self_convergence", "leverage_scores", "gram_slices", "gram", "cholesky",
+    "sketch_config", "self_convergence", "leverage_scores", "gram_slices", "gram_engine", "gram", "cholesky",
     "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
     "launch_count", "set_devices", "PointCloud", "read_cloud", "read_cloud_binary", "read_cloud_csv",
     "read_cloud_device", "read_points_csv", "write_cloud_binary", "write_cloud_csv",

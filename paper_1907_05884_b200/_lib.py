@@ -87,7 +87,7 @@ EXPORTS = [
     "fstk_gpu_refit_factor", "fstk_gpu_refit_correction", "fstk_gpu_refit_apply",
     "fstk_gpu_refit_finish", "fstk_gpu_evaluate_grid", "fstk_gpu_reconstruct_grid",
     "fstk_gpu_self_convergence", "fstk_gpu_leverage_scores", "fstk_gpu_point_major_to_soa",
-    "fstk_gpu_refit_normal_equations_native", "fstk_gpu_gram_slices", "fstk_gpu_gram_device",
+    "fstk_gpu_refit_normal_equations_native", "fstk_gpu_gram_slices", "fstk_gpu_gram_engine", "fstk_gpu_gram_device",
     "fstk_gpu_refit_normal_equations_level", "fstk_gpu_refit_begin_columns",
     "fstk_gpu_refit_exchange_layout", "fstk_gpu_refit_adopt_rows",
     "fstk_gpu_sample_without_replacement", "fstk_gpu_make_plan", "fstk_gpu_set_devices",
@@ -148,6 +148,8 @@ def lib():
                                                          C.POINTER(Err)]
     L.fstk_gpu_gram_slices.argtypes = [C.c_int32]
     L.fstk_gpu_gram_slices.restype = C.c_int32
+    L.fstk_gpu_gram_engine.argtypes = [C.c_int32]
+    L.fstk_gpu_gram_engine.restype = C.c_int32
     L.fstk_gpu_refit_begin_columns.argtypes = [VP, DP, DP, C.c_int64, C.c_int32,
                                                C.POINTER(SketchCfg), C.c_int32, C.c_int32,
                                                C.POINTER(VP), C.POINTER(ReestimateInfo),

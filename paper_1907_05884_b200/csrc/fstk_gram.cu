@@ -402,8 +402,8 @@ __device__ __forceinline__ double i128_to_double(__int128 v) {
   return neg ? -d : d;
 }
 
-template <int NM>
-__global__ void __launch_bounds__(256) crt_fold_kernel(const int32_t* __restrict__ C,
+template <int NM, class CT>
+__global__ void __launch_bounds__(256) crt_fold_kernel(const CT* __restrict__ C,
                                                        int64_t cstride, int64_t m, int w, int c0,
                                                        int n, int k, const int* __restrict__ ex,
                                                        double* __restrict__ G, int64_t ldg,
@@ -411,14 +411,16 @@ __global__ void __launch_bounds__(256) crt_fold_kernel(const int32_t* __restrict
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   if (i >= m || j >= w || i < j || c0 + i >= n || c0 + j >= n) return;
-  const int32_t* c = C + i + static_cast<int64_t>(j) * m;
+  const CT* c = C + i + static_cast<int64_t>(j) * m;
   int y[NM];  // symmetric mixed-radix digits (Garner)
 #pragma unroll
   for (int t = 0; t < NM; ++t) {
     // y_t = (C_t - sum_{l<t} y_l P_{l,t}) P_t^-1 mod m_t, as one reduction of
     // c' inv_t - sum_{l<t} y_l q_{l,t} (|.| < 2^19: no overflow).
     const int mt = kmod(t);
-    int a = (__ldg(c + static_cast<int64_t>(t) * cstride) % mt) * c_crt.inv[t];  // |C| < 2^31
+    // C is the int32 sum (cuBLASLt engine) or its symmetric residue (SYRK
+    // engine): congruent mod m_t, so the digits are identical.
+    int a = (static_cast<int>(__ldg(c + static_cast<int64_t>(t) * cstride)) % mt) * c_crt.inv[t];
 #pragma unroll
     for (int l = 0; l < t; ++l) a -= y[l] * c_crt.q[l][t];
     int v = a % mt;
@@ -472,12 +474,12 @@ void launch_crt(const SRC& src, int64_t s0, int64_t kr, int n, int64_t kp, int64
     residue_kernel<NM, false, SRC><<<g, 256, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
   check_launch("residue_kernel");
 }
-template <int NM>
-void launch_crt_fold(const int32_t* C, int64_t cstride, int64_t m, int64_t wn, int64_t c0, int n,
+template <int NM, class CT>
+void launch_crt_fold(const CT* C, int64_t cstride, int64_t m, int64_t wn, int64_t c0, int n,
                      int k, const int* ex, double* G, int64_t ldg, int acc, int neg, cudaStream_t s) {
   dim3 fg(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(wn));
-  crt_fold_kernel<NM><<<fg, 256, 0, s>>>(C, cstride, m, static_cast<int>(wn), static_cast<int>(c0),
-                                         n, k, ex, G, ldg, acc, neg);
+  crt_fold_kernel<NM, CT><<<fg, 256, 0, s>>>(C, cstride, m, static_cast<int>(wn), static_cast<int>(c0),
+                                             n, k, ex, G, ldg, acc, neg);
   check_launch("crt_fold_kernel");
 }
 
@@ -497,6 +499,26 @@ void launch_crt_fold(const int32_t* C, int64_t cstride, int64_t m, int64_t wn, i
   }
 
 }  // namespace
+
+namespace {
+std::atomic<int> g_engine{-1};
+}
+
+int gram_engine() {
+  int v = g_engine.load();
+  if (v < 0) {
+    const char* e = std::getenv("FSTK_GRAM_GEMM");
+    v = (e && std::string(e) == "cublaslt") ? 2 : 1;
+    g_engine.store(v);
+  }
+  return v;
+}
+
+int set_gram_engine(int engine) {
+  const int prev = gram_engine();
+  if (engine == 1 || engine == 2) g_engine.store(engine);
+  return prev;
+}
 
 int gram_slices() {
   int v = g_slices.load();
@@ -623,8 +645,10 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   if (ldg < 0) ldg = n;
   require(ns >= 4 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: 4..7 plane-equivalents");
   const int k = 7 * ns - 1;
-  LtState& st = lt_state(device);
-  const int64_t np = round_up(static_cast<int64_t>(n), 16);
+  // SYRK engine: 256-column tiles and 128-byte K blocks (zero padding).
+  const bool syrk = gram_engine() == 1;
+  const int64_t np = round_up(static_cast<int64_t>(n), syrk ? 256 : 16);
+  const int64_t kalign = syrk ? 128 : 16;
   static const int64_t seg_cap = [] {
     const char* e = std::getenv("FSTK_GRAM_SEG");
     return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(32768);
@@ -646,21 +670,28 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   const int64_t have = static_cast<int64_t>(sc.X.n);
   const int64_t budget = std::min<int64_t>(int64_t(24) << 30, (static_cast<int64_t>(free_b) + have) / 3);
   kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, budget / (nm_need * np)));
-  kmax &= ~int64_t(15);
-  const int64_t kp = std::min<int64_t>(kmax, round_up(rows, 16));
+  kmax &= ~(kalign - 1);
+  const int64_t kp = std::min<int64_t>(kmax, round_up(rows, kalign));
   const int nm = crt_moduli(k, kp);
   require(nm >= 8 && nm <= 17, FSTK_E_COMPUTE, "internal: CRT modulus count out of range");
   static const int64_t block_cap = [] {
     const char* e = std::getenv("FSTK_GRAM_BLOCK");
     return e ? std::max<int64_t>(256, std::atoll(e)) : int64_t(2048);
   }();
-  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * 4));
-  w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), 16), np);
-  if (w > block_cap && np > block_cap) w = round_up(block_cap, 16);
+  const int64_t cbytes = syrk ? 1 : 4;
+  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * cbytes));
+  w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), syrk ? 256 : 16), np);
+  if (w > block_cap && np > block_cap) w = round_up(block_cap, syrk ? 256 : 16);
   sc.X.ensure(static_cast<size_t>(nm) * kp * np);
-  sc.C.ensure(static_cast<size_t>(nm) * np * w);
+  if (syrk) {
+    sc.C8.ensure(static_cast<size_t>(nm) * np * w);
+  } else {
+    sc.C.ensure(static_cast<size_t>(nm) * np * w);
+    sc.ws.ensure(size_t(32) << 20);
+  }
   sc.ex.ensure(static_cast<size_t>(np));
-  sc.ws.ensure(size_t(32) << 20);
+  int moduli[kSyrkMaxModuli];
+  for (int t = 0; t < nm; ++t) moduli[t] = kmod(t);
   double ops = 0.0;
   bool first = true;
   for (int64_t s0 = 0; s0 < rows; s0 += kp) {
@@ -673,17 +704,27 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
     for (int64_t c0 = 0; c0 < np; c0 += w) {
       const int64_t wn = std::min(w, np - c0);
       const int64_t m = np - c0;
-      for (int t = 0; t < nm; ++t) {
-        const int8_t* Rt = sc.X.p + static_cast<int64_t>(t) * kp * np;
-        ops += 2.0 * static_cast<double>(m) * static_cast<double>(wn) * static_cast<double>(kp);
-        imma_tn(st, sc.ws, m, wn, kp, Rt + c0 * kp, kp, Rt + c0 * kp, kp,
-                sc.C.p + static_cast<int64_t>(t) * m * wn, m, s);
-      }
       const int acc = (!first || beta != 0.0) ? 1 : 0;
+      if (syrk) {
+        // One persistent tcgen05 launch: every modulus, lower tiles only.
+        ops += syrk_i8_residues(sc.X.p, nm, kp, np, c0, wn, m, moduli, sc.C8.p, m * wn, device, s);
 #define FSTK_CRT_FOLD(NMV) \
-  launch_crt_fold<NMV>(sc.C.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
-      FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
+  launch_crt_fold<NMV, int8_t>(sc.C8.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
+        FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
 #undef FSTK_CRT_FOLD
+      } else {
+        LtState& st = lt_state(device);
+        for (int t = 0; t < nm; ++t) {
+          const int8_t* Rt = sc.X.p + static_cast<int64_t>(t) * kp * np;
+          ops += 2.0 * static_cast<double>(m) * static_cast<double>(wn) * static_cast<double>(kp);
+          imma_tn(st, sc.ws, m, wn, kp, Rt + c0 * kp, kp, Rt + c0 * kp, kp,
+                  sc.C.p + static_cast<int64_t>(t) * m * wn, m, s);
+        }
+#define FSTK_CRT_FOLD(NMV) \
+  launch_crt_fold<NMV, int32_t>(sc.C.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
+        FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
+#undef FSTK_CRT_FOLD
+      }
     }
     first = false;
   }

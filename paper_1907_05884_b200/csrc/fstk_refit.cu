@@ -2509,6 +2509,7 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* rf, double* gram,
 }
 
 int32_t fstk_gpu_gram_slices(int32_t slices) { return fstk_gpu::set_gram_slices(slices); }
+int32_t fstk_gpu_gram_engine(int32_t engine) { return fstk_gpu::set_gram_engine(engine); }
 
 int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t n, double* gram,
                              int32_t slices, int32_t device, void* stream, fstk_gpu_error* err) {

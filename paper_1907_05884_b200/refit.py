@@ -57,6 +57,18 @@ def gram_slices(slices: int | None = None) -> int:
     return int(lib().fstk_gpu_gram_slices(-1 if slices is None else int(slices)))
 
 
+def gram_engine(engine: str | None = None) -> str:
+    """Int8 GEMM engine of the CRT Gram: "tcgen05" (the hand-written sm_100a
+    SYRK in fstk_syrk.cu, default) or "cublaslt" (library IMMA GEMMs, kept for
+    comparison).  Returns the current engine; with `engine` given, sets it
+    first and returns the previous one.  Both give the identical Gram."""
+    names = {1: "tcgen05", 2: "cublaslt"}
+    code = {"tcgen05": 1, "cublaslt": 2}
+    if engine is not None and engine not in code:
+        raise ValueError(f"gram engine must be one of {sorted(code)}")
+    return names[int(lib().fstk_gpu_gram_engine(0 if engine is None else code[engine]))]
+
+
 def gram(a, slices: int | None = None):
     """Lower triangle of A^T A for a CUDA float64 tensor A (rows x n) through
     fstk_gpu_gram_device; `slices` digit planes (default: the process

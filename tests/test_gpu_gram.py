@@ -304,3 +304,54 @@ def test_blocked_cholesky_reports_indefinite():
     assert info != 0
     _, info0 = F.cholesky(g, slices=0)
     assert info0 != 0
+
+
+@pytest.mark.parametrize("rows,n", [(1000, 300), (70_000, 257), (333, 4000), (4099, 5000),
+                                    (17, 263), (40_000, 2600), (128, 512)])
+@pytest.mark.parametrize("ns", [4, 7])
+def test_tcgen05_syrk_engine_equals_library_gemms(rows, n, ns):
+    # The hand-written tcgen05 SYRK (fstk_syrk.cu: lower-triangle tiles,
+    # residues reduced in the epilogue) and the cuBLASLt IMMA GEMMs feed the
+    # same Garner fold with congruent values: the Grams are identical bit for
+    # bit -- across several row segments (rows > 32768), column blocks
+    # (n > 2048) and ragged edges (n, rows not multiples of 256 / 128).
+    torch = _torch()
+    gen = torch.Generator(device="cuda").manual_seed(rows + 31 * n + ns)
+    a = torch.randn(rows, n, dtype=torch.float64, device="cuda", generator=gen)
+    a[:, n // 3] *= 2.0 ** 30
+    prev = F.gram_engine("cublaslt")
+    try:
+        g_lib = F.gram(a, slices=ns)
+        F.gram_engine("tcgen05")
+        g_tc = F.gram(a, slices=ns)
+    finally:
+        F.gram_engine(prev)
+    assert F.gram_engine() == prev
+    assert torch.equal(g_tc, g_lib)
+    _check_bound(a, g_tc, ns)
+
+
+def test_tcgen05_syrk_exact_integer_gram():
+    # Integer columns below 2^13 fit the level-4 integers exactly: the Gram is
+    # the exact integer A^T A, so the tensor-core path is checked against
+    # integer arithmetic, not only against the library engine.
+    torch = _torch()
+    rng = np.random.default_rng(21)
+    rows, n = 33_000, 700
+    ai = rng.integers(-8191, 8192, size=(rows, n))
+    ai[0, :] = 8191
+    a = torch.tensor(ai, dtype=torch.float64, device="cuda")
+    exact = ai.T.astype(np.int64) @ ai.astype(np.int64)
+    prev = F.gram_engine("tcgen05")
+    try:
+        g = F.gram(a, slices=4).cpu().numpy()
+    finally:
+        F.gram_engine(prev)
+    low = np.tril(np.ones((n, n), dtype=bool))
+    assert np.array_equal(g[low], exact[low].astype(np.float64))
+
+
+def test_gram_engine_setting():
+    assert F.gram_engine() in ("tcgen05", "cublaslt")
+    with pytest.raises(ValueError):
+        F.gram_engine("wgmma")
