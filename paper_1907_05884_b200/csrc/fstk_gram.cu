@@ -37,6 +37,7 @@
 #include <tuple>
 
 #include "fstk_common.cuh"
+#include "fstk_crt.cuh"
 #include "fstk_internal.h"
 
 namespace fstk_gpu {
@@ -260,38 +261,6 @@ void imma_tn(LtState& st, DevBuf<uint8_t>& ws, int64_t M, int64_t N, int64_t K, 
 // M = prod m_i), which is converted to fp64 once (exact whenever
 // representable) and scaled by 2^(e_a + e_b - 2k).  At ns = 5 that is 11 GEMMs of K rows instead of the
 // digit scheme's 15; at ns = 7, 15 instead of 28.
-// Pairwise coprime moduli <= 255 (residues fit int8 in symmetric form).
-__host__ __device__ constexpr int kmod(int i) {
-  constexpr int t[20] = {255, 254, 253, 251, 247, 241, 239, 233, 229, 227,
-                         223, 211, 199, 197, 193, 191, 181, 179, 173, 167};
-  return t[i];
-}
-constexpr int kMaxModuli = 20;
-constexpr int cx_inv(int a, int m) {  // a^-1 mod m (gcd(a, m) = 1)
-  for (int x = 1; x < m; ++x)
-    if ((static_cast<long long>(a) * x) % m == 1) return x;
-  return 0;
-}
-struct CrtTables {
-  int pmod[kMaxModuli][kMaxModuli];  // (prod_{l<j} m_l) mod m_i, j < i
-  int inv[kMaxModuli];               // (prod_{l<i} m_l)^-1 mod m_i
-  int q[kMaxModuli][kMaxModuli];     // pmod[l][i] inv[i] mod m_i (Garner, one reduction per digit)
-};
-constexpr CrtTables make_crt_tables() {
-  CrtTables t{};
-  for (int i = 0; i < kMaxModuli; ++i) {
-    long long p = 1;  // prod_{l<j} m_l mod m_i, built up over j
-    for (int j = 0; j < kMaxModuli; ++j) {
-      t.pmod[j][i] = static_cast<int>(p);
-      if (j < i) p = (p * kmod(j)) % kmod(i);
-    }
-    t.inv[i] = i == 0 ? 1 : cx_inv(static_cast<int>(p % kmod(i)), kmod(i));
-    for (int j = 0; j < kMaxModuli; ++j)
-      t.q[j][i] = static_cast<int>((static_cast<long long>(t.pmod[j][i]) * t.inv[i]) % kmod(i));
-  }
-  return t;
-}
-__constant__ CrtTables c_crt = make_crt_tables();
 
 // Symmetric residue of x modulo a compile-time m (unrolled callers), in
 // 32-bit arithmetic: x itself when it fits (k <= 30), else two 31-bit halves
@@ -366,42 +335,6 @@ __global__ void residue_kernel(const SRC src, int64_t s0, int64_t rows, int n, i
   }
 }
 
-// P_s = prod_{t<s} m_t, and the split of an NM-digit Garner value into two
-// halves that are exact in fp64: the smallest s with prod_{s<=t<NM} m_t and
-// P_s both below 2^53 (0 = none; then the 128-bit path).
-__host__ __device__ constexpr unsigned long long crt_prefix(int s) {
-  unsigned long long p = 1;
-  for (int t = 0; t < s; ++t) p *= static_cast<unsigned long long>(kmod(t));
-  return p;
-}
-__host__ __device__ constexpr int crt_split(int nm) {
-  constexpr unsigned long long lim = 1ull << 53;
-  for (int s = 1; s < nm; ++s) {
-    unsigned long long q = 1;
-    bool ok = true;
-    for (int t = s; t < nm; ++t) {
-      if (q > lim / static_cast<unsigned long long>(kmod(t))) { ok = false; break; }
-      q *= static_cast<unsigned long long>(kmod(t));
-    }
-    if (ok && q < lim && crt_prefix(s) < lim) return s;
-  }
-  return 0;
-}
-static_assert(crt_split(9) > 0 && crt_split(11) > 0 && crt_split(12) > 0, "CRT split");
-
-// 128-bit integer -> double on the magnitude: exact whenever the value is
-// representable (both 64-bit halves then carry <= 53 significant bits and the
-// fused sum is exact), otherwise within one ulp.
-__device__ __forceinline__ double i128_to_double(__int128 v) {
-  const bool neg = v < 0;
-  const unsigned __int128 u = neg ? static_cast<unsigned __int128>(0) - static_cast<unsigned __int128>(v)
-                                  : static_cast<unsigned __int128>(v);
-  const double hi = static_cast<double>(static_cast<unsigned long long>(u >> 64));
-  const double lo = static_cast<double>(static_cast<unsigned long long>(u));
-  const double d = fma(hi, 18446744073709551616.0, lo);
-  return neg ? -d : d;
-}
-
 template <int NM, class CT>
 __global__ void __launch_bounds__(256) crt_fold_kernel(const CT* __restrict__ C,
                                                        int64_t cstride, int64_t m, int w, int c0,
@@ -412,42 +345,12 @@ __global__ void __launch_bounds__(256) crt_fold_kernel(const CT* __restrict__ C,
   const int j = blockIdx.y;
   if (i >= m || j >= w || i < j || c0 + i >= n || c0 + j >= n) return;
   const CT* c = C + i + static_cast<int64_t>(j) * m;
-  int y[NM];  // symmetric mixed-radix digits (Garner)
+  int r[NM];
 #pragma unroll
-  for (int t = 0; t < NM; ++t) {
-    // y_t = (C_t - sum_{l<t} y_l P_{l,t}) P_t^-1 mod m_t, as one reduction of
-    // c' inv_t - sum_{l<t} y_l q_{l,t} (|.| < 2^19: no overflow).
-    const int mt = kmod(t);
-    // C is the int32 sum (cuBLASLt engine) or its symmetric residue (SYRK
-    // engine): congruent mod m_t, so the digits are identical.
-    int a = (static_cast<int>(__ldg(c + static_cast<int64_t>(t) * cstride)) % mt) * c_crt.inv[t];
-#pragma unroll
-    for (int l = 0; l < t; ++l) a -= y[l] * c_crt.q[l][t];
-    int v = a % mt;
-    if (v < 0) v += mt;
-    if (v > mt / 2) v -= mt;
-    y[t] = v;
-  }
-  double accd;
-  constexpr int SPLIT = crt_split(NM);
-  if constexpr (SPLIT > 0) {
-    // V = V_lo + P_s V_hi with both halves and P_s below 2^53 (exact int64
-    // Horner, exact doubles); one fma rounds V once: correctly rounded, so
-    // exact whenever V is representable, like the 128-bit evaluation.
-    long long hi = y[NM - 1];
-#pragma unroll
-    for (int t = NM - 2; t >= SPLIT; --t) hi = hi * kmod(t) + y[t];
-    long long lo = y[SPLIT - 1];
-#pragma unroll
-    for (int t = SPLIT - 2; t >= 0; --t) lo = lo * kmod(t) + y[t];
-    accd = fma(static_cast<double>(hi), static_cast<double>(crt_prefix(SPLIT)), static_cast<double>(lo));
-  } else {
-    __int128 acc = y[NM - 1];
-#pragma unroll
-    for (int t = NM - 2; t >= 0; --t) acc = acc * kmod(t) + y[t];
-    accd = i128_to_double(acc);
-  }
-  const double v0 = ldexp(accd, ex[c0 + i] + ex[c0 + j] - 2 * k);
+  for (int t = 0; t < NM; ++t) r[t] = static_cast<int>(__ldg(c + static_cast<int64_t>(t) * cstride));
+  // C is the int32 sum (cuBLASLt engine) or its symmetric residue: congruent
+  // mod m_t, so the Garner digits are identical.
+  const double v0 = crt_scale(crt_value<NM, sizeof(CT) == 1>(r), ex[c0 + i] + ex[c0 + j] - 2 * k);
   const double v = negate ? -v0 : v0;
   double* g = G + (c0 + i) + static_cast<int64_t>(c0 + j) * ldg;
   *g = accumulate ? *g + v : v;
@@ -655,7 +558,8 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   }();
   // int32-exact: K * 127^2 < 2^31; residue planes within a third of free
   // memory (<= 24 GB).
-  int64_t kmax = std::min<int64_t>(seg_cap, ((int64_t(1) << 31) - 1) / (127 * 127));
+  // (The SYRK engine's integer epilogue needs |sums| < 2^30: <= 65536 rows.)
+  int64_t kmax = std::min<int64_t>(seg_cap, syrk ? int64_t(65536) : ((int64_t(1) << 31) - 1) / (127 * 127));
   size_t free_b = 0, total_b = 0;
   if (device_mem_info(&free_b, &total_b) != cudaSuccess) {
     cudaGetLastError();
@@ -678,20 +582,17 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
     const char* e = std::getenv("FSTK_GRAM_BLOCK");
     return e ? std::max<int64_t>(256, std::atoll(e)) : int64_t(2048);
   }();
-  const int64_t cbytes = syrk ? 1 : 4;
-  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * cbytes));
-  w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), syrk ? 256 : 16), np);
-  if (w > block_cap && np > block_cap) w = round_up(block_cap, syrk ? 256 : 16);
+  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * 4));
+  w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), 16), np);
+  if (w > block_cap && np > block_cap) w = round_up(block_cap, 16);
   sc.X.ensure(static_cast<size_t>(nm) * kp * np);
   if (syrk) {
-    sc.C8.ensure(static_cast<size_t>(nm) * np * w);
+    sc.C8.ensure(syrk_crt_scratch_bytes(nm, device));
   } else {
     sc.C.ensure(static_cast<size_t>(nm) * np * w);
     sc.ws.ensure(size_t(32) << 20);
   }
   sc.ex.ensure(static_cast<size_t>(np));
-  int moduli[kSyrkMaxModuli];
-  for (int t = 0; t < nm; ++t) moduli[t] = kmod(t);
   double ops = 0.0;
   bool first = true;
   for (int64_t s0 = 0; s0 < rows; s0 += kp) {
@@ -701,19 +602,17 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
 #define FSTK_CRT_RES(NMV) launch_crt<NMV, SRC>(src, s0, kr, n, kp, np, k, sc.ex.p, sc.X.p, s)
     FSTK_CRT_SWITCH(nm, FSTK_CRT_RES)
 #undef FSTK_CRT_RES
-    for (int64_t c0 = 0; c0 < np; c0 += w) {
-      const int64_t wn = std::min(w, np - c0);
-      const int64_t m = np - c0;
-      const int acc = (!first || beta != 0.0) ? 1 : 0;
-      if (syrk) {
-        // One persistent tcgen05 launch: every modulus, lower tiles only.
-        ops += syrk_i8_residues(sc.X.p, nm, kp, np, c0, wn, m, moduli, sc.C8.p, m * wn, device, s);
-#define FSTK_CRT_FOLD(NMV) \
-  launch_crt_fold<NMV, int8_t>(sc.C8.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
-        FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
-#undef FSTK_CRT_FOLD
-      } else {
-        LtState& st = lt_state(device);
+    const int acc = (!first || beta != 0.0) ? 1 : 0;
+    if (syrk) {
+      // One persistent tcgen05 launch: the whole lower triangle, every
+      // modulus, Garner fold in the epilogue.
+      ops += syrk_crt_fold(sc.X.p, nm, kp, np, n, k, sc.ex.p, gram, ldg, acc != 0, negate, sc.C8.p,
+                           device, s);
+    } else {
+      LtState& st = lt_state(device);
+      for (int64_t c0 = 0; c0 < np; c0 += w) {
+        const int64_t wn = std::min(w, np - c0);
+        const int64_t m = np - c0;
         for (int t = 0; t < nm; ++t) {
           const int8_t* Rt = sc.X.p + static_cast<int64_t>(t) * kp * np;
           ops += 2.0 * static_cast<double>(m) * static_cast<double>(wn) * static_cast<double>(kp);

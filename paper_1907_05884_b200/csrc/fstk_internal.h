@@ -197,7 +197,7 @@ void launch_mode_general(const GenModeDev& G, const double* xs, int64_t n, int64
 struct GramScratch {
   DevBuf<int8_t> X, Y;     // digit planes, column a at a * ns * kp
   DevBuf<int32_t> C;       // ns planes of one column block (digit scheme / cuBLASLt engine)
-  DevBuf<int8_t> C8;       // CRT residues of one column block (tcgen05 SYRK engine)
+  DevBuf<uint8_t> C8;      // per-CTA residue scratch of the tcgen05 SYRK engine
   DevBuf<int> ex;          // per-column exponents of the current segment
   DevBuf<uint8_t> ws;      // cuBLASLt workspace
   int64_t kp = 0;          // segment rows, fixed by the first call
@@ -207,15 +207,17 @@ int gram_slices();                      // 0 = native fp64 DSYRK/DGEMM Gram
 // (fstk_syrk.cu, default), 2 = cuBLASLt IMMA GEMMs (comparison).
 int gram_engine();
 int set_gram_engine(int engine);        // returns the previous setting; 0 = query
-// fstk_syrk.cu: for every modulus t < nm and every 256 x 256 tile (tile row >=
-// tile column) of the column block [c0, c0 + wn) x [c0, np) of R_t^T R_t
-// (R_t = the kp x np int8 plane t at planes + t kp np, column-major),
-// C[t cstride + i + j m] = symmetric residue of the int32 sum mod moduli[t]
-// (i, j relative to c0).  Returns the int8 ops issued.
+// fstk_syrk.cu: G (lower triangle, n x n, ldg) = [G +] (-1)^negate sum over
+// the rows of one segment of the exact CRT Gram: the int8 planes R_t (kp x np,
+// column-major, plane t at planes + t kp np) give C_t = R_t^T R_t on the
+// tcgen05 tensor cores; Garner folds the nm residues of every entry and scales
+// by 2^(ex_a + ex_b - 2k).  scratch: syrk_crt_scratch_bytes(nm) bytes.
+// Returns the int8 ops issued.
 constexpr int kSyrkMaxModuli = 20;
-double syrk_i8_residues(const int8_t* planes, int nm, int64_t kp, int64_t np, int64_t c0, int64_t wn,
-                        int64_t m, const int* moduli, int8_t* C, int64_t cstride, int device,
-                        cudaStream_t s);
+size_t syrk_crt_scratch_bytes(int nm, int device);
+double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n, int k, const int* ex,
+                     double* G, int64_t ldg, bool accumulate, bool negate, uint8_t* scratch, int device,
+                     cudaStream_t s);
 int set_gram_slices(int slices);        // returns the previous setting
 bool gram_sliced_applies(int64_t rows, int n);
 // gram = beta * gram + the plane sums t_lo..slices+1 of A^T A (t_lo = 2:

@@ -1,37 +1,47 @@
-// Hand-written sm_100a int8 SYRK for the CRT Gram (fstk_gram.cu): the
-// tensor-core stage of A^T A (randls.cpp:112-123 solves the sketched system
-// whose normal equations these are; randls.cpp:315-348 builds it).
+// Hand-written sm_100a int8 SYRK + CRT fold for the Gram of the sketched
+// system (fstk_gram.cu): the tensor-core stage of A^T A (randls.cpp:112-123
+// solves the sketched least-squares system whose normal equations these are;
+// randls.cpp:315-348 builds it).
 //
-// For every modulus t of one row segment, C_t = R_t^T R_t where R_t is the
-// kp x np int8 residue plane (column a contiguous along K).  Only the lower
-// triangle of C_t is needed (G is symmetric), so only 256 x 256 tiles with
-// tile row >= tile column are computed -- the library GEMMs this replaces
-// computed whole rectangular column blocks.  The epilogue reduces each int32
-// sum modulo m_t and stores the symmetric residue as one byte: the Garner
-// fold (crt_fold_kernel) needs nothing more, so the C planes it streams are
-// 4x smaller than int32 sums and the fold's arithmetic is unchanged.
+// One launch per row segment computes the whole lower triangle of G's update:
+// for every 256 x 256 tile (tile row >= tile column) and every modulus t,
+// C_t = R_t^T R_t on the int8 tensor cores (R_t = the kp x np residue plane
+// t), and after the last modulus the epilogue rebuilds each exact integer sum
+// by Garner's algorithm and adds 2^(e_a+e_b-2k) times it into G -- no int32
+// planes, no separate fold kernel.  The library GEMMs this replaces computed
+// whole rectangular column blocks (~6% of the upper triangle) and needed an
+// HBM round trip of 36 bytes per entry into a fold kernel.
 //
-// Structure (one persistent kernel for all moduli and tiles of a column block):
+// Structure (persistent; one CTA pair per two SMs):
 //  * CTA pairs (__cluster_dims__(2)) run tcgen05.mma.cta_group::2.kind::i8,
 //    M = 256 (128 rows per CTA), N = 256, K = 32 per instruction; each CTA
 //    TMA-loads (cp.async.bulk.tensor, 128B swizzle) its 128-row halves of
-//    the A and B panels, 128 bytes of K per stage, 6 stages deep.
+//    the A and B panels, 128 bytes of K per stage, 7 stages deep.
 //  * warp 0: TMA producer; warp 1 (leader CTA): the single MMA-issuing
-//    thread; warp 2: TMEM allocator; warps 4-7: epilogue.
+//    thread; warp 2: TMEM allocator; warps 4-11: epilogue.
 //  * Accumulators live in TMEM (2 x 256 columns, double-buffered, so the
-//    epilogue of tile i overlaps the MMAs of tile i+1) and are read back
-//    with tcgen05.ld.
-// Exactness: |C_t| <= kp * 127^2 < 2^31 for kp <= 133,152, so the int32
-// accumulation is exact, as with the library GEMMs; the stored residues are
-// congruent to the library's int32 sums modulo m_t, so the fold produces the
-// identical Gram bit for bit.
+//    epilogue of modulus t overlaps the MMAs of modulus t+1) and are read
+//    back with tcgen05.ld by 8 epilogue warps (two per TMEM lane quarter).
+//    Each modulus leaves its symmetric residues (one byte per entry) in a
+//    per-CTA L2-resident scratch and frees the accumulator at once; after
+//    the tile's last modulus the epilogue folds all NM of them into G while
+//    the MMAs of the next tile run.
+//  * Tiles are taken in bands of 8 tile columns, tile columns fastest, all
+//    moduli of a tile on one pair: the 74 concurrent pairs share ~17 panels
+//    of one plane in L2 at any time.
+// Exactness: |C_t| <= kp * 127^2 < 2^30 for kp <= 66,560, so the int32
+// accumulation is exact; residues are congruent to the int32 sums, so the
+// Garner digits -- and G -- equal the library engine's bit for bit.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "fstk_common.cuh"
+#include "fstk_crt.cuh"
 #include "fstk_internal.h"
 
 namespace fstk_gpu {
@@ -41,29 +51,52 @@ namespace {
 constexpr int kTile = 256;                    // output tile edge (CTA pair)
 constexpr int kHalf = 128;                    // rows per CTA
 constexpr int kKB = 128;                      // K bytes per stage (one swizzle row)
-constexpr int kStages = 6;
 constexpr int kPanelBytes = kHalf * kKB;      // 16 KB: one operand half
 constexpr int kStageBytes = 2 * kPanelBytes;  // A half + B half
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 8;   // two per TMEM lane quarter, 128 columns each
+constexpr int kThreads = 32 * (4 + kEpiWarps);
+constexpr int kStages = 7;
 constexpr int kAccCols = 256;                 // TMEM columns per accumulator
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 
+constexpr int kBandTiles = 8;   // tile columns per band
+constexpr int kMaxBands = 64;
+
 struct SyrkParams {
-  int nm;               // moduli (residue planes)
   int kblocks;          // kp / 128
   int np;               // columns per plane (rows of the tensor map per plane)
-  int c0;               // first column of the block
-  int ntj;              // tile columns of the block
-  int nti;              // tile rows of the block
-  int tri;              // ntj (ntj + 1) / 2: tiles of the diagonal band
-  int per_mod;          // tiles per modulus
-  int ntasks;           // nm * per_mod
-  long long ldc;        // C rows (m)
-  long long cstride;    // plane stride of C
-  int8_t* C;
+  int nt;               // tiles per side (np / 256)
+  int nbands;
+  int band_start[kMaxBands + 1];  // first task of each band
+  int ntasks;
+  int n;                // valid columns of G
+  int k;                // integer bits (scale 2^-2k)
+  int accumulate, negate;
+  int hint;             // 0: none, 1: L2 evict_last, 2: evict_first (experiments)
+  long long ldg;
+  double* G;
+  const int* ex;        // per-column exponents of this segment
+  uint8_t* scratch;     // per CTA: NM x 128 x 256 residue bytes
   int mod[kSyrkMaxModuli];
-  double inv[kSyrkMaxModuli];
+  unsigned p16[kSyrkMaxModuli];   // 2^16 mod m
+  unsigned off[kSyrkMaxModuli];   // a multiple of m >= 2^22 (makes the folded value >= 0)
+  unsigned magic[kSyrkMaxModuli]; // floor(2^32 / m)
 };
+
+// Symmetric residue of an int32 sum |x| < 2^30 modulo m <= 255 in integer
+// ALU operations only (the epilogue shares the SM with the tensor pipe; fp64
+// or conversion-pipe arithmetic here measured math-pipe-throttled):
+// x = hi 2^16 + lo folds to y = hi (2^16 mod m) + lo + off in [0, 2^23),
+// then Barrett with floor(2^32/m) gives q in {floor(y/m) - 1, floor(y/m)}.
+__device__ __forceinline__ int sym_residue(int x, int m, unsigned p16, unsigned off, unsigned magic) {
+  const unsigned y = static_cast<unsigned>((x >> 16) * static_cast<int>(p16)) +
+                     static_cast<unsigned>(x & 0xFFFF) + off;
+  const unsigned q = __umulhi(y, magic);
+  int r = static_cast<int>(y - q * static_cast<unsigned>(m));
+  if (r >= m) r -= m;
+  if (r > (m >> 1)) r -= m;
+  return r;
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -79,6 +112,22 @@ __device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
   uint32_t out;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
   return out;
+}
+// Blocking wait with a hardware suspend hint: the waiting thread sleeps until
+// the phase completes (or ~0.5 ms pass) instead of spinning on try_wait -- the
+// epilogue warps wait ~100 us per tile and the kernel runs at the power cap,
+// where issue slots spent spinning cost clock speed.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(500000u)
+        : "memory");
+  } while (!ok);
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -111,6 +160,14 @@ __device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2sm_hint(void* dst, const CUtensorMap* map, int x, int y,
+                                                  uint32_t bar_cluster, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -141,26 +198,35 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Task -> (modulus, tile row, tile column), tile row >= tile column: per
-// modulus the diagonal band first (tile rows 0..ntj-1, triangular), then the
-// full rows below it, tile columns fastest -- consecutive tasks (which run
-// concurrently on neighbouring pairs) share their A and B panels in L2.
-__device__ __forceinline__ void decode_task(const SyrkParams& p, int task, int& t, int& ti, int& tj) {
-  t = task / p.per_mod;
-  int r = task - t * p.per_mod;
-  if (r < p.tri) {
-    ti = 0;
-    while ((ti + 1) * (ti + 2) / 2 <= r) ++ti;
-    tj = r - ti * (ti + 1) / 2;
+// Task -> (tile row, tile column), tile row >= tile column: bands of
+// kBandTiles tile columns; in each band the diagonal triangle first, then the
+// full rows below it, tile columns fastest.
+__device__ __forceinline__ void decode_task(const SyrkParams& p, int task, int& ti, int& tj) {
+  int b = 0;
+  while (b + 1 < p.nbands && p.band_start[b + 1] <= task) ++b;
+  int r = task - p.band_start[b];
+  const int c0 = b * kBandTiles;
+  const int wb = min(kBandTiles, p.nt - c0);
+  const int tri = wb * (wb + 1) / 2;
+  if (r < tri) {
+    int a = 0;
+    while ((a + 1) * (a + 2) / 2 <= r) ++a;
+    ti = c0 + a;
+    tj = c0 + r - a * (a + 1) / 2;
   } else {
-    r -= p.tri;
-    ti = p.ntj + r / p.ntj;
-    tj = r - (ti - p.ntj) * p.ntj;
+    r -= tri;
+    ti = c0 + wb + r / wb;
+    tj = c0 + r % wb;
   }
 }
 
+__device__ __forceinline__ int sext_byte(uint32_t w, int b) {
+  return static_cast<int>(w << (24 - 8 * b)) >> 24;
+}
+
+template <int NM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    syrk_i8_kernel(const __grid_constant__ CUtensorMap map, const SyrkParams p) {
+    syrk_crt_kernel(const __grid_constant__ CUtensorMap map, const SyrkParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -185,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps x 2 CTAs
     }
     fence_mbar_init();
   }
@@ -205,22 +271,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---- TMA producer (both CTAs): this CTA's 128-row halves of A and B.
       uint32_t stage = 0, phase = 0;
+      uint64_t policy = 0;
+      if (p.hint == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
+      if (p.hint == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       for (int task = pair; task < p.ntasks; task += npairs) {
-        int t, ti, tj;
-        decode_task(p, task, t, ti, tj);
-        const int base = t * p.np + p.c0 + static_cast<int>(rank) * kHalf;
-        const int rowA = base + ti * kTile;
-        const int rowB = base + tj * kTile;
-        for (int kb = 0; kb < p.kblocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * kStageBytes;
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
-          const uint32_t bar = map_rank(&full[stage], 0);
-          tma_load_2sm(sa, &map, kb * kKB, rowA, bar);
-          tma_load_2sm(sa + kPanelBytes, &map, kb * kKB, rowB, bar);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+        int ti, tj;
+        decode_task(p, task, ti, tj);
+        for (int t = 0; t < NM; ++t) {
+          const int base = t * p.np + static_cast<int>(rank) * kHalf;
+          const int rowA = base + ti * kTile;
+          const int rowB = base + tj * kTile;
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * kStageBytes;
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+            const uint32_t bar = map_rank(&full[stage], 0);
+            if (p.hint) {
+              tma_load_2sm_hint(sa, &map, kb * kKB, rowA, bar, policy);
+              tma_load_2sm_hint(sa + kPanelBytes, &map, kb * kKB, rowB, bar, policy);
+            } else {
+              tma_load_2sm(sa, &map, kb * kKB, rowA, bar);
+              tma_load_2sm(sa + kPanelBytes, &map, kb * kKB, rowB, bar);
+            }
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -230,68 +306,120 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---- MMA issuer (leader CTA, one thread).
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
       for (int task = pair; task < p.ntasks; task += npairs) {
-        mbar_wait(&tempty[acc], aphase ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + acc * kAccCols;
-        for (int kb = 0; kb < p.kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
+        for (int t = 0; t < NM; ++t) {
+          mbar_wait(&tempty[acc], aphase ^ 1);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-          const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kPanelBytes);
+          const uint32_t d = tmem + acc * kAccCols;
+          for (int kb = 0; kb < p.kblocks; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+            const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kPanelBytes);
 #pragma unroll
-          for (int k = 0; k < kKB / 32; ++k)
-            mma_i8(d, da + 2 * k, db + 2 * k, (kb | k) != 0 ? 1u : 0u);
-          mma_commit_pair(&empty[stage]);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+            for (int k = 0; k < kKB / 32; ++k)
+              mma_i8(d, da + 2 * k, db + 2 * k, (kb | k) != 0 ? 1u : 0u);
+            mma_commit_pair(&empty[stage]);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
+          mma_commit_pair(&tfull[acc]);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1;
         }
-        mma_commit_pair(&tfull[acc]);
-        acc ^= 1;
-        if (acc == 0) aphase ^= 1;
       }
     }
   } else if (warp >= 4) {
-    // ---- Epilogue (both CTAs): TMEM lanes 32q..32q+31 = this warp's rows.
+    // ---- Epilogue (both CTAs): warp w reads TMEM lanes 32 (w % 4) .. +31
+    // (this CTA's rows) and columns 128 ((w - 4) / 4) .. +127 of the tile.
     const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const int row = q * 32 + lane;  // row of this CTA's half tile
     const uint32_t tempty_leader0 = map_rank(&tempty[0], 0);
     const uint32_t tempty_leader1 = map_rank(&tempty[1], 0);
+    // This thread's scratch row: modulus t at t * 128 * 256, 256 columns contiguous.
+    uint8_t* srow = p.scratch + static_cast<size_t>(blockIdx.x) * NM * kHalf * kTile +
+                    static_cast<size_t>(row) * kTile + half * (kTile / 2);
     uint32_t acc = 0, aphase = 0;
     for (int task = pair; task < p.ntasks; task += npairs) {
-      int t, ti, tj;
-      decode_task(p, task, t, ti, tj);
-      const int mt = p.mod[t];
-      const double inv = p.inv[t];
-      const long long i = static_cast<long long>(ti) * kTile + rank * kHalf + q * 32 + lane;
-      int8_t* crow = p.C + t * p.cstride + i + static_cast<long long>(tj) * kTile * p.ldc;
-      mbar_wait(&tfull[acc], aphase);
-      tc_fence_after();
-      const uint32_t tbase = tmem + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+      int ti, tj;
+      decode_task(p, task, ti, tj);
 #pragma unroll 1
-      for (int ch = 0; ch < kAccCols / 32; ++ch) {
-        uint32_t v[32];
-        tmem_ld32(tbase + ch * 32, v);
+      for (int t = 0; t < NM; ++t) {
+        const int mt = p.mod[t];
+        const unsigned p16 = p.p16[t], off = p.off[t], magic = p.magic[t];
+        mbar_wait_sleep(&tfull[acc], aphase);
+        tc_fence_after();
+        const uint32_t tbase =
+            tmem + acc * kAccCols + half * (kAccCols / 2) + (static_cast<uint32_t>(q * 32) << 16);
+        uint8_t* dst = srow + static_cast<size_t>(t) * kHalf * kTile;
+#pragma unroll 1
+        for (int ch = 0; ch < kAccCols / 64; ++ch) {
+          uint32_t v[32];
+          tmem_ld32(tbase + ch * 32, v);
+          uint32_t w[8];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int x = static_cast<int>(v[c]);
-          // Symmetric residue: |x| < 2^31 is exact in fp64 and x/m is never
-          // within 2^-21 of a half-integer unless it is one (then either
-          // representative, |r| <= 127, is congruent).
-          const int qq = static_cast<int>(rint(static_cast<double>(x) * inv));
-          const int r = x - qq * mt;
-          crow[static_cast<long long>(ch * 32 + c) * p.ldc] = static_cast<int8_t>(r);
+          for (int u = 0; u < 8; ++u) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int r = sym_residue(static_cast<int>(v[4 * u + b]), mt, p16, off, magic);
+              x |= (static_cast<uint32_t>(r) & 0xFFu) << (8 * b);
+            }
+            w[u] = x;
+          }
+          uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
+          __stcg(d4, make_uint4(w[0], w[1], w[2], w[3]));
+          __stcg(d4 + 1, make_uint4(w[4], w[5], w[6], w[7]));
+        }
+        // The accumulator is free as soon as its residues are out.
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t bar = acc ? tempty_leader1 : tempty_leader0;
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar)
+                       : "memory");
+        }
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+      // Fold the tile's NM residues of every entry of this thread's 128
+      // columns into G while the MMAs of the next tile run.
+      const int gi = ti * kTile + static_cast<int>(rank) * kHalf + row;
+      const int ei = gi < p.n ? __ldg(p.ex + gi) : 0;
+      const int gjb = tj * kTile + half * (kTile / 2);
+#pragma unroll 1
+      for (int ch = 0; ch < kTile / 64; ++ch) {
+        const int gj0 = gjb + ch * 32;
+        const int ej_lane = (gj0 + lane < p.n) ? __ldg(p.ex + gj0 + lane) : 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint4 wv[NM];
+#pragma unroll
+          for (int s2 = 0; s2 < NM; ++s2)
+            wv[s2] = __ldcg(reinterpret_cast<const uint4*>(srow + static_cast<size_t>(s2) * kHalf * kTile +
+                                                           ch * 32 + h * 16));
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const int cc = h * 16 + c;
+            const int ej = __shfl_sync(0xffffffffu, ej_lane, cc);
+            const int gj = gj0 + cc;
+            if (gi >= gj && gi < p.n && gj < p.n) {
+              int r[NM];
+#pragma unroll
+              for (int s2 = 0; s2 < NM; ++s2) {
+                const uint32_t word = (c < 4) ? wv[s2].x : (c < 8) ? wv[s2].y : (c < 12) ? wv[s2].z : wv[s2].w;
+                r[s2] = sext_byte(word, c & 3);
+              }
+              const double v0 = crt_scale(crt_value<NM, true>(r), ei + ej - 2 * p.k);
+              const double val = p.negate ? -v0 : v0;
+              double* g = p.G + gi + static_cast<long long>(gj) * p.ldg;
+              *g = p.accumulate ? *g + val : val;
+            }
+          }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        const uint32_t bar = acc ? tempty_leader1 : tempty_leader0;
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar)
-                     : "memory");
-      }
-      acc ^= 1;
-      if (acc == 0) aphase ^= 1;
     }
   }
 
@@ -318,9 +446,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-}  // namespace
-
-int syrk_i8_sm_count(int device) {
+int sm_count(int device) {
   static std::mutex mu;
   static int cached[64] = {0};
   std::lock_guard<std::mutex> lk(mu);
@@ -333,19 +459,35 @@ int syrk_i8_sm_count(int device) {
   return cached[device];
 }
 
-double syrk_i8_residues(const int8_t* planes, int nm, int64_t kp, int64_t np, int64_t c0, int64_t wn,
-                        int64_t m, const int* moduli, int8_t* C, int64_t cstride, int device,
-                        cudaStream_t s) {
-  require(nm >= 1 && nm <= kSyrkMaxModuli, FSTK_E_COMPUTE, "internal: SYRK modulus count");
-  require(kp % kKB == 0 && kp > 0 && kp <= 133120, FSTK_E_COMPUTE, "internal: SYRK segment rows");
-  require(np % kTile == 0 && c0 % kTile == 0 && wn % kTile == 0 && m % kTile == 0 && c0 + m == np,
-          FSTK_E_COMPUTE, "internal: SYRK block shape");
+template <int NM>
+void launch_syrk(const CUtensorMap& map, const SyrkParams& p, int pairs, int device, cudaStream_t s) {
+  static std::atomic<uint64_t> attr_set{0};
+  const uint64_t bit = uint64_t(1) << (device & 63);
+  if (!(attr_set.load() & bit)) {
+    cudaFuncSetAttribute(syrk_crt_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr_set.fetch_or(bit);
+  }
+  syrk_crt_kernel<NM><<<2 * pairs, kThreads, kSmemBytes, s>>>(map, p);
+  check_launch("syrk_crt_kernel");
+}
+
+}  // namespace
+
+size_t syrk_crt_scratch_bytes(int nm, int device) {
+  return static_cast<size_t>(sm_count(device)) * nm * kHalf * kTile;
+}
+
+double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n, int k, const int* ex,
+                     double* G, int64_t ldg, bool accumulate, bool negate, uint8_t* scratch, int device,
+                     cudaStream_t s) {
+  require(nm >= 8 && nm <= 17, FSTK_E_COMPUTE, "internal: SYRK modulus count");
+  require(kp % kKB == 0 && kp > 0 && kp <= 66560, FSTK_E_COMPUTE, "internal: SYRK segment rows");
+  require(np % kTile == 0 && np >= n && n > 0, FSTK_E_COMPUTE, "internal: SYRK plane shape");
   require(static_cast<int64_t>(nm) * np < (int64_t(1) << 31), FSTK_E_COMPUTE,
           "internal: SYRK plane rows exceed the tensor-map range");
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(syrk_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-  });
+  const int nt = static_cast<int>(np / kTile);
+  const int nbands = (nt + kBandTiles - 1) / kBandTiles;
+  require(nbands <= kMaxBands, FSTK_E_COMPUTE, "internal: SYRK Gram too wide (> 131072 columns)");
   CUtensorMap map;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(kp), static_cast<cuuint64_t>(nm * np)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(kp)};
@@ -357,26 +499,53 @@ double syrk_i8_residues(const int8_t* planes, int nm, int64_t kp, int64_t np, in
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) fail(FSTK_E_COMPUTE, "cuTensorMapEncodeTiled failed for the SYRK planes");
   SyrkParams p{};
-  p.nm = nm;
   p.kblocks = static_cast<int>(kp / kKB);
   p.np = static_cast<int>(np);
-  p.c0 = static_cast<int>(c0);
-  p.ntj = static_cast<int>(wn / kTile);
-  p.nti = static_cast<int>(m / kTile);
-  p.tri = p.ntj * (p.ntj + 1) / 2;
-  p.per_mod = p.tri + (p.nti - p.ntj) * p.ntj;
-  p.ntasks = nm * p.per_mod;
-  p.ldc = m;
-  p.cstride = cstride;
-  p.C = C;
-  for (int t = 0; t < nm; ++t) {
-    p.mod[t] = moduli[t];
-    p.inv[t] = 1.0 / static_cast<double>(moduli[t]);
+  p.nt = nt;
+  p.nbands = nbands;
+  int task = 0;
+  for (int b = 0; b < nbands; ++b) {
+    p.band_start[b] = task;
+    const int wb = std::min(kBandTiles, nt - b * kBandTiles);
+    task += wb * (wb + 1) / 2 + (nt - b * kBandTiles - wb) * wb;
   }
-  const int pairs = std::max(1, std::min(p.ntasks, syrk_i8_sm_count(device) / 2));
-  syrk_i8_kernel<<<2 * pairs, kThreads, kSmemBytes, s>>>(map, p);
-  check_launch("syrk_i8_kernel");
-  return 2.0 * static_cast<double>(p.ntasks) * kTile * kTile * static_cast<double>(kp);
+  p.band_start[nbands] = task;
+  p.ntasks = task;
+  p.n = n;
+  p.k = k;
+  p.accumulate = accumulate ? 1 : 0;
+  p.negate = negate ? 1 : 0;
+  static const int hint = [] {
+    const char* e = std::getenv("FSTK_SYRK_HINT");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.hint = hint;
+  p.ldg = ldg;
+  p.G = G;
+  p.ex = ex;
+  p.scratch = scratch;
+  for (int t = 0; t < nm; ++t) {
+    const unsigned m = static_cast<unsigned>(kmod(t));
+    p.mod[t] = kmod(t);
+    p.p16[t] = 65536u % m;
+    p.off[t] = ((1u << 22) / m + 1u) * m;
+    p.magic[t] = static_cast<unsigned>((uint64_t(1) << 32) / m);
+  }
+  const int pairs = std::max(1, std::min(p.ntasks, sm_count(device) / 2));
+  switch (nm) {
+    case 8: launch_syrk<8>(map, p, pairs, device, s); break;
+    case 9: launch_syrk<9>(map, p, pairs, device, s); break;
+    case 10: launch_syrk<10>(map, p, pairs, device, s); break;
+    case 11: launch_syrk<11>(map, p, pairs, device, s); break;
+    case 12: launch_syrk<12>(map, p, pairs, device, s); break;
+    case 13: launch_syrk<13>(map, p, pairs, device, s); break;
+    case 14: launch_syrk<14>(map, p, pairs, device, s); break;
+    case 15: launch_syrk<15>(map, p, pairs, device, s); break;
+    case 16: launch_syrk<16>(map, p, pairs, device, s); break;
+    case 17: launch_syrk<17>(map, p, pairs, device, s); break;
+    default: fail(FSTK_E_COMPUTE, "internal: unsupported CRT modulus count");
+  }
+  return 2.0 * static_cast<double>(p.ntasks) * nm * kTile * kTile * static_cast<double>(kp);
 }
 
 }  // namespace fstk_gpu
