@@ -104,19 +104,26 @@ struct DesignSrc {
     double scale;
     __device__ double operator()(int64_t r) const {
       double v = u[0][r];
-      for (int k = 1; k < d; ++k) v = xmul(v, u[k][r]);
+#pragma unroll
+      for (int k = 1; k < kMaxOrder; ++k)
+        if (k < d) v = xmul(v, u[k][r]);
       return xmul(scale, v);
     }
   };
+  // (Loops unrolled over kMaxOrder so u[] stays in registers.)
   __device__ Col col(int a) const {
     Col c;
     c.d = s.d;
     c.scale = s.scale;
     int64_t rem = a;
-    for (int k = 0; k < s.d; ++k) {
-      const int64_t jk = rem % s.ranks.v[k];
-      rem /= s.ranks.v[k];
-      c.u[k] = s.tables + s.toff.v[k] + jk * s.ldt + s.row0;
+#pragma unroll
+    for (int k = 0; k < kMaxOrder; ++k) {
+      c.u[k] = s.tables;
+      if (k < s.d) {
+        const int64_t jk = rem % s.ranks.v[k];
+        rem /= s.ranks.v[k];
+        c.u[k] = s.tables + s.toff.v[k] + jk * s.ldt + s.row0;
+      }
     }
     return c;
   }
@@ -281,13 +288,18 @@ __device__ __forceinline__ int sym_mod(long long x, int m) {
   return r;
 }
 
-// Thread per 4 consecutive rows of one column; plane i at X + i * kp * np.
+// Thread per RPT consecutive rows of one column (RPT = 16 on the 32-bit
+// path: 16 independent loads in flight and one 16-byte store per modulus,
+// 4 on the 64-bit path); plane i at X + i * kp * np.  kp % RPT == 0.
+template <bool X32>
+constexpr int residue_rows() { return X32 ? 16 : 4; }
 template <int NM, bool X32, class SRC>
-__global__ void residue_kernel(const SRC src, int64_t s0, int64_t rows, int n, int64_t kp,
+__global__ void __launch_bounds__(128) residue_kernel(const SRC src, int64_t s0, int64_t rows, int n, int64_t kp,
                                int64_t np, int k, const int* __restrict__ ex,
                                int8_t* __restrict__ X) {
+  constexpr int RPT = residue_rows<X32>();
   const int a = blockIdx.y;
-  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * RPT;
   if (r0 >= kp) return;
   const Pow2Scale sc(k - ex[a]);
   int8_t* dst = X + static_cast<int64_t>(a) * kp + r0;
@@ -295,26 +307,37 @@ __global__ void residue_kernel(const SRC src, int64_t s0, int64_t rows, int n, i
     // |x| <= 2^30: 32-bit conversion, and each residue as an unsigned
     // remainder of x + (a multiple of m above 2^30) -- no signed-division
     // fix-ups.  Same symmetric residues as sym_mod.
-    int x[4] = {0, 0, 0, 0};
+    int x[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) x[u] = 0;
     if (a < n) {
       const auto col = src.col(a);
+      if (r0 + RPT <= rows) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (r0 + u < rows) x[u] = __double2int_rn(sc(col(s0 + r0 + u)));
+        for (int u = 0; u < RPT; ++u) x[u] = __double2int_rn(sc(col(s0 + r0 + u)));
+      } else {
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+          if (r0 + u < rows) x[u] = __double2int_rn(sc(col(s0 + r0 + u)));
+      }
     }
 #pragma unroll
     for (int i = 0; i < NM; ++i) {
       const unsigned m = static_cast<unsigned>(kmod(i));
       const unsigned off = ((1u << 30) / m + 1u) * m;
-      signed char r[4];
+      uint32_t w[RPT / 4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int v = static_cast<int>((static_cast<unsigned>(x[u]) + off) % m);
-        if (v > static_cast<int>(m / 2)) v -= static_cast<int>(m);
-        r[u] = static_cast<signed char>(v);
+      for (int g = 0; g < RPT / 4; ++g) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          int v = static_cast<int>((static_cast<unsigned>(x[4 * g + b]) + off) % m);
+          if (v > static_cast<int>(m / 2)) v -= static_cast<int>(m);
+          word |= (static_cast<uint32_t>(v) & 0xFFu) << (8 * b);
+        }
+        w[g] = word;
       }
-      *reinterpret_cast<char4*>(dst + static_cast<int64_t>(i) * kp * np) =
-          make_char4(r[0], r[1], r[2], r[3]);
+      *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(i) * kp * np) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     return;
   }
@@ -370,11 +393,13 @@ int crt_moduli(int k, int64_t kp) {
 template <int NM, class SRC>
 void launch_crt(const SRC& src, int64_t s0, int64_t kr, int n, int64_t kp, int64_t np, int k,
                 const int* ex, int8_t* X, cudaStream_t s) {
-  dim3 g(static_cast<unsigned>(ceil_div(kp / 4, 256)), static_cast<unsigned>(np));
-  if (k <= 30)
-    residue_kernel<NM, true, SRC><<<g, 256, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
-  else
-    residue_kernel<NM, false, SRC><<<g, 256, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
+  if (k <= 30) {
+    dim3 g(static_cast<unsigned>(ceil_div(kp / residue_rows<true>(), 128)), static_cast<unsigned>(np));
+    residue_kernel<NM, true, SRC><<<g, 128, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
+  } else {
+    dim3 g(static_cast<unsigned>(ceil_div(kp / residue_rows<false>(), 128)), static_cast<unsigned>(np));
+    residue_kernel<NM, false, SRC><<<g, 128, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
+  }
   check_launch("residue_kernel");
 }
 template <int NM, class CT>
