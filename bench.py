@@ -625,11 +625,21 @@ def gram_roofline(gram_flops, info, t, peak_fp64, i8=None):
         ach = info["gram_int8_ops"] / t / 1e12
         pk = i8["tops"] if i8 else 4500.0
         src = i8["source"] if i8 else "nominal B200 dense int8 (live probe unavailable)"
+        import paper_1907_05884_b200 as F
+
+        eng = F.gram_engine()
+        if eng == "tcgen05":
+            kern = (f"syrk_crt_kernel (fstk_syrk.cu): hand-written tcgen05.mma.cta_group::2.kind::i8 "
+                    f"SYRK, lower-triangle 256x256 tiles of every CRT modulus in one persistent launch "
+                    f"per row segment, Garner fold into G in the epilogue; plane-accuracy level "
+                    f"{info['gram_slices']}; residue/exponent kernels in fstk_gram.cu")
+        else:
+            kern = (f"cuBLASLt int8 IMMA GEMMs, one per CRT modulus, at plane-accuracy level "
+                    f"{info['gram_slices']} (residue/fold kernels in fstk_gram.cu)")
         return {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TOP/s (int8)",
-                "frac": ach / pk, "peak_source": src,
+                "frac": ach / pk, "peak_source": src, "engine": eng,
                 "fp64_equivalent_tflops": gram_flops / t / 1e12, "fp64_peak_tflops": peak_fp64,
-                "kernel": f"cuBLASLt int8 IMMA GEMMs, one per CRT modulus, at plane-accuracy level "
-                          f"{info['gram_slices']} (residue/fold kernels in fstk_gram.cu)"}
+                "kernel": kern}
     ach = gram_flops / t / 1e12
     return {"bound": "tensor", "achieved": ach, "peak": peak_fp64, "unit": "TFLOP/s",
             "frac": ach / peak_fp64 if peak_fp64 else None,

@@ -573,8 +573,16 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   if (ldg < 0) ldg = n;
   require(ns >= 4 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: 4..7 plane-equivalents");
   const int k = 7 * ns - 1;
-  // SYRK engine: 256-column tiles and 128-byte K blocks (zero padding).
-  const bool syrk = gram_engine() == 1;
+  // SYRK engine: 256-column tiles and 128-byte K blocks (zero padding).  It
+  // folds each tile in its epilogue while the next tile's MMAs run, which
+  // hides the fold only when a tile's K loop is long: short updates (the
+  // blocked Cholesky's 2048-row trailing updates, outside the hot path) keep
+  // the library GEMMs and the separate fold kernel.
+  static const int64_t syrk_min_rows = [] {
+    const char* e = std::getenv("FSTK_SYRK_MIN_ROWS");
+    return e ? std::atoll(e) : int64_t(8192);
+  }();
+  const bool syrk = gram_engine() == 1 && rows >= syrk_min_rows;
   const int64_t np = round_up(static_cast<int64_t>(n), syrk ? 256 : 16);
   const int64_t kalign = syrk ? 128 : 16;
   static const int64_t seg_cap = [] {

@@ -16,10 +16,17 @@
 //                                 held in shared memory, and only the S sampled
 //                                 rows are written (scaled, DCT post-rotation
 //                                 fused) into A;
-//   solve_system (:112-123)       A^T A and A^T b (cuBLAS DSYRK/DGEMV on the
-//                                 materialised sketch), Cholesky (cuSOLVER
-//                                 potrf/potrs, timed separately), minimum-norm
-//                                 eigen fallback when not positive definite;
+//   solve_system (:112-123)       A^T A on the int8 tensor cores (exact CRT
+//                                 residue products: the hand-written tcgen05
+//                                 SYRK of fstk_syrk.cu with its Garner fold,
+//                                 fstk_gram.cu; native fp64 DSYRK only as the
+//                                 escalation fallback) and A^T b (DGEMV), a
+//                                 Cholesky factor (blocked, int8 trailing
+//                                 updates; timed separately) refined against A
+//                                 itself to the least-squares solution; the
+//                                 rank decision and minimum-norm solution of a
+//                                 deficient system follow the reference's
+//                                 ColPivHouseholderQR + COD (fstk_rank.cu);
 //   relative_residual (:350-356)  device evaluation of the validation points.
 #include <cublas_v2.h>
 #include <cusolverDn.h>
