@@ -265,6 +265,35 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* refit, double* gr
  * counterpart (an arithmetic choice of this backend; the solution still
  * matches the reference's QR). */
 int32_t fstk_gpu_gram_slices(int32_t slices);
+
+/* ---- scattered-to-grid interpolation ----
+ * interpolate_to_grid (proj/src/ingest.cpp:265-383; ingest.hpp:44-62):
+ * k-nearest-neighbour inverse-distance weighting over the reference's
+ * uniform-binning spatial index, on the GPU.  points: Q x d column-major
+ * (Eigen layout), values: Q; box_lo/box_hi: the cloud's bounding box (NULL =
+ * the points' own, as PointCloud::from_data computes it); sizes / grid_lo /
+ * grid_hi: the StructuredGrid (sizes >= 2, lo < hi); neighbors <= 0 selects
+ * 2d + 2 (at most 64); power > 0.  out: prod(sizes) values, mode-0 fastest
+ * (DenseTensor order).  report (optional) mirrors InterpolationReport;
+ * neighbor_ids (optional): per node the k retained sample ids in ascending
+ * (distance, id) order.  Errors as the reference: Shape (dimension), Data
+ * (empty, non-finite, box), Parameter (grid, power).  The _device variant
+ * takes device pointers and a stream. */
+typedef struct fstk_interp_report {
+  int32_t box_covered;
+  double max_nearest_distance;
+  double extrapolated_fraction;
+} fstk_interp_report;
+int32_t fstk_gpu_interpolate_to_grid(const double* points, const double* values, int64_t q, int32_t d,
+                                     const double* box_lo, const double* box_hi, const int64_t* sizes,
+                                     const double* grid_lo, const double* grid_hi, int32_t neighbors,
+                                     double power, double* out, fstk_interp_report* report,
+                                     uint32_t* neighbor_ids, int32_t device, fstk_gpu_error* err);
+int32_t fstk_gpu_interpolate_to_grid_device(const double* points, const double* values, int64_t q, int32_t d,
+                                            const double* box_lo, const double* box_hi, const int64_t* sizes,
+                                            const double* grid_lo, const double* grid_hi, int32_t neighbors,
+                                            double power, double* out, fstk_interp_report* report,
+                                            uint32_t* neighbor_ids, void* stream, fstk_gpu_error* err);
 /* The int8 GEMM engine of the CRT Gram: 1 = the hand-written sm_100a
  * tcgen05 SYRK (default: lower-triangle 256x256 tiles of all moduli in one
  * persistent launch, residues reduced in the epilogue), 2 = cuBLASLt IMMA

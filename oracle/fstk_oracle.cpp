@@ -31,6 +31,7 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <limits>
 #include <map>
 #include <mutex>
 #include <numeric>
@@ -859,6 +860,254 @@ int guarded(F&& f) {
   }
 }
 
+// ------------------------------------------- IDW interpolation (§8f-4) ---
+// ingest.cpp:117-383 restated: uniform-binning spatial index over the grid
+// box (build_index :140-190), fixed-size max-heap of (d2, id) pairs under
+// lexicographic order (NeighborHeap :194-212, std::push_heap/pop_heap as the
+// reference uses them, so the weight sums run in the reference's order),
+// Chebyshev rings (for_ring :217-260) with the reference's stop rule, exact
+// hits, inverse-distance weights and the report (:265-383).
+struct IdwIndex {
+  int d;
+  std::vector<std::int64_t> nbins;
+  std::vector<double> lo, width;
+  std::vector<std::uint32_t> offsets, items;
+  double min_width = 0.0, bin_diag = 0.0;
+  std::int64_t bin_of(int k, double x) const {
+    const auto b = static_cast<std::int64_t>(std::floor((x - lo[k]) / width[k]));
+    return std::min<std::int64_t>(nbins[k] - 1, std::max<std::int64_t>(0, b));
+  }
+  std::int64_t flat(const std::vector<std::int64_t>& c) const {
+    std::int64_t f = 0;
+    for (int k = d - 1; k >= 0; --k) f = f * nbins[k] + c[k];
+    return f;
+  }
+};
+
+static IdwIndex idw_build_index(const double* pts, std::int64_t q, int d, const double* box_lo,
+                                const double* box_hi, const std::int64_t* sizes, const double* glo,
+                                const double* ghi) {
+  IdwIndex ix;
+  ix.d = d;
+  ix.nbins.resize(d);
+  ix.lo.resize(d);
+  ix.width.resize(d);
+  const double per_mode = std::pow(std::max(1.0, static_cast<double>(q) / 4.0), 1.0 / d);
+  std::int64_t total = 1;
+  for (int k = 0; k < d; ++k) {
+    const std::int64_t cells = sizes[k] - 1;
+    ix.nbins[k] = std::max<std::int64_t>(
+        1, std::min<std::int64_t>(cells, static_cast<std::int64_t>(std::llround(per_mode))));
+    total *= ix.nbins[k];
+  }
+  while (total > (std::int64_t(1) << 22)) {
+    total = 1;
+    for (int k = 0; k < d; ++k) {
+      ix.nbins[k] = std::max<std::int64_t>(1, ix.nbins[k] / 2);
+      total *= ix.nbins[k];
+    }
+  }
+  double min_w = std::numeric_limits<double>::infinity();
+  double diag2 = 0.0;
+  for (int k = 0; k < d; ++k) {
+    ix.lo[k] = std::min(glo[k], box_lo[k]);
+    const double hi = std::max(ghi[k], box_hi[k]);
+    ix.width[k] = (hi - ix.lo[k]) / static_cast<double>(ix.nbins[k]);
+    if (ix.width[k] <= 0.0) ix.width[k] = 1.0;
+    min_w = std::min(min_w, ix.width[k]);
+    diag2 += ix.width[k] * ix.width[k];
+  }
+  ix.min_width = min_w;
+  ix.bin_diag = std::sqrt(diag2);
+  std::vector<std::uint32_t> bin_id(static_cast<std::size_t>(q));
+  std::vector<std::uint32_t> counts(static_cast<std::size_t>(total) + 1, 0);
+  std::vector<std::int64_t> c(d);
+  for (std::int64_t i = 0; i < q; ++i) {
+    for (int k = 0; k < d; ++k) c[k] = ix.bin_of(k, pts[i + k * q]);
+    bin_id[i] = static_cast<std::uint32_t>(ix.flat(c));
+    ++counts[bin_id[i] + 1];
+  }
+  for (std::size_t b = 1; b < counts.size(); ++b) counts[b] += counts[b - 1];
+  ix.items.resize(static_cast<std::size_t>(q));
+  std::vector<std::uint32_t> cursor(counts.begin(), counts.end() - 1);
+  for (std::int64_t i = 0; i < q; ++i) ix.items[cursor[bin_id[i]]++] = static_cast<std::uint32_t>(i);
+  ix.offsets = std::move(counts);
+  return ix;
+}
+
+struct IdwHeap {
+  std::vector<std::pair<double, std::uint32_t>> heap;
+  std::size_t cap;
+  explicit IdwHeap(std::size_t k) : cap(k) { heap.reserve(k); }
+  bool full() const { return heap.size() >= cap; }
+  double worst() const { return heap.front().first; }
+  void push(double d2, std::uint32_t id) {
+    const std::pair<double, std::uint32_t> p{d2, id};
+    if (heap.size() < cap) {
+      heap.push_back(p);
+      std::push_heap(heap.begin(), heap.end());
+    } else if (p < heap.front()) {
+      std::pop_heap(heap.begin(), heap.end());
+      heap.back() = p;
+      std::push_heap(heap.begin(), heap.end());
+    }
+  }
+};
+
+template <typename Fn>
+static void idw_for_ring(const IdwIndex& ix, const std::vector<std::int64_t>& center, std::int64_t rho,
+                         Fn&& fn) {
+  const int d = ix.d;
+  std::vector<std::int64_t> c(d);
+  if (rho == 0) {
+    for (int k = 0; k < d; ++k) c[k] = center[k];
+    fn(c);
+    return;
+  }
+  std::vector<std::int64_t> lo(d), hi(d);
+  for (int axis = 0; axis < d; ++axis) {
+    for (int side = 0; side < 2; ++side) {
+      const std::int64_t fixed = center[axis] + (side == 0 ? -rho : rho);
+      if (fixed < 0 || fixed >= ix.nbins[axis]) continue;
+      bool empty = false;
+      for (int k = 0; k < d; ++k) {
+        if (k == axis) {
+          lo[k] = hi[k] = fixed;
+          continue;
+        }
+        const std::int64_t r = k < axis ? rho - 1 : rho;
+        lo[k] = std::max<std::int64_t>(0, center[k] - r);
+        hi[k] = std::min(ix.nbins[k] - 1, center[k] + r);
+        if (lo[k] > hi[k]) empty = true;
+      }
+      if (empty) continue;
+      for (int k = 0; k < d; ++k) c[k] = lo[k];
+      for (;;) {
+        fn(c);
+        int k = 0;
+        while (k < d && (k == axis || ++c[k] > hi[k])) {
+          if (k != axis) c[k] = lo[k];
+          ++k;
+        }
+        if (k == d) break;
+      }
+    }
+  }
+}
+
+// out: prod(sizes) values, mode-0 fastest.  report: box_covered,
+// max_nearest_distance, extrapolated_fraction.  nbr (optional): per node the
+// k retained ids sorted by (d2, id), padded with UINT32_MAX.
+static void interpolate_to_grid(const double* pts, const double* vals, std::int64_t q, int d,
+                                const double* box_lo_in, const double* box_hi_in,
+                                const std::int64_t* sizes, const double* glo, const double* ghi,
+                                int neighbors, double power, double* out, double* report,
+                                std::uint32_t* nbr) {
+  require(d >= 1 && d <= 8, Shape, "point cloud dimension must be in [1, 8]");
+  require(q >= 1, Data, "point cloud is empty");
+  std::vector<double> box_lo(d), box_hi(d);
+  for (int k = 0; k < d; ++k) {
+    double mn = pts[k * q], mx = pts[k * q];
+    for (std::int64_t i = 0; i < q; ++i) {
+      require(std::isfinite(pts[i + k * q]), Data, "point coordinates must be finite");
+      mn = std::min(mn, pts[i + k * q]);
+      mx = std::max(mx, pts[i + k * q]);
+    }
+    box_lo[k] = box_lo_in ? box_lo_in[k] : mn;
+    box_hi[k] = box_hi_in ? box_hi_in[k] : mx;
+    require(mn >= box_lo[k] && mx <= box_hi[k], Data, "bounding box does not cover the points");
+  }
+  for (std::int64_t i = 0; i < q; ++i) require(std::isfinite(vals[i]), Data, "point cloud values must be finite");
+  for (int k = 0; k < d; ++k) {
+    require(sizes[k] >= 2, Parameter, "grid sizes must be >= 2");
+    require(glo[k] < ghi[k], Parameter, "grid intervals must be nondegenerate");
+  }
+  const int kn = neighbors > 0 ? neighbors : 2 * d + 2;
+  require(power > 0.0, Parameter, "IDW power must be positive");
+  const IdwIndex ix = idw_build_index(pts, q, d, box_lo.data(), box_hi.data(), sizes, glo, ghi);
+  double cell_diag2 = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double h = (ghi[k] - glo[k]) / static_cast<double>(sizes[k] - 1);
+    cell_diag2 += h * h;
+  }
+  const double hit_tol2 = 1e-24 * cell_diag2;
+  bool covered = true;
+  for (int k = 0; k < d; ++k)
+    if (box_lo[k] < glo[k] || box_hi[k] > ghi[k]) covered = false;
+  std::int64_t n_nodes = 1;
+  for (int k = 0; k < d; ++k) n_nodes *= sizes[k];
+  std::mutex mu;
+  double max_nearest = 0.0;
+  std::int64_t n_extra = 0;
+  parallel_for(static_cast<std::size_t>(n_nodes), [&](std::size_t begin, std::size_t end) {
+    std::vector<std::int64_t> midx(d), center(d);
+    std::vector<double> y(d);
+    double lmax = 0.0;
+    std::int64_t lextra = 0;
+    for (std::size_t node = begin; node < end; ++node) {
+      std::int64_t rem = static_cast<std::int64_t>(node);
+      for (int k = 0; k < d; ++k) {
+        midx[k] = rem % sizes[k];
+        rem /= sizes[k];
+        y[k] = glo[k] + (ghi[k] - glo[k]) * static_cast<double>(midx[k]) /
+                            static_cast<double>(sizes[k] - 1);
+        center[k] = ix.bin_of(k, y[k]);
+      }
+      IdwHeap heap(static_cast<std::size_t>(kn));
+      std::int64_t max_rho = 0;
+      for (int k = 0; k < d; ++k)
+        max_rho = std::max({max_rho, center[k], ix.nbins[k] - 1 - center[k]});
+      for (std::int64_t rho = 0;; ++rho) {
+        idw_for_ring(ix, center, rho, [&](const std::vector<std::int64_t>& c) {
+          const std::int64_t b = ix.flat(c);
+          for (std::uint32_t ii = ix.offsets[b]; ii < ix.offsets[b + 1]; ++ii) {
+            const std::uint32_t id = ix.items[ii];
+            double d2 = 0.0;
+            for (int k = 0; k < d; ++k) {
+              const double diff = pts[id + k * q] - y[k];
+              d2 += diff * diff;
+            }
+            heap.push(d2, id);
+          }
+        });
+        const double safe = static_cast<double>(rho) * ix.min_width;
+        if (heap.full() && heap.worst() <= safe * safe) break;
+        if (rho >= max_rho) break;
+      }
+      auto best = heap.heap.front();
+      for (const auto& cand : heap.heap) best = std::min(best, cand);
+      double value;
+      if (best.first < hit_tol2) {
+        value = vals[best.second];
+      } else {
+        double wsum = 0.0, vsum = 0.0;
+        for (const auto& e : heap.heap) {
+          const double w = power == 2.0 ? 1.0 / e.first : std::pow(e.first, -0.5 * power);
+          wsum += w;
+          vsum += w * vals[e.second];
+        }
+        value = vsum / wsum;
+      }
+      out[node] = value;
+      if (nbr) {
+        auto sorted = heap.heap;
+        std::sort(sorted.begin(), sorted.end());
+        for (int j = 0; j < kn; ++j)
+          nbr[node * kn + j] = j < static_cast<int>(sorted.size()) ? sorted[j].second : 0xFFFFFFFFu;
+      }
+      const double nearest = std::sqrt(best.first);
+      lmax = std::max(lmax, nearest);
+      if (nearest > ix.bin_diag) ++lextra;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    max_nearest = std::max(max_nearest, lmax);
+    n_extra += lextra;
+  });
+  report[0] = covered ? 1.0 : 0.0;
+  report[1] = max_nearest;
+  report[2] = static_cast<double>(n_extra) / static_cast<double>(n_nodes);
+}
+
 }  // namespace
 
 #define MODEL_ARGS                                                            \
@@ -904,6 +1153,15 @@ int oracle_unitary_fft(double* x_interleaved, std::uint64_t n, int inverse) {
 }
 int oracle_dct2(double* x, std::uint64_t n) {
   return guarded([&] { dct2_orthonormal(x, n); });
+}
+int oracle_interpolate_to_grid(const double* pts, const double* vals, std::int64_t q, int d,
+                               const double* box_lo, const double* box_hi, const std::int64_t* sizes,
+                               const double* glo, const double* ghi, int neighbors, double power,
+                               double* out, double* report, std::uint32_t* nbr) {
+  return guarded([&] {
+    interpolate_to_grid(pts, vals, q, d, box_lo, box_hi, sizes, glo, ghi, neighbors, power, out,
+                        report, nbr);
+  });
 }
 int oracle_wht(double* x, std::uint64_t n) {
   return guarded([&] { wht_orthonormal(x, n); });

@@ -470,3 +470,41 @@ def self_convergence(model, points, values, s_values, seed=0, working_subset=1 <
         dl = np.linalg.norm(alphas[i + 1] - alphas[i])
         out.append((s_values[i], dl / den if den > 0 else dl))
     return out
+
+
+def interpolate_to_grid(points, values, sizes, intervals=None, neighbors=0, power=2.0, box=None,
+                        return_neighbors=False):
+    """ingest.cpp:265-383 restated (kNN inverse-distance weighting over a
+    uniform-binning spatial index).  points: (Q, d); sizes: grid sizes;
+    intervals: [(lo, hi)] per mode (default unit box); box: optional (lo, hi)
+    arrays (default: the points' bounding box, PointCloud::from_data).
+    Returns (grid values of shape sizes, mode-0 fastest; report dict) and,
+    with return_neighbors, per node the retained ids sorted by (d2, id)."""
+    p = np.asfortranarray(np.asarray(points, dtype=np.float64))
+    q, d = p.shape
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    sz = np.ascontiguousarray(sizes, dtype=np.int64)
+    iv = intervals if intervals is not None else [(0.0, 1.0)] * d
+    glo = np.ascontiguousarray([a for a, _ in iv], dtype=np.float64)
+    ghi = np.ascontiguousarray([b for _, b in iv], dtype=np.float64)
+    n = int(np.prod(sz))
+    out = np.empty(n, dtype=np.float64)
+    rep = np.zeros(3, dtype=np.float64)
+    kn = int(neighbors) if neighbors > 0 else 2 * d + 2
+    nbr = np.empty(n * kn, dtype=np.uint32) if return_neighbors else None
+    blo = bhi = None
+    if box is not None:
+        blo = np.ascontiguousarray(box[0], dtype=np.float64)
+        bhi = np.ascontiguousarray(box[1], dtype=np.float64)
+    L = lib()
+    _check(L.oracle_interpolate_to_grid(
+        _dp(p), _dp(v), C.c_int64(q), C.c_int(d), _dp(blo) if blo is not None else None,
+        _dp(bhi) if bhi is not None else None, sz.ctypes.data_as(C.POINTER(C.c_int64)), _dp(glo),
+        _dp(ghi), C.c_int(int(neighbors)), C.c_double(float(power)), _dp(out), _dp(rep),
+        nbr.ctypes.data_as(C.POINTER(C.c_uint32)) if nbr is not None else None))
+    report = {"box_covered": bool(rep[0]), "max_nearest_distance": float(rep[1]),
+              "extrapolated_fraction": float(rep[2])}
+    grid = out.reshape(tuple(int(x) for x in sz), order="F")
+    if return_neighbors:
+        return grid, report, nbr.reshape(n, kn)
+    return grid, report

@@ -8,8 +8,9 @@ proj/python/module.cpp): `Model.evaluate_batch`, `load_model`,
 in libfstk_gpu.so on the GPU; there is no CPU fallback.
 """
 from ._lib import FstkError, FstkIOError, FstkValueError, launch_count, set_devices
-from .cloud import (PointCloud, read_cloud, read_cloud_binary, read_cloud_csv, read_cloud_device,
-                    read_points_csv, write_cloud_binary, write_cloud_csv)
+from .cloud import (InterpolationOptions, InterpolationReport, PointCloud, StructuredGrid,
+                    interpolate_to_grid, read_cloud, read_cloud_binary, read_cloud_csv,
+                    read_cloud_device, read_points_csv, write_cloud_binary, write_cloud_csv)
 from .model import (BasisSpec, Model, ModelMetadata, ModeFunction, eval_basis, evaluate_fields,
                     load_model, save_model)
 from .refit import (RefitSession, build_design_rows, cholesky, gram, gram_engine, gram_slices, leverage_scores, mixed_matrix,
@@ -30,4 +31,5 @@ __all__ = [
     "set_max_threads", "FstkError", "FstkValueError", "FstkIOError",
     "launch_count", "set_devices", "PointCloud", "read_cloud", "read_cloud_binary", "read_cloud_csv",
     "read_cloud_device", "read_points_csv", "write_cloud_binary", "write_cloud_csv",
+    "StructuredGrid", "InterpolationOptions", "InterpolationReport", "interpolate_to_grid",
 ]

@@ -46,6 +46,11 @@ class Err(C.Structure):
                 ("value", C.c_double), ("message", C.c_char * 256)]
 
 
+class InterpReport(C.Structure):
+    _fields_ = [("box_covered", C.c_int32), ("max_nearest_distance", C.c_double),
+                ("extrapolated_fraction", C.c_double)]
+
+
 class ModelDesc(C.Structure):
     _fields_ = [("d", C.c_int32), ("ranks", C.POINTER(C.c_int64)),
                 ("core", C.POINTER(C.c_double)), ("family", C.POINTER(C.c_int32)),
@@ -94,6 +99,7 @@ EXPORTS = [
     "fstk_gpu_cholesky_device", "fstk_gpu_refit_certify", "fstk_gpu_refit_local_qr",
     "fstk_gpu_refit_qr_solve", "fstk_gpu_qr_stack", "fstk_gpu_solve_system",
     "fstk_gpu_refit_sketched_columns", "fstk_gpu_eval_serialize",
+    "fstk_gpu_interpolate_to_grid", "fstk_gpu_interpolate_to_grid_device",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -199,6 +205,12 @@ def lib():
     L.fstk_gpu_leverage_scores.argtypes = [DP, C.c_int64, C.c_int64, DP, C.POINTER(C.c_int32),
                                            C.POINTER(Err)]
     L.fstk_gpu_point_major_to_soa.argtypes = [VP, C.c_int64, C.c_int32, VP, VP, C.POINTER(Err)]
+    L.fstk_gpu_interpolate_to_grid.argtypes = [VP, VP, C.c_int64, C.c_int32, VP, VP, VP, VP, VP,
+                                               C.c_int32, C.c_double, VP, C.POINTER(InterpReport),
+                                               VP, C.c_int32, C.POINTER(Err)]
+    L.fstk_gpu_interpolate_to_grid_device.argtypes = [VP, VP, C.c_int64, C.c_int32, VP, VP, VP, VP,
+                                                      VP, C.c_int32, C.c_double, VP,
+                                                      C.POINTER(InterpReport), VP, VP, C.POINTER(Err)]
     L.fstk_gpu_profile_enable.argtypes = [C.c_int32]
     L.fstk_gpu_profile_enable.restype = None
     L.fstk_gpu_profile_read.argtypes = [DP, C.POINTER(C.c_uint64), C.POINTER(Err)]

@@ -1,8 +1,10 @@
 """Point clouds: FPTC (binary) and CSV I/O, mirroring proj/src/ingest.cpp:19-49
 (PointCloud::from_data / validate) and :600-754 (CSV + FPTC readers/writers,
-docs/format.md:29-55), plus FPTC ingest straight to a device SoA buffer
+docs/format.md:29-55), FPTC ingest straight to a device SoA buffer
 (SURVEY 8f-4): the point-major payload is uploaded as-is and transposed by
-fstk_gpu_point_major_to_soa on the GPU.
+fstk_gpu_point_major_to_soa on the GPU, and scattered-to-grid IDW
+interpolation (interpolate_to_grid, ingest.cpp:265-383) on the GPU
+(fstk_idw.cu).
 """
 from __future__ import annotations
 
@@ -12,7 +14,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import Err, FstkIOError, check, lib, make_error
+from ._lib import Err, FstkIOError, InterpReport, check, lib, make_error
 
 FPTC_MAGIC = b"FPTC"
 FPTC_VERSION = 1
@@ -233,3 +235,99 @@ def read_cloud(path: str) -> PointCloud:
     except OSError as e:
         raise FstkIOError("Io", f"cannot open: {path}") from e
     return read_cloud_binary(path) if magic == FPTC_MAGIC else read_cloud_csv(path)
+
+
+# ------------------------------------------------- grid interpolation ---
+@dataclass
+class StructuredGrid:
+    """ingest.hpp:28-39: sizes I_k >= 2 and intervals [lo, hi] per mode."""
+    sizes: list
+    intervals: list
+
+    @property
+    def dim(self) -> int:
+        return len(self.sizes)
+
+    def node(self, mode: int, i: int) -> float:
+        """ingest.cpp:57-61."""
+        lo, hi = self.intervals[mode]
+        return lo + (hi - lo) * float(i) / float(self.sizes[mode] - 1)
+
+    def coords(self, mode: int) -> np.ndarray:
+        return np.array([self.node(mode, i) for i in range(self.sizes[mode])], dtype=np.float64)
+
+    def validate(self):
+        """ingest.cpp:70-80."""
+        if not (1 <= len(self.sizes) <= K_MAX_ORDER):
+            raise make_error(1, "grid dimension must be in [1, 8]")
+        if len(self.sizes) != len(self.intervals):
+            raise make_error(1, "grid sizes/intervals mismatch")
+        for s, (lo, hi) in zip(self.sizes, self.intervals):
+            if s < 2:
+                raise make_error(1, "grid sizes must be >= 2")
+            if not lo < hi:
+                raise make_error(1, "grid intervals must be nondegenerate")
+
+    @staticmethod
+    def unit(sizes) -> "StructuredGrid":
+        g = StructuredGrid(list(int(s) for s in sizes), [(0.0, 1.0)] * len(sizes))
+        g.validate()
+        return g
+
+
+@dataclass
+class InterpolationOptions:
+    """ingest.hpp:44-47."""
+    neighbors: int = 0    # 0 -> 2d + 2
+    power: float = 2.0    # inverse-distance exponent
+
+
+@dataclass
+class InterpolationReport:
+    """ingest.hpp:49-54."""
+    box_covered: bool = True
+    max_nearest_distance: float = 0.0
+    extrapolated_fraction: float = 0.0
+
+
+def interpolate_to_grid(pc: PointCloud, grid: StructuredGrid, options: InterpolationOptions | None = None,
+                        device=None, return_neighbors: bool = False):
+    """interpolate_to_grid (ingest.cpp:265-383) on the GPU (fstk_idw.cu):
+    kNN inverse-distance weighting over the reference's spatial index.
+    Returns (values with shape grid.sizes, mode-0 fastest like DenseTensor;
+    InterpolationReport), plus the (n_nodes, k) retained sample ids in
+    ascending (distance, id) order with return_neighbors."""
+    opts = options or InterpolationOptions()
+    pc.validate()
+    grid.validate()
+    if pc.dim != grid.dim:
+        raise make_error(2, "cloud/grid dimension mismatch")
+    d = pc.dim
+    sizes = np.ascontiguousarray(grid.sizes, dtype=np.int64)
+    glo = np.ascontiguousarray([a for a, _ in grid.intervals], dtype=np.float64)
+    ghi = np.ascontiguousarray([b for _, b in grid.intervals], dtype=np.float64)
+    n = int(np.prod(sizes))
+    k = int(opts.neighbors) if opts.neighbors > 0 else 2 * d + 2
+    out = np.empty(n, dtype=np.float64)
+    nbr = np.empty(n * k, dtype=np.uint32) if return_neighbors else None
+    pts = np.asfortranarray(pc.points, dtype=np.float64)
+    vals = np.ascontiguousarray(pc.values, dtype=np.float64)
+    blo = np.ascontiguousarray(pc.box_lo, dtype=np.float64)
+    bhi = np.ascontiguousarray(pc.box_hi, dtype=np.float64)
+    if device is None:
+        import torch
+
+        device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    rep = InterpReport()
+    err = Err()
+    check(lib().fstk_gpu_interpolate_to_grid(
+        pts.ctypes.data, vals.ctypes.data, pc.count, d, blo.ctypes.data, bhi.ctypes.data,
+        sizes.ctypes.data, glo.ctypes.data, ghi.ctypes.data, int(opts.neighbors), float(opts.power),
+        out.ctypes.data, C.byref(rep), nbr.ctypes.data if nbr is not None else None, int(device),
+        C.byref(err)), err)
+    report = InterpolationReport(bool(rep.box_covered), float(rep.max_nearest_distance),
+                                 float(rep.extrapolated_fraction))
+    tensor = out.reshape(tuple(int(x) for x in sizes), order="F")
+    if return_neighbors:
+        return tensor, report, nbr.reshape(n, k)
+    return tensor, report
