@@ -4,18 +4,88 @@
 // evaluate every node of a Cartesian grid through evaluate_batch.  On the
 // grid the model is separable: Y = G x_0 U_0 x_1 U_1 ... with U_k the mode
 // values on mode k's grid line (I_k x r_k, mode-value kernel), so the whole
-// grid is a chain of d mode products — one GEMM for mode 0 and strided-batched
-// GEMMs for the others (cuBLAS DGEMM, plain library GEMMs).  At 256^3 with
-// ranks 32^3 that is ~1.1 GFLOP instead of the 1.2 TFLOP of point-wise
-// evaluation, and the output write (8 B per node) bounds it.
-#include <cublas_v2.h>
-
+// grid is a chain of d mode products (the reference's dense mode product,
+// tensor.cpp:104-136) -- each one a batched GEMM with the tiny inner
+// dimension r_k, run by mode_product_kernel on the fp64 tensor cores
+// (DMMA m8n8k4, the contraction kernel's fragment layout).  At 256^3 with
+// ranks 32^3 that is ~1.2 GFLOP instead of the 1.2 TFLOP of point-wise
+// evaluation; the output write (8 B per node) bounds it.
 #include <climits>
 #include <vector>
 
+#include "fstk_common.cuh"
 #include "fstk_internal.h"
 
 using namespace fstk_gpu;
+
+namespace fstk_gpu {
+namespace {
+
+constexpr int kMpTile = 64;   // output tile: 64 rows (p) x 64 columns (i)
+constexpr int kMpKC = 32;     // inner-dimension chunk staged at once
+
+// One mode product in general strided form:
+//   B[p sp + i si + b sb] = sum_{j < r} A[p ap + j aj + b ab] U[i + I j]
+// for p < P, i < I, b < rest.  CTA: a 64 x 64 (p, i) tile of one b; its A
+// and U slabs are staged in shared memory 32 j at a time (zero padded to a
+// multiple of 4) and 8 warps each run 8 DMMA n-tiles per 4-wide j step.
+__global__ void __launch_bounds__(256) mode_product_kernel(const double* __restrict__ A, const double* __restrict__ U,
+                                                           double* __restrict__ B, int64_t P, int r, int64_t I,
+                                                           int64_t rest, int64_t ap, int64_t aj, int64_t ab,
+                                                           int64_t sp, int64_t si, int64_t sb) {
+  __shared__ double As[kMpKC][kMpTile + 1];
+  __shared__ double Us[kMpKC][kMpTile + 1];
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * kMpTile;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.y) * kMpTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  for (int64_t b = blockIdx.z; b < rest; b += gridDim.z) {
+    double c[8][2];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) c[n][0] = c[n][1] = 0.0;
+    for (int j0 = 0; j0 < r; j0 += kMpKC) {
+      const int jn = min(kMpKC, r - j0), j4 = (jn + 3) & ~3;
+      __syncthreads();
+      for (int e = threadIdx.x; e < j4 * kMpTile; e += blockDim.x) {
+        const int j = e / kMpTile, q = e % kMpTile;
+        const int64_t p = p0 + q, i = i0 + q;
+        As[j][q] = (j < jn && p < P) ? A[p * ap + (j0 + j) * aj + b * ab] : 0.0;
+        Us[j][q] = (j < jn && i < I) ? U[i + I * (j0 + j)] : 0.0;
+      }
+      __syncthreads();
+      for (int kk = 0; kk < j4; kk += 4) {
+        const double a = As[kk + t][warp * 8 + g];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) dmma_8x8x4(c[n][0], c[n][1], a, Us[kk + t][n * 8 + g]);
+      }
+    }
+    const int64_t p = p0 + warp * 8 + g;
+    if (p < P) {
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t i = i0 + n * 8 + 2 * t + h;
+          if (i < I) B[p * sp + i * si + b * sb] = c[n][h];
+        }
+      }
+    }
+  }
+}
+
+void mode_product(const double* A, const double* U, double* B, int64_t P, int r, int64_t I, int64_t rest,
+                  int64_t ap, int64_t aj, int64_t ab, int64_t sp, int64_t si, int64_t sb, cudaStream_t s) {
+  require(r >= 1, FSTK_E_COMPUTE, "internal: grid mode product rank");
+  dim3 grid(static_cast<unsigned>(ceil_div(P, kMpTile)), static_cast<unsigned>(ceil_div(I, kMpTile)),
+            static_cast<unsigned>(std::min<int64_t>(rest, 65535)));
+  require(ceil_div(P, kMpTile) < (int64_t(1) << 31) && ceil_div(I, kMpTile) <= 65535, FSTK_E_SHAPE,
+          "grid too large");
+  mode_product_kernel<<<grid, 256, 0, s>>>(A, U, B, P, r, I, rest, ap, aj, ab, sp, si, sb);
+  check_launch("mode_product_kernel");
+}
+
+}  // namespace
+}  // namespace fstk_gpu
 
 extern "C" {
 
@@ -33,8 +103,6 @@ int32_t fstk_gpu_evaluate_grid(const fstk_gpu_model* m, const double* coords, co
     std::lock_guard<std::mutex> lk(m->mu);
     DeviceGuard dg(m->device);
     cudaStream_t s = m->chunk[0].stream;
-    cublasHandle_t h = blas_handle(m->device);
-    cublasSetStream(h, s);
     DevBuf<double> dc(ncoord);
     FSTK_CUDA(cudaMemcpyAsync(dc.p, coords, ncoord * 8, cudaMemcpyHostToDevice, s));
     // Mode values on every grid line: U_k is I_k x r_k (ld = I_k).
@@ -82,25 +150,17 @@ int32_t fstk_gpu_evaluate_grid(const fstk_gpu_model* m, const double* coords, co
     }
     DevBuf<double> A(maxsz), B(maxsz);
     FSTK_CUDA(cudaMemcpyAsync(A.p, m->d_core.p, m->R * 8, cudaMemcpyDeviceToDevice, s));
-    const double one = 1.0, zero = 0.0;
     int64_t P = 1, rest = m->R;
     for (int k = 0; k < d; ++k) {
       const int64_t rk = m->ranks[k], Ik = sizes[k];
       rest /= rk;
       if (P == 1) {
-        // (I_k x rest) = U_k (I_k x r_k) * T (r_k x rest)
-        if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(Ik), static_cast<int>(rest),
-                        static_cast<int>(rk), &one, U.p + uoff[k], static_cast<int>(Ik), A.p,
-                        static_cast<int>(rk), &zero, B.p, static_cast<int>(Ik)) != CUBLAS_STATUS_SUCCESS)
-          fail(FSTK_E_COMPUTE, "cublasDgemm failed");
+        // (I_k x rest) = U_k (I_k x r_k) * T (r_k x rest): rows = the rest
+        // index (larger), columns = grid nodes.
+        mode_product(A.p, U.p + uoff[k], B.p, rest, static_cast<int>(rk), Ik, 1, rk, 1, 0, Ik, 1, 0, s);
       } else {
         // per trailing index b: (P x I_k) = T_b (P x r_k) * U_k^T
-        if (cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_T, static_cast<int>(P),
-                                      static_cast<int>(Ik), static_cast<int>(rk), &one, A.p,
-                                      static_cast<int>(P), P * rk, U.p + uoff[k],
-                                      static_cast<int>(Ik), 0, &zero, B.p, static_cast<int>(P),
-                                      P * Ik, static_cast<int>(rest)) != CUBLAS_STATUS_SUCCESS)
-          fail(FSTK_E_COMPUTE, "cublasDgemmStridedBatched failed");
+        mode_product(A.p, U.p + uoff[k], B.p, P, static_cast<int>(rk), Ik, rest, 1, P, P * rk, 1, P, P * Ik, s);
       }
       count_launch();
       std::swap(A, B);  // whole buffers (pointer, count and block size) trade places

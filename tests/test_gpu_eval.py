@@ -220,6 +220,22 @@ def test_grid_reconstruct_and_slice(O):
     assert e.value.kind == "Domain" and e.value.mode == 1 and e.value.index == 1
 
 
+def test_grid_mode_products_large_tiles(O):
+    """The DMMA mode-product chain (fstk_grid.cu) over several 64 x 64 tiles,
+    ragged edges and ranks above one 32-wide staging chunk equals point-wise
+    evaluation (GPU batch, itself 1e-12 from the oracle) within 1e-12."""
+    m = synth.random_model((40, 36, 8), (12, 12, 12), 6, seed=12)
+    sizes = (130, 70, 3)
+    g = m.reconstruct_grid(sizes)
+    nodes = [np.array([i / (s - 1) for i in range(s)]) for s in sizes]
+    X, Y, Z = np.meshgrid(*nodes, indexing="ij")
+    pts = np.stack([X.ravel(order="F"), Y.ravel(order="F"), Z.ravel(order="F")], axis=1)
+    want = m.evaluate_batch(pts)
+    assert rel(g.reshape(-1, order="F"), want) <= 1e-12
+    sub = np.random.default_rng(3).choice(len(pts), 2000, replace=False)
+    assert rel(g.reshape(-1, order="F")[sub], O.evaluate_batch(m, pts[sub])) <= 1e-12
+
+
 def test_evaluate_fields_shared_points(O):
     # BASELINE C5 shape in small: 8 seeded fields, one shared point set,
     # points uploaded once; each column equals the per-model batch bit for bit.
