@@ -112,6 +112,14 @@ typedef struct fstk_reestimate_info {
    * minimum-norm solution. */
   int32_t qr_path;
   double sigma_ratio;
+  /* Multi-device refit (fstk_gpu_set_devices(n > 1) before the model was
+   * created; fstk_multi.cu): host wall seconds of the column-to-row
+   * all-to-all and of the packed normal-equation reductions, the device
+   * count (0 = single device) and the transport (1 = NCCL, 2 = peer copies). */
+  double t_exchange;
+  double t_reduce;
+  int32_t devices;
+  int32_t multi_transport;
 } fstk_reestimate_info;
 
 typedef struct fstk_gpu_model fstk_gpu_model;

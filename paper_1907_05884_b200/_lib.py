@@ -74,7 +74,9 @@ class ReestimateInfo(C.Structure):
                 ("t_gram", C.c_double), ("t_solve", C.c_double), ("t_residual", C.c_double),
                 ("t_alloc", C.c_double), ("gram_slices", C.c_int32),
                 ("refine_steps", C.c_int32), ("gram_int8_ops", C.c_double),
-                ("qr_path", C.c_int32), ("sigma_ratio", C.c_double)]
+                ("qr_path", C.c_int32), ("sigma_ratio", C.c_double),
+                ("t_exchange", C.c_double), ("t_reduce", C.c_double), ("devices", C.c_int32),
+                ("multi_transport", C.c_int32)]
 
 
 # Every symbol include/fstk_gpu.h declares (checked by tests/test_abi.py).

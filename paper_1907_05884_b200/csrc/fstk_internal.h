@@ -250,6 +250,16 @@ double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n
                                      GramScratch& sc);
 
 
+// ---- multi-device refit (fstk_multi.cu) ----
+int refit_device(const fstk_gpu_refit* rf);
+int64_t refit_order(const fstk_gpu_refit* rf);
+bool refit_awaits_exchange(const fstk_gpu_refit* rf);
+int refit_gram_used(const fstk_gpu_refit* rf);
+bool refit_is_factored(const fstk_gpu_refit* rf);
+int32_t reestimate_core_multi(const fstk_gpu_model* m, const double* points, const double* values,
+                              int64_t q, int32_t d, const fstk_sketch_cfg* cfg, double* core_out,
+                              fstk_reestimate_info* info, fstk_gpu_error* err);
+
 // ---- rank decision (fstk_rank.cu; randls.cpp:112-123) ----
 // Streaming TSQR of a tall matrix with n1 columns, fed in row blocks of at
 // most bmax rows: after fold(), the leading n1 x n1 block of W (ld ldw) is

@@ -2615,6 +2615,16 @@ static void exact_solve(fstk_gpu_refit* rf, double* x_dev) {
   rf->rank_def = def;
 }
 
+// Session accessors for the single-process multi-device orchestrator
+// (fstk_multi.cu).
+extern "C++" {
+int refit_device(const fstk_gpu_refit* rf) { return rf->device; }
+int64_t refit_order(const fstk_gpu_refit* rf) { return rf->R; }
+bool refit_awaits_exchange(const fstk_gpu_refit* rf) { return rf->columns && !rf->exchanged; }
+int refit_gram_used(const fstk_gpu_refit* rf) { return rf->gram_used; }
+bool refit_is_factored(const fstk_gpu_refit* rf) { return rf->factored; }
+}  // extern "C++"
+
 // Re-raises a failed nested C-ABI stage with its full error record.
 static void rethrow_stage(int32_t c, const fstk_gpu_error* err) {
   if (!c) return;
@@ -3258,6 +3268,10 @@ int32_t fstk_gpu_reestimate_core(const fstk_gpu_model* m, const double* points,
                                  const double* values, int64_t q, int32_t d,
                                  const fstk_sketch_cfg* cfg, double* core_out,
                                  fstk_reestimate_info* info, fstk_gpu_error* err) {
+  // A model created after fstk_gpu_set_devices(n > 1) carries replicas: the
+  // refit then runs sharded over all of them in this process (fstk_multi.cu).
+  if (m && !m->replicas.empty())
+    return fstk_gpu::reestimate_core_multi(m, points, values, q, d, cfg, core_out, info, err);
   fstk_gpu_refit* rf = nullptr;
   fstk_reestimate_info local{};
   fstk_reestimate_info* inf = info ? info : &local;

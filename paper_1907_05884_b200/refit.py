@@ -44,9 +44,12 @@ def _info_dict(info: ReestimateInfo) -> dict:
             "padded_rows": int(info.padded_rows), "gram_slices": int(info.gram_slices),
             "refine_steps": int(info.refine_steps), "gram_int8_ops": float(info.gram_int8_ops),
             "qr_path": bool(info.qr_path), "sigma_ratio": float(info.sigma_ratio),
+            "devices": max(1, int(info.devices)),
+            "transport": {0: None, 1: "nccl", 2: "p2p"}.get(int(info.multi_transport)),
             "timings": {"prepare_s": info.t_prepare, "sketch_s": info.t_sketch,
                         "gram_s": info.t_gram, "solve_s": info.t_solve,
-                        "residual_s": info.t_residual, "alloc_s": info.t_alloc}}
+                        "residual_s": info.t_residual, "alloc_s": info.t_alloc,
+                        "exchange_s": info.t_exchange, "reduce_s": info.t_reduce}}
 
 
 def gram_slices(slices: int | None = None) -> int:
@@ -114,7 +117,9 @@ def cholesky(g, slices: int = 5, nb: int = 2048):
 def reestimate_core(model: Model, points, values, seed=0, sample_rows=0,
                     working_subset=1 << 20, transform="dct", validation_fraction=0.05,
                     device=None):
-    """randls.cpp:360-383 on one GPU.  Returns (new_model, info)."""
+    """randls.cpp:360-383.  Returns (new_model, info).  One GPU, or -- for a
+    model created after set_devices([...]) with several devices -- sharded
+    over all of them inside the library (fstk_multi.cu)."""
     require_gpu()
     p, v = _cloud(model, points, values)
     cfg = sketch_config(seed, sample_rows, working_subset, transform, validation_fraction)
