@@ -308,6 +308,12 @@ int32_t fstk_gpu_interpolate_to_grid_device(const double* points, const double* 
  * GEMMs (kept for comparison; $FSTK_GRAM_GEMM=cublaslt).  Both produce the
  * identical Gram bit for bit.  0 only queries.  Returns the previous setting. */
 int32_t fstk_gpu_gram_engine(int32_t engine);
+/* Measurement only (no reference counterpart): the tcgen05 int8 SYRK alone
+ * on device residue planes (nm planes of kp x np int8, column-major; kp a
+ * multiple of 128, np of 256), symmetric residues of the lower-triangle tile
+ * sums into c (nm planes of np x np bytes). */
+int32_t fstk_gpu_debug_syrk(const int8_t* planes, int32_t nm, int64_t kp, int64_t np, int8_t* c,
+                            int32_t device, void* stream, fstk_gpu_error* err);
 /* normal_equations() at an explicit Gram precision: slices 4..7 (sliced,
  * int8 tensor cores) or 0 (native fp64).  solve() and dist.refine_distributed
  * escalate with it: a sliced Gram that cannot precondition the system is

@@ -615,12 +615,15 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
     const char* e = std::getenv("FSTK_GRAM_BLOCK");
     return e ? std::max<int64_t>(256, std::atoll(e)) : int64_t(2048);
   }();
-  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * 4));
-  w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), 16), np);
-  if (w > block_cap && np > block_cap) w = round_up(block_cap, 16);
+  const int64_t wal = syrk ? 256 : 16;
+  int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * (syrk ? 1 : 4)));
+  w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), wal), np);
+  if (w > block_cap && np > block_cap) w = round_up(block_cap, wal);
   sc.X.ensure(static_cast<size_t>(nm) * kp * np);
-  if (syrk) {
+  if (syrk && syrk_fused()) {
     sc.C8.ensure(syrk_crt_scratch_bytes(nm, device));
+  } else if (syrk) {
+    sc.C8.ensure(static_cast<size_t>(nm) * np * w);
   } else {
     sc.C.ensure(static_cast<size_t>(nm) * np * w);
     sc.ws.ensure(size_t(32) << 20);
@@ -636,11 +639,28 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
     FSTK_CRT_SWITCH(nm, FSTK_CRT_RES)
 #undef FSTK_CRT_RES
     const int acc = (!first || beta != 0.0) ? 1 : 0;
-    if (syrk) {
+    if (syrk && syrk_fused()) {
       // One persistent tcgen05 launch: the whole lower triangle, every
       // modulus, Garner fold in the epilogue.
       ops += syrk_crt_fold(sc.X.p, nm, kp, np, n, k, sc.ex.p, gram, ldg, acc != 0, negate, sc.C8.p,
                            device, s);
+    } else if (syrk) {
+      for (int64_t c0 = 0; c0 < np; c0 += w) {
+        const int64_t wn = std::min(w, np - c0);
+        const int64_t m = np - c0;
+        int8_t* c8 = reinterpret_cast<int8_t*>(sc.C8.p);
+        static const bool per_mod = std::getenv("FSTK_SYRK_PERMOD") != nullptr;
+        if (per_mod) {  // experiment: one launch per modulus, like the library GEMMs
+          for (int t = 0; t < nm; ++t)
+            ops += syrk_i8_residues_one(sc.X.p, nm, t, kp, np, c0, wn, m, c8 + t * m * wn, device, s);
+        } else {
+          ops += syrk_i8_residues(sc.X.p, nm, kp, np, c0, wn, m, c8, m * wn, device, s);
+        }
+#define FSTK_CRT_FOLD(NMV) \
+  launch_crt_fold<NMV, int8_t>(c8, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
+        FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
+#undef FSTK_CRT_FOLD
+      }
     } else {
       LtState& st = lt_state(device);
       for (int64_t c0 = 0; c0 < np; c0 += w) {

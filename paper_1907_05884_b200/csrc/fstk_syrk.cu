@@ -36,8 +36,10 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "fstk_common.cuh"
@@ -57,9 +59,10 @@ constexpr int kEpiWarps = 8;   // two per TMEM lane quarter, 128 columns each
 constexpr int kThreads = 32 * (4 + kEpiWarps);
 constexpr int kStages = 7;
 constexpr int kAccCols = 256;                 // TMEM columns per accumulator
+constexpr int kTaskRing = 4;    // dynamic scheduler slots
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 
-constexpr int kBandTiles = 8;   // tile columns per band
+constexpr int kBandTilesDefault = 8;   // tile columns per band
 constexpr int kMaxBands = 64;
 
 struct SyrkParams {
@@ -67,6 +70,7 @@ struct SyrkParams {
   int np;               // columns per plane (rows of the tensor map per plane)
   int nt;               // tiles per side (np / 256)
   int nbands;
+  int band;             // tile columns per band
   int band_start[kMaxBands + 1];  // first task of each band
   int ntasks;
   int n;                // valid columns of G
@@ -77,6 +81,12 @@ struct SyrkParams {
   double* G;
   const int* ex;        // per-column exponents of this segment
   uint8_t* scratch;     // per CTA: NM x 128 x 256 residue bytes
+  int prefetch;         // K blocks of the next modulus prefetched into L2
+  int* counter;         // dynamic tile scheduler: next task (zeroed before the launch)
+  unsigned long long* dbg;  // optional wait-cycle counters ($FSTK_SYRK_DEBUG)
+  unsigned sleep_ns;    // suspend hint of the epilogue's waits (0 = spin)
+  unsigned pc_sleep;    // experiments: suspend hint of the producer / MMA waits
+  int skip;             // experiments: 1 = no scratch stores, 2 = no fold, 3 = neither
   int mod[kSyrkMaxModuli];
   unsigned p16[kSyrkMaxModuli];   // 2^16 mod m
   unsigned off[kSyrkMaxModuli];   // a multiple of m >= 2^22 (makes the folded value >= 0)
@@ -117,7 +127,7 @@ __device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
 // the phase completes (or ~0.5 ms pass) instead of spinning on try_wait -- the
 // epilogue warps wait ~100 us per tile and the kernel runs at the power cap,
 // where issue slots spent spinning cost clock speed.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns = 500000u) {
   uint32_t ok;
   do {
     asm volatile(
@@ -125,9 +135,29 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(500000u)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
         : "memory");
   } while (!ok);
+}
+// Cluster-scope acquire wait (task slots written by the peer CTA) and remote
+// release-arrive on an mbarrier given by its shared::cluster address.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void st_cluster_s32(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -168,6 +198,12 @@ __device__ __forceinline__ void tma_load_2sm_hint(void* dst, const CUtensorMap* 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y)
+               : "memory");
+}
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -205,8 +241,8 @@ __device__ __forceinline__ void decode_task(const SyrkParams& p, int task, int& 
   int b = 0;
   while (b + 1 < p.nbands && p.band_start[b + 1] <= task) ++b;
   int r = task - p.band_start[b];
-  const int c0 = b * kBandTiles;
-  const int wb = min(kBandTiles, p.nt - c0);
+  const int c0 = b * p.band;
+  const int wb = min(p.band, p.nt - c0);
   const int tri = wb * (wb + 1) / 2;
   if (r < tri) {
     int a = 0;
@@ -234,13 +270,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // Dynamic tile scheduler: the leader's producer claims tasks with one
+  // atomic per task and publishes them through a ring of slots in both CTAs,
+  // so the concurrently active tiles stay a contiguous window of the banded
+  // order however the pairs' speeds drift (static round-robin let them
+  // spread and tripled the panel re-reads from DRAM).
+  uint64_t* task_full = tempty + 2;          // per slot, both CTAs: count 1
+  uint64_t* task_empty = task_full + kTaskRing;  // per slot, leader: 1 + 2 kEpiWarps + 1
+  int* task_slot = reinterpret_cast<int*>(task_empty + kTaskRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(task_slot + kTaskRing);
 
   const uint32_t rank = cluster_rank();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
@@ -252,6 +294,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps x 2 CTAs
+    }
+    for (int r = 0; r < kTaskRing; ++r) {
+      mbar_init(&task_full[r], 1);
+      mbar_init(&task_empty[r], 2 + 2 * kEpiWarps);  // MMA + peer producer + epilogue warps
     }
     fence_mbar_init();
   }
@@ -274,7 +320,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint64_t policy = 0;
       if (p.hint == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
       if (p.hint == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      for (int task = pair; task < p.ntasks; task += npairs) {
+      const uint32_t peer_slot0 = map_rank(&task_slot[0], 1);
+      const uint32_t peer_full0 = map_rank(&task_full[0], 1);
+      const uint32_t lead_empty0 = map_rank(&task_empty[0], 0);
+      for (int n = 0;; ++n) {
+        const int r = n % kTaskRing;
+        const uint32_t rph = (n / kTaskRing) & 1;
+        int task;
+        if (rank == 0) {
+          mbar_wait(&task_empty[r], rph ^ 1);
+          task = atomicAdd(p.counter, 1);
+          if (task >= p.ntasks) task = -1;
+          task_slot[r] = task;
+          st_cluster_s32(peer_slot0 + 4 * r, task);
+          mbar_arrive(&task_full[r]);
+          mbar_arrive_remote(peer_full0 + 8 * r);
+        } else {
+          mbar_wait_cluster(&task_full[r], rph);
+          task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+          mbar_arrive_remote(lead_empty0 + 8 * r);
+        }
+        if (task < 0) break;
         int ti, tj;
         decode_task(p, task, ti, tj);
         for (int t = 0; t < NM; ++t) {
@@ -282,7 +348,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int rowA = base + ti * kTile;
           const int rowB = base + tj * kTile;
           for (int kb = 0; kb < p.kblocks; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
+            // Near the end of modulus t, pull the first K blocks of modulus
+            // t + 1's panels into L2 (a cold plane at every switch).
+            if (p.prefetch && t + 1 < NM && kb >= p.kblocks - p.prefetch) {
+              const int pk = kb - (p.kblocks - p.prefetch);
+              tma_prefetch_l2(&map, pk * kKB, rowA + p.np);
+              tma_prefetch_l2(&map, pk * kKB, rowB + p.np);
+            }
+            if (p.pc_sleep) mbar_wait_sleep(&empty[stage], phase ^ 1, p.pc_sleep); else mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * kStageBytes;
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
             const uint32_t bar = map_rank(&full[stage], 0);
@@ -305,13 +378,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (rank == 0 && lane == 0) {
       // ---- MMA issuer (leader CTA, one thread).
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
-      for (int task = pair; task < p.ntasks; task += npairs) {
+      unsigned long long w_empty = 0, w_full = 0, t_begin = clock64();
+      for (int n = 0;; ++n) {
+        const int r = n % kTaskRing;
+        mbar_wait(&task_full[r], (n / kTaskRing) & 1);
+        const int task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+        mbar_arrive(&task_empty[r]);
+        if (task < 0) break;
         for (int t = 0; t < NM; ++t) {
-          mbar_wait(&tempty[acc], aphase ^ 1);
+          unsigned long long c0 = p.dbg ? clock64() : 0;
+          if (p.pc_sleep) mbar_wait_sleep(&tempty[acc], aphase ^ 1, p.pc_sleep); else mbar_wait(&tempty[acc], aphase ^ 1);
+          if (p.dbg) w_empty += clock64() - c0;
           tc_fence_after();
           const uint32_t d = tmem + acc * kAccCols;
           for (int kb = 0; kb < p.kblocks; ++kb) {
-            mbar_wait(&full[stage], phase);
+            if (p.dbg) c0 = clock64();
+            if (p.pc_sleep) mbar_wait_sleep(&full[stage], phase, p.pc_sleep); else mbar_wait(&full[stage], phase);
+            if (p.dbg) w_full += clock64() - c0;
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * kStageBytes);
             const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kPanelBytes);
@@ -329,6 +412,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (acc == 0) aphase ^= 1;
         }
       }
+      if (p.dbg) {
+        atomicAdd(p.dbg + 0, w_empty);
+        atomicAdd(p.dbg + 1, w_full);
+        atomicAdd(p.dbg + 2, clock64() - t_begin);
+      }
     }
   } else if (warp >= 4) {
     // ---- Epilogue (both CTAs): warp w reads TMEM lanes 32 (w % 4) .. +31
@@ -342,14 +430,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* srow = p.scratch + static_cast<size_t>(blockIdx.x) * NM * kHalf * kTile +
                     static_cast<size_t>(row) * kTile + half * (kTile / 2);
     uint32_t acc = 0, aphase = 0;
-    for (int task = pair; task < p.ntasks; task += npairs) {
+    const uint32_t lead_empty0 = map_rank(&task_empty[0], 0);
+    for (int n = 0;; ++n) {
+      const int r = n % kTaskRing;
+      int task = 0;
+      if (lane == 0) {
+        mbar_wait_cluster(&task_full[r], (n / kTaskRing) & 1);
+        task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+        mbar_arrive_remote(lead_empty0 + 8 * r);
+      }
+      task = __shfl_sync(0xffffffffu, task, 0);
+      if (task < 0) break;
       int ti, tj;
       decode_task(p, task, ti, tj);
 #pragma unroll 1
       for (int t = 0; t < NM; ++t) {
         const int mt = p.mod[t];
         const unsigned p16 = p.p16[t], off = p.off[t], magic = p.magic[t];
-        mbar_wait_sleep(&tfull[acc], aphase);
+        if (p.sleep_ns)
+          mbar_wait_sleep(&tfull[acc], aphase, p.sleep_ns);
+        else
+          mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
         const uint32_t tbase =
             tmem + acc * kAccCols + half * (kAccCols / 2) + (static_cast<uint32_t>(q * 32) << 16);
@@ -370,8 +471,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             w[u] = x;
           }
           uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
-          __stcg(d4, make_uint4(w[0], w[1], w[2], w[3]));
-          __stcg(d4 + 1, make_uint4(w[4], w[5], w[6], w[7]));
+          if (!(p.skip & 1)) {
+            __stcg(d4, make_uint4(w[0], w[1], w[2], w[3]));
+            __stcg(d4 + 1, make_uint4(w[4], w[5], w[6], w[7]));
+          } else if (w[0] == 0x12345678u) {
+            p.G[0] = 1.0;  // keep the residue arithmetic live
+          }
         }
         // The accumulator is free as soon as its residues are out.
         tc_fence_before();
@@ -386,6 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       // Fold the tile's NM residues of every entry of this thread's 128
       // columns into G while the MMAs of the next tile run.
+      if (p.skip & 2) continue;
       const int gi = ti * kTile + static_cast<int>(rank) * kHalf + row;
       const int ei = gi < p.n ? __ldg(p.ex + gi) : 0;
       const int gjb = tj * kTile + half * (kTile / 2);
@@ -432,6 +538,162 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                  : "memory");
 }
 
+// ---- Unfused variant (FSTK_SYRK_FUSED=0): one launch per column block
+// [c0, c0 + wn) of the lower triangle, task = (modulus, tile) with the
+// modulus outermost (the library GEMMs' order), symmetric residues stored
+// as bytes into C (column-major, ld m, plane stride cstride); the Garner
+// fold then runs as crt_fold_kernel<NM, int8_t> (fstk_gram.cu).
+struct ResParams {
+  int nm, kblocks, np, c0, ntj, nti, tri, per_mod, ntasks;
+  int plane0;           // first plane (modulus) of this launch
+  int hint_a, hint_b;   // L2 policy of the A / B panel loads: 0 none, 1 evict_last, 2 evict_first, 3 evict_normal
+  long long ldc, cstride;
+  int8_t* C;
+  unsigned pc_sleep;
+  int mod[kSyrkMaxModuli];
+  unsigned p16[kSyrkMaxModuli], off[kSyrkMaxModuli], magic[kSyrkMaxModuli];
+};
+
+__device__ __forceinline__ void decode_res(const ResParams& p, int task, int& t, int& ti, int& tj) {
+  t = task / p.per_mod;
+  int r = task - t * p.per_mod;
+  if (r < p.tri) {
+    ti = 0;
+    while ((ti + 1) * (ti + 2) / 2 <= r) ++ti;
+    tj = r - ti * (ti + 1) / 2;
+  } else {
+    r -= p.tri;
+    ti = p.ntj + r / p.ntj;
+    tj = r - (ti - p.ntj) * p.ntj;
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    syrk_res_kernel(const __grid_constant__ CUtensorMap map, const ResParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t rank = cluster_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (warp == 0 && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * kAccCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      uint64_t pol[4] = {0, 0, 0, 0};
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol[1]));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol[2]));
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol[3]));
+      for (int task = pair; task < p.ntasks; task += npairs) {
+        int t, ti, tj;
+        decode_res(p, task, t, ti, tj);
+        const int base = (p.plane0 + t) * p.np + p.c0 + static_cast<int>(rank) * kHalf;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          if (p.pc_sleep) mbar_wait_sleep(&empty[stage], phase ^ 1, p.pc_sleep); else mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          const uint32_t bar = map_rank(&full[stage], 0);
+          if (p.hint_a) tma_load_2sm_hint(sa, &map, kb * kKB, base + ti * kTile, bar, pol[p.hint_a]);
+          else tma_load_2sm(sa, &map, kb * kKB, base + ti * kTile, bar);
+          if (p.hint_b) tma_load_2sm_hint(sa + kPanelBytes, &map, kb * kKB, base + tj * kTile, bar, pol[p.hint_b]);
+          else tma_load_2sm(sa + kPanelBytes, &map, kb * kKB, base + tj * kTile, bar);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
+      for (int task = pair; task < p.ntasks; task += npairs) {
+        if (p.pc_sleep) mbar_wait_sleep(&tempty[acc], aphase ^ 1, p.pc_sleep); else mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * kAccCols;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          if (p.pc_sleep) mbar_wait_sleep(&full[stage], phase, p.pc_sleep); else mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+          const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kPanelBytes);
+#pragma unroll
+          for (int k = 0; k < kKB / 32; ++k) mma_i8(d, da + 2 * k, db + 2 * k, (kb | k) != 0 ? 1u : 0u);
+          mma_commit_pair(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t te0 = map_rank(&tempty[0], 0), te1 = map_rank(&tempty[1], 0);
+    uint32_t acc = 0, aphase = 0;
+    for (int task = pair; task < p.ntasks; task += npairs) {
+      int t, ti, tj;
+      decode_res(p, task, t, ti, tj);
+      const int mt = p.mod[t];
+      const unsigned p16 = p.p16[t], off = p.off[t], magic = p.magic[t];
+      const long long i = static_cast<long long>(ti) * kTile + rank * kHalf + q * 32 + lane;
+      int8_t* crow = p.C + t * p.cstride + i + static_cast<long long>(tj) * kTile * p.ldc;
+      mbar_wait_sleep(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+      for (int ch = 0; ch < kAccCols / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tbase + ch * 32, v);
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          crow[static_cast<long long>(ch * 32 + c) * p.ldc] =
+              static_cast<int8_t>(sym_residue(static_cast<int>(v[c]), mt, p16, off, magic));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc ? te1 : te0) : "memory");
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kAccCols) : "memory");
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -473,8 +735,86 @@ void launch_syrk(const CUtensorMap& map, const SyrkParams& p, int pairs, int dev
 
 }  // namespace
 
+bool syrk_fused() {
+  static const bool fused = [] {
+    const char* e = std::getenv("FSTK_SYRK_FUSED");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return fused;
+}
+
+static double syrk_res_launch(const int8_t* planes, int nm, int t0, int cnt, int64_t kp, int64_t np, int64_t c0,
+                              int64_t wn, int64_t m, int8_t* C, int64_t cstride, int device, cudaStream_t s);
+double syrk_i8_residues(const int8_t* planes, int nm, int64_t kp, int64_t np, int64_t c0, int64_t wn,
+                        int64_t m, int8_t* C, int64_t cstride, int device, cudaStream_t s) {
+  return syrk_res_launch(planes, nm, 0, nm, kp, np, c0, wn, m, C, cstride, device, s);
+}
+double syrk_i8_residues_one(const int8_t* planes, int nm, int t, int64_t kp, int64_t np, int64_t c0, int64_t wn,
+                            int64_t m, int8_t* C, int device, cudaStream_t s) {
+  return syrk_res_launch(planes, nm, t, 1, kp, np, c0, wn, m, C, 0, device, s);
+}
+static double syrk_res_launch(const int8_t* planes, int nm, int t0, int cnt, int64_t kp, int64_t np, int64_t c0,
+                              int64_t wn, int64_t m, int8_t* C, int64_t cstride, int device, cudaStream_t s) {
+  require(nm >= 1 && nm <= kSyrkMaxModuli, FSTK_E_COMPUTE, "internal: SYRK modulus count");
+  require(kp % kKB == 0 && kp > 0 && kp <= 66560, FSTK_E_COMPUTE, "internal: SYRK segment rows");
+  require(np % kTile == 0 && c0 % kTile == 0 && wn % kTile == 0 && m % kTile == 0 && c0 + m == np,
+          FSTK_E_COMPUTE, "internal: SYRK block shape");
+  static std::atomic<uint64_t> attr_set{0};
+  const uint64_t bit = uint64_t(1) << (device & 63);
+  if (!(attr_set.load() & bit)) {
+    cudaFuncSetAttribute(syrk_res_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr_set.fetch_or(bit);
+  }
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(kp), static_cast<cuuint64_t>(nm * np)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(kp)};
+  const cuuint32_t box[2] = {kKB, kHalf};
+  const cuuint32_t estr[2] = {1, 1};
+  int promo = 2;
+  ResParams p{};
+  p.nm = cnt;
+  p.kblocks = static_cast<int>(kp / kKB);
+  p.np = static_cast<int>(np);
+  p.c0 = static_cast<int>(c0);
+  p.ntj = static_cast<int>(wn / kTile);
+  p.nti = static_cast<int>(m / kTile);
+  p.tri = p.ntj * (p.ntj + 1) / 2;
+  p.per_mod = p.tri + (p.nti - p.ntj) * p.ntj;
+  p.ntasks = cnt * p.per_mod;
+  p.ldc = m;
+  p.cstride = cstride;
+  p.C = C;
+  p.plane0 = t0;
+  const char* e = std::getenv("FSTK_SYRK_PC_SLEEP");
+  p.pc_sleep = e ? static_cast<unsigned>(std::atoi(e)) : 200000u;
+  const char* hh = std::getenv("FSTK_SYRK_HINTS");
+  if (hh && std::strlen(hh) >= 3) {
+    p.hint_a = hh[0] - '0';
+    p.hint_b = hh[2] - '0';
+  }
+  const char* pr = std::getenv("FSTK_SYRK_PROMO");
+  promo = pr ? std::atoi(pr) : 2;
+  for (int t = 0; t < cnt; ++t) {
+    const unsigned mm = static_cast<unsigned>(kmod(t0 + t));
+    p.mod[t] = kmod(t0 + t);
+    p.p16[t] = 65536u % mm;
+    p.off[t] = ((1u << 22) / mm + 1u) * mm;
+    p.magic[t] = static_cast<unsigned>((uint64_t(1) << 32) / mm);
+  }
+  const CUtensorMapL2promotion promos[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+  if (tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(planes), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promos[promo & 3],
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    fail(FSTK_E_COMPUTE, "cuTensorMapEncodeTiled failed for the SYRK planes");
+  const int pairs = std::max(1, std::min(p.ntasks, sm_count(device) / 2));
+  syrk_res_kernel<<<2 * pairs, 256, kSmemBytes, s>>>(map, p);
+  check_launch("syrk_res_kernel");
+  return 2.0 * static_cast<double>(p.ntasks) * kTile * kTile * static_cast<double>(kp);
+}
+
 size_t syrk_crt_scratch_bytes(int nm, int device) {
-  return static_cast<size_t>(sm_count(device)) * nm * kHalf * kTile;
+  return static_cast<size_t>(sm_count(device)) * nm * kHalf * kTile + 256;  // + the task counter
 }
 
 double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n, int k, const int* ex,
@@ -486,8 +826,12 @@ double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n
   require(static_cast<int64_t>(nm) * np < (int64_t(1) << 31), FSTK_E_COMPUTE,
           "internal: SYRK plane rows exceed the tensor-map range");
   const int nt = static_cast<int>(np / kTile);
-  const int nbands = (nt + kBandTiles - 1) / kBandTiles;
-  require(nbands <= kMaxBands, FSTK_E_COMPUTE, "internal: SYRK Gram too wide (> 131072 columns)");
+  static const int band = [] {
+    const char* e = std::getenv("FSTK_SYRK_BAND");
+    return e ? std::max(1, std::atoi(e)) : kBandTilesDefault;
+  }();
+  const int nbands = (nt + band - 1) / band;
+  require(nbands <= kMaxBands && band <= 64, FSTK_E_COMPUTE, "internal: SYRK Gram too wide (> 131072 columns)");
   CUtensorMap map;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(kp), static_cast<cuuint64_t>(nm * np)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(kp)};
@@ -503,11 +847,12 @@ double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n
   p.np = static_cast<int>(np);
   p.nt = nt;
   p.nbands = nbands;
+  p.band = band;
   int task = 0;
   for (int b = 0; b < nbands; ++b) {
     p.band_start[b] = task;
-    const int wb = std::min(kBandTiles, nt - b * kBandTiles);
-    task += wb * (wb + 1) / 2 + (nt - b * kBandTiles - wb) * wb;
+    const int wb = std::min(band, nt - b * band);
+    task += wb * (wb + 1) / 2 + (nt - b * band - wb) * wb;
   }
   p.band_start[nbands] = task;
   p.ntasks = task;
@@ -524,12 +869,41 @@ double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n
   p.G = G;
   p.ex = ex;
   p.scratch = scratch;
+  static const int prefetch = [] {
+    const char* e = std::getenv("FSTK_SYRK_PREFETCH");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.prefetch = std::min(prefetch, static_cast<int>(kp / kKB));
+  p.counter = reinterpret_cast<int*>(scratch + static_cast<size_t>(sm_count(device)) * nm * kHalf * kTile);
+  FSTK_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(int), s));
   for (int t = 0; t < nm; ++t) {
     const unsigned m = static_cast<unsigned>(kmod(t));
     p.mod[t] = kmod(t);
     p.p16[t] = 65536u % m;
     p.off[t] = ((1u << 22) / m + 1u) * m;
     p.magic[t] = static_cast<unsigned>((uint64_t(1) << 32) / m);
+  }
+  static const bool debug = std::getenv("FSTK_SYRK_DEBUG") != nullptr;
+  static const unsigned sleep_ns = [] {
+    const char* e = std::getenv("FSTK_SYRK_SLEEP_NS");
+    return e ? static_cast<unsigned>(std::atoi(e)) : 500000u;
+  }();
+  p.sleep_ns = sleep_ns;
+  static const int skip = [] {
+    const char* e = std::getenv("FSTK_SYRK_SKIP");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.skip = skip;
+  static const unsigned pc_sleep = [] {
+    const char* e = std::getenv("FSTK_SYRK_PC_SLEEP");
+    return e ? static_cast<unsigned>(std::atoi(e)) : 200000u;
+  }();
+  p.pc_sleep = pc_sleep;
+  DevBuf<unsigned long long> dbg;
+  if (debug) {
+    dbg.alloc(4);
+    FSTK_CUDA(cudaMemsetAsync(dbg.p, 0, 32, s));
+    p.dbg = dbg.p;
   }
   const int pairs = std::max(1, std::min(p.ntasks, sm_count(device) / 2));
   switch (nm) {
@@ -545,7 +919,26 @@ double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n
     case 17: launch_syrk<17>(map, p, pairs, device, s); break;
     default: fail(FSTK_E_COMPUTE, "internal: unsupported CRT modulus count");
   }
+  if (debug) {
+    unsigned long long h[4];
+    FSTK_CUDA(cudaMemcpyAsync(h, dbg.p, 32, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "syrk: MMA thread cycles total %.3g, waiting tempty %.1f%%, waiting full %.1f%%\n",
+                 double(h[2]), 100.0 * h[0] / double(h[2]), 100.0 * h[1] / double(h[2]));
+  }
   return 2.0 * static_cast<double>(p.ntasks) * nm * kTile * kTile * static_cast<double>(kp);
 }
 
 }  // namespace fstk_gpu
+
+// Measurement entry (no reference counterpart): the unfused tcgen05 SYRK
+// alone on device planes (nm planes of kp x np int8), whole lower triangle
+// into C (np x np x nm bytes).
+extern "C" int32_t fstk_gpu_debug_syrk(const int8_t* planes, int32_t nm, int64_t kp, int64_t np, int8_t* c,
+                                       int32_t device, void* stream, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    DeviceGuard dg(device);
+    syrk_i8_residues(planes, nm, kp, np, 0, np, np, c, np * np, device, static_cast<cudaStream_t>(stream));
+  });
+}

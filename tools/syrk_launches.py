@@ -3,6 +3,8 @@ run, CUPTI via torch.profiler) against the tasks each launch holds, to read
 tail losses; samples SM clocks while it runs.
 usage: python tools/syrk_launches.py [slices] [rows] [n]"""
 import ctypes as C
+
+import numpy as np
 import os
 import subprocess
 import sys
@@ -37,10 +39,10 @@ stop = False
 
 def sample():
     while not stop:
-        o = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits"],
-                           capture_output=True, text=True).stdout.strip()
+        o = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,clocks_throttle_reasons.active",
+                            "--format=csv,noheader,nounits"], capture_output=True, text=True).stdout.strip()
         clk.append(o)
-        time.sleep(0.05)
+        time.sleep(0.02)
 
 
 th = threading.Thread(target=sample)
@@ -59,4 +61,8 @@ grp = 9 if F.gram_engine() == "cublaslt" else 1  # one launch per modulus vs all
 blocks = [sum(d[i:i + grp]) for i in range(0, len(d), grp)]
 per = len(blocks) // max(1, rows // 32768)
 print("  per column block (first segment):", " ".join(f"{b:.2f}" for b in blocks[:per]))
-print("clock/power samples:", clk[:60:3])
+busy = [c for c in clk if not c.startswith("1965")]
+mhz = [float(c.split(",")[0]) for c in busy]
+pw = [float(c.split(",")[1]) for c in busy]
+print(f"busy samples {len(busy)}: median SM clock {np.median(mhz) if mhz else 0:.0f} MHz, "
+      f"median power {np.median(pw) if pw else 0:.0f} W, reasons {sorted(set(c.split(',')[2].strip() for c in busy))}")
