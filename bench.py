@@ -567,6 +567,28 @@ def main():
         # The refit is ONE problem: every rank passes the same (rank-0) cloud.
         rpts, rvals = (pts, vals) if rank == 0 else dataset(args.config, args.points, 0)
         line["refit"] = run_refit(model, rpts, rvals, cfgd, args, rank, world, dev, peak_mma)
+        if NF > 1 and rank == 0 and world == 1:
+            # C5 (BASELINE configs[4]): 8 independent refits with M = 8R each,
+            # one per field, on the shared points (each field's values = its
+            # model at the points + the config's noise).
+            import paper_1907_05884_b200 as F
+
+            per, res = [], []
+            R = int(np.prod(model.ranks))
+            for f, m in enumerate(models):
+                fv = rvals if f == 0 else m.evaluate_batch(rpts) + 1e-2 * np.random.default_rng(
+                    500 + f).normal(size=rpts.shape[0])
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _, finfo = F.reestimate_core(m, rpts, fv, seed=0, sample_rows=cfgd["m_factor"] * R)
+                torch.cuda.synchronize()
+                per.append(round(time.perf_counter() - t0, 4))
+                res.append(round(finfo["residual_after"], 6))
+            line["refit_fields"] = {"fields": NF, "seconds_total": round(sum(per), 4),
+                                    "seconds_per_field": per, "residual_after": res,
+                                    "sample_rows": cfgd["m_factor"] * R,
+                                    "note": "BASELINE C5's 8 independent refits (M = 8R each), "
+                                            "sequential on one GPU through reestimate_core"}
         if args.transform != "none" and not args.no_refit_none:
             # The north star's literal estimator (sampled Kronecker rows, no
             # mixing; A never materialised), measured beside the reference's.

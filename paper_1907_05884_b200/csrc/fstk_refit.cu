@@ -2483,6 +2483,15 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
       info->gram_slices = rf->gram_used;
       info->gram_int8_ops = i8ops;
     }
+    // The residue planes and the SYRK scratch (up to 24 GB) are not needed
+    // by the solve: return them before the Cholesky allocates its own (an
+    // escalation re-forms the Gram from scratch anyway).  The digit scheme
+    // keeps its planes for the progressive upgrade.
+    if (gram_scheme_crt()) {
+      rf->gs.X.release();
+      rf->gs.C.release();
+      rf->gs.C8.release();
+    }
   }
 }
 
