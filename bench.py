@@ -714,9 +714,11 @@ def run_refit(model, pts, vals, cfgd, args, rank, world, dev, peak, transform=No
         t_n = time.perf_counter() - tn
         t_ar = 0.0
         if world > 1:
+            from paper_1907_05884_b200.dist import reduce_normal_equations
+
+            # ONE all-reduce of the packed lower triangle + rhs.
             ta = time.perf_counter()
-            torch.distributed.all_reduce(gram)
-            torch.distributed.all_reduce(rhs)
+            reduce_normal_equations(gram, rhs)
             torch.cuda.synchronize()
             t_ar = time.perf_counter() - ta
         t_hot = time.perf_counter() - t0

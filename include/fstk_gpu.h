@@ -308,6 +308,13 @@ int32_t fstk_gpu_interpolate_to_grid_device(const double* points, const double* 
  * GEMMs (kept for comparison; $FSTK_GRAM_GEMM=cublaslt).  Both produce the
  * identical Gram bit for bit.  0 only queries.  Returns the previous setting. */
 int32_t fstk_gpu_gram_engine(int32_t engine);
+/* Packed normal equations (device pointers): unpack = 0 writes the lower
+ * triangle of gram (n x n, column-major) column by column followed by rhs
+ * into packed (n(n+1)/2 + n doubles); unpack != 0 restores gram's lower
+ * triangle and rhs from packed.  The reduction payload of a row-sharded
+ * refit (4.3 GB at R = 32,768 instead of the 8.6 GB square). */
+int32_t fstk_gpu_pack_normal_equations(const double* gram, const double* rhs, int64_t n, double* packed,
+                                       int32_t unpack, void* stream, fstk_gpu_error* err);
 /* Measurement only (no reference counterpart): the tcgen05 int8 SYRK alone
  * on device residue planes (nm planes of kp x np int8, column-major; kp a
  * multiple of 128, np of 256), symmetric residues of the lower-triangle tile

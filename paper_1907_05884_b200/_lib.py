@@ -102,6 +102,7 @@ EXPORTS = [
     "fstk_gpu_refit_qr_solve", "fstk_gpu_qr_stack", "fstk_gpu_solve_system",
     "fstk_gpu_refit_sketched_columns", "fstk_gpu_eval_serialize",
     "fstk_gpu_interpolate_to_grid", "fstk_gpu_interpolate_to_grid_device", "fstk_gpu_debug_syrk",
+    "fstk_gpu_pack_normal_equations",
 ]
 PROF_KINDS = ["mode_tables", "contract", "transform", "gram", "solve"]
 
@@ -158,6 +159,7 @@ def lib():
     L.fstk_gpu_gram_slices.restype = C.c_int32
     L.fstk_gpu_gram_engine.argtypes = [C.c_int32]
     L.fstk_gpu_gram_engine.restype = C.c_int32
+    L.fstk_gpu_pack_normal_equations.argtypes = [VP, VP, C.c_int64, VP, C.c_int32, VP, C.POINTER(Err)]
     L.fstk_gpu_debug_syrk.argtypes = [VP, C.c_int32, C.c_int64, C.c_int64, VP, C.c_int32, VP, C.POINTER(Err)]
     L.fstk_gpu_refit_begin_columns.argtypes = [VP, DP, DP, C.c_int64, C.c_int32,
                                                C.POINTER(SketchCfg), C.c_int32, C.c_int32,

@@ -488,3 +488,23 @@ int32_t reestimate_core_multi(const fstk_gpu_model* m, const double* points, con
 }
 
 }  // namespace fstk_gpu
+
+// Packed normal equations for callers that reduce them themselves (the
+// one-process-per-GPU torch.distributed path, dist.py): the lower triangle of
+// G (n x n, column-major) and rhs (n) into R(R+1)/2 + R values, and back.
+extern "C" int32_t fstk_gpu_pack_normal_equations(const double* gram, const double* rhs, int64_t n, double* packed,
+                                                  int32_t unpack, void* stream, fstk_gpu_error* err) {
+  using namespace fstk_gpu;
+  return guarded(err, [&] {
+    require(gram && rhs && packed && n > 0, FSTK_E_PARAMETER, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t tri = n * (n + 1) / 2;
+    if (unpack) {
+      unpack_lower(packed, n, const_cast<double*>(gram), s);
+      FSTK_CUDA(cudaMemcpyAsync(const_cast<double*>(rhs), packed + tri, n * 8, cudaMemcpyDeviceToDevice, s));
+    } else {
+      pack_lower(gram, n, packed, s);
+      FSTK_CUDA(cudaMemcpyAsync(packed + tri, rhs, n * 8, cudaMemcpyDeviceToDevice, s));
+    }
+  });
+}
