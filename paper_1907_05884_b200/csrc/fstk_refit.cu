@@ -308,6 +308,7 @@ struct PassParams {
   int compact;              // last pass: destination rows consecutive per CTA
   int list_off;             // byte offset of the per-CTA sampled-element list
   int ct_rounds;            // L == 10: compile-time stage rounds (radix_round_ct)
+  int fuse_last;            // compact complex last pass: stage 9 evaluated in the store
   int swap;                 // staging in x's layout, alternating with x (see kernel)
   // warp_pass2_kernel (last pass of q_pad = 2^20): per-position-class twiddle
   // rows and the sampled elements of each class in destination-row order.
@@ -705,6 +706,10 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
     prefetch(cc + gridDim.y, cur ^ 1);  // staging is free: this column now lives in x
     cur ^= 1;
     // ---- stages, three per register round
+    // The compact last pass of a complex transform folds the tenth stage into
+    // its store: only the sampled outputs (~S / q_pad of them) evaluate their
+    // butterfly, saving a full shared-memory round trip of the tile.
+    const bool fuse_last = !REAL && use_list && L == 10 && P.ct_rounds && P.fuse_last;
     if (L == 10 && P.ct_rounds) {
       constexpr int NE = 1024 * G;
       radix_round_ct<REAL, 3, G, 0, NE>(x, tws);
@@ -713,8 +718,10 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
       __syncthreads();
       radix_round_ct<REAL, 3, G, 6, NE>(x, tws);
       __syncthreads();
-      radix_round_ct<REAL, 1, G, 9, NE>(x, tws);
-      __syncthreads();
+      if (!fuse_last) {
+        radix_round_ct<REAL, 1, G, 9, NE>(x, tws);
+        __syncthreads();
+      }
     } else
     for (int j = 0; j < L; j += 3) {
       const int ns = min(3, L - j);
@@ -737,7 +744,20 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
         if constexpr (REAL) {
           *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(x[spad(e)], P.inv_sqrt_n));
         } else if (P.kind == FSTK_TRANSFORM_DCT) {
-          const double2 V = x[spad(e)];
+          double2 V;
+          if (fuse_last) {
+            // Stage 9 of the pass (radix_round_ct<..., 1, G, 9, ...>): the
+            // class-local index i pairs with i ^ 512; lower u + w y, upper
+            // u - w y, w = tws[(2^9 - 1) G + (i mod 512) G + c] -- the same
+            // separately rounded operations.
+            const int c = e % G, i = e / G, il = i & 511;
+            const double2 u = x[spad(il * G + c)];
+            const double2 t2 = cmul_x(x[spad((il + 512) * G + c)], tws[(511 + il) * G + c]);
+            V = i < 512 ? make_double2(xadd(u.x, t2.x), xadd(u.y, t2.y))
+                        : make_double2(xsub(u.x, t2.x), xsub(u.y, t2.y));
+          } else {
+            V = x[spad(e)];
+          }
           const bool k0 = idx == static_cast<int>(threadIdx.x), k1 = idx == static_cast<int>(threadIdx.x + blockDim.x);
           const double re = k0 ? cre0 : (k1 ? cre1 : __ldg(P.post_re + sl));
           const double im = k0 ? cim0 : (k1 ? cim1 : __ldg(P.post_im + sl));
@@ -746,7 +766,16 @@ __global__ void __launch_bounds__(256, G == 2 ? 2 : 3) transform_pass2_kernel(co
           const bool pos0 = base + (e % G) + static_cast<int64_t>(e / G) * stride == 0;
           *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(pos0 ? P.post_c0 : P.post_ck, val));
         } else {
-          const double2 V = x[spad(e)];
+          double2 V;
+          if (fuse_last) {
+            const int c = e % G, i = e / G, il = i & 511;
+            const double2 u = x[spad(il * G + c)];
+            const double2 t2 = cmul_x(x[spad((il + 512) * G + c)], tws[(511 + il) * G + c]);
+            V = i < 512 ? make_double2(xadd(u.x, t2.x), xadd(u.y, t2.y))
+                        : make_double2(xsub(u.x, t2.x), xsub(u.y, t2.y));
+          } else {
+            V = x[spad(e)];
+          }
           *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
           *store_ptr(P, col, sl, true) = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
         }
@@ -1368,6 +1397,11 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
         return (e && std::atoi(e) == 0) ? 0 : 1;
       }();
       P.ct_rounds = ct_on;
+      static const int fuse_on = [] {
+        const char* e = std::getenv("FSTK_SKETCH_FUSE_LAST");
+        return (e && std::atoi(e) == 0) ? 0 : 1;
+      }();
+      P.fuse_last = fuse_on;
       smem = round_up(static_cast<int64_t>(smem), 16);
       P.list_off = static_cast<int>(smem);
       if (P.compact) smem += static_cast<size_t>(E * P.G) * sizeof(uint16_t);
