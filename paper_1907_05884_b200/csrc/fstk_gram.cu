@@ -582,7 +582,9 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
     const char* e = std::getenv("FSTK_SYRK_MIN_ROWS");
     return e ? std::atoll(e) : int64_t(8192);
   }();
-  const bool syrk = gram_engine() == 1 && rows >= syrk_min_rows;
+  // (The SYRK's band table covers up to 131,072 columns; wider Grams keep the
+  // library engine.)
+  const bool syrk = gram_engine() == 1 && rows >= syrk_min_rows && n <= 131072;
   const int64_t np = round_up(static_cast<int64_t>(n), syrk ? 256 : 16);
   const int64_t kalign = syrk ? 128 : 16;
   static const int64_t seg_cap = [] {

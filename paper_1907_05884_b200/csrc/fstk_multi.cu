@@ -265,7 +265,13 @@ std::unique_ptr<Transport> make_transport(const std::vector<int>& devs) {
   std::sort(sorted.begin(), sorted.end());
   const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
   if (!force_p2p && distinct) {
-    if (Nccl* n = Nccl::load()) return std::make_unique<NcclTransport>(n, devs);
+    if (Nccl* n = Nccl::load()) {
+      try {
+        return std::make_unique<NcclTransport>(n, devs);
+      } catch (const Error&) {
+        // NCCL present but unusable here (e.g. no P2P topology): peer copies.
+      }
+    }
   }
   return std::make_unique<P2PTransport>(devs);
 }

@@ -81,7 +81,7 @@ struct SyrkParams {
   double* G;
   const int* ex;        // per-column exponents of this segment
   uint8_t* scratch;     // per CTA: NM x 128 x 256 residue bytes
-  int prefetch;         // K blocks of the next modulus prefetched into L2
+  int lookahead;        // L2 prefetch distance in K blocks (0 = off)
   int* counter;         // dynamic tile scheduler: next task (zeroed before the launch)
   unsigned long long* dbg;  // optional wait-cycle counters ($FSTK_SYRK_DEBUG)
   unsigned sleep_ns;    // suspend hint of the epilogue's waits (0 = spin)
@@ -348,12 +348,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int rowA = base + ti * kTile;
           const int rowB = base + tj * kTile;
           for (int kb = 0; kb < p.kblocks; ++kb) {
-            // Near the end of modulus t, pull the first K blocks of modulus
-            // t + 1's panels into L2 (a cold plane at every switch).
-            if (p.prefetch && t + 1 < NM && kb >= p.kblocks - p.prefetch) {
-              const int pk = kb - (p.kblocks - p.prefetch);
-              tma_prefetch_l2(&map, pk * kKB, rowA + p.np);
-              tma_prefetch_l2(&map, pk * kKB, rowB + p.np);
+            // Steady L2 lookahead: the K block `lookahead` stages ahead of
+            // this one (continuing into the next modulus's panels) is pulled
+            // into L2, so the TMA loads meet L2 rather than DRAM latency --
+            // the 7-stage shared-memory ring covers ~2.5 us.
+            if (p.lookahead) {
+              const int fk = kb + p.lookahead;
+              if (fk < p.kblocks) {
+                tma_prefetch_l2(&map, fk * kKB, rowA);
+                tma_prefetch_l2(&map, fk * kKB, rowB);
+              } else if (t + 1 < NM) {
+                tma_prefetch_l2(&map, (fk - p.kblocks) * kKB, rowA + p.np);
+                tma_prefetch_l2(&map, (fk - p.kblocks) * kKB, rowB + p.np);
+              }
             }
             if (p.pc_sleep) mbar_wait_sleep(&empty[stage], phase ^ 1, p.pc_sleep); else mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * kStageBytes;
@@ -869,11 +876,11 @@ double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n
   p.G = G;
   p.ex = ex;
   p.scratch = scratch;
-  static const int prefetch = [] {
-    const char* e = std::getenv("FSTK_SYRK_PREFETCH");
+  static const int lookahead = [] {
+    const char* e = std::getenv("FSTK_SYRK_LOOKAHEAD");
     return e ? std::atoi(e) : 0;
   }();
-  p.prefetch = std::min(prefetch, static_cast<int>(kp / kKB));
+  p.lookahead = lookahead;
   p.counter = reinterpret_cast<int*>(scratch + static_cast<size_t>(sm_count(device)) * nm * kHalf * kTile);
   FSTK_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(int), s));
   for (int t = 0; t < nm; ++t) {
