@@ -595,6 +595,8 @@ def main():
             line["refit_none"] = run_refit(model, rpts, rvals, cfgd, args, rank, world, dev,
                                            peak_mma, transform="none")
 
+    if rank == 0 and world == 1 and vals is not None and args.config in ("C1", "C2"):
+        line["upstream_idw"] = run_idw(pts, vals, cfgd, args)
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_eval_baseline(model, pts)
         if vals is not None and not args.no_refit:
@@ -606,6 +608,39 @@ def main():
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return 0
+
+
+def run_idw(pts, vals, cfgd, args) -> dict:
+    """the upstream interpolation of this config's cloud onto its
+    grid (C1: 64^3, C2: 256^3; interpolate_to_grid, ingest.cpp:265-383) on the
+    GPU through the public call (host arrays in and out), median of three,
+    with the oracle restatement on all host cores over a 32^3 sub-grid of the
+    same cloud (its index build included) beside it."""
+    import paper_1907_05884_b200 as F
+
+    n = 256 if args.config == "C2" else int(cfgd.get("grid", 64))
+    pc = F.PointCloud.from_data(pts, vals)
+    grid = F.StructuredGrid.unit([n] * pts.shape[1])
+    F.interpolate_to_grid(pc, grid)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        _, rep = F.interpolate_to_grid(pc, grid)
+        ts.append(time.perf_counter() - t0)
+    out = {"nodes": n ** pts.shape[1], "points": int(pts.shape[0]), "seconds": float(np.median(ts)),
+           "nodes_per_s": n ** pts.shape[1] / float(np.median(ts)),
+           "report": {"box_covered": rep.box_covered, "max_nearest_distance": rep.max_nearest_distance,
+                      "extrapolated_fraction": rep.extrapolated_fraction},
+           "path": "interpolate_to_grid (fstk_gpu_interpolate_to_grid, host arrays)"}
+    if not args.no_cpu:
+        from oracle import oracle as O
+
+        t0 = time.perf_counter()
+        O.interpolate_to_grid(pts, vals, (32,) * pts.shape[1])
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"seconds_32cubed": dt, "cores": O.max_threads(), "kind": "port",
+                               "sample": "the same cloud onto a 32^3 grid (index build included)"}
+    return out
 
 
 def sketch_roofline(model, info, t, transform, world):
