@@ -563,9 +563,15 @@ def main():
             "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": ck}
 
     # ---- refit (one problem; rows sharded across ranks; one all-reduce)
+    if NF > 1 and vals is None and not args.no_refit:
+        # C5's fields: seeded tanh fronts with distinct offsets and widths plus
+        # Gaussian kernels (BASELINE configs[4]) on the shared points.
+        vals = c5_field_values(pts, 0)
     if not args.no_refit and vals is not None:
         # The refit is ONE problem: every rank passes the same (rank-0) cloud.
         rpts, rvals = (pts, vals) if rank == 0 else dataset(args.config, args.points, 0)
+        if rvals is None:  # C5 on ranks > 0
+            rvals = c5_field_values(rpts, 0)
         line["refit"] = run_refit(model, rpts, rvals, cfgd, args, rank, world, dev, peak_mma)
         if NF > 1 and rank == 0 and world == 1:
             # C5 (BASELINE configs[4]): 8 independent refits with M = 8R each,
@@ -576,8 +582,7 @@ def main():
             per, res = [], []
             R = int(np.prod(model.ranks))
             for f, m in enumerate(models):
-                fv = rvals if f == 0 else m.evaluate_batch(rpts) + 1e-2 * np.random.default_rng(
-                    500 + f).normal(size=rpts.shape[0])
+                fv = rvals if f == 0 else c5_field_values(rpts, f)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 _, finfo = F.reestimate_core(m, rpts, fv, seed=0, sample_rows=cfgd["m_factor"] * R)
@@ -608,6 +613,20 @@ def main():
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return 0
+
+
+def c5_field_values(pts, f: int) -> np.ndarray:
+    """Field f of BASELINE configs[4]: a tanh front with its own offset and
+    width plus 4 seeded Gaussian kernels, noise sigma 1e-2."""
+    rng = np.random.default_rng(700 + f)
+    x, y, z = pts[:, 0], pts[:, 1], pts[:, 2]
+    off, width = 0.35 + 0.04 * f, 0.015 + 0.004 * f
+    v = np.tanh((z - off - 0.05 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y)) / width)
+    for _ in range(4):
+        cx, cy, cz = rng.random(3)
+        w, a = rng.uniform(0.02, 0.1), rng.normal(0.0, 0.2)
+        v = v + a * np.exp(-((x - cx) ** 2 + (y - cy) ** 2 + (z - cz) ** 2) / (w * w))
+    return v + 1e-2 * rng.normal(size=pts.shape[0])
 
 
 def run_idw(pts, vals, cfgd, args) -> dict:

@@ -86,7 +86,6 @@ struct SyrkParams {
   unsigned long long* dbg;  // optional wait-cycle counters ($FSTK_SYRK_DEBUG)
   unsigned sleep_ns;    // suspend hint of the epilogue's waits (0 = spin)
   unsigned pc_sleep;    // experiments: suspend hint of the producer / MMA waits
-  int skip;             // experiments: 1 = no scratch stores, 2 = no fold, 3 = neither
   int mod[kSyrkMaxModuli];
   unsigned p16[kSyrkMaxModuli];   // 2^16 mod m
   unsigned off[kSyrkMaxModuli];   // a multiple of m >= 2^22 (makes the folded value >= 0)
@@ -478,12 +477,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             w[u] = x;
           }
           uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
-          if (!(p.skip & 1)) {
-            __stcg(d4, make_uint4(w[0], w[1], w[2], w[3]));
-            __stcg(d4 + 1, make_uint4(w[4], w[5], w[6], w[7]));
-          } else if (w[0] == 0x12345678u) {
-            p.G[0] = 1.0;  // keep the residue arithmetic live
-          }
+          __stcg(d4, make_uint4(w[0], w[1], w[2], w[3]));
+          __stcg(d4 + 1, make_uint4(w[4], w[5], w[6], w[7]));
         }
         // The accumulator is free as soon as its residues are out.
         tc_fence_before();
@@ -498,7 +493,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       // Fold the tile's NM residues of every entry of this thread's 128
       // columns into G while the MMAs of the next tile run.
-      if (p.skip & 2) continue;
       const int gi = ti * kTile + static_cast<int>(rank) * kHalf + row;
       const int ei = gi < p.n ? __ldg(p.ex + gi) : 0;
       const int gjb = tj * kTile + half * (kTile / 2);
@@ -896,11 +890,6 @@ double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n
     return e ? static_cast<unsigned>(std::atoi(e)) : 500000u;
   }();
   p.sleep_ns = sleep_ns;
-  static const int skip = [] {
-    const char* e = std::getenv("FSTK_SYRK_SKIP");
-    return e ? std::atoi(e) : 0;
-  }();
-  p.skip = skip;
   static const unsigned pc_sleep = [] {
     const char* e = std::getenv("FSTK_SYRK_PC_SLEEP");
     return e ? static_cast<unsigned>(std::atoi(e)) : 200000u;
