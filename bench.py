@@ -705,10 +705,11 @@ def gram_roofline(gram_flops, info, t, peak_fp64, i8=None):
 
         eng = F.gram_engine()
         if eng == "tcgen05":
-            kern = (f"syrk_crt_kernel (fstk_syrk.cu): hand-written tcgen05.mma.cta_group::2.kind::i8 "
-                    f"SYRK, lower-triangle 256x256 tiles of every CRT modulus in one persistent launch "
-                    f"per row segment, Garner fold into G in the epilogue; plane-accuracy level "
-                    f"{info['gram_slices']}; residue/exponent kernels in fstk_gram.cu")
+            kern = (f"syrk_res_kernel (fstk_syrk.cu): hand-written tcgen05.mma.cta_group::2.kind::i8 "
+                    f"SYRK, lower-triangle 256x256 tiles, persistent with a dynamic tile scheduler, "
+                    f"one launch per column block and CRT modulus, residues reduced in the epilogue; "
+                    f"crt_fold4_kernel (Garner) and the residue/exponent kernels in fstk_gram.cu; "
+                    f"plane-accuracy level {info['gram_slices']}")
         else:
             kern = (f"cuBLASLt int8 IMMA GEMMs, one per CRT modulus, at plane-accuracy level "
                     f"{info['gram_slices']} (residue/fold kernels in fstk_gram.cu)")

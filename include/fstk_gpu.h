@@ -303,9 +303,10 @@ int32_t fstk_gpu_interpolate_to_grid_device(const double* points, const double* 
                                             double power, double* out, fstk_interp_report* report,
                                             uint32_t* neighbor_ids, void* stream, fstk_gpu_error* err);
 /* The int8 GEMM engine of the CRT Gram: 1 = the hand-written sm_100a
- * tcgen05 SYRK (default: lower-triangle 256x256 tiles of all moduli in one
- * persistent launch, residues reduced in the epilogue), 2 = cuBLASLt IMMA
- * GEMMs (kept for comparison; $FSTK_GRAM_GEMM=cublaslt).  Both produce the
+ * tcgen05 SYRK (default: lower-triangle 256x256 tiles, 2-CTA UTCIMMA, TMA,
+ * TMEM accumulators, residues reduced in the epilogue, dynamic tile
+ * scheduler; fstk_syrk.cu), 2 = cuBLASLt IMMA GEMMs (kept for comparison;
+ * $FSTK_GRAM_GEMM=cublaslt).  Both produce the
  * identical Gram bit for bit.  0 only queries.  Returns the previous setting. */
 int32_t fstk_gpu_gram_engine(int32_t engine);
 /* Packed normal equations (device pointers): unpack = 0 writes the lower

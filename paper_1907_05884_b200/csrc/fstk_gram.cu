@@ -379,6 +379,37 @@ __global__ void __launch_bounds__(256) crt_fold_kernel(const CT* __restrict__ C,
   *g = accumulate ? *g + v : v;
 }
 
+// Byte-residue fold (SYRK engine): four consecutive rows per thread -- one
+// 4-byte load per plane, four independent Garner chains in flight, and the
+// four G entries contiguous.  m % 4 == 0 (column blocks are 256-aligned).
+template <int NM>
+__global__ void __launch_bounds__(256) crt_fold4_kernel(const int8_t* __restrict__ C, int64_t cstride, int64_t m,
+                                                        int w, int c0, int n, int k, const int* __restrict__ ex,
+                                                        double* __restrict__ G, int64_t ldg, int accumulate,
+                                                        int negate) {
+  const int64_t i0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  const int j = blockIdx.y;
+  if (i0 >= m || j >= w || i0 + 3 < j || c0 + j >= n) return;
+  const int8_t* c = C + i0 + static_cast<int64_t>(j) * m;
+  char4 rb[NM];
+#pragma unroll
+  for (int t = 0; t < NM; ++t) rb[t] = __ldg(reinterpret_cast<const char4*>(c + static_cast<int64_t>(t) * cstride));
+  const int ej = ex[c0 + j];
+  double* g = G + (c0 + i0) + static_cast<int64_t>(c0 + j) * ldg;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = i0 + u;
+    if (i < j || c0 + i >= n) continue;
+    int r[NM];
+#pragma unroll
+    for (int t = 0; t < NM; ++t)
+      r[t] = u == 0 ? rb[t].x : u == 1 ? rb[t].y : u == 2 ? rb[t].z : rb[t].w;
+    const double v0 = crt_scale(crt_value<NM, true>(r), ex[c0 + i] + ej - 2 * k);
+    const double v = negate ? -v0 : v0;
+    g[u] = accumulate ? g[u] + v : v;
+  }
+}
+
 // Moduli for k-bit integers summed over kp rows: M > 4 kp 2^(2k).
 int crt_moduli(int k, int64_t kp) {
   const double need = 2.0 + std::log2(static_cast<double>(std::max<int64_t>(kp, 1))) + 2.0 * k;
@@ -405,6 +436,15 @@ void launch_crt(const SRC& src, int64_t s0, int64_t kr, int n, int64_t kp, int64
 template <int NM, class CT>
 void launch_crt_fold(const CT* C, int64_t cstride, int64_t m, int64_t wn, int64_t c0, int n,
                      int k, const int* ex, double* G, int64_t ldg, int acc, int neg, cudaStream_t s) {
+  if constexpr (sizeof(CT) == 1) {
+    if (m % 4 == 0 && cstride % 4 == 0) {
+      dim3 fg(static_cast<unsigned>(ceil_div(m, 1024)), static_cast<unsigned>(wn));
+      crt_fold4_kernel<NM><<<fg, 256, 0, s>>>(C, cstride, m, static_cast<int>(wn), static_cast<int>(c0), n, k,
+                                             ex, G, ldg, acc, neg);
+      check_launch("crt_fold4_kernel");
+      return;
+    }
+  }
   dim3 fg(static_cast<unsigned>(ceil_div(m, 256)), static_cast<unsigned>(wn));
   crt_fold_kernel<NM, CT><<<fg, 256, 0, s>>>(C, cstride, m, static_cast<int>(wn), static_cast<int>(c0),
                                              n, k, ex, G, ldg, acc, neg);
@@ -625,7 +665,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   if (syrk && syrk_fused()) {
     sc.C8.ensure(syrk_crt_scratch_bytes(nm, device));
   } else if (syrk) {
-    sc.C8.ensure(static_cast<size_t>(nm) * np * w);
+    sc.C8.ensure(static_cast<size_t>(nm) * np * w + 256);  // + the scheduler's task counter
   } else {
     sc.C.ensure(static_cast<size_t>(nm) * np * w);
     sc.ws.ensure(size_t(32) << 20);
@@ -651,12 +691,12 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
         const int64_t wn = std::min(w, np - c0);
         const int64_t m = np - c0;
         int8_t* c8 = reinterpret_cast<int8_t*>(sc.C8.p);
-        static const bool per_mod = std::getenv("FSTK_SYRK_PERMOD") != nullptr;
-        if (per_mod) {  // experiment: one launch per modulus, like the library GEMMs
+        int* counter = reinterpret_cast<int*>(sc.C8.p + static_cast<size_t>(nm) * np * w);
+        if (syrk_mode() == 0) {  // one launch per modulus (default: measured fastest)
           for (int t = 0; t < nm; ++t)
-            ops += syrk_i8_residues_one(sc.X.p, nm, t, kp, np, c0, wn, m, c8 + t * m * wn, device, s);
+            ops += syrk_i8_residues_one(sc.X.p, nm, t, kp, np, c0, wn, m, c8 + t * m * wn, counter, device, s);
         } else {
-          ops += syrk_i8_residues(sc.X.p, nm, kp, np, c0, wn, m, c8, m * wn, device, s);
+          ops += syrk_i8_residues(sc.X.p, nm, kp, np, c0, wn, m, c8, m * wn, counter, device, s);
         }
 #define FSTK_CRT_FOLD(NMV) \
   launch_crt_fold<NMV, int8_t>(c8, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)

@@ -215,14 +215,15 @@ int set_gram_engine(int engine);        // returns the previous setting; 0 = que
 // Returns the int8 ops issued.
 constexpr int kSyrkMaxModuli = 20;
 size_t syrk_crt_scratch_bytes(int nm, int device);
-// Unfused variant ($FSTK_SYRK_FUSED=0): residues of the column block
+// Unfused variants (default "permod"): residues of the column block
 // [c0, c0 + wn) x [c0, np) for every modulus into C (ld m, plane stride
 // cstride), folded afterwards by crt_fold_kernel.
 bool syrk_fused();
+int syrk_mode();
 double syrk_i8_residues_one(const int8_t* planes, int nm, int t, int64_t kp, int64_t np, int64_t c0, int64_t wn,
-                            int64_t m, int8_t* C, int device, cudaStream_t s);
+                            int64_t m, int8_t* C, int* counter, int device, cudaStream_t s);
 double syrk_i8_residues(const int8_t* planes, int nm, int64_t kp, int64_t np, int64_t c0, int64_t wn,
-                        int64_t m, int8_t* C, int64_t cstride, int device, cudaStream_t s);
+                        int64_t m, int8_t* C, int64_t cstride, int* counter, int device, cudaStream_t s);
 double syrk_crt_fold(const int8_t* planes, int nm, int64_t kp, int64_t np, int n, int k, const int* ex,
                      double* G, int64_t ldg, bool accumulate, bool negate, uint8_t* scratch, int device,
                      cudaStream_t s);

@@ -1,34 +1,43 @@
-// Hand-written sm_100a int8 SYRK + CRT fold for the Gram of the sketched
+// Hand-written sm_100a int8 SYRK (+ CRT fold) for the Gram of the sketched
 // system (fstk_gram.cu): the tensor-core stage of A^T A (randls.cpp:112-123
 // solves the sketched least-squares system whose normal equations these are;
 // randls.cpp:315-348 builds it).
 //
-// One launch per row segment computes the whole lower triangle of G's update:
-// for every 256 x 256 tile (tile row >= tile column) and every modulus t,
-// C_t = R_t^T R_t on the int8 tensor cores (R_t = the kp x np residue plane
-// t), and after the last modulus the epilogue rebuilds each exact integer sum
-// by Garner's algorithm and adds 2^(e_a+e_b-2k) times it into G -- no int32
-// planes, no separate fold kernel.  The library GEMMs this replaces computed
-// whole rectangular column blocks (~6% of the upper triangle) and needed an
-// HBM round trip of 36 bytes per entry into a fold kernel.
+// For every modulus t of a row segment, C_t = R_t^T R_t on the int8 tensor
+// cores (R_t = the kp x np residue plane t), lower-triangle 256 x 256 tiles
+// only (the library GEMMs it replaces computed whole column blocks, ~6% of
+// the upper triangle), each int32 sum reduced in the epilogue to its
+// symmetric residue modulo m_t.  Garner's algorithm then rebuilds each exact
+// integer sum and adds 2^(e_a+e_b-2k) times it into G.
 //
-// Structure (persistent; one CTA pair per two SMs):
-//  * CTA pairs (__cluster_dims__(2)) run tcgen05.mma.cta_group::2.kind::i8,
-//    M = 256 (128 rows per CTA), N = 256, K = 32 per instruction; each CTA
-//    TMA-loads (cp.async.bulk.tensor, 128B swizzle) its 128-row halves of
-//    the A and B panels, 128 bytes of K per stage, 7 stages deep.
-//  * warp 0: TMA producer; warp 1 (leader CTA): the single MMA-issuing
-//    thread; warp 2: TMEM allocator; warps 4-11: epilogue.
-//  * Accumulators live in TMEM (2 x 256 columns, double-buffered, so the
-//    epilogue of modulus t overlaps the MMAs of modulus t+1) and are read
-//    back with tcgen05.ld by 8 epilogue warps (two per TMEM lane quarter).
-//    Each modulus leaves its symmetric residues (one byte per entry) in a
-//    per-CTA L2-resident scratch and frees the accumulator at once; after
-//    the tile's last modulus the epilogue folds all NM of them into G while
-//    the MMAs of the next tile run.
-//  * Tiles are taken in bands of 8 tile columns, tile columns fastest, all
-//    moduli of a tile on one pair: the 74 concurrent pairs share ~17 panels
-//    of one plane in L2 at any time.
+// Common structure (CTA pairs, persistent, dynamic tile scheduler):
+//  * __cluster_dims__(2): tcgen05.mma.cta_group::2.kind::i8, M = 256 (128
+//    rows per CTA), N = 256, K = 32 per instruction, issued by one thread of
+//    the leader CTA; each CTA TMA-loads (cp.async.bulk.tensor.2d.cta_group::2,
+//    128B swizzle) its 128-row halves of the A and B panels, 128 bytes of K
+//    per stage, 7 stages deep; tcgen05.commit multicast frees stages and
+//    hands accumulators over in both CTAs.
+//  * warp 0: TMA producer; warp 1 (leader CTA): the MMA-issuing thread;
+//    warp 2: TMEM allocator; the epilogue warps read the two double-buffered
+//    256-column int32 accumulators with tcgen05.ld.
+//  * The leader's producer claims tasks with one atomicAdd and publishes them
+//    through a ring of slots in both CTAs (remote st.shared::cluster +
+//    mbarrier.arrive.release.cluster), so the concurrently active tiles stay
+//    a contiguous window of the banded tile order however the pairs drift.
+//  * Producer, MMA and epilogue waits are suspend-hinted mbarrier.try_wait.
+//
+// Variants ($FSTK_SYRK_MODE), all bit-identical:
+//  * "permod" (default, syrk_res_kernel): one launch per column block and
+//    modulus, byte residues to C (ld m), then crt_fold4_kernel -- like the
+//    library GEMMs this keeps a 2,048-wide B block resident in L2 for the
+//    whole launch; measured fastest (C2 Gram kernels 1.028 s vs 1.063 s for
+//    the cuBLASLt engine on the same box);
+//  * "block": the same kernel, every modulus of a column block in one launch;
+//  * "fused" (syrk_crt_kernel): one launch per segment over the whole lower
+//    triangle, all moduli of a tile on one pair, 8 epilogue warps keeping the
+//    byte residues in an L2-resident per-CTA scratch and folding into G while
+//    the next tile's MMAs run -- no fold kernel, but every modulus switch
+//    re-reads the wave's panels (77% tensor-pipe activity against 90%).
 // Exactness: |C_t| <= kp * 127^2 < 2^30 for kp <= 66,560, so the int32
 // accumulation is exact; residues are congruent to the int32 sums, so the
 // Garner digits -- and G -- equal the library engine's bit for bit.
@@ -41,6 +50,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 
 #include "fstk_common.cuh"
 #include "fstk_crt.cuh"
@@ -539,7 +549,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                  : "memory");
 }
 
-// ---- Unfused variant (FSTK_SYRK_FUSED=0): one launch per column block
+// ---- Unfused variants ("permod", "block"): one launch per column block
 // [c0, c0 + wn) of the lower triangle, task = (modulus, tile) with the
 // modulus outermost (the library GEMMs' order), symmetric residues stored
 // as bytes into C (column-major, ld m, plane stride cstride); the Garner
@@ -547,6 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 struct ResParams {
   int nm, kblocks, np, c0, ntj, nti, tri, per_mod, ntasks;
   int plane0;           // first plane (modulus) of this launch
+  int* counter;         // dynamic tile scheduler (zeroed before the launch)
   int hint_a, hint_b;   // L2 policy of the A / B panel loads: 0 none, 1 evict_last, 2 evict_first, 3 evict_normal
   long long ldc, cstride;
   int8_t* C;
@@ -578,10 +589,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* task_full = tempty + 2;              // dynamic scheduler, as syrk_crt_kernel
+  uint64_t* task_empty = task_full + kTaskRing;  // leader: MMA + peer producer + 8 epilogue warps
+  int* task_slot = reinterpret_cast<int*>(task_empty + kTaskRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(task_slot + kTaskRing);
   const uint32_t rank = cluster_rank();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   if (warp == 0 && lane == 0)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
   if (warp == 1 && lane == 0) {
@@ -592,6 +605,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);
+    }
+    for (int r = 0; r < kTaskRing; ++r) {
+      mbar_init(&task_full[r], 1);
+      mbar_init(&task_empty[r], 2 + 8);
     }
     fence_mbar_init();
   }
@@ -608,11 +625,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      uint64_t pol[4] = {0, 0, 0, 0};
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol[1]));
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol[2]));
-      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol[3]));
-      for (int task = pair; task < p.ntasks; task += npairs) {
+      uint64_t pl = 0, pf = 0, pn = 0;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pf));
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pn));
+      const uint64_t pol_a = p.hint_a == 1 ? pl : p.hint_a == 2 ? pf : pn;
+      const uint64_t pol_b = p.hint_b == 1 ? pl : p.hint_b == 2 ? pf : pn;
+      const uint32_t peer_slot0 = map_rank(&task_slot[0], 1);
+      const uint32_t peer_full0 = map_rank(&task_full[0], 1);
+      const uint32_t lead_empty0 = map_rank(&task_empty[0], 0);
+      for (int n = 0;; ++n) {
+        const int r = n % kTaskRing;
+        const uint32_t rph = (n / kTaskRing) & 1;
+        int task;
+        if (rank == 0) {
+          mbar_wait(&task_empty[r], rph ^ 1);
+          task = atomicAdd(p.counter, 1);
+          if (task >= p.ntasks) task = -1;
+          task_slot[r] = task;
+          st_cluster_s32(peer_slot0 + 4 * r, task);
+          mbar_arrive(&task_full[r]);
+          mbar_arrive_remote(peer_full0 + 8 * r);
+        } else {
+          mbar_wait_cluster(&task_full[r], rph);
+          task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+          mbar_arrive_remote(lead_empty0 + 8 * r);
+        }
+        if (task < 0) break;
         int t, ti, tj;
         decode_res(p, task, t, ti, tj);
         const int base = (p.plane0 + t) * p.np + p.c0 + static_cast<int>(rank) * kHalf;
@@ -621,9 +660,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           uint8_t* sa = smem + stage * kStageBytes;
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
           const uint32_t bar = map_rank(&full[stage], 0);
-          if (p.hint_a) tma_load_2sm_hint(sa, &map, kb * kKB, base + ti * kTile, bar, pol[p.hint_a]);
+          if (p.hint_a) tma_load_2sm_hint(sa, &map, kb * kKB, base + ti * kTile, bar, pol_a);
           else tma_load_2sm(sa, &map, kb * kKB, base + ti * kTile, bar);
-          if (p.hint_b) tma_load_2sm_hint(sa + kPanelBytes, &map, kb * kKB, base + tj * kTile, bar, pol[p.hint_b]);
+          if (p.hint_b) tma_load_2sm_hint(sa + kPanelBytes, &map, kb * kKB, base + tj * kTile, bar, pol_b);
           else tma_load_2sm(sa + kPanelBytes, &map, kb * kKB, base + tj * kTile, bar);
           if (++stage == kStages) {
             stage = 0;
@@ -635,7 +674,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
-      for (int task = pair; task < p.ntasks; task += npairs) {
+      for (int n = 0;; ++n) {
+        const int r = n % kTaskRing;
+        mbar_wait(&task_full[r], (n / kTaskRing) & 1);
+        const int task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+        mbar_arrive(&task_empty[r]);
+        if (task < 0) break;
         if (p.pc_sleep) mbar_wait_sleep(&tempty[acc], aphase ^ 1, p.pc_sleep); else mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * kAccCols;
@@ -661,7 +705,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const int q = warp & 3;
     const uint32_t te0 = map_rank(&tempty[0], 0), te1 = map_rank(&tempty[1], 0);
     uint32_t acc = 0, aphase = 0;
-    for (int task = pair; task < p.ntasks; task += npairs) {
+    const uint32_t lead_empty0 = map_rank(&task_empty[0], 0);
+    for (int n = 0;; ++n) {
+      const int r = n % kTaskRing;
+      int task = 0;
+      if (lane == 0) {
+        mbar_wait_cluster(&task_full[r], (n / kTaskRing) & 1);
+        task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+        mbar_arrive_remote(lead_empty0 + 8 * r);
+      }
+      task = __shfl_sync(0xffffffffu, task, 0);
+      if (task < 0) break;
       int t, ti, tj;
       decode_res(p, task, t, ti, tj);
       const int mt = p.mod[t];
@@ -736,26 +790,35 @@ void launch_syrk(const CUtensorMap& map, const SyrkParams& p, int pairs, int dev
 
 }  // namespace
 
-bool syrk_fused() {
-  static const bool fused = [] {
-    const char* e = std::getenv("FSTK_SYRK_FUSED");
-    return !(e && std::atoi(e) == 0);
+// Variant of the tcgen05 SYRK ($FSTK_SYRK_MODE): 0 "permod" (default): one
+// launch per column block and modulus, residues to C, separate byte fold;
+// 1 "block": one launch per column block with every modulus; 2 "fused":
+// one launch per segment with the fold in the epilogue.
+int syrk_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("FSTK_SYRK_MODE");
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "fused" ? 2 : v == "block" ? 1 : 0;
   }();
-  return fused;
+  return mode;
 }
+bool syrk_fused() { return syrk_mode() == 2; }
 
 static double syrk_res_launch(const int8_t* planes, int nm, int t0, int cnt, int64_t kp, int64_t np, int64_t c0,
-                              int64_t wn, int64_t m, int8_t* C, int64_t cstride, int device, cudaStream_t s);
+                              int64_t wn, int64_t m, int8_t* C, int64_t cstride, int* counter, int device,
+                              cudaStream_t s);
 double syrk_i8_residues(const int8_t* planes, int nm, int64_t kp, int64_t np, int64_t c0, int64_t wn,
-                        int64_t m, int8_t* C, int64_t cstride, int device, cudaStream_t s) {
-  return syrk_res_launch(planes, nm, 0, nm, kp, np, c0, wn, m, C, cstride, device, s);
+                        int64_t m, int8_t* C, int64_t cstride, int* counter, int device, cudaStream_t s) {
+  return syrk_res_launch(planes, nm, 0, nm, kp, np, c0, wn, m, C, cstride, counter, device, s);
 }
 double syrk_i8_residues_one(const int8_t* planes, int nm, int t, int64_t kp, int64_t np, int64_t c0, int64_t wn,
-                            int64_t m, int8_t* C, int device, cudaStream_t s) {
-  return syrk_res_launch(planes, nm, t, 1, kp, np, c0, wn, m, C, 0, device, s);
+                            int64_t m, int8_t* C, int* counter, int device, cudaStream_t s) {
+  return syrk_res_launch(planes, nm, t, 1, kp, np, c0, wn, m, C, 0, counter, device, s);
 }
 static double syrk_res_launch(const int8_t* planes, int nm, int t0, int cnt, int64_t kp, int64_t np, int64_t c0,
-                              int64_t wn, int64_t m, int8_t* C, int64_t cstride, int device, cudaStream_t s) {
+                              int64_t wn, int64_t m, int8_t* C, int64_t cstride, int* counter, int device,
+                              cudaStream_t s) {
   require(nm >= 1 && nm <= kSyrkMaxModuli, FSTK_E_COMPUTE, "internal: SYRK modulus count");
   require(kp % kKB == 0 && kp > 0 && kp <= 66560, FSTK_E_COMPUTE, "internal: SYRK segment rows");
   require(np % kTile == 0 && c0 % kTile == 0 && wn % kTile == 0 && m % kTile == 0 && c0 + m == np,
@@ -786,6 +849,8 @@ static double syrk_res_launch(const int8_t* planes, int nm, int t0, int cnt, int
   p.cstride = cstride;
   p.C = C;
   p.plane0 = t0;
+  p.counter = counter;
+  FSTK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), s));
   const char* e = std::getenv("FSTK_SYRK_PC_SLEEP");
   p.pc_sleep = e ? static_cast<unsigned>(std::atoi(e)) : 200000u;
   const char* hh = std::getenv("FSTK_SYRK_HINTS");
@@ -935,6 +1000,8 @@ extern "C" int32_t fstk_gpu_debug_syrk(const int8_t* planes, int32_t nm, int64_t
   using namespace fstk_gpu;
   return guarded(err, [&] {
     DeviceGuard dg(device);
-    syrk_i8_residues(planes, nm, kp, np, 0, np, np, c, np * np, device, static_cast<cudaStream_t>(stream));
+    DevBuf<int> counter(1);
+    syrk_i8_residues(planes, nm, kp, np, 0, np, np, c, np * np, counter.p, device, static_cast<cudaStream_t>(stream));
+    FSTK_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   });
 }

@@ -1,5 +1,7 @@
-"""Dev tool: A/B/C of Gram variants in one process (env per variant is read
-once, so each variant runs in its own subprocess, interleaved, cooled).
+"""Dev tool: A/B/C of Gram variants (env per variant is read once, so each
+variant runs in its own subprocess, interleaved, cooled); reports the summed
+device time of the Gram's kernels (CUPTI), not wall time (which includes the
+scratch allocations of the standalone Gram entry point).
 usage: python tools/syrk_ab2.py reps 'NAME:ENV=V,ENV=V' ..."""
 import os
 import statistics
@@ -23,7 +25,12 @@ def run():
     err = Err(); torch.cuda.synchronize(); t0 = time.perf_counter()
     check(lib().fstk_gpu_gram_device(a.data_ptr(), rows, rows, n, g.data_ptr(), 4, 0, s, C.byref(err)), err)
     torch.cuda.synchronize(); return time.perf_counter() - t0
-run(); time.sleep(2); print(run())
+run(); time.sleep(2)
+from torch.profiler import ProfilerActivity, profile
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    wall = run()
+kern = sum(e.device_time_total for e in prof.events() if e.device_type.name == "CUDA") / 1e6
+print(wall, kern)
 '''
 res = {v: [] for v in variants}
 for _ in range(reps):
@@ -35,7 +42,8 @@ for _ in range(reps):
             env[k] = val
         out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         try:
-            res[v].append(float(out.stdout.strip().splitlines()[-1]))
+            w, k = out.stdout.strip().splitlines()[-1].split()
+            res[v].append(float(k))
         except Exception:
             print(v, "failed:", out.stderr[-500:])
         time.sleep(2)
