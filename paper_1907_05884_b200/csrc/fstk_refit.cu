@@ -1756,6 +1756,13 @@ struct fstk_gpu_refit {
   bool factored = false;
   bool rank_def = false;
   double sigma_ratio = 0.0;  // certificate sigma_min(A) / max column norm (0 = not computed)
+  // The certificate's lambda_min(L L^T) power iteration, started by factor()
+  // on a side stream (own cuBLAS handle) so it overlaps the refinement --
+  // which only reads L too -- in the one-call solve and the staged path alike.
+  LambdaMinEstimate est;
+  cudaStream_t est_stream = nullptr;
+  cudaEvent_t est_event = nullptr;
+  bool est_live = false;
   DevBuf<double> tmp_r;   // local residual rows
   // transform = none: mode tables of this shard's sampled rows (A generated on demand)
   bool none = false;
@@ -1776,6 +1783,11 @@ struct fstk_gpu_refit {
   int64_t toff[kMaxOrder] = {0};
   int64_t ldt = 0;
   ~fstk_gpu_refit() {
+    if (est_stream) {
+      cudaStreamSynchronize(est_stream);
+      cudaStreamDestroy(est_stream);
+    }
+    if (est_event) cudaEventDestroy(est_event);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -2846,6 +2858,10 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
     cusolverDnSetStream(h.solver, s);
     const int n = static_cast<int>(rf->R);
     EventTimer ts(s);
+    if (rf->est_live) {  // L is about to be overwritten: the estimate must be done with it
+      FSTK_CUDA(cudaStreamSynchronize(rf->est_stream));
+      rf->est_live = false;
+    }
     rf->L.ensure(static_cast<size_t>(n) * n);
     FSTK_CUDA(cudaMemcpyAsync(rf->L.p, gram_in, static_cast<size_t>(n) * n * 8, cudaMemcpyDeviceToDevice, s));
     FSTK_CUDA(cudaMemcpyAsync(x_dev, rhs_in, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, s));
@@ -2903,6 +2919,17 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
       count_launch();
     } else {
       FSTK_CUDA(cudaMemsetAsync(x_dev, 0, static_cast<size_t>(n) * 8, s));
+    }
+    if (rf->factored) {
+      if (!rf->est_stream) {
+        FSTK_CUDA(cudaStreamCreateWithFlags(&rf->est_stream, cudaStreamNonBlocking));
+        FSTK_CUDA(cudaEventCreateWithFlags(&rf->est_event, cudaEventDisableTiming));
+      }
+      FSTK_CUDA(cudaEventRecord(rf->est_event, s));
+      FSTK_CUDA(cudaStreamWaitEvent(rf->est_stream, rf->est_event, 0));
+      rf->est = LambdaMinEstimate();
+      rf->est.start(rf->L.p, n, 3, rf->est_stream, rf->device);
+      rf->est_live = true;
     }
     FSTK_CUDA(cudaStreamSynchronize(s));
     if (info) {
@@ -2994,7 +3021,12 @@ int32_t fstk_gpu_refit_certify(fstk_gpu_refit* rf, const double* gram_in, double
     require(rf && gram_in && certified, FSTK_E_PARAMETER, "null argument");
     require(rf->factored, FSTK_E_PARAMETER, "refit_certify: no Cholesky factor");
     DeviceGuard dg(rf->device);
-    rf->sigma_ratio = refit_sigma_ratio(rf, gram_in);
+    double lam = -1.0;
+    if (rf->est_live) {
+      lam = rf->est.result();
+      rf->est_live = false;
+    }
+    rf->sigma_ratio = refit_sigma_ratio(rf, gram_in, lam);
     if (sigma_ratio) *sigma_ratio = rf->sigma_ratio;
     *certified = certified_full_rank(rf, rf->sigma_ratio) ? 1 : 0;
     if (*certified) rf->rank_def = false;
@@ -3092,36 +3124,10 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     DevBuf<double> g2, r2;
     const double* gcur = gram_in;
     const double* rcur = rhs_in;
-    // The certificate's power iteration reads the Cholesky factor on a side
-    // stream while the refinement streams A on the main one (latency-bound
-    // triangular solves beside HBM-bound GEMVs).
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_l = nullptr;
-    FSTK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    FSTK_CUDA(cudaEventCreateWithFlags(&ev_l, cudaEventDisableTiming));
-    struct SideGuard {
-      cudaStream_t s;
-      cudaEvent_t e;
-      ~SideGuard() {
-        cudaStreamSynchronize(s);
-        cudaStreamDestroy(s);
-        cudaEventDestroy(e);
-      }
-    } side_guard{side, ev_l};
-    LambdaMinEstimate est;
-    bool est_fresh = false;
-    auto start_estimate = [&]() {
-      FSTK_CUDA(cudaEventRecord(ev_l, rf->stream));
-      FSTK_CUDA(cudaStreamWaitEvent(side, ev_l, 0));
-      est = LambdaMinEstimate();
-      est.start(rf->L.p, n, 3, side, rf->device);
-      est_fresh = true;
-    };
+    // The certificate's power iteration runs on the session's side stream,
+    // started by each successful factor() (see fstk_gpu_refit_factor).
     auto escalate = [&]() -> bool {
       if (rf->gram_used == 0) return false;
-      // The factor is about to be overwritten: the estimate must be done with it.
-      FSTK_CUDA(cudaStreamSynchronize(side));
-      est_fresh = false;
       // Next level: kGramUpgradeSlices planes' accuracy, then the native Gram.
       const int to = rf->gram_used < kGramUpgradeSlices ? kGramUpgradeSlices : 0;
       fstk_reestimate_info li{};
@@ -3151,7 +3157,6 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
     bool need_qr = !rf->factored;
     if (rf->factored) {
       EventTimer tref(rf->stream);
-      start_estimate();
       double prev = 1e300;
       for (int it = 0; it < 8; ++it) {
         rc(fstk_gpu_refit_correction(rf, x.p, sv.p, err));
@@ -3171,7 +3176,6 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
         if (flat || slow || last) {
           if (rf->gram_used > 0) {
             if (!escalate_until_factored()) break;
-            start_estimate();
             prev = 1e300;
             it = -1;
             continue;
@@ -3184,7 +3188,11 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
         prev = step;
       }
       if (!need_qr && rf->factored) {
-        const double lam = est_fresh ? est.result() : -1.0;
+        double lam = -1.0;
+        if (rf->est_live) {
+          lam = rf->est.result();
+          rf->est_live = false;
+        }
         rf->sigma_ratio = refit_sigma_ratio(rf, gcur, lam);
         need_qr = !certified_full_rank(rf, rf->sigma_ratio);
       } else if (!rf->factored) {
