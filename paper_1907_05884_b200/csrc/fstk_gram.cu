@@ -35,6 +35,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "fstk_common.cuh"
 #include "fstk_crt.cuh"
@@ -312,6 +313,19 @@ __global__ void __launch_bounds__(128) residue_kernel(const SRC src, int64_t s0,
     for (int u = 0; u < RPT; ++u) x[u] = 0;
     if (a < n) {
       const auto col = src.col(a);
+      if constexpr (std::is_same<SRC, DenseSrc>::value) {
+        // A streams through once per segment: 16-byte loads, no L1 allocation.
+        const double* p = col.p + s0 + r0;
+        if (r0 + RPT <= rows && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+          for (int u = 0; u < RPT; u += 2) {
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(p + u));
+            x[u] = __double2int_rn(sc(v.x));
+            x[u + 1] = __double2int_rn(sc(v.y));
+          }
+          goto residues;
+        }
+      }
       if (r0 + RPT <= rows) {
 #pragma unroll
         for (int u = 0; u < RPT; ++u) x[u] = __double2int_rn(sc(col(s0 + r0 + u)));
@@ -321,6 +335,7 @@ __global__ void __launch_bounds__(128) residue_kernel(const SRC src, int64_t s0,
           if (r0 + u < rows) x[u] = __double2int_rn(sc(col(s0 + r0 + u)));
       }
     }
+  residues:
 #pragma unroll
     for (int i = 0; i < NM; ++i) {
       const unsigned m = static_cast<unsigned>(kmod(i));
