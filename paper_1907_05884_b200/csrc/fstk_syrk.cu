@@ -558,6 +558,7 @@ struct ResParams {
   int nm, kblocks, np, c0, ntj, nti, tri, per_mod, ntasks;
   int plane0;           // first plane (modulus) of this launch
   int* counter;         // dynamic tile scheduler (zeroed before the launch)
+  unsigned long long* dbg;  // optional MMA-thread wait counters ($FSTK_SYRK_DEBUG)
   int hint_a, hint_b;   // L2 policy of the A / B panel loads: 0 none, 1 evict_last, 2 evict_first, 3 evict_normal
   long long ldc, cstride;
   int8_t* C;
@@ -674,17 +675,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
+      unsigned long long w_empty = 0, w_full = 0, c0 = 0;
+      const unsigned long long t_begin = clock64();
       for (int n = 0;; ++n) {
         const int r = n % kTaskRing;
         mbar_wait(&task_full[r], (n / kTaskRing) & 1);
         const int task = *reinterpret_cast<volatile int*>(&task_slot[r]);
         mbar_arrive(&task_empty[r]);
         if (task < 0) break;
+        if (p.dbg) c0 = clock64();
         if (p.pc_sleep) mbar_wait_sleep(&tempty[acc], aphase ^ 1, p.pc_sleep); else mbar_wait(&tempty[acc], aphase ^ 1);
+        if (p.dbg) w_empty += clock64() - c0;
         tc_fence_after();
         const uint32_t d = tmem + acc * kAccCols;
         for (int kb = 0; kb < p.kblocks; ++kb) {
+          if (p.dbg) c0 = clock64();
           if (p.pc_sleep) mbar_wait_sleep(&full[stage], phase, p.pc_sleep); else mbar_wait(&full[stage], phase);
+          if (p.dbg) w_full += clock64() - c0;
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * kStageBytes);
           const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kPanelBytes);
@@ -699,6 +706,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         mma_commit_pair(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
+      }
+      if (p.dbg) {
+        atomicAdd(p.dbg + 0, w_empty);
+        atomicAdd(p.dbg + 1, w_full);
+        atomicAdd(p.dbg + 2, clock64() - t_begin);
       }
     }
   } else if (warp >= 4) {
@@ -745,6 +757,223 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   __syncwarp();
   tc_fence_before();
   cluster_sync_all();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kAccCols) : "memory");
+}
+
+// ---- Two CTA pairs per cluster ($FSTK_SYRK_CLUSTER=4): the pairs compute
+// the tiles (2 rp, tj) and (2 rp + 1, tj), which share their B panel, so
+// each CTA loads its A half (16 KB per stage) and half of its B half (8 KB)
+// and multicasts the latter to the same-parity CTA of the other pair --
+// 24 KB of L2-to-SM traffic per CTA and stage instead of 32.  Stage slots
+// are written by both pairs, so every CTA's empty barrier waits for both
+// pair leaders' MMA commits (multicast to all four CTAs).
+__device__ __forceinline__ void tma_load_2sm_mc(void* dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                                uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "h"(mask), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster4_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Cluster task -> (modulus, tile-row pair rp, tile column tj): per modulus,
+// row pairs in order, columns tj < min(2 rp + 2, ntj) fastest.
+__device__ __forceinline__ void decode_res4(const ResParams& p, int task, int& t, int& rp, int& tj) {
+  t = task / p.per_mod;
+  int r = task - t * p.per_mod;
+  rp = 0;
+  for (;;) {
+    const int cnt = min(2 * rp + 2, p.ntj);
+    if (r < cnt) break;
+    r -= cnt;
+    ++rp;
+  }
+  tj = r;
+}
+
+__global__ void __launch_bounds__(256, 1) syrk_res4_kernel(const __grid_constant__ CUtensorMap mapA,
+                                                           const __grid_constant__ CUtensorMap mapB,
+                                                           const ResParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* task_full = tempty + 2;
+  uint64_t* task_empty = task_full + kTaskRing;  // rank 0: 2 MMA + 3 producers + 16 epilogue warps
+  int* task_slot = reinterpret_cast<int*>(task_empty + kTaskRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(task_slot + kTaskRing);
+  const uint32_t crank = cluster_rank();  // 0..3
+  const uint32_t pair = crank >> 1, prank = crank & 1, lead = crank & ~1u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);  // both pair leaders' commits
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    for (int r = 0; r < kTaskRing; ++r) {
+      mbar_init(&task_full[r], 1);
+      mbar_init(&task_empty[r], 2 + 3 + 16);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * kAccCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster4_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+  const uint32_t lead_empty0 = map_rank(&task_empty[0], 0);
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      const uint16_t bmask = static_cast<uint16_t>((1u << prank) | (1u << (prank + 2)));
+      for (int n = 0;; ++n) {
+        const int r = n % kTaskRing;
+        const uint32_t rph = (n / kTaskRing) & 1;
+        int task;
+        if (crank == 0) {
+          mbar_wait(&task_empty[r], rph ^ 1);
+          task = atomicAdd(p.counter, 1);
+          if (task >= p.ntasks) task = -1;
+          task_slot[r] = task;
+          for (uint32_t q = 1; q < 4; ++q) st_cluster_s32(map_rank(&task_slot[r], q), task);
+          mbar_arrive(&task_full[r]);
+          for (uint32_t q = 1; q < 4; ++q) mbar_arrive_remote(map_rank(&task_full[r], q));
+        } else {
+          mbar_wait_cluster(&task_full[r], rph);
+          task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+          mbar_arrive_remote(lead_empty0 + 8 * r);
+        }
+        if (task < 0) break;
+        int t, rp, tj;
+        decode_res4(p, task, t, rp, tj);
+        int ti = 2 * rp + static_cast<int>(pair);
+        if (ti >= p.nti) ti = 2 * rp;  // odd tile-row count: a duplicate tile, not stored
+        const int plane = (p.plane0 + t) * p.np + p.c0;
+        const int rowA = plane + ti * kTile + static_cast<int>(prank) * kHalf;
+        const int rowB = plane + tj * kTile + static_cast<int>(prank) * kHalf + static_cast<int>(pair) * (kHalf / 2);
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          if (p.pc_sleep) mbar_wait_sleep(&empty[stage], phase ^ 1, p.pc_sleep); else mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          if (prank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          tma_load_2sm(sa, &mapA, kb * kKB, rowA, map_rank(&full[stage], lead));
+          tma_load_2sm_mc(sa + kPanelBytes + pair * (kPanelBytes / 2), &mapB, kb * kKB, rowB,
+                          smem_u32(&full[stage]) & 0xFEFFFFFFu, bmask);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (prank == 0 && lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, aphase = 0;
+      const uint16_t pmask = static_cast<uint16_t>(3u << crank);
+      for (int n = 0;; ++n) {
+        const int r = n % kTaskRing;
+        if (crank == 0) {
+          mbar_wait(&task_full[r], (n / kTaskRing) & 1);
+        } else {
+          mbar_wait_cluster(&task_full[r], (n / kTaskRing) & 1);
+        }
+        const int task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+        if (crank == 0) mbar_arrive(&task_empty[r]); else mbar_arrive_remote(lead_empty0 + 8 * r);
+        if (task < 0) break;
+        if (p.pc_sleep) mbar_wait_sleep(&tempty[acc], aphase ^ 1, p.pc_sleep); else mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * kAccCols;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          if (p.pc_sleep) mbar_wait_sleep(&full[stage], phase, p.pc_sleep); else mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+          const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kPanelBytes);
+#pragma unroll
+          for (int k = 0; k < kKB / 32; ++k) mma_i8(d, da + 2 * k, db + 2 * k, (kb | k) != 0 ? 1u : 0u);
+          mma_commit_mask(&empty[stage], static_cast<uint16_t>(0xF));
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_mask(&tfull[acc], pmask);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t te0 = map_rank(&tempty[0], lead), te1 = map_rank(&tempty[1], lead);
+    uint32_t acc = 0, aphase = 0;
+    for (int n = 0;; ++n) {
+      const int r = n % kTaskRing;
+      int task = 0;
+      if (lane == 0) {
+        mbar_wait_cluster(&task_full[r], (n / kTaskRing) & 1);
+        task = *reinterpret_cast<volatile int*>(&task_slot[r]);
+        mbar_arrive_remote(lead_empty0 + 8 * r);
+      }
+      task = __shfl_sync(0xffffffffu, task, 0);
+      if (task < 0) break;
+      int t, rp, tj;
+      decode_res4(p, task, t, rp, tj);
+      const int ti = 2 * rp + static_cast<int>(pair);
+      const bool store = ti < p.nti;
+      const int mt = p.mod[t];
+      const unsigned p16 = p.p16[t], off = p.off[t], magic = p.magic[t];
+      const long long i = static_cast<long long>(ti) * kTile + prank * kHalf + q * 32 + lane;
+      int8_t* crow = p.C + t * p.cstride + i + static_cast<long long>(tj) * kTile * p.ldc;
+      mbar_wait_sleep(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+      for (int ch = 0; ch < kAccCols / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tbase + ch * 32, v);
+        if (store) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            crow[static_cast<long long>(ch * 32 + c) * p.ldc] =
+                static_cast<int8_t>(sym_residue(static_cast<int>(v[c]), mt, p16, off, magic));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc ? te1 : te0) : "memory");
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster4_sync_all();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kAccCols) : "memory");
 }
@@ -873,9 +1102,73 @@ static double syrk_res_launch(const int8_t* planes, int nm, int t0, int cnt, int
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promos[promo & 3],
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     fail(FSTK_E_COMPUTE, "cuTensorMapEncodeTiled failed for the SYRK planes");
+  static const bool debug = std::getenv("FSTK_SYRK_DEBUG") != nullptr;
+  static unsigned long long* dbg = nullptr;  // accumulated over launches; printed by the caller's tool
+  if (debug && !dbg) {
+    FSTK_CUDA(cudaMalloc(&dbg, 32));
+    FSTK_CUDA(cudaMemset(dbg, 0, 32));
+  }
+  p.dbg = debug ? dbg : nullptr;
+  static const int cluster = [] {
+    const char* e = std::getenv("FSTK_SYRK_CLUSTER");
+    return (e && std::atoi(e) == 4) ? 4 : 2;
+  }();
+  if (cluster == 4) {
+    // Cluster tasks: tile-row pairs x tile columns (the two pairs share tj).
+    int per = 0;
+    for (int rp = 0; 2 * rp < p.nti; ++rp) per += std::min(2 * rp + 2, p.ntj);
+    p.per_mod = per;
+    p.ntasks = cnt * per;
+    CUtensorMap mapB;
+    const cuuint32_t boxB[2] = {kKB, kHalf / 2};
+    if (tensor_map_encoder()(&mapB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(planes), dims, strides,
+                             boxB, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promos[promo & 3],
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      fail(FSTK_E_COMPUTE, "cuTensorMapEncodeTiled failed for the SYRK B planes");
+    static std::atomic<uint64_t> attr4{0};
+    const uint64_t bit = uint64_t(1) << (device & 63);
+    if (!(attr4.load() & bit)) {
+      cudaFuncSetAttribute(syrk_res4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      attr4.fetch_or(bit);
+    }
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static int max_clusters[64] = {0};
+    int& mc = max_clusters[device & 63];
+    if (!mc) {
+      cfg.gridDim = dim3(4 * (sm_count(device) / 4));
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, syrk_res4_kernel, &cfg) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = sm_count(device) / 4;
+      }
+      mc = n;
+    }
+    cfg.gridDim = dim3(4 * std::max(1, std::min(p.ntasks, mc)));
+    FSTK_CUDA(cudaLaunchKernelEx(&cfg, syrk_res4_kernel, map, mapB, p));
+    check_launch("syrk_res4_kernel");
+    return 2.0 * static_cast<double>(p.ntasks) * 2 * kTile * kTile * static_cast<double>(kp);
+  }
   const int pairs = std::max(1, std::min(p.ntasks, sm_count(device) / 2));
   syrk_res_kernel<<<2 * pairs, 256, kSmemBytes, s>>>(map, p);
   check_launch("syrk_res_kernel");
+  if (debug && c0 + wn == np && t0 + cnt == nm) {  // last launch of a segment: report
+    unsigned long long h[4];
+    FSTK_CUDA(cudaMemcpyAsync(h, dbg, 32, cudaMemcpyDeviceToHost, s));
+    FSTK_CUDA(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "syrk_res: MMA thread cycles %.3g, waiting tempty %.1f%%, waiting full %.1f%%\n",
+                 double(h[2]), 100.0 * h[0] / double(h[2]), 100.0 * h[1] / double(h[2]));
+    FSTK_CUDA(cudaMemsetAsync(dbg, 0, 32, s));
+  }
   return 2.0 * static_cast<double>(p.ntasks) * kTile * kTile * static_cast<double>(kp);
 }
 
