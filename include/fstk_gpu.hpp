@@ -163,6 +163,25 @@ inline std::vector<double> reestimate_core(const Model& m, const double* points,
   return core;
 }
 
+// interpolate_to_grid (ingest.cpp:265-383): points Q x d column-major,
+// values Q, the cloud box (nullptr = the points' own), the grid sizes and
+// intervals; returns prod(sizes) values, mode-0 fastest (DenseTensor order).
+inline std::vector<double> interpolate_to_grid(const double* points, const double* values, int64_t q,
+                                               int32_t d, const double* box_lo, const double* box_hi,
+                                               const std::vector<int64_t>& sizes,
+                                               const std::vector<double>& lo, const std::vector<double>& hi,
+                                               int32_t neighbors = 0, double power = 2.0,
+                                               fstk_interp_report* report = nullptr, int32_t device = 0) {
+  int64_t n = 1;
+  for (auto s : sizes) n *= s;
+  std::vector<double> out(static_cast<size_t>(n > 0 ? n : 0));
+  fstk_gpu_error e{};
+  check(fstk_gpu_interpolate_to_grid(points, values, q, d, box_lo, box_hi, sizes.data(), lo.data(), hi.data(),
+                                     neighbors, power, out.data(), report, nullptr, device, &e),
+        e);
+  return out;
+}
+
 inline fstk_sketch_cfg default_sketch_config() {  // randls.hpp:15-24 defaults
   fstk_sketch_cfg c{};
   c.seed = 0;

@@ -95,7 +95,12 @@ int main(int argc, char** argv) {
   } catch (const fstk_gpu_shim::Error& e) {
     kind = e.kind(); mode = e.mode(); index = (long long)e.index(); value = e.value();
   }
+  // interpolate_to_grid through the shim: the cloud (pts, vals) onto 7 x 6 x 5.
+  fstk_interp_report rep{};
+  const std::vector<double> grid = fstk_gpu_shim::interpolate_to_grid(
+      pts.data(), vals.data(), q, d, nullptr, nullptr, {7, 6, 5}, {0.0, 0.0, 0.0}, {1.0, 1.0, 1.0}, 0, 2.0, &rep);
   std::ofstream out(argv[2], std::ios::binary);
+  wrv(out, grid);
   wrv(out, y);
   out.write(reinterpret_cast<const char*>(&y3), 8);
   wrv(out, mv);
@@ -163,6 +168,7 @@ def test_cpp_shim_evaluates_and_refits_on_the_gpu(tmp_path, O):
         o += n * np.dtype(dt).itemsize
         return a
 
+    grid = take(7 * 6 * 5)
     y = take(q)
     y3 = take(1)[0]
     mv = take(m.ranks[0] * 5)
@@ -185,3 +191,5 @@ def test_cpp_shim_evaluates_and_refits_on_the_gpu(tmp_path, O):
     assert bool(rk) == info_o["rank_deficient"]
     assert kind == 3 - 1  # FSTK_E_DOMAIN = ErrorKind::Domain + 1 (error.hpp:11-19)
     assert (int(mode), int(index), float(value)) == (1, 5, 1.5)
+    go, _ = O.interpolate_to_grid(pts, vals, (7, 6, 5))
+    assert float(np.abs(grid - go.reshape(-1, order="F")).max()) <= 1e-12

@@ -355,3 +355,36 @@ def test_gram_engine_setting():
     assert F.gram_engine() in ("tcgen05", "cublaslt")
     with pytest.raises(ValueError):
         F.gram_engine("wgmma")
+
+
+_VARIANT_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_1907_05884_b200 as F
+gen = torch.Generator(device="cuda").manual_seed(77)
+a = torch.randn(41_000, 2600, dtype=torch.float64, device="cuda", generator=gen)
+F.gram_engine("tcgen05")
+g = F.gram(a, slices=4)
+F.gram_engine("cublaslt")
+h = F.gram(a, slices=4)
+print("EQUAL" if torch.equal(g, h) else "DIFFER")
+"""
+
+
+@pytest.mark.parametrize("env", [{"FSTK_SYRK_MODE": "block"}, {"FSTK_SYRK_MODE": "fused"},
+                                 {"FSTK_SYRK_CLUSTER": "4"},
+                                 {"FSTK_SYRK_MODE": "block", "FSTK_SYRK_CLUSTER": "4"}])
+def test_tcgen05_syrk_variants_bit_identical(env):
+    # Every tcgen05 SYRK variant (environment, read once per process, hence a
+    # subprocess): two segments, two column blocks, ragged edges -- the Gram
+    # equals the library engine's bit for bit.
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT.format(root=ROOT)],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1] == "EQUAL"
