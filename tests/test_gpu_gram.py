@@ -92,10 +92,11 @@ def test_gram_bitexact_when_entries_fit_the_planes():
     ai[:, 1] = 0
     ai[0, :] = 2047  # ... then the planes hold every entry exactly
     a = torch.tensor(ai, dtype=torch.float64, device="cuda")
-    exact = ai.T.astype(np.int64) @ ai.astype(np.int64)
+    af = ai.astype(np.float64)
+    exact = af.T @ af  # integers below 2^38: exact in the fp64 BLAS product
     g = F.gram(a, slices=7).cpu().numpy()
     low = np.tril(np.ones((n, n), dtype=bool))
-    assert np.array_equal(g[low], exact[low].astype(np.float64))
+    assert np.array_equal(g[low], exact[low])
 
 
 def test_gram_rejects_bad_arguments():
@@ -341,14 +342,17 @@ def test_tcgen05_syrk_exact_integer_gram():
     ai = rng.integers(-8191, 8192, size=(rows, n))
     ai[0, :] = 8191
     a = torch.tensor(ai, dtype=torch.float64, device="cuda")
-    exact = ai.T.astype(np.int64) @ ai.astype(np.int64)
+    # |products| < 2^26 summed over 33,000 rows stay below 2^53: the fp64 BLAS
+    # product is the exact integer Gram (and fast, unlike int64 numpy).
+    af = ai.astype(np.float64)
+    exact = af.T @ af
     prev = F.gram_engine("tcgen05")
     try:
         g = F.gram(a, slices=4).cpu().numpy()
     finally:
         F.gram_engine(prev)
     low = np.tril(np.ones((n, n), dtype=bool))
-    assert np.array_equal(g[low], exact[low].astype(np.float64))
+    assert np.array_equal(g[low], exact[low])
 
 
 def test_gram_engine_setting():
