@@ -155,8 +155,8 @@ __global__ void col_exponent_kernel(const SRC src, int64_t s0, int64_t rows, int
 __global__ void slice_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int n,
                              int64_t kp, int ns, const int* __restrict__ ex,
                              int8_t* __restrict__ X, int8_t* __restrict__ Y) {
-  const int a = blockIdx.y;
-  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  const int a = blockIdx.x;  // column on grid.x (any n)
+  const int64_t r0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * 4;
   if (r0 >= kp) return;
   const Pow2Scale sc(6 - ex[a]);
   double v[4];
@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(128) residue_kernel(const SRC src, int64_t s0,
                                int64_t np, int k, const int* __restrict__ ex,
                                int8_t* __restrict__ X) {
   constexpr int RPT = residue_rows<X32>();
-  const int a = blockIdx.y;
-  const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * RPT;
+  const int a = blockIdx.x;  // column (grid.x: any R; rows on grid.y)
+  const int64_t r0 = (static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x) * RPT;
   if (r0 >= kp) return;
   const Pow2Scale sc(k - ex[a]);
   int8_t* dst = X + static_cast<int64_t>(a) * kp + r0;
@@ -440,10 +440,10 @@ template <int NM, class SRC>
 void launch_crt(const SRC& src, int64_t s0, int64_t kr, int n, int64_t kp, int64_t np, int k,
                 const int* ex, int8_t* X, cudaStream_t s) {
   if (k <= 30) {
-    dim3 g(static_cast<unsigned>(ceil_div(kp / residue_rows<true>(), 128)), static_cast<unsigned>(np));
+    dim3 g(static_cast<unsigned>(np), static_cast<unsigned>(ceil_div(kp / residue_rows<true>(), 128)));
     residue_kernel<NM, true, SRC><<<g, 128, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
   } else {
-    dim3 g(static_cast<unsigned>(ceil_div(kp / residue_rows<false>(), 128)), static_cast<unsigned>(np));
+    dim3 g(static_cast<unsigned>(np), static_cast<unsigned>(ceil_div(kp / residue_rows<false>(), 128)));
     residue_kernel<NM, false, SRC><<<g, 128, 0, s>>>(src, s0, kr, n, kp, np, k, ex, X);
   }
   check_launch("residue_kernel");
@@ -589,7 +589,7 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
     col_exponent_kernel<DenseSrc><<<static_cast<unsigned>(np), 256, 0, s>>>(DenseSrc{A, lda}, s0, kr, n,
                                                                            ex.p);
     check_launch("col_exponent_kernel");
-    dim3 sg(static_cast<unsigned>(ceil_div(kp / 4, 256)), static_cast<unsigned>(np));
+    dim3 sg(static_cast<unsigned>(np), static_cast<unsigned>(ceil_div(kp / 4, 256)));
     slice_kernel<<<sg, 256, 0, s>>>(A + s0, lda, kr, n, kp, ns, ex.p, X.p, Y.p);
     check_launch("slice_kernel");
     for (int64_t c0 = 0; c0 < np; c0 += w) {

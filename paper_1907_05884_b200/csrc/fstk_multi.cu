@@ -46,17 +46,18 @@ namespace {
 
 // ------------------------------------------------------------ kernels ---
 // packed[off(j) + i - j] = G[i + j n] for i >= j, off(j) = j n - j (j - 1) / 2.
+// (Columns strided over gridDim.y, so any n fits the 65,535 grid limit.)
 __global__ void pack_lower_kernel(const double* __restrict__ g, int64_t n, double* __restrict__ packed) {
-  const int64_t j = blockIdx.y;
-  const int64_t i = j + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  packed[j * n - j * (j - 1) / 2 + (i - j)] = g[i + j * n];
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    const int64_t i = j + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) packed[j * n - j * (j - 1) / 2 + (i - j)] = g[i + j * n];
+  }
 }
 __global__ void unpack_lower_kernel(const double* __restrict__ packed, int64_t n, double* __restrict__ g) {
-  const int64_t j = blockIdx.y;
-  const int64_t i = j + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  g[i + j * n] = packed[j * n - j * (j - 1) / 2 + (i - j)];
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    const int64_t i = j + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) g[i + j * n] = packed[j * n - j * (j - 1) / 2 + (i - j)];
+  }
 }
 __global__ void add_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -65,12 +66,12 @@ __global__ void add_kernel(double* __restrict__ y, const double* __restrict__ x,
 }
 
 void pack_lower(const double* g, int64_t n, double* packed, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(n));
+  dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(std::min<int64_t>(n, 65535)));
   pack_lower_kernel<<<grid, 256, 0, s>>>(g, n, packed);
   check_launch("pack_lower_kernel");
 }
 void unpack_lower(const double* packed, int64_t n, double* g, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(n));
+  dim3 grid(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(std::min<int64_t>(n, 65535)));
   unpack_lower_kernel<<<grid, 256, 0, s>>>(packed, n, g);
   check_launch("unpack_lower_kernel");
 }
