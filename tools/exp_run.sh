@@ -1,4 +1,4 @@
-# scratch experiment driver (gpurun): Gram tests + fold profile + Gram time
-python -m pytest tests/test_gpu_gram.py tests/test_gpu_refit.py -x -q > gpurun_out/exp_tests.log 2>&1; tail -n 1 gpurun_out/exp_tests.log
-python tools/prof_gram.py 4 > gpurun_out/pg.log 2>&1; python tools/prof_gram.py 4 >> gpurun_out/pg.log 2>&1; cat gpurun_out/pg.log
-ncu --set full --clock-control none -k regex:"crt_fold" -s 20 -c 1 -o gpurun_out/fold2 python tools/prof_gram.py 4 > /dev/null 2>&1
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests_a.log 2>&1; tail -n 3 gpurun_out/gputests_a.log
+python bench.py > gpurun_out/bench_a.log 2>&1; tail -n 2 gpurun_out/bench_a.log
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_a.log 2>&1; tail -n 1 gpurun_out/bench_ref_a.log
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_bench_r02.csv python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_a.log 2>&1; tail -n 2 gpurun_out/ncu_a.log
