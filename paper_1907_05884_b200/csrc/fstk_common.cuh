@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -126,6 +127,7 @@ struct DeviceCache {
   std::mutex mu;
   std::vector<CachedBlock> free_blocks;
   size_t cached = 0;
+  size_t cached_small = 0;  // of which blocks below kCacheMinBytes
 };
 inline DeviceCache& device_cache() {
   static DeviceCache* c = new DeviceCache();  // leaked: no teardown-order hazards at exit
@@ -166,6 +168,7 @@ inline void device_cache_trim(int device) {
     cudaSetDevice(b.device);
     cudaFree(b.p);
     c.cached -= b.bytes;
+    if (b.bytes < kCacheMinBytes) c.cached_small -= b.bytes;
     c.free_blocks.erase(c.free_blocks.begin() + i);
   }
   if (prev >= 0) cudaSetDevice(prev);
@@ -181,29 +184,85 @@ struct DeviceCacheSession {
   DeviceCacheSession(const DeviceCacheSession&) = delete;
   DeviceCacheSession& operator=(const DeviceCacheSession&) = delete;
 };
+// Driver-call accounting of the large-block path (FSTK_DEBUG_TIMING prints it).
+struct DriverAllocStats {
+  std::atomic<uint64_t> mallocs{0}, frees{0}, ns{0};
+  std::atomic<uint64_t> small_calls{0}, small_ns{0};  // blocks below the cache's size class
+};
+inline DriverAllocStats& driver_alloc_stats() {
+  static DriverAllocStats st;
+  return st;
+}
+struct DriverCallTimer {
+  bool small;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit DriverCallTimer(bool sm = false) : small(sm) {}
+  ~DriverCallTimer() {
+    (small ? driver_alloc_stats().small_ns : driver_alloc_stats().ns) += static_cast<uint64_t>(
+        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+// FSTK_DEBUG_TIMING: cumulative driver calls of the large-block path so far.
+inline void debug_alloc_report(const char* tag) {
+  static const bool on = std::getenv("FSTK_DEBUG_TIMING") != nullptr;
+  if (!on) return;
+  DriverAllocStats& st = driver_alloc_stats();
+  size_t fb = 0, tb = 0;
+  cudaMemGetInfo(&fb, &tb);
+  std::fprintf(stderr,
+               "fstk alloc @%s: cudaMalloc %llu cudaFree %llu driver %.1f ms; small blocks %llu calls %.1f ms; "
+               "free %.1f GB\n",
+               tag, static_cast<unsigned long long>(st.mallocs.load()),
+               static_cast<unsigned long long>(st.frees.load()), st.ns.load() * 1e-6,
+               static_cast<unsigned long long>(st.small_calls.load()), st.small_ns.load() * 1e-6, fb * 1e-9);
+}
+inline cudaError_t timed_malloc(void** p, size_t bytes, bool small = false) {
+  DriverCallTimer t(small);
+  ++(small ? driver_alloc_stats().small_calls : driver_alloc_stats().mallocs);
+  return cudaMalloc(p, bytes);
+}
+inline void timed_free(void* p, bool small = false) {
+  DriverCallTimer t(small);
+  ++(small ? driver_alloc_stats().small_calls : driver_alloc_stats().frees);
+  cudaFree(p);
+}
+// Small blocks (below the large-block size class) are cached in power-of-two
+// size buckets: a refit makes ~50 of them (scratch, index tables, solver
+// workspaces), and their cudaMalloc/cudaFree calls cost 30-100 ms per C2
+// refit in the driver -- up to 90 ms for a single cudaFree inside the blocked
+// Cholesky (FSTK_DEBUG_TIMING), the cause of its 0.2 -> 0.7 s outliers.
+constexpr size_t kSmallCacheCap = size_t(4) << 30;  // cached small blocks per process
+inline size_t small_bucket(size_t bytes) {
+  size_t b = 256;
+  while (b < bytes) b <<= 1;
+  return b;
+}
 inline cudaError_t device_alloc(void** p, size_t bytes, size_t* got) {
-  *got = bytes;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (bytes >= kCacheMinBytes && device_cache_enabled()) {
+  const bool small = bytes < kCacheMinBytes;
+  if (small && device_cache_enabled()) bytes = small_bucket(bytes);
+  *got = bytes;
+  if (device_cache_enabled()) {
     DeviceCache& c = device_cache();
     std::lock_guard<std::mutex> lk(c.mu);
     int best = -1;
     for (size_t i = 0; i < c.free_blocks.size(); ++i) {
       const CachedBlock& b = c.free_blocks[i];
-      if (b.device == dev && b.bytes >= bytes && b.bytes - bytes <= bytes / 8 &&
-          (best < 0 || b.bytes < c.free_blocks[best].bytes))
-        best = static_cast<int>(i);
+      if (b.device != dev) continue;
+      const bool fits = small ? b.bytes == bytes : (b.bytes >= bytes && b.bytes - bytes <= bytes / 8);
+      if (fits && (best < 0 || b.bytes < c.free_blocks[best].bytes)) best = static_cast<int>(i);
     }
     if (best >= 0) {
       *p = c.free_blocks[best].p;
       *got = c.free_blocks[best].bytes;
       c.cached -= c.free_blocks[best].bytes;
+      if (small) c.cached_small -= c.free_blocks[best].bytes;
       c.free_blocks.erase(c.free_blocks.begin() + best);  // keep release order (oldest first)
       return cudaSuccess;
     }
   }
-  if (bytes >= kCacheMinBytes && device_cache_enabled()) {
+  if (!small && device_cache_enabled()) {
     // A block beyond the cache's cap (C4's 137 GB sketch) means this
     // session's working set cannot stay cached: return everything now, once,
     // rather than evicting block by block inside the timed stages later.
@@ -211,7 +270,7 @@ inline cudaError_t device_alloc(void** p, size_t bytes, size_t* got) {
     if (cudaMemGetInfo(&fb, &tb) == cudaSuccess && bytes > tb / 4 * 3) device_cache_trim(dev);
     cudaGetLastError();
   }
-  cudaError_t e = cudaMalloc(p, bytes);
+  cudaError_t e = timed_malloc(p, bytes, small);
   // Out of memory: return cached blocks of this device to the driver, least
   // recently released first, one at a time until the request fits.
   while (e == cudaErrorMemoryAllocation) {
@@ -222,15 +281,17 @@ inline cudaError_t device_alloc(void** p, size_t bytes, size_t* got) {
       std::lock_guard<std::mutex> lk(c.mu);
       for (size_t i = 0; i < c.free_blocks.size(); ++i) {
         if (c.free_blocks[i].device != dev) continue;
-        cudaFree(c.free_blocks[i].p);
+        const bool sm = c.free_blocks[i].bytes < kCacheMinBytes;
+        timed_free(c.free_blocks[i].p, sm);
         c.cached -= c.free_blocks[i].bytes;
+        if (sm) c.cached_small -= c.free_blocks[i].bytes;
         c.free_blocks.erase(c.free_blocks.begin() + i);
         freed = true;
         break;
       }
     }
     if (!freed) break;
-    e = cudaMalloc(p, bytes);
+    e = timed_malloc(p, bytes, small);
   }
   return e;
 }
@@ -251,45 +312,60 @@ inline cudaError_t device_mem_info(size_t* free_b, size_t* total_b) {
 inline void device_free(void* p, size_t bytes) {
   if (!p) return;
   cudaPointerAttributes at{};
-  if (bytes >= kCacheMinBytes && device_cache_keeps() &&
-      cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice) {
+  const bool small = bytes < kCacheMinBytes;
+  // Small blocks are cached only in their bucket sizes (allocated while the cache was on).
+  const bool cacheable = !small || (bytes & (bytes - 1)) == 0;
+  if (cacheable && device_cache_keeps() && cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+      at.type == cudaMemoryTypeDevice) {
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != at.device) cudaSetDevice(at.device);
-    size_t total = 0, freeb = 0;
-    cudaMemGetInfo(&freeb, &total);
+    size_t cap = kSmallCacheCap;
+    if (!small) {
+      size_t total = 0, freeb = 0;
+      cudaMemGetInfo(&freeb, &total);
+      cap = total / 4 * 3;
+    }
     DeviceCache& c = device_cache();
     std::unique_lock<std::mutex> lk(c.mu);
-    const size_t cap = total / 4 * 3;
     const bool keep = bytes <= cap;
     if (keep) {
       // cudaFree would have synchronised the device; a cached block must
       // likewise be idle before the next owner's stream touches it.
       cudaDeviceSynchronize();
       // Least recently released blocks go first, so the latest session's
-      // working set is what stays cached.
-      size_t on_dev = 0;
+      // working set is what stays cached.  Large blocks are capped per
+      // device, small ones by their total.
+      size_t held = 0;
       for (const CachedBlock& b : c.free_blocks)
-        if (b.device == at.device) on_dev += b.bytes;
-      for (size_t i = 0; on_dev + bytes > cap && i < c.free_blocks.size();) {
-        if (c.free_blocks[i].device != at.device) {
+        if (small ? b.bytes < kCacheMinBytes : (b.device == at.device && b.bytes >= kCacheMinBytes))
+          held += b.bytes;
+      for (size_t i = 0; held + bytes > cap && i < c.free_blocks.size();) {
+        const CachedBlock& b = c.free_blocks[i];
+        const bool same_class = small ? b.bytes < kCacheMinBytes
+                                      : (b.device == at.device && b.bytes >= kCacheMinBytes);
+        if (!same_class) {
           ++i;
           continue;
         }
-        cudaFree(c.free_blocks[i].p);
-        on_dev -= c.free_blocks[i].bytes;
-        c.cached -= c.free_blocks[i].bytes;
+        if (b.device != at.device) cudaSetDevice(b.device);
+        timed_free(b.p, small);
+        if (b.device != at.device) cudaSetDevice(at.device);
+        held -= b.bytes;
+        c.cached -= b.bytes;
+        if (small) c.cached_small -= b.bytes;
         c.free_blocks.erase(c.free_blocks.begin() + i);
       }
       c.free_blocks.push_back({p, bytes, at.device});
       c.cached += bytes;
+      if (small) c.cached_small += bytes;
     }
     lk.unlock();
     if (prev >= 0 && prev != at.device) cudaSetDevice(prev);
     if (keep) return;
   }
   cudaGetLastError();
-  cudaFree(p);
+  timed_free(p, small);
 }
 
 // RAII device buffer.

@@ -958,130 +958,239 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
 }
 
 // ------------------------------------------- warp-level last pass (K3b) ---
-// Stages 10..19 of a q_pad = 2^20 complex sketch.  A CTA of 8 warps owns the
-// 8 adjacent position classes lo0..lo0+7 (positions t 1024 + lo, t < 1024),
-// i.e. whole 128-byte runs of the intermediate, and loops over the batch's
-// columns, so each class's twiddles are fetched once per launch: stages
-// 10..14 from a shared copy, stages 15..19 held in registers.
-// Phase A: lane (a_sub, c) of warp w loads t = 32 a + b (a = 4 w + a_sub,
-// b = 0..31) of class lo0 + c -- four full lines per load -- and runs stages
-// 10..14 (len 2^11..2^15) in registers.  One CTA exchange (per-class rows of
-// 33, class stride 1057: conflict-free both ways) gives warp w class lo0 + w
-// with lane b' holding t = 32 a + b', a = 0..31, for stages 15..19.  The
-// result is parked in the warp's class rows while the next column's loads
-// are in flight, and the class's sampled elements (destination rows
-// lo_start[lo] ..) are post-rotated (DCT) or split (FFT) and stored
-// row-contiguously.  Same butterflies and epilogue as transform_pass2_kernel,
-// in the same order.
-constexpr int kWp2Cls = 8;                     // classes (warps) per CTA
-constexpr int kWp2Stride = 32 * kWp1Row + 1;   // double2 per class row block
-constexpr int kWp2Cap = 512;                   // sampled elements per class cached in shared memory
-constexpr size_t kWp2Smem = (kWp2Cls * kWp2Stride + kWp2Cls * 31) * sizeof(double2) +
-                            kWp2Cls * kWp2Cap * (2 * sizeof(double) + sizeof(uint16_t));
+// Stages 10..19 of a q_pad = 2^20 complex sketch without a CTA barrier.
+// A CTA owns the two adjacent position classes lo0, lo0 + 1 (positions
+// t 1024 + lo, t < 1024: 32-byte runs of the intermediate), keeps their 2 x
+// 1023 replayed twiddles in shared memory, and its kPp2Pairs warp pairs work
+// on kPp2Pairs different columns at once: the twiddles are shared by every
+// warp and no warp waits on another column's data.
+// Warp h of a pair first takes the half t = 512 h + (0..511) of both classes:
+// Loads: lane l reads t = 512 h + 16 l + b (b = 0..15) with 256-bit loads,
+// one whole 32-byte sector (both classes' elements) per lane and load.  (With
+// 16-byte loads at this 16 KB stride the small L1 left beside the shared
+// memory caps the requests in flight: 1.8 TB/s against 4.7 TB/s, measured by
+// tools/stride_read2.cu.)
+// Phase A: stages 10..13 (len 2^11..2^14) over b, in registers, both classes.
+// A warp-private 32 x 32 transpose (XOR-swizzled rows: conflict-free both
+// ways) gives lane (class, b) the 32 elements a = t bits 4..8 for
+// Phase B: stages 14..18.  The result is parked in the warp's buffer; after
+// a 64-thread named barrier warp h takes class lo0 + h from both buffers,
+// lane (c', b) the elements with t bit 4 = c' of both halves, for
+// Phase C: stage 19 in registers.  Register j of lane l is then output
+// t = 32 j + l of the class; destination rows are assigned class by class in
+// ascending t (build_inputs), so a ballot over each register's sampled flags
+// compacts the sampled outputs (~S / q_pad of them) into consecutive
+// shared-memory slots, from which they are post-rotated (DCT) or split (FFT)
+// and stored row-contiguously while the next column's loads are in flight.
+// Same butterflies and epilogue as transform_pass2_kernel, in the same order,
+// so A is bit-identical.
+constexpr int kPp2Pairs = 5;                   // columns in flight per CTA
+constexpr int kPp2Warps = 2 * kPp2Pairs;
+constexpr int kPp2Buf = 1024;                  // double2 per warp
+// CTAs of kPp2Cluster adjacent class pairs form a cluster and stay within one
+// column of each other (split cluster barrier), so the 128-byte lines they
+// share are fetched from DRAM once and hit in L2 for the others.
+constexpr int kPp2Cluster = 4;
+constexpr int kPp2Cap = 384;                   // sampled elements per class with cached DCT rotations
+constexpr size_t kPp2Smem = (2 * 1023 + kPp2Warps * kPp2Buf) * sizeof(double2) +
+                            2 * kPp2Cap * 2 * sizeof(double) + 64 * sizeof(uint32_t);
 
-__device__ __forceinline__ void wp2_load(double2 (&v)[32], const double2* src) {
-#pragma unroll
-  for (int b = 0; b < 32; ++b) v[b] = __ldcs(src + static_cast<int64_t>(b) * 1024);
+__device__ __forceinline__ void pair_barrier(int pair) {
+  asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
 }
 
-__global__ void __launch_bounds__(kWp2Cls * 32, 1) warp_pass2_kernel(const PassParams P, int ncols_batch) {
+// One 32-byte sector: the elements of classes lo0 and lo0 + 1 at one t.
+template <int LD>
+__device__ __forceinline__ void ld_sector(const double2* p, double2& c0, double2& c1) {
+#define FSTK_LD256(Q)                                                          \
+  asm volatile("ld.global.L1::no_allocate." Q ".v4.b64 {%0,%1,%2,%3}, [%4];"   \
+               : "=d"(c0.x), "=d"(c0.y), "=d"(c1.x), "=d"(c1.y)                \
+               : "l"(p))
+  if constexpr (LD == 0) FSTK_LD256("L2::evict_first");
+  if constexpr (LD == 1) FSTK_LD256("L2::evict_normal");
+  if constexpr (LD == 2) FSTK_LD256("L2::evict_last");
+  if constexpr (LD == 3) FSTK_LD256("L2::evict_normal.L2::128B");
+  if constexpr (LD == 4) FSTK_LD256("L2::evict_last.L2::128B");
+#undef FSTK_LD256
+}
+
+__device__ __forceinline__ void butterfly(double2& lo, double2& hi, const double2 w) {
+  const double2 uu = lo;
+  const double2 t2 = cmul_x(hi, w);
+  lo = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
+  hi = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
+}
+
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
+template <int LD>
+__global__ void __cluster_dims__(kPp2Cluster, 1, 1) __launch_bounds__(kPp2Warps * 32, 1)
+pair_pass2_kernel(const PassParams P, int ncols_batch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double2* Xc = reinterpret_cast<double2*>(smem_raw);
-  double2* tA = Xc + kWp2Cls * kWp2Stride;  // [class][31]
-  // Per class, the first kWp2Cap sampled elements: t and the DCT rotation,
-  // the same for every column (loaded once per class group).
-  double* cre = reinterpret_cast<double*>(tA + kWp2Cls * 31) + warp * kWp2Cap;
-  double* cim = reinterpret_cast<double*>(tA + kWp2Cls * 31) + (kWp2Cls + warp) * kWp2Cap;
-  uint16_t* ct = reinterpret_cast<uint16_t*>(reinterpret_cast<double*>(tA + kWp2Cls * 31) +
-                                             2 * kWp2Cls * kWp2Cap) + warp * kWp2Cap;
-  const int c = lane & 7, a = 4 * warp + (lane >> 3);
-  double2* xo = Xc + c * kWp2Stride + a * kWp1Row;
-  double2* xw = Xc + warp * kWp2Stride;
-  for (int lg = blockIdx.x; lg < 1024 / kWp2Cls; lg += gridDim.x) {
-    const int lo0 = lg * kWp2Cls, lo = lo0 + warp;
-    __syncthreads();  // previous class group done with tA
-    for (int i = threadIdx.x; i < kWp2Cls * 31; i += blockDim.x)
-      tA[i] = P.tw2[static_cast<int64_t>(lo0 + i / 31) * 1023 + i % 31];
-    // stages 15..19 twiddles of class lo for this lane: k = lo + 1024 (b' + 32 m)
-    double2 twB[31];
-    {
-      const double2* twr = P.tw2 + static_cast<int64_t>(lo) * 1023 + lane;
-#pragma unroll
-      for (int i = 0; i < 5; ++i)
-#pragma unroll
-        for (int m = 0; m < (1 << i); ++m) twB[(1 << i) - 1 + m] = __ldg(twr + (32 << i) - 1 + 32 * m);
-    }
-    const double2* tc = tA + 31 * c;
-    const int first = P.lo_start[lo], cnt = P.lo_start[lo + 1] - first;
-    const bool dct = P.kind == FSTK_TRANSFORM_DCT;
-    for (int i = lane; i < min(cnt, kWp2Cap); i += 32) {
-      ct[i] = P.t_list[first + i];
-      if (dct) {
-        cre[i] = P.post_re[first + i];
-        cim[i] = P.post_im[first + i];
+  const int pair = warp >> 1, h = warp & 1;
+  double2* tw = reinterpret_cast<double2*>(smem_raw);              // [2][1023]
+  double2* Xall = tw + 2 * 1023;
+  double2* X = Xall + warp * kPp2Buf;                              // this warp's buffer
+  const double2* X0 = Xall + (2 * pair) * kPp2Buf;                 // t < 512 half of the pair
+  const double2* X1 = X0 + kPp2Buf;                                // t >= 512 half
+  double* cre_all = reinterpret_cast<double*>(Xall + kPp2Warps * kPp2Buf);
+  double* cim_all = cre_all + 2 * kPp2Cap;
+  uint32_t* mask_all = reinterpret_cast<uint32_t*>(cim_all + 2 * kPp2Cap);  // [2][32]
+  const int lo0 = 2 * static_cast<int>(blockIdx.x);
+  const bool dct = P.kind == FSTK_TRANSFORM_DCT;
+  for (int i = threadIdx.x; i < 2 * 1023; i += blockDim.x) tw[i] = P.tw2[static_cast<int64_t>(lo0) * 1023 + i];
+  if (threadIdx.x < 64) mask_all[threadIdx.x] = 0;
+  __syncthreads();
+  // Sampled flags of both classes: bit j of mask[class][l] is t = 32 j + l.
+  {
+    const int f0 = P.lo_start[lo0], f2 = P.lo_start[lo0 + 2], f1 = P.lo_start[lo0 + 1];
+    for (int i = f0 + threadIdx.x; i < f2; i += blockDim.x) {
+      const int cl = i >= f1 ? 1 : 0;
+      const int t = P.t_list[i];
+      atomicOr(mask_all + 32 * cl + (t & 31), 1u << (t >> 5));
+      const int k = i - (cl ? f1 : f0);
+      if (dct && k < kPp2Cap) {
+        cre_all[cl * kPp2Cap + k] = P.post_re[i];
+        cim_all[cl * kPp2Cap + k] = P.post_im[i];
       }
     }
-    const double2* src0 = P.cbuf + lo0 + c + static_cast<int64_t>(32 * a) * 1024;
-    double2 v[32];
-    wp2_load(v, src0);
-    __syncthreads();  // tA ready
-    for (int cc = 0; cc < ncols_batch; ++cc) {
-      const int64_t col = P.col0 + cc;
-      // ---- stages 10..14: k = lo + 1024 (b mod 2^j)
+  }
+  __syncthreads();
+  const double2* src0 = P.cbuf + lo0 + static_cast<int64_t>(512 * h + 16 * lane) * 1024;
+  // Output coordinates: warp h stores class lo0 + h.
+  const int lo = lo0 + h;
+  const int first = P.lo_start[lo], cnt = P.lo_start[lo + 1] - first;
+  // rows [row_lo, row_hi) of this shard within the class's rows first + [0, cnt)
+  const int ilo = static_cast<int>(max(int64_t(0), min(int64_t(cnt), P.row_lo - first)));
+  const int ihi = static_cast<int>(max(int64_t(0), min(int64_t(cnt), P.row_hi - first)));
+  const uint32_t M = mask_all[32 * h + lane];
+  const uint32_t lt = (1u << lane) - 1u;
+  const bool zero_first = lo == 0 && cnt > 0 && (M & 1u) && lane == 0;  // t = 0 of class 0: dct_post(k = 0)
+  const double2* twh = tw + 1023 * h;
+  const double* cre = cre_all + h * kPp2Cap;
+  const double* cim = cim_all + h * kPp2Cap;
+  const int pc = lane >> 4, pb = lane & 15;  // phase B/C lane coordinates
+  const double2* twc = tw + 1023 * pc;
+  const int cstep = static_cast<int>(gridDim.y) * kPp2Pairs;
+  int cc = static_cast<int>(blockIdx.y) * kPp2Pairs + pair;
+  // Every warp of the cluster runs the same number of rounds (the cluster
+  // barrier counts all of them); a pair without a column left idles through.
+  const int rounds = (ncols_batch - static_cast<int>(blockIdx.y) * kPp2Pairs + cstep - 1) / cstep;
+  double2 v[32];
+  if (cc < ncols_batch) {
+    const double2* src = src0 + static_cast<int64_t>(cc) * P.n;
 #pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        const int half = 1 << j;
+    for (int b = 0; b < 16; ++b) ld_sector<LD>(src + static_cast<int64_t>(b) * 1024, v[b], v[16 + b]);
+  }
+  cluster_arrive_relaxed();
+  for (int rnd = 0; rnd < rounds; ++rnd, cc += cstep) {
+    if (cc >= ncols_batch) {
+      cluster_wait();
+      cluster_arrive_relaxed();
+      continue;
+    }
+    const int64_t col = P.col0 + cc;
+    // ---- phase A, stages 10..13: registers (class, b), k = lo + 1024 (b mod 2^j)
 #pragma unroll
-        for (int b = 0; b < 32; ++b) {
+    for (int j = 0; j < 4; ++j) {
+      const int half = 1 << j;
+#pragma unroll
+      for (int cl = 0; cl < 2; ++cl) {
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
           if (b & half) continue;
-          const double2 w = tc[half - 1 + (b & (half - 1))];
-          const double2 uu = v[b];
-          const double2 t2 = cmul_x(v[b + half], w);
-          v[b] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
-          v[b + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
+          butterfly(v[16 * cl + b], v[16 * cl + b + half], tw[1023 * cl + half - 1 + (b & (half - 1))]);
         }
       }
-      // ---- exchange: warp w takes class lo0 + w, lane b' the elements 32 a + b'
-      __syncthreads();  // previous column's output reads done
+    }
+    // ---- transpose: register r = 16 class + b of lane a  ->  register a of lane r.
+    // Element (a, r) lives at 32 a + (r ^ a).
+    __syncwarp();
 #pragma unroll
-      for (int b = 0; b < 32; ++b) xo[b] = v[b];
-      __syncthreads();
+    for (int r = 0; r < 32; ++r) X[32 * lane + (r ^ lane)] = v[r];
+    __syncwarp();
 #pragma unroll
-      for (int aa = 0; aa < 32; ++aa) v[aa] = xw[aa * kWp1Row + lane];
-      // ---- stages 15..19: k = lo + 1024 (b' + 32 (a mod 2^i))
+    for (int a2 = 0; a2 < 32; ++a2) v[a2] = X[32 * a2 + (lane ^ a2)];
+    // ---- phase B, stages 14..18: k = lo + 1024 (b + 16 (a mod 2^i))
 #pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        const int half = 1 << i;
+    for (int i = 0; i < 5; ++i) {
+      const int half = 1 << i;
 #pragma unroll
-        for (int m = 0; m < half; ++m) {
-          const double2 w = twB[half - 1 + m];
+      for (int m = 0; m < half; ++m) {
+        const double2 w = twc[(16 << i) - 1 + 16 * m + pb];
 #pragma unroll
-          for (int aa = m; aa < 32; aa += 2 * half) {
-            const double2 uu = v[aa];
-            const double2 t2 = cmul_x(v[aa + half], w);
-            v[aa] = make_double2(xadd(uu.x, t2.x), xadd(uu.y, t2.y));
-            v[aa + half] = make_double2(xsub(uu.x, t2.x), xsub(uu.y, t2.y));
-          }
-        }
+        for (int a2 = m; a2 < 32; a2 += 2 * half) butterfly(v[a2], v[a2 + half], w);
       }
-      __syncwarp();
+    }
+    __syncwarp();
 #pragma unroll
-      for (int aa = 0; aa < 32; ++aa) xw[aa * kWp1Row + lane] = v[aa];
-      __syncwarp();
-      if (cc + 1 < ncols_batch) wp2_load(v, src0 + static_cast<int64_t>(cc + 1) * P.n);
-      // ---- sampled rows of this class (consecutive destination rows)
-      for (int i = lane; i < cnt; i += 32) {
-        const int64_t sl = first + i;
-        if (sl < P.row_lo || sl >= P.row_hi) continue;
-        const bool cached = i < kWp2Cap;
-        const int t = cached ? ct[i] : P.t_list[sl];
-        const double2 V = xw[(t >> 5) * kWp1Row + (t & 31)];
-        if (dct) {
-          const double re = cached ? cre[i] : __ldg(P.post_re + sl);
-          const double im = cached ? cim[i] : __ldg(P.post_im + sl);
+    for (int a2 = 0; a2 < 32; ++a2) X[32 * a2 + (lane ^ a2)] = v[a2];
+    pair_barrier(pair);  // both halves parked
+    // ---- phase C: class lo0 + h; lane (c', b) takes a = 2 a4 + c' of both halves
+#pragma unroll
+    for (int a4 = 0; a4 < 16; ++a4) {
+      const int a2 = 2 * a4 + pc;
+      const int idx = 32 * a2 + ((16 * h + pb) ^ a2);
+      v[a4] = X0[idx];
+      v[16 + a4] = X1[idx];
+    }
+    pair_barrier(pair);  // both buffers read: free for the compaction and the next column
+    // stage 19: k = lo + 1024 (32 a4 + lane)
+#pragma unroll
+    for (int a4 = 0; a4 < 16; ++a4) butterfly(v[a4], v[16 + a4], twh[511 + 32 * a4 + lane]);
+    // ---- compaction: register j is t = 32 j + lane; ascending t = ballot order
+    {
+      int base = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const bool on = (M >> j) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, on);
+        if (on) X[base + __popc(bal & lt)] = v[j];
+        base += __popc(bal);
+      }
+    }
+    __syncwarp();
+    cluster_wait();  // every CTA of the cluster has issued this round's loads
+    if (cc + cstep < ncols_batch) {
+      const double2* src = src0 + static_cast<int64_t>(cc + cstep) * P.n;
+#pragma unroll
+      for (int b = 0; b < 16; ++b) ld_sector<LD>(src + static_cast<int64_t>(b) * 1024, v[b], v[16 + b]);
+    }
+    cluster_arrive_relaxed();
+    // ---- sampled outputs of class lo: consecutive destination rows
+    if (!P.packed) {
+      double* out = ((col == P.R) ? P.b : P.A + P.lda * col) + (first - P.row_lo);
+      if (dct) {
+#pragma unroll 4
+        for (int i = ilo + lane; i < ihi; i += 32) {
+          const double2 V = X[i];
+          const bool cached = i < kPp2Cap;
+          const double re = cached ? cre[i] : __ldg(P.post_re + first + i);
+          const double im = cached ? cim[i] : __ldg(P.post_im + first + i);
           const double val = xsub(xmul(re, V.x), xmul(im, V.y));
-          const double cf = (t == 0 && lo == 0) ? P.post_c0 : P.post_ck;  // dct_post(k = t 1024 + lo)
+          const double cf = (zero_first && i == 0) ? P.post_c0 : P.post_ck;  // dct_post(k = t 1024 + lo)
+          out[i] = xmul(P.scale, xmul(cf, val));
+        }
+      } else {
+#pragma unroll 4
+        for (int i = ilo + lane; i < ihi; i += 32) {
+          const double2 V = X[i];
+          out[i] = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
+          out[i + P.im_off] = xmul(P.scale, xmul(V.y, P.inv_sqrt_n));
+        }
+      }
+    } else {
+      // column-sharded sketch: rows go to their owners' packed send blocks
+      for (int i = ilo + lane; i < ihi; i += 32) {
+        const int64_t sl = first + i;
+        const double2 V = X[i];
+        if (dct) {
+          const double val = xsub(xmul(__ldg(P.post_re + sl), V.x), xmul(__ldg(P.post_im + sl), V.y));
+          const double cf = (zero_first && i == 0) ? P.post_c0 : P.post_ck;
           *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(cf, val));
         } else {
           *store_ptr(P, col, sl, false) = xmul(P.scale, xmul(V.x, P.inv_sqrt_n));
@@ -1090,6 +1199,7 @@ __global__ void __launch_bounds__(kWp2Cls * 32, 1) warp_pass2_kernel(const PassP
       }
     }
   }
+  cluster_wait();
 }
 
 // u0[p] *= s_p for every function (sign folded into the mode-0 table: since
@@ -1308,7 +1418,11 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<3, 12>));
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<4, 8>));
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<4, 12>));
-    attr_w(reinterpret_cast<const void*>(warp_pass2_kernel));
+    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<0>));
+    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<1>));
+    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<2>));
+    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<3>));
+    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<4>));
   });
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1430,10 +1544,22 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
         P.tw2 = tw2->p;
         P.lo_start = J.lo_start;
         P.t_list = J.t_list;
-        const size_t wsm = kWp2Smem;
-        const unsigned wgrid = static_cast<unsigned>(std::min<int64_t>(sms, 1024 / kWp2Cls));
-        warp_pass2_kernel<<<wgrid, kWp2Cls * 32, wsm, s>>>(P, nb);
-        check_launch("warp_pass2_kernel");
+        // One CTA per class pair and column slice: ~7 waves of CTAs.
+        const int64_t ysplit = std::max<int64_t>(1, std::min<int64_t>(ceil_div(static_cast<int64_t>(nb), kPp2Pairs),
+                                                                      ceil_div(int64_t(sms) * 7, 512)));
+        dim3 pgrid(512, static_cast<unsigned>(ysplit));
+        static const int ldm = [] {
+          const char* e = std::getenv("FSTK_PP2_LD");
+          return e ? std::atoi(e) : 0;
+        }();
+        switch (ldm) {
+          case 1: pair_pass2_kernel<1><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
+          case 2: pair_pass2_kernel<2><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
+          case 3: pair_pass2_kernel<3><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
+          case 4: pair_pass2_kernel<4><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
+          default: pair_pass2_kernel<0><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
+        }
+        check_launch("pair_pass2_kernel");
         continue;
       }
       if (warp_mode != 0 && !real && pass == 0 && !P.last && P.L == 10 && dt > 0) {
@@ -2201,8 +2327,10 @@ int32_t fstk_gpu_refit_begin(const fstk_gpu_model* m, const double* points, cons
                              int64_t q, int32_t d, const fstk_sketch_cfg* cfg, int32_t shard,
                              int32_t shards, fstk_gpu_refit** out, fstk_reestimate_info* info,
                              fstk_gpu_error* err) {
-  return fstk_gpu::refit_begin_impl(m, points, values, q, d, cfg, shard, shards, false, out, info,
-                                    err);
+  const int32_t rc = fstk_gpu::refit_begin_impl(m, points, values, q, d, cfg, shard, shards, false, out,
+                                                info, err);
+  fstk_gpu::debug_alloc_report("begin");
+  return rc;
 }
 
 int32_t fstk_gpu_refit_begin_columns(const fstk_gpu_model* m, const double* points,
@@ -2548,6 +2676,7 @@ int32_t fstk_gpu_refit_normal_equations(fstk_gpu_refit* rf, double* gram, double
   return guarded(err, [&] {
     require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
     normal_equations(rf, gram, rhs, info, -1);
+    debug_alloc_report("normal_equations");
   });
 }
 
@@ -2873,6 +3002,7 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
       // Blocked Cholesky with int8 tensor-core trailing updates; a block that
       // is not positive definite there is retried with cuSOLVER's dpotrf.
       static const bool dbg = std::getenv("FSTK_DEBUG_TIMING") != nullptr;
+      if (dbg) debug_alloc_report("factor start");
       const auto tc0 = std::chrono::steady_clock::now();
       bool chol_ok = false;
       try {
@@ -2883,9 +3013,11 @@ int32_t fstk_gpu_refit_factor(fstk_gpu_refit* rf, const double* gram_in, const d
         cudaGetLastError();
         FSTK_CUDA(cudaStreamSynchronize(s));
       }
-      if (dbg)
+      if (dbg) {
         std::fprintf(stderr, "fstk factor: chol_crt %8.2f ms\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count());
+        debug_alloc_report("factor");
+      }
       if (chol_ok) {
         hinfo = 0;
       } else {
