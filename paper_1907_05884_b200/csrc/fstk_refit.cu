@@ -226,7 +226,7 @@ static std::shared_ptr<DevBuf<double2>> twiddles(int device, uint64_t n) {
   return buf;
 }
 
-// Twiddle rows of warp_pass2_kernel for n = 2^20: row lo holds, at local
+// Twiddle rows of pair_pass2_kernel for n = 2^20: row lo holds, at local
 // index (2^J - 1) + t' (J = 0..9, t' < 2^J), the replayed twiddle of stage
 // 10 + J for k = lo + 1024 t', i.e. tw[(2^(10+J) - 1) + lo + 1024 t'].
 static std::map<TwiddleKey, std::shared_ptr<DevBuf<double2>>> g_tw2;
@@ -246,17 +246,15 @@ static std::shared_ptr<DevBuf<double2>> warp_pass2_twiddles(int device, uint64_t
   return buf;
 }
 
-// Whether the last pass of a sketch runs warp_pass2_kernel: complex
+// Whether the last pass of a sketch runs pair_pass2_kernel: complex
 // transforms with q_pad = 2^20 (two passes of 10 stages), when
-// FSTK_SKETCH_WARP2=1.  Off by default: at C2 it reads the intermediate once
-// (4.3 GB per 256 columns) but takes 2.67 ms against ~2.5 ms for
-// transform_pass2_kernel -- 8 warps per SM (255 registers with the stage
-// 15..19 twiddles resident, some spilled) leave shared-memory latency
-// exposed (4.4 ms before the per-class sampled-row cache).  Measured and
-// dropped on the way: one class per warp (3.1 ms; each column re-reads the
-// 16 MB of class twiddle rows), 4-class CTAs class-group major (3.4 ms) or
-// two per SM (5.0 ms; 64-byte runs over-fetch the intermediate 1.5x).
-// build_inputs orders destination rows to match.
+// FSTK_SKETCH_WARP2=1.  Off by default: it reads the intermediate once
+// (4.36 GB per 256 columns) but takes 2.24-2.35 ms against 2.3 ms for
+// transform_pass2_kernel (see the kernel's header).  Measured and dropped on
+// the way (round 1/2): one class per warp (3.1 ms; each column re-reads the
+// 16 MB of class twiddle rows), 4-class CTAs (3.4-5.0 ms), 8-class CTAs with
+// the stage 15..19 twiddles in registers (2.67 ms at 8 warps per SM).
+// build_inputs orders destination rows to match (class, then t).
 static bool warp_last_pass(int kind, uint64_t n) {
   static const bool on = [] {
     const char* e = std::getenv("FSTK_SKETCH_WARP2");
@@ -296,7 +294,7 @@ struct PassParams {
   const double* post_im;    // per destination row (DCT: sin)
   const double* post_c;     // per destination row (DCT: c_k)
   double scale;             // plan.scale (sqrt(q_pad/S)) or 1
-  double post_c0, post_ck;  // DCT normalisation c_0, c_k (dct_post; warp_pass2_kernel)
+  double post_c0, post_ck;  // DCT normalisation c_0, c_k (dct_post; pair_pass2_kernel)
   double inv_sqrt_n;        // 1/sqrt(n) (FFT, WHT)
   int64_t row_lo, row_hi;   // destination rows owned by this shard
   int64_t im_off;           // FFT: rows of the Re block in A (Im block follows)
@@ -310,7 +308,7 @@ struct PassParams {
   int ct_rounds;            // L == 10: compile-time stage rounds (radix_round_ct)
   int fuse_last;            // compact complex last pass: stage 9 evaluated in the store
   int swap;                 // staging in x's layout, alternating with x (see kernel)
-  // warp_pass2_kernel (last pass of q_pad = 2^20): per-position-class twiddle
+  // pair_pass2_kernel (last pass of q_pad = 2^20): per-position-class twiddle
   // rows and the sampled elements of each class in destination-row order.
   const double2* tw2;       // 1024 rows of 1023 twiddles (warp_pass2_twiddles)
   const int32_t* lo_start;  // class lo owns destination rows [lo_start[lo], lo_start[lo+1])
@@ -981,9 +979,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
 // ascending t (build_inputs), so a ballot over each register's sampled flags
 // compacts the sampled outputs (~S / q_pad of them) into consecutive
 // shared-memory slots, from which they are post-rotated (DCT) or split (FFT)
-// and stored row-contiguously while the next column's loads are in flight.
+// and stored row-contiguously; the next column's loads are issued after them
+// (a spill reload behind the 16 outstanding sector loads waits for DRAM).
 // Same butterflies and epilogue as transform_pass2_kernel, in the same order,
 // so A is bit-identical.
+// Measured at C2 (profiles/ncu_sketch_r02.txt): 2.24-2.35 ms per 256 columns
+// against 2.3 ms for transform_pass2_kernel, so it stays opt-in
+// (FSTK_SKETCH_WARP2=1): with 10 warps per SM (168 registers, 209 KB) the
+// three shared-memory round trips and the pair / cluster barriers leave the
+// fp64 pipe at 37%.
 constexpr int kPp2Pairs = 5;                   // columns in flight per CTA
 constexpr int kPp2Warps = 2 * kPp2Pairs;
 constexpr int kPp2Buf = 1024;                  // double2 per warp
@@ -1000,18 +1004,13 @@ __device__ __forceinline__ void pair_barrier(int pair) {
 }
 
 // One 32-byte sector: the elements of classes lo0 and lo0 + 1 at one t.
-template <int LD>
+// One 32-byte sector: the elements of classes lo0 and lo0 + 1 at one t.  Normal
+// L2 eviction priority: the neighbouring class pairs of the cluster take the
+// rest of the 128-byte line from L2 (evict_first re-fetched it from DRAM).
 __device__ __forceinline__ void ld_sector(const double2* p, double2& c0, double2& c1) {
-#define FSTK_LD256(Q)                                                          \
-  asm volatile("ld.global.L1::no_allocate." Q ".v4.b64 {%0,%1,%2,%3}, [%4];"   \
-               : "=d"(c0.x), "=d"(c0.y), "=d"(c1.x), "=d"(c1.y)                \
-               : "l"(p))
-  if constexpr (LD == 0) FSTK_LD256("L2::evict_first");
-  if constexpr (LD == 1) FSTK_LD256("L2::evict_normal");
-  if constexpr (LD == 2) FSTK_LD256("L2::evict_last");
-  if constexpr (LD == 3) FSTK_LD256("L2::evict_normal.L2::128B");
-  if constexpr (LD == 4) FSTK_LD256("L2::evict_last.L2::128B");
-#undef FSTK_LD256
+  asm volatile("ld.global.L1::no_allocate.L2::evict_normal.v4.b64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(c0.x), "=d"(c0.y), "=d"(c1.x), "=d"(c1.y)
+               : "l"(p));
 }
 
 __device__ __forceinline__ void butterfly(double2& lo, double2& hi, const double2 w) {
@@ -1026,7 +1025,6 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
-template <int LD>
 __global__ void __cluster_dims__(kPp2Cluster, 1, 1) __launch_bounds__(kPp2Warps * 32, 1)
 pair_pass2_kernel(const PassParams P, int ncols_batch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1084,7 +1082,7 @@ pair_pass2_kernel(const PassParams P, int ncols_batch) {
   if (cc < ncols_batch) {
     const double2* src = src0 + static_cast<int64_t>(cc) * P.n;
 #pragma unroll
-    for (int b = 0; b < 16; ++b) ld_sector<LD>(src + static_cast<int64_t>(b) * 1024, v[b], v[16 + b]);
+    for (int b = 0; b < 16; ++b) ld_sector(src + static_cast<int64_t>(b) * 1024, v[b], v[16 + b]);
   }
   cluster_arrive_relaxed();
   for (int rnd = 0; rnd < rounds; ++rnd, cc += cstep) {
@@ -1154,13 +1152,15 @@ pair_pass2_kernel(const PassParams P, int ncols_batch) {
       }
     }
     __syncwarp();
-    cluster_wait();  // every CTA of the cluster has issued this round's loads
-    if (cc + cstep < ncols_batch) {
-      const double2* src = src0 + static_cast<int64_t>(cc + cstep) * P.n;
+    auto prefetch = [&] {
+      cluster_wait();  // every CTA of the cluster has issued this round's loads
+      if (cc + cstep < ncols_batch) {
+        const double2* src = src0 + static_cast<int64_t>(cc + cstep) * P.n;
 #pragma unroll
-      for (int b = 0; b < 16; ++b) ld_sector<LD>(src + static_cast<int64_t>(b) * 1024, v[b], v[16 + b]);
-    }
-    cluster_arrive_relaxed();
+        for (int b = 0; b < 16; ++b) ld_sector(src + static_cast<int64_t>(b) * 1024, v[b], v[16 + b]);
+      }
+      cluster_arrive_relaxed();
+    };
     // ---- sampled outputs of class lo: consecutive destination rows
     if (!P.packed) {
       double* out = ((col == P.R) ? P.b : P.A + P.lda * col) + (first - P.row_lo);
@@ -1198,6 +1198,7 @@ pair_pass2_kernel(const PassParams P, int ncols_batch) {
         }
       }
     }
+    prefetch();
   }
   cluster_wait();
 }
@@ -1418,11 +1419,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<3, 12>));
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<4, 8>));
     attr_w(reinterpret_cast<const void*>(warp_pass1_kernel<4, 12>));
-    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<0>));
-    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<1>));
-    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<2>));
-    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<3>));
-    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel<4>));
+    attr_w(reinterpret_cast<const void*>(pair_pass2_kernel));
   });
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1532,7 +1529,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
       const int dt = (P.src == SRC_TABLES && (J.d == 3 || J.d == 4)) ? J.d : 0;
       const int nb = static_cast<int>(bc);
       // Warp-level first pass (warp_pass1_kernel): complex transforms with
-      // a design-table source and a later pass, and warp_pass2_kernel for
+      // a design-table source and a later pass, and pair_pass2_kernel for
       // the last pass of q_pad = 2^20 (FSTK_SKETCH_WARP=0 disables both;
       // FSTK_SKETCH_WARP=8 runs 8 warps per CTA instead of 12).
       static const int warp_mode = [] {
@@ -1548,17 +1545,7 @@ static void run_sketch(int device, const SketchJob& J, cudaStream_t s) {
         const int64_t ysplit = std::max<int64_t>(1, std::min<int64_t>(ceil_div(static_cast<int64_t>(nb), kPp2Pairs),
                                                                       ceil_div(int64_t(sms) * 7, 512)));
         dim3 pgrid(512, static_cast<unsigned>(ysplit));
-        static const int ldm = [] {
-          const char* e = std::getenv("FSTK_PP2_LD");
-          return e ? std::atoi(e) : 0;
-        }();
-        switch (ldm) {
-          case 1: pair_pass2_kernel<1><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
-          case 2: pair_pass2_kernel<2><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
-          case 3: pair_pass2_kernel<3><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
-          case 4: pair_pass2_kernel<4><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
-          default: pair_pass2_kernel<0><<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb); break;
-        }
+pair_pass2_kernel<<<pgrid, kPp2Warps * 32, kPp2Smem, s>>>(P, nb);
         check_launch("pair_pass2_kernel");
         continue;
       }
@@ -1720,7 +1707,7 @@ static void build_inputs(int kind, uint64_t n, uint64_t q_w, const std::vector<d
     const uint64_t stride = uint64_t(1) << s0;
     const uint64_t G = std::min<uint64_t>(static_cast<uint64_t>(pass_group(s0)), stride);
     const uint64_t lo_blocks = stride / G;
-    const bool wl = warp_last_pass(kind, n);  // warp_pass2_kernel: class lo, then t
+    const bool wl = warp_last_pass(kind, n);  // pair_pass2_kernel: class lo, then t
     auto order_key = [&](uint64_t k) {
       if (wl) return ((k & 1023) << 32) | (k >> 10);
       const uint64_t low = k & (stride - 1);
