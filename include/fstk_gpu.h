@@ -129,7 +129,9 @@ int32_t fstk_gpu_abi_version(void);
 int32_t fstk_gpu_device_count(void);
 /* Kernel launches issued by this process so far (evidence counter). */
 uint64_t fstk_gpu_launch_count(void);
-/* Large-block device cache (blocks >= 256 MB; see fstk_common.cuh).  policy
+/* Device block cache (see fstk_common.cuh): released blocks >= 256 MB are
+ * reused by size class, smaller ones in power-of-two buckets (<= 4 GB in
+ * total), instead of going through cudaFree/cudaMalloc each time.  policy
  * 0 = off; 1 = per session (default): blocks are reused only while a refit
  * session is open and all go back to the driver when the last one ends, so
  * reestimate_core returns holding no idle HBM; 2 = persistent across

@@ -327,12 +327,13 @@ inline void device_free(void* p, size_t bytes) {
       cap = total / 4 * 3;
     }
     DeviceCache& c = device_cache();
-    std::unique_lock<std::mutex> lk(c.mu);
     const bool keep = bytes <= cap;
+    // cudaFree would have synchronised the device; a cached block must
+    // likewise be idle before the next owner's stream touches it.  (Outside
+    // the cache's lock: other host threads keep allocating meanwhile.)
+    if (keep) cudaDeviceSynchronize();
+    std::unique_lock<std::mutex> lk(c.mu);
     if (keep) {
-      // cudaFree would have synchronised the device; a cached block must
-      // likewise be idle before the next owner's stream touches it.
-      cudaDeviceSynchronize();
       // Least recently released blocks go first, so the latest session's
       // working set is what stays cached.  Large blocks are capped per
       // device, small ones by their total.

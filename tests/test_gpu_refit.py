@@ -379,3 +379,23 @@ def test_cached_device_blocks_reused_bit_identically():
     c, _ = F.reestimate_core(m, pts, vals, seed=54, sample_rows=131_072)
     assert np.array_equal(a.core, c.core)
     assert _lib.trim_device_cache(-1) == 0
+
+
+def test_pair_last_pass_variant_bitexact():
+    # The opt-in barrier-free last pass (pair_pass2_kernel, FSTK_SKETCH_WARP2=1:
+    # read once per process) must reproduce the oracle's A and b bit for bit
+    # like the default kernel: the q_pad = 2^20 sketch tests (DCT and FFT, full
+    # and zero-padded working sets, 4-mode model) and a column-sharded sketch
+    # re-run in a child process with the flag set.
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FSTK_SKETCH_WARP2="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q",
+                        os.path.join(root, "tests", "test_gpu_refit.py"),
+                        os.path.join(root, "tests", "test_gpu_columns.py"),
+                        "-k", "two_pass_1m or column"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
