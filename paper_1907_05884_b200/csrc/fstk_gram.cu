@@ -624,7 +624,8 @@ bool gram_scheme_crt() {
 template <class SRC>
 static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, double* gram,
                                       double beta, int ns, cudaStream_t s, int device,
-                                      GramScratch& sc, int64_t ldg = -1, bool negate = false) {
+                                      GramScratch& sc, int64_t ldg = -1, bool negate = false,
+                                      cudaEvent_t first_block_done = nullptr) {
   if (ldg < 0) ldg = n;
   require(ns >= 4 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: 4..7 plane-equivalents");
   const int k = 7 * ns - 1;
@@ -676,6 +677,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * (syrk ? 1 : 4)));
   w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), wal), np);
   if (w > block_cap && np > block_cap) w = round_up(block_cap, wal);
+  sc.last_block_w = (syrk && syrk_fused()) ? 0 : w;  // fused: no per-block order to hook into
   sc.X.ensure(static_cast<size_t>(nm) * kp * np);
   if (syrk && syrk_fused()) {
     sc.C8.ensure(syrk_crt_scratch_bytes(nm, device));
@@ -717,6 +719,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   launch_crt_fold<NMV, int8_t>(c8, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
         FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
 #undef FSTK_CRT_FOLD
+        if (first_block_done && c0 == 0 && s0 + kp >= rows) FSTK_CUDA(cudaEventRecord(first_block_done, s));
       }
     } else {
       LtState& st = lt_state(device);
@@ -733,6 +736,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   launch_crt_fold<NMV, int32_t>(sc.C.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
         FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
 #undef FSTK_CRT_FOLD
+        if (first_block_done && c0 == 0 && s0 + kp >= rows) FSTK_CUDA(cudaEventRecord(first_block_done, s));
       }
     }
     first = false;
@@ -746,8 +750,16 @@ double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, do
 }
 
 double gram_update_crt(const double* T, int64_t ldt, int64_t rows, int n, double* G, int64_t ldg,
-                       int ns, cudaStream_t s, int device, GramScratch& sc) {
-  return gram_accumulate_crt_src(DenseSrc{T, ldt}, rows, n, G, 1.0, ns, s, device, sc, ldg, true);
+                       int ns, cudaStream_t s, int device, GramScratch& sc,
+                       cudaEvent_t first_block_done, int64_t* first_block_cols) {
+  // The first column block is min(2048, n) columns wide (block_cap) unless the
+  // scratch budget narrows it; a caller overlapping work with the rest of the
+  // update must wait for the whole update when the block is narrower than it needs.
+  if (first_block_cols) *first_block_cols = 0;
+  const double ops = gram_accumulate_crt_src(DenseSrc{T, ldt}, rows, n, G, 1.0, ns, s, device, sc, ldg, true,
+                                             first_block_done);
+  if (first_block_cols) *first_block_cols = sc.last_block_w;
+  return ops;
 }
 
 double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n, double* gram,

@@ -201,6 +201,7 @@ struct GramScratch {
   DevBuf<int> ex;          // per-column exponents of the current segment
   DevBuf<uint8_t> ws;      // cuBLASLt workspace
   int64_t kp = 0;          // segment rows, fixed by the first call
+  int64_t last_block_w = 0;  // column-block width of the latest CRT call (0: no block order)
 };
 int gram_slices();                      // 0 = native fp64 DSYRK/DGEMM Gram
 // Int8 GEMM engine of the CRT Gram: 1 = the hand-written tcgen05 SYRK
@@ -250,8 +251,13 @@ struct DesignSpec {
 // G (lower triangle, n x n inside a matrix of leading dimension ldg) -= T^T T
 // for T = rows x n (column-major, ldt), through the CRT int8 Gram at `slices`
 // plane-accuracy: the trailing update of the blocked Cholesky (chol_crt).
+// first_block_done (optional) is recorded on s once the update's first column
+// block (*first_block_cols columns wide, 0 when the engine has no block order)
+// has been folded into G: the blocked Cholesky's lookahead starts the next
+// panel there.
 double gram_update_crt(const double* T, int64_t ldt, int64_t rows, int n, double* G, int64_t ldg,
-                       int slices, cudaStream_t s, int device, GramScratch& sc);
+                       int slices, cudaStream_t s, int device, GramScratch& sc,
+                       cudaEvent_t first_block_done = nullptr, int64_t* first_block_cols = nullptr);
 // The sliced (CRT) Gram of those rows without materialising them.
 bool gram_scheme_crt();
 double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n, double* gram,

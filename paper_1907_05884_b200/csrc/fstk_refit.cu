@@ -2844,8 +2844,32 @@ __global__ void transpose_panel_kernel(const double* __restrict__ L, int64_t ldl
 // Returns false when a diagonal block is not positive definite.
 static bool chol_crt(cublasHandle_t blas, cusolverDnHandle_t solver, double* G, int n, int nb,
                      int slices, cudaStream_t s, int device) {
-  cublasSetStream(blas, s);
-  cusolverDnSetStream(solver, s);
+  // Lookahead: the trailing update runs on s in column blocks, the next
+  // panel's columns first; once those are folded (an event from
+  // gram_update_crt) the next panel's potrf, DTRSM and transpose run on a
+  // second stream beside the rest of the update (fp64 pipe and DTRSM beside
+  // int8 MMAs and HBM-bound folds).  FSTK_CHOL_LOOKAHEAD=0 keeps one stream.
+  static const bool lookahead = [] {
+    const char* e = std::getenv("FSTK_CHOL_LOOKAHEAD");
+    return !(e && std::atoi(e) == 0);
+  }();
+  struct Side {
+    cudaStream_t st = nullptr;
+    cudaEvent_t panel = nullptr, block = nullptr, done = nullptr;
+    ~Side() {
+      if (panel) cudaEventDestroy(panel);
+      if (block) cudaEventDestroy(block);
+      if (done) cudaEventDestroy(done);
+      if (st) cudaStreamDestroy(st);
+    }
+  } side;
+  if (lookahead) {
+    FSTK_CUDA(cudaStreamCreateWithFlags(&side.st, cudaStreamNonBlocking));
+    FSTK_CUDA(cudaEventCreateWithFlags(&side.panel, cudaEventDisableTiming));
+    FSTK_CUDA(cudaEventCreateWithFlags(&side.block, cudaEventDisableTiming));
+    FSTK_CUDA(cudaEventCreateWithFlags(&side.done, cudaEventDisableTiming));
+  }
+  const cudaStream_t sp = lookahead ? side.st : s;  // panel stream
   const int npan = (n + nb - 1) / nb;
   int lwork = 0;
   if (cusolverDnDpotrf_bufferSize(solver, CUBLAS_FILL_MODE_LOWER, nb, G, n, &lwork) !=
@@ -2854,26 +2878,66 @@ static bool chol_crt(cublasHandle_t blas, cusolverDnHandle_t solver, double* G, 
   DevBuf<double> work(std::max(lwork, 1));
   DevBuf<int> dinfo(npan);
   FSTK_CUDA(cudaMemsetAsync(dinfo.p, 0, npan * sizeof(int), s));
-  DevBuf<double> T(static_cast<size_t>(nb) * std::max(n - nb, 1));
+  // Two transposed panels: the update of panel p still reads T[p & 1] while
+  // the lookahead writes panel p + 1's.
+  const size_t tsz = static_cast<size_t>(nb) * std::max(n - nb, 1);
+  DevBuf<double> T(lookahead ? 2 * tsz : tsz);
   GramScratch sc;
   const double one = 1.0;
-  for (int p = 0; p < npan; ++p) {
+  cublasSetStream(blas, sp);
+  cusolverDnSetStream(solver, sp);
+  if (lookahead) {  // the panel stream starts after what s holds so far (the copy of G)
+    FSTK_CUDA(cudaEventRecord(side.done, s));
+    FSTK_CUDA(cudaStreamWaitEvent(sp, side.done, 0));
+  }
+  // Panel p: potrf of the diagonal block, DTRSM of the block column below it,
+  // and its transpose, on the panel stream.
+  auto panel = [&](int p) {
     const int i0 = p * nb, b = std::min(nb, n - i0), rest = n - i0 - b;
     double* Gii = G + static_cast<int64_t>(i0) * n + i0;
     if (cusolverDnDpotrf(solver, CUBLAS_FILL_MODE_LOWER, b, Gii, n, work.p, lwork, dinfo.p + p) !=
         CUSOLVER_STATUS_SUCCESS)
       fail(FSTK_E_COMPUTE, "potrf failed");
-    if (rest == 0) break;
+    if (rest == 0) return;
     double* A21 = Gii + b;
     if (cublasDtrsm(blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
                     CUBLAS_DIAG_NON_UNIT, rest, b, &one, Gii, n, A21, n) != CUBLAS_STATUS_SUCCESS)
       fail(FSTK_E_COMPUTE, "cublasDtrsm failed");
     dim3 tg(static_cast<unsigned>(ceil_div(rest, 32)), static_cast<unsigned>(ceil_div(b, 32)));
-    transpose_panel_kernel<<<tg, dim3(32, 8), 0, s>>>(A21, n, rest, b, T.p);
+    transpose_panel_kernel<<<tg, dim3(32, 8), 0, sp>>>(A21, n, rest, b, T.p + (lookahead ? (p & 1) * tsz : 0));
     check_launch("transpose_panel_kernel");
-    gram_update_crt(T.p, b, b, rest, A21 + static_cast<int64_t>(b) * n, n, slices, s, device, sc);
-    count_launch(3);
+    count_launch(2);
+  };
+  panel(0);
+  for (int p = 0; p < npan; ++p) {
+    const int i0 = p * nb, b = std::min(nb, n - i0), rest = n - i0 - b;
+    if (rest == 0) break;
+    double* A22 = G + static_cast<int64_t>(i0 + b) * n + i0 + b;
+    const double* Tp = T.p + (lookahead ? (p & 1) * tsz : 0);
+    if (!lookahead) {
+      gram_update_crt(Tp, b, b, rest, A22, n, slices, s, device, sc);
+      count_launch();
+      panel(p + 1);
+      continue;
+    }
+    FSTK_CUDA(cudaEventRecord(side.panel, sp));
+    FSTK_CUDA(cudaStreamWaitEvent(s, side.panel, 0));  // panel p factored and transposed
+    int64_t bw = 0;
+    gram_update_crt(Tp, b, b, rest, A22, n, slices, s, device, sc, side.block, &bw);
+    count_launch();
+    // The next panel needs its nb columns of the trailing matrix final: the
+    // first block when that is wide enough, else the whole update.
+    const int nextb = std::min(nb, rest);
+    if (bw < nextb) FSTK_CUDA(cudaEventRecord(side.block, s));
+    FSTK_CUDA(cudaStreamWaitEvent(sp, side.block, 0));
+    panel(p + 1);
   }
+  if (lookahead) {  // s continues after the last panel
+    FSTK_CUDA(cudaEventRecord(side.panel, sp));
+    FSTK_CUDA(cudaStreamWaitEvent(s, side.panel, 0));
+  }
+  cublasSetStream(blas, s);
+  cusolverDnSetStream(solver, s);
   std::vector<int> hinfo(npan);
   FSTK_CUDA(cudaMemcpyAsync(hinfo.data(), dinfo.p, npan * sizeof(int), cudaMemcpyDeviceToHost, s));
   FSTK_CUDA(cudaStreamSynchronize(s));
