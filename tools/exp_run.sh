@@ -1,7 +1,4 @@
-# scratch experiment driver (gpurun): bench refit with the Cholesky lookahead on/off
-for la in 0 1; do FSTK_CHOL_LOOKAHEAD=$la FSTK_DEBUG_TIMING=1 python bench.py --steps 3 --warmup 3 --no-cpu --no-refit-none --refit-reps 6 > gpurun_out/bench_la$la.log 2> gpurun_out/bench_la$la.err; grep -E "chol_crt" gpurun_out/bench_la$la.err | tr '\n' ' '; python - <<PY
-import json
-l=[x for x in open('gpurun_out/bench_la$la.log') if x.startswith('{')][-1]
-d=json.loads(l); print('\nlookahead=$la', d['refit']['samples_s'], [s['solve'] for s in d['refit']['sample_stages_s']])
-PY
-done
+# scratch experiment driver (gpurun): the other BASELINE configs at full size (round-2 records)
+python bench.py --config C3 --points 134217728 --steps 5 --warmup 3 --no-cpu --no-refit > gpurun_out/bench_c3.log 2>&1; tail -c 300 gpurun_out/bench_c3.log; echo
+python bench.py --config C4 --points 268435456 --steps 3 --warmup 3 --no-cpu --no-refit-none > gpurun_out/bench_c4.log 2>&1; tail -c 300 gpurun_out/bench_c4.log; echo
+python bench.py --config C1 --no-cpu > gpurun_out/bench_c1.log 2>&1; tail -c 300 gpurun_out/bench_c1.log; echo
