@@ -46,11 +46,11 @@ namespace fstk_gpu {
 namespace {
 
 constexpr int kDigitMax = 64;
-constexpr int kDefaultSlices = 4;
+constexpr int kDefaultSlices = 3;
 constexpr int kMaxSlices = 7;
 std::atomic<int> g_slices{-1};
 
-int clamp_slices(int v) { return v <= 0 ? 0 : std::min(std::max(v, 4), kMaxSlices); }
+int clamp_slices(int v) { return v <= 0 ? 0 : std::min(std::max(v, 3), kMaxSlices); }
 
 struct LtState {
   cublasLtHandle_t lt = nullptr;
@@ -483,6 +483,14 @@ void launch_crt_fold(const CT* C, int64_t cstride, int64_t m, int64_t wn, int64_
 
 }  // namespace
 
+// Bits per entry of a CRT Gram level.  Levels 4..7 carry the accuracy of that
+// many 7-bit planes (k = 7 level - 1).  Level 3 is the most 8 moduli carry
+// over 32,768-row segments, k = 23: its Gram costs 8/9 of level 4's, and as a
+// preconditioner it costs the C2 refinement no extra step (first correction
+// 3.3e-3 instead of 2.1e-4, contraction 5e-6 per step; tools/refine_time.py).
+int crt_level_bits(int level) { return level == 3 ? 23 : 7 * level - 1; }
+
+
 namespace {
 std::atomic<int> g_engine{-1};
 }
@@ -533,6 +541,7 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
   if (t_lo == 2 && gram_scheme_crt())
     return gram_accumulate_crt(A, lda, rows, n, gram, beta, ns, s, device, sc);
   double ops = 0.0;
+  if (ns == 3) ns = 4;  // level 3 exists in the CRT scheme only
   require(ns >= 4 && ns <= kMaxSlices, FSTK_E_PARAMETER, "sliced Gram: 4..9 digit planes");
   require(t_lo >= 2 && t_lo <= ns + 1, FSTK_E_PARAMETER, "sliced Gram: bad plane range");
   const int nt = ns + 2 - t_lo;  // plane sums t_lo..ns+1
@@ -627,8 +636,8 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
                                       GramScratch& sc, int64_t ldg = -1, bool negate = false,
                                       cudaEvent_t first_block_done = nullptr) {
   if (ldg < 0) ldg = n;
-  require(ns >= 4 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: 4..7 plane-equivalents");
-  const int k = 7 * ns - 1;
+  require(ns >= 3 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: levels 3..7");
+  const int k = crt_level_bits(ns);
   // SYRK engine: 256-column tiles and 128-byte K blocks (zero padding).  It
   // folds each tile in its epilogue while the next tile's MMAs run, which
   // hides the fold only when a tile's K loop is long: short updates (the
@@ -661,13 +670,14 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   // does not change what a call computes beyond fp64 accumulation order).
   // Sizing for the level-7 count on every call shrank C4's segments to ~20k
   // rows next to its 137 GB sketch (Gram 2.8 s instead of 2.3 s).
-  const int nm_need = crt_moduli(k, kmax);
+  const int nm_need = std::max(8, crt_moduli(k, kmax));
   const int64_t have = static_cast<int64_t>(sc.X.n);
   const int64_t budget = std::min<int64_t>(int64_t(24) << 30, (static_cast<int64_t>(free_b) + have) / 3);
   kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, budget / (nm_need * np)));
   kmax &= ~(kalign - 1);
   const int64_t kp = std::min<int64_t>(kmax, round_up(rows, kalign));
-  const int nm = crt_moduli(k, kp);
+  // (Short segments would need fewer; the kernels are instantiated from 8.)
+  const int nm = std::max(8, crt_moduli(k, kp));
   require(nm >= 8 && nm <= 17, FSTK_E_COMPUTE, "internal: CRT modulus count out of range");
   static const int64_t block_cap = [] {
     const char* e = std::getenv("FSTK_GRAM_BLOCK");

@@ -204,6 +204,7 @@ struct GramScratch {
   int64_t last_block_w = 0;  // column-block width of the latest CRT call (0: no block order)
 };
 int gram_slices();                      // 0 = native fp64 DSYRK/DGEMM Gram
+int crt_level_bits(int level);          // bits per entry of CRT level 3..7
 // Int8 GEMM engine of the CRT Gram: 1 = the hand-written tcgen05 SYRK
 // (fstk_syrk.cu, default), 2 = cuBLASLt IMMA GEMMs (comparison).
 int gram_engine();
@@ -237,6 +238,7 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
                               double beta, int slices, int t_lo, cudaStream_t s, int device,
                               GramScratch& sc);
 constexpr int kGramUpgradeSlices = 7;   // escalation target before the native Gram
+constexpr double kDoneFloor = 1e-14;    // refinement: extrapolated remaining ||dx||/||x|| that ends it
 // transform = "none" design rows A[r][ell] = scale ((u0 u1) u2 ...)(row0 + r)
 // generated from mode tables (column j_k of mode k at toff[k] + j_k ldt).
 struct DesignSpec {

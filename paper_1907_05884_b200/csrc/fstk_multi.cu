@@ -433,6 +433,8 @@ int32_t reestimate_core_multi(const fstk_gpu_model* m, const double* points, con
       stage(fstk_gpu_refit_apply(rf[0], sv[0].p, xs[0].p, &step, &gerr[0]), gerr[0]);
       ++steps;
       if (step <= 1e-15) break;
+      // converged by extrapolation (see fstk_gpu_refit_solve)
+      if (it >= 1 && step < 0.1 * prev && step * (step / prev) <= kDoneFloor) break;
       constexpr double kStallFloor = 1e-11;
       const bool flat = it >= 1 && step > 0.5 * prev;
       if (flat && step <= kStallFloor) break;

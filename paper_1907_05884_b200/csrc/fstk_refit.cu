@@ -2672,8 +2672,8 @@ int32_t fstk_gpu_refit_normal_equations_level(fstk_gpu_refit* rf, int32_t slices
                                               fstk_gpu_error* err) {
   return guarded(err, [&] {
     require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
-    require(slices == 0 || (slices >= 4 && slices <= 7), FSTK_E_PARAMETER,
-            "normal_equations_level: slices must be 0 (native) or 4..7");
+    require(slices == 0 || (slices >= 3 && slices <= 7), FSTK_E_PARAMETER,
+            "normal_equations_level: slices must be 0 (native) or 3..7");
     normal_equations(rf, gram, rhs, info, slices);
   });
 }
@@ -2695,8 +2695,8 @@ int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t
   return guarded(err, [&] {
     require(a && gram, FSTK_E_PARAMETER, "null argument");
     require(n > 0 && rows > 0 && lda >= rows, FSTK_E_SHAPE, "gram: need n > 0, rows > 0, lda >= rows");
-    require(slices == 0 || (slices >= 4 && slices <= 7), FSTK_E_PARAMETER,
-            "gram: slices must be 0 (native fp64) or 4..7");
+    require(slices == 0 || (slices >= 3 && slices <= 7), FSTK_E_PARAMETER,
+            "gram: slices must be 0 (native fp64) or 3..7");
     require((rows <= INT32_MAX && lda <= INT32_MAX) || slices > 0, FSTK_E_SHAPE,
             "gram: native path needs rows, lda < 2^31");
     DeviceGuard dg(device);
@@ -3347,6 +3347,11 @@ int32_t fstk_gpu_refit_solve(fstk_gpu_refit* rf, const double* gram_in, const do
         rc(fstk_gpu_refit_apply(rf, sv.p, x.p, &step, err));
         ++steps;
         if (step <= 1e-15) break;
+        // Converged by extrapolation: contracting by rho = step / prev < 0.1,
+        // the error left after this step is ~ rho * step; once that is below
+        // kDoneFloor (under the rounding floor of ||dx|| / ||x||, ~2e-13 at
+        // C2) another step over A could only confirm it.
+        if (it >= 1 && step < 0.1 * prev && step * (step / prev) <= kDoneFloor) break;
         // Stagnation at the rounding floor (||dx||/||x|| ~ cond(A) eps, about
         // 1e-13 at C2) is convergence.  Above kStallFloor: not contracting,
         // contracting slower than 10x per step on a sliced Gram, or out of

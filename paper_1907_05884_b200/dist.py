@@ -64,6 +64,7 @@ def evaluate_sharded(model, points, rank: int, world: int):
 
 
 STALL_FLOOR = 1e-11  # ||dx||/||x|| below which a flat refinement has converged
+DONE_FLOOR = 1e-14   # extrapolated remaining ||dx||/||x|| that ends the refinement (kDoneFloor)
 UPGRADE_SLICES = 7   # escalation target of a sliced Gram before the native one
 
 
@@ -202,6 +203,10 @@ def refine_distributed(sess, gram, rhs, max_iter: int = 8, group=None, used=None
         step = _max_over_ranks_f(sess.apply(s, x), group)
         sess.info.refine_steps += 1
         if step <= 1e-15:
+            break
+        # Converged by extrapolation: contracting by rho = step / prev < 0.1, the
+        # error left is ~ rho * step (see fstk_gpu_refit_solve).
+        if it >= 1 and step < 0.1 * prev and step * (step / prev) <= DONE_FLOOR:
             break
         # Flat at the rounding floor is convergence (see fstk_gpu_refit_solve).
         flat = it >= 1 and step > 0.5 * prev

@@ -54,7 +54,8 @@ def _info_dict(info: ReestimateInfo) -> dict:
 
 def gram_slices(slices: int | None = None) -> int:
     """Gram arithmetic of this process: returns the current precision level
-    (the accuracy of that many 7-bit planes, 4..7; 0 = native fp64 Gram); with
+    (the accuracy of that many 7-bit planes, 4..7; 3 = 23-bit entries on 8 CRT
+    moduli, the default; 0 = native fp64 Gram); with
     `slices` given, sets it first and returns the previous value.  See
     fstk_gram.cu."""
     return int(lib().fstk_gpu_gram_slices(-1 if slices is None else int(slices)))

@@ -123,9 +123,21 @@ def _refine(sess, used=None):
 
 
 def test_refine_converges_at_rounding_floor_without_escalation():
-    s = _ScriptedSession([True], [1e-9, 2e-13, 1.5e-13])
+    # Contracting 125x in the second step, the extrapolated remainder (6e-14)
+    # stays above the done floor; the third step is flat below the stall
+    # floor: converged at the rounding floor.
+    s = _ScriptedSession([True], [1e-9, 8e-12, 6e-12])
     _refine(s)
     assert "native" not in s.calls and "upgrade7" not in s.calls and s.info.refine_steps == 3
+
+
+def test_refine_stops_by_extrapolation():
+    # rho = 2e-4: the error left after the second step (~4e-17) is below the
+    # done floor, so no third pass over A is made.
+    s = _ScriptedSession([True], [1e-9, 2e-13, 1.5e-13])
+    _refine(s)
+    assert "native" not in s.calls and "upgrade7" not in s.calls and s.info.refine_steps == 2
+    assert s.calls[-1] == "certify"
 
 
 def test_refine_not_pd_escalates_upgrade_then_native():
@@ -176,9 +188,10 @@ def test_refine_native_not_pd_goes_to_qr():
 
 
 def test_refine_fast_contraction_keeps_five_planes():
+    # 2e5x per step: the second step's extrapolated remainder ends it.
     s = _ScriptedSession([True], [1e-6, 1e-11 * 0.5, 1e-16])
     _refine(s)
-    assert s.calls.count("apply") == 3 and "upgrade7" not in s.calls
+    assert s.calls.count("apply") == 2 and "upgrade7" not in s.calls
 
 
 def _gloo_refine_worker(rank, world, port, q):

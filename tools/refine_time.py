@@ -36,11 +36,14 @@ for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
 
     t0 = time.perf_counter()
     t("factor", lambda: s.factor(g, rhs, x))
-    for it in range(6):
+    steps = []
+    for it in range(8):
         t(f"correction{it}", lambda: s.correction(x, sv))
         step = t(f"apply{it}", lambda: s.apply(sv, x))
-        if step <= 1e-11:
+        steps.append(step)
+        if step <= 1e-11 or (it >= 1 and step > 0.5 * steps[-2]):
             break
+    print("   steps ||dx||/||x||: " + " ".join(f"{v:.2e}" for v in steps), flush=True)
     t("certify", lambda: s.certify(g))
     tot = time.perf_counter() - t0
     print(f"rep {rep}: total {tot:.3f} s; " + ", ".join(f"{n} {v * 1e3:.1f} ms" for n, v in marks), flush=True)
