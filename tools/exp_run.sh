@@ -1,14 +1,4 @@
-# scratch experiment driver (gpurun): level-3 Gram default + extrapolated stop: parity suite, C4/C5 refits
-python -m pytest tests -m gpu -x -q > gpurun_out/gputests_c.log 2>&1; tail -n 3 gpurun_out/gputests_c.log
-python bench.py --config C4 --no-cpu --no-refit-none --steps 3 --warmup 3 > gpurun_out/bench_c4b.log 2>&1; python - <<'PY'
-import json
-l=[x for x in open('gpurun_out/bench_c4b.log') if x.startswith('{')][-1]
-d=json.loads(l)
-r=d['refit']; print('C4', r['seconds'], r['samples_s'], 'hot', r['hot_path_seconds'], 'steps', r['refine_steps'], 'lvl', r['gram_slices'], r['sample_stages_s'][0], 'res', r['residual_after'])
-PY
-python bench.py --config C5 --no-cpu --no-refit-none --steps 3 --warmup 3 > gpurun_out/bench_c5b.log 2>&1; python - <<'PY'
-import json
-l=[x for x in open('gpurun_out/bench_c5b.log') if x.startswith('{')][-1]
-d=json.loads(l)
-r=d['refit']; print('C5', r['seconds'], r['samples_s'], 'steps', r['refine_steps'], 'lvl', r['gram_slices']); print(d.get('refit_fields'))
-PY
+# scratch experiment driver (gpurun): final records: default bench, reference arm, launch list
+python bench.py > gpurun_out/bench_d.log 2>&1; tail -c 300 gpurun_out/bench_d.log; echo
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_d.log 2>&1; tail -c 200 gpurun_out/bench_ref_d.log; echo
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_bench_r02_v2.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-refit-none --refit-warmup 0 --refit-reps 1 > gpurun_out/ncu_d.log 2>&1; tail -n 1 gpurun_out/ncu_d.log | cut -c1-200
