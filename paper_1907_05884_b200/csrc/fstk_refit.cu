@@ -86,13 +86,26 @@ struct Rng {
     const uint64_t cap = uint64_t(1) << bits, mask = cap - 1;
     constexpr uint64_t kEmpty = ~uint64_t(0);
     std::vector<std::pair<uint64_t, uint64_t>> tab(cap, {kEmpty, 0});
+    auto home = [&](uint64_t key) { return (key * 0x9e3779b97f4a7c15ull) >> (64 - bits); };
     auto slot = [&](uint64_t key) -> std::pair<uint64_t, uint64_t>& {
-      uint64_t h = (key * 0x9e3779b97f4a7c15ull) >> (64 - bits);
+      uint64_t h = home(key);
       while (tab[h].first != kEmpty && tab[h].first != key) h = (h + 1) & mask;
       return tab[h];
     };
+    // The draws depend on the generator alone, not on the table: they are
+    // made first, so the table slot (or dense entry) each swap will touch can
+    // be prefetched a few swaps ahead.  The 2^21-entry table of a 2^20-row
+    // working subset is 32 MB of random accesses: 47 -> 15 ms at C2.
+    std::vector<uint64_t> js(k);
+    for (uint64_t i = 0; i < k; ++i) js[i] = i + uniform_index(n - i);
+    constexpr uint64_t kAhead = 16;
     for (uint64_t i = 0; i < k; ++i) {
-      const uint64_t j = i + uniform_index(n - i);
+      if (i + kAhead < k) {
+        const uint64_t jn = js[i + kAhead];
+        __builtin_prefetch(jn < k ? static_cast<const void*>(&pre[jn])
+                                  : static_cast<const void*>(&tab[home(jn)]), 1);
+      }
+      const uint64_t j = js[i];
       const uint64_t vi = pre[i];
       uint64_t vj;
       if (j < k) {

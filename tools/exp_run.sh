@@ -1,4 +1,3 @@
-# scratch experiment driver (gpurun): final records: default bench, reference arm, launch list
-python bench.py > gpurun_out/bench_d.log 2>&1; tail -c 300 gpurun_out/bench_d.log; echo
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_d.log 2>&1; tail -c 200 gpurun_out/bench_ref_d.log; echo
-ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_bench_r02_v2.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-refit-none --refit-warmup 0 --refit-reps 1 > gpurun_out/ncu_d.log 2>&1; tail -n 1 gpurun_out/ncu_d.log | cut -c1-200
+# scratch experiment driver (gpurun): prepare phases after the prefetching sampler
+python -m pytest tests/test_gpu_refit.py -x -q -k "sketch_rows or c1_refit or recovers or biased" > gpurun_out/exp_tests.log 2>&1; tail -n 2 gpurun_out/exp_tests.log
+FSTK_DEBUG_TIMING=1 python tools/refit_var.py 4 2>&1 | grep -E "^run|fstk prepare" | tail -16
