@@ -489,6 +489,14 @@ void launch_crt_fold(const CT* C, int64_t cstride, int64_t m, int64_t wn, int64_
 // preconditioner it costs the C2 refinement no extra step (first correction
 // 3.3e-3 instead of 2.1e-4, contraction 5e-6 per step; tools/refine_time.py).
 int crt_level_bits(int level) { return level == 3 ? 23 : 7 * level - 1; }
+// Level 3 for segments of kp rows: the most bits 8 moduli carry (23 up to
+// 32,768 rows, 22 up to 65,536), capped at 23.
+int crt_level3_bits(int64_t kp) {
+  double have = 0.0;
+  for (int i = 0; i < 8; ++i) have += std::log2(static_cast<double>(kmod(i)));
+  const double room = have - 0.25 - 2.0 - std::log2(static_cast<double>(std::max<int64_t>(kp, 1)));
+  return std::max(16, std::min(23, static_cast<int>(std::floor(room / 2.0 - 1e-9))));
+}
 
 
 namespace {
@@ -637,7 +645,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
                                       cudaEvent_t first_block_done = nullptr) {
   if (ldg < 0) ldg = n;
   require(ns >= 3 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: levels 3..7");
-  const int k = crt_level_bits(ns);
+  int k = crt_level_bits(ns);
   // SYRK engine: 256-column tiles and 128-byte K blocks (zero padding).  It
   // folds each tile in its epilogue while the next tile's MMAs run, which
   // hides the fold only when a tile's K loop is long: short updates (the
@@ -670,12 +678,14 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   // does not change what a call computes beyond fp64 accumulation order).
   // Sizing for the level-7 count on every call shrank C4's segments to ~20k
   // rows next to its 137 GB sketch (Gram 2.8 s instead of 2.3 s).
-  const int nm_need = std::max(8, crt_moduli(k, kmax));
+  // Level 3 is 8 moduli whatever the segment length; its bits follow from kp below.
+  const int nm_need = ns == 3 ? 8 : std::max(8, crt_moduli(k, kmax));
   const int64_t have = static_cast<int64_t>(sc.X.n);
   const int64_t budget = std::min<int64_t>(int64_t(24) << 30, (static_cast<int64_t>(free_b) + have) / 3);
   kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, budget / (nm_need * np)));
   kmax &= ~(kalign - 1);
   const int64_t kp = std::min<int64_t>(kmax, round_up(rows, kalign));
+  if (ns == 3) k = crt_level3_bits(kp);
   // (Short segments would need fewer; the kernels are instantiated from 8.)
   const int nm = std::max(8, crt_moduli(k, kp));
   require(nm >= 8 && nm <= 17, FSTK_E_COMPUTE, "internal: CRT modulus count out of range");
