@@ -996,19 +996,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1) warp_pass1_kernel(const WarpPas
 // (a spill reload behind the 16 outstanding sector loads waits for DRAM).
 // Same butterflies and epilogue as transform_pass2_kernel, in the same order,
 // so A is bit-identical.
-// Measured at C2 (profiles/ncu_sketch_r02.txt): 2.24-2.35 ms per 256 columns
-// against 2.3 ms for transform_pass2_kernel, so it stays opt-in
-// (FSTK_SKETCH_WARP2=1): with 10 warps per SM (168 registers, 209 KB) the
-// three shared-memory round trips and the pair / cluster barriers leave the
-// fp64 pipe at 37%.
-constexpr int kPp2Pairs = 5;                   // columns in flight per CTA
+// Measured at C2 (profiles/ncu_sketch_r02.txt): 2.2-2.35 ms per 256 columns
+// against 2.3 ms for transform_pass2_kernel (C2 sketch 0.443 s against
+// 0.445 s), so it stays opt-in (FSTK_SKETCH_WARP2=1): with 10-12 warps per SM
+// (168 registers; 12 warps fill 224 KB once the DCT rotations are read from
+// L2 instead of a shared copy) the three shared-memory round trips and the
+// pair / cluster barriers leave the fp64 pipe at 37%.
+constexpr int kPp2Pairs = 6;                   // columns in flight per CTA
 constexpr int kPp2Warps = 2 * kPp2Pairs;
 constexpr int kPp2Buf = 1024;                  // double2 per warp
 // CTAs of kPp2Cluster adjacent class pairs form a cluster and stay within one
 // column of each other (split cluster barrier), so the 128-byte lines they
 // share are fetched from DRAM once and hit in L2 for the others.
 constexpr int kPp2Cluster = 4;
-constexpr int kPp2Cap = 384;                   // sampled elements per class with cached DCT rotations
+constexpr int kPp2Cap = 0;                     // sampled elements per class with DCT rotations cached in shared memory (0: read from L2)
 constexpr size_t kPp2Smem = (2 * 1023 + kPp2Warps * kPp2Buf) * sizeof(double2) +
                             2 * kPp2Cap * 2 * sizeof(double) + 64 * sizeof(uint32_t);
 

@@ -1,3 +1,4 @@
-# scratch experiment driver (gpurun): level-3 Gram with 65,536-row segments (22 bits) against 32,768 (23 bits)
-for seg in 32768 65536; do echo "seg=$seg"; FSTK_GRAM_SEG=$seg python tools/refit_var.py 4 2>&1 | grep -E "^run" | tail -3; done
-FSTK_GRAM_SEG=65536 python -m pytest tests/test_gpu_gram.py tests/test_gpu_fullsize_refit.py -x -q > gpurun_out/exp_tests.log 2>&1; tail -n 2 gpurun_out/exp_tests.log
+# scratch experiment driver (gpurun): pair-pass sketch with 6 pairs (12 warps), rotations from L2
+FSTK_SKETCH_WARP2=1 timeout 600 python -m pytest tests/test_gpu_refit.py -x -q -k "two_pass_1m" > gpurun_out/exp_tests.log 2>&1; tail -n 2 gpurun_out/exp_tests.log
+FSTK_SKETCH_WARP2=1 timeout 300 python tools/sketch_time.py 3 2>&1 | tail -n 2
+FSTK_SKETCH_WARP2=0 timeout 300 python tools/sketch_time.py 3 2>&1 | tail -n 1
