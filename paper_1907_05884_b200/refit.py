@@ -242,7 +242,7 @@ class RefitSession:
             self._h, gram_t.data_ptr(), rhs_t.data_ptr(), C.byref(self.info), C.byref(err)), err)
 
     def normal_equations_level(self, slices, gram_t, rhs_t):
-        """normal_equations() at an explicit Gram precision: 4..7 (sliced,
+        """normal_equations() at an explicit Gram precision: 3..7 (sliced,
         int8 tensor cores) or 0 (native fp64)."""
         err = Err()
         check(lib().fstk_gpu_refit_normal_equations_level(
