@@ -268,9 +268,11 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* refit, double* gr
                                                fstk_gpu_error* err);
 /* Process-wide Gram arithmetic: slices > 0 runs A^T A on the int8 tensor
  * cores at the accuracy of that many 7-bit planes (levels 4..7: entries
- * rounded to (7 slices - 1)-bit integers per column and segment), or at level
- * 3 (the default, or $FSTK_GRAM_SLICES): 23-bit entries, the most 8 CRT moduli
- * carry, a preconditioner-grade Gram that the refinement against A corrects.
+ * rounded to (7 slices - 1)-bit integers per column and segment), or at the
+ * preconditioner grades 3 and 2: 23- and 19-bit entries, the most that 8 and
+ * 7 CRT moduli carry.  The default ($FSTK_GRAM_SLICES) is 2; the refinement
+ * against A corrects what the Gram rounds away, and transform = none takes
+ * at least level 3 from this setting (its rows are worse conditioned).
  * Products are exact (CRT over int8 residues; the
  * digit-plane split with FSTK_GRAM_SCHEME=digits); 0 selects the native fp64
  * Gram; < 0 only queries.  Returns the previous setting.  No reference
@@ -326,7 +328,7 @@ int32_t fstk_gpu_pack_normal_equations(const double* gram, const double* rhs, in
  * sums into c (nm planes of np x np bytes). */
 int32_t fstk_gpu_debug_syrk(const int8_t* planes, int32_t nm, int64_t kp, int64_t np, int8_t* c,
                             int32_t device, void* stream, fstk_gpu_error* err);
-/* normal_equations() at an explicit Gram precision: slices 3..7 (sliced,
+/* normal_equations() at an explicit Gram precision: slices 2..7 (sliced,
  * int8 tensor cores) or 0 (native fp64).  solve() and dist.refine_distributed
  * escalate with it: a sliced Gram that cannot precondition the system is
  * recomputed at 7, then at 0. */
@@ -334,7 +336,7 @@ int32_t fstk_gpu_refit_normal_equations_level(fstk_gpu_refit* refit, int32_t sli
                                               double* gram, double* rhs,
                                               fstk_reestimate_info* info, fstk_gpu_error* err);
 /* gram (n x n, column-major, lower triangle written) = A^T A for a DEVICE
- * matrix A (rows x n, column-major, lda), at `slices` plane-accuracy (3..7)
+ * matrix A (rows x n, column-major, lda), at `slices` plane-accuracy (2..7)
  * or native fp64 DSYRK/DGEMM (0), on `stream` (cudaStream_t, NULL = default).
  * The Gram stage of normal_equations() on its own, for tests and callers
  * that build their own design matrices. */

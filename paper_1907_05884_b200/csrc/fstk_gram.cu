@@ -46,11 +46,11 @@ namespace fstk_gpu {
 namespace {
 
 constexpr int kDigitMax = 64;
-constexpr int kDefaultSlices = 3;
+constexpr int kDefaultSlices = 2;
 constexpr int kMaxSlices = 7;
 std::atomic<int> g_slices{-1};
 
-int clamp_slices(int v) { return v <= 0 ? 0 : std::min(std::max(v, 3), kMaxSlices); }
+int clamp_slices(int v) { return v <= 0 ? 0 : std::min(std::max(v, 2), kMaxSlices); }
 
 struct LtState {
   cublasLtHandle_t lt = nullptr;
@@ -468,6 +468,7 @@ void launch_crt_fold(const CT* C, int64_t cstride, int64_t m, int64_t wn, int64_
 
 #define FSTK_CRT_SWITCH(NMV, CALL)                                              \
   switch (NMV) {                                                                \
+    case 7: CALL(7); break;                                                     \
     case 8: CALL(8); break;                                                     \
     case 9: CALL(9); break;                                                     \
     case 10: CALL(10); break;                                                   \
@@ -484,18 +485,20 @@ void launch_crt_fold(const CT* C, int64_t cstride, int64_t m, int64_t wn, int64_
 }  // namespace
 
 // Bits per entry of a CRT Gram level.  Levels 4..7 carry the accuracy of that
-// many 7-bit planes (k = 7 level - 1).  Level 3 is the most 8 moduli carry
-// over 32,768-row segments, k = 23: its Gram costs 8/9 of level 4's, and as a
-// preconditioner it costs the C2 refinement no extra step (first correction
-// 3.3e-3 instead of 2.1e-4, contraction 5e-6 per step; tools/refine_time.py).
-int crt_level_bits(int level) { return level == 3 ? 23 : 7 * level - 1; }
-// Level 3 for segments of kp rows: the most bits 8 moduli carry (23 up to
-// 32,768 rows, 22 up to 65,536), capped at 23.
-int crt_level3_bits(int64_t kp) {
+// many 7-bit planes (k = 7 level - 1).  Levels 3 and 2 are defined from the
+// other side: the most bits that 8 and 7 moduli carry over a segment (23 and
+// 19 at 32,768 rows).  As preconditioners of a mixed sketch they keep the
+// refinement's contraction per step below 2e-4 and 3e-3 at C2
+// (tools/refine_time.py), well inside the 0.1 that escalates, for 8/9 and 7/9
+// of level 4's int8 work.  Level 2 is the default (DESIGN 3.4).
+int crt_level_bits(int level) { return level == 3 ? 23 : (level == 2 ? 19 : 7 * level - 1); }
+int crt_low_level_moduli(int level) { return level == 3 ? 8 : 7; }
+int crt_low_level_bits(int level, int64_t kp) {
+  const int nm = crt_low_level_moduli(level);
   double have = 0.0;
-  for (int i = 0; i < 8; ++i) have += std::log2(static_cast<double>(kmod(i)));
+  for (int i = 0; i < nm; ++i) have += std::log2(static_cast<double>(kmod(i)));
   const double room = have - 0.25 - 2.0 - std::log2(static_cast<double>(std::max<int64_t>(kp, 1)));
-  return std::max(16, std::min(23, static_cast<int>(std::floor(room / 2.0 - 1e-9))));
+  return std::max(12, std::min(crt_level_bits(level), static_cast<int>(std::floor(room / 2.0 - 1e-9))));
 }
 
 
@@ -549,8 +552,8 @@ double gram_accumulate_sliced(const double* A, int64_t lda, int64_t rows, int n,
   if (t_lo == 2 && gram_scheme_crt())
     return gram_accumulate_crt(A, lda, rows, n, gram, beta, ns, s, device, sc);
   double ops = 0.0;
-  if (ns == 3) ns = 4;  // level 3 exists in the CRT scheme only
-  require(ns >= 4 && ns <= kMaxSlices, FSTK_E_PARAMETER, "sliced Gram: 4..9 digit planes");
+  if (ns < 4) ns = 4;  // levels 2 and 3 exist in the CRT scheme only
+  require(ns >= 4 && ns <= kMaxSlices, FSTK_E_PARAMETER, "sliced Gram: 4..7 digit planes");
   require(t_lo >= 2 && t_lo <= ns + 1, FSTK_E_PARAMETER, "sliced Gram: bad plane range");
   const int nt = ns + 2 - t_lo;  // plane sums t_lo..ns+1
   LtState& st = lt_state(device);
@@ -644,7 +647,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
                                       GramScratch& sc, int64_t ldg = -1, bool negate = false,
                                       cudaEvent_t first_block_done = nullptr) {
   if (ldg < 0) ldg = n;
-  require(ns >= 3 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: levels 3..7");
+  require(ns >= 2 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: levels 2..7");
   int k = crt_level_bits(ns);
   // SYRK engine: 256-column tiles and 128-byte K blocks (zero padding).  It
   // folds each tile in its epilogue while the next tile's MMAs run, which
@@ -658,6 +661,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   // (The SYRK's band table covers up to 131,072 columns; wider Grams keep the
   // library engine.)
   const bool syrk = gram_engine() == 1 && rows >= syrk_min_rows && n <= 131072;
+  const bool fused = syrk && syrk_fused() && ns > 2;  // the fused kernel is instantiated from 8 moduli
   const int64_t np = round_up(static_cast<int64_t>(n), syrk ? 256 : 16);
   const int64_t kalign = syrk ? 128 : 16;
   static const int64_t seg_cap = [] {
@@ -678,17 +682,18 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   // does not change what a call computes beyond fp64 accumulation order).
   // Sizing for the level-7 count on every call shrank C4's segments to ~20k
   // rows next to its 137 GB sketch (Gram 2.8 s instead of 2.3 s).
-  // Level 3 is 8 moduli whatever the segment length; its bits follow from kp below.
-  const int nm_need = ns == 3 ? 8 : std::max(8, crt_moduli(k, kmax));
+  // Levels 2 and 3 are 7 and 8 moduli whatever the segment length; their bits
+  // follow from kp below.
+  const int nm_need = ns <= 3 ? crt_low_level_moduli(ns) : std::max(8, crt_moduli(k, kmax));
   const int64_t have = static_cast<int64_t>(sc.X.n);
   const int64_t budget = std::min<int64_t>(int64_t(24) << 30, (static_cast<int64_t>(free_b) + have) / 3);
   kmax = std::min<int64_t>(kmax, std::max<int64_t>(1024, budget / (nm_need * np)));
   kmax &= ~(kalign - 1);
   const int64_t kp = std::min<int64_t>(kmax, round_up(rows, kalign));
-  if (ns == 3) k = crt_level3_bits(kp);
-  // (Short segments would need fewer; the kernels are instantiated from 8.)
-  const int nm = std::max(8, crt_moduli(k, kp));
-  require(nm >= 8 && nm <= 17, FSTK_E_COMPUTE, "internal: CRT modulus count out of range");
+  if (ns <= 3) k = crt_low_level_bits(ns, kp);
+  // (Short segments would need fewer; the kernels are instantiated from 7.)
+  const int nm = std::max(ns <= 3 ? crt_low_level_moduli(ns) : 8, crt_moduli(k, kp));
+  require(nm >= 7 && nm <= 17, FSTK_E_COMPUTE, "internal: CRT modulus count out of range");
   static const int64_t block_cap = [] {
     const char* e = std::getenv("FSTK_GRAM_BLOCK");
     return e ? std::max<int64_t>(256, std::atoll(e)) : int64_t(2048);
@@ -697,9 +702,9 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   int64_t w = std::max<int64_t>(256, (int64_t(4) << 30) / (np * nm * (syrk ? 1 : 4)));
   w = std::min<int64_t>(round_up(std::min<int64_t>(w, np), wal), np);
   if (w > block_cap && np > block_cap) w = round_up(block_cap, wal);
-  sc.last_block_w = (syrk && syrk_fused()) ? 0 : w;  // fused: no per-block order to hook into
+  sc.last_block_w = fused ? 0 : w;  // fused: no per-block order to hook into
   sc.X.ensure(static_cast<size_t>(nm) * kp * np);
-  if (syrk && syrk_fused()) {
+  if (fused) {
     sc.C8.ensure(syrk_crt_scratch_bytes(nm, device));
   } else if (syrk) {
     sc.C8.ensure(static_cast<size_t>(nm) * np * w + 256);  // + the scheduler's task counter
@@ -718,7 +723,7 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
     FSTK_CRT_SWITCH(nm, FSTK_CRT_RES)
 #undef FSTK_CRT_RES
     const int acc = (!first || beta != 0.0) ? 1 : 0;
-    if (syrk && syrk_fused()) {
+    if (fused) {
       // One persistent tcgen05 launch: the whole lower triangle, every
       // modulus, Garner fold in the epilogue.
       ops += syrk_crt_fold(sc.X.p, nm, kp, np, n, k, sc.ex.p, gram, ldg, acc != 0, negate, sc.C8.p,

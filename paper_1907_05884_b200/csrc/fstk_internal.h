@@ -204,7 +204,7 @@ struct GramScratch {
   int64_t last_block_w = 0;  // column-block width of the latest CRT call (0: no block order)
 };
 int gram_slices();                      // 0 = native fp64 DSYRK/DGEMM Gram
-int crt_level_bits(int level);          // bits per entry of CRT level 3..7
+int crt_level_bits(int level);          // bits per entry of CRT level 2..7 (at 32,768-row segments)
 // Int8 GEMM engine of the CRT Gram: 1 = the hand-written tcgen05 SYRK
 // (fstk_syrk.cu, default), 2 = cuBLASLt IMMA GEMMs (comparison).
 int gram_engine();

@@ -2570,7 +2570,7 @@ static void generate_design_block(const fstk_gpu_refit* rf, int64_t row0, int64_
 
 namespace fstk_gpu {
 // slices < 0: the process setting (gram_slices()); 0: native fp64 Gram;
-// 4..7: the sliced Gram at that precision level.
+// 2..7: the sliced Gram at that precision level.
 static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
                              fstk_reestimate_info* info, int slices) {
   {
@@ -2595,7 +2595,13 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
       // is split into nb column blocks: block row i below the diagonal is one
       // DGEMM A_i^T [A_0 .. A_{i-1}] and each diagonal block one DSYRK, so
       // (nb-1)/nb of the flops run in large GEMMs.
-      const int level = slices < 0 ? gram_slices() : slices;
+      int level = slices < 0 ? gram_slices() : slices;
+      // The unmixed estimator's rows are worse conditioned than a mixed
+      // sketch's: at C2 a level-2 Gram leaves its first iterate 38% off and
+      // contracts 0.09 per step, at the edge of the escalation rule (level 3:
+      // 1.9e-2, then 2e-5 and 5e-3).  The process setting therefore means at
+      // least level 3 there; an explicit level (normal_equations_level) is kept.
+      if (slices < 0 && rf->none && level == 2) level = 3;
       const bool sliced = level > 0 && gram_sliced_applies(arows, n);
       rf->gram_used = sliced ? level : 0;
       if (rf->none && sliced && gram_scheme_crt()) {
@@ -2686,8 +2692,8 @@ int32_t fstk_gpu_refit_normal_equations_level(fstk_gpu_refit* rf, int32_t slices
                                               fstk_gpu_error* err) {
   return guarded(err, [&] {
     require(rf && gram && rhs, FSTK_E_PARAMETER, "null argument");
-    require(slices == 0 || (slices >= 3 && slices <= 7), FSTK_E_PARAMETER,
-            "normal_equations_level: slices must be 0 (native) or 3..7");
+    require(slices == 0 || (slices >= 2 && slices <= 7), FSTK_E_PARAMETER,
+            "normal_equations_level: slices must be 0 (native) or 2..7");
     normal_equations(rf, gram, rhs, info, slices);
   });
 }
@@ -2709,8 +2715,8 @@ int32_t fstk_gpu_gram_device(const double* a, int64_t lda, int64_t rows, int32_t
   return guarded(err, [&] {
     require(a && gram, FSTK_E_PARAMETER, "null argument");
     require(n > 0 && rows > 0 && lda >= rows, FSTK_E_SHAPE, "gram: need n > 0, rows > 0, lda >= rows");
-    require(slices == 0 || (slices >= 3 && slices <= 7), FSTK_E_PARAMETER,
-            "gram: slices must be 0 (native fp64) or 3..7");
+    require(slices == 0 || (slices >= 2 && slices <= 7), FSTK_E_PARAMETER,
+            "gram: slices must be 0 (native fp64) or 2..7");
     require((rows <= INT32_MAX && lda <= INT32_MAX) || slices > 0, FSTK_E_SHAPE,
             "gram: native path needs rows, lda < 2^31");
     DeviceGuard dg(device);

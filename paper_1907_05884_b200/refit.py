@@ -54,8 +54,8 @@ def _info_dict(info: ReestimateInfo) -> dict:
 
 def gram_slices(slices: int | None = None) -> int:
     """Gram arithmetic of this process: returns the current precision level
-    (the accuracy of that many 7-bit planes, 4..7; 3 = 23-bit entries on 8 CRT
-    moduli, the default; 0 = native fp64 Gram); with
+    (the accuracy of that many 7-bit planes, 4..7; 3 and 2 = 23- and 19-bit
+    entries on 8 and 7 CRT moduli, 2 being the default; 0 = native fp64 Gram); with
     `slices` given, sets it first and returns the previous value.  See
     fstk_gram.cu."""
     return int(lib().fstk_gpu_gram_slices(-1 if slices is None else int(slices)))
@@ -242,7 +242,7 @@ class RefitSession:
             self._h, gram_t.data_ptr(), rhs_t.data_ptr(), C.byref(self.info), C.byref(err)), err)
 
     def normal_equations_level(self, slices, gram_t, rhs_t):
-        """normal_equations() at an explicit Gram precision: 3..7 (sliced,
+        """normal_equations() at an explicit Gram precision: 2..7 (sliced,
         int8 tensor cores) or 0 (native fp64)."""
         err = Err()
         check(lib().fstk_gpu_refit_normal_equations_level(

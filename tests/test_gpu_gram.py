@@ -44,10 +44,10 @@ def _check_bound(a, g, ns):
 
 @pytest.mark.parametrize("rows,n", [(1000, 300), (70_000, 257), (333, 4000), (500, 5000),
                                     (17, 263), (4099, 1024)])
-@pytest.mark.parametrize("ns", [7, 5, 3])
+@pytest.mark.parametrize("ns", [7, 5, 3, 2])
 def test_gram_within_digit_plane_bound(rows, n, ns):
-    # Level 3 (the default: 8 moduli, 23-bit entries) sits inside the bound of
-    # three 7-bit planes.
+    # Levels 3 and 2 (8 and 7 moduli: 23- and 19-bit entries; 2 is the default)
+    # sit inside the bounds of three and two 7-bit planes.
     torch = _torch()
     gen = torch.Generator(device="cuda").manual_seed(rows * 7 + n)
     a = torch.randn(rows, n, dtype=torch.float64, device="cuda", generator=gen)
@@ -76,7 +76,7 @@ def test_gram_wild_column_scales_and_zero_columns():
     a[:, 7] = 0.0
     a[:, 300] = 0.0
     a[123, 55] = 1e9  # one outlier dominating its column
-    for ns in (7, 6, 4, 3):
+    for ns in (7, 6, 4, 3, 2):
         g = F.gram(a, slices=ns)
         _check_bound(a, g, ns)
         assert bool((g[7, :] == 0).all()) and bool((g[:, 300] == 0).all())
@@ -105,7 +105,7 @@ def test_gram_rejects_bad_arguments():
     torch = _torch()
     a = torch.randn(10, 300, dtype=torch.float64, device="cuda")
     with pytest.raises(F.FstkValueError):
-        F.gram(a, slices=2)
+        F.gram(a, slices=1)
     with pytest.raises(F.FstkValueError):
         F.gram(a, slices=8)
 
@@ -213,7 +213,7 @@ def test_gram_levels_converge_to_the_native_gram():
     sess = F.RefitSession(m, pts, vals, seed=2)
     out = {}
     try:
-        for lvl in (3, 5, 7, 0):
+        for lvl in (2, 3, 5, 7, 0):
             g = torch.empty(R * R, dtype=torch.float64, device="cuda")
             r = torch.empty(R, dtype=torch.float64, device="cuda")
             sess.normal_equations_level(lvl, g, r)
@@ -230,7 +230,8 @@ def test_gram_levels_converge_to_the_native_gram():
     e7 = float(((out[7][0] - GN).abs() / sc)[low].max())
     e5 = float(((out[5][0] - GN).abs() / sc)[low].max())
     e3 = float(((out[3][0] - GN).abs() / sc)[low].max())
-    assert e7 < 1e-13 and e5 < 1e-9 and e7 < e5 and e5 < e3 < 1e-5
+    e2 = float(((out[2][0] - GN).abs() / sc)[low].max())
+    assert e7 < 1e-13 and e5 < 1e-9 and e7 < e5 and e5 < e3 < 1e-5 and e3 < e2 < 1e-4
     assert torch.equal(out[5][1], out[0][1]) and torch.equal(out[7][1], out[0][1])
 
 
@@ -252,9 +253,9 @@ def test_gram_slices_setting_roundtrip():
         assert F.gram_slices(5) == prev
         assert F.gram_slices() == 5
         F.gram_slices(12)
-        assert F.gram_slices() == 7  # clamped to 3..7
-        F.gram_slices(2)
-        assert F.gram_slices() == 3
+        assert F.gram_slices() == 7  # clamped to 2..7
+        F.gram_slices(1)
+        assert F.gram_slices() == 2
         F.gram_slices(0)
         assert F.gram_slices() == 0
     finally:

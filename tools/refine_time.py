@@ -1,7 +1,7 @@
 """Dev tool: wall time of every stage call of the C2 refit's solve
 (factor / correction / apply / certify) as dist.refine_distributed issues them
 on one GPU, to locate the host time between the device-timed stages.
-usage: python tools/refine_time.py [reps]"""
+usage: python tools/refine_time.py [reps] [transform]"""
 import os
 import sys
 import time
@@ -17,7 +17,8 @@ from paper_1907_05884_b200 import _lib
 model, pts, vals, c = workload("C2", 0, 0)
 R = int(np.prod(model.ranks))
 for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
-    s = F.RefitSession(model, pts, vals, seed=0, sample_rows=c["m_factor"] * R)
+    s = F.RefitSession(model, pts, vals, seed=0, sample_rows=c["m_factor"] * R,
+                       transform=sys.argv[2] if len(sys.argv) > 2 else "dct")
     g = _lib.device_tensor(R * R, "cuda")
     rhs = torch.empty(R, dtype=torch.float64, device="cuda")
     s.normal_equations(g, rhs)
