@@ -5,6 +5,8 @@
 #include <cusolverDn.h>
 #include <cuda_runtime.h>
 
+#include <functional>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -320,8 +322,23 @@ struct LambdaMinEstimate {
   int n = 0, device = 0;
   cudaStream_t s = nullptr;
   bool started = false;
+  // The enqueue job of start_async on the library's side worker thread.
+  std::shared_future<void> enqueued;
   void start(const double* L, int n, int iters, cudaStream_t s, int device);
+  // start() on the side worker: the chain is ~400 cuBLAS calls and more
+  // kernels than the driver queues at once, so enqueueing it blocks the
+  // calling thread for about as long as the chain runs (80 ms at C2).
+  void start_async(const double* L, int n, int iters, cudaStream_t s, int device);
+  // Blocks until the chain is enqueued (rethrows what the job threw).
+  void wait_enqueued();
   double result();
+  LambdaMinEstimate() = default;
+  LambdaMinEstimate(const LambdaMinEstimate&) = delete;
+  LambdaMinEstimate& operator=(const LambdaMinEstimate&) = delete;
+  ~LambdaMinEstimate();
 };
+// Runs jobs in submission order on one long-lived host thread (its own
+// thread-local cuBLAS handles are created once).
+std::shared_future<void> side_worker_submit(std::function<void()> job);
 double chol_lambda_min_estimate(const double* L, int n, int iters, cudaStream_t s, int device);
 }  // namespace fstk_gpu

@@ -35,6 +35,9 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <thread>
 #include <vector>
 
 #include "fstk_internal.h"
@@ -476,8 +479,8 @@ void LambdaMinEstimate::start(const double* L, int n_, int iters, cudaStream_t s
     z ^= z >> 31;
     v = static_cast<double>(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
   }
-  X.alloc(h.size());
-  norms.alloc(NV);
+  X.ensure(h.size());  // (kept across the factorisations of a session)
+  norms.ensure(NV);
   FSTK_CUDA(cudaMemcpyAsync(X.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s));
   FSTK_CUDA(cudaStreamSynchronize(s));  // h is a host temporary
   cublasHandle_t blas = blas_side_handle(device);
@@ -492,7 +495,70 @@ void LambdaMinEstimate::start(const double* L, int n_, int iters, cudaStream_t s
   started = true;
 }
 
+// ---- side worker: one detached host thread running jobs in order ----
+namespace {
+struct SideWorker {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<std::packaged_task<void()>> q;
+  SideWorker() {
+    std::thread([this] {
+      for (;;) {
+        std::packaged_task<void()> job;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [this] { return !q.empty(); });
+          job = std::move(q.front());
+          q.pop_front();
+        }
+        job();  // exceptions land in the task's future
+      }
+    }).detach();
+  }
+};
+}  // namespace
+
+std::shared_future<void> side_worker_submit(std::function<void()> job) {
+  static SideWorker* w = new SideWorker();  // leaked: no teardown-order hazards at exit
+  std::packaged_task<void()> task(std::move(job));
+  std::shared_future<void> f = task.get_future().share();
+  {
+    std::lock_guard<std::mutex> lk(w->mu);
+    w->q.push_back(std::move(task));
+  }
+  w->cv.notify_one();
+  return f;
+}
+
+void LambdaMinEstimate::start_async(const double* L, int n_, int iters, cudaStream_t s_, int device_) {
+  wait_enqueued();
+  s = s_;
+  device = device_;
+  enqueued = side_worker_submit([this, L, n_, iters, s_, device_] {
+    FSTK_CUDA(cudaSetDevice(device_));
+    start(L, n_, iters, s_, device_);
+  });
+}
+
+void LambdaMinEstimate::wait_enqueued() {
+  if (!enqueued.valid()) return;
+  std::shared_future<void> f = enqueued;
+  enqueued = std::shared_future<void>();
+  f.get();
+}
+
+LambdaMinEstimate::~LambdaMinEstimate() {
+  // Only the enqueue job is waited for here.  The stream may already be gone
+  // (a session destroys its side stream, after synchronising it, before its
+  // members): releasing X and norms synchronises the device like cudaFree.
+  try {
+    wait_enqueued();
+  } catch (...) {
+  }
+}
+
 double LambdaMinEstimate::result() {
+  wait_enqueued();
   if (!started) return 0.0;
   double hn[kVectors];
   FSTK_CUDA(cudaMemcpyAsync(hn, norms.p, sizeof(hn), cudaMemcpyDeviceToHost, s));
