@@ -37,6 +37,8 @@
 #include <tuple>
 #include <type_traits>
 
+#include <functional>
+
 #include "fstk_common.cuh"
 #include "fstk_crt.cuh"
 #include "fstk_internal.h"
@@ -645,7 +647,8 @@ template <class SRC>
 static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, double* gram,
                                       double beta, int ns, cudaStream_t s, int device,
                                       GramScratch& sc, int64_t ldg = -1, bool negate = false,
-                                      cudaEvent_t first_block_done = nullptr) {
+                                      cudaEvent_t first_block_done = nullptr,
+                                      const std::function<void()>* after_first_block = nullptr) {
   if (ldg < 0) ldg = n;
   require(ns >= 2 && ns <= 7, FSTK_E_PARAMETER, "CRT Gram: levels 2..7");
   int k = crt_level_bits(ns);
@@ -744,7 +747,13 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   launch_crt_fold<NMV, int8_t>(c8, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
         FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
 #undef FSTK_CRT_FOLD
-        if (first_block_done && c0 == 0 && s0 + kp >= rows) FSTK_CUDA(cudaEventRecord(first_block_done, s));
+        if (first_block_done && c0 == 0 && s0 + kp >= rows) {
+          FSTK_CUDA(cudaEventRecord(first_block_done, s));
+          // The caller's dependent work is enqueued here, ahead of the other
+          // blocks' launches: the launch queue is finite, and work issued after
+          // this whole update would reach the GPU only as the update drains.
+          if (after_first_block) (*after_first_block)();
+        }
       }
     } else {
       LtState& st = lt_state(device);
@@ -761,7 +770,13 @@ static double gram_accumulate_crt_src(const SRC& src, int64_t rows, int n, doubl
   launch_crt_fold<NMV, int32_t>(sc.C.p, m * wn, m, wn, c0, n, k, sc.ex.p, gram, ldg, acc, negate ? 1 : 0, s)
         FSTK_CRT_SWITCH(nm, FSTK_CRT_FOLD)
 #undef FSTK_CRT_FOLD
-        if (first_block_done && c0 == 0 && s0 + kp >= rows) FSTK_CUDA(cudaEventRecord(first_block_done, s));
+        if (first_block_done && c0 == 0 && s0 + kp >= rows) {
+          FSTK_CUDA(cudaEventRecord(first_block_done, s));
+          // The caller's dependent work is enqueued here, ahead of the other
+          // blocks' launches: the launch queue is finite, and work issued after
+          // this whole update would reach the GPU only as the update drains.
+          if (after_first_block) (*after_first_block)();
+        }
       }
     }
     first = false;
@@ -776,13 +791,30 @@ double gram_accumulate_crt(const double* A, int64_t lda, int64_t rows, int n, do
 
 double gram_update_crt(const double* T, int64_t ldt, int64_t rows, int n, double* G, int64_t ldg,
                        int ns, cudaStream_t s, int device, GramScratch& sc,
-                       cudaEvent_t first_block_done, int64_t* first_block_cols) {
+                       cudaEvent_t first_block_done, int64_t* first_block_cols,
+                       const std::function<void()>* after_first_block, int64_t need_cols) {
   // The first column block is min(2048, n) columns wide (block_cap) unless the
   // scratch budget narrows it; a caller overlapping work with the rest of the
   // update must wait for the whole update when the block is narrower than it needs.
   if (first_block_cols) *first_block_cols = 0;
+  // The callback runs inside only when the first block will be wide enough
+  // for the caller (block_cap columns unless the scratch budget narrows it:
+  // known only inside, so the width is checked there through last_block_w).
+  struct Gate {
+    GramScratch& sc;
+    const std::function<void()>* cb;
+    int64_t need;
+    bool fired = false;
+  } gate{sc, after_first_block, need_cols};
+  std::function<void()> gated = [&gate] {
+    if (gate.cb && gate.sc.last_block_w >= gate.need) {
+      (*gate.cb)();
+      gate.fired = true;
+    }
+  };
   const double ops = gram_accumulate_crt_src(DenseSrc{T, ldt}, rows, n, G, 1.0, ns, s, device, sc, ldg, true,
-                                             first_block_done);
+                                             first_block_done, after_first_block ? &gated : nullptr);
+  if (after_first_block && !gate.fired) sc.last_block_w = 0;  // tell the caller to wait for the whole update
   if (first_block_cols) *first_block_cols = sc.last_block_w;
   return ops;
 }

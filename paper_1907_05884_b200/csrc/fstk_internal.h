@@ -258,10 +258,12 @@ struct DesignSpec {
 // first_block_done (optional) is recorded on s once the update's first column
 // block (*first_block_cols columns wide, 0 when the engine has no block order)
 // has been folded into G: the blocked Cholesky's lookahead starts the next
-// panel there.
+// panel there.  after_first_block (optional) is called right after that record
+// when the block is at least need_cols wide (else *first_block_cols = 0).
 double gram_update_crt(const double* T, int64_t ldt, int64_t rows, int n, double* G, int64_t ldg,
                        int slices, cudaStream_t s, int device, GramScratch& sc,
-                       cudaEvent_t first_block_done = nullptr, int64_t* first_block_cols = nullptr);
+                       cudaEvent_t first_block_done = nullptr, int64_t* first_block_cols = nullptr,
+                       const std::function<void()>* after_first_block = nullptr, int64_t need_cols = 0);
 // The sliced (CRT) Gram of those rows without materialising them.
 bool gram_scheme_crt();
 double gram_accumulate_sliced_design(const DesignSpec& spec, int64_t rows, int n, double* gram,

@@ -2946,15 +2946,25 @@ static bool chol_crt(cublasHandle_t blas, cusolverDnHandle_t solver, double* G, 
     }
     FSTK_CUDA(cudaEventRecord(side.panel, sp));
     FSTK_CUDA(cudaStreamWaitEvent(s, side.panel, 0));  // panel p factored and transposed
-    int64_t bw = 0;
-    gram_update_crt(Tp, b, b, rest, A22, n, slices, s, device, sc, side.block, &bw);
-    count_launch();
     // The next panel needs its nb columns of the trailing matrix final: the
-    // first block when that is wide enough, else the whole update.
+    // update's first column block when that is wide enough (the panel is then
+    // enqueued from inside the update, ahead of its other blocks' launches),
+    // else the whole update.
+    int64_t bw = 0;
     const int nextb = std::min(nb, rest);
-    if (bw < nextb) FSTK_CUDA(cudaEventRecord(side.block, s));
-    FSTK_CUDA(cudaStreamWaitEvent(sp, side.block, 0));
-    panel(p + 1);
+    bool issued = false;
+    const std::function<void()> next_panel = [&] {
+      FSTK_CUDA(cudaStreamWaitEvent(sp, side.block, 0));
+      panel(p + 1);
+      issued = true;
+    };
+    gram_update_crt(Tp, b, b, rest, A22, n, slices, s, device, sc, side.block, &bw, &next_panel, nextb);
+    count_launch();
+    if (!issued) {
+      FSTK_CUDA(cudaEventRecord(side.block, s));
+      FSTK_CUDA(cudaStreamWaitEvent(sp, side.block, 0));
+      panel(p + 1);
+    }
   }
   if (lookahead) {  // s continues after the last panel
     FSTK_CUDA(cudaEventRecord(side.panel, sp));
