@@ -59,6 +59,15 @@ struct Rng {
   uint64_t next_u64() { return engine(); }
   uint64_t uniform_index(uint64_t n) {
     require(n > 0, FSTK_E_PARAMETER, "uniform_index: n must be positive");
+    // rng.cpp rejects x >= limit = UINT64_MAX - UINT64_MAX % n.  For n < 2^32
+    // the limit exceeds 2^64 - 2^32, so a draw below that is accepted without
+    // the second 64-bit division (all but one draw in 4e9): same decisions.
+    if (n <= 0xffffffffull) {
+      const uint64_t x0 = next_u64();
+      if (x0 < 0xffffffff00000000ull) return x0 % n;
+      const uint64_t limit0 = UINT64_MAX - UINT64_MAX % n;
+      if (x0 < limit0) return x0 % n;
+    }
     const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
     uint64_t x;
     do {
@@ -96,10 +105,37 @@ struct Rng {
     // made first, so the table slot (or dense entry) each swap will touch can
     // be prefetched a few swaps ahead.  The 2^21-entry table of a 2^20-row
     // working subset is 32 MB of random accesses: 47 -> 15 ms at C2.
+    // Large samples: a second host thread makes the draws (generator and two
+    // 64-bit divisions each) while this one applies the swaps behind it.
     std::vector<uint64_t> js(k);
-    for (uint64_t i = 0; i < k; ++i) js[i] = i + uniform_index(n - i);
+    std::atomic<uint64_t> drawn{0};
+    constexpr uint64_t kChunk = uint64_t(1) << 14;
+    auto draw_all = [&] {
+      for (uint64_t i = 0; i < k; ++i) {
+        js[i] = i + uniform_index(n - i);
+        if (((i + 1) & (kChunk - 1)) == 0) drawn.store(i + 1, std::memory_order_release);
+      }
+      drawn.store(k, std::memory_order_release);
+    };
+    std::thread drawer;
+    if (k >= (uint64_t(1) << 17))
+      drawer = std::thread(draw_all);
+    else
+      draw_all();
+    struct Join {
+      std::thread& t;
+      ~Join() {
+        if (t.joinable()) t.join();
+      }
+    } join{drawer};
     constexpr uint64_t kAhead = 16;
+    uint64_t ready = 0;
     for (uint64_t i = 0; i < k; ++i) {
+      // draws [0, ready) are published; the prefetch below looks kAhead ahead
+      while (ready < std::min(k, i + kAhead + 1)) {
+        ready = drawn.load(std::memory_order_acquire);
+        if (ready < std::min(k, i + kAhead + 1)) std::this_thread::yield();
+      }
       if (i + kAhead < k) {
         const uint64_t jn = js[i + kAhead];
         __builtin_prefetch(jn < k ? static_cast<const void*>(&pre[jn])

@@ -1,4 +1,3 @@
-# scratch experiment driver (gpurun): Cholesky lookahead with the next panel enqueued from inside the update
-python -m pytest tests/test_gpu_gram.py tests/test_gpu_refit.py -x -q 2>&1 | tail -n 1
-FSTK_DEBUG_TIMING=1 python tools/refit_var.py 6 2>&1 | grep -E "^run|chol_crt" | tail -10
-python tools/chol_time.py 4 2>&1 | grep "slices=5"
+# scratch experiment driver (gpurun): prepare phases with the two-thread sampler
+FSTK_DEBUG_TIMING=1 python tools/refit_var.py 4 2>&1 | grep -E "^run|working subset|sketch plan" | tail -9
+python -m pytest tests/test_gpu_refit.py -x -q -k "sketch_rows or c1_refit" 2>&1 | tail -n 1
