@@ -1,3 +1,5 @@
-# scratch experiment driver (gpurun): single-CTA triangular block solves against cuBLAS TRSV/TRSM
-python -m pytest tests/test_gpu_rank.py tests/test_gpu_refit.py tests/test_gpu_gram.py tests/test_gpu_multi.py tests/test_gpu_fullsize_refit.py -x -q 2>&1 | tail -n 1
-for c in 0 1; do echo "custom=$c"; FSTK_TRI_CUSTOM=$c python tools/refit_var.py 5 2>&1 | grep -E "^run" | tail -3; FSTK_TRI_CUSTOM=$c python tools/refine_time.py 1 2>&1 | grep -E "rep 0" | cut -c1-260; done
+# scratch driver for one gpurun call (last use: the round's closing validation)
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests_h.log 2>&1; tail -n 2 gpurun_out/gputests_h.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_h.log 2>&1; tail -n 1 gpurun_out/smoke_h.log | cut -c1-220
+python bench.py > gpurun_out/bench_h.log 2>&1; tail -c 200 gpurun_out/bench_h.log; echo
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_h.log 2>&1; tail -c 150 gpurun_out/bench_ref_h.log; echo
