@@ -396,3 +396,19 @@ def test_tcgen05_syrk_variants_bit_identical(env):
                        env={**os.environ, **env}, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().splitlines()[-1] == "EQUAL"
+
+
+def test_default_level_by_transform(O):
+    # The process default is CRT level 2 (19-bit entries on 7 moduli) for the
+    # mixing transforms and level 3 for the unmixed estimator, whose rows are
+    # worse conditioned; both land on the oracle's core.
+    m, pts, vals = _problem((8, 8, 6), 60_000, 23)
+    assert F.gram_slices() == 2
+    new_d, info_d = F.reestimate_core(m, pts, vals, seed=5)
+    new_n, info_n = F.reestimate_core(m, pts, vals, seed=5, transform="none")
+    assert info_d["gram_slices"] in (2, 7, 0) and info_n["gram_slices"] in (3, 7, 0)
+    assert info_d["gram_slices"] == 2 and info_n["gram_slices"] == 3  # benign system: no escalation
+    core_o, _ = O.reestimate_core(m, pts, vals, seed=5)
+    assert rel(new_d.core.reshape(-1, order="F"), core_o) <= CORE_TOL
+    core_on, _ = O.reestimate_core(m, pts, vals, seed=5, transform="none")
+    assert rel(new_n.core.reshape(-1, order="F"), core_on) <= CORE_TOL
