@@ -271,8 +271,9 @@ int32_t fstk_gpu_refit_normal_equations_native(fstk_gpu_refit* refit, double* gr
  * rounded to (7 slices - 1)-bit integers per column and segment), or at the
  * preconditioner grades 3 and 2: 23- and 19-bit entries, the most that 8 and
  * 7 CRT moduli carry.  The default ($FSTK_GRAM_SLICES) is 2; the refinement
- * against A corrects what the Gram rounds away, and transform = none takes
- * at least level 3 from this setting (its rows are worse conditioned).
+ * against A corrects what the Gram rounds away; transform = none and
+ * sketches with fewer than 8 R rows take at least level 3 from this setting
+ * (their systems are worse conditioned).
  * Products are exact (CRT over int8 residues; the
  * digit-plane split with FSTK_GRAM_SCHEME=digits); 0 selects the native fp64
  * Gram; < 0 only queries.  Returns the previous setting.  No reference

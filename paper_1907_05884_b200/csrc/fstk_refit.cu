@@ -2639,9 +2639,12 @@ static void normal_equations(fstk_gpu_refit* rf, double* gram, double* rhs,
       // The unmixed estimator's rows are worse conditioned than a mixed
       // sketch's: at C2 a level-2 Gram leaves its first iterate 38% off and
       // contracts 0.09 per step, at the edge of the escalation rule (level 3:
-      // 1.9e-2, then 2e-5 and 5e-3).  The process setting therefore means at
-      // least level 3 there; an explicit level (normal_equations_level) is kept.
-      if (slices < 0 && rf->none && level == 2) level = 3;
+      // 1.9e-2, then 2e-5 and 5e-3).  So is a thinly oversampled sketch: C1's
+      // M = 4R system escalates from level 2 and not from level 3 (C2/C5 at
+      // 8R and C4 at 16R contract 3e-3 per step or better at level 2).  The
+      // process setting therefore means at least level 3 for transform = none
+      // and for M < 8R; an explicit level (normal_equations_level) is kept.
+      if (slices < 0 && level == 2 && (rf->none || rf->S < 8 * static_cast<uint64_t>(rf->R))) level = 3;
       const bool sliced = level > 0 && gram_sliced_applies(arows, n);
       rf->gram_used = sliced ? level : 0;
       if (rf->none && sliced && gram_scheme_crt()) {

@@ -399,16 +399,19 @@ def test_tcgen05_syrk_variants_bit_identical(env):
 
 
 def test_default_level_by_transform(O):
-    # The process default is CRT level 2 (19-bit entries on 7 moduli) for the
-    # mixing transforms and level 3 for the unmixed estimator, whose rows are
-    # worse conditioned; both land on the oracle's core.
+    # The process default is CRT level 2 (19-bit entries on 7 moduli) for a
+    # mixed sketch oversampled at least 8x, and level 3 for thinner sketches
+    # (the reference's default M = 2.5 R) and for the unmixed estimator, whose
+    # systems are worse conditioned; all land on the oracle's core.
     m, pts, vals = _problem((8, 8, 6), 60_000, 23)
+    R = 384
     assert F.gram_slices() == 2
+    new_8, info_8 = F.reestimate_core(m, pts, vals, seed=5, sample_rows=8 * R)
     new_d, info_d = F.reestimate_core(m, pts, vals, seed=5)
-    new_n, info_n = F.reestimate_core(m, pts, vals, seed=5, transform="none")
-    assert info_d["gram_slices"] in (2, 7, 0) and info_n["gram_slices"] in (3, 7, 0)
-    assert info_d["gram_slices"] == 2 and info_n["gram_slices"] == 3  # benign system: no escalation
-    core_o, _ = O.reestimate_core(m, pts, vals, seed=5)
-    assert rel(new_d.core.reshape(-1, order="F"), core_o) <= CORE_TOL
-    core_on, _ = O.reestimate_core(m, pts, vals, seed=5, transform="none")
-    assert rel(new_n.core.reshape(-1, order="F"), core_on) <= CORE_TOL
+    new_n, info_n = F.reestimate_core(m, pts, vals, seed=5, sample_rows=8 * R, transform="none")
+    # benign system: no escalation
+    assert info_8["gram_slices"] == 2 and info_d["gram_slices"] == 3 and info_n["gram_slices"] == 3
+    for new, kw in ((new_8, dict(sample_rows=8 * R)), (new_d, {}),
+                    (new_n, dict(sample_rows=8 * R, transform="none"))):
+        core_o, _ = O.reestimate_core(m, pts, vals, seed=5, **kw)
+        assert rel(new.core.reshape(-1, order="F"), core_o) <= CORE_TOL
