@@ -1,8 +1,4 @@
-# scratch driver for one gpurun call: level rule by oversampling: tests + C1/C2 refits
-python -m pytest tests/test_gpu_gram.py tests/test_gpu_refit.py tests/test_gpu_rank.py tests/test_gpu_multi.py tests/test_gpu_dist.py -x -q 2>&1 | tail -n 1
-python bench.py --config C1 --no-cpu --steps 3 --warmup 3 > gpurun_out/bench_c1c.log 2>&1; python - <<'PY'
-import json
-d=json.loads([x for x in open('gpurun_out/bench_c1c.log') if x.startswith('{')][-1])
-r=d['refit']; print('C1:', r['seconds'], r['samples_s'], 'steps', r['refine_steps'], 'used', r['gram_slices'])
-PY
-python tools/refit_var.py 3 2>&1 | grep -E "^run" | tail -2
+# scratch driver for one gpurun call (last use: the round's closing validation of HEAD)
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests_i.log 2>&1; tail -n 2 gpurun_out/gputests_i.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_i.log 2>&1; tail -n 1 gpurun_out/smoke_i.log | cut -c1-220
+python bench.py --steps 5 --warmup 3 > gpurun_out/bench_i.log 2>&1; tail -c 150 gpurun_out/bench_i.log; echo
