@@ -2971,8 +2971,31 @@ static bool chol_crt(cublasHandle_t blas, cusolverDnHandle_t solver, double* G, 
     check_launch("transpose_panel_kernel");
     count_launch(2);
   };
+  // FSTK_DEBUG_TIMING: device time between the ends of consecutive trailing
+  // updates (events on s), and the host time spent enqueueing each.
+  static const bool dbg_chol = std::getenv("FSTK_DEBUG_TIMING") != nullptr;
+  std::vector<cudaEvent_t> pev;
+  std::vector<double> host_ms;
+  auto stamp = [&] {
+    if (!dbg_chol) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    pev.push_back(e);
+  };
+  stamp();
   panel(0);
   for (int p = 0; p < npan; ++p) {
+    const auto th0 = std::chrono::steady_clock::now();
+    struct HostStamp {
+      std::vector<double>& v;
+      std::chrono::steady_clock::time_point t0;
+      bool on;
+      ~HostStamp() {
+        if (on) v.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      }
+    } hs{host_ms, th0, dbg_chol};
+    if (p > 0) stamp();
     const int i0 = p * nb, b = std::min(nb, n - i0), rest = n - i0 - b;
     if (rest == 0) break;
     double* A22 = G + static_cast<int64_t>(i0 + b) * n + i0 + b;
@@ -3013,7 +3036,20 @@ static bool chol_crt(cublasHandle_t blas, cusolverDnHandle_t solver, double* G, 
   cusolverDnSetStream(solver, s);
   std::vector<int> hinfo(npan);
   FSTK_CUDA(cudaMemcpyAsync(hinfo.data(), dinfo.p, npan * sizeof(int), cudaMemcpyDeviceToHost, s));
+  stamp();
   FSTK_CUDA(cudaStreamSynchronize(s));
+  if (dbg_chol && pev.size() > 1) {
+    std::string line = "fstk chol panels (device ms | host enqueue ms):";
+    for (size_t i = 0; i + 1 < pev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pev[i], pev[i + 1]);
+      char buf[48];
+      std::snprintf(buf, sizeof buf, " %.1f|%.1f", ms, i < host_ms.size() ? host_ms[i] : 0.0);
+      line += buf;
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
+  for (cudaEvent_t e : pev) cudaEventDestroy(e);
   for (int v : hinfo)
     if (v != 0) return false;
   return true;
