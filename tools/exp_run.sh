@@ -1,4 +1,8 @@
-# scratch driver for one gpurun call (last use: HEAD sanity after the debug instrumentation)
-python -m pytest tests/test_gpu_gram.py tests/test_gpu_refit.py tests/test_gpu_rank.py -x -q 2>&1 | tail -n 1
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -n 1 | cut -c1-160
-python tools/refit_var.py 4 2>&1 | grep -E "^run" | tail -3
+# scratch driver for one gpurun call: 2 ranks on one GPU through gloo (host logic of the N > 1 bench path) on HEAD
+FSTK_BENCH_BACKEND=gloo timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --no-refit-none > gpurun_out/bench_g2b.log 2>&1; python - <<'PY'
+import json
+L=[x for x in open('gpurun_out/bench_g2b.log') if x.startswith('{')]
+d=json.loads(L[-1]); r=d['refit']
+print('n_gpus', d['n_gpus'], 'value', d['value'], 'refit', r['seconds'], r['samples_s'], 'steps', r['refine_steps'], 'lvl', r['gram_slices'], 'res', r['residual_after'])
+PY
+FSTK_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29514 bench.py --impl reference --gpus 2 --steps 1 --warmup 1 > gpurun_out/bench_g2ref.log 2>&1; grep -c '"impl": "reference"' gpurun_out/bench_g2ref.log
